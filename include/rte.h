@@ -1,0 +1,166 @@
+/* rte.h -- C ABI of the B200-native hot path of arXiv 2604.23265
+ * ("A filtered MgNet solver for radiative transfer equations").
+ *
+ * The hot path is the inner loop of an MgNet-preconditioned restarted GMRES
+ * solve of the discretised steady RTE in x-y geometry:
+ *   one discrete-ordinates operator apply  (rte_apply: upwind stencil + dense
+ *   M x M Henyey-Greenstein scattering contraction, PAPER.md:90-104 eq:DORTE_2d),
+ *   one MgNet V-cycle (mgnet_vcycle), and the Arnoldi/Givens
+ *   bookkeeping (gmres_solve).
+ * Readings of the paper (R1..R30) are listed in DESIGN.md §3; the operator is
+ * the psi-space discrete-ordinates operator (R1).
+ *
+ * Conventions
+ *  - Every call returns rte_status; RTE_OK == 0.  On failure a thread-local
+ *    message is available from rte_last_error().  No call aborts the process.
+ *  - "host" pointers are ordinary CPU memory, read during the call only (the
+ *    library copies what it keeps; the caller may free them on return).
+ *  - "_dev" pointers are caller-owned CUDA device memory (e.g. PyTorch
+ *    tensors), contiguous, 16-byte aligned, in the layout stated.  Input and
+ *    output buffers of one call must not alias.
+ *  - stream: a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    Calls only enqueue work on it, except gmres_solve, which synchronises it
+ *    once per inner iteration to read an 8-byte convergence flag.
+ *  - Unknown layout: psi[b][j][i][m] (batch, y-index j, x-index i, ordinate m
+ *    fastest), float32 unless stated; n = batch*N*N*M elements.  Cell (j,i)
+ *    covers [i h,(i+1) h] x [j h,(j+1) h], h = 1/N.  Ordinates are ordered
+ *    quadrant-major (+,+),(-,+),(-,-),(+,-), then polar, then azimuth
+ *    (R3); rte_get_ordinates returns them.
+ *  - A handle is not thread-safe: serialise calls on one handle (it owns
+ *    scratch).  Distinct handles may run concurrently on distinct streams.
+ */
+#ifndef RTE_H
+#define RTE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  RTE_OK = 0,
+  RTE_EINVAL = 1,    /* invalid argument (message says which) */
+  RTE_ENOMEM = 2,    /* device or host allocation failed */
+  RTE_ECUDA = 3,     /* CUDA error (message holds cudaGetErrorString) */
+  RTE_EINTERNAL = 4
+} rte_status;
+
+/* Uniform grid on the unit square; nx == ny == N required; h = 1/N. */
+typedef struct { int batch, nx, ny; } rte_grid;
+
+/* Angular quadrature.  If c == NULL the built-in product set is
+ * used: n_polar Gauss-Legendre zeta nodes on (0,1) x n_azim offset-uniform
+ * azimuths, M = n_polar*n_azim, weights summing to 4 pi (R2, R3).
+ * Otherwise c, s, zeta, w (host, length M) are taken as given: requires
+ * sum w = 4 pi within 1e-12, c_m != 0, s_m != 0, M % 4 == 0. */
+typedef struct {
+  int M, n_polar, n_azim;
+  const double *c, *s, *zeta, *w;
+} rte_ordinates;
+
+typedef struct rte_problem rte_problem;   /* opaque; immutable after setup except scratch */
+typedef struct mgnet_net mgnet_net;       /* opaque */
+
+/* rte_setup -- build the discrete problem (PAPER.md:23-37 eq:RTE + BCs, 69-74 eq:RTE_xy,
+ * 90-104 eq:DORTE_2d, 113-117 cell values).
+ *  sigma_T, sigma_a, q, eps : host float32 [batch][ny][nx] cell values.
+ *  g                         : host float32 [batch], HG anisotropy, |g| < 1.
+ *  inflow                    : host float32 [batch][4][N][M], faces in order
+ *      L (x=0, indexed by j), R (x=1, by j), B (y=0, by i), T (y=1, by i);
+ *      only incoming entries (u_m . n < 0) are read; may be NULL (zero inflow).
+ * Computes (host, fp64): the quadrature, the row-normalised HG matrix
+ * S = K W (R4, R5), per-cell sigma_t = sigma_T/eps,
+ * sigma_s = sigma_T/eps - eps sigma_a, f = eps q (R7), and uploads them.
+ * Errors (RTE_EINVAL): N < 1, nx != ny, batch < 1, bad ordinates, eps not in
+ * (0,1], any sigma < 0, |g| >= 1, sigma_T/eps < eps sigma_a in a cell. */
+rte_status rte_setup(const rte_grid* grid, const rte_ordinates* ord,
+                     const float* sigma_T, const float* sigma_a, const float* q,
+                     const float* eps, const float* g, const float* inflow,
+                     rte_problem** out);
+void rte_destroy(rte_problem* p);
+
+/* Sizes of a problem: batch, N, M and n = batch*N*N*M. Any pointer may be NULL. */
+rte_status rte_problem_info(const rte_problem* p, int* batch, int* N, int* M, int64_t* n);
+
+/* Copy the ordinate set actually used (host arrays of length M; any may be NULL). */
+rte_status rte_get_ordinates(const rte_problem* p, double* c, double* s, double* zeta, double* w);
+
+/* Host-only setup helpers (no device work; usable without a GPU):
+ * rte_quadrature fills the built-in product set (R2, R3; arrays of n_polar*n_azim);
+ * rte_hg_matrix fills S = K W, [M][M] row-major, for ordinates c, s, zeta, w and anisotropy g
+ * (PAPER.md:30-32 eq:hg; row normalisation sum_n K_mn w_n = 1, R4, R5). */
+rte_status rte_quadrature(int n_polar, int n_azim, double* c, double* s, double* zeta, double* w);
+rte_status rte_hg_matrix(int M, const double* c, const double* s, const double* zeta, const double* w,
+                         double g, double* S);
+
+/* b = eps q + inflow ghost terms: b_dev float32 [n]. */
+rte_status rte_rhs(const rte_problem* p, float* b_dev, void* stream);
+
+/* y = A x, the discrete-ordinates operator (R9):
+ *  (A psi)_{jim} = (|c_m|/h + |s_m|/h + sigma_t) psi_{jim} - (|c_m|/h) psi_{j,i-sgn c_m,m}
+ *                  - (|s_m|/h) psi_{j-sgn s_m,i,m} - sigma_s sum_n S_mn psi_{jin},
+ * neighbours outside the grid are 0.  Fused upwind stencil + dense [cells x M].[M x M]
+ * scattering GEMM (3xTF32 on tcgen05 tensor cores where M allows; fp32 accumulate).
+ * x_dev, y_dev float32 [n]. */
+rte_status rte_apply(const rte_problem* p, const float* x_dev, float* y_dev, void* stream);
+
+/* Same operator in float64 (used for the fp64 restart residual; exported for tests). */
+rte_status rte_apply_f64(const rte_problem* p, const double* x_dev, double* y_dev, void* stream);
+
+/* mgnet_create -- linear MgNet V-cycle preconditioner (R12-R20).
+ *  levels L >= 1, c0 = channels at level 0 (C_l = c0 2^l), nu = smoothing steps pre/post.
+ *  weights: host float32, packed in the order of DESIGN.md R20 (PyTorch layouts):
+ *    Lambda [c0][M][1][1]; for l = 0..L-1: A^l [C_l][C_l][3][3], pre B^{l,1..nu},
+ *    post B'^{l,1..nu}; if l < L-1: R^l [C_{l+1}][C_l][3][3] (OIHW) and
+ *    P^l [C_{l+1}][C_l][4][4] (conv_transpose IOHW); finally Theta [M][c0][1][1].
+ *  n_floats must equal that count.  N must be divisible by 2^(L-1).
+ * The net keeps its own device copies of the weights and its activation workspace. */
+rte_status mgnet_create(const rte_problem* p, int levels, int c0, int nu,
+                        const float* weights, size_t n_floats, mgnet_net** out);
+void mgnet_destroy(mgnet_net* net);
+
+/* z = [r +] V(r): one V-cycle on f^0 = Lambda r; z = Theta u^0 (+ r if add_identity).
+ * r_dev, z_dev float32 [n], NHWC with M channels (the unknown layout). */
+rte_status mgnet_vcycle(const mgnet_net* net, const float* r_dev, float* z_dev,
+                        int add_identity, void* stream);
+
+/* Restarted right-preconditioned GMRES(m) (R21, R22).
+ * Preconditioner P = I + V (precond=1, requires net) or P = I (precond=0).
+ * Iterate x is float64; the Krylov basis is float32; dot products accumulate in
+ * float64; every restart recomputes r = b - A x in float64.  The batch's
+ * samples are independent solves with their own Arnoldi/Givens state. */
+typedef struct {
+  int restart;       /* m, 1..64 */
+  int maxit;         /* cap on total inner iterations per sample */
+  double rtol;       /* stop when ||b - A x|| <= rtol ||b|| */
+  int precond;       /* 0 none, 1 MgNet (I + V) */
+  int reorth;        /* 0 = CGS2: two Gram-Schmidt passes (default); 1 = one CGS pass */
+} gmres_opts;
+
+typedef struct {
+  int iterations;    /* total inner iterations */
+  int restarts;      /* cycles started */
+  int converged;     /* true residual <= rtol ||b|| at exit */
+  int breakdown;     /* lucky breakdown happened */
+  double relres_true;/* ||b - A x|| / ||b|| in float64 at exit */
+  double relres_est; /* last Arnoldi estimate |g_{j+1}| / ||b|| */
+  double* history;   /* optional caller buffer, >= maxit doubles: estimate after each iteration */
+  double* hessenberg;/* optional caller buffer, (restart+1)*restart doubles: the first cycle's
+                        unrotated Hessenberg matrix H[i][j], row-major */
+} gmres_report;
+
+/* b_dev float32 [n]; x_dev float64 [n] (in: x0, out: x); rep: array of `batch` reports. */
+rte_status gmres_solve(const rte_problem* p, const mgnet_net* net, const float* b_dev,
+                       double* x_dev, const gmres_opts* opts, gmres_report* rep, void* stream);
+
+/* Kernel launches issued by this thread since the last call (reset to 0). */
+int64_t rte_launch_count(int reset);
+
+const char* rte_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RTE_H */

@@ -176,7 +176,8 @@ def apply(prob: Problem, psi: np.ndarray) -> np.ndarray:
     ax = np.abs(prob.qd.c) / h
     ay = np.abs(prob.qd.s) / h
     px, py = _upwind_neighbours(psi, prob.qd)
-    scatter = np.einsum("bjin,bmn->bjim", psi, prob.S)           # sum_n S_mn psi_n
+    B, N, _, M = psi.shape
+    scatter = (psi.reshape(B, N * N, M) @ np.transpose(prob.S, (0, 2, 1))).reshape(psi.shape)  # sum_n S_mn psi_n
     return ((ax + ay)[None, None, None, :] + prob.sig_t[..., None]) * psi \
         - ax * px - ay * py - prob.sig_s[..., None] * scatter
 

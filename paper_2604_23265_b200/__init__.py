@@ -1,0 +1,207 @@
+"""B200-native hot path of arXiv 2604.23265 (MgNet-preconditioned GMRES for the steady RTE).
+
+Thin Python binding over the C ABI in ``include/rte.h`` (``librte_b200.so``).  The functions
+keep the C names; they only marshal arguments.  Device buffers are torch CUDA tensors and the
+stream is torch's current stream.  Every step of the path runs in the library's CUDA kernels;
+there is no CPU fallback (importing raises if the library is missing).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import RteError, check, gmres_opts, gmres_report, lib
+
+__all__ = ["Problem", "MgNet", "rte_setup", "rte_rhs", "rte_apply", "rte_apply_f64", "mgnet_create",
+           "mgnet_vcycle", "gmres_solve", "rte_quadrature", "rte_hg_matrix", "rte_launch_count", "RteError", "LIB_PATH"]
+
+LIB_PATH = _lib.LIB_PATH
+
+
+def _stream(stream=None) -> int:
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return int(stream.cuda_stream) if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _f32(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float32))
+
+
+def _fptr(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_float))
+
+
+def _dptr(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _dev(t, dtype_name: str):
+    import torch
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.is_contiguous()):
+        raise ValueError("expected a contiguous CUDA tensor")
+    want = {"f32": torch.float32, "f64": torch.float64}[dtype_name]
+    if t.dtype != want:
+        raise ValueError(f"expected dtype {want}, got {t.dtype}")
+    return C.c_void_p(t.data_ptr())
+
+
+class Problem:
+    """Owner of an ``rte_problem*`` handle (rte_setup / rte_destroy)."""
+
+    def __init__(self, handle: C.c_void_p):
+        self._h = handle
+        b, n, m, tot = C.c_int(), C.c_int(), C.c_int(), C.c_int64()
+        check("rte_problem_info", lib.rte_problem_info(self._h, C.byref(b), C.byref(n), C.byref(m), C.byref(tot)))
+        self.batch, self.N, self.M, self.n = b.value, n.value, m.value, tot.value
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def shape(self):
+        return (self.batch, self.N, self.N, self.M)
+
+    def ordinates(self):
+        arrs = [np.zeros(self.M) for _ in range(4)]
+        check("rte_get_ordinates", lib.rte_get_ordinates(self._h, *[_dptr(a) for a in arrs]))
+        return tuple(arrs)   # c, s, zeta, w
+
+    def close(self):
+        if self._h:
+            lib.rte_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def rte_setup(N: int, sigma_T, sigma_a, q, eps, g, inflow=None, *, n_polar: int = 0, n_azim: int = 0,
+              ordinates: Optional[Sequence[np.ndarray]] = None, batch: Optional[int] = None) -> Problem:
+    """rte_setup(grid, ordinates, sigma_T, sigma_a, q, eps, g, inflow) -> Problem (host inputs)."""
+    sT, sA, qq, ee = (_f32(a) for a in (sigma_T, sigma_a, q, eps))
+    B = batch if batch is not None else (sT.shape[0] if sT.ndim == 3 else 1)
+    gg = _f32(np.broadcast_to(np.asarray(g, np.float32), (B,)))
+    grid = _lib.rte_grid(B, N, N)
+    if ordinates is None:
+        ordn = _lib.rte_ordinates(n_polar * n_azim, n_polar, n_azim, None, None, None, None)
+        keep = ()
+    else:
+        keep = tuple(np.ascontiguousarray(np.asarray(a, np.float64)) for a in ordinates)
+        ordn = _lib.rte_ordinates(keep[0].size, 0, 0, *[_dptr(a) for a in keep])
+    inf = _fptr(_f32(inflow)) if inflow is not None else None
+    infa = _f32(inflow) if inflow is not None else None
+    h = C.c_void_p()
+    check("rte_setup", lib.rte_setup(C.byref(grid), C.byref(ordn), _fptr(sT), _fptr(sA), _fptr(qq), _fptr(ee),
+                                     _fptr(gg), _fptr(infa) if infa is not None else None, C.byref(h)))
+    del keep, inf
+    return Problem(h)
+
+
+def rte_quadrature(n_polar: int, n_azim: int):
+    """Host-only: the built-in product quadrature (c, s, zeta, w)."""
+    M = n_polar * n_azim
+    arrs = [np.zeros(M) for _ in range(4)]
+    check("rte_quadrature", lib.rte_quadrature(n_polar, n_azim, *[_dptr(a) for a in arrs]))
+    return tuple(arrs)
+
+
+def rte_hg_matrix(c, s, zeta, w, g: float) -> np.ndarray:
+    """Host-only: the row-normalised HG matrix S = K W ([M][M])."""
+    arrs = [np.ascontiguousarray(np.asarray(a, np.float64)) for a in (c, s, zeta, w)]
+    M = arrs[0].size
+    S = np.zeros((M, M))
+    check("rte_hg_matrix", lib.rte_hg_matrix(M, *[_dptr(a) for a in arrs], float(g), _dptr(S)))
+    return S
+
+
+def rte_rhs(p: Problem, b, stream=None) -> None:
+    check("rte_rhs", lib.rte_rhs(p.handle, _dev(b, "f32"), C.c_void_p(_stream(stream))))
+
+
+def rte_apply(p: Problem, x, y, stream=None) -> None:
+    check("rte_apply", lib.rte_apply(p.handle, _dev(x, "f32"), _dev(y, "f32"), C.c_void_p(_stream(stream))))
+
+
+def rte_apply_f64(p: Problem, x, y, stream=None) -> None:
+    check("rte_apply_f64", lib.rte_apply_f64(p.handle, _dev(x, "f64"), _dev(y, "f64"), C.c_void_p(_stream(stream))))
+
+
+class MgNet:
+    """Owner of an ``mgnet_net*`` handle (mgnet_create / mgnet_destroy)."""
+
+    def __init__(self, handle, problem: Problem, levels: int, c0: int, nu: int):
+        self._h = handle
+        self.problem = problem  # keep the problem alive
+        self.levels, self.c0, self.nu = levels, c0, nu
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if self._h:
+            lib.mgnet_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def mgnet_create(p: Problem, levels: int, c0: int, nu: int, weights) -> MgNet:
+    w = _f32(weights).ravel()
+    h = C.c_void_p()
+    check("mgnet_create", lib.mgnet_create(p.handle, levels, c0, nu, _fptr(w), w.size, C.byref(h)))
+    return MgNet(h, p, levels, c0, nu)
+
+
+def mgnet_vcycle(net: MgNet, r, z, add_identity: bool = True, stream=None) -> None:
+    check("mgnet_vcycle", lib.mgnet_vcycle(net.handle, _dev(r, "f32"), _dev(z, "f32"), int(add_identity),
+                                           C.c_void_p(_stream(stream))))
+
+
+def gmres_solve(p: Problem, net: Optional[MgNet], b, x, *, restart: int = 30, maxit: int = 1000,
+                rtol: float = 1e-8, precond: Optional[int] = None, reorth: int = 0,
+                history: bool = True, hessenberg: bool = False, stream=None):
+    """Restarted right-preconditioned GMRES; x (float64 CUDA tensor) holds x0 on entry, x on exit.
+
+    Returns a list of per-sample dicts (iterations, restarts, converged, breakdown, relres_true,
+    relres_est, history [, hessenberg])."""
+    if precond is None:
+        precond = 1 if net is not None else 0
+    opts = gmres_opts(restart, maxit, rtol, precond, reorth)
+    B = p.batch
+    reps = (gmres_report * B)()
+    hist = [np.zeros(max(maxit, 1)) for _ in range(B)]
+    hess = [np.zeros((restart + 1) * restart) for _ in range(B)]
+    for i in range(B):
+        reps[i].history = _dptr(hist[i]) if history else None
+        reps[i].hessenberg = _dptr(hess[i]) if hessenberg else None
+    check("gmres_solve", lib.gmres_solve(p.handle, net.handle if net is not None else None, _dev(b, "f32"),
+                                         _dev(x, "f64"), C.byref(opts), reps, C.c_void_p(_stream(stream))))
+    out = []
+    for i in range(B):
+        r = reps[i]
+        d = dict(iterations=r.iterations, restarts=r.restarts, converged=bool(r.converged),
+                 breakdown=bool(r.breakdown), relres_true=r.relres_true, relres_est=r.relres_est)
+        if history:
+            d["history"] = hist[i][:r.iterations].copy()
+        if hessenberg:
+            d["hessenberg"] = hess[i].reshape(restart + 1, restart)
+        out.append(d)
+    return out
+
+
+def rte_launch_count(reset: bool = False) -> int:
+    return int(lib.rte_launch_count(int(reset)))

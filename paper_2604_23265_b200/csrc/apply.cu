@@ -1,0 +1,163 @@
+// Discrete-ordinates operator kernels: rhs, fp32 apply (SIMT reference path for any M),
+// fp64 apply (restart residual).  The tensor-core 3xTF32 apply lives in apply_tc.cu.
+//
+// Operator (PAPER.md:91-93 eq:DORTE_2d with the upwind stencil of DESIGN.md R9):
+//   (A psi)_{jim} = (|c_m|/h + |s_m|/h + sigma_t) psi_{jim} - (|c_m|/h) psi_{j,i-sgn c_m,m}
+//                   - (|s_m|/h) psi_{j-sgn s_m,i,m} - sigma_s sum_n S_mn psi_{jin}
+// Layout psi[b][j][i][m]; the scattering term is the GEMM  Psi[cells x M] . S^T[M x M].
+#include "common.h"
+
+namespace rte {
+namespace {
+
+// b = eps q + ghost terms.  One thread per unknown.
+__global__ void rhs_kernel(int B, int N, int M, const float* __restrict__ f, const float* __restrict__ inflow,
+                           const float* __restrict__ ax, const float* __restrict__ ay,
+                           const int8_t* __restrict__ sgx, const int8_t* __restrict__ sgy,
+                           float* __restrict__ b) {
+  int64_t n = (int64_t)B * N * N * M;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    int m = (int)(e % M);
+    int64_t cell = e / M;
+    int i = (int)(cell % N);
+    int j = (int)((cell / N) % N);
+    int bb = (int)(cell / ((int64_t)N * N));
+    double v = f[cell];
+    if (inflow) {
+      const float* fin = inflow + (int64_t)bb * 4 * N * M;
+      if (sgx[m] > 0 && i == 0) v += (double)ax[m] * fin[(0 * N + j) * M + m];
+      if (sgx[m] < 0 && i == N - 1) v += (double)ax[m] * fin[(1 * N + j) * M + m];
+      if (sgy[m] > 0 && j == 0) v += (double)ay[m] * fin[(2 * N + i) * M + m];
+      if (sgy[m] < 0 && j == N - 1) v += (double)ay[m] * fin[(3 * N + i) * M + m];
+    }
+    b[e] = (float)v;
+  }
+}
+
+// SIMT fused stencil + scattering GEMM.  Tile = TP cells x TMO ordinates (TP*TMO = 4096),
+// 256 threads, each 4 cells x 4 ordinates, K chunks of 16 ordinates through shared memory.
+template <typename T, int TMO>
+__global__ void __launch_bounds__(256) apply_simt_kernel(
+    int N, int M, const T* __restrict__ x, T* __restrict__ y, const T* __restrict__ St,
+    const T* __restrict__ sig_t, const T* __restrict__ sig_s, const T* __restrict__ axv,
+    const T* __restrict__ ayv, const int8_t* __restrict__ sgx, const int8_t* __restrict__ sgy,
+    const float* __restrict__ bvec, const double* __restrict__ alpha, int alpha_stride) {
+  constexpr int TP = 4096 / TMO;
+  constexpr int KC = 16;
+  constexpr int TX = TMO / 4;          // threads along ordinates
+  __shared__ __align__(16) T As[KC][TP + 4];
+  __shared__ __align__(16) T Bs[KC][TMO + 4];
+  const int tid = threadIdx.x;
+  const int tx = tid % TX, ty = tid / TX;
+  const int bsample = blockIdx.z;
+  const int64_t cells = (int64_t)N * N;
+  const int64_t c0 = (int64_t)blockIdx.x * TP;        // first cell (within sample) of the tile
+  const int m0 = blockIdx.y * TMO;
+  const T* xs = x + (int64_t)bsample * cells * M;
+  const T* Sts = St + (int64_t)bsample * M * M;
+  T acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[a][c] = T(0);
+
+  for (int k0 = 0; k0 < M; k0 += KC) {
+    // A chunk: TP cells x KC ordinates (x[cell][k0..k0+15]) -> As[k][cell]
+    for (int e = tid; e < TP * KC; e += 256) {
+      int cl = e / KC, kk = e % KC;
+      int64_t cell = c0 + cl;
+      T v = T(0);
+      if (cell < cells && k0 + kk < M) v = xs[cell * M + k0 + kk];
+      As[kk][cl] = v;
+    }
+    // B chunk: St[k0+kk][m0 + o]
+    for (int e = tid; e < KC * TMO; e += 256) {
+      int kk = e / TMO, o = e % TMO;
+      T v = T(0);
+      if (k0 + kk < M && m0 + o < M) v = Sts[(int64_t)(k0 + kk) * M + m0 + o];
+      Bs[kk][o] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < KC; ++kk) {
+      T av[4], bv[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) av[a] = As[kk][ty * 4 + a];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) bv[c] = Bs[kk][tx * 4 + c];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[a][c] = fma(av[a], bv[c], acc[a][c]);
+    }
+    __syncthreads();
+  }
+  // epilogue: stencil + diagonal - sigma_s * (S psi)
+  const T al = alpha ? (T)alpha[(int64_t)bsample * alpha_stride] : T(1);
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    int64_t cell = c0 + ty * 4 + a;
+    if (cell >= cells) continue;
+    int i = (int)(cell % N), j = (int)(cell / N);
+    int64_t gcell = (int64_t)bsample * cells + cell;
+    T st = sig_t[gcell], ss = sig_s[gcell];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      int m = m0 + tx * 4 + c;
+      if (m >= M) continue;
+      T ax = axv[m], ay = ayv[m];
+      T psi = xs[cell * M + m];
+      T v = (ax + ay + st) * psi - ss * acc[a][c];
+      int ii = i - sgx[m], jj = j - sgy[m];
+      if (ii >= 0 && ii < N) v -= ax * xs[(cell - sgx[m]) * M + m];
+      if (jj >= 0 && jj < N) v -= ay * xs[(cell - (int64_t)sgy[m] * N) * M + m];
+      v *= al;
+      int64_t o = gcell * M + m;
+      if (bvec) v = (T)bvec[o] - v;
+      y[o] = v;
+    }
+  }
+}
+
+template <typename T>
+void launch_simt(const rte_problem* p, const T* x, T* y, const T* St, const T* st, const T* ss,
+                 const T* ax, const T* ay, const float* b, const double* alpha, int alpha_stride,
+                 cudaStream_t stream) {
+  int64_t cells = (int64_t)p->N * p->N;
+  auto go = [&](auto tmo_tag) {
+    constexpr int TMO = decltype(tmo_tag)::value;
+    constexpr int TP = 4096 / TMO;
+    dim3 grid((unsigned)((cells + TP - 1) / TP), (unsigned)((p->M + TMO - 1) / TMO), (unsigned)p->B);
+    apply_simt_kernel<T, TMO><<<grid, 256, 0, stream>>>(p->N, p->M, x, y, St, st, ss, ax, ay, p->sgx, p->sgy,
+                                                         b, alpha, alpha_stride);
+  };
+  if (p->M <= 16) go(std::integral_constant<int, 16>{});
+  else if (p->M <= 32) go(std::integral_constant<int, 32>{});
+  else go(std::integral_constant<int, 64>{});
+}
+
+}  // namespace
+
+void launch_rhs(const rte_problem* p, float* b, cudaStream_t st) {
+  int64_t n = p->n;
+  int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 16);
+  rhs_kernel<<<blocks, 256, 0, st>>>(p->B, p->N, p->M, p->f, p->inflow, p->ax, p->ay, p->sgx, p->sgy, b);
+  after_launch("rhs_kernel");
+}
+
+void launch_apply_f32(const rte_problem* p, const float* x, float* y, const double* alpha, int alpha_stride,
+                      cudaStream_t st) {
+  if (p->tc_apply) {
+    launch_apply_tc(p, x, y, alpha, alpha_stride, st);
+    return;
+  }
+  launch_simt<float>(p, x, y, p->St32, p->sig_t, p->sig_s, p->ax, p->ay, nullptr, alpha, alpha_stride, st);
+  after_launch("apply_simt_kernel<float>");
+}
+
+void launch_apply_f64(const rte_problem* p, const double* x, double* y, const float* b, cudaStream_t st) {
+  launch_simt<double>(p, x, y, p->St64, p->sig_t64, p->sig_s64, p->ax64, p->ay64, b, nullptr, 0, st);
+  after_launch("apply_simt_kernel<double>");
+}
+
+}  // namespace rte

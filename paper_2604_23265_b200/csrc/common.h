@@ -1,0 +1,105 @@
+// Internal declarations shared by the library's translation units (NOT part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/rte.h"
+
+namespace rte {
+
+// ---- error handling -------------------------------------------------------
+void set_error(const std::string& msg);
+struct Fail {
+  rte_status st;
+};
+#define RTE_CHECK_CUDA(expr)                                                     \
+  do {                                                                           \
+    cudaError_t e__ = (expr);                                                    \
+    if (e__ != cudaSuccess) {                                                    \
+      ::rte::set_error(std::string(#expr) + ": " + cudaGetErrorString(e__));     \
+      throw ::rte::Fail{RTE_ECUDA};                                              \
+    }                                                                            \
+  } while (0)
+#define RTE_REQUIRE(cond, msg)                                                   \
+  do {                                                                           \
+    if (!(cond)) {                                                               \
+      ::rte::set_error(msg);                                                     \
+      throw ::rte::Fail{RTE_EINVAL};                                             \
+    }                                                                            \
+  } while (0)
+// Check for launch errors after a kernel launch and count it.
+void after_launch(const char* what);
+
+template <typename T>
+T* dalloc(size_t n) {
+  void* p = nullptr;
+  if (n == 0) n = 1;
+  cudaError_t e = cudaMalloc(&p, n * sizeof(T));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    set_error(std::string("cudaMalloc failed: ") + cudaGetErrorString(e));
+    throw Fail{RTE_ENOMEM};
+  }
+  return static_cast<T*>(p);
+}
+void dfree(void* p);
+template <typename T>
+void upload(T* d, const T* h, size_t n) {
+  RTE_CHECK_CUDA(cudaMemcpy(d, h, n * sizeof(T), cudaMemcpyHostToDevice));
+}
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int num_sms();
+
+}  // namespace rte
+
+// ---- problem ----------------------------------------------------------------
+struct rte_problem {
+  int B, N, M;
+  int64_t ncell;      // B*N*N
+  int64_t n;          // ncell*M
+  // host copies (fp64)
+  std::vector<double> c, s, zeta, w;
+  std::vector<double> S;   // [B][M][M] row-stochastic K W
+  // device
+  float* sig_t = nullptr;   // [B][N][N]
+  float* sig_s = nullptr;
+  float* f = nullptr;
+  double* sig_t64 = nullptr;
+  double* sig_s64 = nullptr;
+  float* S32 = nullptr;     // [B][M][M]  S[m][n]   (row m, n contiguous)  = GEMM B operand N x K, K-major
+  float* St32 = nullptr;    // [B][M][M]  S^T[n][m] (for the SIMT path)
+  double* St64 = nullptr;   // [B][M][M]  S^T fp64
+  float* S_hi = nullptr;    // [B][M][M]  tf32 hi of S[m][n]
+  float* S_lo = nullptr;    // [B][M][M]  tf32 lo
+  float* ax = nullptr;      // [M]  |c_m|/h  (fp32)
+  float* ay = nullptr;      // [M]  |s_m|/h
+  double* ax64 = nullptr;
+  double* ay64 = nullptr;
+  int8_t* sgx = nullptr;    // [M]  sign(c_m)
+  int8_t* sgy = nullptr;    // [M]  sign(s_m)
+  float* inflow = nullptr;  // [B][4][N][M]
+  bool tc_apply = false;    // tensor-core apply path available for this M
+  mutable void* tc_state = nullptr;  // lazily created TMA descriptors etc.
+  mutable double* scratch64 = nullptr;  // small device scratch
+};
+
+// ---- kernel launchers (apply.cu) --------------------------------------------
+namespace rte {
+void launch_rhs(const rte_problem* p, float* b, cudaStream_t st);
+// y = alpha * A x  (alpha scales the input, i.e. A(alpha x)); alpha_dev may be NULL (1).
+void launch_apply_f32(const rte_problem* p, const float* x, float* y, const double* alpha_dev,
+                      int alpha_stride, cudaStream_t st);
+// y = A x (fp64); if b != NULL: y = b - A x.
+void launch_apply_f64(const rte_problem* p, const double* x, double* y, const float* b, cudaStream_t st);
+bool apply_tc_supported(int M);
+void free_tc_state(rte_problem* p);
+void free_gmres_work(const rte_problem* p);
+void launch_apply_tc(const rte_problem* p, const float* x, float* y, const double* alpha_dev,
+                     int alpha_stride, cudaStream_t st);
+}  // namespace rte

@@ -1,0 +1,542 @@
+// Restarted right-preconditioned GMRES(m) on the device (
+// DESIGN.md R21, R22).  Host C++ drives the loop; every vector operation runs in the kernels
+// below.  Design:
+//  - Krylov basis V in float32, stored UNNORMALISED: column i holds alpha_i^{-1} v_i, with the
+//    per-sample scale alpha_i kept in fp64 on the device.  Consumers (V-cycle lift, apply input,
+//    dots, updates, combination) fold alpha_i in, so no separate normalisation pass is needed.
+//  - Classical Gram-Schmidt with re-orthogonalisation (CGS2) in three fused streaming passes:
+//      A: h1 = alpha V^T w;   B: v' = w - V (alpha h1) and h2 = alpha V^T v', ||v'||^2;
+//      C: v'' = v' - V (alpha h2) and ||v''||^2.
+//    Every dot product accumulates in fp64 with a deterministic (fixed-order) two-level reduction
+//    (warp shuffles -> per-block partials -> last-block finalisation).
+//  - Givens rotations, least squares and the convergence decision run in tiny per-sample device
+//    kernels; the host reads one 32-byte status record per sample per iteration.
+//  - The iterate x is float64 and every restart recomputes r = b - A x in float64.
+#include <math.h>
+
+#include <algorithm>
+#include <map>
+#include <mutex>
+#include <vector>
+
+#include "common.h"
+#include "mgnet.h"
+
+namespace rte {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kMaxRestart = 64;
+
+struct RedArgs {
+  double* partials;   // [B][nblk][nq]
+  unsigned* counters; // [B]
+  double* out;        // [B][out_ld]
+  int out_ld;
+  int nblk;
+};
+
+// Block-reduce NQ doubles per thread, write partials, last block finalises (fixed order).
+// scale_q (may be NULL) multiplies quantity q at finalisation.
+template <int NQ>
+__device__ void reduce_finalize(double (&acc)[NQ], const RedArgs& ra, int b, const double* scale, int nscale) {
+  __shared__ double red[kThreads / 32][NQ > 0 ? NQ : 1];
+  __shared__ bool last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    double v = acc[q];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[warp][q] = v;
+  }
+  __syncthreads();
+  double* part = ra.partials + ((int64_t)b * ra.nblk + blockIdx.x) * NQ;
+  for (int q = threadIdx.x; q < NQ; q += blockDim.x) {
+    double v = 0.0;
+    for (int w = 0; w < kThreads / 32; ++w) v += red[w][q];
+    part[q] = v;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned prev = atomicAdd(ra.counters + b, 1u);
+    last = (prev == (unsigned)ra.nblk - 1);
+  }
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    const double* pb = ra.partials + (int64_t)b * ra.nblk * NQ;
+    for (int q = threadIdx.x; q < NQ; q += blockDim.x) {
+      double v = 0.0;
+      for (int k = 0; k < ra.nblk; ++k) v += ((volatile const double*)pb)[(int64_t)k * NQ + q];
+      if (scale && q < nscale) v *= scale[q];
+      ra.out[(int64_t)b * ra.out_ld + q] = v;
+    }
+    if (threadIdx.x == 0) ra.counters[b] = 0u;
+  }
+}
+
+// One CGS pass over NV basis vectors (see file header).
+//  UPDATE: dst = src - sum_i (hin_i alpha_i) V_i   (else dst = src, not written)
+//  DOTS  : out[i] = alpha_i <V_i, dst>, i < NV ;  always out[NV] = ||dst||^2
+template <int NV, bool UPDATE, bool DOTS>
+__global__ void __launch_bounds__(kThreads, 1) cgs_kernel(
+    const float* __restrict__ V, int64_t vld, const double* __restrict__ alpha, int alpha_ld,
+    const double* __restrict__ hin, int hin_ld, const float* src, float* dst, int64_t ns,
+    const int* __restrict__ active, RedArgs ra) {
+  constexpr int NQ = (DOTS ? NV : 0) + 1;
+  const int b = blockIdx.y;
+  if (active && !active[b]) return;
+  __shared__ float coef[NV > 0 ? NV : 1];
+  if (UPDATE) {
+    for (int i = threadIdx.x; i < NV; i += blockDim.x)
+      coef[i] = (float)(hin[(int64_t)b * hin_ld + i] * alpha[(int64_t)b * alpha_ld + i]);
+    __syncthreads();
+  }
+  double acc[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
+  const int64_t n4 = ns / 4;
+  const float4* s4 = reinterpret_cast<const float4*>(src + (int64_t)b * ns);
+  float4* d4 = reinterpret_cast<float4*>(dst + (int64_t)b * ns);
+  const float* Vb = V + (int64_t)b * ns;
+  for (int64_t q = (int64_t)blockIdx.x * kThreads + threadIdx.x; q < n4; q += (int64_t)ra.nblk * kThreads) {
+    float4 s = s4[q];
+    float4 v[NV > 0 ? NV : 1];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) v[i] = reinterpret_cast<const float4*>(Vb + (int64_t)i * vld)[q];
+    if (UPDATE) {
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        s.x = fmaf(-coef[i], v[i].x, s.x);
+        s.y = fmaf(-coef[i], v[i].y, s.y);
+        s.z = fmaf(-coef[i], v[i].z, s.z);
+        s.w = fmaf(-coef[i], v[i].w, s.w);
+      }
+      d4[q] = s;
+    }
+    if (DOTS) {
+#pragma unroll
+      for (int i = 0; i < NV; ++i)
+        acc[i] += (double)v[i].x * s.x + (double)v[i].y * s.y + (double)v[i].z * s.z + (double)v[i].w * s.w;
+    }
+    acc[NQ - 1] += (double)s.x * s.x + (double)s.y * s.y + (double)s.z * s.z + (double)s.w * s.w;
+  }
+  reduce_finalize<NQ>(acc, ra, b, DOTS ? alpha + (int64_t)b * alpha_ld : nullptr, DOTS ? NV : 0);
+}
+
+// ||x||^2 per sample (x fp32 or fp64); optionally writes xo = (float)x.
+template <typename T>
+__global__ void __launch_bounds__(kThreads) norm_kernel(const T* __restrict__ x, float* __restrict__ xo, int64_t ns,
+                                                         RedArgs ra) {
+  const int b = blockIdx.y;
+  double acc[1] = {0.0};
+  const T* xb = x + (int64_t)b * ns;
+  for (int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x; e < ns; e += (int64_t)ra.nblk * kThreads) {
+    double v = (double)xb[e];
+    acc[0] += v * v;
+    if (xo) xo[(int64_t)b * ns + e] = (float)v;
+  }
+  reduce_finalize<1>(acc, ra, b, nullptr, 0);
+}
+
+// dst = sum_{i < k_b} coef_i V_i   (coef already includes alpha), fp64 accumulation.
+__global__ void __launch_bounds__(kThreads) combine_kernel(const float* __restrict__ V, int64_t vld,
+                                                            const double* __restrict__ coef, int coef_ld,
+                                                            const int* __restrict__ kcols, float* __restrict__ dst,
+                                                            int64_t ns, int nblk) {
+  const int b = blockIdx.y;
+  const int k = kcols[b];
+  const double* cb = coef + (int64_t)b * coef_ld;
+  const float* Vb = V + (int64_t)b * ns;
+  for (int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x; e < ns; e += (int64_t)nblk * kThreads) {
+    double s = 0.0;
+    for (int i = 0; i < k; ++i) s += cb[i] * (double)Vb[(int64_t)i * vld + e];
+    dst[(int64_t)b * ns + e] = (float)s;
+  }
+}
+
+// x += z  for samples with kcols > 0.
+__global__ void axpy64_kernel(double* __restrict__ x, const float* __restrict__ z, const int* __restrict__ kcols,
+                              int64_t ns, int nblk) {
+  const int b = blockIdx.y;
+  if (kcols[b] <= 0) return;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < ns; e += (int64_t)nblk * blockDim.x)
+    x[(int64_t)b * ns + e] += (double)z[(int64_t)b * ns + e];
+}
+
+struct Status {      // per-sample record read by the host each iteration (32 bytes)
+  double est;        // |g_{j+1}| / ||b||   (or true relres at cycle start)
+  int active;        // still iterating in this cycle
+  int breakdown;     // lucky breakdown happened at this step
+  int kcols;         // Krylov columns usable at cycle end
+  int converged;     // (cycle start) true residual <= rtol ||b||
+  int pad[2];
+};
+
+// Cycle start: beta = ||r||, alpha_0 = 1/beta, g = beta e_1, convergence by the true residual.
+__global__ void cycle_init_kernel(int B, const double* __restrict__ rnorm2, const double* __restrict__ bnorm,
+                                  double rtol, int stop_all, double* alpha, int alpha_ld, double* g, int g_ld,
+                                  int* active, int* kcols, const int* done, Status* st) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  double beta = sqrt(fmax(rnorm2[b], 0.0));
+  double rel = bnorm[b] > 0 ? beta / bnorm[b] : 0.0;
+  int conv = (beta <= rtol * bnorm[b]);
+  int act = (!conv && !stop_all && !done[b]) ? 1 : 0;
+  active[b] = act;
+  kcols[b] = 0;
+  alpha[(int64_t)b * alpha_ld] = beta > 0 ? 1.0 / beta : 0.0;
+  for (int i = 0; i < g_ld; ++i) g[(int64_t)b * g_ld + i] = 0.0;
+  g[(int64_t)b * g_ld] = beta;
+  st[b].est = rel;
+  st[b].active = act;
+  st[b].breakdown = 0;
+  st[b].kcols = 0;
+  st[b].converged = conv;
+}
+
+// Givens update of column j (per sample).  h1/h2: pass outputs ([.., j] dots, [j+1] = ||.||^2).
+__global__ void givens_kernel(int B, int j, int m, const double* __restrict__ h1, const double* __restrict__ h2,
+                              int h_ld, const double* __restrict__ nrm2, int nrm_ld, double* Hr, double* Hraw,
+                              int save_raw, double* cs, double* sn, double* g, double* alpha, int alpha_ld,
+                              const double* __restrict__ bnorm, double rtol, int last, int* active, int* kcols,
+                              Status* st) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  if (!active[b]) {
+    st[b].active = 0;
+    st[b].breakdown = 0;
+    return;
+  }
+  double col[kMaxRestart + 1];
+  for (int i = 0; i <= j; ++i) col[i] = h1[(int64_t)b * h_ld + i] + (h2 ? h2[(int64_t)b * h_ld + i] : 0.0);
+  double hj1 = sqrt(fmax(nrm2[(int64_t)b * nrm_ld], 0.0));
+  const int ldh = m;  // H stored [B][m+1][m]
+  double* Hb = Hr + (int64_t)b * (m + 1) * m;
+  if (save_raw) {
+    double* R = Hraw + (int64_t)b * (m + 1) * m;
+    for (int i = 0; i <= j; ++i) R[i * ldh + j] = col[i];
+    R[(j + 1) * ldh + j] = hj1;
+  }
+  double* csb = cs + (int64_t)b * m;
+  double* snb = sn + (int64_t)b * m;
+  for (int i = 0; i < j; ++i) {
+    double t = csb[i] * col[i] + snb[i] * col[i + 1];
+    col[i + 1] = -snb[i] * col[i] + csb[i] * col[i + 1];
+    col[i] = t;
+  }
+  double den = hypot(col[j], hj1);
+  double c = den > 0 ? col[j] / den : 1.0, s = den > 0 ? hj1 / den : 0.0;
+  csb[j] = c;
+  snb[j] = s;
+  for (int i = 0; i < j; ++i) Hb[i * ldh + j] = col[i];
+  Hb[j * ldh + j] = den;
+  double* gb = g + (int64_t)b * (m + 1);
+  gb[j + 1] = -s * gb[j];
+  gb[j] = c * gb[j];
+  double est = fabs(gb[j + 1]) / bnorm[b];
+  int brk = (hj1 <= 1e-14 * den) ? 1 : 0;
+  alpha[(int64_t)b * alpha_ld + j + 1] = brk ? 0.0 : 1.0 / hj1;
+  int stop = brk || (fabs(gb[j + 1]) <= rtol * bnorm[b]) || last || (j + 1 == m);
+  if (stop) {
+    active[b] = 0;
+    kcols[b] = j + 1;
+  }
+  st[b].est = est;
+  st[b].active = !stop;
+  st[b].breakdown = brk;
+  st[b].kcols = stop ? j + 1 : 0;
+}
+
+// y = R^{-1} g (k_b columns) and coef_i = y_i alpha_i.
+__global__ void backsolve_kernel(int B, int m, const double* __restrict__ Hr, const double* __restrict__ g,
+                                 const double* __restrict__ alpha, int alpha_ld, const int* __restrict__ kcols,
+                                 double* coef, int coef_ld) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  int k = kcols[b];
+  const double* Hb = Hr + (int64_t)b * (m + 1) * m;
+  const double* gb = g + (int64_t)b * (m + 1);
+  double y[kMaxRestart];
+  for (int i = k - 1; i >= 0; --i) {
+    double s = gb[i];
+    for (int l = i + 1; l < k; ++l) s -= Hb[i * m + l] * y[l];
+    y[i] = s / Hb[i * m + i];
+  }
+  for (int i = 0; i < k; ++i) coef[(int64_t)b * coef_ld + i] = y[i] * alpha[(int64_t)b * alpha_ld + i];
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------------------
+struct GmresWork {
+  int B = 0, m = 0;
+  int64_t ns = 0;
+  int nblk = 0;
+  float* V = nullptr;      // (m+1) x n
+  float* w = nullptr;      // n
+  float* z = nullptr;      // n
+  double* r64 = nullptr;   // n
+  double *Hr = nullptr, *Hraw = nullptr, *cs = nullptr, *sn = nullptr, *g = nullptr, *alpha = nullptr;
+  double *h1 = nullptr, *h2 = nullptr, *h3 = nullptr, *coef = nullptr, *bnorm = nullptr, *rn2 = nullptr;
+  double* partials = nullptr;
+  unsigned* counters = nullptr;
+  int *active = nullptr, *kcols = nullptr, *done = nullptr;
+  Status* st_dev = nullptr;
+  Status* st_host = nullptr;  // pinned
+  void release() {
+    void* ps[] = {V, w, z, r64, Hr, Hraw, cs, sn, g, alpha, h1, h2, h3, coef, bnorm, rn2, partials, counters,
+                  active, kcols, done, st_dev};
+    for (void* p : ps) dfree(p);
+    if (st_host) cudaFreeHost(st_host);
+    *this = GmresWork();
+  }
+};
+
+static void launch_cgs(const GmresWork& W, int nv, bool update, bool dots, const double* hin, const float* src,
+                       float* dst, double* out, cudaStream_t st) {
+  RedArgs ra{W.partials, W.counters, out, kMaxRestart + 2, W.nblk};
+  dim3 grid(W.nblk, W.B);
+  const int64_t vld = W.ns * W.B;
+  auto go = [&](auto nv_tag, auto up_tag, auto dot_tag) {
+    constexpr int NV = decltype(nv_tag)::value;
+    constexpr bool UP = decltype(up_tag)::value;
+    constexpr bool DT = decltype(dot_tag)::value;
+    cgs_kernel<NV, UP, DT><<<grid, kThreads, 0, st>>>(W.V, vld, W.alpha, W.m + 1, hin, kMaxRestart + 2, src, dst,
+                                                      W.ns, W.active, ra);
+  };
+  using T = std::true_type;
+  using F = std::false_type;
+  auto pick = [&](auto nv_tag) {
+    if (update && dots) go(nv_tag, T{}, T{});
+    else if (update) go(nv_tag, T{}, F{});
+    else go(nv_tag, F{}, T{});
+  };
+  switch (nv) {
+#define RTE_NV_CASE(K) case K: pick(std::integral_constant<int, K>{}); break;
+    RTE_NV_CASE(1) RTE_NV_CASE(2) RTE_NV_CASE(3) RTE_NV_CASE(4) RTE_NV_CASE(5) RTE_NV_CASE(6) RTE_NV_CASE(7)
+    RTE_NV_CASE(8) RTE_NV_CASE(9) RTE_NV_CASE(10) RTE_NV_CASE(11) RTE_NV_CASE(12) RTE_NV_CASE(13)
+    RTE_NV_CASE(14) RTE_NV_CASE(15) RTE_NV_CASE(16) RTE_NV_CASE(17) RTE_NV_CASE(18) RTE_NV_CASE(19)
+    RTE_NV_CASE(20) RTE_NV_CASE(21) RTE_NV_CASE(22) RTE_NV_CASE(23) RTE_NV_CASE(24) RTE_NV_CASE(25)
+    RTE_NV_CASE(26) RTE_NV_CASE(27) RTE_NV_CASE(28) RTE_NV_CASE(29) RTE_NV_CASE(30) RTE_NV_CASE(31)
+    RTE_NV_CASE(32)
+#undef RTE_NV_CASE
+    default:
+      set_error("gmres: restart > 32 is not supported by the fused CGS kernels");
+      throw Fail{RTE_EINVAL};
+  }
+  after_launch("cgs_kernel");
+}
+
+template <typename T>
+static void launch_norm(const GmresWork& W, const T* x, float* xo, double* out, cudaStream_t st) {
+  RedArgs ra{W.partials, W.counters, out, 1, W.nblk};
+  norm_kernel<T><<<dim3(W.nblk, W.B), kThreads, 0, st>>>(x, xo, W.ns, ra);
+  after_launch("norm_kernel");
+}
+
+}  // namespace rte
+
+using namespace rte;
+
+// Workspace cache keyed by problem (freed by rte_destroy through free_gmres_work).
+static std::mutex g_wmu;
+static std::map<const rte_problem*, GmresWork> g_work;
+
+void rte::free_gmres_work(const rte_problem* p) {
+  std::lock_guard<std::mutex> lk(g_wmu);
+  auto it = g_work.find(p);
+  if (it != g_work.end()) {
+    it->second.release();
+    g_work.erase(it);
+  }
+}
+
+static GmresWork& get_work(const rte_problem* p, int m) {
+  std::lock_guard<std::mutex> lk(g_wmu);
+  GmresWork& W = g_work[p];
+  if (W.V && W.m >= m) return W;
+  W.release();
+  W.B = p->B;
+  W.m = m;
+  W.ns = p->n / p->B;
+  int64_t n4 = W.ns / 4;
+  int want = std::max(1, (2 * num_sms() + W.B - 1) / W.B);
+  W.nblk = (int)std::max<int64_t>(1, std::min<int64_t>(want, (n4 + kThreads - 1) / kThreads));
+  const int64_t n = p->n;
+  const int B = p->B;
+  W.V = dalloc<float>((size_t)(m + 1) * n);
+  W.w = dalloc<float>(n);
+  W.z = dalloc<float>(n);
+  W.r64 = dalloc<double>(n);
+  W.Hr = dalloc<double>((size_t)B * (m + 1) * m);
+  W.Hraw = dalloc<double>((size_t)B * (m + 1) * m);
+  W.cs = dalloc<double>((size_t)B * m);
+  W.sn = dalloc<double>((size_t)B * m);
+  W.g = dalloc<double>((size_t)B * (m + 1));
+  W.alpha = dalloc<double>((size_t)B * (m + 1));
+  W.h1 = dalloc<double>((size_t)B * (kMaxRestart + 2));
+  W.h2 = dalloc<double>((size_t)B * (kMaxRestart + 2));
+  W.h3 = dalloc<double>((size_t)B * (kMaxRestart + 2));
+  W.coef = dalloc<double>((size_t)B * (m + 1));
+  W.bnorm = dalloc<double>(B);
+  W.rn2 = dalloc<double>(B);
+  W.partials = dalloc<double>((size_t)B * W.nblk * (kMaxRestart + 2));
+  W.counters = dalloc<unsigned>(B);
+  W.active = dalloc<int>(B);
+  W.kcols = dalloc<int>(B);
+  W.done = dalloc<int>(B);
+  W.st_dev = dalloc<Status>(B);
+  RTE_CHECK_CUDA(cudaMemset(W.counters, 0, sizeof(unsigned) * B));
+  RTE_CHECK_CUDA(cudaMemset(W.Hraw, 0, sizeof(double) * B * (m + 1) * m));
+  RTE_CHECK_CUDA(cudaHostAlloc(&W.st_host, sizeof(Status) * B, cudaHostAllocDefault));
+  return W;
+}
+
+extern "C" rte_status gmres_solve(const rte_problem* p, const mgnet_net* net, const float* b_dev, double* x_dev,
+                                  const gmres_opts* opts, gmres_report* rep, void* stream) {
+  try {
+    RTE_REQUIRE(p && b_dev && x_dev && opts && rep, "gmres_solve: NULL argument");
+    const int m = opts->restart;
+    RTE_REQUIRE(m >= 1 && m <= 32, "gmres_solve: restart must be in [1, 32]");
+    RTE_REQUIRE(opts->maxit >= 0, "gmres_solve: maxit must be >= 0");
+    RTE_REQUIRE(opts->rtol > 0.0, "gmres_solve: rtol must be > 0");
+    RTE_REQUIRE(opts->precond == 0 || (opts->precond == 1 && net), "gmres_solve: precond=1 requires a net");
+    RTE_REQUIRE(!net || net->prob == p, "gmres_solve: net was created for another problem");
+    cudaStream_t st = as_stream(stream);
+    GmresWork& W = get_work(p, m);
+    const int B = p->B;
+    const int64_t n = p->n;
+    const int hld = kMaxRestart + 2;
+    const bool sel = opts->reorth == 1;
+    std::vector<int> total(B, 0), restarts(B, 0), brk(B, 0), conv(B, 0), done(B, 0);
+    std::vector<double> est_last(B, 0.0), relres(B, 0.0);
+    for (int b = 0; b < B; ++b) {
+      rep[b].iterations = 0;
+      rep[b].restarts = 0;
+      rep[b].converged = 0;
+      rep[b].breakdown = 0;
+      rep[b].relres_true = 0;
+      rep[b].relres_est = 0;
+    }
+    RTE_CHECK_CUDA(cudaMemsetAsync(W.done, 0, sizeof(int) * B, st));
+    // ||b|| per sample
+    launch_norm<float>(W, b_dev, nullptr, W.rn2, st);
+    {
+      std::vector<double> bn2(B);
+      RTE_CHECK_CUDA(cudaMemcpyAsync(bn2.data(), W.rn2, sizeof(double) * B, cudaMemcpyDeviceToHost, st));
+      RTE_CHECK_CUDA(cudaStreamSynchronize(st));
+      for (double& v : bn2) v = sqrt(v);
+      RTE_CHECK_CUDA(cudaMemcpyAsync(W.bnorm, bn2.data(), sizeof(double) * B, cudaMemcpyHostToDevice, st));
+      RTE_CHECK_CUDA(cudaStreamSynchronize(st));
+    }
+    bool first_cycle = true;
+    int total_all = 0;  // lockstep inner iterations
+    while (true) {
+      // r = b - A x (fp64), v0 = r (fp32, unnormalised), ||r||^2
+      launch_apply_f64(p, x_dev, W.r64, b_dev, st);
+      launch_norm<double>(W, W.r64, W.V, W.rn2, st);
+      int stop_all = (total_all >= opts->maxit) ? 1 : 0;
+      cycle_init_kernel<<<(B + 63) / 64, 64, 0, st>>>(B, W.rn2, W.bnorm, opts->rtol, stop_all, W.alpha, m + 1, W.g,
+                                                      m + 1, W.active, W.kcols, W.done, W.st_dev);
+      after_launch("cycle_init_kernel");
+      RTE_CHECK_CUDA(cudaMemcpyAsync(W.st_host, W.st_dev, sizeof(Status) * B, cudaMemcpyDeviceToHost, st));
+      RTE_CHECK_CUDA(cudaStreamSynchronize(st));
+      int n_active = 0;
+      for (int b = 0; b < B; ++b) {
+        relres[b] = W.st_host[b].est;
+        conv[b] = W.st_host[b].converged;
+        if (W.st_host[b].active) {
+          ++n_active;
+          ++restarts[b];
+        }
+      }
+      if (n_active == 0) break;
+      for (int j = 0; j < m; ++j) {
+        // z = P(alpha_j V_j)  or  alpha_j V_j
+        const float* vj = W.V + (size_t)j * n;
+        if (opts->precond == 1) {
+          vcycle_run(net, vj, W.z, true, W.alpha + j, m + 1, st);
+          launch_apply_f32(p, W.z, W.w, nullptr, 0, st);
+        } else {
+          launch_apply_f32(p, vj, W.w, W.alpha + j, m + 1, st);
+        }
+        float* vnext = W.V + (size_t)(j + 1) * n;
+        launch_cgs(W, j + 1, false, true, nullptr, W.w, nullptr, W.h1, st);      // pass A
+        const double* h2 = nullptr;
+        const double* nrm = nullptr;
+        if (!sel) {
+          launch_cgs(W, j + 1, true, true, W.h1, W.w, vnext, W.h2, st);          // pass B
+          launch_cgs(W, j + 1, true, false, W.h2, vnext, vnext, W.h3, st);       // pass C
+          h2 = W.h2;
+          nrm = W.h3;  // update-only passes put ||.||^2 at index 0
+        } else {
+          launch_cgs(W, j + 1, true, false, W.h1, W.w, vnext, W.h2, st);         // CGS1 only
+          h2 = nullptr;
+          nrm = W.h2;
+        }
+        ++total_all;
+        int last = (total_all >= opts->maxit) ? 1 : 0;
+        givens_kernel<<<(B + 63) / 64, 64, 0, st>>>(B, j, m, W.h1, h2, hld, nrm, hld, W.Hr, W.Hraw,
+                                                    first_cycle ? 1 : 0, W.cs, W.sn, W.g, W.alpha, m + 1, W.bnorm,
+                                                    opts->rtol, last, W.active, W.kcols, W.st_dev);
+        after_launch("givens_kernel");
+        RTE_CHECK_CUDA(cudaMemcpyAsync(W.st_host, W.st_dev, sizeof(Status) * B, cudaMemcpyDeviceToHost, st));
+        RTE_CHECK_CUDA(cudaStreamSynchronize(st));
+        int still = 0;
+        for (int b = 0; b < B; ++b) {
+          const Status& s = W.st_host[b];
+          bool was_active = (s.active || s.kcols == j + 1);
+          if (!was_active) continue;
+          if (rep[b].history) rep[b].history[total[b]] = s.est;
+          ++total[b];
+          est_last[b] = s.est;
+          if (s.breakdown) brk[b] = 1;
+          if (s.active) ++still;
+        }
+        if (still == 0) break;
+      }
+      if (first_cycle) {
+        for (int b = 0; b < B; ++b)
+          if (rep[b].hessenberg)
+            RTE_CHECK_CUDA(cudaMemcpyAsync(rep[b].hessenberg, W.Hraw + (size_t)b * (m + 1) * m,
+                                           sizeof(double) * (m + 1) * m, cudaMemcpyDeviceToHost, st));
+      }
+      first_cycle = false;
+      // x += P(V y)
+      backsolve_kernel<<<(B + 63) / 64, 64, 0, st>>>(B, m, W.Hr, W.g, W.alpha, m + 1, W.kcols, W.coef, m + 1);
+      after_launch("backsolve_kernel");
+      combine_kernel<<<dim3(W.nblk, B), kThreads, 0, st>>>(W.V, n, W.coef, m + 1, W.kcols, W.w, W.ns, W.nblk);
+      after_launch("combine_kernel");
+      const float* corr = W.w;
+      if (opts->precond == 1) {
+        vcycle_run(net, W.w, W.z, true, nullptr, 0, st);
+        corr = W.z;
+      }
+      axpy64_kernel<<<dim3(W.nblk, B), kThreads, 0, st>>>(x_dev, corr, W.kcols, W.ns, W.nblk);
+      after_launch("axpy64_kernel");
+      // samples that broke down stop (oracle: breakdown ends the solve)
+      bool any_brk = false;
+      for (int b = 0; b < B; ++b)
+        if (brk[b] && !done[b]) { done[b] = 1; any_brk = true; }
+      if (any_brk) RTE_CHECK_CUDA(cudaMemcpyAsync(W.done, done.data(), sizeof(int) * B, cudaMemcpyHostToDevice, st));
+    }
+    for (int b = 0; b < B; ++b) {
+      rep[b].iterations = total[b];
+      rep[b].restarts = restarts[b];
+      rep[b].converged = conv[b];
+      rep[b].breakdown = brk[b];
+      rep[b].relres_true = relres[b];
+      rep[b].relres_est = est_last[b];
+    }
+    RTE_CHECK_CUDA(cudaStreamSynchronize(st));
+    return RTE_OK;
+  } catch (const Fail& f) {
+    return f.st;
+  } catch (const std::exception& e) {
+    set_error(std::string("internal: ") + e.what());
+    return RTE_EINTERNAL;
+  }
+}

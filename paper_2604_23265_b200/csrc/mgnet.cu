@@ -1,0 +1,380 @@
+// MgNet V-cycle (§3.3; R12-R20): linear smoother
+//   u <- u + B * (f - A * u)   (modulation a = abar = 1, R13),
+// stride-2 3x3 conv restriction of the residual, stride-2 4x4 transposed-conv prolongation,
+// channel doubling C_l = C0 2^l, 1x1 lift Lambda (M -> C0) and head Theta (C0 -> M) with the
+// pass-through P(r) = r + Theta u^0 (R17).  Activations are NHWC float32.
+//
+// Convolutions run as implicit GEMMs: D[pixels x Co] = sum_taps X_tap[pixels x Ci] . W_tap[Ci x Co].
+// This file holds the SIMT (fp32 FMA) implicit-GEMM kernel used for every conv shape; the
+// tcgen05 3xTF32 kernel (conv_tc.cu) takes the shapes it supports.
+#include <algorithm>
+#include <memory>
+#include <vector>
+
+#include "common.h"
+#include "mgnet.h"
+
+namespace rte {
+namespace {
+
+// MODE 0: KSxKS conv, stride 1, pad KS/2.  MODE 1: 3x3 conv, stride 2, pad 1.
+// MODE 2: 4x4 transposed conv, stride 2, pad 1, one output parity class per blockIdx.z % 4.
+// out = (addend ? add_scale*addend : 0) + sign * in_scale * acc
+template <int MODE, int KS, int TCO>
+__global__ void __launch_bounds__(256) conv_simt_kernel(
+    int Hi, int Wi, int Ci, int Ho, int Wo, int Co, const float* __restrict__ in, const float* __restrict__ Wk,
+    float* out, const float* addend, float sign, const double* __restrict__ alpha, int alpha_stride,
+    int alpha_on_input, int alpha_on_addend) {
+  constexpr int TP = 4096 / TCO;
+  constexpr int KC = 16;
+  constexpr int TX = TCO / 4;
+  constexpr int NTAPS = (MODE == 2) ? 4 : KS * KS;
+  __shared__ __align__(16) float As[KC][TP + 4];
+  __shared__ __align__(16) float Bs[KC][TCO + 4];
+  const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
+  int bz = blockIdx.z;
+  int py = 0, px = 0;
+  int Hc = Ho, Wc = Wo;  // extent of the pixel set this block iterates
+  if (MODE == 2) {
+    int cls = bz & 3;
+    bz >>= 2;
+    py = cls >> 1;
+    px = cls & 1;
+    Hc = Ho / 2;
+    Wc = Wo / 2;
+  }
+  const int b = bz;
+  const int64_t npix = (int64_t)Hc * Wc;
+  const int64_t p0 = (int64_t)blockIdx.x * TP;
+  const int co0 = blockIdx.y * TCO;
+  const float* inb = in + (int64_t)b * Hi * Wi * Ci;
+  float acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[a][c] = 0.f;
+
+  for (int tap = 0; tap < NTAPS; ++tap) {
+    int ky, kx;
+    if (MODE == 2) {  // taps with ky = (py+1)%2 + 2*ty_, kx = (px+1)%2 + 2*tx_
+      ky = ((py + 1) & 1) + 2 * (tap >> 1);
+      kx = ((px + 1) & 1) + 2 * (tap & 1);
+    } else {
+      ky = tap / KS;
+      kx = tap % KS;
+    }
+    const int wtap = (MODE == 2) ? (ky * 4 + kx) : tap;
+    for (int ci0 = 0; ci0 < Ci; ci0 += KC) {
+      for (int e = tid; e < TP * KC; e += 256) {
+        int pl = e / KC, kk = e % KC;
+        int64_t p = p0 + pl;
+        float v = 0.f;
+        if (p < npix && ci0 + kk < Ci) {
+          int yo = (int)(p / Wc), xo = (int)(p % Wc);
+          int yi, xi;
+          bool ok;
+          if (MODE == 0) {
+            yi = yo + ky - KS / 2; xi = xo + kx - KS / 2;
+            ok = true;
+          } else if (MODE == 1) {
+            yi = 2 * yo + ky - 1; xi = 2 * xo + kx - 1;
+            ok = true;
+          } else {
+            int Y = 2 * yo + py, X = 2 * xo + px;    // output pixel
+            int yy = Y + 1 - ky, xx = X + 1 - kx;     // = 2*yi, 2*xi (even by construction)
+            yi = yy >> 1; xi = xx >> 1;
+            ok = (yy >= 0) && (xx >= 0);
+          }
+          ok = ok && yi >= 0 && yi < Hi && xi >= 0 && xi < Wi;
+          if (ok) v = inb[((int64_t)yi * Wi + xi) * Ci + ci0 + kk];
+        }
+        As[kk][pl] = v;
+      }
+      for (int e = tid; e < KC * TCO; e += 256) {
+        int kk = e / TCO, o = e % TCO;
+        float v = 0.f;
+        if (ci0 + kk < Ci && co0 + o < Co) v = Wk[((int64_t)wtap * Ci + ci0 + kk) * Co + co0 + o];
+        Bs[kk][o] = v;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int kk = 0; kk < KC; ++kk) {
+        float av[4], bv[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) av[a] = As[kk][ty * 4 + a];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) bv[c] = Bs[kk][tx * 4 + c];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) acc[a][c] = fmaf(av[a], bv[c], acc[a][c]);
+      }
+      __syncthreads();
+    }
+  }
+  const float al = alpha ? alpha[(int64_t)b * alpha_stride] : 1.f;
+  const float s_in = (alpha_on_input ? al : 1.f) * sign;
+  const float s_add = alpha_on_addend ? al : 1.f;
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    int64_t p = p0 + ty * 4 + a;
+    if (p >= npix) continue;
+    int64_t opix;
+    if (MODE == 2) {
+      int yo = (int)(p / Wc), xo = (int)(p % Wc);
+      opix = (int64_t)(2 * yo + py) * Wo + (2 * xo + px);
+    } else {
+      opix = p;
+    }
+    int64_t base = ((int64_t)b * Ho * Wo + opix) * Co;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      int co = co0 + tx * 4 + c;
+      if (co >= Co) continue;
+      float v = s_in * acc[a][c];
+      if (addend) v += s_add * addend[base + co];
+      out[base + co] = v;
+    }
+  }
+}
+
+}  // namespace
+
+void launch_conv(const ConvDesc& d, const float* in, const float* Wk, float* out, const float* addend, float sign,
+                 const double* alpha, int alpha_stride, bool alpha_on_input, bool alpha_on_addend,
+                 cudaStream_t st) {
+  if (conv_tc_try(d, in, out, addend, sign, alpha, alpha_stride, alpha_on_input, alpha_on_addend, st)) return;
+  auto go = [&](auto mode_tag, auto ks_tag, auto tco_tag) {
+    constexpr int MODE = decltype(mode_tag)::value;
+    constexpr int KS = decltype(ks_tag)::value;
+    constexpr int TCO = decltype(tco_tag)::value;
+    constexpr int TP = 4096 / TCO;
+    int64_t npix = (MODE == 2) ? (int64_t)(d.Ho / 2) * (d.Wo / 2) : (int64_t)d.Ho * d.Wo;
+    dim3 grid((unsigned)((npix + TP - 1) / TP), (unsigned)((d.Co + TCO - 1) / TCO),
+              (unsigned)(d.B * (MODE == 2 ? 4 : 1)));
+    conv_simt_kernel<MODE, KS, TCO><<<grid, 256, 0, st>>>(d.Hi, d.Wi, d.Ci, d.Ho, d.Wo, d.Co, in, Wk, out, addend,
+                                                          sign, alpha, alpha_stride, alpha_on_input ? 1 : 0,
+                                                          alpha_on_addend ? 1 : 0);
+  };
+  auto by_tco = [&](auto mode_tag, auto ks_tag) {
+    if (d.Co <= 16) go(mode_tag, ks_tag, std::integral_constant<int, 16>{});
+    else if (d.Co <= 32) go(mode_tag, ks_tag, std::integral_constant<int, 32>{});
+    else go(mode_tag, ks_tag, std::integral_constant<int, 64>{});
+  };
+  using I0 = std::integral_constant<int, 0>;
+  using I1 = std::integral_constant<int, 1>;
+  using I2 = std::integral_constant<int, 2>;
+  using K1 = std::integral_constant<int, 1>;
+  using K3 = std::integral_constant<int, 3>;
+  using K4 = std::integral_constant<int, 4>;
+  if (d.mode == 0 && d.ks == 1) by_tco(I0{}, K1{});
+  else if (d.mode == 0) by_tco(I0{}, K3{});
+  else if (d.mode == 1) by_tco(I1{}, K3{});
+  else by_tco(I2{}, K4{});
+  after_launch("conv_simt_kernel");
+}
+
+}  // namespace rte
+
+using namespace rte;
+
+// ---- weights --------------------------------------------------------------------------
+// Reorganise a PyTorch-layout weight into the implicit-GEMM operand layouts:
+//   kn : [tap][ci][co]  (SIMT B operand, co contiguous)
+//   nk : [co][tap][ci]  (tensor-core B operand, N x K with K contiguous; kept on host until
+//                        conv_tc_prepare uploads its tf32 hi/lo split)
+// kind 0: OIHW [Co][Ci][k][k] (k = 1 or 3);  kind 1: IOHW [Ci][Co][4][4] (conv_transpose).
+namespace rte {
+
+void ConvW::build(const float* w, int kind_, int Co_, int Ci_, int ks_) {
+  kind = kind_;
+  Co = Co_;
+  Ci = Ci_;
+  ks = ks_;
+  taps = ks * ks;
+  std::vector<float> kn((size_t)taps * Ci * Co), nk((size_t)taps * Ci * Co);
+  for (int co = 0; co < Co; ++co)
+    for (int ci = 0; ci < Ci; ++ci)
+      for (int ky = 0; ky < ks; ++ky)
+        for (int kx = 0; kx < ks; ++kx) {
+          float v = (kind == 1) ? w[(((size_t)ci * Co + co) * ks + ky) * ks + kx]
+                                : w[(((size_t)co * Ci + ci) * ks + ky) * ks + kx];
+          int tap = ky * ks + kx;
+          kn[((size_t)tap * Ci + ci) * Co + co] = v;
+          nk[((size_t)co * taps + tap) * Ci + ci] = v;
+        }
+  d_kn = dalloc<float>(kn.size());
+  upload(d_kn, kn.data(), kn.size());
+  host_nk = std::move(nk);
+}
+
+void ConvW::release() {
+  dfree(d_kn);
+  dfree(d_hi);
+  dfree(d_lo);
+  d_kn = d_hi = d_lo = nullptr;
+}
+
+}  // namespace rte
+
+extern "C" {
+
+void mgnet_destroy(mgnet_net* net) {
+  if (!net) return;
+  for (auto& c : net->convs) c.release();
+  for (auto& lv : net->lv) {
+    dfree(lv.f);
+    dfree(lv.u);
+    dfree(lv.t);
+  }
+  delete net;
+}
+
+rte_status mgnet_create(const rte_problem* p, int levels, int c0, int nu, const float* weights, size_t n_floats,
+                        mgnet_net** out) {
+  mgnet_net* net = nullptr;
+  try {
+    RTE_REQUIRE(p && weights && out, "mgnet_create: NULL argument");
+    *out = nullptr;
+    RTE_REQUIRE(levels >= 1 && levels <= 12, "mgnet_create: levels must be in [1,12]");
+    RTE_REQUIRE(c0 >= 1 && nu >= 0, "mgnet_create: c0 >= 1 and nu >= 0 required");
+    RTE_REQUIRE(p->N % (1 << (levels - 1)) == 0, "mgnet_create: N must be divisible by 2^(levels-1)");
+    const int M = p->M;
+    size_t need = (size_t)c0 * M * 2;
+    for (int l = 0; l < levels; ++l) {
+      size_t C = (size_t)c0 << l;
+      need += (size_t)(1 + 2 * nu) * C * C * 9;
+      if (l < levels - 1) need += 2 * C * C * 9 + 2 * C * C * 16;
+    }
+    RTE_REQUIRE(n_floats == need, "mgnet_create: weight count mismatch (expected " + std::to_string(need) +
+                                      ", got " + std::to_string(n_floats) + ")");
+    net = new mgnet_net();
+    net->prob = p;
+    net->B = p->B;
+    net->N = p->N;
+    net->M = M;
+    net->L = levels;
+    net->C0 = c0;
+    net->nu = nu;
+    const float* w = weights;
+    auto take = [&](int kind, int Co, int Ci, int ks) {
+      ConvW cw;
+      cw.build(w, kind, Co, Ci, ks);
+      w += (size_t)Co * Ci * ks * ks;
+      net->convs.push_back(std::move(cw));
+      return (int)net->convs.size() - 1;
+    };
+    net->lift = take(0, c0, M, 1);
+    net->lv.resize(levels);
+    for (int l = 0; l < levels; ++l) {
+      int C = c0 << l;
+      Level& L = net->lv[l];
+      L.C = C;
+      L.H = p->N >> l;
+      L.A = take(0, C, C, 3);
+      for (int i = 0; i < nu; ++i) L.Bpre.push_back(take(0, C, C, 3));
+      for (int i = 0; i < nu; ++i) L.Bpost.push_back(take(0, C, C, 3));
+      if (l < levels - 1) {
+        L.R = take(0, 2 * C, C, 3);
+        L.P = take(1, C, 2 * C, 4);  // IOHW: Ci = 2C (coarse), Co = C (fine)
+      }
+      size_t act = (size_t)p->B * L.H * L.H * C;
+      L.f = dalloc<float>(act);
+      L.u = dalloc<float>(act);
+      L.t = dalloc<float>(act);
+    }
+    net->head = take(0, M, c0, 1);
+    conv_tc_prepare(net);
+    *out = net;
+    return RTE_OK;
+  } catch (const Fail& f) {
+    mgnet_destroy(net);
+    return f.st;
+  } catch (const std::exception& e) {
+    mgnet_destroy(net);
+    set_error(std::string("internal: ") + e.what());
+    return RTE_EINTERNAL;
+  }
+}
+
+rte_status mgnet_vcycle(const mgnet_net* net, const float* r_dev, float* z_dev, int add_identity, void* stream) {
+  try {
+    RTE_REQUIRE(net && r_dev && z_dev, "mgnet_vcycle: NULL argument");
+    RTE_REQUIRE((const void*)r_dev != (const void*)z_dev, "mgnet_vcycle: r and z must not alias");
+    vcycle_run(net, r_dev, z_dev, add_identity != 0, nullptr, 0, as_stream(stream));
+    return RTE_OK;
+  } catch (const Fail& f) {
+    return f.st;
+  }
+}
+
+}  // extern "C"
+
+namespace rte {
+
+static ConvDesc desc_for(const mgnet_net* n, int mode, int ks, int H_in, int Ci, int H_out, int Co) {
+  ConvDesc d;
+  d.B = n->B;
+  d.mode = mode;
+  d.ks = ks;
+  d.Hi = d.Wi = H_in;
+  d.Ci = Ci;
+  d.Ho = d.Wo = H_out;
+  d.Co = Co;
+  return d;
+}
+
+// One V-cycle.  alpha (device, per sample, stride alpha_stride) scales the input r (the
+// Krylov vector is stored unnormalised, see krylov.cu); NULL means 1.
+void vcycle_run(const mgnet_net* net, const float* r, float* z, bool add_identity, const double* alpha,
+                int alpha_stride, cudaStream_t st) {
+  const int L = net->L, M = net->M, N = net->N;
+  auto conv = [&](int widx, ConvDesc d, const float* in, float* out, const float* addend, float sign,
+                  bool a_in = false, bool a_add = false) {
+    d.w = &net->convs[widx];
+    launch_conv(d, in, net->convs[widx].d_kn, out, addend, sign, alpha, alpha_stride, a_in, a_add, st);
+  };
+  // f^0 = Lambda (alpha r)
+  {
+    const Level& L0 = net->lv[0];
+    conv(net->lift, desc_for(net, 0, 1, N, M, N, L0.C), r, L0.f, nullptr, 1.f, true, false);
+  }
+  auto smooth = [&](int l, int bidx, bool first) {
+    const Level& V = net->lv[l];
+    ConvDesc d = desc_for(net, 0, 3, V.H, V.C, V.H, V.C);
+    if (first) {  // u = 0: u <- B * f  (A * 0 = 0 exactly)
+      conv(bidx, d, V.f, V.u, nullptr, 1.f);
+    } else {
+      conv(V.A, d, V.u, V.t, V.f, -1.f);   // t = f - A * u
+      conv(bidx, d, V.t, V.u, V.u, 1.f);   // u = u + B * t
+    }
+  };
+  for (int l = 0; l < L; ++l) {
+    const Level& V = net->lv[l];
+    std::vector<int> steps(V.Bpre.begin(), V.Bpre.end());
+    if (l == L - 1) steps.insert(steps.end(), V.Bpost.begin(), V.Bpost.end());
+    if (steps.empty()) RTE_CHECK_CUDA(cudaMemsetAsync(V.u, 0, sizeof(float) * (size_t)net->B * V.H * V.H * V.C, st));
+    for (size_t i = 0; i < steps.size(); ++i) smooth(l, steps[i], i == 0);
+    if (l < L - 1) {
+      const Level& W = net->lv[l + 1];
+      ConvDesc d = desc_for(net, 0, 3, V.H, V.C, V.H, V.C);
+      if (steps.empty()) {
+        conv(V.R, desc_for(net, 1, 3, V.H, V.C, W.H, W.C), V.f, W.f, nullptr, 1.f);
+      } else {
+        conv(V.A, d, V.u, V.t, V.f, -1.f);                                          // t = f - A * u
+        conv(V.R, desc_for(net, 1, 3, V.H, V.C, W.H, W.C), V.t, W.f, nullptr, 1.f);  // f^{l+1} = R *_2 t
+      }
+    }
+  }
+  for (int l = L - 2; l >= 0; --l) {
+    const Level& V = net->lv[l];
+    const Level& W = net->lv[l + 1];
+    conv(V.P, desc_for(net, 2, 4, W.H, W.C, V.H, V.C), W.u, V.u, V.u, 1.f);   // u += P^T *_2 u^{l+1}
+    for (size_t i = 0; i < V.Bpost.size(); ++i) smooth(l, V.Bpost[i], false);
+  }
+  // z = [alpha r] + Theta u^0
+  const Level& L0 = net->lv[0];
+  conv(net->head, desc_for(net, 0, 1, N, L0.C, N, M), L0.u, z, add_identity ? r : nullptr, 1.f, false, true);
+}
+
+}  // namespace rte

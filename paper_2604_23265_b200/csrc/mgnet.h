@@ -1,0 +1,55 @@
+// Internal MgNet structures (NOT part of the ABI).
+#pragma once
+
+#include <vector>
+
+#include "common.h"
+
+namespace rte {
+
+struct ConvW {
+  int kind = 0;       // 0: OIHW conv, 1: IOHW conv_transpose
+  int Co = 0, Ci = 0, ks = 0, taps = 0;
+  float* d_kn = nullptr;   // [tap][ci][co]
+  float* d_hi = nullptr;   // tensor-core operand: [co][tap][ci] tf32 hi
+  float* d_lo = nullptr;   //                       tf32 lo
+  std::vector<float> host_nk;  // [co][tap][ci]
+  void build(const float* w, int kind, int Co, int Ci, int ks);
+  void release();
+};
+
+struct ConvDesc {
+  int B = 1, mode = 0, ks = 3;       // mode 0: stride-1 (ks 1 or 3), 1: stride-2 3x3, 2: transposed 4x4 s2
+  int Hi = 0, Wi = 0, Ci = 0, Ho = 0, Wo = 0, Co = 0;
+  const ConvW* w = nullptr;
+};
+
+struct Level {
+  int C = 0, H = 0;
+  int A = -1, R = -1, P = -1;
+  std::vector<int> Bpre, Bpost;
+  float* f = nullptr;   // [B][H][H][C]
+  float* u = nullptr;
+  float* t = nullptr;
+};
+
+void launch_conv(const ConvDesc& d, const float* in, const float* Wk, float* out, const float* addend, float sign,
+                 const double* alpha, int alpha_stride, bool alpha_on_input, bool alpha_on_addend, cudaStream_t st);
+// tensor-core path (conv_tc.cu): returns false when the shape is not supported there.
+bool conv_tc_try(const ConvDesc& d, const float* in, float* out, const float* addend, float sign,
+                 const double* alpha, int alpha_stride, bool alpha_on_input, bool alpha_on_addend, cudaStream_t st);
+void conv_tc_prepare(struct ::mgnet_net* net);
+
+void vcycle_run(const struct ::mgnet_net* net, const float* r, float* z, bool add_identity, const double* alpha,
+                int alpha_stride, cudaStream_t st);
+
+}  // namespace rte
+
+struct mgnet_net {
+  const rte_problem* prob = nullptr;
+  int B = 1, N = 0, M = 0, L = 0, C0 = 0, nu = 0;
+  std::vector<rte::ConvW> convs;
+  std::vector<rte::Level> lv;
+  int lift = -1, head = -1;
+  bool tc = false;
+};

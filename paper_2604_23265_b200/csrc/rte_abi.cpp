@@ -1,0 +1,347 @@
+// C-ABI entry points for the problem (rte_setup / rte_rhs / rte_apply / rte_apply_f64) and
+// the library's error/launch bookkeeping.  Host setup runs in fp64 (PAPER.md:29-33, 79-94,
+// 113-117); everything on the per-iteration path runs in the CUDA kernels.
+#include <math.h>
+#include <string.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "common.h"
+
+namespace rte {
+
+static thread_local std::string g_err;
+static thread_local int64_t g_launches = 0;
+
+void set_error(const std::string& msg) { g_err = msg; }
+
+void after_launch(const char* what) {
+  ++g_launches;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string("launch of ") + what + " failed: " + cudaGetErrorString(e));
+    throw Fail{RTE_ECUDA};
+  }
+}
+
+void dfree(void* p) {
+  if (p) cudaFree(p);
+}
+
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+  }
+  return n;
+}
+
+// ---- angular quadrature (R2, R3) ------------------------------
+// Gauss-Legendre nodes/weights on [-1,1] by Newton iteration on P_n (three-term recurrence).
+static void gauss_legendre(int n, std::vector<double>& x, std::vector<double>& wt) {
+  x.assign(n, 0.0);
+  wt.assign(n, 0.0);
+  for (int i = 0; i < n; ++i) {
+    double z = cos(M_PI * (i + 0.75) / (n + 0.5));
+    double dp = 0.0;
+    for (int it = 0; it < 100; ++it) {
+      double p0 = 1.0, p1 = z;
+      for (int k = 2; k <= n; ++k) {
+        double p2 = ((2.0 * k - 1.0) * z * p1 - (k - 1.0) * p0) / k;
+        p0 = p1;
+        p1 = p2;
+      }
+      if (n == 1) { p1 = z; p0 = 1.0; }
+      dp = n * (z * p1 - p0) / (z * z - 1.0);
+      double dz = p1 / dp;
+      z -= dz;
+      if (fabs(dz) < 1e-16) break;
+    }
+    // recompute derivative at the converged node
+    double p0 = 1.0, p1 = z;
+    for (int k = 2; k <= n; ++k) {
+      double p2 = ((2.0 * k - 1.0) * z * p1 - (k - 1.0) * p0) / k;
+      p0 = p1;
+      p1 = p2;
+    }
+    dp = n * (z * p1 - p0) / (z * z - 1.0);
+    x[i] = -z;  // ascending
+    wt[i] = 2.0 / ((1.0 - z * z) * dp * dp);
+  }
+}
+
+static void product_quadrature(int np, int na, std::vector<double>& c, std::vector<double>& s,
+                               std::vector<double>& zeta, std::vector<double>& w) {
+  std::vector<double> x, a;
+  gauss_legendre(np, x, a);
+  int nq = na / 4;
+  c.clear(); s.clear(); zeta.clear(); w.clear();
+  for (int quad = 0; quad < 4; ++quad)
+    for (int p = 0; p < np; ++p)
+      for (int kk = 0; kk < nq; ++kk) {
+        int k = quad * nq + kk;
+        double th = (k + 0.5) * 2.0 * M_PI / na;
+        double z = 0.5 * (x[p] + 1.0);
+        double r = sqrt(1.0 - z * z);
+        c.push_back(r * cos(th));
+        s.push_back(r * sin(th));
+        zeta.push_back(z);
+        w.push_back(4.0 * M_PI * (0.5 * a[p]) / na);
+      }
+}
+
+// Row-normalised HG scattering matrix S = K W (R4, R5).
+static void hg_matrix(const std::vector<double>& c, const std::vector<double>& s, const std::vector<double>& z,
+                      const std::vector<double>& w, double g, double* S) {
+  int M = (int)c.size();
+  auto hgf = [g](double mu) { return (1.0 - g * g) / pow(1.0 + g * g - 2.0 * g * mu, 1.5); };
+  std::vector<double> kh(M);
+  for (int m = 0; m < M; ++m) {
+    double rs = 0.0;
+    for (int n = 0; n < M; ++n) {
+      double pl = c[m] * c[n] + s[m] * s[n];
+      double zz = z[m] * z[n];
+      kh[n] = 0.5 * (hgf(pl + zz) + hgf(pl - zz));
+      rs += kh[n] * w[n];
+    }
+    for (int n = 0; n < M; ++n) S[(size_t)m * M + n] = kh[n] / rs * w[n];
+  }
+}
+
+// Round-to-nearest TF32 (10 explicit mantissa bits), as cvt.rna.tf32.f32.
+static float tf32_rna(float v) {
+  uint32_t u;
+  memcpy(&u, &v, 4);
+  if ((u & 0x7f800000u) != 0x7f800000u) u = (u + 0x1000u) & 0xffffe000u;
+  float r;
+  memcpy(&r, &u, 4);
+  return r;
+}
+
+}  // namespace rte
+
+using namespace rte;
+
+#define RTE_API_BEGIN try {
+#define RTE_API_END                                   \
+  }                                                   \
+  catch (const Fail& f) { return f.st; }              \
+  catch (const std::exception& e) {                   \
+    set_error(std::string("internal: ") + e.what());  \
+    return RTE_EINTERNAL;                             \
+  }                                                   \
+  return RTE_OK;
+
+extern "C" {
+
+const char* rte_last_error(void) { return g_err.c_str(); }
+
+int64_t rte_launch_count(int reset) {
+  int64_t v = g_launches;
+  if (reset) g_launches = 0;
+  return v;
+}
+
+static void free_problem(rte_problem* p) {
+  if (!p) return;
+  void* ptrs[] = {p->sig_t, p->sig_s, p->f, p->sig_t64, p->sig_s64, p->S32, p->St32, p->St64, p->S_hi,
+                  p->S_lo, p->ax, p->ay, p->ax64, p->ay64, p->sgx, p->sgy, p->inflow, p->scratch64};
+  for (void* q : ptrs) dfree(q);
+  free_tc_state(p);
+  free_gmres_work(p);
+  delete p;
+}
+
+void rte_destroy(rte_problem* p) { free_problem(p); }
+
+rte_status rte_setup(const rte_grid* grid, const rte_ordinates* ord, const float* sigma_T, const float* sigma_a,
+                     const float* q, const float* eps, const float* g, const float* inflow, rte_problem** out) {
+  rte_problem* p = nullptr;
+  try {
+    RTE_REQUIRE(grid && ord && sigma_T && sigma_a && q && eps && g && out, "rte_setup: NULL argument");
+    *out = nullptr;
+    RTE_REQUIRE(grid->batch >= 1, "rte_setup: batch must be >= 1");
+    RTE_REQUIRE(grid->nx >= 1 && grid->nx == grid->ny, "rte_setup: nx must equal ny and be >= 1");
+    p = new rte_problem();
+    p->B = grid->batch;
+    p->N = grid->nx;
+    if (ord->c == nullptr) {
+      RTE_REQUIRE(ord->n_polar >= 1 && ord->n_azim >= 4 && ord->n_azim % 4 == 0,
+                  "rte_setup: built-in quadrature needs n_polar >= 1 and n_azim % 4 == 0");
+      RTE_REQUIRE(ord->M == 0 || ord->M == ord->n_polar * ord->n_azim, "rte_setup: M != n_polar*n_azim");
+      product_quadrature(ord->n_polar, ord->n_azim, p->c, p->s, p->zeta, p->w);
+    } else {
+      RTE_REQUIRE(ord->M >= 4 && ord->M % 4 == 0 && ord->s && ord->zeta && ord->w,
+                  "rte_setup: user ordinates need M % 4 == 0 and c, s, zeta, w");
+      p->c.assign(ord->c, ord->c + ord->M);
+      p->s.assign(ord->s, ord->s + ord->M);
+      p->zeta.assign(ord->zeta, ord->zeta + ord->M);
+      p->w.assign(ord->w, ord->w + ord->M);
+      double sw = 0.0;
+      for (int m = 0; m < ord->M; ++m) {
+        RTE_REQUIRE(p->c[m] != 0.0 && p->s[m] != 0.0, "rte_setup: ordinate with c_m == 0 or s_m == 0");
+        RTE_REQUIRE(p->w[m] > 0.0, "rte_setup: non-positive weight");
+        sw += p->w[m];
+      }
+      RTE_REQUIRE(fabs(sw - 4.0 * M_PI) <= 1e-12 * 4.0 * M_PI, "rte_setup: weights must sum to 4 pi");
+    }
+    p->M = (int)p->c.size();
+    const int B = p->B, N = p->N, M = p->M;
+    p->ncell = (int64_t)B * N * N;
+    p->n = p->ncell * M;
+    const double h = 1.0 / N;
+    // coefficients (R7)
+    std::vector<float> st(p->ncell), ss(p->ncell), ff(p->ncell);
+    std::vector<double> st64(p->ncell), ss64(p->ncell);
+    for (int64_t k = 0; k < p->ncell; ++k) {
+      double e = eps[k], sT = sigma_T[k], sA = sigma_a[k];
+      RTE_REQUIRE(e > 0.0 && e <= 1.0, "rte_setup: eps must lie in (0,1]");
+      RTE_REQUIRE(sT >= 0.0 && sA >= 0.0 && q[k] >= 0.0, "rte_setup: sigma_T, sigma_a, q must be >= 0");
+      double t = sT / e, sc = sT / e - e * sA;
+      RTE_REQUIRE(sc >= 0.0, "rte_setup: sigma_T/eps < eps*sigma_a (negative scattering) in a cell");
+      st64[k] = t;
+      ss64[k] = sc;
+      st[k] = (float)t;
+      ss[k] = (float)sc;
+      ff[k] = (float)(e * (double)q[k]);
+    }
+    // scattering matrices per sample
+    p->S.assign((size_t)B * M * M, 0.0);
+    for (int b = 0; b < B; ++b) {
+      RTE_REQUIRE(fabs((double)g[b]) < 1.0, "rte_setup: |g| must be < 1");
+      hg_matrix(p->c, p->s, p->zeta, p->w, (double)g[b], p->S.data() + (size_t)b * M * M);
+    }
+    std::vector<float> S32((size_t)B * M * M), St32((size_t)B * M * M), Shi((size_t)B * M * M), Slo((size_t)B * M * M);
+    std::vector<double> St64((size_t)B * M * M);
+    for (int b = 0; b < B; ++b)
+      for (int m = 0; m < M; ++m)
+        for (int n = 0; n < M; ++n) {
+          size_t o = (size_t)b * M * M;
+          double v = p->S[o + (size_t)m * M + n];
+          float v32 = (float)v;
+          S32[o + (size_t)m * M + n] = v32;
+          St32[o + (size_t)n * M + m] = v32;
+          St64[o + (size_t)n * M + m] = v;
+          float hi = tf32_rna(v32);
+          Shi[o + (size_t)m * M + n] = hi;
+          Slo[o + (size_t)m * M + n] = tf32_rna(v32 - hi);
+        }
+    std::vector<float> ax(M), ay(M);
+    std::vector<double> ax64(M), ay64(M);
+    std::vector<int8_t> sgx(M), sgy(M);
+    for (int m = 0; m < M; ++m) {
+      ax64[m] = fabs(p->c[m]) / h;
+      ay64[m] = fabs(p->s[m]) / h;
+      ax[m] = (float)ax64[m];
+      ay[m] = (float)ay64[m];
+      sgx[m] = p->c[m] > 0 ? 1 : -1;
+      sgy[m] = p->s[m] > 0 ? 1 : -1;
+    }
+    // upload
+    p->sig_t = dalloc<float>(p->ncell); upload(p->sig_t, st.data(), p->ncell);
+    p->sig_s = dalloc<float>(p->ncell); upload(p->sig_s, ss.data(), p->ncell);
+    p->f = dalloc<float>(p->ncell); upload(p->f, ff.data(), p->ncell);
+    p->sig_t64 = dalloc<double>(p->ncell); upload(p->sig_t64, st64.data(), p->ncell);
+    p->sig_s64 = dalloc<double>(p->ncell); upload(p->sig_s64, ss64.data(), p->ncell);
+    size_t mm = (size_t)B * M * M;
+    p->S32 = dalloc<float>(mm); upload(p->S32, S32.data(), mm);
+    p->St32 = dalloc<float>(mm); upload(p->St32, St32.data(), mm);
+    p->St64 = dalloc<double>(mm); upload(p->St64, St64.data(), mm);
+    p->S_hi = dalloc<float>(mm); upload(p->S_hi, Shi.data(), mm);
+    p->S_lo = dalloc<float>(mm); upload(p->S_lo, Slo.data(), mm);
+    p->ax = dalloc<float>(M); upload(p->ax, ax.data(), M);
+    p->ay = dalloc<float>(M); upload(p->ay, ay.data(), M);
+    p->ax64 = dalloc<double>(M); upload(p->ax64, ax64.data(), M);
+    p->ay64 = dalloc<double>(M); upload(p->ay64, ay64.data(), M);
+    p->sgx = dalloc<int8_t>(M); upload(p->sgx, sgx.data(), M);
+    p->sgy = dalloc<int8_t>(M); upload(p->sgy, sgy.data(), M);
+    if (inflow) {
+      size_t ni = (size_t)B * 4 * N * M;
+      p->inflow = dalloc<float>(ni);
+      upload(p->inflow, inflow, ni);
+    }
+    p->scratch64 = dalloc<double>(64);
+    p->tc_apply = apply_tc_supported(M) && getenv("RTE_DISABLE_TC") == nullptr;
+    *out = p;
+    return RTE_OK;
+  } catch (const Fail& f) {
+    free_problem(p);
+    return f.st;
+  } catch (const std::exception& e) {
+    free_problem(p);
+    set_error(std::string("internal: ") + e.what());
+    return RTE_EINTERNAL;
+  }
+}
+
+rte_status rte_problem_info(const rte_problem* p, int* batch, int* N, int* M, int64_t* n) {
+  if (!p) { set_error("rte_problem_info: NULL problem"); return RTE_EINVAL; }
+  if (batch) *batch = p->B;
+  if (N) *N = p->N;
+  if (M) *M = p->M;
+  if (n) *n = p->n;
+  return RTE_OK;
+}
+
+rte_status rte_get_ordinates(const rte_problem* p, double* c, double* s, double* zeta, double* w) {
+  if (!p) { set_error("rte_get_ordinates: NULL problem"); return RTE_EINVAL; }
+  if (c) memcpy(c, p->c.data(), p->M * sizeof(double));
+  if (s) memcpy(s, p->s.data(), p->M * sizeof(double));
+  if (zeta) memcpy(zeta, p->zeta.data(), p->M * sizeof(double));
+  if (w) memcpy(w, p->w.data(), p->M * sizeof(double));
+  return RTE_OK;
+}
+
+rte_status rte_quadrature(int n_polar, int n_azim, double* c, double* s, double* zeta, double* w) {
+  RTE_API_BEGIN
+  RTE_REQUIRE(n_polar >= 1 && n_azim >= 4 && n_azim % 4 == 0, "rte_quadrature: need n_polar >= 1, n_azim % 4 == 0");
+  std::vector<double> vc, vs, vz, vw;
+  product_quadrature(n_polar, n_azim, vc, vs, vz, vw);
+  size_t M = vc.size();
+  if (c) memcpy(c, vc.data(), M * sizeof(double));
+  if (s) memcpy(s, vs.data(), M * sizeof(double));
+  if (zeta) memcpy(zeta, vz.data(), M * sizeof(double));
+  if (w) memcpy(w, vw.data(), M * sizeof(double));
+  RTE_API_END
+}
+
+rte_status rte_hg_matrix(int M, const double* c, const double* s, const double* zeta, const double* w, double g,
+                         double* S) {
+  RTE_API_BEGIN
+  RTE_REQUIRE(M >= 1 && c && s && zeta && w && S, "rte_hg_matrix: bad argument");
+  RTE_REQUIRE(fabs(g) < 1.0, "rte_hg_matrix: |g| must be < 1");
+  std::vector<double> vc(c, c + M), vs(s, s + M), vz(zeta, zeta + M), vw(w, w + M);
+  hg_matrix(vc, vs, vz, vw, g, S);
+  RTE_API_END
+}
+
+rte_status rte_rhs(const rte_problem* p, float* b_dev, void* stream) {
+  RTE_API_BEGIN
+  RTE_REQUIRE(p && b_dev, "rte_rhs: NULL argument");
+  launch_rhs(p, b_dev, as_stream(stream));
+  RTE_API_END
+}
+
+rte_status rte_apply(const rte_problem* p, const float* x_dev, float* y_dev, void* stream) {
+  RTE_API_BEGIN
+  RTE_REQUIRE(p && x_dev && y_dev, "rte_apply: NULL argument");
+  RTE_REQUIRE((const void*)x_dev != (const void*)y_dev, "rte_apply: x and y must not alias");
+  launch_apply_f32(p, x_dev, y_dev, nullptr, 0, as_stream(stream));
+  RTE_API_END
+}
+
+rte_status rte_apply_f64(const rte_problem* p, const double* x_dev, double* y_dev, void* stream) {
+  RTE_API_BEGIN
+  RTE_REQUIRE(p && x_dev && y_dev, "rte_apply_f64: NULL argument");
+  RTE_REQUIRE((const void*)x_dev != (const void*)y_dev, "rte_apply_f64: x and y must not alias");
+  launch_apply_f64(p, x_dev, y_dev, nullptr, as_stream(stream));
+  RTE_API_END
+}
+
+}  // extern "C"

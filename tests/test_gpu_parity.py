@@ -1,0 +1,281 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on the same seeded inputs.
+
+Tolerances (BASELINE.json north_star): single rte_apply and V-cycle relative L2
+<= 1e-5 (V-cycle measured on V(r) = z - r, R27); rhs <= 1e-7 (fp32 output of an
+fp64 formula); fp64 apply <= 1e-12; GMRES on converging configs: iteration count within +-1
+and final solution relative L2 <= 1e-4; non-converging configs: the first Arnoldi columns
+<= 1e-5 (DESIGN.md §6 GMRES protocol).
+"""
+import numpy as np
+import pytest
+
+import workloads as W
+from oracle import rte as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def _rel(a, b):
+    a = np.asarray(a, np.float64).ravel()
+    b = np.asarray(b, np.float64).ravel()
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def _gpu_problem(cfg, media):
+    import paper_2604_23265_b200 as P
+    return P.rte_setup(cfg.N, media.sigma_T, media.sigma_a, media.q, media.eps, media.g, media.inflow,
+                       n_polar=cfg.n_polar, n_azim=cfg.n_azim)
+
+
+def _dev(a, dtype=None):
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    if dtype is not None:
+        t = t.to(dtype)
+    return t.cuda()
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_2604_23265_b200  # noqa: F401  (fails loudly if the library is missing)
+    yield
+
+
+SMALL = [
+    W.small_config(1, N=1, M=16),
+    W.small_config(2, N=5, M=8, n_polar=1, n_azim=8),        # ragged N, M < 16
+    W.small_config(3, N=12, M=12, n_polar=1, n_azim=12),     # M not a multiple of 16
+    W.small_config(4, N=9, M=16, n_polar=2, n_azim=8, B=3),  # batch, ragged tiles
+    W.small_config(5, N=33, M=64, n_polar=4, n_azim=16),     # several tiles + ragged tail
+]
+
+
+@pytest.mark.parametrize("cfg", [W.config(k) for k in (1, 2, 3, 4, 5)] + SMALL,
+                         ids=lambda c: f"cfg{c.k}-N{c.N}-M{c.M}-B{c.B}")
+def test_apply_and_rhs_parity(cfg):
+    import paper_2604_23265_b200 as P
+    media = W.make_media(cfg)
+    p = _gpu_problem(cfg, media)
+    op = O.setup_from_media(cfg, media)
+    x = W.make_vector(cfg)
+    xd = _dev(x)
+    y = torch.empty_like(xd)
+    P.rte_apply(p, xd, y)
+    b = torch.empty_like(xd)
+    P.rte_rhs(p, b)
+    torch.cuda.synchronize()
+    y_ref = O.apply(op, x)
+    assert _rel(y.cpu().numpy(), y_ref) <= 1e-5
+    assert _rel(b.cpu().numpy(), O.rhs(op)) <= 1e-7
+
+
+@pytest.mark.parametrize("cfg", [W.config(k) for k in (1, 2, 3)] + SMALL, ids=lambda c: f"cfg{c.k}-N{c.N}-M{c.M}")
+def test_apply_f64_parity(cfg):
+    import paper_2604_23265_b200 as P
+    media = W.make_media(cfg)
+    p = _gpu_problem(cfg, media)
+    op = O.setup_from_media(cfg, media)
+    x = W.make_vector(cfg, 1).astype(np.float64)
+    xd = _dev(x)
+    y = torch.empty_like(xd)
+    P.rte_apply_f64(p, xd, y)
+    torch.cuda.synchronize()
+    assert _rel(y.cpu().numpy(), O.apply(op, x)) <= 1e-12
+
+
+def test_apply_manufactured_constant():
+    """q = C sigma_a, inflow C: b - A(C 1) = 0 up to fp32 rounding (closed form)."""
+    import paper_2604_23265_b200 as P
+    N, M, C = 16, 32, 1.5
+    rng = np.random.default_rng(0)
+    sT = np.exp(rng.standard_normal((1, N, N))).astype(np.float32)
+    sA = np.full((1, N, N), 0.5, np.float32)
+    p = P.rte_setup(N, sT, sA, C * sA, np.full((1, N, N), 0.2, np.float32), [0.6],
+                    np.full((1, 4, N, M), C, np.float32), n_polar=2, n_azim=16)
+    xd = torch.full((1, N, N, M), C, dtype=torch.float64, device="cuda")
+    y = torch.empty_like(xd)
+    P.rte_apply_f64(p, xd, y)
+    b = torch.empty((1, N, N, M), dtype=torch.float32, device="cuda")
+    P.rte_rhs(p, b)
+    torch.cuda.synchronize()
+    assert _rel(y.cpu().numpy(), b.cpu().numpy().astype(np.float64)) < 1e-6
+
+
+# ---------------------------------------------------------------------------------------
+def _net_pair(cfg, std=0.02):
+    import paper_2604_23265_b200 as P
+    media = W.make_media(cfg)
+    p = _gpu_problem(cfg, media)
+    w = W.make_weights(cfg, std=std)
+    net = P.mgnet_create(p, cfg.L, cfg.C0, cfg.nu, w)
+    onet = O.make_mgnet(w, cfg.M, cfg.L, cfg.C0, cfg.nu)
+    return p, net, onet, media
+
+
+VSMALL = [
+    W.small_config(1, N=8, M=16, L=2, C0=4),
+    W.small_config(2, N=24, M=8, n_polar=1, n_azim=8, L=3, C0=8, B=2),
+    W.small_config(3, N=16, M=16, n_polar=2, n_azim=8, L=1, C0=16),
+    W.small_config(5, N=32, M=32, n_polar=2, n_azim=16, L=4, C0=32),
+]
+
+
+@pytest.mark.parametrize("cfg", [W.config(k) for k in (1, 2, 3)] + VSMALL, ids=lambda c: f"cfg{c.k}-N{c.N}-L{c.L}")
+def test_vcycle_parity(cfg):
+    import paper_2604_23265_b200 as P
+    p, net, onet, _ = _net_pair(cfg, std=0.05)
+    r = W.make_vector(cfg, 2)
+    rd = _dev(r)
+    z = torch.empty_like(rd)
+    P.mgnet_vcycle(net, rd, z, add_identity=True)
+    torch.cuda.synchronize()
+    v_gpu = z.cpu().numpy().astype(np.float64) - r
+    v_ref = O.vcycle(onet, r, add_identity=False)
+    assert _rel(v_gpu, v_ref) <= 1e-5
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("k", [4, 5])
+def test_vcycle_parity_large(k):
+    """Full-size configs 4 and 5 (config 4: oracle on the first two samples)."""
+    import paper_2604_23265_b200 as P
+    cfg = W.config(k)
+    p, net, onet, _ = _net_pair(cfg)
+    r = W.make_vector(cfg, 2)
+    rd = _dev(r)
+    z = torch.empty_like(rd)
+    P.mgnet_vcycle(net, rd, z, add_identity=False)
+    torch.cuda.synchronize()
+    nb = 2 if k == 4 else 1
+    v_gpu = z[:nb].cpu().numpy()
+    v_ref = O.vcycle(onet, r[:nb], add_identity=False)
+    assert _rel(v_gpu, v_ref) <= 1e-5
+
+
+def test_vcycle_zero_weights_is_identity():
+    import paper_2604_23265_b200 as P
+    cfg = W.small_config(2, N=16, M=16, n_polar=2, n_azim=8, L=3, C0=8)
+    media = W.make_media(cfg)
+    p = _gpu_problem(cfg, media)
+    net = P.mgnet_create(p, cfg.L, cfg.C0, cfg.nu, np.zeros(W.mgnet_weight_count(cfg.M, cfg.L, cfg.C0, cfg.nu)))
+    r = _dev(W.make_vector(cfg))
+    z = torch.empty_like(r)
+    P.mgnet_vcycle(net, r, z)
+    torch.cuda.synchronize()
+    assert torch.equal(z, r)
+
+
+def test_vcycle_linear_and_deterministic():
+    import paper_2604_23265_b200 as P
+    cfg = W.small_config(3, N=32, M=16, n_polar=2, n_azim=8, L=3, C0=16)
+    p, net, _, _ = _net_pair(cfg, std=0.05)
+    r1 = _dev(W.make_vector(cfg, 0))
+    r2 = _dev(W.make_vector(cfg, 1))
+    out = [torch.empty_like(r1) for _ in range(4)]
+    P.mgnet_vcycle(net, r1, out[0], add_identity=False)
+    P.mgnet_vcycle(net, r2, out[1], add_identity=False)
+    comb = (2.0 * r1 - 0.5 * r2).contiguous()
+    P.mgnet_vcycle(net, comb, out[2], add_identity=False)
+    P.mgnet_vcycle(net, r1, out[3], add_identity=False)
+    torch.cuda.synchronize()
+    lin = 2.0 * out[0] - 0.5 * out[1]
+    assert (torch.linalg.norm(out[2] - lin) / torch.linalg.norm(lin)).item() < 1e-5
+    assert torch.equal(out[0], out[3])   # bitwise run-to-run determinism
+
+
+def test_mgnet_rejects_bad_weight_count():
+    import paper_2604_23265_b200 as P
+    cfg = W.small_config(1, N=8, M=16, L=2, C0=4)
+    p = _gpu_problem(cfg, W.make_media(cfg))
+    n = W.mgnet_weight_count(cfg.M, cfg.L, cfg.C0, cfg.nu)
+    with pytest.raises(P.RteError):
+        P.mgnet_create(p, cfg.L, cfg.C0, cfg.nu, np.zeros(n - 1))
+    with pytest.raises(P.RteError):
+        P.mgnet_create(p, 5, cfg.C0, cfg.nu, np.zeros(n))   # N=8 not divisible by 2^4
+
+
+# ---------------------------------------------------------------------------------------
+def _gmres_pair(cfg, precond, rtol, maxit, std=0.02):
+    import paper_2604_23265_b200 as P
+    media = W.make_media(cfg)
+    p = _gpu_problem(cfg, media)
+    op = O.setup_from_media(cfg, media)
+    bd = torch.empty(p.shape, dtype=torch.float32, device="cuda")
+    P.rte_rhs(p, bd)
+    b32 = bd.cpu().numpy().astype(np.float64)          # same (fp32) system on both sides
+    x = torch.zeros(p.shape, dtype=torch.float64, device="cuda")
+    net = onet = None
+    if precond:
+        w = W.make_weights(cfg, std=std)
+        net = P.mgnet_create(p, cfg.L, cfg.C0, cfg.nu, w)
+        onet = O.make_mgnet(w, cfg.M, cfg.L, cfg.C0, cfg.nu)
+    rep = P.gmres_solve(p, net, bd, x, restart=cfg.restart, maxit=maxit, rtol=rtol)
+    ref = O.gmres(lambda v: O.apply(op, v), b32, P=(lambda v: O.vcycle(onet, v)) if precond else None,
+                  restart=cfg.restart, rtol=rtol, maxit=maxit)
+    return rep, x.cpu().numpy(), ref
+
+
+@pytest.mark.parametrize("precond", [False, True])
+def test_gmres_config1_converges_like_oracle(precond):
+    cfg = W.config(1)
+    rep, x, ref = _gmres_pair(cfg, precond, cfg.rtol, cfg.maxit)
+    r = rep[0]
+    assert ref.converged and r["converged"]
+    assert abs(r["iterations"] - ref.iterations) <= 1
+    assert _rel(x, ref.x) <= 1e-4
+    assert r["relres_true"] <= cfg.rtol
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("precond", [False, True])
+def test_gmres_config2_converges_like_oracle(precond):
+    cfg = W.config(2)
+    rep, x, ref = _gmres_pair(cfg, precond, cfg.rtol, cfg.maxit)
+    r = rep[0]
+    assert ref.converged and r["converged"]
+    assert abs(r["iterations"] - ref.iterations) <= 1
+    assert _rel(x, ref.x) <= 1e-4
+
+
+def test_gmres_small_batch_independent_solves():
+    """Config-4 style batch: each sample's solve matches the oracle solve of that sample alone."""
+    cfg = W.small_config(4, N=8, M=16, n_polar=2, n_azim=8, B=3, L=2, C0=8)
+    rep, x, _ = _gmres_pair(cfg, True, 1e-6, 600)
+    media = W.make_media(cfg)
+    op = O.setup_from_media(cfg, media)
+    w = W.make_weights(cfg)
+    onet = O.make_mgnet(w, cfg.M, cfg.L, cfg.C0, cfg.nu)
+    b_all = O.rhs(op).astype(np.float32).astype(np.float64)
+    for s in range(cfg.B):
+        ops = O.Problem(op.N, op.qd, op.sig_t[s:s + 1], op.sig_s[s:s + 1], op.f[s:s + 1], op.S[s:s + 1],
+                        op.inflow[s:s + 1])
+        ref = O.gmres(lambda v: O.apply(ops, v), b_all[s:s + 1], P=lambda v: O.vcycle(onet, v),
+                      restart=cfg.restart, rtol=1e-6, maxit=600)
+        assert ref.converged == rep[s]["converged"]
+        if ref.converged:
+            assert abs(rep[s]["iterations"] - ref.iterations) <= 1
+            assert _rel(x[s], ref.x[0]) <= 1e-4
+
+
+@pytest.mark.parametrize("k,steps", [(3, 5), (2, 8)])
+def test_gmres_first_arnoldi_columns(k, steps):
+    """Non-converging protocol: the first Arnoldi columns (unrotated H) agree to 1e-5."""
+    import paper_2604_23265_b200 as P
+    cfg = W.config(k)
+    media = W.make_media(cfg)
+    p = _gpu_problem(cfg, media)
+    op = O.setup_from_media(cfg, media)
+    w = W.make_weights(cfg)
+    net = P.mgnet_create(p, cfg.L, cfg.C0, cfg.nu, w)
+    onet = O.make_mgnet(w, cfg.M, cfg.L, cfg.C0, cfg.nu)
+    bd = torch.empty(p.shape, dtype=torch.float32, device="cuda")
+    P.rte_rhs(p, bd)
+    x = torch.zeros(p.shape, dtype=torch.float64, device="cuda")
+    rep = P.gmres_solve(p, net, bd, x, restart=cfg.restart, maxit=steps, rtol=1e-30, hessenberg=True)
+    H = rep[0]["hessenberg"][:steps + 1, :steps]
+    Href = O.arnoldi_columns(lambda v: O.apply(op, v), bd.cpu().numpy().astype(np.float64),
+                             lambda v: O.vcycle(onet, v), steps)
+    for j in range(steps):
+        assert _rel(H[:j + 2, j], Href[:j + 2, j]) <= 1e-5, j
