@@ -1,0 +1,398 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path: GMRES iterations/s of the MgNet-preconditioned restarted GMRES
+solve (rte_apply + MgNet V-cycle + CGS2 Arnoldi + Givens per iteration) on one config of
+BASELINE.json (default: config 5, 512^2 cells x M=256 ordinates, MgNet L=6 C0=32, GMRES(30)).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config k] [--impl ours|reference]
+
+A "step" is one GMRES inner iteration.  The timed region is ONE gmres_solve call
+of exactly K inner iterations from x0 = 0 (so it also carries the restart work: the fp64 residual
+at cycle start and the cycle-end update, amortised over the K steps), bracketed by a barrier and
+torch.cuda.synchronize() on both sides and timed with CUDA events on the launching stream; the
+reported time is the max over ranks.  Config-5 vectors are 256 MiB (> 126 MB L2), so every step
+streams its inputs from HBM ("inputs larger than L2").  Multi-GPU: config 5 is ONE medium and does
+not shard without a halo exchange, so N ranks run N independent replicas (DESIGN.md §8,
+"replicas only"); value = total iterations of all ranks / max-over-ranks time ("scaling": "weak").
+
+Rank 0 prints ONE JSON line.  --impl reference times the fp64 CPU oracle (oracle/, the
+reference arm of this tier) on the host cores for the same metric and config.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "GMRES iter/s (rte_apply + MgNet V-cycle) at N²×M; % of roofline"
+UNIT = "GMRES iter/s"
+TF32_PER_BF16 = 1.1 / 2.25      # guide's nominal dense ratio (B200_PROFILING.md table)
+N_SM = 148
+
+
+def _peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+                "sm_max_mhz": 1965.0}, "fallback"
+
+
+def _workload_name(cfg):
+    return (f"cfg{cfg.k}: {cfg.B}x{cfg.N}^2 cells x M={cfg.M} ordinates "
+            f"({cfg.B * cfg.N * cfg.N * cfg.M / 1e6:.1f}M unknowns), MgNet L={cfg.L} C0={cfg.C0} nu={cfg.nu}, "
+            f"GMRES({cfg.restart}) fixed budget")
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws <= 1:
+        return None, 0, 1, 0
+    import torch
+    import torch.distributed as dist
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    backend = "nccl" if torch.cuda.is_available() else "gloo"
+    if torch.cuda.is_available():
+        torch.cuda.set_device(local)
+    dist.init_process_group(backend=backend)
+    return dist, rank, ws, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region (B200_PROFILING.md)."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev_index):
+        self.proc = None
+        self.dev = dev_index
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def _device_index(torch, local):
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+    if vis:
+        ids = [v.strip() for v in vis.split(",") if v.strip()]
+        if local < len(ids):
+            return ids[local]
+    return local
+
+
+def _roofline(classes, peaks, src):
+    """Roofline of the dominant kernel class (max total device time in the timed region)."""
+    if not classes:
+        return None, None
+    top = max(classes, key=lambda c: c["ms"])
+    avg_ms = top["ms"] / max(top["launches"], 1)
+    per_launch_flops = top["flops"] / max(top["launches"], 1)
+    per_launch_bytes = top["bytes"] / max(top["launches"], 1)
+    sus = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
+    smax = peaks.get("sm_max_mhz", 1965.0)
+    kind = top["kind"]
+    if kind == "hbm":
+        ach = per_launch_bytes / (avg_ms * 1e-3) / 1e9
+        peak, unit, bound = peaks["hbm_gbs"], "GB/s", "hbm"
+        note = f"HBM copy bandwidth ({src} MEASURED_PEAKS.json hbm_gbs)"
+    elif kind == "tensor_3xtf32":
+        ach = per_launch_flops / (avg_ms * 1e-3) / 1e12
+        peak = sus * TF32_PER_BF16 / 3.0
+        unit, bound = "TFLOP/s", "tensor"
+        note = (f"3xTF32 fp32-emulation peak = {src} sustained bf16 {sus} TF x {TF32_PER_BF16:.3f} (nominal "
+                "tf32/bf16) / 3 MMAs per product; achieved counts algorithmic fp32 flops")
+    elif kind == "fp32_simt":
+        ach = per_launch_flops / (avg_ms * 1e-3) / 1e12
+        peak = N_SM * 128 * 2 * smax * 1e6 / 1e12
+        unit, bound = "TFLOP/s", "alu"
+        note = f"fp32 FMA peak = 148 SMs x 128 lanes x 2 flop x {smax} MHz (DESIGN.md §5)"
+    elif kind == "fp64_simt":
+        ach = per_launch_flops / (avg_ms * 1e-3) / 1e12
+        peak = N_SM * 64 * 2 * smax * 1e6 / 1e12
+        unit, bound = "TFLOP/s", "alu"
+        note = f"fp64 FMA peak = 148 SMs x 64 lanes x 2 flop x {smax} MHz (DESIGN.md §5)"
+    else:
+        ach, peak, unit, bound, note = None, None, None, "latency", "tiny latency-bound kernel"
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            with open(tpath) as f:
+                traffic = json.load(f).get(top["name"])
+        except Exception:
+            traffic = None
+    roof = {"kernel": top["name"], "bound": bound, "achieved": ach, "peak": peak, "unit": unit,
+            "frac": (ach / peak) if (ach is not None and peak) else None, "traffic": traffic,
+            "avg_launch_ms": avg_ms, "launches": top["launches"],
+            "algorithmic_flops_per_launch": per_launch_flops, "algorithmic_bytes_per_launch": per_launch_bytes,
+            "peak_source": note}
+    return roof, top
+
+
+def _cpu_baseline(cfg, media, weights):
+    """The fp64 oracle as it stands, on the host cores: one Arnoldi step (V-cycle + apply + MGS)."""
+    from oracle import rte as O
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        cores = os.cpu_count()
+    op = O.setup_from_media(cfg, media)
+    onet = O.make_mgnet(weights, cfg.M, cfg.L, cfg.C0, cfg.nu)
+    b = O.rhs(op)
+    t0 = time.perf_counter()
+    O.arnoldi_columns(lambda v: O.apply(op, v), b, lambda v: O.vcycle(onet, v), 1)
+    dt = time.perf_counter() - t0
+    return {"value": 1.0 / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"one GMRES inner iteration of the fp64 numpy oracle on the full {cfg.k}-config problem "
+                      f"(oracle.arnoldi_columns steps=1: P=I+V-cycle, apply, MGS, norm), {dt:.1f} s wall; "
+                      f"BLAS threads={cores}, host cpus={os.cpu_count()}"}
+
+
+def run_reference(args, cfg):
+    """Reference arm: the fp64 CPU oracle (oracle/) on the host cores, same metric and config."""
+    dist, rank, ws, _ = _dist()
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+    import workloads as W
+    from oracle import rte as O
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        cores = os.cpu_count()
+    media = W.make_media(cfg)
+    weights = W.make_weights(cfg)
+    op = O.setup_from_media(cfg, media)
+    onet = O.make_mgnet(weights, cfg.M, cfg.L, cfg.C0, cfg.nu)
+    b = O.rhs(op)
+    A = lambda v: O.apply(op, v)
+    Pc = lambda v: O.vcycle(onet, v)
+    # warm-up: W Arnoldi steps on a small copy of the workload (loads BLAS, touches code paths)
+    small = W.small_config(cfg.k, N=min(cfg.N, 32), M=min(cfg.M, 16), L=min(cfg.L, 3))
+    sm = W.make_media(small)
+    sop = O.setup_from_media(small, sm)
+    snet = O.make_mgnet(W.make_weights(small), small.M, small.L, small.C0, small.nu)
+    O.arnoldi_columns(lambda v: O.apply(sop, v), O.rhs(sop), lambda v: O.vcycle(snet, v), max(1, args.warmup))
+    # bounded sample: at most K steps, capped so the run ends within a few minutes
+    cap = max(2, int(3e8 // max(cfg.unknowns, 1)))
+    steps = max(1, min(args.steps, cap))
+    t0 = time.perf_counter()
+    O.arnoldi_columns(A, b, Pc, steps)
+    dt = time.perf_counter() - t0
+    val = steps / dt
+    line = {"metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus, "steps": steps,
+            "warmup": args.warmup, "ms_per_step": dt / steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": _workload_name(cfg), "unknowns": cfg.unknowns},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"{steps} Arnoldi steps (oracle.arnoldi_columns: V-cycle + apply + MGS) "
+                                       f"of the fp64 numpy oracle on the full config-{cfg.k} problem "
+                                       f"(steps capped from {args.steps} to bound the run)"},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def run_ours(args, cfg):
+    import torch
+    dist, rank, ws, local = _dist()
+    import paper_2604_23265_b200 as P
+    import workloads as W
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    media = W.make_media(cfg)
+    weights = W.make_weights(cfg)
+    p = P.rte_setup(cfg.N, media.sigma_T, media.sigma_a, media.q, media.eps, media.g, media.inflow,
+                    n_polar=cfg.n_polar, n_azim=cfg.n_azim)
+    net = P.mgnet_create(p, cfg.L, cfg.C0, cfg.nu, weights)
+    b = torch.empty(p.shape, dtype=torch.float32, device=dev)
+    P.rte_rhs(p, b)
+    x = torch.zeros(p.shape, dtype=torch.float64, device=dev)
+    K, Wm = args.steps, args.warmup
+    solve = lambda xx, bb, k: P.gmres_solve(p, net, bb, xx, restart=cfg.restart, maxit=k, rtol=1e-300,
+                                            history=False)
+    # warm-up: W inner iterations (one solve), untimed
+    solve(x, b, max(Wm, 1))
+    torch.cuda.synchronize()
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    # ---- timed region: one solve of exactly K inner iterations --------------------------
+    x.zero_()
+    sampler = ClockSampler(_device_index(torch, local))
+    sampler.start()
+    P.rte_launch_count(reset=True)
+    P.rte_timing_enable(True)
+    P.rte_timing_reset()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    rep = solve(x, b, K)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms = ev0.elapsed_time(ev1)
+    launches = P.rte_launch_count(reset=True)
+    classes = P.rte_timing_get()
+    P.rte_timing_enable(False)
+    clocks = sampler.stop()
+    iters = rep[0]["iterations"] if cfg.B == 1 else sum(r["iterations"] for r in rep) / cfg.B
+    assert iters == K, f"solve ran {iters} iterations, expected {K}"
+    ms_max = ms
+    if dist is not None:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max = float(t.item())
+    value = K * ws / (ms_max * 1e-3)
+
+    # ---- e2e: same solve through the public API with HOST buffers -----------------------
+    b_host = torch.empty(p.shape, dtype=torch.float32, pin_memory=True)
+    b_host.copy_(b)
+    x_host = torch.empty(p.shape, dtype=torch.float64, pin_memory=True)
+    b2 = torch.empty_like(b)
+    torch.cuda.synchronize()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    b2.copy_(b_host, non_blocking=True)
+    x.zero_()
+    solve(x, b2, K)
+    x_host.copy_(x, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms_e2e = e0.elapsed_time(e1)
+    if dist is not None:
+        t = torch.tensor([ms_e2e], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_e2e = float(t.item())
+    h2d = b_host.numel() * 4
+    d2h = x_host.numel() * 8
+
+    # ---- single-op throughputs (north star: applies/s, V-cycles/s), device events ----------
+    ops = {}
+    if rank == 0:
+        y = torch.empty_like(b)
+        z = torch.empty_like(b)
+        for name, fn in (("rte_apply_per_s", lambda: P.rte_apply(p, b, y)),
+                         ("mgnet_vcycle_per_s", lambda: P.mgnet_vcycle(net, b, z, True))):
+            fn()
+            torch.cuda.synchronize()
+            reps = 5
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            for _ in range(reps):
+                fn()
+            a1.record(stream)
+            torch.cuda.synchronize()
+            ops[name] = reps / (a0.elapsed_time(a1) * 1e-3)
+
+    if rank == 0:
+        peaks, src = _peaks()
+        roof, top = _roofline(classes, peaks, src)
+        tot_ms = sum(c["ms"] for c in classes) or 1.0
+        kernels = sorted(({"name": c["name"], "kind": c["kind"], "launches": c["launches"],
+                           "ms": round(c["ms"], 4), "share": round(c["ms"] / tot_ms, 4)} for c in classes),
+                         key=lambda d: -d["ms"])
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": Wm,
+                "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f32", "data": "synthetic",
+                "config": {"workload": _workload_name(cfg), "unknowns": cfg.unknowns,
+                           "l2": "inputs larger than L2 (each vector 4 B x unknowns)" if cfg.unknowns * 4 > 126e6
+                           else "working set L2-resident (small config)",
+                           "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
+                           "precision": "fp32 storage/arithmetic, fp64 iterate, reductions and restart residual"},
+                "roofline": roof,
+                "e2e": {"value": K * ws / (ms_e2e * 1e-3), "unit": UNIT,
+                        "h2d_bytes_per_step": h2d / K, "d2h_bytes_per_step": d2h / K,
+                        "note": f"one solve of K={K} iterations per measurement: b (fp32) copied H2D from pinned "
+                                "host memory before it and x (fp64) D2H after it; bytes amortised per step"},
+                "gpu_launches": launches, "clocks": clocks, "ops": ops, "kernels": kernels[:12]}
+        if ws == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = _cpu_baseline(cfg, media, weights)
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
+    import workloads as W
+    cfg = W.config(args.config)
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

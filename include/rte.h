@@ -158,6 +158,21 @@ rte_status gmres_solve(const rte_problem* p, const mgnet_net* net, const float* 
 /* Kernel launches issued by this thread since the last call (reset to 0). */
 int64_t rte_launch_count(int reset);
 
+/* Per-launch device timing (measurement only; not on the product path unless enabled).
+ * rte_timing_enable(1): every kernel launch of this thread is bracketed by a CUDA-event pair
+ * recorded on the stream it is launched on, and tagged with its ALGORITHMIC flops and bytes
+ * (DESIGN.md §5 states the per-unit figures).  rte_timing_get resolves the events (it
+ * synchronises on the last one) and returns the aggregate of kernel class `idx`:
+ * name (NUL-terminated, truncated to name_len), kind (0 HBM streaming, 1 3xTF32 tensor-core
+ * contraction, 2 fp32 SIMT contraction, 3 fp64 SIMT, 4 latency-bound tiny kernel), launches,
+ * total device ms, total algorithmic flops and bytes; *count receives the number of classes
+ * (idx = -1 only queries the count).  rte_timing_reset clears the aggregates.  Any output
+ * pointer may be NULL.  Errors: RTE_EINVAL (idx out of range), RTE_ECUDA. */
+rte_status rte_timing_enable(int on);
+rte_status rte_timing_reset(void);
+rte_status rte_timing_get(int idx, char* name, int name_len, int* kind, int64_t* launches, double* ms,
+                          double* flops, double* bytes, int* count);
+
 const char* rte_last_error(void);
 
 #ifdef __cplusplus

@@ -16,7 +16,8 @@ from . import _lib
 from ._lib import RteError, check, gmres_opts, gmres_report, lib
 
 __all__ = ["Problem", "MgNet", "rte_setup", "rte_rhs", "rte_apply", "rte_apply_f64", "mgnet_create",
-           "mgnet_vcycle", "gmres_solve", "rte_quadrature", "rte_hg_matrix", "rte_launch_count", "RteError", "LIB_PATH"]
+           "mgnet_vcycle", "gmres_solve", "rte_quadrature", "rte_hg_matrix", "rte_launch_count", "rte_timing_enable", "rte_timing_reset",
+           "rte_timing_get", "RteError", "LIB_PATH"]
 
 LIB_PATH = _lib.LIB_PATH
 
@@ -205,3 +206,31 @@ def gmres_solve(p: Problem, net: Optional[MgNet], b, x, *, restart: int = 30, ma
 
 def rte_launch_count(reset: bool = False) -> int:
     return int(lib.rte_launch_count(int(reset)))
+
+
+def rte_timing_enable(on: bool = True) -> None:
+    check("rte_timing_enable", lib.rte_timing_enable(int(on)))
+
+
+def rte_timing_reset() -> None:
+    check("rte_timing_reset", lib.rte_timing_reset())
+
+
+KINDS = {0: "hbm", 1: "tensor_3xtf32", 2: "fp32_simt", 3: "fp64_simt", 4: "latency"}
+
+
+def rte_timing_get():
+    """Per-kernel-class aggregates since the last reset: list of dicts (name, kind, launches, ms,
+    flops, bytes), all algorithmic flops/bytes as tagged by the library."""
+    cnt = C.c_int()
+    check("rte_timing_get", lib.rte_timing_get(-1, None, 0, None, None, None, None, None, C.byref(cnt)))
+    out = []
+    for i in range(cnt.value):
+        name = C.create_string_buffer(128)
+        kind, la = C.c_int(), C.c_int64()
+        ms, fl, by = C.c_double(), C.c_double(), C.c_double()
+        check("rte_timing_get", lib.rte_timing_get(i, name, 128, C.byref(kind), C.byref(la), C.byref(ms),
+                                                   C.byref(fl), C.byref(by), None))
+        out.append(dict(name=name.value.decode(), kind=KINDS.get(kind.value, str(kind.value)),
+                        launches=la.value, ms=ms.value, flops=fl.value, bytes=by.value))
+    return out

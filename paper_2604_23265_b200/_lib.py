@@ -65,6 +65,11 @@ SIGS = {
     "gmres_solve": (C.c_int, [_vp, _vp, _vp, _vp, C.POINTER(gmres_opts), C.POINTER(gmres_report), _vp]),
     "rte_launch_count": (C.c_int64, [C.c_int]),
     "rte_last_error": (C.c_char_p, []),
+    "rte_timing_enable": (C.c_int, [C.c_int]),
+    "rte_timing_reset": (C.c_int, []),
+    "rte_timing_get": (C.c_int, [C.c_int, C.c_char_p, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int64),
+                                 C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                 C.POINTER(C.c_int)]),
 }
 EXPORTED = tuple(SIGS)
 for _name, (_res, _args) in SIGS.items():

@@ -138,11 +138,20 @@ void launch_simt(const rte_problem* p, const T* x, T* y, const T* St, const T* s
 
 }  // namespace
 
+// Algorithmic work of one apply: 2 B N^2 M^2 flops for the scattering GEMM plus
+// 8 per unknown for the stencil; bytes = read x once + write y once (+ read b) + 2 coefficients
+// per cell + the B M x M scattering matrices (+ the 2 M stencil weights, negligible).
+double apply_flops(const rte_problem* p) { return 2.0 * (double)p->ncell * p->M * p->M + 8.0 * (double)p->n; }
+double apply_bytes(const rte_problem* p, int elt, int b_elt) {
+  return (double)p->n * (2 * elt + b_elt) + 2.0 * elt * (double)p->ncell + (double)elt * p->B * p->M * p->M;
+}
+
 void launch_rhs(const rte_problem* p, float* b, cudaStream_t st) {
   int64_t n = p->n;
   int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 16);
+  prof_begin(st);
   rhs_kernel<<<blocks, 256, 0, st>>>(p->B, p->N, p->M, p->f, p->inflow, p->ax, p->ay, p->sgx, p->sgy, b);
-  after_launch("rhs_kernel");
+  after_launch("rhs", st, 0.0, 4.0 * (double)n + 4.0 * p->ncell, 0);
 }
 
 void launch_apply_f32(const rte_problem* p, const float* x, float* y, const double* alpha, int alpha_stride,
@@ -151,13 +160,15 @@ void launch_apply_f32(const rte_problem* p, const float* x, float* y, const doub
     launch_apply_tc(p, x, y, alpha, alpha_stride, st);
     return;
   }
+  prof_begin(st);
   launch_simt<float>(p, x, y, p->St32, p->sig_t, p->sig_s, p->ax, p->ay, nullptr, alpha, alpha_stride, st);
-  after_launch("apply_simt_kernel<float>");
+  after_launch("apply_f32_simt", st, apply_flops(p), apply_bytes(p, 4, 0), 2);
 }
 
 void launch_apply_f64(const rte_problem* p, const double* x, double* y, const float* b, cudaStream_t st) {
+  prof_begin(st);
   launch_simt<double>(p, x, y, p->St64, p->sig_t64, p->sig_s64, p->ax64, p->ay64, b, nullptr, 0, st);
-  after_launch("apply_simt_kernel<double>");
+  after_launch("apply_f64_simt", st, apply_flops(p), apply_bytes(p, 8, b ? 4 : 0), 3);
 }
 
 }  // namespace rte

@@ -31,8 +31,14 @@ struct Fail {
       throw ::rte::Fail{RTE_EINVAL};                                             \
     }                                                                            \
   } while (0)
-// Check for launch errors after a kernel launch and count it.
-void after_launch(const char* what);
+// Launch bookkeeping.  prof_begin(st) goes right before a kernel launch, after_launch right
+// after it: it checks the launch, counts it and -- when per-launch timing is on
+// (rte_timing_enable) -- records a CUDA-event pair on the launching stream together with the
+// launch's ALGORITHMIC flops and bytes (DESIGN.md §5 gives the per-unit figures).
+// kind: 0 HBM-bound streaming, 1 3xTF32 tensor-core contraction, 2 fp32 SIMT contraction,
+//       3 fp64 SIMT, 4 tiny/latency (Givens etc.).
+void prof_begin(cudaStream_t st);
+void after_launch(const char* what, cudaStream_t st = 0, double flops = 0.0, double bytes = 0.0, int kind = 4);
 
 template <typename T>
 T* dalloc(size_t n) {
@@ -98,6 +104,8 @@ void launch_apply_f32(const rte_problem* p, const float* x, float* y, const doub
 // y = A x (fp64); if b != NULL: y = b - A x.
 void launch_apply_f64(const rte_problem* p, const double* x, double* y, const float* b, cudaStream_t st);
 bool apply_tc_supported(int M);
+double apply_flops(const rte_problem* p);
+double apply_bytes(const rte_problem* p, int elt, int b_elt);
 void free_tc_state(rte_problem* p);
 void free_gmres_work(const rte_problem* p);
 void launch_apply_tc(const rte_problem* p, const float* x, float* y, const double* alpha_dev,

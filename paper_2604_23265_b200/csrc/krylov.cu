@@ -300,6 +300,7 @@ static void launch_cgs(const GmresWork& W, int nv, bool update, bool dots, const
   RedArgs ra{W.partials, W.counters, out, kMaxRestart + 2, W.nblk};
   dim3 grid(W.nblk, W.B);
   const int64_t vld = W.ns * W.B;
+  prof_begin(st);
   auto go = [&](auto nv_tag, auto up_tag, auto dot_tag) {
     constexpr int NV = decltype(nv_tag)::value;
     constexpr bool UP = decltype(up_tag)::value;
@@ -327,14 +328,21 @@ static void launch_cgs(const GmresWork& W, int nv, bool update, bool dots, const
       set_error("gmres: restart > 32 is not supported by the fused CGS kernels");
       throw Fail{RTE_EINVAL};
   }
-  after_launch("cgs_kernel");
+  // bytes: NV basis vectors + src read, dst written if updating; flops: 2 per (vector, element)
+  // for each of the update and the dots, + 2 per element for the norm.
+  const double ne = (double)W.ns * W.B;
+  const double bytes = 4.0 * ne * (nv + 1 + (update ? 1 : 0));
+  const double flops = ne * (2.0 * nv * ((update ? 1 : 0) + (dots ? 1 : 0)) + 2.0);
+  after_launch(update ? (dots ? "cgs_update_dots" : "cgs_update") : "cgs_dots", st, flops, bytes, 0);
 }
 
 template <typename T>
 static void launch_norm(const GmresWork& W, const T* x, float* xo, double* out, cudaStream_t st) {
   RedArgs ra{W.partials, W.counters, out, 1, W.nblk};
+  prof_begin(st);
   norm_kernel<T><<<dim3(W.nblk, W.B), kThreads, 0, st>>>(x, xo, W.ns, ra);
-  after_launch("norm_kernel");
+  const double ne = (double)W.ns * W.B;
+  after_launch("norm", st, 2.0 * ne, ne * (sizeof(T) + (xo ? 4.0 : 0.0)), 0);
 }
 
 }  // namespace rte
@@ -439,9 +447,10 @@ extern "C" rte_status gmres_solve(const rte_problem* p, const mgnet_net* net, co
       launch_apply_f64(p, x_dev, W.r64, b_dev, st);
       launch_norm<double>(W, W.r64, W.V, W.rn2, st);
       int stop_all = (total_all >= opts->maxit) ? 1 : 0;
+      prof_begin(st);
       cycle_init_kernel<<<(B + 63) / 64, 64, 0, st>>>(B, W.rn2, W.bnorm, opts->rtol, stop_all, W.alpha, m + 1, W.g,
                                                       m + 1, W.active, W.kcols, W.done, W.st_dev);
-      after_launch("cycle_init_kernel");
+      after_launch("cycle_init", st);
       RTE_CHECK_CUDA(cudaMemcpyAsync(W.st_host, W.st_dev, sizeof(Status) * B, cudaMemcpyDeviceToHost, st));
       RTE_CHECK_CUDA(cudaStreamSynchronize(st));
       int n_active = 0;
@@ -479,10 +488,11 @@ extern "C" rte_status gmres_solve(const rte_problem* p, const mgnet_net* net, co
         }
         ++total_all;
         int last = (total_all >= opts->maxit) ? 1 : 0;
-        givens_kernel<<<(B + 63) / 64, 64, 0, st>>>(B, j, m, W.h1, h2, hld, nrm, hld, W.Hr, W.Hraw,
+        prof_begin(st);
+      givens_kernel<<<(B + 63) / 64, 64, 0, st>>>(B, j, m, W.h1, h2, hld, nrm, hld, W.Hr, W.Hraw,
                                                     first_cycle ? 1 : 0, W.cs, W.sn, W.g, W.alpha, m + 1, W.bnorm,
                                                     opts->rtol, last, W.active, W.kcols, W.st_dev);
-        after_launch("givens_kernel");
+        after_launch("givens", st);
         RTE_CHECK_CUDA(cudaMemcpyAsync(W.st_host, W.st_dev, sizeof(Status) * B, cudaMemcpyDeviceToHost, st));
         RTE_CHECK_CUDA(cudaStreamSynchronize(st));
         int still = 0;
@@ -506,17 +516,20 @@ extern "C" rte_status gmres_solve(const rte_problem* p, const mgnet_net* net, co
       }
       first_cycle = false;
       // x += P(V y)
+      prof_begin(st);
       backsolve_kernel<<<(B + 63) / 64, 64, 0, st>>>(B, m, W.Hr, W.g, W.alpha, m + 1, W.kcols, W.coef, m + 1);
-      after_launch("backsolve_kernel");
+      after_launch("backsolve", st);
+      prof_begin(st);
       combine_kernel<<<dim3(W.nblk, B), kThreads, 0, st>>>(W.V, n, W.coef, m + 1, W.kcols, W.w, W.ns, W.nblk);
-      after_launch("combine_kernel");
+      after_launch("combine", st, 2.0 * m * (double)n, 4.0 * (double)n * (m + 1), 0);
       const float* corr = W.w;
       if (opts->precond == 1) {
         vcycle_run(net, W.w, W.z, true, nullptr, 0, st);
         corr = W.z;
       }
+      prof_begin(st);
       axpy64_kernel<<<dim3(W.nblk, B), kThreads, 0, st>>>(x_dev, corr, W.kcols, W.ns, W.nblk);
-      after_launch("axpy64_kernel");
+      after_launch("axpy64", st, (double)n, 20.0 * (double)n, 0);
       // samples that broke down stop (oracle: breakdown ends the solve)
       bool any_brk = false;
       for (int b = 0; b < B; ++b)

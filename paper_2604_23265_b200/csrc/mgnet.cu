@@ -140,10 +140,30 @@ __global__ void __launch_bounds__(256) conv_simt_kernel(
 
 }  // namespace
 
+// Algorithmic work of one conv launch: 2 * out_pixels * Co * Ci * taps_per_output
+// flops (taps = k*k; the stride-2 transposed 4x4 conv touches 4 taps per output pixel); bytes =
+// read the input once, the weights once, the addend once (if any), write the output once.
+double conv_flops(const ConvDesc& d) {
+  double taps = (d.mode == 2) ? 4.0 : (double)d.ks * d.ks;
+  return 2.0 * d.B * (double)d.Ho * d.Wo * d.Co * d.Ci * taps;
+}
+double conv_bytes(const ConvDesc& d, bool has_addend) {
+  double in = (double)d.B * d.Hi * d.Wi * d.Ci, out = (double)d.B * d.Ho * d.Wo * d.Co;
+  double wts = (double)d.Co * d.Ci * ((d.mode == 2) ? 16.0 : (double)d.ks * d.ks);
+  return 4.0 * (in + out * (has_addend ? 2.0 : 1.0) + wts);
+}
+const char* conv_class_name(const ConvDesc& d, bool tc) {
+  if (d.mode == 0 && d.ks == 1) return tc ? "conv1x1_tc" : "conv1x1_simt";
+  if (d.mode == 0) return tc ? "conv3x3_tc" : "conv3x3_simt";
+  if (d.mode == 1) return tc ? "conv3x3s2_tc" : "conv3x3s2_simt";
+  return tc ? "convT4x4s2_tc" : "convT4x4s2_simt";
+}
+
 void launch_conv(const ConvDesc& d, const float* in, const float* Wk, float* out, const float* addend, float sign,
                  const double* alpha, int alpha_stride, bool alpha_on_input, bool alpha_on_addend,
                  cudaStream_t st) {
   if (conv_tc_try(d, in, out, addend, sign, alpha, alpha_stride, alpha_on_input, alpha_on_addend, st)) return;
+  prof_begin(st);
   auto go = [&](auto mode_tag, auto ks_tag, auto tco_tag) {
     constexpr int MODE = decltype(mode_tag)::value;
     constexpr int KS = decltype(ks_tag)::value;
@@ -171,7 +191,7 @@ void launch_conv(const ConvDesc& d, const float* in, const float* Wk, float* out
   else if (d.mode == 0) by_tco(I0{}, K3{});
   else if (d.mode == 1) by_tco(I1{}, K3{});
   else by_tco(I2{}, K4{});
-  after_launch("conv_simt_kernel");
+  after_launch(conv_class_name(d, false), st, conv_flops(d), conv_bytes(d, addend != nullptr), 2);
 }
 
 }  // namespace rte

@@ -33,6 +33,9 @@ struct Level {
   float* t = nullptr;
 };
 
+double conv_flops(const ConvDesc& d);
+double conv_bytes(const ConvDesc& d, bool has_addend);
+const char* conv_class_name(const ConvDesc& d, bool tc);
 void launch_conv(const ConvDesc& d, const float* in, const float* Wk, float* out, const float* addend, float sign,
                  const double* alpha, int alpha_stride, bool alpha_on_input, bool alpha_on_addend, cudaStream_t st);
 // tensor-core path (conv_tc.cu): returns false when the shape is not supported there.

@@ -19,12 +19,82 @@ static thread_local int64_t g_launches = 0;
 
 void set_error(const std::string& msg) { g_err = msg; }
 
-void after_launch(const char* what) {
+// ---- per-launch timing (rte_timing_*) -------------------------------------------------
+// Each timed launch gets an event pair recorded on its own stream; durations are resolved
+// lazily in rte_timing_get (one synchronisation), then aggregated per kernel class.
+namespace {
+struct ProfRec {
+  std::string name;
+  cudaEvent_t e0, e1;
+  double flops, bytes;
+  int kind;
+};
+struct ProfClass {
+  std::string name;
+  int kind = 4;
+  int64_t launches = 0;
+  double ms = 0.0, flops = 0.0, bytes = 0.0;
+};
+thread_local bool g_prof_on = false;
+thread_local cudaEvent_t g_prof_pending = nullptr;
+thread_local std::vector<ProfRec> g_prof_recs;
+thread_local std::vector<cudaEvent_t> g_prof_pool;
+thread_local std::vector<ProfClass> g_prof_classes;
+
+cudaEvent_t prof_event() {
+  if (!g_prof_pool.empty()) {
+    cudaEvent_t e = g_prof_pool.back();
+    g_prof_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  RTE_CHECK_CUDA(cudaEventCreate(&e));
+  return e;
+}
+
+void prof_resolve() {
+  if (g_prof_recs.empty()) return;
+  RTE_CHECK_CUDA(cudaEventSynchronize(g_prof_recs.back().e1));
+  for (ProfRec& r : g_prof_recs) {
+    float ms = 0.f;
+    RTE_CHECK_CUDA(cudaEventSynchronize(r.e1));
+    RTE_CHECK_CUDA(cudaEventElapsedTime(&ms, r.e0, r.e1));
+    ProfClass* c = nullptr;
+    for (ProfClass& k : g_prof_classes)
+      if (k.name == r.name) c = &k;
+    if (!c) {
+      g_prof_classes.push_back(ProfClass{r.name, r.kind});
+      c = &g_prof_classes.back();
+    }
+    c->launches += 1;
+    c->ms += ms;
+    c->flops += r.flops;
+    c->bytes += r.bytes;
+    g_prof_pool.push_back(r.e0);
+    g_prof_pool.push_back(r.e1);
+  }
+  g_prof_recs.clear();
+}
+}  // namespace
+
+void prof_begin(cudaStream_t st) {
+  if (!g_prof_on) return;
+  if (!g_prof_pending) g_prof_pending = prof_event();
+  RTE_CHECK_CUDA(cudaEventRecord(g_prof_pending, st));
+}
+
+void after_launch(const char* what, cudaStream_t st, double flops, double bytes, int kind) {
   ++g_launches;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("launch of ") + what + " failed: " + cudaGetErrorString(e));
     throw Fail{RTE_ECUDA};
+  }
+  if (g_prof_on && g_prof_pending) {
+    cudaEvent_t e1 = prof_event();
+    RTE_CHECK_CUDA(cudaEventRecord(e1, st));
+    g_prof_recs.push_back(ProfRec{what, g_prof_pending, e1, flops, bytes, kind});
+    g_prof_pending = nullptr;
   }
 }
 
@@ -146,6 +216,40 @@ int64_t rte_launch_count(int reset) {
   int64_t v = g_launches;
   if (reset) g_launches = 0;
   return v;
+}
+
+rte_status rte_timing_enable(int on) {
+  RTE_API_BEGIN
+  g_prof_on = on != 0;
+  RTE_API_END
+}
+
+rte_status rte_timing_reset(void) {
+  RTE_API_BEGIN
+  prof_resolve();
+  g_prof_classes.clear();
+  RTE_API_END
+}
+
+rte_status rte_timing_get(int idx, char* name, int name_len, int* kind, int64_t* launches, double* ms,
+                          double* flops, double* bytes, int* count) {
+  RTE_API_BEGIN
+  prof_resolve();
+  if (count) *count = (int)g_prof_classes.size();
+  if (idx >= 0) {
+    RTE_REQUIRE(idx < (int)g_prof_classes.size(), "rte_timing_get: index out of range");
+    const ProfClass& c = g_prof_classes[idx];
+    if (name && name_len > 0) {
+      strncpy(name, c.name.c_str(), name_len - 1);
+      name[name_len - 1] = 0;
+    }
+    if (kind) *kind = c.kind;
+    if (launches) *launches = c.launches;
+    if (ms) *ms = c.ms;
+    if (flops) *flops = c.flops;
+    if (bytes) *bytes = c.bytes;
+  }
+  RTE_API_END
 }
 
 static void free_problem(rte_problem* p) {
