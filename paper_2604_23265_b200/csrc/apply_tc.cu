@@ -1,12 +1,110 @@
-// Tensor-core (tcgen05, 3xTF32) fused stencil + scattering GEMM apply.  Placeholder until the
-// tcgen05 kernel lands: reports "unsupported" so rte_apply takes the SIMT kernel in apply.cu.
+// rte_apply on the tcgen05 tensor cores: the scattering contraction Psi[cells x M] . S^T[M x M]
+// (eq:DORTE_2d with the row-normalised HG matrix, R4-R5) as a 3xTF32
+// GEMM (tc_gemm.cuh, mode 0 / 1x1 "conv" with Ci = Co = M), fused with the upwind stencil and
+// the sigma_t diagonal in the epilogue (R9):
+//   y_{jim} = alpha [ (|c_m|/h + |s_m|/h + sigma_t) psi_{jim} - sigma_s (Psi S^T)_{jim}
+//                     - (|c_m|/h) psi_{j,i-sgn c_m,m} - (|s_m|/h) psi_{j-sgn s_m,i,m} ]
+// Each epilogue thread owns one cell (a TMEM lane) and 32 ordinates per TMEM load; psi at the cell
+// and at its two upwind neighbours is re-read from L2 (the A tiles just streamed through it).
+// Per-sample S (config 4) is selected by the B-operand row offset b*M.
+#include <algorithm>
+
 #include "common.h"
+#include "tc_gemm.cuh"
+#include "tc_host.h"
 
 namespace rte {
-bool apply_tc_supported(int) { return false; }
-void free_tc_state(rte_problem*) {}
-void launch_apply_tc(const rte_problem*, const float*, float*, const double*, int, cudaStream_t) {
-  set_error("tensor-core apply not available");
-  throw Fail{RTE_EINTERNAL};
+namespace tc {
+
+struct EpiApply {
+  const float* x;
+  float* y;
+  const float* sig_t;
+  const float* sig_s;
+  const float* ax;
+  const float* ay;
+  const int8_t* sgx;
+  const int8_t* sgy;
+  const double* alpha;
+  int alpha_stride, N, M;
+
+  __device__ __forceinline__ void store(int b, int, int j, int i, int m0, const float (&v)[32]) const {
+    const long long cell = ((long long)b * N + j) * N + i;
+    const float st = sig_t[cell], ss = sig_s[cell];
+    const float al = alpha ? (float)alpha[(long long)b * alpha_stride] : 1.f;
+    const float4* xc = reinterpret_cast<const float4*>(x + cell * M + m0);
+    float4* yo = reinterpret_cast<float4*>(y + cell * M + m0);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float4 p4 = xc[q];
+      const float pv[4] = {p4.x, p4.y, p4.z, p4.w};
+      float r[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int m = m0 + 4 * q + e;
+        const float a_x = ax[m], a_y = ay[m];
+        const int sx = sgx[m], sy = sgy[m];
+        float val = (a_x + a_y + st) * pv[e] - ss * v[4 * q + e];
+        const int ii = i - sx, jj = j - sy;
+        if (ii >= 0 && ii < N) val -= a_x * x[(cell - sx) * M + m];
+        if (jj >= 0 && jj < N) val -= a_y * x[(cell - (long long)sy * N) * M + m];
+        r[e] = val * al;
+      }
+      yo[q] = make_float4(r[0], r[1], r[2], r[3]);
+    }
+  }
+  __device__ __forceinline__ void store_partial(int, int, int, int, int, int, const float (&)[32]) const {}
+};
+
+template <int BN>
+void launch_apply_bn(const Geom& g, int mtiles, const CUtensorMap& ta, const CUtensorMap& tbh,
+                     const CUtensorMap& tbl, const EpiApply& epi, cudaStream_t st) {
+  auto kern = gemm3xtf32_kernel<BN, EpiApply>;
+  constexpr int smem = gemm_smem_bytes<BN>();
+  ensure_smem((const void*)kern, smem);
+  kern<<<dim3(mtiles, epi.M / BN, 1), kGemmThreads, smem, st>>>(ta, tbh, tbl, g, epi);
 }
+
+}  // namespace tc
+
+bool apply_tc_supported(int M) { return M >= 32 && M <= 1024 && M % 32 == 0; }
+
+void free_tc_state(rte_problem*) {}
+
+void launch_apply_tc(const rte_problem* p, const float* x, float* y, const double* alpha, int alpha_stride,
+                     cudaStream_t st) {
+  const int N = p->N, M = p->M, B = p->B;
+  int BN = 32;
+  while (BN < 256 && BN * 2 <= M && M % (BN * 2) == 0) BN *= 2;
+  tc::Geom g{};
+  g.mode = 0;
+  g.ks = 1;
+  g.cchunks = M / 32;
+  g.taps = 1;
+  g.classes = 1;
+  g.Hc = g.Wc = N;
+  g.TW = std::min(N, 128);
+  g.TH = std::min(N, std::max(1, 128 / g.TW));
+  g.tiles_x = (N + g.TW - 1) / g.TW;
+  g.tiles_y = (N + g.TH - 1) / g.TH;
+  g.kb_total = g.cchunks;
+  g.kb_per_split = g.kb_total;
+  g.nsplit = 1;
+  g.b_rows_class = 0;
+  g.b_rows_batch = M;
+  const int mtiles = B * g.tiles_y * g.tiles_x;
+  CUtensorMap ta = tc::make_map_act(x, M, N, N, B, g.TW, g.TH, 1);
+  CUtensorMap tbh = tc::make_map_kmajor(p->S_hi, M, B * M, BN);
+  CUtensorMap tbl = tc::make_map_kmajor(p->S_lo, M, B * M, BN);
+  tc::EpiApply epi{x, y, p->sig_t, p->sig_s, p->ax, p->ay, p->sgx, p->sgy, alpha, alpha_stride, N, M};
+  prof_begin(st);
+  switch (BN) {
+    case 32: tc::launch_apply_bn<32>(g, mtiles, ta, tbh, tbl, epi, st); break;
+    case 64: tc::launch_apply_bn<64>(g, mtiles, ta, tbh, tbl, epi, st); break;
+    case 128: tc::launch_apply_bn<128>(g, mtiles, ta, tbh, tbl, epi, st); break;
+    default: tc::launch_apply_bn<256>(g, mtiles, ta, tbh, tbl, epi, st); break;
+  }
+  after_launch("apply_f32_tc", st, apply_flops(p), apply_bytes(p, 4, 0), p->M >= 256 ? 1 : 0);
+}
+
 }  // namespace rte

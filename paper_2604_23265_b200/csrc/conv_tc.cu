@@ -1,11 +1,367 @@
-// Tensor-core (tcgen05, 3xTF32) implicit-GEMM convolutions.  Placeholder until the tcgen05
-// kernel lands: every shape falls back to the SIMT implicit GEMM in mgnet.cu.
+// MgNet convolutions on the tcgen05 tensor cores, 3xTF32 (R26, §5).
+//
+// Every conv of the V-cycle is an implicit GEMM
+//   out[pixels x Co] = sum_{tap, ci-chunk} X_shift(tap)[pixels x 32] . W_tap[Co x 32]^T
+// run by the warp-specialised kernel of tc_gemm.cuh:
+//   mode 0: 3x3 (or 1x1) stride 1, pad 1 (0)          -- smoother convs, lift, head
+//   mode 1: 3x3 stride 2, pad 1 (TMA traversal stride 2) -- restriction R
+//   mode 2: 4x4 stride-2 transposed, pad 1: split into its 4 output parity classes, each a
+//           2x2 stride-1 conv on the coarse grid (sub-pixel decomposition) -- prolongation P
+// The zero padding is the TMA out-of-bounds fill.  The epilogue fuses the smoother's residual /
+// update (out = sign * s_in * acc + s_add * addend) and the Krylov scale alpha.  Small grids use
+// deterministic split-K (fp32 partials, fixed-order reduction kernel that applies the epilogue).
+// Shapes the kernel does not take (Ci % 32 != 0, Co not a multiple of the N tile) return false
+// and run on the SIMT implicit GEMM in mgnet.cu.
+#include <math.h>
+#include <string.h>
+
+#include <algorithm>
+#include <mutex>
+#include <set>
+#include <string>
+#include <vector>
+
 #include "mgnet.h"
+#include "tc_gemm.cuh"
+#include "tc_host.h"
 
 namespace rte {
-bool conv_tc_try(const ConvDesc&, const float*, float*, const float*, float, const double*, int, bool, bool,
-                 cudaStream_t) {
-  return false;
+namespace tc {
+
+// ---- host helpers (tc_host.h) ------------------------------------------------------------
+namespace {
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  if (!fn) {
+    set_error("cuTensorMapEncodeTiled is not available from the driver");
+    throw Fail{RTE_ECUDA};
+  }
+  return fn;
 }
-void conv_tc_prepare(mgnet_net* net) { net->tc = false; }
+
+void encode(CUtensorMap* m, int rank, const void* base, const cuuint64_t* dims, const cuuint64_t* strides,
+            const cuuint32_t* box, const cuuint32_t* es) {
+  CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (cuuint32_t)rank, const_cast<void*>(base), dims,
+                           strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (code " + std::to_string((int)r) + ")");
+    throw Fail{RTE_ECUDA};
+  }
+}
+}  // namespace
+
+CUtensorMap make_map_act(const float* base, int C, int W, int H, int B, int box_w, int box_h, int es) {
+  CUtensorMap m;
+  cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)B};
+  cuuint64_t strides[3] = {(cuuint64_t)C * 4, (cuuint64_t)W * C * 4, (cuuint64_t)H * W * C * 4};
+  cuuint32_t box[4] = {32u, (cuuint32_t)(box_w * es), (cuuint32_t)(box_h * es), 1u};
+  cuuint32_t est[4] = {1u, (cuuint32_t)es, (cuuint32_t)es, 1u};
+  encode(&m, 4, base, dims, strides, box, est);
+  return m;
+}
+
+CUtensorMap make_map_kmajor(const float* base, int K, int rows, int box_rows) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)K * 4};
+  cuuint32_t box[2] = {32u, (cuuint32_t)box_rows};
+  cuuint32_t est[2] = {1u, 1u};
+  encode(&m, 2, base, dims, strides, box, est);
+  return m;
+}
+
+float tf32_rna_host(float v) {
+  uint32_t u;
+  memcpy(&u, &v, 4);
+  if ((u & 0x7f800000u) != 0x7f800000u) u = (u + 0x1000u) & 0xffffe000u;
+  float r;
+  memcpy(&r, &u, 4);
+  return r;
+}
+
+void split_host(const std::vector<float>& w, std::vector<float>& hi, std::vector<float>& lo) {
+  hi.resize(w.size());
+  lo.resize(w.size());
+  for (size_t i = 0; i < w.size(); ++i) {
+    hi[i] = tf32_rna_host(w[i]);
+    lo[i] = tf32_rna_host(w[i] - hi[i]);
+  }
+}
+
+void ensure_smem(const void* kernel, int bytes) {
+  static std::mutex mu;
+  static std::set<const void*> done;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count(kernel)) return;
+  RTE_CHECK_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  done.insert(kernel);
+}
+
+// ---- conv epilogue -------------------------------------------------------------------------
+struct EpiConv {
+  float* out;
+  const float* addend;
+  const double* alpha;
+  float* part;            // split-K partials (nsplit x output elements) or NULL
+  long long part_stride;  // elements per split
+  float sign;
+  int alpha_stride, a_in, a_add;
+  int mode, Ho, Wo, Co;
+
+  __device__ __forceinline__ long long index(int b, int cls, int oy, int ox, int col) const {
+    int Y = oy, X = ox;
+    if (mode == 2) {
+      Y = 2 * oy + (cls >> 1);
+      X = 2 * ox + (cls & 1);
+    }
+    return (((long long)b * Ho + Y) * Wo + X) * Co + col;
+  }
+  __device__ __forceinline__ void store(int b, int cls, int oy, int ox, int col, const float (&v)[32]) const {
+    const long long o = index(b, cls, oy, ox, col);
+    const float al = alpha ? (float)alpha[(long long)b * alpha_stride] : 1.f;
+    const float s_in = sign * (a_in ? al : 1.f);
+    const float s_add = a_add ? al : 1.f;
+    float4* dst = reinterpret_cast<float4*>(out + o);
+    const float4* ad = reinterpret_cast<const float4*>(addend + o);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      float4 r = make_float4(s_in * v[4 * i], s_in * v[4 * i + 1], s_in * v[4 * i + 2], s_in * v[4 * i + 3]);
+      if (addend) {
+        const float4 a = ad[i];
+        r.x = fmaf(s_add, a.x, r.x);
+        r.y = fmaf(s_add, a.y, r.y);
+        r.z = fmaf(s_add, a.z, r.z);
+        r.w = fmaf(s_add, a.w, r.w);
+      }
+      dst[i] = r;
+    }
+  }
+  __device__ __forceinline__ void store_partial(int split, int b, int cls, int oy, int ox, int col,
+                                                const float (&v)[32]) const {
+    float4* dst = reinterpret_cast<float4*>(part + split * part_stride + index(b, cls, oy, ox, col));
+#pragma unroll
+    for (int i = 0; i < 8; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+  }
+};
+
+// Deterministic split-K reduction + epilogue: out[e] = s_in * sum_s partial[s][e] + s_add * addend[e].
+__global__ void splitk_reduce_kernel(const float4* __restrict__ part, long long stride4, int nsplit, float4* out,
+                                     const float4* addend, float sign, const double* __restrict__ alpha,
+                                     int alpha_stride, int a_in, int a_add, long long n4, long long per_sample4) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n4; e += (long long)gridDim.x * blockDim.x) {
+    float4 s = part[e];
+    for (int k = 1; k < nsplit; ++k) {
+      const float4 p = part[k * stride4 + e];
+      s.x += p.x;
+      s.y += p.y;
+      s.z += p.z;
+      s.w += p.w;
+    }
+    const int b = (int)(e / per_sample4);
+    const float al = alpha ? (float)alpha[(long long)b * alpha_stride] : 1.f;
+    const float si = sign * (a_in ? al : 1.f), sa = a_add ? al : 1.f;
+    float4 r = make_float4(si * s.x, si * s.y, si * s.z, si * s.w);
+    if (addend) {
+      const float4 a = addend[e];
+      r.x = fmaf(sa, a.x, r.x);
+      r.y = fmaf(sa, a.y, r.y);
+      r.z = fmaf(sa, a.z, r.z);
+      r.w = fmaf(sa, a.w, r.w);
+    }
+    out[e] = r;
+  }
+}
+
+}  // namespace tc
+
+// ---- planning --------------------------------------------------------------------------------
+namespace {
+
+struct Plan {
+  bool ok = false;
+  int BN = 0;
+  tc::Geom g{};
+  int mtiles = 0, ntiles = 0;
+  long long out_elems = 0;
+};
+
+Plan make_plan(const ConvDesc& d) {
+  Plan P;
+  if (d.Ci % 32 != 0 || d.Co % 32 != 0) return P;
+  if (d.mode == 0 && !(d.ks == 1 || d.ks == 3)) return P;
+  if (d.mode == 2 && (d.Ho % 2 || d.Wo % 2)) return P;
+  int BN = 32;
+  while (BN < 256 && BN * 2 <= d.Co && d.Co % (BN * 2) == 0) BN *= 2;
+  P.BN = BN;
+  tc::Geom& g = P.g;
+  g.mode = d.mode;
+  g.ks = (d.mode == 2) ? 4 : d.ks;
+  g.cchunks = d.Ci / 32;
+  g.taps = (d.mode == 2) ? 4 : d.ks * d.ks;
+  g.classes = (d.mode == 2) ? 4 : 1;
+  g.Hc = (d.mode == 2) ? d.Ho / 2 : d.Ho;
+  g.Wc = (d.mode == 2) ? d.Wo / 2 : d.Wo;
+  g.TW = std::min(g.Wc, 128);
+  g.TH = std::max(1, 128 / g.TW);
+  g.TH = std::min(g.TH, g.Hc);
+  g.tiles_x = (g.Wc + g.TW - 1) / g.TW;
+  g.tiles_y = (g.Hc + g.TH - 1) / g.TH;
+  g.kb_total = g.taps * g.cchunks;
+  g.b_rows_class = (d.mode == 2) ? d.Co : 0;
+  g.b_rows_batch = 0;
+  P.mtiles = d.B * g.classes * g.tiles_y * g.tiles_x;
+  P.ntiles = d.Co / BN;
+  const int ctas = P.mtiles * P.ntiles;
+  const int target = num_sms();
+  int nsplit = 1;
+  if (ctas < target) nsplit = std::min((target + ctas - 1) / ctas, std::max(1, g.kb_total / 4));
+  g.kb_per_split = (g.kb_total + nsplit - 1) / nsplit;
+  g.nsplit = (g.kb_total + g.kb_per_split - 1) / g.kb_per_split;
+  P.out_elems = (long long)d.B * d.Ho * d.Wo * d.Co;
+  P.ok = true;
+  return P;
+}
+
+template <int BN>
+void launch_bn(const Plan& P, const CUtensorMap& ta, const CUtensorMap& tbh, const CUtensorMap& tbl,
+               const tc::EpiConv& epi, cudaStream_t st) {
+  auto kern = tc::gemm3xtf32_kernel<BN, tc::EpiConv>;
+  constexpr int smem = tc::gemm_smem_bytes<BN>();
+  tc::ensure_smem((const void*)kern, smem);
+  dim3 grid(P.mtiles, P.ntiles, P.g.nsplit);
+  kern<<<grid, tc::kGemmThreads, smem, st>>>(ta, tbh, tbl, P.g, epi);
+}
+
+}  // namespace
+
+bool conv_tc_try(const ConvDesc& d, const float* in, float* out, const float* addend, float sign,
+                 const double* alpha, int alpha_stride, bool alpha_on_input, bool alpha_on_addend, cudaStream_t st) {
+  if (!d.w || !d.w->d_hi || !d.ws_owner || !d.ws_owner->tc) return false;
+  Plan P = make_plan(d);
+  if (!P.ok) return false;
+  const tc::Geom& g = P.g;
+  const int es = (d.mode == 1) ? 2 : 1;
+  CUtensorMap ta = tc::make_map_act(in, d.Ci, d.Wi, d.Hi, d.B, g.TW, g.TH, es);
+  CUtensorMap tbh = tc::make_map_kmajor(d.w->d_hi, d.w->tc_K, d.w->tc_rows, P.BN);
+  CUtensorMap tbl = tc::make_map_kmajor(d.w->d_lo, d.w->tc_K, d.w->tc_rows, P.BN);
+  tc::EpiConv epi;
+  epi.out = out;
+  epi.addend = addend;
+  epi.alpha = alpha;
+  epi.sign = sign;
+  epi.alpha_stride = alpha_stride;
+  epi.a_in = alpha_on_input ? 1 : 0;
+  epi.a_add = alpha_on_addend ? 1 : 0;
+  epi.mode = d.mode;
+  epi.Ho = d.Ho;
+  epi.Wo = d.Wo;
+  epi.Co = d.Co;
+  epi.part = nullptr;
+  epi.part_stride = P.out_elems;
+  if (g.nsplit > 1) {
+    if ((long long)g.nsplit * P.out_elems > (long long)d.ws_owner->tc_ws_elems) {
+      set_error("conv_tc: split-K workspace too small (internal planning mismatch)");
+      throw Fail{RTE_EINTERNAL};
+    }
+    epi.part = d.ws_owner->tc_ws;
+  }
+  prof_begin(st);
+  switch (P.BN) {
+    case 32: launch_bn<32>(P, ta, tbh, tbl, epi, st); break;
+    case 64: launch_bn<64>(P, ta, tbh, tbl, epi, st); break;
+    case 128: launch_bn<128>(P, ta, tbh, tbl, epi, st); break;
+    default: launch_bn<256>(P, ta, tbh, tbl, epi, st); break;
+  }
+  const bool split = g.nsplit > 1;
+  after_launch(conv_class_name(d, true), st, conv_flops(d), split ? 0.0 : conv_bytes(d, addend != nullptr), 1);
+  if (split) {
+    prof_begin(st);
+    const long long n4 = P.out_elems / 4;
+    const long long per4 = n4 / d.B;
+    const int blocks = (int)std::min<long long>((n4 + 255) / 256, (long long)num_sms() * 8);
+    tc::splitk_reduce_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const float4*>(d.ws_owner->tc_ws), n4,
+                                                     g.nsplit, reinterpret_cast<float4*>(out),
+                                                     reinterpret_cast<const float4*>(addend), sign, alpha,
+                                                     alpha_stride, epi.a_in, epi.a_add, n4, per4);
+    // the conv's algorithmic bytes are booked on the reduction (it writes the output)
+    after_launch("splitk_reduce", st, 0.0, conv_bytes(d, addend != nullptr) + 4.0 * g.nsplit * P.out_elems, 0);
+  }
+  return true;
+}
+
+// Upload the tensor-core operand layouts of every conv weight and size the split-K workspace.
+void conv_tc_prepare(mgnet_net* net) {
+  net->tc = (getenv("RTE_DISABLE_TC") == nullptr);
+  if (!net->tc) return;
+  for (ConvW& w : net->convs) {
+    std::vector<float> mat;
+    if (w.kind == 0) {
+      w.tc_rows = w.Co;
+      w.tc_K = w.taps * w.Ci;
+      mat = w.host_nk;  // [co][tap][ci]
+    } else {
+      // transposed 4x4: 4 parity classes (py,px) stacked as rows, K = (tap t, ci) with
+      // ky = (py ? 0 : 1) + 2 (t >> 1), kx = (px ? 0 : 1) + 2 (t & 1)
+      w.tc_rows = 4 * w.Co;
+      w.tc_K = 4 * w.Ci;
+      mat.assign((size_t)w.tc_rows * w.tc_K, 0.f);
+      for (int cls = 0; cls < 4; ++cls)
+        for (int co = 0; co < w.Co; ++co)
+          for (int t = 0; t < 4; ++t)
+            for (int ci = 0; ci < w.Ci; ++ci) {
+              const int ky = ((cls >> 1) ? 0 : 1) + 2 * (t >> 1);
+              const int kx = ((cls & 1) ? 0 : 1) + 2 * (t & 1);
+              mat[((size_t)cls * w.Co + co) * w.tc_K + (size_t)t * w.Ci + ci] =
+                  w.host_nk[((size_t)co * 16 + ky * 4 + kx) * w.Ci + ci];
+            }
+    }
+    std::vector<float> hi, lo;
+    tc::split_host(mat, hi, lo);
+    w.d_hi = dalloc<float>(hi.size());
+    upload(w.d_hi, hi.data(), hi.size());
+    w.d_lo = dalloc<float>(lo.size());
+    upload(w.d_lo, lo.data(), lo.size());
+  }
+  // split-K workspace: the largest nsplit * output over every conv shape of the V-cycle
+  size_t need = 0;
+  auto consider = [&](int mode, int ks, int Hi, int Ci, int Ho, int Co) {
+    ConvDesc d;
+    d.B = net->B;
+    d.mode = mode;
+    d.ks = ks;
+    d.Hi = d.Wi = Hi;
+    d.Ci = Ci;
+    d.Ho = d.Wo = Ho;
+    d.Co = Co;
+    Plan P = make_plan(d);
+    if (P.ok && P.g.nsplit > 1) need = std::max(need, (size_t)P.g.nsplit * (size_t)P.out_elems);
+  };
+  consider(0, 1, net->N, net->M, net->N, net->C0);
+  consider(0, 1, net->N, net->C0, net->N, net->M);
+  for (int l = 0; l < net->L; ++l) {
+    const Level& V = net->lv[l];
+    consider(0, 3, V.H, V.C, V.H, V.C);
+    if (l < net->L - 1) {
+      consider(1, 3, V.H, V.C, V.H / 2, 2 * V.C);
+      consider(2, 4, V.H / 2, 2 * V.C, V.H, V.C);
+    }
+  }
+  if (need) {
+    net->tc_ws = dalloc<float>(need);
+    net->tc_ws_elems = need;
+  }
+}
+
 }  // namespace rte

@@ -242,6 +242,7 @@ extern "C" {
 void mgnet_destroy(mgnet_net* net) {
   if (!net) return;
   for (auto& c : net->convs) c.release();
+  dfree(net->tc_ws);
   for (auto& lv : net->lv) {
     dfree(lv.f);
     dfree(lv.u);
@@ -352,6 +353,7 @@ void vcycle_run(const mgnet_net* net, const float* r, float* z, bool add_identit
   auto conv = [&](int widx, ConvDesc d, const float* in, float* out, const float* addend, float sign,
                   bool a_in = false, bool a_add = false) {
     d.w = &net->convs[widx];
+    d.ws_owner = net;
     launch_conv(d, in, net->convs[widx].d_kn, out, addend, sign, alpha, alpha_stride, a_in, a_add, st);
   };
   // f^0 = Lambda (alpha r)

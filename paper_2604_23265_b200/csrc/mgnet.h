@@ -11,8 +11,9 @@ struct ConvW {
   int kind = 0;       // 0: OIHW conv, 1: IOHW conv_transpose
   int Co = 0, Ci = 0, ks = 0, taps = 0;
   float* d_kn = nullptr;   // [tap][ci][co]
-  float* d_hi = nullptr;   // tensor-core operand: [co][tap][ci] tf32 hi
+  float* d_hi = nullptr;   // tensor-core operand [tc_rows][tc_K] K-major, tf32 hi (conv_tc.cu)
   float* d_lo = nullptr;   //                       tf32 lo
+  int tc_rows = 0, tc_K = 0;
   std::vector<float> host_nk;  // [co][tap][ci]
   void build(const float* w, int kind, int Co, int Ci, int ks);
   void release();
@@ -22,6 +23,7 @@ struct ConvDesc {
   int B = 1, mode = 0, ks = 3;       // mode 0: stride-1 (ks 1 or 3), 1: stride-2 3x3, 2: transposed 4x4 s2
   int Hi = 0, Wi = 0, Ci = 0, Ho = 0, Wo = 0, Co = 0;
   const ConvW* w = nullptr;
+  const struct ::mgnet_net* ws_owner = nullptr;  // net owning the split-K workspace (tensor-core path)
 };
 
 struct Level {
@@ -54,5 +56,7 @@ struct mgnet_net {
   std::vector<rte::ConvW> convs;
   std::vector<rte::Level> lv;
   int lift = -1, head = -1;
-  bool tc = false;
+  bool tc = false;                 // tensor-core convs enabled (conv_tc_prepare)
+  float* tc_ws = nullptr;          // split-K partials
+  size_t tc_ws_elems = 0;
 };

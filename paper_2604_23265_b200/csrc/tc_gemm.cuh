@@ -1,0 +1,249 @@
+// Warp-specialised 3xTF32 implicit GEMM on tcgen05 (sm_100a), shared by the MgNet convolutions
+// (conv_tc.cu) and the scattering contraction of rte_apply (apply_tc.cu).  NOT part of the ABI.
+//
+// One CTA computes a 128-pixel x BN-channel output tile over a range of K blocks (split-K):
+//   D[128 x BN] (TMEM, fp32) = sum_kb  A_kb[128 x 32] . B_kb[BN x 32]^T
+// where a K block kb = (tap, 32-channel chunk).  A_kb is a shifted (and for the stride-2
+// restriction, strided) window of the NHWC activation, fetched by a 4-D TMA tiled load whose
+// out-of-bounds zero fill implements the convolution's zero padding; B_kb is a 32-wide K slice of
+// the weights stored [rows][K] K-major.  3xTF32 (R26): A is split in shared memory into
+// hi = rna_tf32(a) (in place) and lo = rna_tf32(a - hi); the weights arrive pre-split; each
+// k-step issues lo.hi + hi.lo + hi.hi into the same TMEM accumulator.
+//
+// Warp roles (192 threads): warp 0 = TMA producer, warp 1 = TMEM allocator + MMA issuer (one
+// elected lane), warps 2..5 = A-operand hi/lo converters, then the epilogue (TMEM -> registers ->
+// global; warp w owns TMEM lanes 32*(w%4) .. +31).  Pipelines: full[s] (TMA bytes landed) ->
+// conv[s] (hi/lo written) -> empty[s] (MMAs done, tcgen05.commit) and tmem_full (last MMA done).
+#pragma once
+
+#include <cuda.h>
+#include <stdint.h>
+
+#include "tc_common.cuh"
+
+namespace rte {
+namespace tc {
+
+constexpr int kGemmThreads = 192;
+constexpr int kTileM = 128;
+constexpr int kABytes = kTileM * 128;   // 128 rows x 32 fp32
+
+// Geometry of the A/B K-block walk (see header comment).
+struct Geom {
+  int mode;         // 0: KSxKS stride 1 (pad KS/2); 1: 3x3 stride 2 pad 1; 2: 4x4 stride-2 transposed, per class
+  int ks;           // mode 0/1 kernel size
+  int cchunks;      // Ci / 32
+  int taps;         // taps per output pixel (ks*ks, or 4 for mode 2)
+  int TW, TH;       // output tile (TW*TH <= 128 pixels of the output (class) grid)
+  int tiles_x, tiles_y;
+  int classes;      // 1, or 4 parity classes (mode 2)
+  int Hc, Wc;       // output (class) grid size
+  int kb_total;     // taps * cchunks
+  int kb_per_split;
+  int nsplit;
+  int b_rows_class; // B-operand row offset per class (mode 2)
+  int b_rows_batch; // B-operand row offset per batch sample (per-sample operators)
+};
+
+template <int BN>
+struct Smem {
+  static constexpr int kBBytes = BN * 128;
+  static constexpr int kStage = 2 * kABytes + 2 * kBBytes;
+};
+
+template <int BN>
+constexpr int gemm_stages() {
+  return (2 * kABytes + 2 * BN * 128) * 4 <= 200 * 1024 ? 4 : ((2 * kABytes + 2 * BN * 128) * 3 <= 200 * 1024 ? 3 : 2);
+}
+
+template <int BN>
+constexpr int gemm_smem_bytes() {
+  return gemm_stages<BN>() * Smem<BN>::kStage + 1024 /*align*/ + 256 /*barriers*/;
+}
+
+struct TileCoord {
+  int b, cls, ty, tx;
+};
+
+__device__ __forceinline__ TileCoord decode_tile(const Geom& g, int t) {
+  TileCoord c;
+  c.tx = t % g.tiles_x;
+  t /= g.tiles_x;
+  c.ty = t % g.tiles_y;
+  t /= g.tiles_y;
+  c.cls = t % g.classes;
+  c.b = t / g.classes;
+  return c;
+}
+
+// A-window origin (x, y) in the input tensor for K block kb of tile c.
+__device__ __forceinline__ void a_origin(const Geom& g, const TileCoord& c, int tap, int& xA, int& yA) {
+  if (g.mode == 0) {
+    const int ky = tap / g.ks, kx = tap % g.ks, p = g.ks / 2;
+    xA = c.tx * g.TW + kx - p;
+    yA = c.ty * g.TH + ky - p;
+  } else if (g.mode == 1) {
+    const int ky = tap / 3, kx = tap % 3;
+    xA = 2 * (c.tx * g.TW) + kx - 1;
+    yA = 2 * (c.ty * g.TH) + ky - 1;
+  } else {
+    const int py = c.cls >> 1, px = c.cls & 1, ty_ = tap >> 1, tx_ = tap & 1;
+    yA = c.ty * g.TH + (py ? 1 - ty_ : -ty_);
+    xA = c.tx * g.TW + (px ? 1 - tx_ : -tx_);
+  }
+}
+
+// Epilogue interface:  epi.store(b, cls, oy, ox, n0, col0, v[32]) for every valid output pixel
+// (oy, ox) of the class grid, columns n0+col0 .. +31;  epi.store_partial(split, b, cls, oy, ox, ...)
+// when split-K is active (nsplit > 1).
+template <int BN, class Epi>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    gemm3xtf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBhi,
+                      const __grid_constant__ CUtensorMap tmBlo, const Geom g, const Epi epi) {
+  constexpr int STAGES = gemm_stages<BN>();
+  constexpr int BBYTES = Smem<BN>::kBBytes;
+  constexpr int STAGE = Smem<BN>::kStage;
+  constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE);
+  uint64_t* full = bars;
+  uint64_t* conv = bars + STAGES;
+  uint64_t* empty = bars + 2 * STAGES;
+  uint64_t* tfull = bars + 3 * STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const TileCoord tc = decode_tile(g, blockIdx.x);
+  const int n0 = blockIdx.y * BN;
+  const int split = blockIdx.z;
+  const int kb0 = split * g.kb_per_split;
+  const int kb1 = min(g.kb_total, kb0 + g.kb_per_split);
+  const int rows = g.TW * g.TH;
+  const uint32_t a_bytes = (uint32_t)rows * 128u;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&conv[s], 4);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmBhi);
+    tma_prefetch(&tmBlo);
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ===== TMA producer =====
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      const int brow = n0 + tc.cls * g.b_rows_class + tc.b * g.b_rows_batch;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(&empty[s], ph ^ 1);
+        uint8_t* sa = smem + s * STAGE;
+        uint8_t* sbh = sa + 2 * kABytes;
+        uint8_t* sbl = sbh + BBYTES;
+        const int tap = kb / g.cchunks, ci0 = (kb % g.cchunks) * 32;
+        int xA, yA;
+        a_origin(g, tc, tap, xA, yA);
+        mbar_arrive_expect_tx(&full[s], a_bytes + 2u * BBYTES);
+        tma_load_4d(sa, &tmA, &full[s], ci0, xA, yA, tc.b);
+        tma_load_2d(sbh, &tmBhi, &full[s], kb * 32, brow);
+        tma_load_2d(sbl, &tmBlo, &full[s], kb * 32, brow);
+        if (++s == STAGES) { s = 0; ph ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    // ===== MMA issuer =====
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_tf32(kTileM, BN);
+      int s = 0;
+      uint32_t ph = 0;
+      uint32_t acc = 0;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(&conv[s], ph);
+        tc_fence_after();
+        const uint32_t sa = smem_u32(smem + s * STAGE);
+        const uint32_t sal = sa + kABytes;
+        const uint32_t sbh = sa + 2 * kABytes;
+        const uint32_t sbl = sbh + BBYTES;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t o = 32u * k;
+          mma_tf32(tmem, sdesc_sw128(sal + o), sdesc_sw128(sbh + o), idesc, acc);
+          acc = 1;
+          mma_tf32(tmem, sdesc_sw128(sa + o), sdesc_sw128(sbl + o), idesc, 1);
+          mma_tf32(tmem, sdesc_sw128(sa + o), sdesc_sw128(sbh + o), idesc, 1);
+        }
+        mma_commit(&empty[s]);
+        if (++s == STAGES) { s = 0; ph ^= 1; }
+      }
+      mma_commit(tfull);
+    }
+  } else {
+    // ===== converters (warps 2..5), then epilogue =====
+    const int ct = threadIdx.x - 64;  // 0..127
+    {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(&full[s], ph);
+        float4* a = reinterpret_cast<float4*>(smem + s * STAGE);
+        float4* al = reinterpret_cast<float4*>(smem + s * STAGE + kABytes);
+#pragma unroll
+        for (int i = 0; i < kABytes / 16 / 128; ++i) {
+          const int q = ct + 128 * i;
+          float4 v = a[q], h, l;
+          split_tf32(v.x, h.x, l.x);
+          split_tf32(v.y, h.y, l.y);
+          split_tf32(v.z, h.z, l.z);
+          split_tf32(v.w, h.w, l.w);
+          a[q] = h;
+          al[q] = l;
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&conv[s]);
+        if (++s == STAGES) { s = 0; ph ^= 1; }
+      }
+    }
+    // epilogue
+    mbar_wait(tfull, 0);
+    tc_fence_after();
+    const int quarter = warp & 3;
+    const int r = quarter * 32 + lane;  // tile row = TMEM lane
+    const int ly = r / g.TW, lx = r - ly * g.TW;
+    const int oy = tc.ty * g.TH + ly, ox = tc.tx * g.TW + lx;
+    const bool valid = (r < rows) && (oy < g.Hc) && (ox < g.Wc);
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+      float v[32];
+      tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c0, v);
+      if (valid) {
+        if (g.nsplit > 1)
+          epi.store_partial(split, tc.b, tc.cls, oy, ox, n0 + c0, v);
+        else
+          epi.store(tc.b, tc.cls, oy, ox, n0 + c0, v);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, TMEM_COLS);
+  }
+}
+
+}  // namespace tc
+}  // namespace rte
