@@ -62,7 +62,7 @@ void launch_apply_bn(const Geom& g, int mtiles, const CUtensorMap& ta, const CUt
   auto kern = gemm3xtf32_kernel<BN, EpiApply>;
   constexpr int smem = gemm_smem_bytes<BN>();
   ensure_smem((const void*)kern, smem);
-  kern<<<dim3(mtiles, epi.M / BN, 1), kGemmThreads, smem, st>>>(ta, tbh, tbl, g, epi);
+  kern<<<dim3(mtiles * g.ntiles, 1, 1), kGemmThreads, smem, st>>>(ta, tbh, tbl, g, epi);
 }
 
 }  // namespace tc
@@ -75,7 +75,7 @@ void launch_apply_tc(const rte_problem* p, const float* x, float* y, const doubl
                      cudaStream_t st) {
   const int N = p->N, M = p->M, B = p->B;
   int BN = 32;
-  while (BN < 256 && BN * 2 <= M && M % (BN * 2) == 0) BN *= 2;
+  while (BN < 128 && BN * 2 <= M && M % (BN * 2) == 0) BN *= 2;
   tc::Geom g{};
   g.mode = 0;
   g.ks = 1;
@@ -92,6 +92,7 @@ void launch_apply_tc(const rte_problem* p, const float* x, float* y, const doubl
   g.nsplit = 1;
   g.b_rows_class = 0;
   g.b_rows_batch = M;
+  g.ntiles = M / BN;
   const int mtiles = B * g.tiles_y * g.tiles_x;
   CUtensorMap ta = tc::make_map_act(x, M, N, N, B, g.TW, g.TH, 1);
   CUtensorMap tbh = tc::make_map_kmajor(p->S_hi, M, B * M, BN);
@@ -101,8 +102,7 @@ void launch_apply_tc(const rte_problem* p, const float* x, float* y, const doubl
   switch (BN) {
     case 32: tc::launch_apply_bn<32>(g, mtiles, ta, tbh, tbl, epi, st); break;
     case 64: tc::launch_apply_bn<64>(g, mtiles, ta, tbh, tbl, epi, st); break;
-    case 128: tc::launch_apply_bn<128>(g, mtiles, ta, tbh, tbl, epi, st); break;
-    default: tc::launch_apply_bn<256>(g, mtiles, ta, tbh, tbl, epi, st); break;
+    default: tc::launch_apply_bn<128>(g, mtiles, ta, tbh, tbl, epi, st); break;
   }
   after_launch("apply_f32_tc", st, apply_flops(p), apply_bytes(p, 4, 0), p->M >= 256 ? 1 : 0);
 }

@@ -203,7 +203,7 @@ Plan make_plan(const ConvDesc& d) {
   if (d.mode == 0 && !(d.ks == 1 || d.ks == 3)) return P;
   if (d.mode == 2 && (d.Ho % 2 || d.Wo % 2)) return P;
   int BN = 32;
-  while (BN < 256 && BN * 2 <= d.Co && d.Co % (BN * 2) == 0) BN *= 2;
+  while (BN < 128 && BN * 2 <= d.Co && d.Co % (BN * 2) == 0) BN *= 2;
   P.BN = BN;
   tc::Geom& g = P.g;
   g.mode = d.mode;
@@ -223,6 +223,7 @@ Plan make_plan(const ConvDesc& d) {
   g.b_rows_batch = 0;
   P.mtiles = d.B * g.classes * g.tiles_y * g.tiles_x;
   P.ntiles = d.Co / BN;
+  g.ntiles = P.ntiles;
   const int ctas = P.mtiles * P.ntiles;
   const int target = num_sms();
   int nsplit = 1;
@@ -240,7 +241,7 @@ void launch_bn(const Plan& P, const CUtensorMap& ta, const CUtensorMap& tbh, con
   auto kern = tc::gemm3xtf32_kernel<BN, tc::EpiConv>;
   constexpr int smem = tc::gemm_smem_bytes<BN>();
   tc::ensure_smem((const void*)kern, smem);
-  dim3 grid(P.mtiles, P.ntiles, P.g.nsplit);
+  dim3 grid(P.mtiles * P.ntiles, 1, P.g.nsplit);
   kern<<<grid, tc::kGemmThreads, smem, st>>>(ta, tbh, tbl, P.g, epi);
 }
 
@@ -281,8 +282,7 @@ bool conv_tc_try(const ConvDesc& d, const float* in, float* out, const float* ad
   switch (P.BN) {
     case 32: launch_bn<32>(P, ta, tbh, tbl, epi, st); break;
     case 64: launch_bn<64>(P, ta, tbh, tbl, epi, st); break;
-    case 128: launch_bn<128>(P, ta, tbh, tbl, epi, st); break;
-    default: launch_bn<256>(P, ta, tbh, tbl, epi, st); break;
+    default: launch_bn<128>(P, ta, tbh, tbl, epi, st); break;
   }
   const bool split = g.nsplit > 1;
   after_launch(conv_class_name(d, true), st, conv_flops(d), split ? 0.0 : conv_bytes(d, addend != nullptr), 1);

@@ -10,10 +10,11 @@
 // hi = rna_tf32(a) (in place) and lo = rna_tf32(a - hi); the weights arrive pre-split; each
 // k-step issues lo.hi + hi.lo + hi.hi into the same TMEM accumulator.
 //
-// Warp roles (192 threads): warp 0 = TMA producer, warp 1 = TMEM allocator + MMA issuer (one
-// elected lane), warps 2..5 = A-operand hi/lo converters, then the epilogue (TMEM -> registers ->
-// global; warp w owns TMEM lanes 32*(w%4) .. +31).  Pipelines: full[s] (TMA bytes landed) ->
-// conv[s] (hi/lo written) -> empty[s] (MMAs done, tcgen05.commit) and tmem_full (last MMA done).
+// Warp roles (320 threads): warp 0 = TMA producer, warp 1 = TMEM allocator + MMA issuer (one
+// elected lane), warps 2..5 = A-operand hi/lo converters, warps 6..9 = accumulator promotion and
+// the epilogue (TMEM -> registers -> global; warp w owns TMEM lanes 32*(w%4) .. +31).  Pipelines:
+// full[s] (TMA bytes landed) -> conv[s] (hi/lo written) -> empty[s] (MMAs done, tcgen05.commit);
+// mfull[t] / mempty[t] hand the two main-accumulator TMEM buffers between MMA and promoters.
 #pragma once
 
 #include <cuda.h>
@@ -24,7 +25,8 @@
 namespace rte {
 namespace tc {
 
-constexpr int kGemmThreads = 192;
+constexpr int kGemmThreads = 320;   // 10 warps (see kernel)
+constexpr int kPromoteKB = 4;       // K blocks per TMEM accumulation group
 constexpr int kTileM = 128;
 constexpr int kABytes = kTileM * 128;   // 128 rows x 32 fp32
 
@@ -43,6 +45,7 @@ struct Geom {
   int nsplit;
   int b_rows_class; // B-operand row offset per class (mode 2)
   int b_rows_batch; // B-operand row offset per batch sample (per-sample operators)
+  int ntiles;       // N tiles; blockIdx.x = m_tile * ntiles + n_tile (N fastest: A tile reuse in L2)
 };
 
 template <int BN>
@@ -58,7 +61,7 @@ constexpr int gemm_stages() {
 
 template <int BN>
 constexpr int gemm_smem_bytes() {
-  return gemm_stages<BN>() * Smem<BN>::kStage + 1024 /*align*/ + 256 /*barriers*/;
+  return gemm_stages<BN>() * Smem<BN>::kStage + 1024 /*align*/ + 512 /*barriers*/;
 }
 
 struct TileCoord {
@@ -93,32 +96,45 @@ __device__ __forceinline__ void a_origin(const Geom& g, const TileCoord& c, int 
   }
 }
 
-// Epilogue interface:  epi.store(b, cls, oy, ox, n0, col0, v[32]) for every valid output pixel
-// (oy, ox) of the class grid, columns n0+col0 .. +31;  epi.store_partial(split, b, cls, oy, ox, ...)
-// when split-K is active (nsplit > 1).
+// Epilogue interface:  epi.store(b, cls, oy, ox, col, v[32]) for every valid output pixel
+// (oy, ox) of the class grid, columns col .. col+31;  epi.store_partial(split, b, cls, oy, ox,
+// col, v) when split-K is active (nsplit > 1).
+//
+// Accumulation precision.  The tensor core's fp32 accumulation does not round to nearest (a
+// biased, truncating add), so a long K loop into one TMEM accumulator drifts by ~K/8 * 2^-24
+// relative.  Two measures keep the GEMM at fp32 accuracy:
+//   - the small 3xTF32 cross terms (lo.hi + hi.lo, ~2^-11 of the result) go to their own TMEM
+//     accumulator X, so the main accumulator sees one add per k-step;
+//   - the main product hi.hi accumulates for at most kPromoteKB K blocks in one of two TMEM
+//     buffers; four promoter warps then add the buffer into fp32 registers (round-to-nearest)
+//     while the MMA warp fills the other buffer (the "promotion" used by FP8 GEMMs).
 template <int BN, class Epi>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm3xtf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBhi,
                       const __grid_constant__ CUtensorMap tmBlo, const Geom g, const Epi epi) {
+  static_assert(BN == 32 || BN == 64 || BN == 128, "N tile must be 32, 64 or 128");
   constexpr int STAGES = gemm_stages<BN>();
   constexpr int BBYTES = Smem<BN>::kBBytes;
   constexpr int STAGE = Smem<BN>::kStage;
-  constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
+  constexpr uint32_t TMEM_COLS = BN == 32 ? 128 : (BN == 64 ? 256 : 512);  // >= 3*BN, power of 2
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE);
   uint64_t* full = bars;
   uint64_t* conv = bars + STAGES;
   uint64_t* empty = bars + 2 * STAGES;
-  uint64_t* tfull = bars + 3 * STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 1);
+  uint64_t* mfull = bars + 3 * STAGES;       // [2]
+  uint64_t* mempty = bars + 3 * STAGES + 2;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const TileCoord tc = decode_tile(g, blockIdx.x);
-  const int n0 = blockIdx.y * BN;
+  const TileCoord tc = decode_tile(g, blockIdx.x / g.ntiles);
+  const int n0 = (blockIdx.x % g.ntiles) * BN;
   const int split = blockIdx.z;
   const int kb0 = split * g.kb_per_split;
   const int kb1 = min(g.kb_total, kb0 + g.kb_per_split);
+  const int nkb = kb1 - kb0;
+  const int ngroups = (nkb + kPromoteKB - 1) / kPromoteKB;
   const int rows = g.TW * g.TH;
   const uint32_t a_bytes = (uint32_t)rows * 128u;
 
@@ -128,7 +144,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       mbar_init(&conv[s], 4);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tfull, 1);
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&mfull[t], 1);
+      mbar_init(&mempty[t], 4);
+    }
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
@@ -141,6 +160,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem_x = tmem + 2 * BN;  // cross-term accumulator columns
 
   if (warp == 0) {
     // ===== TMA producer =====
@@ -169,66 +189,95 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       constexpr uint32_t idesc = idesc_tf32(kTileM, BN);
       int s = 0;
       uint32_t ph = 0;
-      uint32_t acc = 0;
-      for (int kb = kb0; kb < kb1; ++kb) {
-        mbar_wait(&conv[s], ph);
+      uint32_t acc_x = 0;
+      for (int grp = 0; grp < ngroups; ++grp) {
+        const int t = grp & 1;
+        const uint32_t use = (uint32_t)(grp >> 1);
+        mbar_wait(&mempty[t], (use & 1u) ^ 1u);
         tc_fence_after();
-        const uint32_t sa = smem_u32(smem + s * STAGE);
-        const uint32_t sal = sa + kABytes;
-        const uint32_t sbh = sa + 2 * kABytes;
-        const uint32_t sbl = sbh + BBYTES;
+        const uint32_t tm = tmem + (uint32_t)(t * BN);
+        uint32_t acc_m = 0;
+        const int kbe = min(kb1, kb0 + (grp + 1) * kPromoteKB);
+        for (int kb = kb0 + grp * kPromoteKB; kb < kbe; ++kb) {
+          mbar_wait(&conv[s], ph);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + s * STAGE);
+          const uint32_t sal = sa + kABytes;
+          const uint32_t sbh = sa + 2 * kABytes;
+          const uint32_t sbl = sbh + BBYTES;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const uint32_t o = 32u * k;
-          mma_tf32(tmem, sdesc_sw128(sal + o), sdesc_sw128(sbh + o), idesc, acc);
-          acc = 1;
-          mma_tf32(tmem, sdesc_sw128(sa + o), sdesc_sw128(sbl + o), idesc, 1);
-          mma_tf32(tmem, sdesc_sw128(sa + o), sdesc_sw128(sbh + o), idesc, 1);
+          for (int k = 0; k < 4; ++k) {
+            const uint32_t o = 32u * k;
+            mma_tf32(tmem_x, sdesc_sw128(sal + o), sdesc_sw128(sbh + o), idesc, acc_x);
+            acc_x = 1;
+            mma_tf32(tmem_x, sdesc_sw128(sa + o), sdesc_sw128(sbl + o), idesc, 1);
+            mma_tf32(tm, sdesc_sw128(sa + o), sdesc_sw128(sbh + o), idesc, acc_m);
+            acc_m = 1;
+          }
+          mma_commit(&empty[s]);
+          if (++s == STAGES) { s = 0; ph ^= 1; }
         }
-        mma_commit(&empty[s]);
-        if (++s == STAGES) { s = 0; ph ^= 1; }
+        mma_commit(&mfull[t]);
       }
-      mma_commit(tfull);
+    }
+  } else if (warp < 6) {
+    // ===== converters (warps 2..5): A tile -> hi (in place) + lo =====
+    const int ct = threadIdx.x - 64;  // 0..127
+    int s = 0;
+    uint32_t ph = 0;
+    for (int kb = kb0; kb < kb1; ++kb) {
+      mbar_wait(&full[s], ph);
+      float4* a = reinterpret_cast<float4*>(smem + s * STAGE);
+      float4* al = reinterpret_cast<float4*>(smem + s * STAGE + kABytes);
+#pragma unroll
+      for (int i = 0; i < kABytes / 16 / 128; ++i) {
+        const int q = ct + 128 * i;
+        float4 v = a[q], h, l;
+        split_tf32(v.x, h.x, l.x);
+        split_tf32(v.y, h.y, l.y);
+        split_tf32(v.z, h.z, l.z);
+        split_tf32(v.w, h.w, l.w);
+        a[q] = h;
+        al[q] = l;
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&conv[s]);
+      if (++s == STAGES) { s = 0; ph ^= 1; }
     }
   } else {
-    // ===== converters (warps 2..5), then epilogue =====
-    const int ct = threadIdx.x - 64;  // 0..127
-    {
-      int s = 0;
-      uint32_t ph = 0;
-      for (int kb = kb0; kb < kb1; ++kb) {
-        mbar_wait(&full[s], ph);
-        float4* a = reinterpret_cast<float4*>(smem + s * STAGE);
-        float4* al = reinterpret_cast<float4*>(smem + s * STAGE + kABytes);
-#pragma unroll
-        for (int i = 0; i < kABytes / 16 / 128; ++i) {
-          const int q = ct + 128 * i;
-          float4 v = a[q], h, l;
-          split_tf32(v.x, h.x, l.x);
-          split_tf32(v.y, h.y, l.y);
-          split_tf32(v.z, h.z, l.z);
-          split_tf32(v.w, h.w, l.w);
-          a[q] = h;
-          al[q] = l;
-        }
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&conv[s]);
-        if (++s == STAGES) { s = 0; ph ^= 1; }
-      }
-    }
-    // epilogue
-    mbar_wait(tfull, 0);
-    tc_fence_after();
+    // ===== promoters + epilogue (warps 6..9; warp w owns TMEM lanes 32*(w%4) .. +31) =====
     const int quarter = warp & 3;
+    const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+    float acc[BN];
+#pragma unroll
+    for (int i = 0; i < BN; ++i) acc[i] = 0.f;
+    for (int grp = 0; grp < ngroups; ++grp) {
+      const int t = grp & 1;
+      mbar_wait(&mfull[t], (uint32_t)(grp >> 1) & 1u);
+      tc_fence_after();
+#pragma unroll
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        float v[32];
+        tmem_ld32(tmem + lane_base + (uint32_t)(t * BN + c0), v);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) acc[c0 + i] += v[i];
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&mempty[t]);
+    }
+    // the last group's commit covers every MMA, including the cross-term accumulator
     const int r = quarter * 32 + lane;  // tile row = TMEM lane
     const int ly = r / g.TW, lx = r - ly * g.TW;
     const int oy = tc.ty * g.TH + ly, ox = tc.tx * g.TW + lx;
     const bool valid = (r < rows) && (oy < g.Hc) && (ox < g.Wc);
-#pragma unroll 1
+#pragma unroll
     for (int c0 = 0; c0 < BN; c0 += 32) {
       float v[32];
-      tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c0, v);
+      tmem_ld32(tmem_x + lane_base + (uint32_t)c0, v);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] += acc[c0 + i];
       if (valid) {
         if (g.nsplit > 1)
           epi.store_partial(split, tc.b, tc.cls, oy, ox, n0 + c0, v);
