@@ -4,7 +4,8 @@
 // Operator (PAPER.md:91-93 eq:DORTE_2d with the upwind stencil of DESIGN.md R9):
 //   (A psi)_{jim} = (|c_m|/h + |s_m|/h + sigma_t) psi_{jim} - (|c_m|/h) psi_{j,i-sgn c_m,m}
 //                   - (|s_m|/h) psi_{j-sgn s_m,i,m} - sigma_s sum_n S_mn psi_{jin}
-// Layout psi[b][j][i][m]; the scattering term is the GEMM  Psi[cells x M] . S^T[M x M].
+// Layout psi[b][j][i][m]; the scattering term is the GEMM  Psi[cells x M] . S^T[M x M], computed
+// in the conservation-preserving form S psi = c + S (psi - c), c = psi_{cell, m=0} (apply_tc.cu).
 #include "common.h"
 
 namespace rte {
@@ -62,12 +63,13 @@ __global__ void __launch_bounds__(256) apply_simt_kernel(
     for (int c = 0; c < 4; ++c) acc[a][c] = T(0);
 
   for (int k0 = 0; k0 < M; k0 += KC) {
-    // A chunk: TP cells x KC ordinates (x[cell][k0..k0+15]) -> As[k][cell]
+    // A chunk: TP cells x KC ordinates (x[cell][k0..k0+15] - c_cell) -> As[k][cell]; the
+    // contraction is S psi = c + S (psi - c) with c = psi at ordinate 0 (S row-stochastic, R5)
     for (int e = tid; e < TP * KC; e += 256) {
       int cl = e / KC, kk = e % KC;
       int64_t cell = c0 + cl;
       T v = T(0);
-      if (cell < cells && k0 + kk < M) v = xs[cell * M + k0 + kk];
+      if (cell < cells && k0 + kk < M) v = xs[cell * M + k0 + kk] - xs[cell * M];
       As[kk][cl] = v;
     }
     // B chunk: St[k0+kk][m0 + o]
@@ -101,13 +103,14 @@ __global__ void __launch_bounds__(256) apply_simt_kernel(
     int i = (int)(cell % N), j = (int)(cell / N);
     int64_t gcell = (int64_t)bsample * cells + cell;
     T st = sig_t[gcell], ss = sig_s[gcell];
+    const T cc = xs[cell * M];
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       int m = m0 + tx * 4 + c;
       if (m >= M) continue;
       T ax = axv[m], ay = ayv[m];
       T psi = xs[cell * M + m];
-      T v = (ax + ay + st) * psi - ss * acc[a][c];
+      T v = (ax + ay + st) * psi - ss * (cc + acc[a][c]);
       int ii = i - sgx[m], jj = j - sgy[m];
       if (ii >= 0 && ii < N) v -= ax * xs[(cell - sgx[m]) * M + m];
       if (jj >= 0 && jj < N) v -= ay * xs[(cell - (int64_t)sgy[m] * N) * M + m];

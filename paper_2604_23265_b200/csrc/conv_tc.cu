@@ -111,6 +111,7 @@ void ensure_smem(const void* kernel, int bytes) {
 
 // ---- conv epilogue -------------------------------------------------------------------------
 struct EpiConv {
+  static constexpr bool kCenter = false;
   float* out;
   const float* addend;
   const double* alpha;
@@ -128,7 +129,7 @@ struct EpiConv {
     }
     return (((long long)b * Ho + Y) * Wo + X) * Co + col;
   }
-  __device__ __forceinline__ void store(int b, int cls, int oy, int ox, int col, const float (&v)[32]) const {
+  __device__ __forceinline__ void store(int b, int cls, int oy, int ox, int col, const float (&v)[32], float) const {
     const long long o = index(b, cls, oy, ox, col);
     const float al = alpha ? (float)alpha[(long long)b * alpha_stride] : 1.f;
     const float s_in = sign * (a_in ? al : 1.f);
@@ -224,13 +225,30 @@ Plan make_plan(const ConvDesc& d) {
   P.mtiles = d.B * g.classes * g.tiles_y * g.tiles_x;
   P.ntiles = d.Co / BN;
   g.ntiles = P.ntiles;
-  const int ctas = P.mtiles * P.ntiles;
-  const int target = num_sms();
-  int nsplit = 1;
-  if (ctas < target) nsplit = std::min((target + ctas - 1) / ctas, std::max(1, g.kb_total / 4));
-  g.kb_per_split = (g.kb_total + nsplit - 1) / nsplit;
-  g.nsplit = (g.kb_total + g.kb_per_split - 1) / g.kb_per_split;
+  g.mtiles = P.mtiles;
+  g.bn = BN;
   P.out_elems = (long long)d.B * d.Ho * d.Wo * d.Co;
+  // split-K from a wave model of the persistent kernel: time = ceil(units / SMs) * (k blocks per
+  // unit * t_kb + t_unit) + (split-K reduction: (nsplit + 2) output-sized streams at ~6 TB/s)
+  const int sms = num_sms();
+  const double t_kb = std::max(12.0 * BN / 2.0, 700.0) / 1.9e3;  // us per K block (MMA vs convert)
+  const double t_unit = 0.5;
+  const double out_us = 4.0 * (double)P.out_elems / 6.0e6;
+  double best = 1e300;
+  int best_kps = g.kb_total;
+  for (int ns = 1; ns <= std::max(1, std::min(64, g.kb_total / 2)); ++ns) {
+    const int kps = (g.kb_total + ns - 1) / ns;
+    const int nsr = (g.kb_total + kps - 1) / kps;
+    const long long units = (long long)P.mtiles * P.ntiles * nsr;
+    const double waves = (double)((units + sms - 1) / sms);
+    const double t = waves * (kps * t_kb + t_unit) + (nsr > 1 ? (nsr + 2) * out_us + 3.0 : 0.0);
+    if (t < best * 0.97) {
+      best = t;
+      best_kps = kps;
+    }
+  }
+  g.kb_per_split = best_kps;
+  g.nsplit = (g.kb_total + best_kps - 1) / best_kps;
   P.ok = true;
   return P;
 }
@@ -241,7 +259,8 @@ void launch_bn(const Plan& P, const CUtensorMap& ta, const CUtensorMap& tbh, con
   auto kern = tc::gemm3xtf32_kernel<BN, tc::EpiConv>;
   constexpr int smem = tc::gemm_smem_bytes<BN>();
   tc::ensure_smem((const void*)kern, smem);
-  dim3 grid(P.mtiles * P.ntiles, 1, P.g.nsplit);
+  const long long units = (long long)P.mtiles * P.ntiles * P.g.nsplit;
+  const int grid = (int)std::min<long long>(units, num_sms());
   kern<<<grid, tc::kGemmThreads, smem, st>>>(ta, tbh, tbl, P.g, epi);
 }
 

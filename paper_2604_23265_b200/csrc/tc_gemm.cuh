@@ -45,7 +45,9 @@ struct Geom {
   int nsplit;
   int b_rows_class; // B-operand row offset per class (mode 2)
   int b_rows_batch; // B-operand row offset per batch sample (per-sample operators)
-  int ntiles;       // N tiles; blockIdx.x = m_tile * ntiles + n_tile (N fastest: A tile reuse in L2)
+  int ntiles;       // N tiles
+  int mtiles;       // M tiles (B * classes * tiles_y * tiles_x)
+  int bn;           // N tile (the kernel's BN)
 };
 
 template <int BN>
@@ -61,7 +63,7 @@ constexpr int gemm_stages() {
 
 template <int BN>
 constexpr int gemm_smem_bytes() {
-  return gemm_stages<BN>() * Smem<BN>::kStage + 1024 /*align*/ + 512 /*barriers*/;
+  return gemm_stages<BN>() * Smem<BN>::kStage + 1024 /*align*/ + 512 /*barriers*/ + 1024 /*row centres*/;
 }
 
 struct TileCoord {
@@ -77,6 +79,27 @@ __device__ __forceinline__ TileCoord decode_tile(const Geom& g, int t) {
   c.cls = t % g.classes;
   c.b = t / g.classes;
   return c;
+}
+
+// Persistent schedule: CTA c processes work units u = c, c + gridDim.x, ...; a unit is
+// (split, m tile, n tile) with the N tile fastest (consecutive units share their A tile in L2) and
+// the split slowest (concurrent units share their K range of the weights).
+struct Unit {
+  TileCoord tc;
+  int n0, split, kb0, kb1;
+};
+
+__device__ __forceinline__ Unit decode_unit(const Geom& g, int u) {
+  Unit w;
+  const int nt = u % g.ntiles;
+  u /= g.ntiles;
+  const int mt = u % g.mtiles;
+  w.split = u / g.mtiles;
+  w.tc = decode_tile(g, mt);
+  w.n0 = nt * g.bn;
+  w.kb0 = w.split * g.kb_per_split;
+  w.kb1 = min(g.kb_total, w.kb0 + g.kb_per_split);
+  return w;
 }
 
 // A-window origin (x, y) in the input tensor for K block kb of tile c.
@@ -96,8 +119,9 @@ __device__ __forceinline__ void a_origin(const Geom& g, const TileCoord& c, int 
   }
 }
 
-// Epilogue interface:  epi.store(b, cls, oy, ox, col, v[32]) for every valid output pixel
-// (oy, ox) of the class grid, columns col .. col+31;  epi.store_partial(split, b, cls, oy, ox,
+// Epilogue interface:  epi.store(b, cls, oy, ox, col, v[32], c_row) for every valid output pixel
+// (oy, ox) of the class grid, columns col .. col+31 (c_row = the row centre when Epi::kCenter: the
+// GEMM then computed (a - c_row 1) . B^T);  epi.store_partial(split, b, cls, oy, ox,
 // col, v) when split-K is active (nsplit > 1).
 //
 // Accumulation precision.  The tensor core's fp32 accumulation does not round to nearest (a
@@ -116,25 +140,24 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   constexpr int STAGES = gemm_stages<BN>();
   constexpr int BBYTES = Smem<BN>::kBBytes;
   constexpr int STAGE = Smem<BN>::kStage;
-  constexpr uint32_t TMEM_COLS = BN == 32 ? 128 : (BN == 64 ? 256 : 512);  // >= 3*BN, power of 2
+  // TMEM: main accumulator buffers M0, M1 at columns [0, 2BN), cross-term buffers X0, X1 at [2BN, 4BN)
+  constexpr uint32_t TMEM_COLS = BN == 32 ? 128 : (BN == 64 ? 256 : 512);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE);
-  uint64_t* full = bars;
-  uint64_t* conv = bars + STAGES;
-  uint64_t* empty = bars + 2 * STAGES;
-  uint64_t* mfull = bars + 3 * STAGES;       // [2]
-  uint64_t* mempty = bars + 3 * STAGES + 2;  // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 4);
+  uint64_t* full = bars;                       // [STAGES] TMA bytes landed
+  uint64_t* conv = bars + STAGES;              // [STAGES] hi/lo written (4 converter warps)
+  uint64_t* empty = bars + 2 * STAGES;         // [STAGES] MMAs done with the stage
+  uint64_t* mfull = bars + 3 * STAGES;         // [2] main buffer ready for promotion
+  uint64_t* mempty = bars + 3 * STAGES + 2;    // [2] main buffer drained (4 promoter warps)
+  uint64_t* xempty = bars + 3 * STAGES + 4;    // [2] cross buffer drained by the epilogue
+  uint64_t* cfull = bars + 3 * STAGES + 6;     // [2] row centres written (128 converter threads)
+  uint64_t* cempty = bars + 3 * STAGES + 8;    // [2] row centres read (128 epilogue threads)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 10);
+  float* cvec = reinterpret_cast<float*>(smem + STAGES * STAGE + 512);  // [2][128] row centres
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const TileCoord tc = decode_tile(g, blockIdx.x / g.ntiles);
-  const int n0 = (blockIdx.x % g.ntiles) * BN;
-  const int split = blockIdx.z;
-  const int kb0 = split * g.kb_per_split;
-  const int kb1 = min(g.kb_total, kb0 + g.kb_per_split);
-  const int nkb = kb1 - kb0;
-  const int ngroups = (nkb + kPromoteKB - 1) / kPromoteKB;
+  const int units = g.mtiles * g.ntiles * g.nsplit;
   const int rows = g.TW * g.TH;
   const uint32_t a_bytes = (uint32_t)rows * 128u;
 
@@ -147,6 +170,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     for (int t = 0; t < 2; ++t) {
       mbar_init(&mfull[t], 1);
       mbar_init(&mempty[t], 4);
+      mbar_init(&xempty[t], 4);
+      mbar_init(&cfull[t], 128);
+      mbar_init(&cempty[t], 128);
     }
     fence_barrier_init();
   }
@@ -160,27 +186,29 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tmem_x = tmem + 2 * BN;  // cross-term accumulator columns
 
   if (warp == 0) {
     // ===== TMA producer =====
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
-      const int brow = n0 + tc.cls * g.b_rows_class + tc.b * g.b_rows_batch;
-      for (int kb = kb0; kb < kb1; ++kb) {
-        mbar_wait(&empty[s], ph ^ 1);
-        uint8_t* sa = smem + s * STAGE;
-        uint8_t* sbh = sa + 2 * kABytes;
-        uint8_t* sbl = sbh + BBYTES;
-        const int tap = kb / g.cchunks, ci0 = (kb % g.cchunks) * 32;
-        int xA, yA;
-        a_origin(g, tc, tap, xA, yA);
-        mbar_arrive_expect_tx(&full[s], a_bytes + 2u * BBYTES);
-        tma_load_4d(sa, &tmA, &full[s], ci0, xA, yA, tc.b);
-        tma_load_2d(sbh, &tmBhi, &full[s], kb * 32, brow);
-        tma_load_2d(sbl, &tmBlo, &full[s], kb * 32, brow);
-        if (++s == STAGES) { s = 0; ph ^= 1; }
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const Unit w = decode_unit(g, u);
+        const int brow = w.n0 + w.tc.cls * g.b_rows_class + w.tc.b * g.b_rows_batch;
+        for (int kb = w.kb0; kb < w.kb1; ++kb) {
+          mbar_wait(&empty[s], ph ^ 1);
+          uint8_t* sa = smem + s * STAGE;
+          uint8_t* sbh = sa + 2 * kABytes;
+          uint8_t* sbl = sbh + BBYTES;
+          const int tap = kb / g.cchunks, ci0 = (kb % g.cchunks) * 32;
+          int xA, yA;
+          a_origin(g, w.tc, tap, xA, yA);
+          mbar_arrive_expect_tx(&full[s], a_bytes + 2u * BBYTES);
+          tma_load_4d(sa, &tmA, &full[s], ci0, xA, yA, w.tc.b);
+          tma_load_2d(sbh, &tmBhi, &full[s], kb * 32, brow);
+          tma_load_2d(sbl, &tmBlo, &full[s], kb * 32, brow);
+          if (++s == STAGES) { s = 0; ph ^= 1; }
+        }
       }
     }
   } else if (warp == 1) {
@@ -189,100 +217,150 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       constexpr uint32_t idesc = idesc_tf32(kTileM, BN);
       int s = 0;
       uint32_t ph = 0;
-      uint32_t acc_x = 0;
-      for (int grp = 0; grp < ngroups; ++grp) {
-        const int t = grp & 1;
-        const uint32_t use = (uint32_t)(grp >> 1);
-        mbar_wait(&mempty[t], (use & 1u) ^ 1u);
+      int gcount = 0;  // main-buffer groups issued so far (all units)
+      int li = 0;      // local unit index
+      for (int u = blockIdx.x; u < units; u += gridDim.x, ++li) {
+        const Unit w = decode_unit(g, u);
+        const int xt = li & 1;
+        mbar_wait(&xempty[xt], ((uint32_t)(li >> 1) & 1u) ^ 1u);
         tc_fence_after();
-        const uint32_t tm = tmem + (uint32_t)(t * BN);
-        uint32_t acc_m = 0;
-        const int kbe = min(kb1, kb0 + (grp + 1) * kPromoteKB);
-        for (int kb = kb0 + grp * kPromoteKB; kb < kbe; ++kb) {
-          mbar_wait(&conv[s], ph);
+        const uint32_t tx = tmem + (uint32_t)(2 * BN + xt * BN);
+        uint32_t acc_x = 0;
+        for (int kbg = w.kb0; kbg < w.kb1; kbg += kPromoteKB, ++gcount) {
+          const int t = gcount & 1;
+          mbar_wait(&mempty[t], ((uint32_t)(gcount >> 1) & 1u) ^ 1u);
           tc_fence_after();
-          const uint32_t sa = smem_u32(smem + s * STAGE);
-          const uint32_t sal = sa + kABytes;
-          const uint32_t sbh = sa + 2 * kABytes;
-          const uint32_t sbl = sbh + BBYTES;
+          const uint32_t tm = tmem + (uint32_t)(t * BN);
+          uint32_t acc_m = 0;
+          const int kbe = min(w.kb1, kbg + kPromoteKB);
+          for (int kb = kbg; kb < kbe; ++kb) {
+            mbar_wait(&conv[s], ph);
+            tc_fence_after();
+            const uint32_t sa = smem_u32(smem + s * STAGE);
+            const uint32_t sal = sa + kABytes;
+            const uint32_t sbh = sa + 2 * kABytes;
+            const uint32_t sbl = sbh + BBYTES;
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const uint32_t o = 32u * k;
-            mma_tf32(tmem_x, sdesc_sw128(sal + o), sdesc_sw128(sbh + o), idesc, acc_x);
-            acc_x = 1;
-            mma_tf32(tmem_x, sdesc_sw128(sa + o), sdesc_sw128(sbl + o), idesc, 1);
-            mma_tf32(tm, sdesc_sw128(sa + o), sdesc_sw128(sbh + o), idesc, acc_m);
-            acc_m = 1;
+            for (int k = 0; k < 4; ++k) {
+              const uint32_t o = 32u * k;
+              mma_tf32(tx, sdesc_sw128(sal + o), sdesc_sw128(sbh + o), idesc, acc_x);
+              acc_x = 1;
+              mma_tf32(tx, sdesc_sw128(sa + o), sdesc_sw128(sbl + o), idesc, 1);
+              mma_tf32(tm, sdesc_sw128(sa + o), sdesc_sw128(sbh + o), idesc, acc_m);
+              acc_m = 1;
+            }
+            mma_commit(&empty[s]);
+            if (++s == STAGES) { s = 0; ph ^= 1; }
           }
-          mma_commit(&empty[s]);
-          if (++s == STAGES) { s = 0; ph ^= 1; }
+          mma_commit(&mfull[t]);
         }
-        mma_commit(&mfull[t]);
       }
     }
   } else if (warp < 6) {
-    // ===== converters (warps 2..5): A tile -> hi (in place) + lo =====
+    // ===== converters (warps 2..5): A tile -> [centre] -> hi (in place) + lo =====
     const int ct = threadIdx.x - 64;  // 0..127
     int s = 0;
     uint32_t ph = 0;
-    for (int kb = kb0; kb < kb1; ++kb) {
-      mbar_wait(&full[s], ph);
-      float4* a = reinterpret_cast<float4*>(smem + s * STAGE);
-      float4* al = reinterpret_cast<float4*>(smem + s * STAGE + kABytes);
+    int li = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++li) {
+      const Unit w = decode_unit(g, u);
+      float* cv = cvec + (li & 1) * 128;
+      for (int kb = w.kb0; kb < w.kb1; ++kb) {
+        mbar_wait(&full[s], ph);
+        float4* a = reinterpret_cast<float4*>(smem + s * STAGE);
+        float4* al = reinterpret_cast<float4*>(smem + s * STAGE + kABytes);
+        if constexpr (Epi::kCenter) {
+          // row centre c_r = the row's first element (K index 0 of the unit's first K block);
+          // the GEMM then runs on a - c_r (see EpiApply)
+          if (kb == w.kb0) {
+            mbar_wait(&cempty[li & 1], ((uint32_t)(li >> 1) & 1u) ^ 1u);
+            cv[ct] = reinterpret_cast<const float*>(a)[ct * 32 + ((ct & 7) << 2)];
+            named_bar_sync(1, 128);
+            mbar_arrive(&cfull[li & 1]);
+          }
+        }
 #pragma unroll
-      for (int i = 0; i < kABytes / 16 / 128; ++i) {
-        const int q = ct + 128 * i;
-        float4 v = a[q], h, l;
-        split_tf32(v.x, h.x, l.x);
-        split_tf32(v.y, h.y, l.y);
-        split_tf32(v.z, h.z, l.z);
-        split_tf32(v.w, h.w, l.w);
-        a[q] = h;
-        al[q] = l;
+        for (int i = 0; i < kABytes / 16 / 128; ++i) {
+          const int q = ct + 128 * i;
+          float4 v = a[q], h, l;
+          if constexpr (Epi::kCenter) {
+            const float c = cv[q >> 3];
+            v.x -= c;
+            v.y -= c;
+            v.z -= c;
+            v.w -= c;
+          }
+          split_tf32(v.x, h.x, l.x);
+          split_tf32(v.y, h.y, l.y);
+          split_tf32(v.z, h.z, l.z);
+          split_tf32(v.w, h.w, l.w);
+          a[q] = h;
+          al[q] = l;
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&conv[s]);
+        if (++s == STAGES) { s = 0; ph ^= 1; }
       }
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&conv[s]);
-      if (++s == STAGES) { s = 0; ph ^= 1; }
     }
   } else {
     // ===== promoters + epilogue (warps 6..9; warp w owns TMEM lanes 32*(w%4) .. +31) =====
     const int quarter = warp & 3;
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
-    float acc[BN];
+    const int r = quarter * 32 + lane;  // tile row = TMEM lane
+    int gcount = 0;
+    int li = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++li) {
+      const Unit w = decode_unit(g, u);
+      float acc[BN];
 #pragma unroll
-    for (int i = 0; i < BN; ++i) acc[i] = 0.f;
-    for (int grp = 0; grp < ngroups; ++grp) {
-      const int t = grp & 1;
-      mbar_wait(&mfull[t], (uint32_t)(grp >> 1) & 1u);
-      tc_fence_after();
+      for (int i = 0; i < BN; ++i) acc[i] = 0.f;
+      for (int kbg = w.kb0; kbg < w.kb1; kbg += kPromoteKB, ++gcount) {
+        const int t = gcount & 1;
+        mbar_wait(&mfull[t], (uint32_t)(gcount >> 1) & 1u);
+        tc_fence_after();
+#pragma unroll
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          float v[32];
+          tmem_ld32(tmem + lane_base + (uint32_t)(t * BN + c0), v);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) acc[c0 + i] += v[i];
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&mempty[t]);
+      }
+      // the unit's last group commit covers every MMA of the unit, including its X buffer
+      const int xt = li & 1;
 #pragma unroll
       for (int c0 = 0; c0 < BN; c0 += 32) {
         float v[32];
-        tmem_ld32(tmem + lane_base + (uint32_t)(t * BN + c0), v);
+        tmem_ld32(tmem + lane_base + (uint32_t)(2 * BN + xt * BN + c0), v);
 #pragma unroll
         for (int i = 0; i < 32; ++i) acc[c0 + i] += v[i];
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&mempty[t]);
-    }
-    // the last group's commit covers every MMA, including the cross-term accumulator
-    const int r = quarter * 32 + lane;  // tile row = TMEM lane
-    const int ly = r / g.TW, lx = r - ly * g.TW;
-    const int oy = tc.ty * g.TH + ly, ox = tc.tx * g.TW + lx;
-    const bool valid = (r < rows) && (oy < g.Hc) && (ox < g.Wc);
+      if (lane == 0) mbar_arrive(&xempty[xt]);
+      float crow = 0.f;
+      if constexpr (Epi::kCenter) {
+        mbar_wait(&cfull[xt], (uint32_t)(li >> 1) & 1u);
+        crow = cvec[xt * 128 + r];
+        mbar_arrive(&cempty[xt]);
+      }
+      const int ly = r / g.TW, lx = r - ly * g.TW;
+      const int oy = w.tc.ty * g.TH + ly, ox = w.tc.tx * g.TW + lx;
+      if ((r < rows) && (oy < g.Hc) && (ox < g.Wc)) {
 #pragma unroll
-    for (int c0 = 0; c0 < BN; c0 += 32) {
-      float v[32];
-      tmem_ld32(tmem_x + lane_base + (uint32_t)c0, v);
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          float v[32];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] += acc[c0 + i];
-      if (valid) {
-        if (g.nsplit > 1)
-          epi.store_partial(split, tc.b, tc.cls, oy, ox, n0 + c0, v);
-        else
-          epi.store(tc.b, tc.cls, oy, ox, n0 + c0, v);
+          for (int i = 0; i < 32; ++i) v[i] = acc[c0 + i];
+          if (g.nsplit > 1)
+            epi.store_partial(w.split, w.tc.b, w.tc.cls, oy, ox, w.n0 + c0, v);
+          else
+            epi.store(w.tc.b, w.tc.cls, oy, ox, w.n0 + c0, v, crow);
+        }
       }
     }
   }

@@ -4,7 +4,7 @@ cd "${GRAFT_REPO_ROOT:-/root/repo}"
 mkdir -p gpurun_out
 KREGEX="${1:-gemm3xtf32}"
 TESTS="${TESTS:-tests}"
-timeout 1500 python -m pytest $TESTS -m gpu -q -x -p no:cacheprovider --timeout 600 > gpurun_out/pytest_gpu.log 2>&1
+timeout 1500 python -m pytest $TESTS -m gpu -q ${PYX--x} -p no:cacheprovider --timeout 600 > gpurun_out/pytest_gpu.log 2>&1
 PT=$?
 echo "pytest exit $PT" >> gpurun_out/pytest_gpu.log
 tail -3 gpurun_out/pytest_gpu.log
