@@ -136,7 +136,8 @@ typedef struct {
   int maxit;         /* cap on total inner iterations per sample */
   double rtol;       /* stop when ||b - A x|| <= rtol ||b|| */
   int precond;       /* 0 none, 1 MgNet (I + V) */
-  int reorth;        /* 0 = CGS2: two Gram-Schmidt passes (default); 1 = one CGS pass */
+  int reorth;        /* 0 = CGS2: two classical Gram-Schmidt passes (default); 1 = one CGS pass;
+                        2 = selective (DGKS): the second pass runs only when ||v'|| < ||w||/sqrt(2) */
 } gmres_opts;
 
 typedef struct {

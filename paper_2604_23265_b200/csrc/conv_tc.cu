@@ -100,6 +100,14 @@ void split_host(const std::vector<float>& w, std::vector<float>& hi, std::vector
   }
 }
 
+int tc_debug_flags() {
+  static int v = [] {
+    const char* e = getenv("RTE_TC_DBG");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
 void ensure_smem(const void* kernel, int bytes) {
   static std::mutex mu;
   static std::set<const void*> done;
@@ -227,6 +235,7 @@ Plan make_plan(const ConvDesc& d) {
   g.ntiles = P.ntiles;
   g.mtiles = P.mtiles;
   g.bn = BN;
+  g.dbg = tc_debug_flags();
   P.out_elems = (long long)d.B * d.Ho * d.Wo * d.Co;
   // split-K from a wave model of the persistent kernel: time = ceil(units / SMs) * (k blocks per
   // unit * t_kb + t_unit) + (split-K reduction: (nsplit + 2) output-sized streams at ~6 TB/s)

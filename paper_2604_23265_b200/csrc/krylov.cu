@@ -84,10 +84,14 @@ template <int NV, bool UPDATE, bool DOTS>
 __global__ void __launch_bounds__(kThreads, 1) cgs_kernel(
     const float* __restrict__ V, int64_t vld, const double* __restrict__ alpha, int alpha_ld,
     const double* __restrict__ hin, int hin_ld, const float* src, float* dst, int64_t ns,
-    const int* __restrict__ active, RedArgs ra) {
+    const int* __restrict__ active, RedArgs ra, const double* __restrict__ sel_w2,
+    const double* __restrict__ sel_v2) {
   constexpr int NQ = (DOTS ? NV : 0) + 1;
   const int b = blockIdx.y;
   if (active && !active[b]) return;
+  // selective re-orthogonalisation (DGKS, "twice is enough"): this second pass runs only when
+  // ||v'||^2 < ||w||^2 / 2 (both from the previous passes); otherwise v' already is v_{j+1}
+  if (sel_w2 && !(sel_v2[(int64_t)b * hin_ld] < 0.5 * sel_w2[(int64_t)b * hin_ld])) return;
   __shared__ float coef[NV > 0 ? NV : 1];
   if (UPDATE) {
     for (int i = threadIdx.x; i < NV; i += blockDim.x)
@@ -199,7 +203,7 @@ __global__ void cycle_init_kernel(int B, const double* __restrict__ rnorm2, cons
 
 // Givens update of column j (per sample).  h1/h2: pass outputs ([.., j] dots, [j+1] = ||.||^2).
 __global__ void givens_kernel(int B, int j, int m, const double* __restrict__ h1, const double* __restrict__ h2,
-                              int h_ld, const double* __restrict__ nrm2, int nrm_ld, double* Hr, double* Hraw,
+                              int h_ld, const double* __restrict__ nrm2, int nrm_ld, int selective, double* Hr, double* Hraw,
                               int save_raw, double* cs, double* sn, double* g, double* alpha, int alpha_ld,
                               const double* __restrict__ bnorm, double rtol, int last, int* active, int* kcols,
                               Status* st) {
@@ -210,9 +214,17 @@ __global__ void givens_kernel(int B, int j, int m, const double* __restrict__ h1
     st[b].breakdown = 0;
     return;
   }
+  // selective mode: the re-orthogonalisation pass ran iff ||v'||^2 < ||w||^2 / 2 (h1[j+1] = ||w||^2,
+  // h2[j+1] = ||v'||^2); without it the column is h1 and h_{j+1,j} = ||v'||
+  bool use_h2 = h2 != nullptr;
+  const double* nr = nrm2 + (int64_t)b * nrm_ld;
+  if (selective) {
+    use_h2 = h2[(int64_t)b * h_ld + j + 1] < 0.5 * h1[(int64_t)b * h_ld + j + 1];
+    if (!use_h2) nr = h2 + (int64_t)b * h_ld + j + 1;
+  }
   double col[kMaxRestart + 1];
-  for (int i = 0; i <= j; ++i) col[i] = h1[(int64_t)b * h_ld + i] + (h2 ? h2[(int64_t)b * h_ld + i] : 0.0);
-  double hj1 = sqrt(fmax(nrm2[(int64_t)b * nrm_ld], 0.0));
+  for (int i = 0; i <= j; ++i) col[i] = h1[(int64_t)b * h_ld + i] + (use_h2 ? h2[(int64_t)b * h_ld + i] : 0.0);
+  double hj1 = sqrt(fmax(*nr, 0.0));
   const int ldh = m;  // H stored [B][m+1][m]
   double* Hb = Hr + (int64_t)b * (m + 1) * m;
   if (save_raw) {
@@ -296,7 +308,8 @@ struct GmresWork {
 };
 
 static void launch_cgs(const GmresWork& W, int nv, bool update, bool dots, const double* hin, const float* src,
-                       float* dst, double* out, cudaStream_t st) {
+                       float* dst, double* out, cudaStream_t st, const double* sel_w2 = nullptr,
+                       const double* sel_v2 = nullptr) {
   RedArgs ra{W.partials, W.counters, out, kMaxRestart + 2, W.nblk};
   dim3 grid(W.nblk, W.B);
   const int64_t vld = W.ns * W.B;
@@ -306,7 +319,7 @@ static void launch_cgs(const GmresWork& W, int nv, bool update, bool dots, const
     constexpr bool UP = decltype(up_tag)::value;
     constexpr bool DT = decltype(dot_tag)::value;
     cgs_kernel<NV, UP, DT><<<grid, kThreads, 0, st>>>(W.V, vld, W.alpha, W.m + 1, hin, kMaxRestart + 2, src, dst,
-                                                      W.ns, W.active, ra);
+                                                      W.ns, W.active, ra, sel_w2, sel_v2);
   };
   using T = std::true_type;
   using F = std::false_type;
@@ -333,7 +346,10 @@ static void launch_cgs(const GmresWork& W, int nv, bool update, bool dots, const
   const double ne = (double)W.ns * W.B;
   const double bytes = 4.0 * ne * (nv + 1 + (update ? 1 : 0));
   const double flops = ne * (2.0 * nv * ((update ? 1 : 0) + (dots ? 1 : 0)) + 2.0);
-  after_launch(update ? (dots ? "cgs_update_dots" : "cgs_update") : "cgs_dots", st, flops, bytes, 0);
+  if (sel_w2)  // selective pass: whether it streamed is decided on the device, so no bytes are booked
+    after_launch("cgs_reorth_selective", st, 0.0, 0.0, 0);
+  else
+    after_launch(update ? (dots ? "cgs_update_dots" : "cgs_update") : "cgs_dots", st, flops, bytes, 0);
 }
 
 template <typename T>
@@ -418,7 +434,8 @@ extern "C" rte_status gmres_solve(const rte_problem* p, const mgnet_net* net, co
     const int B = p->B;
     const int64_t n = p->n;
     const int hld = kMaxRestart + 2;
-    const bool sel = opts->reorth == 1;
+    const int reorth = opts->reorth;  // 0 CGS2, 1 CGS1, 2 selective (DGKS)
+    RTE_REQUIRE(reorth >= 0 && reorth <= 2, "gmres_solve: reorth must be 0, 1 or 2");
     std::vector<int> total(B, 0), restarts(B, 0), brk(B, 0), conv(B, 0), done(B, 0);
     std::vector<double> est_last(B, 0.0), relres(B, 0.0);
     for (int b = 0; b < B; ++b) {
@@ -476,9 +493,12 @@ extern "C" rte_status gmres_solve(const rte_problem* p, const mgnet_net* net, co
         launch_cgs(W, j + 1, false, true, nullptr, W.w, nullptr, W.h1, st);      // pass A
         const double* h2 = nullptr;
         const double* nrm = nullptr;
-        if (!sel) {
+        if (reorth != 1) {
           launch_cgs(W, j + 1, true, true, W.h1, W.w, vnext, W.h2, st);          // pass B
-          launch_cgs(W, j + 1, true, false, W.h2, vnext, vnext, W.h3, st);       // pass C
+          if (reorth == 2)                                                        // pass C (selective)
+            launch_cgs(W, j + 1, true, false, W.h2, vnext, vnext, W.h3, st, W.h1 + (j + 1), W.h2 + (j + 1));
+          else
+            launch_cgs(W, j + 1, true, false, W.h2, vnext, vnext, W.h3, st);     // pass C
           h2 = W.h2;
           nrm = W.h3;  // update-only passes put ||.||^2 at index 0
         } else {
@@ -489,7 +509,7 @@ extern "C" rte_status gmres_solve(const rte_problem* p, const mgnet_net* net, co
         ++total_all;
         int last = (total_all >= opts->maxit) ? 1 : 0;
         prof_begin(st);
-      givens_kernel<<<(B + 63) / 64, 64, 0, st>>>(B, j, m, W.h1, h2, hld, nrm, hld, W.Hr, W.Hraw,
+        givens_kernel<<<(B + 63) / 64, 64, 0, st>>>(B, j, m, W.h1, h2, hld, nrm, hld, reorth == 2 ? 1 : 0, W.Hr, W.Hraw,
                                                     first_cycle ? 1 : 0, W.cs, W.sn, W.g, W.alpha, m + 1, W.bnorm,
                                                     opts->rtol, last, W.active, W.kcols, W.st_dev);
         after_launch("givens", st);

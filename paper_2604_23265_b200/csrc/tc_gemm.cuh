@@ -48,6 +48,8 @@ struct Geom {
   int ntiles;       // N tiles
   int mtiles;       // M tiles (B * classes * tiles_y * tiles_x)
   int bn;           // N tile (the kernel's BN)
+  int dbg;          // perf-experiment switches (RTE_TC_DBG; 0 in production): bit0 skip the hi/lo
+                    // conversion, bit1 skip the B-lo load and MMA, bit2 skip the cross-term MMAs
 };
 
 template <int BN>
@@ -203,10 +205,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           const int tap = kb / g.cchunks, ci0 = (kb % g.cchunks) * 32;
           int xA, yA;
           a_origin(g, w.tc, tap, xA, yA);
-          mbar_arrive_expect_tx(&full[s], a_bytes + 2u * BBYTES);
+          const bool no_blo = (g.dbg & 2) != 0;
+          mbar_arrive_expect_tx(&full[s], a_bytes + (no_blo ? 1u : 2u) * BBYTES);
           tma_load_4d(sa, &tmA, &full[s], ci0, xA, yA, w.tc.b);
           tma_load_2d(sbh, &tmBhi, &full[s], kb * 32, brow);
-          tma_load_2d(sbl, &tmBlo, &full[s], kb * 32, brow);
+          if (!no_blo) tma_load_2d(sbl, &tmBlo, &full[s], kb * 32, brow);
           if (++s == STAGES) { s = 0; ph ^= 1; }
         }
       }
@@ -243,9 +246,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               const uint32_t o = 32u * k;
-              mma_tf32(tx, sdesc_sw128(sal + o), sdesc_sw128(sbh + o), idesc, acc_x);
+              if (!(g.dbg & 4)) {
+                mma_tf32(tx, sdesc_sw128(sal + o), sdesc_sw128(sbh + o), idesc, acc_x);
+                if (!(g.dbg & 2)) mma_tf32(tx, sdesc_sw128(sa + o), sdesc_sw128(sbl + o), idesc, 1);
+              } else if (!acc_x) {
+                mma_tf32(tx, sdesc_sw128(sal + o), sdesc_sw128(sbh + o), idesc, 0);
+              }
               acc_x = 1;
-              mma_tf32(tx, sdesc_sw128(sa + o), sdesc_sw128(sbl + o), idesc, 1);
               mma_tf32(tm, sdesc_sw128(sa + o), sdesc_sw128(sbh + o), idesc, acc_m);
               acc_m = 1;
             }
@@ -281,6 +288,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
 #pragma unroll
         for (int i = 0; i < kABytes / 16 / 128; ++i) {
+          if (g.dbg & 1) break;
           const int q = ct + 128 * i;
           float4 v = a[q], h, l;
           if constexpr (Epi::kCenter) {

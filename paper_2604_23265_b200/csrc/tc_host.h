@@ -21,6 +21,9 @@ CUtensorMap make_map_kmajor(const float* base, int K, int rows, int box_rows);
 float tf32_rna_host(float v);
 void split_host(const std::vector<float>& w, std::vector<float>& hi, std::vector<float>& lo);
 
+// RTE_TC_DBG perf-experiment switches (see Geom::dbg); 0 unless the variable is set.
+int tc_debug_flags();
+
 // Opt a kernel into `bytes` of dynamic shared memory (once per kernel pointer).
 void ensure_smem(const void* kernel, int bytes);
 
