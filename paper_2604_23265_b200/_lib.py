@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "librte_b200.so")
+LIB_PATH = os.environ.get("RTE_LIB_PATH") or os.path.join(HERE, "librte_b200.so")  # override: perf experiments
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2604_23265_b200.build` "

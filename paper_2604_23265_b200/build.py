@@ -44,16 +44,26 @@ def _compile(src: str, verbose: bool) -> str:
     return obj
 
 
-def build(verbose: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
-    with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
-        objs = list(ex.map(lambda s: _compile(s, verbose), SOURCES))
-    if not os.path.exists(OUT) or os.path.getmtime(OUT) < max(os.path.getmtime(o) for o in objs):
-        cmd = [NVCC] + ARCH + ["-shared", "-o", OUT] + objs + ["-lcuda", "-Xlinker", "--version-script=" + os.path.join(CSRC, "exports.map")]
+def build(verbose: bool = False, defines=(), out: str = OUT, objdir: str = BUILD) -> str:
+    """Compile and link; `defines` (e.g. ["RTE_TC_STAGES=2"]) and a different `out`/`objdir` are
+    for perf-experiment variants only."""
+    global FLAGS, BUILD
+    saved = (FLAGS, BUILD)
+    FLAGS = FLAGS + ["-D" + d for d in defines]
+    BUILD = objdir
+    try:
+        os.makedirs(BUILD, exist_ok=True)
+        with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
+            objs = list(ex.map(lambda s: _compile(s, verbose), SOURCES))
+    finally:
+        FLAGS, BUILD = saved
+    OUTP = out
+    if not os.path.exists(OUTP) or os.path.getmtime(OUTP) < max(os.path.getmtime(o) for o in objs):
+        cmd = [NVCC] + ARCH + ["-shared", "-o", OUTP] + objs + ["-lcuda", "-Xlinker", "--version-script=" + os.path.join(CSRC, "exports.map")]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}\n{r.stdout}")
-    return OUT
+    return OUTP
 
 
 if __name__ == "__main__":

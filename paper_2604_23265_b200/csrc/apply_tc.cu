@@ -105,7 +105,7 @@ void launch_apply_tc(const rte_problem* p, const float* x, float* y, const doubl
   const int mtiles = B * g.tiles_y * g.tiles_x;
   g.mtiles = mtiles;
   g.bn = BN;
-  g.dbg = tc_debug_flags();
+  g.dbg = tc::tc_debug_flags();
   CUtensorMap ta = tc::make_map_act(x, M, N, N, B, g.TW, g.TH, 1);
   CUtensorMap tbh = tc::make_map_kmajor(p->S_hi, M, B * M, BN);
   CUtensorMap tbl = tc::make_map_kmajor(p->S_lo, M, B * M, BN);

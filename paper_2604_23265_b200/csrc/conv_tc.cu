@@ -235,7 +235,7 @@ Plan make_plan(const ConvDesc& d) {
   g.ntiles = P.ntiles;
   g.mtiles = P.mtiles;
   g.bn = BN;
-  g.dbg = tc_debug_flags();
+  g.dbg = tc::tc_debug_flags();
   P.out_elems = (long long)d.B * d.Ho * d.Wo * d.Co;
   // split-K from a wave model of the persistent kernel: time = ceil(units / SMs) * (k blocks per
   // unit * t_kb + t_unit) + (split-K reduction: (nsplit + 2) output-sized streams at ~6 TB/s)

@@ -60,6 +60,9 @@ struct Smem {
 
 template <int BN>
 constexpr int gemm_stages() {
+#ifdef RTE_TC_STAGES
+  if ((2 * kABytes + 2 * BN * 128) * RTE_TC_STAGES <= 200 * 1024) return RTE_TC_STAGES;
+#endif
   return (2 * kABytes + 2 * BN * 128) * 4 <= 200 * 1024 ? 4 : ((2 * kABytes + 2 * BN * 128) * 3 <= 200 * 1024 ? 3 : 2);
 }
 
