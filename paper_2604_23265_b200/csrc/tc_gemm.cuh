@@ -49,7 +49,8 @@ struct Geom {
   int mtiles;       // M tiles (B * classes * tiles_y * tiles_x)
   int bn;           // N tile (the kernel's BN)
   int dbg;          // perf-experiment switches (RTE_TC_DBG; 0 in production): bit0 skip the hi/lo
-                    // conversion, bit1 skip the B-lo load and MMA, bit2 skip the cross-term MMAs
+                    // conversion, bit1 skip the B-lo load and MMA, bit2 skip the cross-term MMAs,
+                    // bit3 no MMAs at all, bit4 no TMA loads, bit5 no epilogue global traffic
 };
 
 template <int BN>
@@ -209,10 +210,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           int xA, yA;
           a_origin(g, w.tc, tap, xA, yA);
           const bool no_blo = (g.dbg & 2) != 0;
-          mbar_arrive_expect_tx(&full[s], a_bytes + (no_blo ? 1u : 2u) * BBYTES);
-          tma_load_4d(sa, &tmA, &full[s], ci0, xA, yA, w.tc.b);
-          tma_load_2d(sbh, &tmBhi, &full[s], kb * 32, brow);
-          if (!no_blo) tma_load_2d(sbl, &tmBlo, &full[s], kb * 32, brow);
+          if (g.dbg & 16) {
+            mbar_arrive(&full[s]);
+          } else {
+            mbar_arrive_expect_tx(&full[s], a_bytes + (no_blo ? 1u : 2u) * BBYTES);
+            tma_load_4d(sa, &tmA, &full[s], ci0, xA, yA, w.tc.b);
+            tma_load_2d(sbh, &tmBhi, &full[s], kb * 32, brow);
+            if (!no_blo) tma_load_2d(sbl, &tmBlo, &full[s], kb * 32, brow);
+          }
           if (++s == STAGES) { s = 0; ph ^= 1; }
         }
       }
@@ -248,6 +253,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             const uint32_t sbl = sbh + BBYTES;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
+              if (g.dbg & 8) break;
               const uint32_t o = 32u * k;
               if (!(g.dbg & 4)) {
                 mma_tf32(tx, sdesc_sw128(sal + o), sdesc_sw128(sbh + o), idesc, acc_x);
@@ -361,7 +367,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
       const int ly = r / g.TW, lx = r - ly * g.TW;
       const int oy = w.tc.ty * g.TH + ly, ox = w.tc.tx * g.TW + lx;
-      if ((r < rows) && (oy < g.Hc) && (ox < g.Wc)) {
+      if ((r < rows) && (oy < g.Hc) && (ox < g.Wc) && !(g.dbg & 32)) {
 #pragma unroll
         for (int c0 = 0; c0 < BN; c0 += 32) {
           float v[32];
