@@ -145,6 +145,25 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// Shared-memory vector access by 32-bit shared address (keeps the compiler off generic LD/ST).
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+
+// Fast 3xTF32 split for the A operand: hi = round-half-away of x to TF32 done on the bit pattern
+// (identical to cvt.rna.tf32.f32 for finite x), lo = x - hi exact in fp32 and NOT rounded again:
+// the tensor core reads lo's leading TF32 bits, so |x - hi - lo_read| <= 2^-21 |x|.
+__device__ __forceinline__ void split_tf32_fast(float x, float& hi, float& lo) {
+  hi = __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+  lo = x - hi;
+}
+
 // Round-to-nearest (ties away) to TF32, result in fp32 format with the low 13 bits zero.
 __device__ __forceinline__ float to_tf32(float x) {
   uint32_t r;

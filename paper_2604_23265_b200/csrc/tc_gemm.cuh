@@ -283,36 +283,39 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       float* cv = cvec + (li & 1) * 128;
       for (int kb = w.kb0; kb < w.kb1; ++kb) {
         mbar_wait(&full[s], ph);
-        float4* a = reinterpret_cast<float4*>(smem + s * STAGE);
-        float4* al = reinterpret_cast<float4*>(smem + s * STAGE + kABytes);
+        const uint32_t a_s = smem_u32(smem + s * STAGE);  // A tile (hi written in place)
+        const uint32_t al_s = a_s + kABytes;                // lo tile
         if constexpr (Epi::kCenter) {
           // row centre c_r = the row's first element (K index 0 of the unit's first K block);
           // the GEMM then runs on a - c_r (see EpiApply)
           if (kb == w.kb0) {
             mbar_wait(&cempty[li & 1], ((uint32_t)(li >> 1) & 1u) ^ 1u);
-            cv[ct] = reinterpret_cast<const float*>(a)[ct * 32 + ((ct & 7) << 2)];
+            cv[ct] = reinterpret_cast<const float*>(smem + s * STAGE)[ct * 32 + ((ct & 7) << 2)];
             named_bar_sync(1, 128);
             mbar_arrive(&cfull[li & 1]);
           }
         }
+        if (!(g.dbg & 1)) {
+          float4 v[kABytes / 16 / 128];
 #pragma unroll
-        for (int i = 0; i < kABytes / 16 / 128; ++i) {
-          if (g.dbg & 1) break;
-          const int q = ct + 128 * i;
-          float4 v = a[q], h, l;
-          if constexpr (Epi::kCenter) {
-            const float c = cv[q >> 3];
-            v.x -= c;
-            v.y -= c;
-            v.z -= c;
-            v.w -= c;
+          for (int i = 0; i < kABytes / 16 / 128; ++i) v[i] = lds128(a_s + 16u * (ct + 128 * i));
+#pragma unroll
+          for (int i = 0; i < kABytes / 16 / 128; ++i) {
+            float4 x = v[i], h, l;
+            if constexpr (Epi::kCenter) {
+              const float c = cv[(ct + 128 * i) >> 3];
+              x.x -= c;
+              x.y -= c;
+              x.z -= c;
+              x.w -= c;
+            }
+            split_tf32_fast(x.x, h.x, l.x);
+            split_tf32_fast(x.y, h.y, l.y);
+            split_tf32_fast(x.z, h.z, l.z);
+            split_tf32_fast(x.w, h.w, l.w);
+            sts128(a_s + 16u * (ct + 128 * i), h);
+            sts128(al_s + 16u * (ct + 128 * i), l);
           }
-          split_tf32(v.x, h.x, l.x);
-          split_tf32(v.y, h.y, l.y);
-          split_tf32(v.z, h.z, l.z);
-          split_tf32(v.w, h.w, l.w);
-          a[q] = h;
-          al[q] = l;
         }
         fence_proxy_async_smem();
         __syncwarp();
