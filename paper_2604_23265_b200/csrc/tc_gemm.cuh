@@ -138,6 +138,17 @@ __device__ __forceinline__ void a_origin(const Geom& g, const TileCoord& c, int 
 //   - the main product hi.hi accumulates for at most kPromoteKB K blocks in one of two TMEM
 //     buffers; four promoter warps then add the buffer into fp32 registers (round-to-nearest)
 //     while the MMA warp fills the other buffer (the "promotion" used by FP8 GEMMs).
+// dbg bit6: block 0 reports per-role cycles spent waiting (printf at exit; experiments only)
+__device__ __forceinline__ void tw_wait(uint64_t* bar, uint32_t par, bool on, long long& acc) {
+  if (!on) {
+    mbar_wait(bar, par);
+    return;
+  }
+  const long long t0 = clock64();
+  mbar_wait(bar, par);
+  acc += clock64() - t0;
+}
+
 template <int BN, class Epi>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm3xtf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBhi,
@@ -164,6 +175,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int units = g.mtiles * g.ntiles * g.nsplit;
+  const bool prof = (g.dbg & 64) && blockIdx.x == 0 && lane == 0;
+  long long w_a = 0, w_b = 0, w_c = 0;
+  const long long t_start = clock64();
+  int n_kb = 0;
   const int rows = g.TW * g.TH;
   const uint32_t a_bytes = (uint32_t)rows * 128u;
 
@@ -201,8 +216,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
         const Unit w = decode_unit(g, u);
         const int brow = w.n0 + w.tc.cls * g.b_rows_class + w.tc.b * g.b_rows_batch;
-        for (int kb = w.kb0; kb < w.kb1; ++kb) {
-          mbar_wait(&empty[s], ph ^ 1);
+        for (int kb = w.kb0; kb < w.kb1; ++kb, ++n_kb) {
+          tw_wait(&empty[s], ph ^ 1, prof, w_a);
           uint8_t* sa = smem + s * STAGE;
           uint8_t* sbh = sa + 2 * kABytes;
           uint8_t* sbl = sbh + BBYTES;
@@ -233,19 +248,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       for (int u = blockIdx.x; u < units; u += gridDim.x, ++li) {
         const Unit w = decode_unit(g, u);
         const int xt = li & 1;
-        mbar_wait(&xempty[xt], ((uint32_t)(li >> 1) & 1u) ^ 1u);
+        tw_wait(&xempty[xt], ((uint32_t)(li >> 1) & 1u) ^ 1u, prof, w_c);
         tc_fence_after();
         const uint32_t tx = tmem + (uint32_t)(2 * BN + xt * BN);
         uint32_t acc_x = 0;
         for (int kbg = w.kb0; kbg < w.kb1; kbg += kPromoteKB, ++gcount) {
           const int t = gcount & 1;
-          mbar_wait(&mempty[t], ((uint32_t)(gcount >> 1) & 1u) ^ 1u);
+          tw_wait(&mempty[t], ((uint32_t)(gcount >> 1) & 1u) ^ 1u, prof, w_b);
           tc_fence_after();
           const uint32_t tm = tmem + (uint32_t)(t * BN);
           uint32_t acc_m = 0;
           const int kbe = min(w.kb1, kbg + kPromoteKB);
-          for (int kb = kbg; kb < kbe; ++kb) {
-            mbar_wait(&conv[s], ph);
+          for (int kb = kbg; kb < kbe; ++kb, ++n_kb) {
+            tw_wait(&conv[s], ph, prof, w_a);
             tc_fence_after();
             const uint32_t sa = smem_u32(smem + s * STAGE);
             const uint32_t sal = sa + kABytes;
@@ -281,8 +296,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++li) {
       const Unit w = decode_unit(g, u);
       float* cv = cvec + (li & 1) * 128;
-      for (int kb = w.kb0; kb < w.kb1; ++kb) {
-        mbar_wait(&full[s], ph);
+      for (int kb = w.kb0; kb < w.kb1; ++kb, ++n_kb) {
+        tw_wait(&full[s], ph, prof, w_a);
         const uint32_t a_s = smem_u32(smem + s * STAGE);  // A tile (hi written in place)
         const uint32_t al_s = a_s + kABytes;                // lo tile
         if constexpr (Epi::kCenter) {
@@ -337,8 +352,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       for (int i = 0; i < BN; ++i) acc[i] = 0.f;
       for (int kbg = w.kb0; kbg < w.kb1; kbg += kPromoteKB, ++gcount) {
         const int t = gcount & 1;
-        mbar_wait(&mfull[t], (uint32_t)(gcount >> 1) & 1u);
+        tw_wait(&mfull[t], (uint32_t)(gcount >> 1) & 1u, prof, w_a);
         tc_fence_after();
+        const long long tl0 = prof ? clock64() : 0;
 #pragma unroll
         for (int c0 = 0; c0 < BN; c0 += 32) {
           float v[32];
@@ -346,6 +362,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
           for (int i = 0; i < 32; ++i) acc[c0 + i] += v[i];
         }
+        if (prof) w_b += clock64() - tl0;
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&mempty[t]);
@@ -384,6 +401,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
     }
   }
+  if (prof && (warp <= 2 || warp == 6))
+    printf("tcprof BN=%d units=%d grid=%d warp=%d kb=%d total=%lld waitA=%lld waitB=%lld waitC=%lld\n", BN, units,
+           gridDim.x, warp, n_kb, clock64() - t_start, w_a, w_b, w_c);
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {

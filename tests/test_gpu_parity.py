@@ -197,7 +197,7 @@ def test_mgnet_rejects_bad_weight_count():
 
 
 # ---------------------------------------------------------------------------------------
-def _gmres_pair(cfg, precond, rtol, maxit, std=0.02):
+def _gmres_pair(cfg, precond, rtol, maxit, std=0.02, reorth=0):
     import paper_2604_23265_b200 as P
     media = W.make_media(cfg)
     p = _gpu_problem(cfg, media)
@@ -211,16 +211,17 @@ def _gmres_pair(cfg, precond, rtol, maxit, std=0.02):
         w = W.make_weights(cfg, std=std)
         net = P.mgnet_create(p, cfg.L, cfg.C0, cfg.nu, w)
         onet = O.make_mgnet(w, cfg.M, cfg.L, cfg.C0, cfg.nu)
-    rep = P.gmres_solve(p, net, bd, x, restart=cfg.restart, maxit=maxit, rtol=rtol)
+    rep = P.gmres_solve(p, net, bd, x, restart=cfg.restart, maxit=maxit, rtol=rtol, reorth=reorth)
     ref = O.gmres(lambda v: O.apply(op, v), b32, P=(lambda v: O.vcycle(onet, v)) if precond else None,
                   restart=cfg.restart, rtol=rtol, maxit=maxit)
     return rep, x.cpu().numpy(), ref
 
 
-@pytest.mark.parametrize("precond", [False, True])
-def test_gmres_config1_converges_like_oracle(precond):
+@pytest.mark.parametrize("precond,reorth", [(False, 0), (True, 0), (False, 2), (True, 2), (True, 1)])
+def test_gmres_config1_converges_like_oracle(precond, reorth):
+    """reorth 0 = CGS2, 1 = CGS1, 2 = selective (DGKS); all equal MGS in exact arithmetic."""
     cfg = W.config(1)
-    rep, x, ref = _gmres_pair(cfg, precond, cfg.rtol, cfg.maxit)
+    rep, x, ref = _gmres_pair(cfg, precond, cfg.rtol, cfg.maxit, reorth=reorth)
     r = rep[0]
     assert ref.converged and r["converged"]
     assert abs(r["iterations"] - ref.iterations) <= 1
@@ -259,8 +260,8 @@ def test_gmres_small_batch_independent_solves():
             assert _rel(x[s], ref.x[0]) <= 1e-4
 
 
-@pytest.mark.parametrize("k,steps", [(3, 5), (2, 8)])
-def test_gmres_first_arnoldi_columns(k, steps):
+@pytest.mark.parametrize("k,steps,reorth", [(3, 5, 0), (2, 8, 0), (3, 5, 2), (2, 8, 2)])
+def test_gmres_first_arnoldi_columns(k, steps, reorth):
     """Non-converging protocol: the first Arnoldi columns (unrotated H) agree to 1e-5."""
     import paper_2604_23265_b200 as P
     cfg = W.config(k)
@@ -273,7 +274,8 @@ def test_gmres_first_arnoldi_columns(k, steps):
     bd = torch.empty(p.shape, dtype=torch.float32, device="cuda")
     P.rte_rhs(p, bd)
     x = torch.zeros(p.shape, dtype=torch.float64, device="cuda")
-    rep = P.gmres_solve(p, net, bd, x, restart=cfg.restart, maxit=steps, rtol=1e-30, hessenberg=True)
+    rep = P.gmres_solve(p, net, bd, x, restart=cfg.restart, maxit=steps, rtol=1e-30, hessenberg=True,
+                        reorth=reorth)
     H = rep[0]["hessenberg"][:steps + 1, :steps]
     Href = O.arnoldi_columns(lambda v: O.apply(op, v), bd.cpu().numpy().astype(np.float64),
                              lambda v: O.vcycle(onet, v), steps)
