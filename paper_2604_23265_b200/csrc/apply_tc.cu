@@ -4,7 +4,7 @@
 // the sigma_t diagonal in the epilogue (R9):
 //   y_{jim} = alpha [ (|c_m|/h + |s_m|/h + sigma_t) psi_{jim} - sigma_s (Psi S^T)_{jim}
 //                     - (|c_m|/h) psi_{j,i-sgn c_m,m} - (|s_m|/h) psi_{j-sgn s_m,i,m} ]
-// Each epilogue thread owns one cell (a TMEM lane) and 32 ordinates per TMEM load; psi at the cell
+// The epilogue runs warp-per-cell with lane = ordinate (coalesced 128-byte rows); psi at the cell
 // and at its two upwind neighbours is re-read from L2 (the A tiles just streamed through it).
 // Conservation-preserving contraction: because S is row-stochastic (R5),
 // S psi = c + S (psi - c) for any per-cell scalar c.  The GEMM runs on psi - c with c = psi at the
@@ -36,32 +36,18 @@ struct EpiApply {
   const double* alpha;
   int alpha_stride, N, M;
 
-  __device__ __forceinline__ void store(int b, int, int j, int i, int m0, const float (&v)[32], float c) const {
+  __device__ __forceinline__ void store1(int b, int, int j, int i, int m, float v, float c) const {
     const long long cell = ((long long)b * N + j) * N + i;
     const float st = sig_t[cell], ss = sig_s[cell];
     const float al = alpha ? (float)alpha[(long long)b * alpha_stride] : 1.f;
-    const float4* xc = reinterpret_cast<const float4*>(x + cell * M + m0);
-    float4* yo = reinterpret_cast<float4*>(y + cell * M + m0);
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      // the 4 ordinates of a float4 share a quadrant (M % 16 == 0), hence both upwind signs
-      const int m = m0 + 4 * q;
-      const int sx = sgx[m], sy = sgy[m];
-      const float4 a_x = *reinterpret_cast<const float4*>(ax + m);
-      const float4 a_y = *reinterpret_cast<const float4*>(ay + m);
-      const float4 p = xc[q];
-      float4 nx = make_float4(0.f, 0.f, 0.f, 0.f), ny = nx;
-      if ((unsigned)(i - sx) < (unsigned)N) nx = *reinterpret_cast<const float4*>(x + (cell - sx) * M + m);
-      if ((unsigned)(j - sy) < (unsigned)N) ny = *reinterpret_cast<const float4*>(x + (cell - (long long)sy * N) * M + m);
-      float4 r;
-      r.x = al * ((a_x.x + a_y.x + st) * p.x - ss * (c + v[4 * q + 0]) - a_x.x * nx.x - a_y.x * ny.x);
-      r.y = al * ((a_x.y + a_y.y + st) * p.y - ss * (c + v[4 * q + 1]) - a_x.y * nx.y - a_y.y * ny.y);
-      r.z = al * ((a_x.z + a_y.z + st) * p.z - ss * (c + v[4 * q + 2]) - a_x.z * nx.z - a_y.z * ny.z);
-      r.w = al * ((a_x.w + a_y.w + st) * p.w - ss * (c + v[4 * q + 3]) - a_x.w * nx.w - a_y.w * ny.w);
-      yo[q] = r;
-    }
+    const float a_x = ax[m], a_y = ay[m];
+    const int sx = sgx[m], sy = sgy[m];
+    float val = (a_x + a_y + st) * x[cell * M + m] - ss * (c + v);
+    if ((unsigned)(i - sx) < (unsigned)N) val -= a_x * x[(cell - sx) * M + m];
+    if ((unsigned)(j - sy) < (unsigned)N) val -= a_y * x[(cell - (long long)sy * N) * M + m];
+    y[cell * M + m] = val * al;
   }
-  __device__ __forceinline__ void store_partial(int, int, int, int, int, int, const float (&)[32]) const {}
+  __device__ __forceinline__ void store_partial1(int, int, int, int, int, int, float) const {}
 };
 
 template <int BN>

@@ -137,31 +137,15 @@ struct EpiConv {
     }
     return (((long long)b * Ho + Y) * Wo + X) * Co + col;
   }
-  __device__ __forceinline__ void store(int b, int cls, int oy, int ox, int col, const float (&v)[32], float) const {
+  __device__ __forceinline__ void store1(int b, int cls, int oy, int ox, int col, float v, float) const {
     const long long o = index(b, cls, oy, ox, col);
     const float al = alpha ? (float)alpha[(long long)b * alpha_stride] : 1.f;
-    const float s_in = sign * (a_in ? al : 1.f);
-    const float s_add = a_add ? al : 1.f;
-    float4* dst = reinterpret_cast<float4*>(out + o);
-    const float4* ad = reinterpret_cast<const float4*>(addend + o);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      float4 r = make_float4(s_in * v[4 * i], s_in * v[4 * i + 1], s_in * v[4 * i + 2], s_in * v[4 * i + 3]);
-      if (addend) {
-        const float4 a = ad[i];
-        r.x = fmaf(s_add, a.x, r.x);
-        r.y = fmaf(s_add, a.y, r.y);
-        r.z = fmaf(s_add, a.z, r.z);
-        r.w = fmaf(s_add, a.w, r.w);
-      }
-      dst[i] = r;
-    }
+    float r = sign * (a_in ? al : 1.f) * v;
+    if (addend) r = fmaf(a_add ? al : 1.f, addend[o], r);
+    out[o] = r;
   }
-  __device__ __forceinline__ void store_partial(int split, int b, int cls, int oy, int ox, int col,
-                                                const float (&v)[32]) const {
-    float4* dst = reinterpret_cast<float4*>(part + split * part_stride + index(b, cls, oy, ox, col));
-#pragma unroll
-    for (int i = 0; i < 8; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+  __device__ __forceinline__ void store_partial1(int split, int b, int cls, int oy, int ox, int col, float v) const {
+    part[split * part_stride + index(b, cls, oy, ox, col)] = v;
   }
 };
 

@@ -53,6 +53,9 @@ struct Geom {
                     // bit3 no MMAs at all, bit4 no TMA loads, bit5 no epilogue global traffic
 };
 
+constexpr int kEpiLd = 33;                      // padded row of the epilogue staging tile
+constexpr int kEpiBytes = kTileM * kEpiLd * 4;  // [128][33] fp32
+
 template <int BN>
 struct Smem {
   static constexpr int kBBytes = BN * 128;
@@ -69,7 +72,7 @@ constexpr int gemm_stages() {
 
 template <int BN>
 constexpr int gemm_smem_bytes() {
-  return gemm_stages<BN>() * Smem<BN>::kStage + 1024 /*align*/ + 512 /*barriers*/ + 1024 /*row centres*/;
+  return gemm_stages<BN>() * Smem<BN>::kStage + 1024 /*align*/ + 512 /*barriers*/ + 1024 /*row centres*/ + kEpiBytes;
 }
 
 struct TileCoord {
@@ -125,10 +128,10 @@ __device__ __forceinline__ void a_origin(const Geom& g, const TileCoord& c, int 
   }
 }
 
-// Epilogue interface:  epi.store(b, cls, oy, ox, col, v[32], c_row) for every valid output pixel
-// (oy, ox) of the class grid, columns col .. col+31 (c_row = the row centre when Epi::kCenter: the
-// GEMM then computed (a - c_row 1) . B^T);  epi.store_partial(split, b, cls, oy, ox,
-// col, v) when split-K is active (nsplit > 1).
+// Epilogue interface (one element per lane, lanes = 32 consecutive columns of one output row):
+// epi.store1(b, cls, oy, ox, col, value, c_row) for every valid output pixel (oy, ox) of the class
+// grid (c_row = the row centre when Epi::kCenter: the GEMM then computed (a - c_row 1) . B^T);
+// epi.store_partial1(split, b, cls, oy, ox, col, value) when split-K is active (nsplit > 1).
 //
 // Accumulation precision.  The tensor core's fp32 accumulation does not round to nearest (a
 // biased, truncating add), so a long K loop into one TMEM accumulator drifts by ~K/8 * 2^-24
@@ -172,6 +175,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* cempty = bars + 3 * STAGES + 8;    // [2] row centres read (128 epilogue threads)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 10);
   float* cvec = reinterpret_cast<float*>(smem + STAGES * STAGE + 512);  // [2][128] row centres
+  float* etile = reinterpret_cast<float*>(smem + STAGES * STAGE + 512 + 1024);  // [128][33] epilogue staging
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int units = g.mtiles * g.ntiles * g.nsplit;
@@ -379,26 +383,34 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&xempty[xt]);
-      float crow = 0.f;
-      if constexpr (Epi::kCenter) {
-        mbar_wait(&cfull[xt], (uint32_t)(li >> 1) & 1u);
-        crow = cvec[xt * 128 + r];
-        mbar_arrive(&cempty[xt]);
-      }
-      const int ly = r / g.TW, lx = r - ly * g.TW;
-      const int oy = w.tc.ty * g.TH + ly, ox = w.tc.tx * g.TW + lx;
-      if ((r < rows) && (oy < g.Hc) && (ox < g.Wc) && !(g.dbg & 32)) {
+      if constexpr (Epi::kCenter) mbar_wait(&cfull[xt], (uint32_t)(li >> 1) & 1u);
+      // Coalesced epilogue: each 32-column chunk of the accumulator is staged through a padded
+      // shared tile; then warp pw handles tile rows pw*32 .. +31 with lane = column, so every
+      // global load/store of a warp is one contiguous 128-byte line.
+      const int pw = warp - 6;
 #pragma unroll
-        for (int c0 = 0; c0 < BN; c0 += 32) {
-          float v[32];
+      for (int c0 = 0; c0 < BN; c0 += 32) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = acc[c0 + i];
-          if (g.nsplit > 1)
-            epi.store_partial(w.split, w.tc.b, w.tc.cls, oy, ox, w.n0 + c0, v);
-          else
-            epi.store(w.tc.b, w.tc.cls, oy, ox, w.n0 + c0, v, crow);
+        for (int i = 0; i < 32; ++i) etile[r * kEpiLd + i] = acc[c0 + i];
+        named_bar_sync(2, 128);
+        if (!(g.dbg & 32)) {
+          for (int i = 0; i < 32; ++i) {
+            const int rr = pw * 32 + i;
+            const int ly = rr / g.TW, lx = rr - ly * g.TW;
+            const int oy = w.tc.ty * g.TH + ly, ox = w.tc.tx * g.TW + lx;
+            if (rr < rows && oy < g.Hc && ox < g.Wc) {
+              const float val = etile[rr * kEpiLd + lane];
+              if (g.nsplit > 1)
+                epi.store_partial1(w.split, w.tc.b, w.tc.cls, oy, ox, w.n0 + c0 + lane, val);
+              else
+                epi.store1(w.tc.b, w.tc.cls, oy, ox, w.n0 + c0 + lane, val,
+                           Epi::kCenter ? cvec[xt * 128 + rr] : 0.f);
+            }
+          }
         }
+        named_bar_sync(2, 128);
       }
+      if constexpr (Epi::kCenter) mbar_arrive(&cempty[xt]);
     }
   }
   if (prof && (warp <= 2 || warp == 6))
