@@ -137,15 +137,23 @@ struct EpiConv {
     }
     return (((long long)b * Ho + Y) * Wo + X) * Co + col;
   }
-  __device__ __forceinline__ void store1(int b, int cls, int oy, int ox, int col, float v, float) const {
+  __device__ __forceinline__ void store4(int b, int cls, int oy, int ox, int col, float4 v, float) const {
     const long long o = index(b, cls, oy, ox, col);
     const float al = alpha ? (float)alpha[(long long)b * alpha_stride] : 1.f;
-    float r = sign * (a_in ? al : 1.f) * v;
-    if (addend) r = fmaf(a_add ? al : 1.f, addend[o], r);
-    out[o] = r;
+    const float si = sign * (a_in ? al : 1.f);
+    float4 r = make_float4(si * v.x, si * v.y, si * v.z, si * v.w);
+    if (addend) {
+      const float sa = a_add ? al : 1.f;
+      const float4 a = *reinterpret_cast<const float4*>(addend + o);
+      r.x = fmaf(sa, a.x, r.x);
+      r.y = fmaf(sa, a.y, r.y);
+      r.z = fmaf(sa, a.z, r.z);
+      r.w = fmaf(sa, a.w, r.w);
+    }
+    *reinterpret_cast<float4*>(out + o) = r;
   }
-  __device__ __forceinline__ void store_partial1(int split, int b, int cls, int oy, int ox, int col, float v) const {
-    part[split * part_stride + index(b, cls, oy, ox, col)] = v;
+  __device__ __forceinline__ void store_partial4(int split, int b, int cls, int oy, int ox, int col, float4 v) const {
+    *reinterpret_cast<float4*>(part + split * part_stride + index(b, cls, oy, ox, col)) = v;
   }
 };
 

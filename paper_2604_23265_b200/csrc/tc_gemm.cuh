@@ -10,9 +10,10 @@
 // hi = rna_tf32(a) (in place) and lo = rna_tf32(a - hi); the weights arrive pre-split; each
 // k-step issues lo.hi + hi.lo + hi.hi into the same TMEM accumulator.
 //
-// Warp roles (320 threads): warp 0 = TMA producer, warp 1 = TMEM allocator + MMA issuer (one
-// elected lane), warps 2..5 = A-operand hi/lo converters, warps 6..9 = accumulator promotion and
-// the epilogue (TMEM -> registers -> global; warp w owns TMEM lanes 32*(w%4) .. +31).  Pipelines:
+// Warp roles (384 threads = 3 warpgroups, registers rebalanced with setmaxnreg): warp 0 = TMA
+// producer, warp 1 = TMEM allocator + MMA issuer (one elected lane), warpgroup 1 = A-operand hi/lo
+// converters, warpgroup 2 = accumulator promotion and the epilogue (TMEM -> registers -> global;
+// warp w owns TMEM lanes 32*(w%4) .. +31).  Pipelines:
 // full[s] (TMA bytes landed) -> conv[s] (hi/lo written) -> empty[s] (MMAs done, tcgen05.commit);
 // mfull[t] / mempty[t] hand the two main-accumulator TMEM buffers between MMA and promoters.
 #pragma once
@@ -25,7 +26,7 @@
 namespace rte {
 namespace tc {
 
-constexpr int kGemmThreads = 320;   // 10 warps (see kernel)
+constexpr int kGemmThreads = 384;   // 3 warpgroups (see kernel)
 constexpr int kPromoteKB = 4;       // K blocks per TMEM accumulation group
 constexpr int kTileM = 128;
 constexpr int kABytes = kTileM * 128;   // 128 rows x 32 fp32
@@ -53,8 +54,7 @@ struct Geom {
                     // bit3 no MMAs at all, bit4 no TMA loads, bit5 no epilogue global traffic
 };
 
-constexpr int kEpiLd = 33;                      // padded row of the epilogue staging tile
-constexpr int kEpiBytes = kTileM * kEpiLd * 4;  // [128][33] fp32
+constexpr int kEpiBytes = 2 * kTileM * 128;    // 2 x [128 rows][32 fp32], float4 chunks swizzled by row & 7
 
 template <int BN>
 struct Smem {
@@ -128,10 +128,10 @@ __device__ __forceinline__ void a_origin(const Geom& g, const TileCoord& c, int 
   }
 }
 
-// Epilogue interface (one element per lane, lanes = 32 consecutive columns of one output row):
-// epi.store1(b, cls, oy, ox, col, value, c_row) for every valid output pixel (oy, ox) of the class
-// grid (c_row = the row centre when Epi::kCenter: the GEMM then computed (a - c_row 1) . B^T);
-// epi.store_partial1(split, b, cls, oy, ox, col, value) when split-K is active (nsplit > 1).
+// Epilogue interface (four consecutive columns per call): epi.store4(b, cls, oy, ox, col, v4,
+// c_row) for every valid output pixel (oy, ox) of the class grid, columns col .. col+3 (c_row = the
+// row centre when Epi::kCenter: the GEMM then computed (a - c_row 1) . B^T);
+// epi.store_partial4(split, b, cls, oy, ox, col, v4) when split-K is active (nsplit > 1).
 //
 // Accumulation precision.  The tensor core's fp32 accumulation does not round to nearest (a
 // biased, truncating add), so a long K loop into one TMEM accumulator drifts by ~K/8 * 2^-24
@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* cempty = bars + 3 * STAGES + 8;    // [2] row centres read (128 epilogue threads)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 10);
   float* cvec = reinterpret_cast<float*>(smem + STAGES * STAGE + 512);  // [2][128] row centres
-  float* etile = reinterpret_cast<float*>(smem + STAGES * STAGE + 512 + 1024);  // [128][33] epilogue staging
+  const uint32_t etile = smem_u32(smem + STAGES * STAGE + 512 + 1024);  // 2 x [128][32] epilogue staging
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int units = g.mtiles * g.ntiles * g.nsplit;
@@ -212,6 +212,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  // Register rebalancing per warpgroup (setmaxnreg at the top of each warpgroup's branch): the
+  // promoters hold BN fp32 accumulators per thread.
+  if (warp < 4) reg_dealloc<56>();
   if (warp == 0) {
     // ===== TMA producer =====
     if (lane == 0) {
@@ -291,9 +294,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
       }
     }
-  } else if (warp < 6) {
-    // ===== converters (warps 2..5): A tile -> [centre] -> hi (in place) + lo =====
-    const int ct = threadIdx.x - 64;  // 0..127
+  } else if (warp < 4) {
+    // warps 2, 3: no role
+  } else if (warp < 8) {
+    // ===== converters (warpgroup 1): A tile -> [centre] -> hi (in place) + lo =====
+    reg_dealloc<120>();
+    const int ct = threadIdx.x - 128;  // 0..127
     int s = 0;
     uint32_t ph = 0;
     int li = 0;
@@ -343,7 +349,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
     }
   } else {
-    // ===== promoters + epilogue (warps 6..9; warp w owns TMEM lanes 32*(w%4) .. +31) =====
+    // ===== promoters + epilogue (warpgroup 2; warp w owns TMEM lanes 32*(w%4) .. +31) =====
+    reg_alloc<232>();
     const int quarter = warp & 3;
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
     const int r = quarter * 32 + lane;  // tile row = TMEM lane
@@ -384,36 +391,42 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&xempty[xt]);
       if constexpr (Epi::kCenter) mbar_wait(&cfull[xt], (uint32_t)(li >> 1) & 1u);
-      // Coalesced epilogue: each 32-column chunk of the accumulator is staged through a padded
-      // shared tile; then warp pw handles tile rows pw*32 .. +31 with lane = column, so every
-      // global load/store of a warp is one contiguous 128-byte line.
-      const int pw = warp - 6;
+      // Coalesced epilogue: each 32-column chunk of the accumulator is staged through a shared tile
+      // (double-buffered, 16-byte chunks XOR-swizzled by row & 7: conflict-free both ways); then
+      // lane l of warp pw handles columns 4(l & 7) .. +3 of tile rows pw*32 + 4 it + (l >> 3), so
+      // each warp instruction moves four full 128-byte rows.
+      const int pw = warp - 8;
 #pragma unroll
       for (int c0 = 0; c0 < BN; c0 += 32) {
+        const uint32_t eb = etile + (uint32_t)(((c0 >> 5) & 1) * kTileM * 128);
 #pragma unroll
-        for (int i = 0; i < 32; ++i) etile[r * kEpiLd + i] = acc[c0 + i];
+        for (int k = 0; k < 8; ++k)
+          sts128(eb + (uint32_t)(r * 128 + ((k ^ (r & 7)) << 4)),
+                 make_float4(acc[c0 + 4 * k], acc[c0 + 4 * k + 1], acc[c0 + 4 * k + 2], acc[c0 + 4 * k + 3]));
         named_bar_sync(2, 128);
         if (!(g.dbg & 32)) {
-          for (int i = 0; i < 32; ++i) {
-            const int rr = pw * 32 + i;
+          const int k = lane & 7;
+#pragma unroll 2
+          for (int it = 0; it < 8; ++it) {
+            const int rr = pw * 32 + 4 * it + (lane >> 3);
             const int ly = rr / g.TW, lx = rr - ly * g.TW;
             const int oy = w.tc.ty * g.TH + ly, ox = w.tc.tx * g.TW + lx;
             if (rr < rows && oy < g.Hc && ox < g.Wc) {
-              const float val = etile[rr * kEpiLd + lane];
+              const float4 val = lds128(eb + (uint32_t)(rr * 128 + ((k ^ (rr & 7)) << 4)));
               if (g.nsplit > 1)
-                epi.store_partial1(w.split, w.tc.b, w.tc.cls, oy, ox, w.n0 + c0 + lane, val);
+                epi.store_partial4(w.split, w.tc.b, w.tc.cls, oy, ox, w.n0 + c0 + 4 * k, val);
               else
-                epi.store1(w.tc.b, w.tc.cls, oy, ox, w.n0 + c0 + lane, val,
+                epi.store4(w.tc.b, w.tc.cls, oy, ox, w.n0 + c0 + 4 * k, val,
                            Epi::kCenter ? cvec[xt * 128 + rr] : 0.f);
             }
           }
         }
-        named_bar_sync(2, 128);
       }
+      named_bar_sync(2, 128);  // staging buffers free before the next unit writes them
       if constexpr (Epi::kCenter) mbar_arrive(&cempty[xt]);
     }
   }
-  if (prof && (warp <= 2 || warp == 6))
+  if (prof && (warp <= 1 || warp == 4 || warp == 8))
     printf("tcprof BN=%d units=%d grid=%d warp=%d kb=%d total=%lld waitA=%lld waitB=%lld waitC=%lld\n", BN, units,
            gridDim.x, warp, n_kb, clock64() - t_start, w_a, w_b, w_c);
   tc_fence_before();
