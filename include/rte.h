@@ -128,8 +128,8 @@ rte_status mgnet_vcycle(const mgnet_net* net, const float* r_dev, float* z_dev,
 
 /* Restarted right-preconditioned GMRES(m) (R21, R22).
  * Preconditioner P = I + V (precond=1, requires net) or P = I (precond=0).
- * Iterate x is float64; the Krylov basis is float32; dot products accumulate in
- * float64; every restart recomputes r = b - A x in float64.  The batch's
+ * Iterate x is float64; the Krylov basis is float32 (precision=0) or float64 (precision=1); dot
+ * products accumulate in float64; every restart recomputes r = b - A x in float64.  The batch's
  * samples are independent solves with their own Arnoldi/Givens state. */
 typedef struct {
   int restart;       /* m, 1..64 */
@@ -138,6 +138,10 @@ typedef struct {
   int precond;       /* 0 none, 1 MgNet (I + V) */
   int reorth;        /* 0 = CGS2: two classical Gram-Schmidt passes (default); 1 = one CGS pass;
                         2 = selective (DGKS): the second pass runs only when ||v'|| < ||w||/sqrt(2) */
+  int precision;     /* 0 = mixed (default): float32 Krylov basis and operator apply, float64 iterate,
+                        reductions and restart residual;  1 = float64 basis and float64 apply (the
+                        fp32 V-cycle acts on a rounded copy and its correction is added in float64):
+                        ~2x the Arnoldi bytes, for tight tolerances and iteration-count parity */
 } gmres_opts;
 
 typedef struct {

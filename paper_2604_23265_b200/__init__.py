@@ -173,7 +173,7 @@ def mgnet_vcycle(net: MgNet, r, z, add_identity: bool = True, stream=None) -> No
 
 
 def gmres_solve(p: Problem, net: Optional[MgNet], b, x, *, restart: int = 30, maxit: int = 1000,
-                rtol: float = 1e-8, precond: Optional[int] = None, reorth: int = 0,
+                rtol: float = 1e-8, precond: Optional[int] = None, reorth: int = 0, precision: int = 0,
                 history: bool = True, hessenberg: bool = False, stream=None):
     """Restarted right-preconditioned GMRES; x (float64 CUDA tensor) holds x0 on entry, x on exit.
 
@@ -181,7 +181,7 @@ def gmres_solve(p: Problem, net: Optional[MgNet], b, x, *, restart: int = 30, ma
     relres_est, history [, hessenberg])."""
     if precond is None:
         precond = 1 if net is not None else 0
-    opts = gmres_opts(restart, maxit, rtol, precond, reorth)
+    opts = gmres_opts(restart, maxit, rtol, precond, reorth, precision)
     B = p.batch
     reps = (gmres_report * B)()
     hist = [np.zeros(max(maxit, 1)) for _ in range(B)]

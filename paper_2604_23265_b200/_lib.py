@@ -33,7 +33,7 @@ class rte_ordinates(C.Structure):
 
 class gmres_opts(C.Structure):
     _fields_ = [("restart", C.c_int), ("maxit", C.c_int), ("rtol", C.c_double),
-                ("precond", C.c_int), ("reorth", C.c_int)]
+                ("precond", C.c_int), ("reorth", C.c_int), ("precision", C.c_int)]
 
 
 class gmres_report(C.Structure):

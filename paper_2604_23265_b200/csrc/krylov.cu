@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <map>
 #include <mutex>
+#include <type_traits>
 #include <vector>
 
 #include "common.h"
@@ -77,62 +78,73 @@ __device__ void reduce_finalize(double (&acc)[NQ], const RedArgs& ra, int b, con
   }
 }
 
-// One CGS pass over NV basis vectors (see file header).
+// 16-byte vector of the basis element type (float4 for the fp32 basis, double2 for fp64).
+template <typename T> struct Vec16;
+template <> struct Vec16<float> { using type = float4; };
+template <> struct Vec16<double> { using type = double2; };
+
+// One CGS pass over NV basis vectors (see file header).  T = basis element type.
 //  UPDATE: dst = src - sum_i (hin_i alpha_i) V_i   (else dst = src, not written)
 //  DOTS  : out[i] = alpha_i <V_i, dst>, i < NV ;  always out[NV] = ||dst||^2
-template <int NV, bool UPDATE, bool DOTS>
+template <typename T, int NV, bool UPDATE, bool DOTS>
 __global__ void __launch_bounds__(kThreads, 1) cgs_kernel(
-    const float* __restrict__ V, int64_t vld, const double* __restrict__ alpha, int alpha_ld,
-    const double* __restrict__ hin, int hin_ld, const float* src, float* dst, int64_t ns,
+    const T* __restrict__ V, int64_t vld, const double* __restrict__ alpha, int alpha_ld,
+    const double* __restrict__ hin, int hin_ld, const T* src, T* dst, int64_t ns,
     const int* __restrict__ active, RedArgs ra, const double* __restrict__ sel_w2,
     const double* __restrict__ sel_v2) {
+  using VT = typename Vec16<T>::type;
+  constexpr int W = (int)(sizeof(VT) / sizeof(T));
   constexpr int NQ = (DOTS ? NV : 0) + 1;
   const int b = blockIdx.y;
   if (active && !active[b]) return;
   // selective re-orthogonalisation (DGKS, "twice is enough"): this second pass runs only when
   // ||v'||^2 < ||w||^2 / 2 (both from the previous passes); otherwise v' already is v_{j+1}
   if (sel_w2 && !(sel_v2[(int64_t)b * hin_ld] < 0.5 * sel_w2[(int64_t)b * hin_ld])) return;
-  __shared__ float coef[NV > 0 ? NV : 1];
+  __shared__ T coef[NV > 0 ? NV : 1];
   if (UPDATE) {
     for (int i = threadIdx.x; i < NV; i += blockDim.x)
-      coef[i] = (float)(hin[(int64_t)b * hin_ld + i] * alpha[(int64_t)b * alpha_ld + i]);
+      coef[i] = (T)(hin[(int64_t)b * hin_ld + i] * alpha[(int64_t)b * alpha_ld + i]);
     __syncthreads();
   }
   double acc[NQ];
 #pragma unroll
   for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
-  const int64_t n4 = ns / 4;
-  const float4* s4 = reinterpret_cast<const float4*>(src + (int64_t)b * ns);
-  float4* d4 = reinterpret_cast<float4*>(dst + (int64_t)b * ns);
-  const float* Vb = V + (int64_t)b * ns;
-  for (int64_t q = (int64_t)blockIdx.x * kThreads + threadIdx.x; q < n4; q += (int64_t)ra.nblk * kThreads) {
-    float4 s = s4[q];
-    float4 v[NV > 0 ? NV : 1];
+  const int64_t nv = ns / W;
+  const VT* s4 = reinterpret_cast<const VT*>(src + (int64_t)b * ns);
+  VT* d4 = reinterpret_cast<VT*>(dst + (int64_t)b * ns);
+  const T* Vb = V + (int64_t)b * ns;
+  for (int64_t q = (int64_t)blockIdx.x * kThreads + threadIdx.x; q < nv; q += (int64_t)ra.nblk * kThreads) {
+    VT sv = s4[q];
+    T* s = reinterpret_cast<T*>(&sv);
+    VT vv[NV > 0 ? NV : 1];
 #pragma unroll
-    for (int i = 0; i < NV; ++i) v[i] = reinterpret_cast<const float4*>(Vb + (int64_t)i * vld)[q];
+    for (int i = 0; i < NV; ++i) vv[i] = reinterpret_cast<const VT*>(Vb + (int64_t)i * vld)[q];
     if (UPDATE) {
 #pragma unroll
       for (int i = 0; i < NV; ++i) {
-        s.x = fmaf(-coef[i], v[i].x, s.x);
-        s.y = fmaf(-coef[i], v[i].y, s.y);
-        s.z = fmaf(-coef[i], v[i].z, s.z);
-        s.w = fmaf(-coef[i], v[i].w, s.w);
+        const T* v = reinterpret_cast<const T*>(&vv[i]);
+#pragma unroll
+        for (int e = 0; e < W; ++e) s[e] = fma(-coef[i], v[e], s[e]);
       }
-      d4[q] = s;
+      d4[q] = sv;
     }
     if (DOTS) {
 #pragma unroll
-      for (int i = 0; i < NV; ++i)
-        acc[i] += (double)v[i].x * s.x + (double)v[i].y * s.y + (double)v[i].z * s.z + (double)v[i].w * s.w;
+      for (int i = 0; i < NV; ++i) {
+        const T* v = reinterpret_cast<const T*>(&vv[i]);
+#pragma unroll
+        for (int e = 0; e < W; ++e) acc[i] += (double)v[e] * (double)s[e];
+      }
     }
-    acc[NQ - 1] += (double)s.x * s.x + (double)s.y * s.y + (double)s.z * s.z + (double)s.w * s.w;
+#pragma unroll
+    for (int e = 0; e < W; ++e) acc[NQ - 1] += (double)s[e] * (double)s[e];
   }
   reduce_finalize<NQ>(acc, ra, b, DOTS ? alpha + (int64_t)b * alpha_ld : nullptr, DOTS ? NV : 0);
 }
 
-// ||x||^2 per sample (x fp32 or fp64); optionally writes xo = (float)x.
-template <typename T>
-__global__ void __launch_bounds__(kThreads) norm_kernel(const T* __restrict__ x, float* __restrict__ xo, int64_t ns,
+// ||x||^2 per sample (x fp32 or fp64); optionally writes xo = (TO)x.
+template <typename T, typename TO>
+__global__ void __launch_bounds__(kThreads) norm_kernel(const T* __restrict__ x, TO* __restrict__ xo, int64_t ns,
                                                          RedArgs ra) {
   const int b = blockIdx.y;
   double acc[1] = {0.0};
@@ -140,34 +152,60 @@ __global__ void __launch_bounds__(kThreads) norm_kernel(const T* __restrict__ x,
   for (int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x; e < ns; e += (int64_t)ra.nblk * kThreads) {
     double v = (double)xb[e];
     acc[0] += v * v;
-    if (xo) xo[(int64_t)b * ns + e] = (float)v;
+    if (xo) xo[(int64_t)b * ns + e] = (TO)v;
   }
   reduce_finalize<1>(acc, ra, b, nullptr, 0);
 }
 
 // dst = sum_{i < k_b} coef_i V_i   (coef already includes alpha), fp64 accumulation.
-__global__ void __launch_bounds__(kThreads) combine_kernel(const float* __restrict__ V, int64_t vld,
+template <typename T, typename TO>
+__global__ void __launch_bounds__(kThreads) combine_kernel(const T* __restrict__ V, int64_t vld,
                                                             const double* __restrict__ coef, int coef_ld,
-                                                            const int* __restrict__ kcols, float* __restrict__ dst,
+                                                            const int* __restrict__ kcols, TO* __restrict__ dst,
                                                             int64_t ns, int nblk) {
   const int b = blockIdx.y;
   const int k = kcols[b];
   const double* cb = coef + (int64_t)b * coef_ld;
-  const float* Vb = V + (int64_t)b * ns;
+  const T* Vb = V + (int64_t)b * ns;
   for (int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x; e < ns; e += (int64_t)nblk * kThreads) {
     double s = 0.0;
     for (int i = 0; i < k; ++i) s += cb[i] * (double)Vb[(int64_t)i * vld + e];
-    dst[(int64_t)b * ns + e] = (float)s;
+    dst[(int64_t)b * ns + e] = (TO)s;
   }
 }
 
-// x += z  for samples with kcols > 0.
-__global__ void axpy64_kernel(double* __restrict__ x, const float* __restrict__ z, const int* __restrict__ kcols,
-                              int64_t ns, int nblk) {
+// x += z (+ q)  for samples with kcols > 0 (z fp32 or fp64; q optional fp32).
+template <typename TZ>
+__global__ void axpy64_kernel(double* __restrict__ x, const TZ* __restrict__ z, const float* __restrict__ q,
+                              const int* __restrict__ kcols, int64_t ns, int nblk) {
   const int b = blockIdx.y;
   if (kcols[b] <= 0) return;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < ns; e += (int64_t)nblk * blockDim.x)
-    x[(int64_t)b * ns + e] += (double)z[(int64_t)b * ns + e];
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < ns; e += (int64_t)nblk * blockDim.x) {
+    const int64_t o = (int64_t)b * ns + e;
+    x[o] += (double)z[o] + (q ? (double)q[o] : 0.0);
+  }
+}
+
+// fp64 mode: z64 = alpha_j V64_j and z32 = (float) z64 (the V-cycle's input).
+__global__ void scale_f64_kernel(const double* __restrict__ v, const double* __restrict__ alpha, int alpha_ld,
+                                 double* __restrict__ z64, float* __restrict__ z32, int64_t ns, int nblk) {
+  const int b = blockIdx.y;
+  const double a = alpha[(int64_t)b * alpha_ld];
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < ns; e += (int64_t)nblk * blockDim.x) {
+    const int64_t o = (int64_t)b * ns + e;
+    const double t = a * v[o];
+    z64[o] = t;
+    if (z32) z32[o] = (float)t;
+  }
+}
+
+// fp64 mode: z64 += q32 (the V-cycle's correction V(z)); z32 = (float) z64 when `to32`.
+__global__ void add_f32_to_f64_kernel(double* __restrict__ z64, const float* __restrict__ q, float* __restrict__ z32,
+                                      int64_t n) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    if (q) z64[e] += (double)q[e];
+    if (z32) z32[e] = (float)z64[e];
+  }
 }
 
 struct Status {      // per-sample record read by the host each iteration (32 bytes)
@@ -298,17 +336,23 @@ struct GmresWork {
   int *active = nullptr, *kcols = nullptr, *done = nullptr;
   Status* st_dev = nullptr;
   Status* st_host = nullptr;  // pinned
+  // fp64-basis mode (gmres_opts.precision = 1), allocated on first use
+  double* V64 = nullptr;   // (m+1) x n
+  double* w64 = nullptr;
+  double* z64 = nullptr;
+  float* q32 = nullptr;    // V-cycle output
   void release() {
     void* ps[] = {V, w, z, r64, Hr, Hraw, cs, sn, g, alpha, h1, h2, h3, coef, bnorm, rn2, partials, counters,
-                  active, kcols, done, st_dev};
+                  active, kcols, done, st_dev, V64, w64, z64, q32};
     for (void* p : ps) dfree(p);
     if (st_host) cudaFreeHost(st_host);
     *this = GmresWork();
   }
 };
 
-static void launch_cgs(const GmresWork& W, int nv, bool update, bool dots, const double* hin, const float* src,
-                       float* dst, double* out, cudaStream_t st, const double* sel_w2 = nullptr,
+template <typename TB>
+static void launch_cgs(const GmresWork& W, const TB* V, int nv, bool update, bool dots, const double* hin,
+                       const TB* src, TB* dst, double* out, cudaStream_t st, const double* sel_w2 = nullptr,
                        const double* sel_v2 = nullptr) {
   RedArgs ra{W.partials, W.counters, out, kMaxRestart + 2, W.nblk};
   dim3 grid(W.nblk, W.B);
@@ -318,8 +362,8 @@ static void launch_cgs(const GmresWork& W, int nv, bool update, bool dots, const
     constexpr int NV = decltype(nv_tag)::value;
     constexpr bool UP = decltype(up_tag)::value;
     constexpr bool DT = decltype(dot_tag)::value;
-    cgs_kernel<NV, UP, DT><<<grid, kThreads, 0, st>>>(W.V, vld, W.alpha, W.m + 1, hin, kMaxRestart + 2, src, dst,
-                                                      W.ns, W.active, ra, sel_w2, sel_v2);
+    cgs_kernel<TB, NV, UP, DT><<<grid, kThreads, 0, st>>>(V, vld, W.alpha, W.m + 1, hin, kMaxRestart + 2, src,
+                                                          dst, W.ns, W.active, ra, sel_w2, sel_v2);
   };
   using T = std::true_type;
   using F = std::false_type;
@@ -344,7 +388,7 @@ static void launch_cgs(const GmresWork& W, int nv, bool update, bool dots, const
   // bytes: NV basis vectors + src read, dst written if updating; flops: 2 per (vector, element)
   // for each of the update and the dots, + 2 per element for the norm.
   const double ne = (double)W.ns * W.B;
-  const double bytes = 4.0 * ne * (nv + 1 + (update ? 1 : 0));
+  const double bytes = (double)sizeof(TB) * ne * (nv + 1 + (update ? 1 : 0));
   const double flops = ne * (2.0 * nv * ((update ? 1 : 0) + (dots ? 1 : 0)) + 2.0);
   if (sel_w2)  // selective pass: whether it streamed is decided on the device, so no bytes are booked
     after_launch("cgs_reorth_selective", st, 0.0, 0.0, 0);
@@ -352,13 +396,13 @@ static void launch_cgs(const GmresWork& W, int nv, bool update, bool dots, const
     after_launch(update ? (dots ? "cgs_update_dots" : "cgs_update") : "cgs_dots", st, flops, bytes, 0);
 }
 
-template <typename T>
-static void launch_norm(const GmresWork& W, const T* x, float* xo, double* out, cudaStream_t st) {
+template <typename T, typename TO>
+static void launch_norm(const GmresWork& W, const T* x, TO* xo, double* out, cudaStream_t st) {
   RedArgs ra{W.partials, W.counters, out, 1, W.nblk};
   prof_begin(st);
-  norm_kernel<T><<<dim3(W.nblk, W.B), kThreads, 0, st>>>(x, xo, W.ns, ra);
+  norm_kernel<T, TO><<<dim3(W.nblk, W.B), kThreads, 0, st>>>(x, xo, W.ns, ra);
   const double ne = (double)W.ns * W.B;
-  after_launch("norm", st, 2.0 * ne, ne * (sizeof(T) + (xo ? 4.0 : 0.0)), 0);
+  after_launch("norm", st, 2.0 * ne, ne * (sizeof(T) + (xo ? sizeof(TO) : 0.0)), 0);
 }
 
 }  // namespace rte
@@ -436,6 +480,14 @@ extern "C" rte_status gmres_solve(const rte_problem* p, const mgnet_net* net, co
     const int hld = kMaxRestart + 2;
     const int reorth = opts->reorth;  // 0 CGS2, 1 CGS1, 2 selective (DGKS)
     RTE_REQUIRE(reorth >= 0 && reorth <= 2, "gmres_solve: reorth must be 0, 1 or 2");
+    RTE_REQUIRE(opts->precision == 0 || opts->precision == 1, "gmres_solve: precision must be 0 or 1");
+    const bool f64 = opts->precision == 1;
+    if (f64 && !W.V64) {
+      W.V64 = dalloc<double>((size_t)(m + 1) * n);
+      W.w64 = dalloc<double>(n);
+      W.z64 = dalloc<double>(n);
+      W.q32 = dalloc<float>(n);
+    }
     std::vector<int> total(B, 0), restarts(B, 0), brk(B, 0), conv(B, 0), done(B, 0);
     std::vector<double> est_last(B, 0.0), relres(B, 0.0);
     for (int b = 0; b < B; ++b) {
@@ -448,7 +500,7 @@ extern "C" rte_status gmres_solve(const rte_problem* p, const mgnet_net* net, co
     }
     RTE_CHECK_CUDA(cudaMemsetAsync(W.done, 0, sizeof(int) * B, st));
     // ||b|| per sample
-    launch_norm<float>(W, b_dev, nullptr, W.rn2, st);
+    launch_norm<float, float>(W, b_dev, nullptr, W.rn2, st);
     {
       std::vector<double> bn2(B);
       RTE_CHECK_CUDA(cudaMemcpyAsync(bn2.data(), W.rn2, sizeof(double) * B, cudaMemcpyDeviceToHost, st));
@@ -460,9 +512,12 @@ extern "C" rte_status gmres_solve(const rte_problem* p, const mgnet_net* net, co
     bool first_cycle = true;
     int total_all = 0;  // lockstep inner iterations
     while (true) {
-      // r = b - A x (fp64), v0 = r (fp32, unnormalised), ||r||^2
+      // r = b - A x (fp64), v0 = r (basis precision, unnormalised), ||r||^2
       launch_apply_f64(p, x_dev, W.r64, b_dev, st);
-      launch_norm<double>(W, W.r64, W.V, W.rn2, st);
+      if (f64)
+        launch_norm<double, double>(W, W.r64, W.V64, W.rn2, st);
+      else
+        launch_norm<double, float>(W, W.r64, W.V, W.rn2, st);
       int stop_all = (total_all >= opts->maxit) ? 1 : 0;
       prof_begin(st);
       cycle_init_kernel<<<(B + 63) / 64, 64, 0, st>>>(B, W.rn2, W.bnorm, opts->rtol, stop_all, W.alpha, m + 1, W.g,
@@ -481,30 +536,52 @@ extern "C" rte_status gmres_solve(const rte_problem* p, const mgnet_net* net, co
       }
       if (n_active == 0) break;
       for (int j = 0; j < m; ++j) {
-        // z = P(alpha_j V_j)  or  alpha_j V_j
-        const float* vj = W.V + (size_t)j * n;
-        if (opts->precond == 1) {
-          vcycle_run(net, vj, W.z, true, W.alpha + j, m + 1, st);
-          launch_apply_f32(p, W.z, W.w, nullptr, 0, st);
-        } else {
-          launch_apply_f32(p, vj, W.w, W.alpha + j, m + 1, st);
-        }
-        float* vnext = W.V + (size_t)(j + 1) * n;
-        launch_cgs(W, j + 1, false, true, nullptr, W.w, nullptr, W.h1, st);      // pass A
+        // Arnoldi step j: w = A P(alpha_j V_j), then CGS passes against V_0..V_j (basis type TB)
         const double* h2 = nullptr;
         const double* nrm = nullptr;
-        if (reorth != 1) {
-          launch_cgs(W, j + 1, true, true, W.h1, W.w, vnext, W.h2, st);          // pass B
-          if (reorth == 2)                                                        // pass C (selective)
-            launch_cgs(W, j + 1, true, false, W.h2, vnext, vnext, W.h3, st, W.h1 + (j + 1), W.h2 + (j + 1));
-          else
-            launch_cgs(W, j + 1, true, false, W.h2, vnext, vnext, W.h3, st);     // pass C
-          h2 = W.h2;
-          nrm = W.h3;  // update-only passes put ||.||^2 at index 0
+        auto cgs_passes = [&](auto* V, auto* wv) {
+          using TB = std::remove_pointer_t<decltype(V)>;
+          TB* vnext = V + (size_t)(j + 1) * n;
+          launch_cgs<TB>(W, V, j + 1, false, true, nullptr, wv, nullptr, W.h1, st);      // pass A
+          if (reorth != 1) {
+            launch_cgs<TB>(W, V, j + 1, true, true, W.h1, wv, vnext, W.h2, st);          // pass B
+            if (reorth == 2)                                                          // pass C (selective)
+              launch_cgs<TB>(W, V, j + 1, true, false, W.h2, vnext, vnext, W.h3, st, W.h1 + (j + 1), W.h2 + (j + 1));
+            else
+              launch_cgs<TB>(W, V, j + 1, true, false, W.h2, vnext, vnext, W.h3, st);     // pass C
+            h2 = W.h2;
+            nrm = W.h3;  // update-only passes put ||.||^2 at index 0
+          } else {
+            launch_cgs<TB>(W, V, j + 1, true, false, W.h1, wv, vnext, W.h2, st);         // CGS1 only
+            h2 = nullptr;
+            nrm = W.h2;
+          }
+        };
+        if (f64) {
+          // fp64 basis: z = alpha_j V_j (+ V(z) from the fp32 V-cycle), w = A z in fp64
+          const double* vj = W.V64 + (size_t)j * n;
+          prof_begin(st);
+          scale_f64_kernel<<<dim3(W.nblk, B), kThreads, 0, st>>>(vj, W.alpha + j, m + 1, W.z64,
+                                                                  opts->precond == 1 ? W.z : nullptr, W.ns, W.nblk);
+          after_launch("scale_f64", st, 0.0, 20.0 * (double)n, 0);
+          if (opts->precond == 1) {
+            vcycle_run(net, W.z, W.q32, false, nullptr, 0, st);
+            prof_begin(st);
+            add_f32_to_f64_kernel<<<W.nblk * B, kThreads, 0, st>>>(W.z64, W.q32, nullptr, n);
+            after_launch("add_f32_to_f64", st, 0.0, 20.0 * (double)n, 0);
+          }
+          launch_apply_f64(p, W.z64, W.w64, nullptr, st);
+          cgs_passes(W.V64, W.w64);
         } else {
-          launch_cgs(W, j + 1, true, false, W.h1, W.w, vnext, W.h2, st);         // CGS1 only
-          h2 = nullptr;
-          nrm = W.h2;
+          // fp32 basis: z = P(alpha_j V_j) or alpha_j V_j, w = A z in fp32
+          const float* vj = W.V + (size_t)j * n;
+          if (opts->precond == 1) {
+            vcycle_run(net, vj, W.z, true, W.alpha + j, m + 1, st);
+            launch_apply_f32(p, W.z, W.w, nullptr, 0, st);
+          } else {
+            launch_apply_f32(p, vj, W.w, W.alpha + j, m + 1, st);
+          }
+          cgs_passes(W.V, W.w);
         }
         ++total_all;
         int last = (total_all >= opts->maxit) ? 1 : 0;
@@ -539,17 +616,36 @@ extern "C" rte_status gmres_solve(const rte_problem* p, const mgnet_net* net, co
       prof_begin(st);
       backsolve_kernel<<<(B + 63) / 64, 64, 0, st>>>(B, m, W.Hr, W.g, W.alpha, m + 1, W.kcols, W.coef, m + 1);
       after_launch("backsolve", st);
-      prof_begin(st);
-      combine_kernel<<<dim3(W.nblk, B), kThreads, 0, st>>>(W.V, n, W.coef, m + 1, W.kcols, W.w, W.ns, W.nblk);
-      after_launch("combine", st, 2.0 * m * (double)n, 4.0 * (double)n * (m + 1), 0);
-      const float* corr = W.w;
-      if (opts->precond == 1) {
-        vcycle_run(net, W.w, W.z, true, nullptr, 0, st);
-        corr = W.z;
+      if (f64) {
+        prof_begin(st);
+        combine_kernel<double, double><<<dim3(W.nblk, B), kThreads, 0, st>>>(W.V64, n, W.coef, m + 1, W.kcols, W.z64,
+                                                                              W.ns, W.nblk);
+        after_launch("combine", st, 2.0 * m * (double)n, 8.0 * (double)n * (m + 1), 0);
+        const float* q = nullptr;
+        if (opts->precond == 1) {
+          prof_begin(st);
+          add_f32_to_f64_kernel<<<W.nblk * B, kThreads, 0, st>>>(W.z64, nullptr, W.z, n);  // z32 = (float) z64
+          after_launch("add_f32_to_f64", st, 0.0, 12.0 * (double)n, 0);
+          vcycle_run(net, W.z, W.q32, false, nullptr, 0, st);
+          q = W.q32;
+        }
+        prof_begin(st);
+        axpy64_kernel<double><<<dim3(W.nblk, B), kThreads, 0, st>>>(x_dev, W.z64, q, W.kcols, W.ns, W.nblk);
+        after_launch("axpy64", st, (double)n, 28.0 * (double)n, 0);
+      } else {
+        prof_begin(st);
+        combine_kernel<float, float><<<dim3(W.nblk, B), kThreads, 0, st>>>(W.V, n, W.coef, m + 1, W.kcols, W.w, W.ns,
+                                                                            W.nblk);
+        after_launch("combine", st, 2.0 * m * (double)n, 4.0 * (double)n * (m + 1), 0);
+        const float* corr = W.w;
+        if (opts->precond == 1) {
+          vcycle_run(net, W.w, W.z, true, nullptr, 0, st);
+          corr = W.z;
+        }
+        prof_begin(st);
+        axpy64_kernel<float><<<dim3(W.nblk, B), kThreads, 0, st>>>(x_dev, corr, nullptr, W.kcols, W.ns, W.nblk);
+        after_launch("axpy64", st, (double)n, 20.0 * (double)n, 0);
       }
-      prof_begin(st);
-      axpy64_kernel<<<dim3(W.nblk, B), kThreads, 0, st>>>(x_dev, corr, W.kcols, W.ns, W.nblk);
-      after_launch("axpy64", st, (double)n, 20.0 * (double)n, 0);
       // samples that broke down stop (oracle: breakdown ends the solve)
       bool any_brk = false;
       for (int b = 0; b < B; ++b)

@@ -391,6 +391,24 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&xempty[xt]);
       if constexpr (Epi::kCenter) mbar_wait(&cfull[xt], (uint32_t)(li >> 1) & 1u);
+#ifndef RTE_EPI_STAGED
+      // Direct epilogue: thread r owns tile row r and writes its BN columns as float4s.
+      {
+        const int ly = r / g.TW, lx = r - ly * g.TW;
+        const int oy = w.tc.ty * g.TH + ly, ox = w.tc.tx * g.TW + lx;
+        const float crow = Epi::kCenter ? cvec[xt * 128 + r] : 0.f;
+        if (r < rows && oy < g.Hc && ox < g.Wc && !(g.dbg & 32)) {
+#pragma unroll
+          for (int c = 0; c < BN; c += 4) {
+            const float4 v = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
+            if (g.nsplit > 1)
+              epi.store_partial4(w.split, w.tc.b, w.tc.cls, oy, ox, w.n0 + c, v);
+            else
+              epi.store4(w.tc.b, w.tc.cls, oy, ox, w.n0 + c, v, crow);
+          }
+        }
+      }
+#else
       // Coalesced epilogue: each 32-column chunk of the accumulator is staged through a shared tile
       // (double-buffered, 16-byte chunks XOR-swizzled by row & 7: conflict-free both ways); then
       // lane l of warp pw handles columns 4(l & 7) .. +3 of tile rows pw*32 + 4 it + (l >> 3), so
@@ -423,6 +441,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
       }
       named_bar_sync(2, 128);  // staging buffers free before the next unit writes them
+#endif
       if constexpr (Epi::kCenter) mbar_arrive(&cempty[xt]);
     }
   }
