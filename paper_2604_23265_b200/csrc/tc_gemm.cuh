@@ -26,7 +26,15 @@
 namespace rte {
 namespace tc {
 
-constexpr int kGemmThreads = 384;   // 3 warpgroups (see kernel)
+#ifdef RTE_TC_WARPS12
+constexpr int kGemmThreads = 384;   // 3 warpgroups, registers rebalanced with setmaxnreg
+constexpr int kConvWarp0 = 4;       // converters: warps 4..7
+constexpr int kPromWarp0 = 8;       // promoters / epilogue: warps 8..11
+#else
+constexpr int kGemmThreads = 320;   // 10 warps
+constexpr int kConvWarp0 = 2;       // converters: warps 2..5
+constexpr int kPromWarp0 = 6;       // promoters / epilogue: warps 6..9
+#endif
 constexpr int kPromoteKB = 4;       // K blocks per TMEM accumulation group
 constexpr int kTileM = 128;
 constexpr int kABytes = kTileM * 128;   // 128 rows x 32 fp32
@@ -214,24 +222,26 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   // Register rebalancing per warpgroup (setmaxnreg at the top of each warpgroup's branch): the
   // promoters hold BN fp32 accumulators per thread.
+#ifdef RTE_TC_WARPS12
   if (warp < 4) reg_dealloc<56>();
+#endif
   if (warp == 0) {
-    // ===== TMA producer =====
-    if (lane == 0) {
-      int s = 0;
-      uint32_t ph = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const Unit w = decode_unit(g, u);
-        const int brow = w.n0 + w.tc.cls * g.b_rows_class + w.tc.b * g.b_rows_batch;
-        for (int kb = w.kb0; kb < w.kb1; ++kb, ++n_kb) {
-          tw_wait(&empty[s], ph ^ 1, prof, w_a);
-          uint8_t* sa = smem + s * STAGE;
-          uint8_t* sbh = sa + 2 * kABytes;
-          uint8_t* sbl = sbh + BBYTES;
-          const int tap = kb / g.cchunks, ci0 = (kb % g.cchunks) * 32;
-          int xA, yA;
-          a_origin(g, w.tc, tap, xA, yA);
-          const bool no_blo = (g.dbg & 2) != 0;
+    // ===== TMA producer: the whole warp walks the pipeline, one elected lane issues =====
+    int s = 0;
+    uint32_t ph = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const Unit w = decode_unit(g, u);
+      const int brow = w.n0 + w.tc.cls * g.b_rows_class + w.tc.b * g.b_rows_batch;
+      for (int kb = w.kb0; kb < w.kb1; ++kb, ++n_kb) {
+        tw_wait(&empty[s], ph ^ 1, prof, w_a);
+        uint8_t* sa = smem + s * STAGE;
+        uint8_t* sbh = sa + 2 * kABytes;
+        uint8_t* sbl = sbh + BBYTES;
+        const int tap = kb / g.cchunks, ci0 = (kb % g.cchunks) * 32;
+        int xA, yA;
+        a_origin(g, w.tc, tap, xA, yA);
+        const bool no_blo = (g.dbg & 2) != 0;
+        if (elect_one()) {
           if (g.dbg & 16) {
             mbar_arrive(&full[s]);
           } else {
@@ -240,66 +250,70 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             tma_load_2d(sbh, &tmBhi, &full[s], kb * 32, brow);
             if (!no_blo) tma_load_2d(sbl, &tmBlo, &full[s], kb * 32, brow);
           }
-          if (++s == STAGES) { s = 0; ph ^= 1; }
         }
+        __syncwarp();
+        if (++s == STAGES) { s = 0; ph ^= 1; }
       }
     }
   } else if (warp == 1) {
-    // ===== MMA issuer =====
-    if (lane == 0) {
-      constexpr uint32_t idesc = idesc_tf32(kTileM, BN);
-      int s = 0;
-      uint32_t ph = 0;
-      int gcount = 0;  // main-buffer groups issued so far (all units)
-      int li = 0;      // local unit index
-      for (int u = blockIdx.x; u < units; u += gridDim.x, ++li) {
-        const Unit w = decode_unit(g, u);
-        const int xt = li & 1;
-        tw_wait(&xempty[xt], ((uint32_t)(li >> 1) & 1u) ^ 1u, prof, w_c);
+    // ===== MMA issuer: the whole warp walks the pipeline, one elected lane issues =====
+    constexpr uint32_t idesc = idesc_tf32(kTileM, BN);
+    const bool no_x = (g.dbg & 4) != 0, no_blo = (g.dbg & 2) != 0, no_mma = (g.dbg & 8) != 0;
+    int s = 0;
+    uint32_t ph = 0;
+    int gcount = 0;  // main-buffer groups issued so far (all units)
+    int li = 0;      // local unit index
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++li) {
+      const Unit w = decode_unit(g, u);
+      const int xt = li & 1;
+      tw_wait(&xempty[xt], ((uint32_t)(li >> 1) & 1u) ^ 1u, prof, w_c);
+      tc_fence_after();
+      const uint32_t tx = tmem + (uint32_t)(2 * BN + xt * BN);
+      uint32_t acc_x = 0;
+      for (int kbg = w.kb0; kbg < w.kb1; kbg += kPromoteKB, ++gcount) {
+        const int t = gcount & 1;
+        tw_wait(&mempty[t], ((uint32_t)(gcount >> 1) & 1u) ^ 1u, prof, w_b);
         tc_fence_after();
-        const uint32_t tx = tmem + (uint32_t)(2 * BN + xt * BN);
-        uint32_t acc_x = 0;
-        for (int kbg = w.kb0; kbg < w.kb1; kbg += kPromoteKB, ++gcount) {
-          const int t = gcount & 1;
-          tw_wait(&mempty[t], ((uint32_t)(gcount >> 1) & 1u) ^ 1u, prof, w_b);
+        const uint32_t tm = tmem + (uint32_t)(t * BN);
+        uint32_t acc_m = 0;
+        const int kbe = min(w.kb1, kbg + kPromoteKB);
+        for (int kb = kbg; kb < kbe; ++kb, ++n_kb) {
+          tw_wait(&conv[s], ph, prof, w_a);
           tc_fence_after();
-          const uint32_t tm = tmem + (uint32_t)(t * BN);
-          uint32_t acc_m = 0;
-          const int kbe = min(w.kb1, kbg + kPromoteKB);
-          for (int kb = kbg; kb < kbe; ++kb, ++n_kb) {
-            tw_wait(&conv[s], ph, prof, w_a);
-            tc_fence_after();
-            const uint32_t sa = smem_u32(smem + s * STAGE);
-            const uint32_t sal = sa + kABytes;
-            const uint32_t sbh = sa + 2 * kABytes;
-            const uint32_t sbl = sbh + BBYTES;
+          const uint32_t sa = smem_u32(smem + s * STAGE);
+          // descriptors of the stage's four operand tiles; a K step of 8 tf32 = 32 B = +2 in the
+          // descriptor's start-address field
+          const uint64_t d_ah = sdesc_sw128(sa), d_al = sdesc_sw128(sa + kABytes);
+          const uint64_t d_bh = sdesc_sw128(sa + 2 * kABytes), d_bl = sdesc_sw128(sa + 2 * kABytes + BBYTES);
+          if (!no_mma) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-              if (g.dbg & 8) break;
-              const uint32_t o = 32u * k;
-              if (!(g.dbg & 4)) {
-                mma_tf32(tx, sdesc_sw128(sal + o), sdesc_sw128(sbh + o), idesc, acc_x);
-                if (!(g.dbg & 2)) mma_tf32(tx, sdesc_sw128(sa + o), sdesc_sw128(sbl + o), idesc, 1);
+              const uint64_t o = 2u * k;
+              if (!no_x) {
+                mma_tf32_elect(tx, d_al + o, d_bh + o, idesc, acc_x);
+                if (!no_blo) mma_tf32_elect(tx, d_ah + o, d_bl + o, idesc, 1);
               } else if (!acc_x) {
-                mma_tf32(tx, sdesc_sw128(sal + o), sdesc_sw128(sbh + o), idesc, 0);
+                mma_tf32_elect(tx, d_al + o, d_bh + o, idesc, 0);
               }
               acc_x = 1;
-              mma_tf32(tm, sdesc_sw128(sa + o), sdesc_sw128(sbh + o), idesc, acc_m);
+              mma_tf32_elect(tm, d_ah + o, d_bh + o, idesc, acc_m);
               acc_m = 1;
             }
-            mma_commit(&empty[s]);
-            if (++s == STAGES) { s = 0; ph ^= 1; }
           }
-          mma_commit(&mfull[t]);
+          mma_commit_elect(&empty[s]);
+          if (++s == STAGES) { s = 0; ph ^= 1; }
         }
+        mma_commit_elect(&mfull[t]);
       }
     }
-  } else if (warp < 4) {
-    // warps 2, 3: no role
-  } else if (warp < 8) {
-    // ===== converters (warpgroup 1): A tile -> [centre] -> hi (in place) + lo =====
+  } else if (warp < kConvWarp0) {
+    // (12-warp layout) warps 2, 3: no role
+  } else if (warp < kConvWarp0 + 4) {
+    // ===== converters: A tile -> [centre] -> hi (in place) + lo =====
+#ifdef RTE_TC_WARPS12
     reg_dealloc<120>();
-    const int ct = threadIdx.x - 128;  // 0..127
+#endif
+    const int ct = threadIdx.x - 32 * kConvWarp0;  // 0..127
     int s = 0;
     uint32_t ph = 0;
     int li = 0;
@@ -349,8 +363,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
     }
   } else {
-    // ===== promoters + epilogue (warpgroup 2; warp w owns TMEM lanes 32*(w%4) .. +31) =====
+    // ===== promoters + epilogue (warp w owns TMEM lanes 32*(w%4) .. +31) =====
+#ifdef RTE_TC_WARPS12
     reg_alloc<232>();
+#endif
     const int quarter = warp & 3;
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
     const int r = quarter * 32 + lane;  // tile row = TMEM lane
@@ -413,7 +429,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       // (double-buffered, 16-byte chunks XOR-swizzled by row & 7: conflict-free both ways); then
       // lane l of warp pw handles columns 4(l & 7) .. +3 of tile rows pw*32 + 4 it + (l >> 3), so
       // each warp instruction moves four full 128-byte rows.
-      const int pw = warp - 8;
+      const int pw = warp - kPromWarp0;
 #pragma unroll
       for (int c0 = 0; c0 < BN; c0 += 32) {
         const uint32_t eb = etile + (uint32_t)(((c0 >> 5) & 1) * kTileM * 128);
@@ -445,7 +461,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       if constexpr (Epi::kCenter) mbar_arrive(&cempty[xt]);
     }
   }
-  if (prof && (warp <= 1 || warp == 4 || warp == 8))
+  if (prof && (warp <= 1 || warp == kConvWarp0 || warp == kPromWarp0))
     printf("tcprof BN=%d units=%d grid=%d warp=%d kb=%d total=%lld waitA=%lld waitB=%lld waitC=%lld\n", BN, units,
            gridDim.x, warp, n_kb, clock64() - t_start, w_a, w_b, w_c);
   tc_fence_before();
