@@ -36,18 +36,26 @@ struct EpiApply {
   const double* alpha;
   int alpha_stride, N, M;
 
-  // columns m .. m+3 share a quadrant (M % 16 == 0), hence both upwind signs
-  __device__ __forceinline__ void store4(int b, int, int j, int i, int m, float4 v, float c) const {
+  struct Row {
+    long long cell;
+    int i, j;
+    float st, ss, al, c;
+  };
+  __device__ __forceinline__ Row row(int b, int, int j, int i, float c) const {
     const long long cell = ((long long)b * N + j) * N + i;
-    const float st = sig_t[cell], ss = sig_s[cell];
-    const float al = alpha ? (float)alpha[(long long)b * alpha_stride] : 1.f;
+    return Row{cell, i, j, sig_t[cell], sig_s[cell], alpha ? (float)alpha[(long long)b * alpha_stride] : 1.f, c};
+  }
+  // columns m .. m+3 share a quadrant (M % 16 == 0), hence both upwind signs
+  __device__ __forceinline__ void store4(const Row& rw, int m, float4 v) const {
+    const long long cell = rw.cell;
     const int sx = sgx[m], sy = sgy[m];
     const float4 a_x = *reinterpret_cast<const float4*>(ax + m);
     const float4 a_y = *reinterpret_cast<const float4*>(ay + m);
     const float4 p = *reinterpret_cast<const float4*>(x + cell * M + m);
     float4 nx = make_float4(0.f, 0.f, 0.f, 0.f), ny = nx;
-    if ((unsigned)(i - sx) < (unsigned)N) nx = *reinterpret_cast<const float4*>(x + (cell - sx) * M + m);
-    if ((unsigned)(j - sy) < (unsigned)N) ny = *reinterpret_cast<const float4*>(x + (cell - (long long)sy * N) * M + m);
+    if ((unsigned)(rw.i - sx) < (unsigned)N) nx = *reinterpret_cast<const float4*>(x + (cell - sx) * M + m);
+    if ((unsigned)(rw.j - sy) < (unsigned)N) ny = *reinterpret_cast<const float4*>(x + (cell - (long long)sy * N) * M + m);
+    const float st = rw.st, ss = rw.ss, al = rw.al, c = rw.c;
     float4 r;
     r.x = al * ((a_x.x + a_y.x + st) * p.x - ss * (c + v.x) - a_x.x * nx.x - a_y.x * ny.x);
     r.y = al * ((a_x.y + a_y.y + st) * p.y - ss * (c + v.y) - a_x.y * nx.y - a_y.y * ny.y);
@@ -55,7 +63,7 @@ struct EpiApply {
     r.w = al * ((a_x.w + a_y.w + st) * p.w - ss * (c + v.w) - a_x.w * nx.w - a_y.w * ny.w);
     *reinterpret_cast<float4*>(y + cell * M + m) = r;
   }
-  __device__ __forceinline__ void store_partial4(int, int, int, int, int, int, float4) const {}
+  __device__ __forceinline__ void store_partial4(int, const Row&, int, float4) const {}
 };
 
 template <int BN>

@@ -137,23 +137,28 @@ struct EpiConv {
     }
     return (((long long)b * Ho + Y) * Wo + X) * Co + col;
   }
-  __device__ __forceinline__ void store4(int b, int cls, int oy, int ox, int col, float4 v, float) const {
-    const long long o = index(b, cls, oy, ox, col);
+  struct Row {
+    long long o;  // output offset of column 0 of this pixel
+    float si, sa;
+  };
+  __device__ __forceinline__ Row row(int b, int cls, int oy, int ox, float) const {
     const float al = alpha ? (float)alpha[(long long)b * alpha_stride] : 1.f;
-    const float si = sign * (a_in ? al : 1.f);
-    float4 r = make_float4(si * v.x, si * v.y, si * v.z, si * v.w);
+    return Row{index(b, cls, oy, ox, 0), sign * (a_in ? al : 1.f), a_add ? al : 1.f};
+  }
+  __device__ __forceinline__ void store4(const Row& rw, int col, float4 v) const {
+    const long long o = rw.o + col;
+    float4 r = make_float4(rw.si * v.x, rw.si * v.y, rw.si * v.z, rw.si * v.w);
     if (addend) {
-      const float sa = a_add ? al : 1.f;
       const float4 a = *reinterpret_cast<const float4*>(addend + o);
-      r.x = fmaf(sa, a.x, r.x);
-      r.y = fmaf(sa, a.y, r.y);
-      r.z = fmaf(sa, a.z, r.z);
-      r.w = fmaf(sa, a.w, r.w);
+      r.x = fmaf(rw.sa, a.x, r.x);
+      r.y = fmaf(rw.sa, a.y, r.y);
+      r.z = fmaf(rw.sa, a.z, r.z);
+      r.w = fmaf(rw.sa, a.w, r.w);
     }
     *reinterpret_cast<float4*>(out + o) = r;
   }
-  __device__ __forceinline__ void store_partial4(int split, int b, int cls, int oy, int ox, int col, float4 v) const {
-    *reinterpret_cast<float4*>(part + split * part_stride + index(b, cls, oy, ox, col)) = v;
+  __device__ __forceinline__ void store_partial4(int split, const Row& rw, int col, float4 v) const {
+    *reinterpret_cast<float4*>(part + split * part_stride + rw.o + col) = v;
   }
 };
 

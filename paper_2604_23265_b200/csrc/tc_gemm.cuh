@@ -136,10 +136,10 @@ __device__ __forceinline__ void a_origin(const Geom& g, const TileCoord& c, int 
   }
 }
 
-// Epilogue interface (four consecutive columns per call): epi.store4(b, cls, oy, ox, col, v4,
-// c_row) for every valid output pixel (oy, ox) of the class grid, columns col .. col+3 (c_row = the
-// row centre when Epi::kCenter: the GEMM then computed (a - c_row 1) . B^T);
-// epi.store_partial4(split, b, cls, oy, ox, col, v4) when split-K is active (nsplit > 1).
+// Epilogue interface: row = epi.row(b, cls, oy, ox, c_row) prepares the per-output-pixel state of a
+// valid pixel (oy, ox) of the class grid (c_row = the row centre when Epi::kCenter: the GEMM then
+// computed (a - c_row 1) . B^T); epi.store4(row, col, v4) finishes columns col .. col+3;
+// epi.store_partial4(split, row, col, v4) stores raw partial sums when split-K is active.
 //
 // Accumulation precision.  The tensor core's fp32 accumulation does not round to nearest (a
 // biased, truncating add), so a long K loop into one TMEM accumulator drifts by ~K/8 * 2^-24
@@ -412,15 +412,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       {
         const int ly = r / g.TW, lx = r - ly * g.TW;
         const int oy = w.tc.ty * g.TH + ly, ox = w.tc.tx * g.TW + lx;
-        const float crow = Epi::kCenter ? cvec[xt * 128 + r] : 0.f;
         if (r < rows && oy < g.Hc && ox < g.Wc && !(g.dbg & 32)) {
+          const typename Epi::Row row = epi.row(w.tc.b, w.tc.cls, oy, ox, Epi::kCenter ? cvec[xt * 128 + r] : 0.f);
 #pragma unroll
           for (int c = 0; c < BN; c += 4) {
             const float4 v = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
             if (g.nsplit > 1)
-              epi.store_partial4(w.split, w.tc.b, w.tc.cls, oy, ox, w.n0 + c, v);
+              epi.store_partial4(w.split, row, w.n0 + c, v);
             else
-              epi.store4(w.tc.b, w.tc.cls, oy, ox, w.n0 + c, v, crow);
+              epi.store4(row, w.n0 + c, v);
           }
         }
       }
@@ -447,11 +447,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             const int oy = w.tc.ty * g.TH + ly, ox = w.tc.tx * g.TW + lx;
             if (rr < rows && oy < g.Hc && ox < g.Wc) {
               const float4 val = lds128(eb + (uint32_t)(rr * 128 + ((k ^ (rr & 7)) << 4)));
+              const typename Epi::Row row = epi.row(w.tc.b, w.tc.cls, oy, ox, Epi::kCenter ? cvec[xt * 128 + rr] : 0.f);
               if (g.nsplit > 1)
-                epi.store_partial4(w.split, w.tc.b, w.tc.cls, oy, ox, w.n0 + c0 + 4 * k, val);
+                epi.store_partial4(w.split, row, w.n0 + c0 + 4 * k, val);
               else
-                epi.store4(w.tc.b, w.tc.cls, oy, ox, w.n0 + c0 + 4 * k, val,
-                           Epi::kCenter ? cvec[xt * 128 + rr] : 0.f);
+                epi.store4(row, w.n0 + c0 + 4 * k, val);
             }
           }
         }
