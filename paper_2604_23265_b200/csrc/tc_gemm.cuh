@@ -6,14 +6,17 @@
 // where a K block kb = (tap, 32-channel chunk).  A_kb is a shifted (and for the stride-2
 // restriction, strided) window of the NHWC activation, fetched by a 4-D TMA tiled load whose
 // out-of-bounds zero fill implements the convolution's zero padding; B_kb is a 32-wide K slice of
-// the weights stored [rows][K] K-major.  3xTF32 (R26): A is split in shared memory into
-// hi = rna_tf32(a) (in place) and lo = rna_tf32(a - hi); the weights arrive pre-split; each
-// k-step issues lo.hi + hi.lo + hi.hi into the same TMEM accumulator.
+// the weights stored [rows][K] K-major.  3xTF32 (R26): the converter warps read each A
+// row once from shared memory, split it into hi + lo and store both into TMEM (tcgen05.st); the
+// MMAs take A from TMEM and only the pre-split weights (B hi, B lo) from shared memory, which keeps
+// the shared-memory traffic per K block at raw-A TMA write + one read + B (the SS form saturated
+// the 128 B/clk shared-memory port).  Each k-step issues lo.hi + hi.lo (cross-term accumulator)
+// and hi.hi (main accumulator).
 //
-// Warp roles (384 threads = 3 warpgroups, registers rebalanced with setmaxnreg): warp 0 = TMA
-// producer, warp 1 = TMEM allocator + MMA issuer (one elected lane), warpgroup 1 = A-operand hi/lo
-// converters, warpgroup 2 = accumulator promotion and the epilogue (TMEM -> registers -> global;
-// warp w owns TMEM lanes 32*(w%4) .. +31).  Pipelines:
+// Warp roles (320 threads): warp 0 = TMA producer, warp 1 = TMEM allocator + MMA issuer (both walk
+// the pipeline warp-wide, one elected lane issues), warps 2..5 = A hi/lo converters (smem -> TMEM),
+// warps 6..9 = accumulator promotion and the epilogue (TMEM -> registers -> global); warp w
+// accesses TMEM lanes 32*(w%4) .. +31.  Pipelines:
 // full[s] (TMA bytes landed) -> conv[s] (hi/lo written) -> empty[s] (MMAs done, tcgen05.commit);
 // mfull[t] / mempty[t] hand the two main-accumulator TMEM buffers between MMA and promoters.
 #pragma once
@@ -26,15 +29,7 @@
 namespace rte {
 namespace tc {
 
-#ifdef RTE_TC_WARPS12
-constexpr int kGemmThreads = 384;   // 3 warpgroups, registers rebalanced with setmaxnreg
-constexpr int kConvWarp0 = 4;       // converters: warps 4..7
-constexpr int kPromWarp0 = 8;       // promoters / epilogue: warps 8..11
-#else
-constexpr int kGemmThreads = 320;   // 10 warps
-constexpr int kConvWarp0 = 2;       // converters: warps 2..5
-constexpr int kPromWarp0 = 6;       // promoters / epilogue: warps 6..9
-#endif
+constexpr int kGemmThreads = 320;   // 10 warps (see kernel)
 constexpr int kPromoteKB = 4;       // K blocks per TMEM accumulation group
 constexpr int kTileM = 128;
 constexpr int kABytes = kTileM * 128;   // 128 rows x 32 fp32
@@ -62,25 +57,31 @@ struct Geom {
                     // bit3 no MMAs at all, bit4 no TMA loads, bit5 no epilogue global traffic
 };
 
-constexpr int kEpiBytes = 2 * kTileM * 128;    // 2 x [128 rows][32 fp32], float4 chunks swizzled by row & 7
 
 template <int BN>
 struct Smem {
   static constexpr int kBBytes = BN * 128;
-  static constexpr int kStage = 2 * kABytes + 2 * kBBytes;
+  static constexpr int kStage = kABytes + 2 * kBBytes;   // raw A tile + B hi + B lo
 };
 
 template <int BN>
 constexpr int gemm_stages() {
 #ifdef RTE_TC_STAGES
-  if ((2 * kABytes + 2 * BN * 128) * RTE_TC_STAGES <= 200 * 1024) return RTE_TC_STAGES;
+  if (Smem<BN>::kStage * RTE_TC_STAGES <= 192 * 1024) return RTE_TC_STAGES;
 #endif
-  return (2 * kABytes + 2 * BN * 128) * 4 <= 200 * 1024 ? 4 : ((2 * kABytes + 2 * BN * 128) * 3 <= 200 * 1024 ? 3 : 2);
+  return Smem<BN>::kStage * 6 <= 192 * 1024 ? 6 : (192 * 1024) / Smem<BN>::kStage;
+}
+
+// TMEM columns: main accumulators M0, M1 [0, 2BN), cross-term accumulator X [2BN, 3BN), then
+// kABufs A buffers of 64 columns (hi: 32 K columns, lo: 32 K columns).
+template <int BN>
+constexpr int tmem_abufs() {
+  return (512 - 3 * BN) / 64 < 6 ? (512 - 3 * BN) / 64 : 6;
 }
 
 template <int BN>
 constexpr int gemm_smem_bytes() {
-  return gemm_stages<BN>() * Smem<BN>::kStage + 1024 /*align*/ + 512 /*barriers*/ + 1024 /*row centres*/ + kEpiBytes;
+  return gemm_stages<BN>() * Smem<BN>::kStage + 1024 /*align*/ + 512 /*barriers*/ + 1024 /*row centres*/;
 }
 
 struct TileCoord {
@@ -166,33 +167,33 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                       const __grid_constant__ CUtensorMap tmBlo, const Geom g, const Epi epi) {
   static_assert(BN == 32 || BN == 64 || BN == 128, "N tile must be 32, 64 or 128");
   constexpr int STAGES = gemm_stages<BN>();
+  constexpr int NA = tmem_abufs<BN>();
   constexpr int BBYTES = Smem<BN>::kBBytes;
   constexpr int STAGE = Smem<BN>::kStage;
-  // TMEM: main accumulator buffers M0, M1 at columns [0, 2BN), cross-term buffers X0, X1 at [2BN, 4BN)
-  constexpr uint32_t TMEM_COLS = BN == 32 ? 128 : (BN == 64 ? 256 : 512);
+  constexpr uint32_t TMEM_COLS = 512;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE);
   uint64_t* full = bars;                       // [STAGES] TMA bytes landed
-  uint64_t* conv = bars + STAGES;              // [STAGES] hi/lo written (4 converter warps)
-  uint64_t* empty = bars + 2 * STAGES;         // [STAGES] MMAs done with the stage
-  uint64_t* mfull = bars + 3 * STAGES;         // [2] main buffer ready for promotion
-  uint64_t* mempty = bars + 3 * STAGES + 2;    // [2] main buffer drained (4 promoter warps)
-  uint64_t* xempty = bars + 3 * STAGES + 4;    // [2] cross buffer drained by the epilogue
-  uint64_t* cfull = bars + 3 * STAGES + 6;     // [2] row centres written (128 converter threads)
-  uint64_t* cempty = bars + 3 * STAGES + 8;    // [2] row centres read (128 epilogue threads)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 10);
+  uint64_t* conv = bars + STAGES;              // [STAGES] A hi/lo in TMEM (4 converter warps)
+  uint64_t* empty = bars + 2 * STAGES;         // [STAGES] MMAs done with the stage's B tiles
+  uint64_t* afree = bars + 3 * STAGES;         // [NA] MMAs done with a TMEM A buffer
+  uint64_t* mfull = afree + NA;                // [2] main buffer ready for promotion
+  uint64_t* mempty = mfull + 2;                // [2] main buffer drained (4 promoter warps)
+  uint64_t* xempty = mempty + 2;               // [1] cross buffer drained by the epilogue
+  uint64_t* cfull = xempty + 1;                // [2] row centres written (128 converter threads)
+  uint64_t* cempty = cfull + 2;                // [2] row centres read (128 epilogue threads)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cempty + 2);
   float* cvec = reinterpret_cast<float*>(smem + STAGES * STAGE + 512);  // [2][128] row centres
-  const uint32_t etile = smem_u32(smem + STAGES * STAGE + 512 + 1024);  // 2 x [128][32] epilogue staging
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int units = g.mtiles * g.ntiles * g.nsplit;
+  const int rows = g.TW * g.TH;
+  const uint32_t a_bytes = (uint32_t)rows * 128u;
   const bool prof = (g.dbg & 64) && blockIdx.x == 0 && lane == 0;
   long long w_a = 0, w_b = 0, w_c = 0;
   const long long t_start = clock64();
   int n_kb = 0;
-  const int rows = g.TW * g.TH;
-  const uint32_t a_bytes = (uint32_t)rows * 128u;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -200,13 +201,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       mbar_init(&conv[s], 4);
       mbar_init(&empty[s], 1);
     }
+    for (int a = 0; a < NA; ++a) mbar_init(&afree[a], 1);
     for (int t = 0; t < 2; ++t) {
       mbar_init(&mfull[t], 1);
       mbar_init(&mempty[t], 4);
-      mbar_init(&xempty[t], 4);
       mbar_init(&cfull[t], 128);
       mbar_init(&cempty[t], 128);
     }
+    mbar_init(xempty, 4);
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
@@ -219,12 +221,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem_x = tmem + 2 * BN;
+  const uint32_t tmem_a = tmem + 3 * BN;
 
-  // Register rebalancing per warpgroup (setmaxnreg at the top of each warpgroup's branch): the
-  // promoters hold BN fp32 accumulators per thread.
-#ifdef RTE_TC_WARPS12
-  if (warp < 4) reg_dealloc<56>();
-#endif
   if (warp == 0) {
     // ===== TMA producer: the whole warp walks the pipeline, one elected lane issues =====
     int s = 0;
@@ -235,20 +234,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       for (int kb = w.kb0; kb < w.kb1; ++kb, ++n_kb) {
         tw_wait(&empty[s], ph ^ 1, prof, w_a);
         uint8_t* sa = smem + s * STAGE;
-        uint8_t* sbh = sa + 2 * kABytes;
-        uint8_t* sbl = sbh + BBYTES;
         const int tap = kb / g.cchunks, ci0 = (kb % g.cchunks) * 32;
         int xA, yA;
         a_origin(g, w.tc, tap, xA, yA);
-        const bool no_blo = (g.dbg & 2) != 0;
         if (elect_one()) {
           if (g.dbg & 16) {
             mbar_arrive(&full[s]);
           } else {
-            mbar_arrive_expect_tx(&full[s], a_bytes + (no_blo ? 1u : 2u) * BBYTES);
+            mbar_arrive_expect_tx(&full[s], a_bytes + 2u * BBYTES);
             tma_load_4d(sa, &tmA, &full[s], ci0, xA, yA, w.tc.b);
-            tma_load_2d(sbh, &tmBhi, &full[s], kb * 32, brow);
-            if (!no_blo) tma_load_2d(sbl, &tmBlo, &full[s], kb * 32, brow);
+            tma_load_2d(sa + kABytes, &tmBhi, &full[s], kb * 32, brow);
+            tma_load_2d(sa + kABytes + BBYTES, &tmBlo, &full[s], kb * 32, brow);
           }
         }
         __syncwarp();
@@ -258,17 +254,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   } else if (warp == 1) {
     // ===== MMA issuer: the whole warp walks the pipeline, one elected lane issues =====
     constexpr uint32_t idesc = idesc_tf32(kTileM, BN);
-    const bool no_x = (g.dbg & 4) != 0, no_blo = (g.dbg & 2) != 0, no_mma = (g.dbg & 8) != 0;
-    int s = 0;
+    const bool no_mma = (g.dbg & 8) != 0;
+    int s = 0, ab = 0;
     uint32_t ph = 0;
     int gcount = 0;  // main-buffer groups issued so far (all units)
     int li = 0;      // local unit index
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++li) {
       const Unit w = decode_unit(g, u);
-      const int xt = li & 1;
-      tw_wait(&xempty[xt], ((uint32_t)(li >> 1) & 1u) ^ 1u, prof, w_c);
+      tw_wait(xempty, ((uint32_t)li & 1u) ^ 1u, prof, w_c);
       tc_fence_after();
-      const uint32_t tx = tmem + (uint32_t)(2 * BN + xt * BN);
       uint32_t acc_x = 0;
       for (int kbg = w.kb0; kbg < w.kb1; kbg += kPromoteKB, ++gcount) {
         const int t = gcount & 1;
@@ -280,93 +274,82 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         for (int kb = kbg; kb < kbe; ++kb, ++n_kb) {
           tw_wait(&conv[s], ph, prof, w_a);
           tc_fence_after();
-          const uint32_t sa = smem_u32(smem + s * STAGE);
-          // descriptors of the stage's four operand tiles; a K step of 8 tf32 = 32 B = +2 in the
-          // descriptor's start-address field
-          const uint64_t d_ah = sdesc_sw128(sa), d_al = sdesc_sw128(sa + kABytes);
-          const uint64_t d_bh = sdesc_sw128(sa + 2 * kABytes), d_bl = sdesc_sw128(sa + 2 * kABytes + BBYTES);
+          const uint32_t sb = smem_u32(smem + s * STAGE) + kABytes;
+          const uint64_t d_bh = sdesc_sw128(sb), d_bl = sdesc_sw128(sb + BBYTES);
+          const uint32_t a_hi = tmem_a + (uint32_t)(64 * ab), a_lo = a_hi + 32;
           if (!no_mma) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-              const uint64_t o = 2u * k;
-              if (!no_x) {
-                mma_tf32_elect(tx, d_al + o, d_bh + o, idesc, acc_x);
-                if (!no_blo) mma_tf32_elect(tx, d_ah + o, d_bl + o, idesc, 1);
-              } else if (!acc_x) {
-                mma_tf32_elect(tx, d_al + o, d_bh + o, idesc, 0);
-              }
+              // K step of 8 tf32: +8 TMEM columns for A, +32 B (= +2) in the B descriptors
+              mma_tf32_ts_elect(tmem_x, a_lo + 8u * k, d_bh + 2u * k, idesc, acc_x);
               acc_x = 1;
-              mma_tf32_elect(tm, d_ah + o, d_bh + o, idesc, acc_m);
+              mma_tf32_ts_elect(tmem_x, a_hi + 8u * k, d_bl + 2u * k, idesc, 1);
+              mma_tf32_ts_elect(tm, a_hi + 8u * k, d_bh + 2u * k, idesc, acc_m);
               acc_m = 1;
             }
           }
           mma_commit_elect(&empty[s]);
+          mma_commit_elect(&afree[ab]);
           if (++s == STAGES) { s = 0; ph ^= 1; }
+          if (++ab == NA) ab = 0;
         }
         mma_commit_elect(&mfull[t]);
       }
     }
-  } else if (warp < kConvWarp0) {
-    // (12-warp layout) warps 2, 3: no role
-  } else if (warp < kConvWarp0 + 4) {
-    // ===== converters: A tile -> [centre] -> hi (in place) + lo =====
-#ifdef RTE_TC_WARPS12
-    reg_dealloc<120>();
-#endif
-    const int ct = threadIdx.x - 32 * kConvWarp0;  // 0..127
-    int s = 0;
+  } else if (warp < 6) {
+    // ===== converters (warps 2..5; warp w owns A rows / TMEM lanes 32*(w%4) .. +31) =====
+    const int r = 32 * (warp & 3) + lane;  // A tile row of this thread
+    const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
+    int s = 0, ab = 0, auses = 0;
     uint32_t ph = 0;
     int li = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++li) {
       const Unit w = decode_unit(g, u);
-      float* cv = cvec + (li & 1) * 128;
+      float c = 0.f;
       for (int kb = w.kb0; kb < w.kb1; ++kb, ++n_kb) {
         tw_wait(&full[s], ph, prof, w_a);
-        const uint32_t a_s = smem_u32(smem + s * STAGE);  // A tile (hi written in place)
-        const uint32_t al_s = a_s + kABytes;                // lo tile
+        tw_wait(&afree[ab], ((uint32_t)(auses / NA) & 1u) ^ 1u, prof, w_b);
+        tc_fence_after();
+        // row r of the raw A tile: 16-byte chunk q sits at chunk position q ^ (r & 7) (SW128)
+        const uint32_t row_s = smem_u32(smem + s * STAGE) + (uint32_t)r * 128u;
+        float hi[32], lo[32];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float4 v = lds128(row_s + (uint32_t)((q ^ (r & 7)) << 4));
+          hi[4 * q] = v.x;
+          hi[4 * q + 1] = v.y;
+          hi[4 * q + 2] = v.z;
+          hi[4 * q + 3] = v.w;
+        }
         if constexpr (Epi::kCenter) {
-          // row centre c_r = the row's first element (K index 0 of the unit's first K block);
-          // the GEMM then runs on a - c_r (see EpiApply)
+          // row centre c_r = the row's first element in the unit's first K block; the GEMM then
+          // runs on a - c_r (see EpiApply); published to the epilogue through cvec
           if (kb == w.kb0) {
+            c = hi[0];
             mbar_wait(&cempty[li & 1], ((uint32_t)(li >> 1) & 1u) ^ 1u);
-            cv[ct] = reinterpret_cast<const float*>(smem + s * STAGE)[ct * 32 + ((ct & 7) << 2)];
-            named_bar_sync(1, 128);
+            cvec[(li & 1) * 128 + r] = c;
             mbar_arrive(&cfull[li & 1]);
           }
         }
-        if (!(g.dbg & 1)) {
-          float4 v[kABytes / 16 / 128];
 #pragma unroll
-          for (int i = 0; i < kABytes / 16 / 128; ++i) v[i] = lds128(a_s + 16u * (ct + 128 * i));
-#pragma unroll
-          for (int i = 0; i < kABytes / 16 / 128; ++i) {
-            float4 x = v[i], h, l;
-            if constexpr (Epi::kCenter) {
-              const float c = cv[(ct + 128 * i) >> 3];
-              x.x -= c;
-              x.y -= c;
-              x.z -= c;
-              x.w -= c;
-            }
-            split_tf32_fast(x.x, h.x, l.x);
-            split_tf32_fast(x.y, h.y, l.y);
-            split_tf32_fast(x.z, h.z, l.z);
-            split_tf32_fast(x.w, h.w, l.w);
-            sts128(a_s + 16u * (ct + 128 * i), h);
-            sts128(al_s + 16u * (ct + 128 * i), l);
-          }
+        for (int e = 0; e < 32; ++e) {
+          const float x = Epi::kCenter ? hi[e] - c : hi[e];
+          split_tf32_fast(x, hi[e], lo[e]);
         }
-        fence_proxy_async_smem();
+        const uint32_t ta = tmem_a + (uint32_t)(64 * ab) + lane_base;
+        tmem_st32(ta, hi);
+        tmem_st32(ta + 32, lo);
+        tmem_wait_st();
+        tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&conv[s]);
         if (++s == STAGES) { s = 0; ph ^= 1; }
+        if (++ab == NA) ab = 0;
+        ++auses;
       }
     }
   } else {
-    // ===== promoters + epilogue (warp w owns TMEM lanes 32*(w%4) .. +31) =====
-#ifdef RTE_TC_WARPS12
-    reg_alloc<232>();
-#endif
+    // ===== promoters + epilogue (warps 6..9; warp w owns TMEM lanes 32*(w%4) .. +31) =====
     const int quarter = warp & 3;
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
     const int r = quarter * 32 + lane;  // tile row = TMEM lane
@@ -381,7 +364,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const int t = gcount & 1;
         tw_wait(&mfull[t], (uint32_t)(gcount >> 1) & 1u, prof, w_a);
         tc_fence_after();
-        const long long tl0 = prof ? clock64() : 0;
 #pragma unroll
         for (int c0 = 0; c0 < BN; c0 += 32) {
           float v[32];
@@ -389,79 +371,44 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
           for (int i = 0; i < 32; ++i) acc[c0 + i] += v[i];
         }
-        if (prof) w_b += clock64() - tl0;
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&mempty[t]);
       }
-      // the unit's last group commit covers every MMA of the unit, including its X buffer
-      const int xt = li & 1;
+      // the unit's last group commit covers every MMA of the unit, including the X buffer
 #pragma unroll
       for (int c0 = 0; c0 < BN; c0 += 32) {
         float v[32];
-        tmem_ld32(tmem + lane_base + (uint32_t)(2 * BN + xt * BN + c0), v);
+        tmem_ld32(tmem_x + lane_base + (uint32_t)c0, v);
 #pragma unroll
         for (int i = 0; i < 32; ++i) acc[c0 + i] += v[i];
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&xempty[xt]);
-      if constexpr (Epi::kCenter) mbar_wait(&cfull[xt], (uint32_t)(li >> 1) & 1u);
-#ifndef RTE_EPI_STAGED
+      if (lane == 0) mbar_arrive(xempty);
+      float crow = 0.f;
+      if constexpr (Epi::kCenter) {
+        mbar_wait(&cfull[li & 1], (uint32_t)(li >> 1) & 1u);
+        crow = cvec[(li & 1) * 128 + r];
+        mbar_arrive(&cempty[li & 1]);
+      }
       // Direct epilogue: thread r owns tile row r and writes its BN columns as float4s.
-      {
-        const int ly = r / g.TW, lx = r - ly * g.TW;
-        const int oy = w.tc.ty * g.TH + ly, ox = w.tc.tx * g.TW + lx;
-        if (r < rows && oy < g.Hc && ox < g.Wc && !(g.dbg & 32)) {
-          const typename Epi::Row row = epi.row(w.tc.b, w.tc.cls, oy, ox, Epi::kCenter ? cvec[xt * 128 + r] : 0.f);
+      const int ly = r / g.TW, lx = r - ly * g.TW;
+      const int oy = w.tc.ty * g.TH + ly, ox = w.tc.tx * g.TW + lx;
+      if (r < rows && oy < g.Hc && ox < g.Wc && !(g.dbg & 32)) {
+        const typename Epi::Row row = epi.row(w.tc.b, w.tc.cls, oy, ox, crow);
 #pragma unroll
-          for (int c = 0; c < BN; c += 4) {
-            const float4 v = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
-            if (g.nsplit > 1)
-              epi.store_partial4(w.split, row, w.n0 + c, v);
-            else
-              epi.store4(row, w.n0 + c, v);
-          }
+        for (int c = 0; c < BN; c += 4) {
+          const float4 v = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
+          if (g.nsplit > 1)
+            epi.store_partial4(w.split, row, w.n0 + c, v);
+          else
+            epi.store4(row, w.n0 + c, v);
         }
       }
-#else
-      // Coalesced epilogue: each 32-column chunk of the accumulator is staged through a shared tile
-      // (double-buffered, 16-byte chunks XOR-swizzled by row & 7: conflict-free both ways); then
-      // lane l of warp pw handles columns 4(l & 7) .. +3 of tile rows pw*32 + 4 it + (l >> 3), so
-      // each warp instruction moves four full 128-byte rows.
-      const int pw = warp - kPromWarp0;
-#pragma unroll
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        const uint32_t eb = etile + (uint32_t)(((c0 >> 5) & 1) * kTileM * 128);
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-          sts128(eb + (uint32_t)(r * 128 + ((k ^ (r & 7)) << 4)),
-                 make_float4(acc[c0 + 4 * k], acc[c0 + 4 * k + 1], acc[c0 + 4 * k + 2], acc[c0 + 4 * k + 3]));
-        named_bar_sync(2, 128);
-        if (!(g.dbg & 32)) {
-          const int k = lane & 7;
-#pragma unroll 2
-          for (int it = 0; it < 8; ++it) {
-            const int rr = pw * 32 + 4 * it + (lane >> 3);
-            const int ly = rr / g.TW, lx = rr - ly * g.TW;
-            const int oy = w.tc.ty * g.TH + ly, ox = w.tc.tx * g.TW + lx;
-            if (rr < rows && oy < g.Hc && ox < g.Wc) {
-              const float4 val = lds128(eb + (uint32_t)(rr * 128 + ((k ^ (rr & 7)) << 4)));
-              const typename Epi::Row row = epi.row(w.tc.b, w.tc.cls, oy, ox, Epi::kCenter ? cvec[xt * 128 + rr] : 0.f);
-              if (g.nsplit > 1)
-                epi.store_partial4(w.split, row, w.n0 + c0 + 4 * k, val);
-              else
-                epi.store4(row, w.n0 + c0 + 4 * k, val);
-            }
-          }
-        }
-      }
-      named_bar_sync(2, 128);  // staging buffers free before the next unit writes them
-#endif
-      if constexpr (Epi::kCenter) mbar_arrive(&cempty[xt]);
     }
   }
-  if (prof && (warp <= 1 || warp == kConvWarp0 || warp == kPromWarp0))
+  if (prof && (warp <= 2 || warp == 6))
     printf("tcprof BN=%d units=%d grid=%d warp=%d kb=%d total=%lld waitA=%lld waitB=%lld waitC=%lld\n", BN, units,
            gridDim.x, warp, n_kb, clock64() - t_start, w_a, w_b, w_c);
   tc_fence_before();
