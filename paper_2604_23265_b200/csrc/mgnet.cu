@@ -9,6 +9,9 @@
 // tcgen05 3xTF32 kernel (conv_tc.cu) takes the shapes it supports.
 #include <algorithm>
 #include <memory>
+#include <mutex>
+#include <set>
+#include <string>
 #include <vector>
 
 #include "common.h"
@@ -153,10 +156,18 @@ double conv_bytes(const ConvDesc& d, bool has_addend) {
   return 4.0 * (in + out * (has_addend ? 2.0 : 1.0) + wts);
 }
 const char* conv_class_name(const ConvDesc& d, bool tc) {
-  if (d.mode == 0 && d.ks == 1) return tc ? "conv1x1_tc" : "conv1x1_simt";
-  if (d.mode == 0) return tc ? "conv3x3_tc" : "conv3x3_simt";
-  if (d.mode == 1) return tc ? "conv3x3s2_tc" : "conv3x3s2_simt";
-  return tc ? "convT4x4s2_tc" : "convT4x4s2_simt";
+  const char* base;
+  if (d.mode == 0 && d.ks == 1) base = tc ? "conv1x1_tc" : "conv1x1_simt";
+  else if (d.mode == 0) base = tc ? "conv3x3_tc" : "conv3x3_simt";
+  else if (d.mode == 1) base = tc ? "conv3x3s2_tc" : "conv3x3s2_simt";
+  else base = tc ? "convT4x4s2_tc" : "convT4x4s2_simt";
+  // per-resolution class (e.g. conv3x3_tc@512x32->32), interned for the lifetime of the process
+  static std::mutex mu;
+  static std::set<std::string> names;
+  const std::string key = std::string(base) + "@" + std::to_string(d.Ho) + "x" + std::to_string(d.Ci) + "->" +
+                          std::to_string(d.Co);
+  std::lock_guard<std::mutex> lk(mu);
+  return names.insert(key).first->c_str();
 }
 
 void launch_conv(const ConvDesc& d, const float* in, const float* Wk, float* out, const float* addend, float sign,
