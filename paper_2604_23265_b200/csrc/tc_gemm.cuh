@@ -13,10 +13,10 @@
 // the 128 B/clk shared-memory port).  Each k-step issues lo.hi + hi.lo (cross-term accumulator)
 // and hi.hi (main accumulator).
 //
-// Warp roles (320 threads): warp 0 = TMA producer, warp 1 = TMEM allocator + MMA issuer (both walk
+// Warp roles (448 threads): warp 0 = TMA producer, warp 1 = TMEM allocator + MMA issuer (both walk
 // the pipeline warp-wide, one elected lane issues), warps 2..5 = A hi/lo converters (smem -> TMEM),
-// warps 6..9 = accumulator promotion and the epilogue (TMEM -> registers -> global); warp w
-// accesses TMEM lanes 32*(w%4) .. +31.  Pipelines:
+// warps 6..13 = accumulator promotion and the epilogue (TMEM -> registers -> global; two warps per
+// lane quarter, each owning half of the columns); warp w accesses TMEM lanes 32*(w%4) .. +31.  Pipelines:
 // full[s] (TMA bytes landed) -> conv[s] (hi/lo written) -> empty[s] (MMAs done, tcgen05.commit);
 // mfull[t] / mempty[t] hand the two main-accumulator TMEM buffers between MMA and promoters.
 #pragma once
@@ -29,7 +29,7 @@
 namespace rte {
 namespace tc {
 
-constexpr int kGemmThreads = 320;   // 10 warps (see kernel)
+constexpr int kGemmThreads = 448;   // 14 warps (see kernel)
 constexpr int kPromoteKB = 4;       // K blocks per TMEM accumulation group
 constexpr int kTileM = 128;
 constexpr int kABytes = kTileM * 128;   // 128 rows x 32 fp32
@@ -72,11 +72,22 @@ constexpr int gemm_stages() {
   return Smem<BN>::kStage * 6 <= 192 * 1024 ? 6 : (192 * 1024) / Smem<BN>::kStage;
 }
 
-// TMEM columns: main accumulators M0, M1 [0, 2BN), cross-term accumulator X [2BN, 3BN), then
-// kABufs A buffers of 64 columns (hi: 32 K columns, lo: 32 K columns).
+// TMEM layout.  Fused form (BN <= 64): two group buffers t = 0, 1 of 2BN columns [main_t | X_t];
+// one MMA hi.[B_hi; B_lo] (N = 2BN) writes both halves and lo.B_hi (N = BN) adds into X_t, so a
+// k-step costs 2 MMAs; both halves are promoted per group.  Split form (BN = 128): main buffers
+// M0, M1 [0, 2BN) and a unit-long cross-term accumulator X [2BN, 3BN), 3 MMAs per k-step.  Then
+// the A buffers, 64 columns each (hi: 32 K columns, lo: 32 K columns).
+template <int BN>
+constexpr bool tmem_fused() {
+  return BN <= 64;
+}
+template <int BN>
+constexpr int tmem_acc_cols() {
+  return tmem_fused<BN>() ? 4 * BN : 3 * BN;
+}
 template <int BN>
 constexpr int tmem_abufs() {
-  return (512 - 3 * BN) / 64 < 6 ? (512 - 3 * BN) / 64 : 6;
+  return (512 - tmem_acc_cols<BN>()) / 64 < 6 ? (512 - tmem_acc_cols<BN>()) / 64 : 6;
 }
 
 template <int BN>
@@ -204,11 +215,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     for (int a = 0; a < NA; ++a) mbar_init(&afree[a], 1);
     for (int t = 0; t < 2; ++t) {
       mbar_init(&mfull[t], 1);
-      mbar_init(&mempty[t], 4);
+      mbar_init(&mempty[t], 8);
       mbar_init(&cfull[t], 128);
-      mbar_init(&cempty[t], 128);
+      mbar_init(&cempty[t], 256);
     }
-    mbar_init(xempty, 4);
+    mbar_init(xempty, 8);
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
@@ -221,8 +232,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tmem_x = tmem + 2 * BN;
-  const uint32_t tmem_a = tmem + 3 * BN;
+  constexpr bool FUSED = tmem_fused<BN>();
+  const uint32_t tmem_x = tmem + 2 * BN;  // split form only
+  const uint32_t tmem_a = tmem + tmem_acc_cols<BN>();
 
   if (warp == 0) {
     // ===== TMA producer: the whole warp walks the pipeline, one elected lane issues =====
@@ -278,14 +290,26 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           const uint64_t d_bh = sdesc_sw128(sb), d_bl = sdesc_sw128(sb + BBYTES);
           const uint32_t a_hi = tmem_a + (uint32_t)(64 * ab), a_lo = a_hi + 32;
           if (!no_mma) {
+            if constexpr (FUSED) {
+              // hi.[B_hi; B_lo] -> [main_t | X_t] (N = 2BN), lo.B_hi -> X_t
+              constexpr uint32_t idesc2 = idesc_tf32(kTileM, 2 * BN);
+              const uint32_t tbuf = tmem + (uint32_t)(t * 2 * BN);
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              // K step of 8 tf32: +8 TMEM columns for A, +32 B (= +2) in the B descriptors
-              mma_tf32_ts_elect(tmem_x, a_lo + 8u * k, d_bh + 2u * k, idesc, acc_x);
-              acc_x = 1;
-              mma_tf32_ts_elect(tmem_x, a_hi + 8u * k, d_bl + 2u * k, idesc, 1);
-              mma_tf32_ts_elect(tm, a_hi + 8u * k, d_bh + 2u * k, idesc, acc_m);
-              acc_m = 1;
+              for (int k = 0; k < 4; ++k) {
+                mma_tf32_ts_elect(tbuf, a_hi + 8u * k, d_bh + 2u * k, idesc2, acc_m);
+                acc_m = 1;
+                mma_tf32_ts_elect(tbuf + BN, a_lo + 8u * k, d_bh + 2u * k, idesc, 1);
+              }
+            } else {
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                // K step of 8 tf32: +8 TMEM columns for A, +32 B (= +2) in the B descriptors
+                mma_tf32_ts_elect(tmem_x, a_lo + 8u * k, d_bh + 2u * k, idesc, acc_x);
+                acc_x = 1;
+                mma_tf32_ts_elect(tmem_x, a_hi + 8u * k, d_bl + 2u * k, idesc, 1);
+                mma_tf32_ts_elect(tm, a_hi + 8u * k, d_bh + 2u * k, idesc, acc_m);
+                acc_m = 1;
+              }
             }
           }
           mma_commit_elect(&empty[s]);
@@ -349,39 +373,53 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
     }
   } else {
-    // ===== promoters + epilogue (warps 6..9; warp w owns TMEM lanes 32*(w%4) .. +31) =====
+    // ===== promoters + epilogue (warps 6..13): warp w owns TMEM lanes 32*(w%4) .. +31 and the
+    // column half h = (w - 6) / 4 of the tile (two warps per lane quarter double the epilogue's
+    // memory-level parallelism) =====
+    constexpr int HB = BN / 2;  // columns per promoter warp
     const int quarter = warp & 3;
+    const int half = (warp - 6) >> 2;
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
     const int r = quarter * 32 + lane;  // tile row = TMEM lane
+    const int cbase = half * HB;
     int gcount = 0;
     int li = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++li) {
       const Unit w = decode_unit(g, u);
-      float acc[BN];
+      float acc[HB];
 #pragma unroll
-      for (int i = 0; i < BN; ++i) acc[i] = 0.f;
+      for (int i = 0; i < HB; ++i) acc[i] = 0.f;
       for (int kbg = w.kb0; kbg < w.kb1; kbg += kPromoteKB, ++gcount) {
         const int t = gcount & 1;
         tw_wait(&mfull[t], (uint32_t)(gcount >> 1) & 1u, prof, w_a);
         tc_fence_after();
+        // fused form: main_t at t*2BN, X_t at t*2BN + BN; split form: main_t at t*BN
+        const uint32_t mcol = FUSED ? (uint32_t)(t * 2 * BN) : (uint32_t)(t * BN);
 #pragma unroll
-        for (int c0 = 0; c0 < BN; c0 += 32) {
-          float v[32];
-          tmem_ld32(tmem + lane_base + (uint32_t)(t * BN + c0), v);
+        for (int c0 = 0; c0 < HB; c0 += 16) {
+          float v[16];
+          tmem_ld16(tmem + lane_base + mcol + (uint32_t)(cbase + c0), v);
 #pragma unroll
-          for (int i = 0; i < 32; ++i) acc[c0 + i] += v[i];
+          for (int i = 0; i < 16; ++i) acc[c0 + i] += v[i];
+          if constexpr (FUSED) {
+            tmem_ld16(tmem + lane_base + mcol + (uint32_t)(BN + cbase + c0), v);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) acc[c0 + i] += v[i];
+          }
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&mempty[t]);
       }
-      // the unit's last group commit covers every MMA of the unit, including the X buffer
+      if constexpr (!FUSED) {
+        // the unit's last group commit covers every MMA of the unit, including the X buffer
 #pragma unroll
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        float v[32];
-        tmem_ld32(tmem_x + lane_base + (uint32_t)c0, v);
+        for (int c0 = 0; c0 < HB; c0 += 16) {
+          float v[16];
+          tmem_ld16(tmem_x + lane_base + (uint32_t)(cbase + c0), v);
 #pragma unroll
-        for (int i = 0; i < 32; ++i) acc[c0 + i] += v[i];
+          for (int i = 0; i < 16; ++i) acc[c0 + i] += v[i];
+        }
       }
       tc_fence_before();
       __syncwarp();
@@ -392,18 +430,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         crow = cvec[(li & 1) * 128 + r];
         mbar_arrive(&cempty[li & 1]);
       }
-      // Direct epilogue: thread r owns tile row r and writes its BN columns as float4s.
+      // Direct epilogue: thread r writes tile row r, columns cbase .. cbase + HB, as float4s.
       const int ly = r / g.TW, lx = r - ly * g.TW;
       const int oy = w.tc.ty * g.TH + ly, ox = w.tc.tx * g.TW + lx;
       if (r < rows && oy < g.Hc && ox < g.Wc && !(g.dbg & 32)) {
         const typename Epi::Row row = epi.row(w.tc.b, w.tc.cls, oy, ox, crow);
 #pragma unroll
-        for (int c = 0; c < BN; c += 4) {
+        for (int c = 0; c < HB; c += 4) {
           const float4 v = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
           if (g.nsplit > 1)
-            epi.store_partial4(w.split, row, w.n0 + c, v);
+            epi.store_partial4(w.split, row, w.n0 + cbase + c, v);
           else
-            epi.store4(row, w.n0 + c, v);
+            epi.store4(row, w.n0 + cbase + c, v);
         }
       }
     }
