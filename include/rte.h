@@ -126,6 +126,12 @@ void mgnet_destroy(mgnet_net* net);
 rte_status mgnet_vcycle(const mgnet_net* net, const float* r_dev, float* z_dev,
                         int add_identity, void* stream);
 
+/* The same V-cycle entirely in float64 (SIMT kernels; fp64 weight copies and activation buffers are
+ * created on first use).  Used by gmres_solve(precision=1) and as the fp64 parity reference of the
+ * V-cycle's data flow.  r_dev, z_dev float64 [n]. */
+rte_status mgnet_vcycle_f64(const mgnet_net* net, const double* r_dev, double* z_dev, int add_identity,
+                            void* stream);
+
 /* Restarted right-preconditioned GMRES(m) (R21, R22).
  * Preconditioner P = I + V (precond=1, requires net) or P = I (precond=0).
  * Iterate x is float64; the Krylov basis is float32 (precision=0) or float64 (precision=1); dot
@@ -138,10 +144,10 @@ typedef struct {
   int precond;       /* 0 none, 1 MgNet (I + V) */
   int reorth;        /* 0 = CGS2: two classical Gram-Schmidt passes (default); 1 = one CGS pass;
                         2 = selective (DGKS): the second pass runs only when ||v'|| < ||w||/sqrt(2) */
-  int precision;     /* 0 = mixed (default): float32 Krylov basis and operator apply, float64 iterate,
-                        reductions and restart residual;  1 = float64 basis and float64 apply (the
-                        fp32 V-cycle acts on a rounded copy and its correction is added in float64):
-                        ~2x the Arnoldi bytes, for tight tolerances and iteration-count parity */
+  int precision;     /* 0 = mixed (default): float32 Krylov basis, operator apply and V-cycle, float64
+                        iterate, reductions and restart residual;  1 = everything in float64 (basis,
+                        apply, V-cycle on SIMT kernels): for tight tolerances and iteration-count
+                        parity with an fp64 reference; not the fast path */
 } gmres_opts;
 
 typedef struct {

@@ -16,7 +16,7 @@ from . import _lib
 from ._lib import RteError, check, gmres_opts, gmres_report, lib
 
 __all__ = ["Problem", "MgNet", "rte_setup", "rte_rhs", "rte_apply", "rte_apply_f64", "mgnet_create",
-           "mgnet_vcycle", "gmres_solve", "rte_quadrature", "rte_hg_matrix", "rte_launch_count", "rte_timing_enable", "rte_timing_reset",
+           "mgnet_vcycle", "mgnet_vcycle_f64", "gmres_solve", "rte_quadrature", "rte_hg_matrix", "rte_launch_count", "rte_timing_enable", "rte_timing_reset",
            "rte_timing_get", "RteError", "LIB_PATH"]
 
 LIB_PATH = _lib.LIB_PATH
@@ -170,6 +170,11 @@ def mgnet_create(p: Problem, levels: int, c0: int, nu: int, weights) -> MgNet:
 def mgnet_vcycle(net: MgNet, r, z, add_identity: bool = True, stream=None) -> None:
     check("mgnet_vcycle", lib.mgnet_vcycle(net.handle, _dev(r, "f32"), _dev(z, "f32"), int(add_identity),
                                            C.c_void_p(_stream(stream))))
+
+
+def mgnet_vcycle_f64(net: MgNet, r, z, add_identity: bool = True, stream=None) -> None:
+    check("mgnet_vcycle_f64", lib.mgnet_vcycle_f64(net.handle, _dev(r, "f64"), _dev(z, "f64"), int(add_identity),
+                                                   C.c_void_p(_stream(stream))))
 
 
 def gmres_solve(p: Problem, net: Optional[MgNet], b, x, *, restart: int = 30, maxit: int = 1000,

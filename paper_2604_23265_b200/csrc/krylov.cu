@@ -157,20 +157,47 @@ __global__ void __launch_bounds__(kThreads) norm_kernel(const T* __restrict__ x,
   reduce_finalize<1>(acc, ra, b, nullptr, 0);
 }
 
-// dst = sum_{i < k_b} coef_i V_i   (coef already includes alpha), fp64 accumulation.
+// dst = sum_{i < k_b} coef_i V_i   (coef already includes alpha), fp64 accumulation; 16-byte
+// vector loads of every basis column (the k_b columns stream once at HBM rate).
 template <typename T, typename TO>
 __global__ void __launch_bounds__(kThreads) combine_kernel(const T* __restrict__ V, int64_t vld,
                                                             const double* __restrict__ coef, int coef_ld,
                                                             const int* __restrict__ kcols, TO* __restrict__ dst,
                                                             int64_t ns, int nblk) {
+  using VT = typename Vec16<T>::type;
+  constexpr int W = (int)(sizeof(VT) / sizeof(T));
   const int b = blockIdx.y;
   const int k = kcols[b];
-  const double* cb = coef + (int64_t)b * coef_ld;
+  __shared__ double cs[kMaxRestart + 1];
+  for (int i = threadIdx.x; i < k; i += blockDim.x) cs[i] = coef[(int64_t)b * coef_ld + i];
+  __syncthreads();
   const T* Vb = V + (int64_t)b * ns;
-  for (int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x; e < ns; e += (int64_t)nblk * kThreads) {
-    double s = 0.0;
-    for (int i = 0; i < k; ++i) s += cb[i] * (double)Vb[(int64_t)i * vld + e];
-    dst[(int64_t)b * ns + e] = (TO)s;
+  const int64_t nv = ns / W;
+  for (int64_t q = (int64_t)blockIdx.x * kThreads + threadIdx.x; q < nv; q += (int64_t)nblk * kThreads) {
+    double acc[W];
+#pragma unroll
+    for (int e = 0; e < W; ++e) acc[e] = 0.0;
+    int i = 0;
+    for (; i + 4 <= k; i += 4) {  // four columns in flight per thread
+      VT v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = reinterpret_cast<const VT*>(Vb + (int64_t)(i + u) * vld)[q];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const T* x = reinterpret_cast<const T*>(&v[u]);
+#pragma unroll
+        for (int e = 0; e < W; ++e) acc[e] += cs[i + u] * (double)x[e];
+      }
+    }
+    for (; i < k; ++i) {
+      const VT v = reinterpret_cast<const VT*>(Vb + (int64_t)i * vld)[q];
+      const T* x = reinterpret_cast<const T*>(&v);
+#pragma unroll
+      for (int e = 0; e < W; ++e) acc[e] += cs[i] * (double)x[e];
+    }
+    TO* d = dst + (int64_t)b * ns + q * W;
+#pragma unroll
+    for (int e = 0; e < W; ++e) d[e] = (TO)acc[e];
   }
 }
 
@@ -558,19 +585,19 @@ extern "C" rte_status gmres_solve(const rte_problem* p, const mgnet_net* net, co
           }
         };
         if (f64) {
-          // fp64 basis: z = alpha_j V_j (+ V(z) from the fp32 V-cycle), w = A z in fp64
+          // fp64 basis: z = P(alpha_j V_j) with the fp64 V-cycle, w = A z in fp64 (W.r64 is free
+          // inside a cycle and holds P z)
           const double* vj = W.V64 + (size_t)j * n;
           prof_begin(st);
-          scale_f64_kernel<<<dim3(W.nblk, B), kThreads, 0, st>>>(vj, W.alpha + j, m + 1, W.z64,
-                                                                  opts->precond == 1 ? W.z : nullptr, W.ns, W.nblk);
-          after_launch("scale_f64", st, 0.0, 20.0 * (double)n, 0);
+          scale_f64_kernel<<<dim3(W.nblk, B), kThreads, 0, st>>>(vj, W.alpha + j, m + 1, W.z64, nullptr, W.ns,
+                                                                  W.nblk);
+          after_launch("scale_f64", st, 0.0, 16.0 * (double)n, 0);
+          const double* zin = W.z64;
           if (opts->precond == 1) {
-            vcycle_run(net, W.z, W.q32, false, nullptr, 0, st);
-            prof_begin(st);
-            add_f32_to_f64_kernel<<<W.nblk * B, kThreads, 0, st>>>(W.z64, W.q32, nullptr, n);
-            after_launch("add_f32_to_f64", st, 0.0, 20.0 * (double)n, 0);
+            vcycle_run_f64(net, W.z64, W.r64, true, st);
+            zin = W.r64;
           }
-          launch_apply_f64(p, W.z64, W.w64, nullptr, st);
+          launch_apply_f64(p, zin, W.w64, nullptr, st);
           cgs_passes(W.V64, W.w64);
         } else {
           // fp32 basis: z = P(alpha_j V_j) or alpha_j V_j, w = A z in fp32
@@ -621,16 +648,13 @@ extern "C" rte_status gmres_solve(const rte_problem* p, const mgnet_net* net, co
         combine_kernel<double, double><<<dim3(W.nblk, B), kThreads, 0, st>>>(W.V64, n, W.coef, m + 1, W.kcols, W.z64,
                                                                               W.ns, W.nblk);
         after_launch("combine", st, 2.0 * m * (double)n, 8.0 * (double)n * (m + 1), 0);
-        const float* q = nullptr;
+        const double* corr = W.z64;
         if (opts->precond == 1) {
-          prof_begin(st);
-          add_f32_to_f64_kernel<<<W.nblk * B, kThreads, 0, st>>>(W.z64, nullptr, W.z, n);  // z32 = (float) z64
-          after_launch("add_f32_to_f64", st, 0.0, 12.0 * (double)n, 0);
-          vcycle_run(net, W.z, W.q32, false, nullptr, 0, st);
-          q = W.q32;
+          vcycle_run_f64(net, W.z64, W.r64, true, st);
+          corr = W.r64;
         }
         prof_begin(st);
-        axpy64_kernel<double><<<dim3(W.nblk, B), kThreads, 0, st>>>(x_dev, W.z64, q, W.kcols, W.ns, W.nblk);
+        axpy64_kernel<double><<<dim3(W.nblk, B), kThreads, 0, st>>>(x_dev, corr, nullptr, W.kcols, W.ns, W.nblk);
         after_launch("axpy64", st, (double)n, 28.0 * (double)n, 0);
       } else {
         prof_begin(st);

@@ -12,6 +12,7 @@
 #include <mutex>
 #include <set>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "common.h"
@@ -23,17 +24,17 @@ namespace {
 // MODE 0: KSxKS conv, stride 1, pad KS/2.  MODE 1: 3x3 conv, stride 2, pad 1.
 // MODE 2: 4x4 transposed conv, stride 2, pad 1, one output parity class per blockIdx.z % 4.
 // out = (addend ? add_scale*addend : 0) + sign * in_scale * acc
-template <int MODE, int KS, int TCO>
+template <typename T, int MODE, int KS, int TCO>
 __global__ void __launch_bounds__(256) conv_simt_kernel(
-    int Hi, int Wi, int Ci, int Ho, int Wo, int Co, const float* __restrict__ in, const float* __restrict__ Wk,
-    float* out, const float* addend, float sign, const double* __restrict__ alpha, int alpha_stride,
+    int Hi, int Wi, int Ci, int Ho, int Wo, int Co, const T* __restrict__ in, const T* __restrict__ Wk,
+    T* out, const T* addend, float sign, const double* __restrict__ alpha, int alpha_stride,
     int alpha_on_input, int alpha_on_addend) {
   constexpr int TP = 4096 / TCO;
   constexpr int KC = 16;
   constexpr int TX = TCO / 4;
   constexpr int NTAPS = (MODE == 2) ? 4 : KS * KS;
-  __shared__ __align__(16) float As[KC][TP + 4];
-  __shared__ __align__(16) float Bs[KC][TCO + 4];
+  __shared__ __align__(16) T As[KC][TP + 4];
+  __shared__ __align__(16) T Bs[KC][TCO + 4];
   const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
   int bz = blockIdx.z;
   int py = 0, px = 0;
@@ -50,12 +51,12 @@ __global__ void __launch_bounds__(256) conv_simt_kernel(
   const int64_t npix = (int64_t)Hc * Wc;
   const int64_t p0 = (int64_t)blockIdx.x * TP;
   const int co0 = blockIdx.y * TCO;
-  const float* inb = in + (int64_t)b * Hi * Wi * Ci;
-  float acc[4][4];
+  const T* inb = in + (int64_t)b * Hi * Wi * Ci;
+  T acc[4][4];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int c = 0; c < 4; ++c) acc[a][c] = 0.f;
+    for (int c = 0; c < 4; ++c) acc[a][c] = T(0);
 
   for (int tap = 0; tap < NTAPS; ++tap) {
     int ky, kx;
@@ -71,7 +72,7 @@ __global__ void __launch_bounds__(256) conv_simt_kernel(
       for (int e = tid; e < TP * KC; e += 256) {
         int pl = e / KC, kk = e % KC;
         int64_t p = p0 + pl;
-        float v = 0.f;
+        T v = T(0);
         if (p < npix && ci0 + kk < Ci) {
           int yo = (int)(p / Wc), xo = (int)(p % Wc);
           int yi, xi;
@@ -95,14 +96,14 @@ __global__ void __launch_bounds__(256) conv_simt_kernel(
       }
       for (int e = tid; e < KC * TCO; e += 256) {
         int kk = e / TCO, o = e % TCO;
-        float v = 0.f;
+        T v = T(0);
         if (ci0 + kk < Ci && co0 + o < Co) v = Wk[((int64_t)wtap * Ci + ci0 + kk) * Co + co0 + o];
         Bs[kk][o] = v;
       }
       __syncthreads();
 #pragma unroll
       for (int kk = 0; kk < KC; ++kk) {
-        float av[4], bv[4];
+        T av[4], bv[4];
 #pragma unroll
         for (int a = 0; a < 4; ++a) av[a] = As[kk][ty * 4 + a];
 #pragma unroll
@@ -110,14 +111,14 @@ __global__ void __launch_bounds__(256) conv_simt_kernel(
 #pragma unroll
         for (int a = 0; a < 4; ++a)
 #pragma unroll
-          for (int c = 0; c < 4; ++c) acc[a][c] = fmaf(av[a], bv[c], acc[a][c]);
+          for (int c = 0; c < 4; ++c) acc[a][c] = fma(av[a], bv[c], acc[a][c]);
       }
       __syncthreads();
     }
   }
-  const float al = alpha ? alpha[(int64_t)b * alpha_stride] : 1.f;
-  const float s_in = (alpha_on_input ? al : 1.f) * sign;
-  const float s_add = alpha_on_addend ? al : 1.f;
+  const T al = alpha ? (T)alpha[(int64_t)b * alpha_stride] : T(1);
+  const T s_in = (alpha_on_input ? al : T(1)) * (T)sign;
+  const T s_add = alpha_on_addend ? al : T(1);
 #pragma unroll
   for (int a = 0; a < 4; ++a) {
     int64_t p = p0 + ty * 4 + a;
@@ -134,7 +135,7 @@ __global__ void __launch_bounds__(256) conv_simt_kernel(
     for (int c = 0; c < 4; ++c) {
       int co = co0 + tx * 4 + c;
       if (co >= Co) continue;
-      float v = s_in * acc[a][c];
+      T v = s_in * acc[a][c];
       if (addend) v += s_add * addend[base + co];
       out[base + co] = v;
     }
@@ -170,10 +171,13 @@ const char* conv_class_name(const ConvDesc& d, bool tc) {
   return names.insert(key).first->c_str();
 }
 
-void launch_conv(const ConvDesc& d, const float* in, const float* Wk, float* out, const float* addend, float sign,
-                 const double* alpha, int alpha_stride, bool alpha_on_input, bool alpha_on_addend,
-                 cudaStream_t st) {
-  if (conv_tc_try(d, in, out, addend, sign, alpha, alpha_stride, alpha_on_input, alpha_on_addend, st)) return;
+template <typename T>
+void launch_conv_t(const ConvDesc& d, const T* in, const T* Wk, T* out, const T* addend, float sign,
+                   const double* alpha, int alpha_stride, bool alpha_on_input, bool alpha_on_addend,
+                   cudaStream_t st) {
+  if constexpr (std::is_same<T, float>::value) {
+    if (conv_tc_try(d, in, out, addend, sign, alpha, alpha_stride, alpha_on_input, alpha_on_addend, st)) return;
+  }
   prof_begin(st);
   auto go = [&](auto mode_tag, auto ks_tag, auto tco_tag) {
     constexpr int MODE = decltype(mode_tag)::value;
@@ -183,7 +187,7 @@ void launch_conv(const ConvDesc& d, const float* in, const float* Wk, float* out
     int64_t npix = (MODE == 2) ? (int64_t)(d.Ho / 2) * (d.Wo / 2) : (int64_t)d.Ho * d.Wo;
     dim3 grid((unsigned)((npix + TP - 1) / TP), (unsigned)((d.Co + TCO - 1) / TCO),
               (unsigned)(d.B * (MODE == 2 ? 4 : 1)));
-    conv_simt_kernel<MODE, KS, TCO><<<grid, 256, 0, st>>>(d.Hi, d.Wi, d.Ci, d.Ho, d.Wo, d.Co, in, Wk, out, addend,
+    conv_simt_kernel<T, MODE, KS, TCO><<<grid, 256, 0, st>>>(d.Hi, d.Wi, d.Ci, d.Ho, d.Wo, d.Co, in, Wk, out, addend,
                                                           sign, alpha, alpha_stride, alpha_on_input ? 1 : 0,
                                                           alpha_on_addend ? 1 : 0);
   };
@@ -202,7 +206,13 @@ void launch_conv(const ConvDesc& d, const float* in, const float* Wk, float* out
   else if (d.mode == 0) by_tco(I0{}, K3{});
   else if (d.mode == 1) by_tco(I1{}, K3{});
   else by_tco(I2{}, K4{});
-  after_launch(conv_class_name(d, false), st, conv_flops(d), conv_bytes(d, addend != nullptr), 2);
+  after_launch(conv_class_name(d, false), st, conv_flops(d), conv_bytes(d, addend != nullptr) * (sizeof(T) / 4),
+               sizeof(T) == 8 ? 3 : 2);
+}
+
+void launch_conv(const ConvDesc& d, const float* in, const float* Wk, float* out, const float* addend, float sign,
+                 const double* alpha, int alpha_stride, bool alpha_on_input, bool alpha_on_addend, cudaStream_t st) {
+  launch_conv_t<float>(d, in, Wk, out, addend, sign, alpha, alpha_stride, alpha_on_input, alpha_on_addend, st);
 }
 
 }  // namespace rte
@@ -241,6 +251,8 @@ void ConvW::build(const float* w, int kind_, int Co_, int Ci_, int ks_) {
 
 void ConvW::release() {
   dfree(d_kn);
+  dfree(d_kn64);
+  d_kn64 = nullptr;
   dfree(d_hi);
   dfree(d_lo);
   d_kn = d_hi = d_lo = nullptr;
@@ -258,6 +270,9 @@ void mgnet_destroy(mgnet_net* net) {
     dfree(lv.f);
     dfree(lv.u);
     dfree(lv.t);
+    dfree(lv.f64);
+    dfree(lv.u64);
+    dfree(lv.t64);
   }
   delete net;
 }
@@ -340,6 +355,18 @@ rte_status mgnet_vcycle(const mgnet_net* net, const float* r_dev, float* z_dev, 
   }
 }
 
+rte_status mgnet_vcycle_f64(const mgnet_net* net, const double* r_dev, double* z_dev, int add_identity,
+                            void* stream) {
+  try {
+    RTE_REQUIRE(net && r_dev && z_dev, "mgnet_vcycle_f64: NULL argument");
+    RTE_REQUIRE((const void*)r_dev != (const void*)z_dev, "mgnet_vcycle_f64: r and z must not alias");
+    vcycle_run_f64(net, r_dev, z_dev, add_identity != 0, as_stream(stream));
+    return RTE_OK;
+  } catch (const Fail& f) {
+    return f.st;
+  }
+}
+
 }  // extern "C"
 
 namespace rte {
@@ -358,56 +385,117 @@ static ConvDesc desc_for(const mgnet_net* n, int mode, int ks, int H_in, int Ci,
 
 // One V-cycle.  alpha (device, per sample, stride alpha_stride) scales the input r (the
 // Krylov vector is stored unnormalised, see krylov.cu); NULL means 1.
-void vcycle_run(const mgnet_net* net, const float* r, float* z, bool add_identity, const double* alpha,
-                int alpha_stride, cudaStream_t st) {
+// Activation buffers of level l in the element type T (fp64 buffers are allocated on first use).
+template <typename T>
+static void level_bufs(const mgnet_net* net, int l, T*& f, T*& u, T*& t);
+template <>
+void level_bufs<float>(const mgnet_net* net, int l, float*& f, float*& u, float*& t) {
+  const Level& V = net->lv[l];
+  f = V.f;
+  u = V.u;
+  t = V.t;
+}
+template <>
+void level_bufs<double>(const mgnet_net* net, int l, double*& f, double*& u, double*& t) {
+  Level& V = const_cast<mgnet_net*>(net)->lv[l];
+  if (!V.f64) {
+    const size_t act = (size_t)net->B * V.H * V.H * V.C;
+    V.f64 = dalloc<double>(act);
+    V.u64 = dalloc<double>(act);
+    V.t64 = dalloc<double>(act);
+  }
+  f = V.f64;
+  u = V.u64;
+  t = V.t64;
+}
+template <typename T>
+static const T* conv_weights(const mgnet_net* net, int widx);
+template <>
+const float* conv_weights<float>(const mgnet_net* net, int widx) {
+  return net->convs[widx].d_kn;
+}
+template <>
+const double* conv_weights<double>(const mgnet_net* net, int widx) {
+  ConvW& w = const_cast<mgnet_net*>(net)->convs[widx];
+  if (!w.d_kn64) {  // [tap][ci][co] in fp64, from the host copy [co][tap][ci]
+    std::vector<double> kn((size_t)w.taps * w.Ci * w.Co);
+    for (int co = 0; co < w.Co; ++co)
+      for (int tap = 0; tap < w.taps; ++tap)
+        for (int ci = 0; ci < w.Ci; ++ci)
+          kn[((size_t)tap * w.Ci + ci) * w.Co + co] = (double)w.host_nk[((size_t)co * w.taps + tap) * w.Ci + ci];
+    w.d_kn64 = dalloc<double>(kn.size());
+    upload(w.d_kn64, kn.data(), kn.size());
+  }
+  return w.d_kn64;
+}
+
+// One V-cycle in element type T (float: tensor-core convs where the shape allows, else SIMT;
+// double: SIMT fp64).  alpha (device, per sample, stride alpha_stride) scales the input r.
+template <typename T>
+void vcycle_run_t(const mgnet_net* net, const T* r, T* z, bool add_identity, const double* alpha,
+                  int alpha_stride, cudaStream_t st) {
   const int L = net->L, M = net->M, N = net->N;
-  auto conv = [&](int widx, ConvDesc d, const float* in, float* out, const float* addend, float sign,
-                  bool a_in = false, bool a_add = false) {
+  auto conv = [&](int widx, ConvDesc d, const T* in, T* out, const T* addend, float sign, bool a_in = false,
+                  bool a_add = false) {
     d.w = &net->convs[widx];
     d.ws_owner = net;
-    launch_conv(d, in, net->convs[widx].d_kn, out, addend, sign, alpha, alpha_stride, a_in, a_add, st);
+    launch_conv_t<T>(d, in, conv_weights<T>(net, widx), out, addend, sign, alpha, alpha_stride, a_in, a_add, st);
   };
+  struct Bufs {
+    T *f, *u, *t;
+  };
+  std::vector<Bufs> bf(L);
+  for (int l = 0; l < L; ++l) level_bufs<T>(net, l, bf[l].f, bf[l].u, bf[l].t);
   // f^0 = Lambda (alpha r)
   {
     const Level& L0 = net->lv[0];
-    conv(net->lift, desc_for(net, 0, 1, N, M, N, L0.C), r, L0.f, nullptr, 1.f, true, false);
+    conv(net->lift, desc_for(net, 0, 1, N, M, N, L0.C), r, bf[0].f, nullptr, 1.f, true, false);
   }
   auto smooth = [&](int l, int bidx, bool first) {
     const Level& V = net->lv[l];
     ConvDesc d = desc_for(net, 0, 3, V.H, V.C, V.H, V.C);
+    const Bufs& b = bf[l];
     if (first) {  // u = 0: u <- B * f  (A * 0 = 0 exactly)
-      conv(bidx, d, V.f, V.u, nullptr, 1.f);
+      conv(bidx, d, b.f, b.u, nullptr, 1.f);
     } else {
-      conv(V.A, d, V.u, V.t, V.f, -1.f);   // t = f - A * u
-      conv(bidx, d, V.t, V.u, V.u, 1.f);   // u = u + B * t
+      conv(V.A, d, b.u, b.t, b.f, -1.f);   // t = f - A * u
+      conv(bidx, d, b.t, b.u, b.u, 1.f);   // u = u + B * t
     }
   };
   for (int l = 0; l < L; ++l) {
     const Level& V = net->lv[l];
     std::vector<int> steps(V.Bpre.begin(), V.Bpre.end());
     if (l == L - 1) steps.insert(steps.end(), V.Bpost.begin(), V.Bpost.end());
-    if (steps.empty()) RTE_CHECK_CUDA(cudaMemsetAsync(V.u, 0, sizeof(float) * (size_t)net->B * V.H * V.H * V.C, st));
+    if (steps.empty()) RTE_CHECK_CUDA(cudaMemsetAsync(bf[l].u, 0, sizeof(T) * (size_t)net->B * V.H * V.H * V.C, st));
     for (size_t i = 0; i < steps.size(); ++i) smooth(l, steps[i], i == 0);
     if (l < L - 1) {
       const Level& W = net->lv[l + 1];
       ConvDesc d = desc_for(net, 0, 3, V.H, V.C, V.H, V.C);
       if (steps.empty()) {
-        conv(V.R, desc_for(net, 1, 3, V.H, V.C, W.H, W.C), V.f, W.f, nullptr, 1.f);
+        conv(V.R, desc_for(net, 1, 3, V.H, V.C, W.H, W.C), bf[l].f, bf[l + 1].f, nullptr, 1.f);
       } else {
-        conv(V.A, d, V.u, V.t, V.f, -1.f);                                          // t = f - A * u
-        conv(V.R, desc_for(net, 1, 3, V.H, V.C, W.H, W.C), V.t, W.f, nullptr, 1.f);  // f^{l+1} = R *_2 t
+        conv(V.A, d, bf[l].u, bf[l].t, bf[l].f, -1.f);                                          // t = f - A * u
+        conv(V.R, desc_for(net, 1, 3, V.H, V.C, W.H, W.C), bf[l].t, bf[l + 1].f, nullptr, 1.f);  // f^{l+1} = R *_2 t
       }
     }
   }
   for (int l = L - 2; l >= 0; --l) {
     const Level& V = net->lv[l];
     const Level& W = net->lv[l + 1];
-    conv(V.P, desc_for(net, 2, 4, W.H, W.C, V.H, V.C), W.u, V.u, V.u, 1.f);   // u += P^T *_2 u^{l+1}
+    conv(V.P, desc_for(net, 2, 4, W.H, W.C, V.H, V.C), bf[l + 1].u, bf[l].u, bf[l].u, 1.f);  // u += P^T *_2 u^{l+1}
     for (size_t i = 0; i < V.Bpost.size(); ++i) smooth(l, V.Bpost[i], false);
   }
   // z = [alpha r] + Theta u^0
   const Level& L0 = net->lv[0];
-  conv(net->head, desc_for(net, 0, 1, N, L0.C, N, M), L0.u, z, add_identity ? r : nullptr, 1.f, false, true);
+  conv(net->head, desc_for(net, 0, 1, N, L0.C, N, M), bf[0].u, z, add_identity ? r : nullptr, 1.f, false, true);
+}
+
+void vcycle_run(const mgnet_net* net, const float* r, float* z, bool add_identity, const double* alpha,
+                int alpha_stride, cudaStream_t st) {
+  vcycle_run_t<float>(net, r, z, add_identity, alpha, alpha_stride, st);
+}
+void vcycle_run_f64(const mgnet_net* net, const double* r, double* z, bool add_identity, cudaStream_t st) {
+  vcycle_run_t<double>(net, r, z, add_identity, nullptr, 0, st);
 }
 
 }  // namespace rte

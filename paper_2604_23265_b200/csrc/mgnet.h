@@ -11,6 +11,7 @@ struct ConvW {
   int kind = 0;       // 0: OIHW conv, 1: IOHW conv_transpose
   int Co = 0, Ci = 0, ks = 0, taps = 0;
   float* d_kn = nullptr;   // [tap][ci][co]
+  double* d_kn64 = nullptr;  // same, fp64 (fp64 V-cycle; created on first use)
   float* d_hi = nullptr;   // tensor-core operand [tc_rows][tc_K] K-major, tf32 hi (conv_tc.cu)
   float* d_lo = nullptr;   //                       tf32 lo
   int tc_rows = 0, tc_K = 0;
@@ -33,6 +34,7 @@ struct Level {
   float* f = nullptr;   // [B][H][H][C]
   float* u = nullptr;
   float* t = nullptr;
+  double *f64 = nullptr, *u64 = nullptr, *t64 = nullptr;  // fp64 V-cycle buffers (first use)
 };
 
 double conv_flops(const ConvDesc& d);
@@ -47,6 +49,10 @@ void conv_tc_prepare(struct ::mgnet_net* net);
 
 void vcycle_run(const struct ::mgnet_net* net, const float* r, float* z, bool add_identity, const double* alpha,
                 int alpha_stride, cudaStream_t st);
+void vcycle_run_f64(const struct ::mgnet_net* net, const double* r, double* z, bool add_identity, cudaStream_t st);
+template <typename T>
+void launch_conv_t(const ConvDesc& d, const T* in, const T* Wk, T* out, const T* addend, float sign,
+                   const double* alpha, int alpha_stride, bool alpha_on_input, bool alpha_on_addend, cudaStream_t st);
 
 }  // namespace rte
 

@@ -136,6 +136,19 @@ def test_vcycle_parity(cfg):
     assert _rel(v_gpu, v_ref) <= 1e-5
 
 
+@pytest.mark.parametrize("cfg", [W.config(k) for k in (1, 2)] + VSMALL, ids=lambda c: f"cfg{c.k}-N{c.N}-L{c.L}")
+def test_vcycle_f64_parity(cfg):
+    """The fp64 V-cycle (SIMT, same data flow) equals the oracle to 1e-12."""
+    import paper_2604_23265_b200 as P
+    p, net, onet, _ = _net_pair(cfg, std=0.05)
+    r = W.make_vector(cfg, 2).astype(np.float64)
+    rd = _dev(r)
+    z = torch.empty_like(rd)
+    P.mgnet_vcycle_f64(net, rd, z, add_identity=True)
+    torch.cuda.synchronize()
+    assert _rel(z.cpu().numpy() - r, O.vcycle(onet, r, add_identity=False)) <= 1e-12
+
+
 @pytest.mark.slow
 @pytest.mark.parametrize("k", [4, 5])
 def test_vcycle_parity_large(k):
@@ -235,8 +248,8 @@ def test_gmres_config1_converges_like_oracle(precond, reorth, precision):
 @pytest.mark.slow
 @pytest.mark.parametrize("precond", [False, True])
 def test_gmres_config2_fp64_basis_iterations_exact(precond):
-    """fp64 Krylov basis + fp64 apply (precision=1): the iteration count is within +-1 of the
-    oracle's and the solution within 1e-4 (north star), on the diffusive config 2."""
+    """Everything in fp64 (precision=1: basis, apply, V-cycle): the iteration count is within +-1
+    of the oracle's and the solution within 1e-4 (north star), on the diffusive config 2."""
     cfg = W.config(2)
     rep, x, ref = _gmres_pair(cfg, precond, cfg.rtol, cfg.maxit, precision=1)
     r = rep[0]
