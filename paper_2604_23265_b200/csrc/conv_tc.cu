@@ -197,6 +197,7 @@ namespace {
 
 struct Plan {
   bool ok = false;
+  bool halo = false;  // stride-1 3x3: one halo tile per channel chunk feeds all 9 taps
   int BN = 0;
   tc::Geom g{};
   int mtiles = 0, ntiles = 0;
@@ -211,6 +212,7 @@ Plan make_plan(const ConvDesc& d) {
   int BN = 32;
   while (BN < 128 && BN * 2 <= d.Co && d.Co % (BN * 2) == 0) BN *= 2;
   P.BN = BN;
+  P.halo = (d.mode == 0 && d.ks == 3);
   tc::Geom& g = P.g;
   g.mode = d.mode;
   g.ks = (d.mode == 2) ? 4 : d.ks;
@@ -242,8 +244,9 @@ Plan make_plan(const ConvDesc& d) {
   const double out_us = 4.0 * (double)P.out_elems / 6.0e6;
   double best = 1e300;
   int best_kps = g.kb_total;
-  for (int ns = 1; ns <= std::max(1, std::min(64, g.kb_total / 2)); ++ns) {
-    const int kps = (g.kb_total + ns - 1) / ns;
+  const int quantum = P.halo ? 9 : 1;  // halo kernels split K in whole channel chunks (9 taps)
+  for (int ns = 1; ns <= std::max(1, std::min(64, g.kb_total / (2 * quantum))); ++ns) {
+    const int kps = ((g.kb_total + ns - 1) / ns + quantum - 1) / quantum * quantum;
     const int nsr = (g.kb_total + kps - 1) / kps;
     const long long units = (long long)P.mtiles * P.ntiles * nsr;
     const double waves = (double)((units + sms - 1) / sms);
@@ -259,11 +262,11 @@ Plan make_plan(const ConvDesc& d) {
   return P;
 }
 
-template <int BN>
+template <int BN, bool HALO>
 void launch_bn(const Plan& P, const CUtensorMap& ta, const CUtensorMap& tbh, const CUtensorMap& tbl,
                const tc::EpiConv& epi, cudaStream_t st) {
-  auto kern = tc::gemm3xtf32_kernel<BN, tc::EpiConv>;
-  constexpr int smem = tc::gemm_smem_bytes<BN>();
+  auto kern = tc::gemm3xtf32_kernel<BN, HALO, tc::EpiConv>;
+  constexpr int smem = tc::gemm_smem_bytes<BN, HALO>();
   tc::ensure_smem((const void*)kern, smem);
   const long long units = (long long)P.mtiles * P.ntiles * P.g.nsplit;
   const int grid = (int)std::min<long long>(units, num_sms());
@@ -279,7 +282,8 @@ bool conv_tc_try(const ConvDesc& d, const float* in, float* out, const float* ad
   if (!P.ok) return false;
   const tc::Geom& g = P.g;
   const int es = (d.mode == 1) ? 2 : 1;
-  CUtensorMap ta = tc::make_map_act(in, d.Ci, d.Wi, d.Hi, d.B, g.TW, g.TH, es);
+  CUtensorMap ta = P.halo ? tc::make_map_act(in, d.Ci, d.Wi, d.Hi, d.B, g.TW + 2, g.TH + 2, 1)
+                          : tc::make_map_act(in, d.Ci, d.Wi, d.Hi, d.B, g.TW, g.TH, es);
   CUtensorMap tbh = tc::make_map_kmajor(d.w->d_hi, d.w->tc_K, d.w->tc_rows, P.BN);
   CUtensorMap tbl = tc::make_map_kmajor(d.w->d_lo, d.w->tc_K, d.w->tc_rows, P.BN);
   tc::EpiConv epi;
@@ -305,9 +309,9 @@ bool conv_tc_try(const ConvDesc& d, const float* in, float* out, const float* ad
   }
   prof_begin(st);
   switch (P.BN) {
-    case 32: launch_bn<32>(P, ta, tbh, tbl, epi, st); break;
-    case 64: launch_bn<64>(P, ta, tbh, tbl, epi, st); break;
-    default: launch_bn<128>(P, ta, tbh, tbl, epi, st); break;
+    case 32: P.halo ? launch_bn<32, true>(P, ta, tbh, tbl, epi, st) : launch_bn<32, false>(P, ta, tbh, tbl, epi, st); break;
+    case 64: P.halo ? launch_bn<64, true>(P, ta, tbh, tbl, epi, st) : launch_bn<64, false>(P, ta, tbh, tbl, epi, st); break;
+    default: P.halo ? launch_bn<128, true>(P, ta, tbh, tbl, epi, st) : launch_bn<128, false>(P, ta, tbh, tbl, epi, st); break;
   }
   const bool split = g.nsplit > 1;
   after_launch(conv_class_name(d, true), st, conv_flops(d), split ? 0.0 : conv_bytes(d, addend != nullptr), 1);

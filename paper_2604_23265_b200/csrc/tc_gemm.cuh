@@ -1,24 +1,32 @@
-// Warp-specialised 3xTF32 implicit GEMM on tcgen05 (sm_100a), shared by the MgNet convolutions
-// (conv_tc.cu) and the scattering contraction of rte_apply (apply_tc.cu).  NOT part of the ABI.
+// Warp-specialised, persistent 3xTF32 implicit GEMM on tcgen05 (sm_100a), shared by the MgNet
+// convolutions (conv_tc.cu) and the scattering contraction of rte_apply (apply_tc.cu).  NOT part
+// of the ABI.
 //
-// One CTA computes a 128-pixel x BN-channel output tile over a range of K blocks (split-K):
+// A work unit computes a 128-pixel x BN-channel output tile over a range of K blocks (split-K):
 //   D[128 x BN] (TMEM, fp32) = sum_kb  A_kb[128 x 32] . B_kb[BN x 32]^T
-// where a K block kb = (tap, 32-channel chunk).  A_kb is a shifted (and for the stride-2
-// restriction, strided) window of the NHWC activation, fetched by a 4-D TMA tiled load whose
-// out-of-bounds zero fill implements the convolution's zero padding; B_kb is a 32-wide K slice of
-// the weights stored [rows][K] K-major.  3xTF32 (R26): the converter warps read each A
-// row once from shared memory, split it into hi + lo and store both into TMEM (tcgen05.st); the
-// MMAs take A from TMEM and only the pre-split weights (B hi, B lo) from shared memory, which keeps
-// the shared-memory traffic per K block at raw-A TMA write + one read + B (the SS form saturated
-// the 128 B/clk shared-memory port).  Each k-step issues lo.hi + hi.lo (cross-term accumulator)
-// and hi.hi (main accumulator).
+// where a K block kb = (tap, 32-channel chunk).  A is an NHWC activation window fetched by a 4-D
+// TMA tiled load whose out-of-bounds zero fill implements the convolution's zero padding; B_kb is
+// a 32-wide K slice of the weights stored [rows][K] K-major (pre-split into TF32 hi and lo).
+//
+//  * HALO (stride-1 3x3 convs): one TMA load brings the (TW+2) x (TH+2) halo of the output tile
+//    for a 32-channel chunk; the 9 taps read their shifted 128-pixel windows out of it, so the
+//    input crosses L2 -> SM once per chunk instead of 9 times.  Other shapes load one A tile per
+//    K block (shifted / strided window).
+//  * 3xTF32 (R26): the converter warps read each A row from shared memory, split it
+//    into hi + lo and store both into TMEM (tcgen05.st); the MMAs take A from TMEM and only the
+//    weights from shared memory (the shared-memory port is the scarce resource).
+//  * Accumulation precision: the tensor core's fp32 accumulation is not round-to-nearest, so the
+//    main product hi.hi accumulates for at most kPromoteKB K blocks in one of two TMEM buffers
+//    before promoter warps add it into fp32 registers; the small cross terms (lo.hi + hi.lo) go to
+//    a separate accumulator.  For N tiles <= 64 a k-step is 2 MMAs (hi.[B_hi; B_lo] with N = 2BN
+//    writing [main_t | X_t], then lo.B_hi into X_t); for BN = 128 it is 3 MMAs with a unit-long X.
 //
 // Warp roles (448 threads): warp 0 = TMA producer, warp 1 = TMEM allocator + MMA issuer (both walk
-// the pipeline warp-wide, one elected lane issues), warps 2..5 = A hi/lo converters (smem -> TMEM),
-// warps 6..13 = accumulator promotion and the epilogue (TMEM -> registers -> global; two warps per
-// lane quarter, each owning half of the columns); warp w accesses TMEM lanes 32*(w%4) .. +31.  Pipelines:
-// full[s] (TMA bytes landed) -> conv[s] (hi/lo written) -> empty[s] (MMAs done, tcgen05.commit);
-// mfull[t] / mempty[t] hand the two main-accumulator TMEM buffers between MMA and promoters.
+// the pipeline warp-wide, one elected lane issues), warps 2..5 = A converters (smem -> TMEM),
+// warps 6..13 = promotion and epilogue (two warps per TMEM lane quarter, half the columns each);
+// warp w accesses TMEM lanes 32*(w%4) .. +31.
+// Pipelines: afull/aempty (A tiles), bfull/bempty (B tiles), conv/afree (TMEM A buffers),
+// mfull/mempty (main accumulator buffers), xempty (unit-long X), cfull/cempty (row centres).
 #pragma once
 
 #include <cuda.h>
@@ -29,7 +37,7 @@
 namespace rte {
 namespace tc {
 
-constexpr int kGemmThreads = 448;   // 14 warps (see kernel)
+constexpr int kGemmThreads = 448;   // 14 warps (see above)
 constexpr int kPromoteKB = 4;       // K blocks per TMEM accumulation group
 constexpr int kTileM = 128;
 constexpr int kABytes = kTileM * 128;   // 128 rows x 32 fp32
@@ -45,38 +53,38 @@ struct Geom {
   int classes;      // 1, or 4 parity classes (mode 2)
   int Hc, Wc;       // output (class) grid size
   int kb_total;     // taps * cchunks
-  int kb_per_split;
+  int kb_per_split; // (halo kernels: a multiple of 9)
   int nsplit;
   int b_rows_class; // B-operand row offset per class (mode 2)
   int b_rows_batch; // B-operand row offset per batch sample (per-sample operators)
   int ntiles;       // N tiles
   int mtiles;       // M tiles (B * classes * tiles_y * tiles_x)
   int bn;           // N tile (the kernel's BN)
-  int dbg;          // perf-experiment switches (RTE_TC_DBG; 0 in production): bit0 skip the hi/lo
-                    // conversion, bit1 skip the B-lo load and MMA, bit2 skip the cross-term MMAs,
-                    // bit3 no MMAs at all, bit4 no TMA loads, bit5 no epilogue global traffic
+  int dbg;          // perf-experiment switches (RTE_TC_DBG; 0 in production): bit3 no MMAs,
+                    // bit4 no TMA loads, bit5 no epilogue global traffic, bit6 role timers
 };
 
-
-template <int BN>
-struct Smem {
-  static constexpr int kBBytes = BN * 128;
-  static constexpr int kStage = kABytes + 2 * kBBytes;   // raw A tile + B hi + B lo
+// Shared-memory plan: A ring (HALO: halo tiles up to 130 x 3 rows; else 128-row tiles) and B ring.
+template <int BN, bool HALO>
+struct Plan {
+  static constexpr int kBBytes = BN * 128;                          // one of B hi / B lo
+  static constexpr int kASlot = HALO ? 50176 : kABytes;             // 392 rows (>= 130 x 3), 1 KB aligned
+  static constexpr int kBSlot = 2 * kBBytes;
+  static constexpr int kBudget = 196 * 1024;
+  static constexpr int kNA = HALO ? 2 : 4;                          // A ring depth
+  static constexpr int kNBraw = (kBudget - kNA * kASlot) / kBSlot;
+  static constexpr int kNB = kNBraw > 8 ? 8 : kNBraw;               // B ring depth
+  static constexpr int kRingBytes = kNA * kASlot + kNB * kBSlot;
 };
 
-template <int BN>
-constexpr int gemm_stages() {
-#ifdef RTE_TC_STAGES
-  if (Smem<BN>::kStage * RTE_TC_STAGES <= 192 * 1024) return RTE_TC_STAGES;
-#endif
-  return Smem<BN>::kStage * 6 <= 192 * 1024 ? 6 : (192 * 1024) / Smem<BN>::kStage;
+template <int BN, bool HALO>
+constexpr int gemm_smem_bytes() {
+  return Plan<BN, HALO>::kRingBytes + 1024 /*align*/ + 1024 /*barriers*/ + 1024 /*row centres*/;
 }
 
-// TMEM layout.  Fused form (BN <= 64): two group buffers t = 0, 1 of 2BN columns [main_t | X_t];
-// one MMA hi.[B_hi; B_lo] (N = 2BN) writes both halves and lo.B_hi (N = BN) adds into X_t, so a
-// k-step costs 2 MMAs; both halves are promoted per group.  Split form (BN = 128): main buffers
-// M0, M1 [0, 2BN) and a unit-long cross-term accumulator X [2BN, 3BN), 3 MMAs per k-step.  Then
-// the A buffers, 64 columns each (hi: 32 K columns, lo: 32 K columns).
+// TMEM layout.  Fused form (BN <= 64): two group buffers t = 0, 1 of 2BN columns [main_t | X_t].
+// Split form (BN = 128): main buffers M0, M1 [0, 2BN) and a unit-long X [2BN, 3BN).  Then the
+// TMEM A buffers, 64 columns each (hi: 32 K columns, lo: 32 K columns).
 template <int BN>
 constexpr bool tmem_fused() {
   return BN <= 64;
@@ -88,11 +96,6 @@ constexpr int tmem_acc_cols() {
 template <int BN>
 constexpr int tmem_abufs() {
   return (512 - tmem_acc_cols<BN>()) / 64 < 6 ? (512 - tmem_acc_cols<BN>()) / 64 : 6;
-}
-
-template <int BN>
-constexpr int gemm_smem_bytes() {
-  return gemm_stages<BN>() * Smem<BN>::kStage + 1024 /*align*/ + 512 /*barriers*/ + 1024 /*row centres*/;
 }
 
 struct TileCoord {
@@ -131,7 +134,19 @@ __device__ __forceinline__ Unit decode_unit(const Geom& g, int u) {
   return w;
 }
 
-// A-window origin (x, y) in the input tensor for K block kb of tile c.
+// K block kb -> (tap, channel chunk).  HALO kernels walk chunk-major (9 taps per halo tile).
+template <bool HALO>
+__device__ __forceinline__ void kb_split(const Geom& g, int kb, int& tap, int& cc) {
+  if (HALO) {
+    cc = kb / 9;
+    tap = kb - 9 * cc;
+  } else {
+    tap = kb / g.cchunks;
+    cc = kb - tap * g.cchunks;
+  }
+}
+
+// A-window origin (x, y) in the input tensor for tap `tap` of tile c (non-halo kernels).
 __device__ __forceinline__ void a_origin(const Geom& g, const TileCoord& c, int tap, int& xA, int& yA) {
   if (g.mode == 0) {
     const int ky = tap / g.ks, kx = tap % g.ks, p = g.ks / 2;
@@ -148,19 +163,6 @@ __device__ __forceinline__ void a_origin(const Geom& g, const TileCoord& c, int 
   }
 }
 
-// Epilogue interface: row = epi.row(b, cls, oy, ox, c_row) prepares the per-output-pixel state of a
-// valid pixel (oy, ox) of the class grid (c_row = the row centre when Epi::kCenter: the GEMM then
-// computed (a - c_row 1) . B^T); epi.store4(row, col, v4) finishes columns col .. col+3;
-// epi.store_partial4(split, row, col, v4) stores raw partial sums when split-K is active.
-//
-// Accumulation precision.  The tensor core's fp32 accumulation does not round to nearest (a
-// biased, truncating add), so a long K loop into one TMEM accumulator drifts by ~K/8 * 2^-24
-// relative.  Two measures keep the GEMM at fp32 accuracy:
-//   - the small 3xTF32 cross terms (lo.hi + hi.lo, ~2^-11 of the result) go to their own TMEM
-//     accumulator X, so the main accumulator sees one add per k-step;
-//   - the main product hi.hi accumulates for at most kPromoteKB K blocks in one of two TMEM
-//     buffers; four promoter warps then add the buffer into fp32 registers (round-to-nearest)
-//     while the MMA warp fills the other buffer (the "promotion" used by FP8 GEMMs).
 // dbg bit6: block 0 reports per-role cycles spent waiting (printf at exit; experiments only)
 __device__ __forceinline__ void tw_wait(uint64_t* bar, uint32_t par, bool on, long long& acc) {
   if (!on) {
@@ -172,47 +174,63 @@ __device__ __forceinline__ void tw_wait(uint64_t* bar, uint32_t par, bool on, lo
   acc += clock64() - t0;
 }
 
-template <int BN, class Epi>
+// Epilogue interface: row = epi.row(b, cls, oy, ox, c_row) prepares the per-output-pixel state of a
+// valid pixel (oy, ox) of the class grid (c_row = the row centre when Epi::kCenter: the GEMM then
+// computed (a - c_row 1) . B^T); epi.store4(row, col, v4) finishes columns col .. col+3;
+// epi.store_partial4(split, row, col, v4) stores raw partial sums when split-K is active.
+template <int BN, bool HALO, class Epi>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm3xtf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBhi,
                       const __grid_constant__ CUtensorMap tmBlo, const Geom g, const Epi epi) {
   static_assert(BN == 32 || BN == 64 || BN == 128, "N tile must be 32, 64 or 128");
-  constexpr int STAGES = gemm_stages<BN>();
+  static_assert(!(HALO && Epi::kCenter), "row centring is for the 1x1 (apply) kernels");
+  using PL = Plan<BN, HALO>;
+  constexpr int NAR = PL::kNA, NBR = PL::kNB;
   constexpr int NA = tmem_abufs<BN>();
-  constexpr int BBYTES = Smem<BN>::kBBytes;
-  constexpr int STAGE = Smem<BN>::kStage;
+  constexpr int BBYTES = PL::kBBytes;
   constexpr uint32_t TMEM_COLS = 512;
+  constexpr bool FUSED = tmem_fused<BN>();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE);
-  uint64_t* full = bars;                       // [STAGES] TMA bytes landed
-  uint64_t* conv = bars + STAGES;              // [STAGES] A hi/lo in TMEM (4 converter warps)
-  uint64_t* empty = bars + 2 * STAGES;         // [STAGES] MMAs done with the stage's B tiles
-  uint64_t* afree = bars + 3 * STAGES;         // [NA] MMAs done with a TMEM A buffer
-  uint64_t* mfull = afree + NA;                // [2] main buffer ready for promotion
-  uint64_t* mempty = mfull + 2;                // [2] main buffer drained (4 promoter warps)
-  uint64_t* xempty = mempty + 2;               // [1] cross buffer drained by the epilogue
-  uint64_t* cfull = xempty + 1;                // [2] row centres written (128 converter threads)
-  uint64_t* cempty = cfull + 2;                // [2] row centres read (128 epilogue threads)
+  uint8_t* aring = smem;
+  uint8_t* bring = smem + NAR * PL::kASlot;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + PL::kRingBytes);
+  uint64_t* afull = bars;              // [NAR] A tile landed
+  uint64_t* aempty = afull + NAR;      // [NAR] converters done reading the A tile (4 warps)
+  uint64_t* bfull = aempty + NAR;      // [NBR] B tiles landed
+  uint64_t* bempty = bfull + NBR;      // [NBR] MMAs done with the B tiles
+  uint64_t* conv = bempty + NBR;       // [NA] TMEM A buffer written (4 converter warps)
+  uint64_t* afree = conv + NA;         // [NA] MMAs done with the TMEM A buffer
+  uint64_t* mfull = afree + NA;        // [2] main buffer ready for promotion
+  uint64_t* mempty = mfull + 2;        // [2] main buffer drained (8 promoter warps)
+  uint64_t* xempty = mempty + 2;       // [1] unit-long X drained (8 promoter warps)
+  uint64_t* cfull = xempty + 1;        // [2] row centres written (128 converter threads)
+  uint64_t* cempty = cfull + 2;        // [2] row centres read (256 epilogue threads)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cempty + 2);
-  float* cvec = reinterpret_cast<float*>(smem + STAGES * STAGE + 512);  // [2][128] row centres
+  float* cvec = reinterpret_cast<float*>(smem + PL::kRingBytes + 1024);  // [2][128] row centres
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int units = g.mtiles * g.ntiles * g.nsplit;
   const int rows = g.TW * g.TH;
-  const uint32_t a_bytes = (uint32_t)rows * 128u;
+  const uint32_t a_bytes = HALO ? (uint32_t)((g.TW + 2) * (g.TH + 2)) * 128u : (uint32_t)rows * 128u;
   const bool prof = (g.dbg & 64) && blockIdx.x == 0 && lane == 0;
   long long w_a = 0, w_b = 0, w_c = 0;
   const long long t_start = clock64();
   int n_kb = 0;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&conv[s], 4);
-      mbar_init(&empty[s], 1);
+    for (int i = 0; i < NAR; ++i) {
+      mbar_init(&afull[i], 1);
+      mbar_init(&aempty[i], 4);
     }
-    for (int a = 0; a < NA; ++a) mbar_init(&afree[a], 1);
+    for (int i = 0; i < NBR; ++i) {
+      mbar_init(&bfull[i], 1);
+      mbar_init(&bempty[i], 1);
+    }
+    for (int i = 0; i < NA; ++i) {
+      mbar_init(&conv[i], 4);
+      mbar_init(&afree[i], 1);
+    }
     for (int t = 0; t < 2; ++t) {
       mbar_init(&mfull[t], 1);
       mbar_init(&mempty[t], 8);
@@ -232,61 +250,82 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  constexpr bool FUSED = tmem_fused<BN>();
   const uint32_t tmem_x = tmem + 2 * BN;  // split form only
   const uint32_t tmem_a = tmem + tmem_acc_cols<BN>();
 
   if (warp == 0) {
     // ===== TMA producer: the whole warp walks the pipeline, one elected lane issues =====
-    int s = 0;
-    uint32_t ph = 0;
+    int as = 0, bs = 0;
+    uint32_t aph = 0, bph = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       const Unit w = decode_unit(g, u);
       const int brow = w.n0 + w.tc.cls * g.b_rows_class + w.tc.b * g.b_rows_batch;
       for (int kb = w.kb0; kb < w.kb1; ++kb, ++n_kb) {
-        tw_wait(&empty[s], ph ^ 1, prof, w_a);
-        uint8_t* sa = smem + s * STAGE;
-        const int tap = kb / g.cchunks, ci0 = (kb % g.cchunks) * 32;
-        int xA, yA;
-        a_origin(g, w.tc, tap, xA, yA);
-        if (elect_one()) {
-          if (g.dbg & 16) {
-            mbar_arrive(&full[s]);
+        int tap, cc;
+        kb_split<HALO>(g, kb, tap, cc);
+        if (!HALO || tap == 0 || kb == w.kb0) {
+          // new A tile: the halo of chunk cc (HALO) or the window of this K block
+          tw_wait(&aempty[as], aph ^ 1, prof, w_a);
+          int xA, yA;
+          if (HALO) {
+            xA = w.tc.tx * g.TW - 1;
+            yA = w.tc.ty * g.TH - 1;
           } else {
-            mbar_arrive_expect_tx(&full[s], a_bytes + 2u * BBYTES);
-            tma_load_4d(sa, &tmA, &full[s], ci0, xA, yA, w.tc.b);
-            tma_load_2d(sa + kABytes, &tmBhi, &full[s], kb * 32, brow);
-            tma_load_2d(sa + kABytes + BBYTES, &tmBlo, &full[s], kb * 32, brow);
+            a_origin(g, w.tc, tap, xA, yA);
+          }
+          if (elect_one()) {
+            if (g.dbg & 16) {
+              mbar_arrive(&afull[as]);
+            } else {
+              mbar_arrive_expect_tx(&afull[as], a_bytes);
+              tma_load_4d(aring + as * PL::kASlot, &tmA, &afull[as], cc * 32, xA, yA, w.tc.b);
+            }
+          }
+          __syncwarp();
+          if (++as == NAR) { as = 0; aph ^= 1; }
+        }
+        tw_wait(&bempty[bs], bph ^ 1, prof, w_b);
+        if (elect_one()) {
+          uint8_t* sb = bring + bs * PL::kBSlot;
+          const int kcol = HALO ? tap * g.cchunks * 32 + cc * 32 : kb * 32;
+          if (g.dbg & 16) {
+            mbar_arrive(&bfull[bs]);
+          } else {
+            mbar_arrive_expect_tx(&bfull[bs], 2u * BBYTES);
+            tma_load_2d(sb, &tmBhi, &bfull[bs], kcol, brow);
+            tma_load_2d(sb + BBYTES, &tmBlo, &bfull[bs], kcol, brow);
           }
         }
         __syncwarp();
-        if (++s == STAGES) { s = 0; ph ^= 1; }
+        if (++bs == NBR) { bs = 0; bph ^= 1; }
       }
     }
   } else if (warp == 1) {
     // ===== MMA issuer: the whole warp walks the pipeline, one elected lane issues =====
     constexpr uint32_t idesc = idesc_tf32(kTileM, BN);
     const bool no_mma = (g.dbg & 8) != 0;
-    int s = 0, ab = 0;
-    uint32_t ph = 0;
+    int bs = 0, ab = 0;
+    uint32_t bph = 0, abph = 0;
     int gcount = 0;  // main-buffer groups issued so far (all units)
     int li = 0;      // local unit index
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++li) {
       const Unit w = decode_unit(g, u);
-      tw_wait(xempty, ((uint32_t)li & 1u) ^ 1u, prof, w_c);
-      tc_fence_after();
+      if constexpr (!FUSED) {
+        tw_wait(xempty, ((uint32_t)li & 1u) ^ 1u, prof, w_c);
+        tc_fence_after();
+      }
       uint32_t acc_x = 0;
       for (int kbg = w.kb0; kbg < w.kb1; kbg += kPromoteKB, ++gcount) {
         const int t = gcount & 1;
         tw_wait(&mempty[t], ((uint32_t)(gcount >> 1) & 1u) ^ 1u, prof, w_b);
         tc_fence_after();
-        const uint32_t tm = tmem + (uint32_t)(t * BN);
         uint32_t acc_m = 0;
         const int kbe = min(w.kb1, kbg + kPromoteKB);
         for (int kb = kbg; kb < kbe; ++kb, ++n_kb) {
-          tw_wait(&conv[s], ph, prof, w_a);
+          tw_wait(&conv[ab], abph, prof, w_a);
+          tw_wait(&bfull[bs], bph, prof, w_a);
           tc_fence_after();
-          const uint32_t sb = smem_u32(smem + s * STAGE) + kABytes;
+          const uint32_t sb = smem_u32(bring + bs * PL::kBSlot);
           const uint64_t d_bh = sdesc_sw128(sb), d_bl = sdesc_sw128(sb + BBYTES);
           const uint32_t a_hi = tmem_a + (uint32_t)(64 * ab), a_lo = a_hi + 32;
           if (!no_mma) {
@@ -301,6 +340,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 mma_tf32_ts_elect(tbuf + BN, a_lo + 8u * k, d_bh + 2u * k, idesc, 1);
               }
             } else {
+              const uint32_t tm = tmem + (uint32_t)(t * BN);
 #pragma unroll
               for (int k = 0; k < 4; ++k) {
                 // K step of 8 tf32: +8 TMEM columns for A, +32 B (= +2) in the B descriptors
@@ -312,38 +352,53 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               }
             }
           }
-          mma_commit_elect(&empty[s]);
+          mma_commit_elect(&bempty[bs]);
           mma_commit_elect(&afree[ab]);
-          if (++s == STAGES) { s = 0; ph ^= 1; }
-          if (++ab == NA) ab = 0;
+          if (++bs == NBR) { bs = 0; bph ^= 1; }
+          if (++ab == NA) { ab = 0; abph ^= 1; }
         }
         mma_commit_elect(&mfull[t]);
       }
     }
   } else if (warp < 6) {
     // ===== converters (warps 2..5; warp w owns A rows / TMEM lanes 32*(w%4) .. +31) =====
-    const int r = 32 * (warp & 3) + lane;  // A tile row of this thread
+    const int r = 32 * (warp & 3) + lane;  // output-tile row of this thread
     const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
-    int s = 0, ab = 0, auses = 0;
-    uint32_t ph = 0;
+    const int rr = r < rows ? r : 0;       // rows beyond the tile read row 0 (results unused)
+    const int ly = rr / g.TW, lx = rr - ly * g.TW;
+    int as = 0, ab = 0;
+    uint32_t aph = 0, abph = 0;
     int li = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++li) {
       const Unit w = decode_unit(g, u);
       float c = 0.f;
       for (int kb = w.kb0; kb < w.kb1; ++kb, ++n_kb) {
-        tw_wait(&full[s], ph, prof, w_a);
-        tw_wait(&afree[ab], ((uint32_t)(auses / NA) & 1u) ^ 1u, prof, w_b);
+        int tap, cc;
+        kb_split<HALO>(g, kb, tap, cc);
+        const bool new_tile = !HALO || tap == 0 || kb == w.kb0;
+        if (new_tile) tw_wait(&afull[as], aph, prof, w_a);
+        tw_wait(&afree[ab], abph ^ 1, prof, w_b);
         tc_fence_after();
-        // row r of the raw A tile: 16-byte chunk q sits at chunk position q ^ (r & 7) (SW128)
-        const uint32_t row_s = smem_u32(smem + s * STAGE) + (uint32_t)r * 128u;
+        // source row in the A tile: the tap-shifted halo row (HALO) or the row itself; 16-byte
+        // chunk q of a row sits at chunk position q ^ (row & 7) (SW128)
+        int arow = rr;
+        if (HALO) arow = (ly + tap / 3) * (g.TW + 2) + lx + tap % 3;
+        const uint32_t row_s = smem_u32(aring + as * PL::kASlot) + (uint32_t)arow * 128u;
         float hi[32], lo[32];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          const float4 v = lds128(row_s + (uint32_t)((q ^ (r & 7)) << 4));
+          const float4 v = lds128(row_s + (uint32_t)((q ^ (arow & 7)) << 4));
           hi[4 * q] = v.x;
           hi[4 * q + 1] = v.y;
           hi[4 * q + 2] = v.z;
           hi[4 * q + 3] = v.w;
+        }
+        // done with this A tile after its last K block
+        const bool last_of_tile = !HALO || tap == 8 || kb + 1 == w.kb1;
+        if (last_of_tile) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&aempty[as]);
+          if (++as == NAR) { as = 0; aph ^= 1; }
         }
         if constexpr (Epi::kCenter) {
           // row centre c_r = the row's first element in the unit's first K block; the GEMM then
@@ -366,16 +421,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&conv[s]);
-        if (++s == STAGES) { s = 0; ph ^= 1; }
-        if (++ab == NA) ab = 0;
-        ++auses;
+        if (lane == 0) mbar_arrive(&conv[ab]);
+        if (++ab == NA) { ab = 0; abph ^= 1; }
       }
     }
   } else {
     // ===== promoters + epilogue (warps 6..13): warp w owns TMEM lanes 32*(w%4) .. +31 and the
-    // column half h = (w - 6) / 4 of the tile (two warps per lane quarter double the epilogue's
-    // memory-level parallelism) =====
+    // column half h = (w - 6) / 4 of the tile =====
     constexpr int HB = BN / 2;  // columns per promoter warp
     const int quarter = warp & 3;
     const int half = (warp - 6) >> 2;
@@ -420,10 +472,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
           for (int i = 0; i < 16; ++i) acc[c0 + i] += v[i];
         }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(xempty);
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(xempty);
       float crow = 0.f;
       if constexpr (Epi::kCenter) {
         mbar_wait(&cfull[li & 1], (uint32_t)(li >> 1) & 1u);
