@@ -267,7 +267,7 @@ def run_ours(args, cfg):
     x = torch.zeros(p.shape, dtype=torch.float64, device=dev)
     K, Wm = args.steps, args.warmup
     solve = lambda xx, bb, k: P.gmres_solve(p, net, bb, xx, restart=cfg.restart, maxit=k, rtol=1e-300,
-                                            history=False)
+                                            history=False, reorth=args.reorth)
     # warm-up: W inner iterations (one solve), untimed
     solve(x, b, max(Wm, 1))
     torch.cuda.synchronize()
@@ -361,7 +361,8 @@ def run_ours(args, cfg):
                            "l2": "inputs larger than L2 (each vector 4 B x unknowns)" if cfg.unknowns * 4 > 126e6
                            else "working set L2-resident (small config)",
                            "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
-                           "precision": "fp32 storage/arithmetic, fp64 iterate, reductions and restart residual"},
+                           "precision": "fp32 storage/arithmetic, fp64 iterate, reductions and restart residual",
+                           "gram_schmidt": {0: "CGS2", 1: "CGS1", 2: "selective (DGKS)"}[args.reorth]},
                 "roofline": roof,
                 "e2e": {"value": K * ws / (ms_e2e * 1e-3), "unit": UNIT,
                         "h2d_bytes_per_step": h2d / K, "d2h_bytes_per_step": d2h / K,
@@ -383,6 +384,8 @@ def main():
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--reorth", type=int, default=0, choices=[0, 1, 2],
+                    help="Gram-Schmidt: 0 CGS2 (default), 1 CGS1, 2 selective re-orthogonalisation")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
