@@ -60,8 +60,9 @@ struct Geom {
   int ntiles;       // N tiles
   int mtiles;       // M tiles (B * classes * tiles_y * tiles_x)
   int bn;           // N tile (the kernel's BN)
-  int dbg;          // perf-experiment switches (RTE_TC_DBG; 0 in production): bit3 no MMAs,
-                    // bit4 no TMA loads, bit5 no epilogue global traffic, bit6 role timers
+  int dbg;          // perf-experiment switches (RTE_TC_DBG; 0 in production): bit0 converters skip
+                    // the row load/split/TMEM store, bit3 no MMAs, bit4 no TMA loads, bit5 no
+                    // epilogue global traffic, bit6 role timers
 };
 
 // Shared-memory plan: A ring (HALO: halo tiles up to 130 x 3 rows; else 128-row tiles) and B ring.
@@ -384,9 +385,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         int arow = rr;
         if (HALO) arow = (ly + tap / 3) * (g.TW + 2) + lx + tap % 3;
         const uint32_t row_s = smem_u32(aring + as * PL::kASlot) + (uint32_t)arow * 128u;
+        const bool skip = (g.dbg & 1) != 0;
         float hi[32], lo[32];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
+          if (skip) break;
           const float4 v = lds128(row_s + (uint32_t)((q ^ (arow & 7)) << 4));
           hi[4 * q] = v.x;
           hi[4 * q + 1] = v.y;
@@ -416,9 +419,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           split_tf32_fast(x, hi[e], lo[e]);
         }
         const uint32_t ta = tmem_a + (uint32_t)(64 * ab) + lane_base;
-        tmem_st32(ta, hi);
-        tmem_st32(ta + 32, lo);
-        tmem_wait_st();
+        if (!skip) {
+          tmem_st32(ta, hi);
+          tmem_st32(ta + 32, lo);
+          tmem_wait_st();
+        }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&conv[ab]);
