@@ -221,9 +221,16 @@ Plan make_plan(const ConvDesc& d) {
   g.classes = (d.mode == 2) ? 4 : 1;
   g.Hc = (d.mode == 2) ? d.Ho / 2 : d.Ho;
   g.Wc = (d.mode == 2) ? d.Wo / 2 : d.Wo;
-  g.TW = std::min(g.Wc, 128);
+  // halo kernels use ~square 32 x 4 tiles (a 34 x 6 halo = 1.6 loaded rows per output row);
+  // others 128-wide rows
+  g.TW = std::min(g.Wc, P.halo ? 32 : 128);
   g.TH = std::max(1, 128 / g.TW);
   g.TH = std::min(g.TH, g.Hc);
+  if (P.halo && (g.TW + 2) * (g.TH + 2) > tc::kHaloRows) {
+    P.halo = false;
+    g.TW = std::min(g.Wc, 128);
+    g.TH = std::min(g.Hc, std::max(1, 128 / g.TW));
+  }
   g.tiles_x = (g.Wc + g.TW - 1) / g.TW;
   g.tiles_y = (g.Hc + g.TH - 1) / g.TH;
   g.kb_total = g.taps * g.cchunks;

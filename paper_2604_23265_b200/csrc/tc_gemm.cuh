@@ -65,13 +65,16 @@ struct Geom {
                     // epilogue global traffic, bit6 role timers
 };
 
-// Shared-memory plan: A ring (HALO: halo tiles up to 130 x 3 rows; else 128-row tiles) and B ring.
+// Shared-memory plan: A ring (HALO: halo tiles of up to kHaloRows rows; else 128-row tiles), B
+// ring, and the epilogue staging tiles (one 128 x 32 fp32 tile per column half).
+constexpr int kHaloRows = 208;                  // (TW+2)(TH+2) <= 208, e.g. 34 x 6 for a 32 x 4 tile
+constexpr int kStageBytes = kTileM * 128;       // 128 rows x 32 fp32 per column half
 template <int BN, bool HALO>
 struct Plan {
   static constexpr int kBBytes = BN * 128;                          // one of B hi / B lo
-  static constexpr int kASlot = HALO ? 50176 : kABytes;             // 392 rows (>= 130 x 3), 1 KB aligned
+  static constexpr int kASlot = HALO ? kHaloRows * 128 : kABytes;   // 1 KB multiples
   static constexpr int kBSlot = 2 * kBBytes;
-  static constexpr int kBudget = 196 * 1024;
+  static constexpr int kBudget = 190 * 1024;                        // rings
   static constexpr int kNA = HALO ? 2 : 4;                          // A ring depth
   static constexpr int kNBraw = (kBudget - kNA * kASlot) / kBSlot;
   static constexpr int kNB = kNBraw > 8 ? 8 : kNBraw;               // B ring depth
@@ -80,7 +83,8 @@ struct Plan {
 
 template <int BN, bool HALO>
 constexpr int gemm_smem_bytes() {
-  return Plan<BN, HALO>::kRingBytes + 1024 /*align*/ + 1024 /*barriers*/ + 1024 /*row centres*/;
+  return Plan<BN, HALO>::kRingBytes + 2 * kStageBytes + 1024 /*align*/ + 1024 /*barriers*/ +
+         1024 /*row centres*/;
 }
 
 // TMEM layout.  Fused form (BN <= 64): two group buffers t = 0, 1 of 2BN columns [main_t | X_t].
@@ -209,6 +213,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* cempty = cfull + 2;        // [2] row centres read (256 epilogue threads)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cempty + 2);
   float* cvec = reinterpret_cast<float*>(smem + PL::kRingBytes + 1024);  // [2][128] row centres
+  const uint32_t stage_s = smem_u32(smem + PL::kRingBytes + 2048);        // [2 halves][128][32] staging
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int units = g.mtiles * g.ntiles * g.nsplit;
@@ -481,26 +486,44 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(xempty);
       }
-      float crow = 0.f;
-      if constexpr (Epi::kCenter) {
-        mbar_wait(&cfull[li & 1], (uint32_t)(li >> 1) & 1u);
-        crow = cvec[(li & 1) * 128 + r];
-        mbar_arrive(&cempty[li & 1]);
-      }
-      // Direct epilogue: thread r writes tile row r, columns cbase .. cbase + HB, as float4s.
-      const int ly = r / g.TW, lx = r - ly * g.TW;
-      const int oy = w.tc.ty * g.TH + ly, ox = w.tc.tx * g.TW + lx;
-      if (r < rows && oy < g.Hc && ox < g.Wc && !(g.dbg & 32)) {
-        const typename Epi::Row row = epi.row(w.tc.b, w.tc.cls, oy, ox, crow);
+      if constexpr (Epi::kCenter) mbar_wait(&cfull[li & 1], (uint32_t)(li >> 1) & 1u);
+      // Coalesced epilogue.  Each column chunk (<= 32 columns) of this half is staged through a
+      // shared tile (row r at r*128 B, 16-byte chunk q at position q ^ (r & 7): conflict-free both
+      // ways), then the half's four warps walk their rows with float4 lanes, so every global
+      // load/store instruction covers whole rows (128 B each) instead of 32 scattered lines.
+      constexpr int CW = HB < 32 ? HB : 32;   // chunk width (columns)
+      constexpr int LPR = CW / 4;             // lanes per row
+      constexpr int RPI = 32 / LPR;           // rows per warp instruction
+      const uint32_t sh = stage_s + (uint32_t)(half * kStageBytes);
 #pragma unroll
-        for (int c = 0; c < HB; c += 4) {
-          const float4 v = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
-          if (g.nsplit > 1)
-            epi.store_partial4(w.split, row, w.n0 + cbase + c, v);
-          else
-            epi.store4(row, w.n0 + cbase + c, v);
+      for (int c0 = 0; c0 < HB; c0 += CW) {
+#pragma unroll
+        for (int k = 0; k < CW / 4; ++k)
+          sts128(sh + (uint32_t)(r * 128 + ((k ^ (r & 7)) << 4)),
+                 make_float4(acc[c0 + 4 * k], acc[c0 + 4 * k + 1], acc[c0 + 4 * k + 2], acc[c0 + 4 * k + 3]));
+        named_bar_sync(2 + half, 128);
+        if (!(g.dbg & 32)) {
+          const int k = lane % LPR;
+#pragma unroll 4
+          for (int it = 0; it < 32 / RPI; ++it) {
+            const int rr = quarter * 32 + it * RPI + lane / LPR;
+            const int ly = rr / g.TW, lx = rr - ly * g.TW;
+            const int oy = w.tc.ty * g.TH + ly, ox = w.tc.tx * g.TW + lx;
+            if (rr < rows && oy < g.Hc && ox < g.Wc) {
+              const float4 v = lds128(sh + (uint32_t)(rr * 128 + ((k ^ (rr & 7)) << 4)));
+              const float crr = Epi::kCenter ? cvec[(li & 1) * 128 + rr] : 0.f;
+              const typename Epi::Row row = epi.row(w.tc.b, w.tc.cls, oy, ox, crr);
+              const int col = w.n0 + cbase + c0 + 4 * k;
+              if (g.nsplit > 1)
+                epi.store_partial4(w.split, row, col, v);
+              else
+                epi.store4(row, col, v);
+            }
+          }
         }
+        named_bar_sync(2 + half, 128);
       }
+      if constexpr (Epi::kCenter) mbar_arrive(&cempty[li & 1]);
     }
   }
   if (prof && (warp <= 2 || warp == 6))
