@@ -180,6 +180,10 @@ int64_t rte_launch_count(int reset);
  * (idx = -1 only queries the count).  rte_timing_reset clears the aggregates.  Any output
  * pointer may be NULL.  Errors: RTE_EINVAL (idx out of range), RTE_ECUDA. */
 rte_status rte_timing_enable(int on);
+/* Experiments only: per-role cycle counters of the tensor-core GEMM (collected when the
+ * environment variable RTE_TC_DBG has bit 6 set); copies min(n, 16) counters, then zeroes them
+ * if reset != 0.  Slot meanings are listed in csrc/tc_gemm.cuh (g_tc_prof). */
+rte_status rte_debug_counters(uint64_t* out, int n, int reset);
 rte_status rte_timing_reset(void);
 rte_status rte_timing_get(int idx, char* name, int name_len, int* kind, int64_t* launches, double* ms,
                           double* flops, double* bytes, int* count);

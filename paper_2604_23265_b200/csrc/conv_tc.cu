@@ -338,6 +338,17 @@ bool conv_tc_try(const ConvDesc& d, const float* in, float* out, const float* ad
 }
 
 // Upload the tensor-core operand layouts of every conv weight and size the split-K workspace.
+// Per-role GEMM cycle counters (tc_gemm.cuh, RTE_TC_DBG bit 6): copy out and optionally reset.
+void tc_debug_counters(unsigned long long* out, int n, bool reset) {
+  unsigned long long h[16];
+  RTE_CHECK_CUDA(cudaMemcpyFromSymbol(h, tc::g_tc_prof, sizeof(h)));
+  for (int i = 0; i < n && i < 16; ++i) out[i] = h[i];
+  if (reset) {
+    unsigned long long z[16] = {0};
+    RTE_CHECK_CUDA(cudaMemcpyToSymbol(tc::g_tc_prof, z, sizeof(z)));
+  }
+}
+
 void conv_tc_prepare(mgnet_net* net) {
   net->tc = (getenv("RTE_DISABLE_TC") == nullptr);
   if (!net->tc) return;

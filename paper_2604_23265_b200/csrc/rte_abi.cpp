@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "common.h"
+#include "mgnet.h"
 
 namespace rte {
 
@@ -216,6 +217,13 @@ int64_t rte_launch_count(int reset) {
   int64_t v = g_launches;
   if (reset) g_launches = 0;
   return v;
+}
+
+rte_status rte_debug_counters(uint64_t* out, int n, int reset) {
+  RTE_API_BEGIN
+  RTE_REQUIRE(out && n > 0, "rte_debug_counters: bad argument");
+  tc_debug_counters(reinterpret_cast<unsigned long long*>(out), n, reset != 0);
+  RTE_API_END
 }
 
 rte_status rte_timing_enable(int on) {

@@ -168,7 +168,13 @@ __device__ __forceinline__ void a_origin(const Geom& g, const TileCoord& c, int 
   }
 }
 
-// dbg bit6: block 0 reports per-role cycles spent waiting (printf at exit; experiments only)
+// dbg bit6: per-role cycle counters accumulated over all CTAs into g_tc_prof (experiments only;
+// read with rte_debug_counters).  Slots: 0 producer total, 1 producer wait; 2 MMA total, 3 MMA
+// wait conv+bfull, 4 MMA wait mempty/xempty, 5 MMA issue; 6 converter total, 7 converter wait,
+// 8 converter work; 9 promoter total, 10 promoter wait mfull, 11 promoter TMEM loads,
+// 12 epilogue; 13 K blocks (per CTA, producer); 14 units.
+__device__ unsigned long long g_tc_prof[16];
+
 __device__ __forceinline__ void tw_wait(uint64_t* bar, uint32_t par, bool on, long long& acc) {
   if (!on) {
     mbar_wait(bar, par);
@@ -219,7 +225,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int units = g.mtiles * g.ntiles * g.nsplit;
   const int rows = g.TW * g.TH;
   const uint32_t a_bytes = HALO ? (uint32_t)((g.TW + 2) * (g.TH + 2)) * 128u : (uint32_t)rows * 128u;
-  const bool prof = (g.dbg & 64) && blockIdx.x == 0 && lane == 0;
+  // bit6 enables the counters; bits 8..15 (if set) restrict them to kernels with that BN, bit16 to
+  // halo kernels
+  const bool prof = (g.dbg & 64) && lane == 0 && (((g.dbg >> 8) & 0xff) == 0 || ((g.dbg >> 8) & 0xff) == BN) &&
+                    (!((g.dbg >> 16) & 1) || HALO);
+  long long w_d = 0, w_e = 0;
   long long w_a = 0, w_b = 0, w_c = 0;
   const long long t_start = clock64();
   int n_kb = 0;
@@ -334,6 +344,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           const uint32_t sb = smem_u32(bring + bs * PL::kBSlot);
           const uint64_t d_bh = sdesc_sw128(sb), d_bl = sdesc_sw128(sb + BBYTES);
           const uint32_t a_hi = tmem_a + (uint32_t)(64 * ab), a_lo = a_hi + 32;
+          const long long ti0 = prof ? clock64() : 0;
           if (!no_mma) {
             if constexpr (FUSED) {
               // hi.[B_hi; B_lo] -> [main_t | X_t] (N = 2BN), lo.B_hi -> X_t
@@ -360,6 +371,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
           mma_commit_elect(&bempty[bs]);
           mma_commit_elect(&afree[ab]);
+          if (prof) w_d += clock64() - ti0;
           if (++bs == NBR) { bs = 0; bph ^= 1; }
           if (++ab == NA) { ab = 0; abph ^= 1; }
         }
@@ -391,6 +403,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if (HALO) arow = (ly + tap / 3) * (g.TW + 2) + lx + tap % 3;
         const uint32_t row_s = smem_u32(aring + as * PL::kASlot) + (uint32_t)arow * 128u;
         const bool skip = (g.dbg & 1) != 0;
+        const long long tc0 = prof ? clock64() : 0;
         float hi[32], lo[32];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
@@ -432,6 +445,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&conv[ab]);
+        if (prof) w_d += clock64() - tc0;
         if (++ab == NA) { ab = 0; abph ^= 1; }
       }
     }
@@ -455,6 +469,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const int t = gcount & 1;
         tw_wait(&mfull[t], (uint32_t)(gcount >> 1) & 1u, prof, w_a);
         tc_fence_after();
+        const long long tl0 = prof ? clock64() : 0;
         // fused form: main_t at t*2BN, X_t at t*2BN + BN; split form: main_t at t*BN
         const uint32_t mcol = FUSED ? (uint32_t)(t * 2 * BN) : (uint32_t)(t * BN);
 #pragma unroll
@@ -472,7 +487,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&mempty[t]);
+        if (prof) w_b += clock64() - tl0;
       }
+      const long long te0 = prof ? clock64() : 0;
       if constexpr (!FUSED) {
         // the unit's last group commit covers every MMA of the unit, including the X buffer
 #pragma unroll
@@ -524,11 +541,31 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         named_bar_sync(2 + half, 128);
       }
       if constexpr (Epi::kCenter) mbar_arrive(&cempty[li & 1]);
+      if (prof) w_e += clock64() - te0;
     }
   }
-  if (prof && (warp <= 2 || warp == 6))
-    printf("tcprof BN=%d units=%d grid=%d warp=%d kb=%d total=%lld waitA=%lld waitB=%lld waitC=%lld\n", BN, units,
-           gridDim.x, warp, n_kb, clock64() - t_start, w_a, w_b, w_c);
+  if (prof && (warp <= 2 || warp == 6)) {
+    const unsigned long long tot = (unsigned long long)(clock64() - t_start);
+    if (warp == 0) {
+      atomicAdd(&g_tc_prof[0], tot);
+      atomicAdd(&g_tc_prof[1], (unsigned long long)(w_a + w_b));
+      atomicAdd(&g_tc_prof[13], (unsigned long long)n_kb);
+    } else if (warp == 1) {
+      atomicAdd(&g_tc_prof[2], tot);
+      atomicAdd(&g_tc_prof[3], (unsigned long long)w_a);
+      atomicAdd(&g_tc_prof[4], (unsigned long long)(w_b + w_c));
+      atomicAdd(&g_tc_prof[5], (unsigned long long)w_d);
+    } else if (warp == 2) {
+      atomicAdd(&g_tc_prof[6], tot);
+      atomicAdd(&g_tc_prof[7], (unsigned long long)(w_a + w_b));
+      atomicAdd(&g_tc_prof[8], (unsigned long long)w_d);
+    } else {
+      atomicAdd(&g_tc_prof[9], tot);
+      atomicAdd(&g_tc_prof[10], (unsigned long long)w_a);
+      atomicAdd(&g_tc_prof[11], (unsigned long long)w_b);
+      atomicAdd(&g_tc_prof[12], (unsigned long long)w_e);
+    }
+  }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
