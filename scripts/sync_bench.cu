@@ -85,7 +85,7 @@ __global__ void fanin(long long* out, int iters) {
   if (threadIdx.x == 0) out[3] = (clock64() - t0) / iters;
 }
 
-int main() {
+int main1() {
   long long* d;
   cudaMalloc(&d, 8 * sizeof(long long));
   cudaMemset(d, 0, 8 * sizeof(long long));
@@ -100,4 +100,72 @@ int main() {
   printf("tcgen05.commit issue only: %lld cycles\n", h[2]);
   printf("4-warp fan-in + reply round trip: %lld cycles\n", h[3]);
   return 0;
+}
+// (appended) costs of per-K-block instructions: tcgen05 fences, clock64, tcgen05.st + wait::st
+__global__ void misc_costs(long long* out, int iters) {
+  __shared__ uint32_t slot;
+  if (threadIdx.x < 32) tmem_alloc(&slot, 128);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tm = slot;
+  float v[32];
+  for (int i = 0; i < 32; ++i) v[i] = (float)i;
+  if (threadIdx.x < 32) {
+    long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) tc_fence_after();
+    long long t1 = clock64();
+    for (int i = 0; i < iters; ++i) tc_fence_before();
+    long long t2 = clock64();
+    long long acc = 0;
+    for (int i = 0; i < iters; ++i) acc += clock64();
+    long long t3 = clock64();
+    for (int i = 0; i < iters; ++i) {
+      tmem_st32(tm, v);
+      tmem_wait_st();
+    }
+    long long t4 = clock64();
+    for (int i = 0; i < iters; ++i) {
+      tmem_st32(tm, v);
+      tmem_st32(tm + 32, v);
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+    }
+    long long t5 = clock64();
+    float w[32];
+    for (int i = 0; i < iters; ++i) tmem_ld32(tm, w);
+    long long t6 = clock64();
+    if (threadIdx.x == 0) {
+      out[4] = (t1 - t0) / iters;
+      out[5] = (t2 - t1) / iters;
+      out[6] = (t3 - t2) / iters + (acc == 42);
+      out[7] = (t4 - t3) / iters;
+      out[8] = (t5 - t4) / iters;
+      out[9] = (t6 - t5) / iters + (w[3] == 1234.f);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) tmem_dealloc(tm, 128);
+}
+
+int main2() {
+  long long* d;
+  cudaMalloc(&d, 16 * sizeof(long long));
+  misc_costs<<<1, 128>>>(d, 1000);
+  cudaError_t e = cudaDeviceSynchronize();
+  long long h[16];
+  cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  printf("tcgen05.fence::after_thread_sync: %lld cycles (%s)\n", h[4], cudaGetErrorString(e));
+  printf("tcgen05.fence::before_thread_sync: %lld cycles\n", h[5]);
+  printf("clock64: %lld cycles\n", h[6]);
+  printf("tcgen05.st x32 + wait::st: %lld cycles\n", h[7]);
+  printf("2x tcgen05.st x32 + wait::st + fence + syncwarp: %lld cycles\n", h[8]);
+  printf("tcgen05.ld x32 + wait::ld: %lld cycles\n", h[9]);
+  return 0;
+}
+int main() {
+  main1();
+  return main2();
 }
