@@ -384,8 +384,8 @@ def main():
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--reorth", type=int, default=0, choices=[0, 1, 2],
-                    help="Gram-Schmidt: 0 CGS2 (default), 1 CGS1, 2 selective re-orthogonalisation")
+    ap.add_argument("--reorth", type=int, default=2, choices=[0, 1, 2],
+                    help="Gram-Schmidt: 2 selective re-orthogonalisation (default), 0 CGS2, 1 CGS1")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

@@ -142,8 +142,9 @@ typedef struct {
   int maxit;         /* cap on total inner iterations per sample */
   double rtol;       /* stop when ||b - A x|| <= rtol ||b|| */
   int precond;       /* 0 none, 1 MgNet (I + V) */
-  int reorth;        /* 0 = CGS2: two classical Gram-Schmidt passes (default); 1 = one CGS pass;
-                        2 = selective (DGKS): the second pass runs only when ||v'|| < ||w||/sqrt(2) */
+  int reorth;        /* 0 = CGS2: two classical Gram-Schmidt passes; 1 = one CGS pass;
+                        2 = selective (DGKS, recommended): the second pass runs only when
+                        ||v'|| < ||w||/sqrt(2), decided on the device */
   int precision;     /* 0 = mixed (default): float32 Krylov basis, operator apply and V-cycle, float64
                         iterate, reductions and restart residual;  1 = everything in float64 (basis,
                         apply, V-cycle on SIMT kernels): for tight tolerances and iteration-count

@@ -178,9 +178,10 @@ def mgnet_vcycle_f64(net: MgNet, r, z, add_identity: bool = True, stream=None) -
 
 
 def gmres_solve(p: Problem, net: Optional[MgNet], b, x, *, restart: int = 30, maxit: int = 1000,
-                rtol: float = 1e-8, precond: Optional[int] = None, reorth: int = 0, precision: int = 0,
+                rtol: float = 1e-8, precond: Optional[int] = None, reorth: int = 2, precision: int = 0,
                 history: bool = True, hessenberg: bool = False, stream=None):
     """Restarted right-preconditioned GMRES; x (float64 CUDA tensor) holds x0 on entry, x on exit.
+    reorth: 2 = selective re-orthogonalisation (default), 0 = CGS2, 1 = CGS1 (gmres_opts).
 
     Returns a list of per-sample dicts (iterations, restarts, converged, breakdown, relres_true,
     relres_est, history [, hessenberg])."""
