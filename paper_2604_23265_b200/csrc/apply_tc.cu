@@ -69,8 +69,8 @@ struct EpiApply {
 template <int BN>
 void launch_apply_bn(const Geom& g, int mtiles, const CUtensorMap& ta, const CUtensorMap& tbh,
                      const CUtensorMap& tbl, const EpiApply& epi, cudaStream_t st) {
-  auto kern = gemm3xtf32_kernel<BN, false, EpiApply>;
-  constexpr int smem = gemm_smem_bytes<BN, false>();
+  auto kern = gemm3xtf32_kernel<BN, false, false, EpiApply>;
+  constexpr int smem = gemm_smem_bytes<BN, false, false>();
   ensure_smem((const void*)kern, smem);
   const int grid = std::min(mtiles * g.ntiles, num_sms());
   kern<<<grid, kGemmThreads, smem, st>>>(ta, tbh, tbl, g, epi);

@@ -19,6 +19,7 @@
 #include <mutex>
 #include <set>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "mgnet.h"
@@ -69,6 +70,17 @@ CUtensorMap make_map_act(const float* base, int C, int W, int H, int B, int box_
   cuuint32_t box[4] = {32u, (cuuint32_t)(box_w * es), (cuuint32_t)(box_h * es), 1u};
   cuuint32_t est[4] = {1u, (cuuint32_t)es, (cuuint32_t)es, 1u};
   encode(&m, 4, base, dims, strides, box, est);
+  return m;
+}
+
+CUtensorMap make_map_act_split(const float* base, int C, int W, int H, int B, int box_w, int box_h, int es) {
+  CUtensorMap m;
+  cuuint64_t dims[5] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, 2u, (cuuint64_t)B};
+  const cuuint64_t plane = (cuuint64_t)H * W * C * 4;
+  cuuint64_t strides[4] = {(cuuint64_t)C * 4, (cuuint64_t)W * C * 4, plane, 2 * plane};
+  cuuint32_t box[5] = {32u, (cuuint32_t)(box_w * es), (cuuint32_t)(box_h * es), 1u, 1u};
+  cuuint32_t est[5] = {1u, (cuuint32_t)es, (cuuint32_t)es, 1u, 1u};
+  encode(&m, 5, base, dims, strides, box, est);
   return m;
 }
 
@@ -128,8 +140,20 @@ struct EpiConv {
   float sign;
   int alpha_stride, a_in, a_add;
   int mode, Ho, Wo, Co;
+  int out_split;  // output and addend stored as hi/lo planes (ConvDesc::out_split)
 
+  __device__ __forceinline__ long long plane() const { return (long long)Ho * Wo * Co; }
+  // offset of (pixel, col) in the output layout (plane 0 for split outputs)
   __device__ __forceinline__ long long index(int b, int cls, int oy, int ox, int col) const {
+    int Y = oy, X = ox;
+    if (mode == 2) {
+      Y = 2 * oy + (cls >> 1);
+      X = 2 * ox + (cls & 1);
+    }
+    return (((long long)b * (out_split ? 2 : 1) * Ho + Y) * Wo + X) * Co + col;
+  }
+  // offset of (pixel, col) in the plain partial-sum layout of split-K
+  __device__ __forceinline__ long long pindex(int b, int cls, int oy, int ox, int col) const {
     int Y = oy, X = ox;
     if (mode == 2) {
       Y = 2 * oy + (cls >> 1);
@@ -139,33 +163,53 @@ struct EpiConv {
   }
   struct Row {
     long long o;  // output offset of column 0 of this pixel
+    long long po; // partial-sum offset of column 0 (split-K)
     float si, sa;
   };
   __device__ __forceinline__ Row row(int b, int cls, int oy, int ox, float) const {
     const float al = alpha ? (float)alpha[(long long)b * alpha_stride] : 1.f;
-    return Row{index(b, cls, oy, ox, 0), sign * (a_in ? al : 1.f), a_add ? al : 1.f};
+    return Row{index(b, cls, oy, ox, 0), pindex(b, cls, oy, ox, 0), sign * (a_in ? al : 1.f), a_add ? al : 1.f};
   }
   __device__ __forceinline__ void store4(const Row& rw, int col, float4 v) const {
     const long long o = rw.o + col;
     float4 r = make_float4(rw.si * v.x, rw.si * v.y, rw.si * v.z, rw.si * v.w);
     if (addend) {
-      const float4 a = *reinterpret_cast<const float4*>(addend + o);
+      float4 a = *reinterpret_cast<const float4*>(addend + o);
+      if (out_split) {
+        const float4 l = *reinterpret_cast<const float4*>(addend + o + plane());
+        a.x += l.x;
+        a.y += l.y;
+        a.z += l.z;
+        a.w += l.w;
+      }
       r.x = fmaf(rw.sa, a.x, r.x);
       r.y = fmaf(rw.sa, a.y, r.y);
       r.z = fmaf(rw.sa, a.z, r.z);
       r.w = fmaf(rw.sa, a.w, r.w);
     }
-    *reinterpret_cast<float4*>(out + o) = r;
+    if (out_split) {
+      float4 h, l;
+      split_tf32_fast(r.x, h.x, l.x);
+      split_tf32_fast(r.y, h.y, l.y);
+      split_tf32_fast(r.z, h.z, l.z);
+      split_tf32_fast(r.w, h.w, l.w);
+      *reinterpret_cast<float4*>(out + o) = h;
+      *reinterpret_cast<float4*>(out + o + plane()) = l;
+    } else {
+      *reinterpret_cast<float4*>(out + o) = r;
+    }
   }
   __device__ __forceinline__ void store_partial4(int split, const Row& rw, int col, float4 v) const {
-    *reinterpret_cast<float4*>(part + split * part_stride + rw.o + col) = v;
+    *reinterpret_cast<float4*>(part + split * part_stride + rw.po + col) = v;
   }
 };
 
 // Deterministic split-K reduction + epilogue: out[e] = s_in * sum_s partial[s][e] + s_add * addend[e].
+// With out_split the output (and the addend) are hi/lo planes: sample b's planes at 2b, 2b+1.
 __global__ void splitk_reduce_kernel(const float4* __restrict__ part, long long stride4, int nsplit, float4* out,
                                      const float4* addend, float sign, const double* __restrict__ alpha,
-                                     int alpha_stride, int a_in, int a_add, long long n4, long long per_sample4) {
+                                     int alpha_stride, int a_in, int a_add, long long n4, long long per_sample4,
+                                     int out_split) {
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n4; e += (long long)gridDim.x * blockDim.x) {
     float4 s = part[e];
     for (int k = 1; k < nsplit; ++k) {
@@ -179,14 +223,33 @@ __global__ void splitk_reduce_kernel(const float4* __restrict__ part, long long 
     const float al = alpha ? (float)alpha[(long long)b * alpha_stride] : 1.f;
     const float si = sign * (a_in ? al : 1.f), sa = a_add ? al : 1.f;
     float4 r = make_float4(si * s.x, si * s.y, si * s.z, si * s.w);
+    // output offset: plain e, split (b, plane 0) = e + b * per_sample4
+    const long long o = out_split ? e + (long long)b * per_sample4 : e;
     if (addend) {
-      const float4 a = addend[e];
+      float4 a = addend[o];
+      if (out_split) {
+        const float4 l = addend[o + per_sample4];
+        a.x += l.x;
+        a.y += l.y;
+        a.z += l.z;
+        a.w += l.w;
+      }
       r.x = fmaf(sa, a.x, r.x);
       r.y = fmaf(sa, a.y, r.y);
       r.z = fmaf(sa, a.z, r.z);
       r.w = fmaf(sa, a.w, r.w);
     }
-    out[e] = r;
+    if (out_split) {
+      float4 h, l;
+      split_tf32_fast(r.x, h.x, l.x);
+      split_tf32_fast(r.y, h.y, l.y);
+      split_tf32_fast(r.z, h.z, l.z);
+      split_tf32_fast(r.w, h.w, l.w);
+      out[o] = h;
+      out[o + per_sample4] = l;
+    } else {
+      out[o] = r;
+    }
   }
 }
 
@@ -269,11 +332,11 @@ Plan make_plan(const ConvDesc& d) {
   return P;
 }
 
-template <int BN, bool HALO>
+template <int BN, bool HALO, bool ASPLIT>
 void launch_bn(const Plan& P, const CUtensorMap& ta, const CUtensorMap& tbh, const CUtensorMap& tbl,
                const tc::EpiConv& epi, cudaStream_t st) {
-  auto kern = tc::gemm3xtf32_kernel<BN, HALO, tc::EpiConv>;
-  constexpr int smem = tc::gemm_smem_bytes<BN, HALO>();
+  auto kern = tc::gemm3xtf32_kernel<BN, HALO, ASPLIT, tc::EpiConv>;
+  constexpr int smem = tc::gemm_smem_bytes<BN, HALO, ASPLIT>();
   tc::ensure_smem((const void*)kern, smem);
   const long long units = (long long)P.mtiles * P.ntiles * P.g.nsplit;
   const int grid = (int)std::min<long long>(units, num_sms());
@@ -289,8 +352,9 @@ bool conv_tc_try(const ConvDesc& d, const float* in, float* out, const float* ad
   if (!P.ok) return false;
   const tc::Geom& g = P.g;
   const int es = (d.mode == 1) ? 2 : 1;
-  CUtensorMap ta = P.halo ? tc::make_map_act(in, d.Ci, d.Wi, d.Hi, d.B, g.TW + 2, g.TH + 2, 1)
-                          : tc::make_map_act(in, d.Ci, d.Wi, d.Hi, d.B, g.TW, g.TH, es);
+  const int bw = P.halo ? g.TW + 2 : g.TW, bh = P.halo ? g.TH + 2 : g.TH, ees = P.halo ? 1 : es;
+  CUtensorMap ta = d.in_split ? tc::make_map_act_split(in, d.Ci, d.Wi, d.Hi, d.B, bw, bh, ees)
+                              : tc::make_map_act(in, d.Ci, d.Wi, d.Hi, d.B, bw, bh, ees);
   CUtensorMap tbh = tc::make_map_kmajor(d.w->d_hi, d.w->tc_K, d.w->tc_rows, P.BN);
   CUtensorMap tbl = tc::make_map_kmajor(d.w->d_lo, d.w->tc_K, d.w->tc_rows, P.BN);
   tc::EpiConv epi;
@@ -305,6 +369,7 @@ bool conv_tc_try(const ConvDesc& d, const float* in, float* out, const float* ad
   epi.Ho = d.Ho;
   epi.Wo = d.Wo;
   epi.Co = d.Co;
+  epi.out_split = d.out_split ? 1 : 0;
   epi.part = nullptr;
   epi.part_stride = P.out_elems;
   if (g.nsplit > 1) {
@@ -315,10 +380,20 @@ bool conv_tc_try(const ConvDesc& d, const float* in, float* out, const float* ad
     epi.part = d.ws_owner->tc_ws;
   }
   prof_begin(st);
+  auto dispatch = [&](auto bn_tag) {
+    constexpr int BN = decltype(bn_tag)::value;
+    if (P.halo) {
+      if (d.in_split) launch_bn<BN, true, true>(P, ta, tbh, tbl, epi, st);
+      else launch_bn<BN, true, false>(P, ta, tbh, tbl, epi, st);
+    } else {
+      if (d.in_split) launch_bn<BN, false, true>(P, ta, tbh, tbl, epi, st);
+      else launch_bn<BN, false, false>(P, ta, tbh, tbl, epi, st);
+    }
+  };
   switch (P.BN) {
-    case 32: P.halo ? launch_bn<32, true>(P, ta, tbh, tbl, epi, st) : launch_bn<32, false>(P, ta, tbh, tbl, epi, st); break;
-    case 64: P.halo ? launch_bn<64, true>(P, ta, tbh, tbl, epi, st) : launch_bn<64, false>(P, ta, tbh, tbl, epi, st); break;
-    default: P.halo ? launch_bn<128, true>(P, ta, tbh, tbl, epi, st) : launch_bn<128, false>(P, ta, tbh, tbl, epi, st); break;
+    case 32: dispatch(std::integral_constant<int, 32>{}); break;
+    case 64: dispatch(std::integral_constant<int, 64>{}); break;
+    default: dispatch(std::integral_constant<int, 128>{}); break;
   }
   const bool split = g.nsplit > 1;
   after_launch(conv_class_name(d, true), st, conv_flops(d), split ? 0.0 : conv_bytes(d, addend != nullptr), 1);
@@ -330,7 +405,8 @@ bool conv_tc_try(const ConvDesc& d, const float* in, float* out, const float* ad
     tc::splitk_reduce_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const float4*>(d.ws_owner->tc_ws), n4,
                                                      g.nsplit, reinterpret_cast<float4*>(out),
                                                      reinterpret_cast<const float4*>(addend), sign, alpha,
-                                                     alpha_stride, epi.a_in, epi.a_add, n4, per4);
+                                                     alpha_stride, epi.a_in, epi.a_add, n4, per4,
+                                                     d.out_split ? 1 : 0);
     // the conv's algorithmic bytes are booked on the reduction (it writes the output)
     after_launch("splitk_reduce", st, 0.0, conv_bytes(d, addend != nullptr) + 4.0 * g.nsplit * P.out_elems, 0);
   }

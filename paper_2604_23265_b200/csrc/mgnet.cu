@@ -24,11 +24,14 @@ namespace {
 // MODE 0: KSxKS conv, stride 1, pad KS/2.  MODE 1: 3x3 conv, stride 2, pad 1.
 // MODE 2: 4x4 transposed conv, stride 2, pad 1, one output parity class per blockIdx.z % 4.
 // out = (addend ? add_scale*addend : 0) + sign * in_scale * acc
-template <typename T, int MODE, int KS, int TCO>
+template <typename T, int MODE, int KS, int TCO, bool IN_SPLIT, bool OUT_SPLIT>
 __global__ void __launch_bounds__(256) conv_simt_kernel(
     int Hi, int Wi, int Ci, int Ho, int Wo, int Co, const T* __restrict__ in, const T* __restrict__ Wk,
     T* out, const T* addend, float sign, const double* __restrict__ alpha, int alpha_stride,
     int alpha_on_input, int alpha_on_addend) {
+  // split formats (float only): value = hi plane + lo plane, planes Hi*Wi*Ci (in) / Ho*Wo*Co (out) apart
+  const int64_t in_plane = IN_SPLIT ? (int64_t)Hi * Wi * Ci : 0;
+  const int64_t out_plane = OUT_SPLIT ? (int64_t)Ho * Wo * Co : 0;
   constexpr int TP = 4096 / TCO;
   constexpr int KC = 16;
   constexpr int TX = TCO / 4;
@@ -51,7 +54,7 @@ __global__ void __launch_bounds__(256) conv_simt_kernel(
   const int64_t npix = (int64_t)Hc * Wc;
   const int64_t p0 = (int64_t)blockIdx.x * TP;
   const int co0 = blockIdx.y * TCO;
-  const T* inb = in + (int64_t)b * Hi * Wi * Ci;
+  const T* inb = in + (int64_t)b * Hi * Wi * Ci * (IN_SPLIT ? 2 : 1);
   T acc[4][4];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
@@ -90,7 +93,11 @@ __global__ void __launch_bounds__(256) conv_simt_kernel(
             ok = (yy >= 0) && (xx >= 0);
           }
           ok = ok && yi >= 0 && yi < Hi && xi >= 0 && xi < Wi;
-          if (ok) v = inb[((int64_t)yi * Wi + xi) * Ci + ci0 + kk];
+          if (ok) {
+            const int64_t ii = ((int64_t)yi * Wi + xi) * Ci + ci0 + kk;
+            v = inb[ii];
+            if (IN_SPLIT) v += inb[ii + in_plane];
+          }
         }
         As[kk][pl] = v;
       }
@@ -130,14 +137,24 @@ __global__ void __launch_bounds__(256) conv_simt_kernel(
     } else {
       opix = p;
     }
-    int64_t base = ((int64_t)b * Ho * Wo + opix) * Co;
+    int64_t base = ((int64_t)b * Ho * Wo * (OUT_SPLIT ? 2 : 1) + opix) * Co;
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       int co = co0 + tx * 4 + c;
       if (co >= Co) continue;
       T v = s_in * acc[a][c];
-      if (addend) v += s_add * addend[base + co];
-      out[base + co] = v;
+      if (addend) {
+        T av = addend[base + co];
+        if (OUT_SPLIT) av += addend[base + co + out_plane];
+        v += s_add * av;
+      }
+      if constexpr (OUT_SPLIT) {
+        const float hi = __uint_as_float((__float_as_uint((float)v) + 0x1000u) & 0xFFFFE000u);
+        out[base + co] = hi;
+        out[base + co + out_plane] = (float)v - hi;
+      } else {
+        out[base + co] = v;
+      }
     }
   }
 }
@@ -187,9 +204,22 @@ void launch_conv_t(const ConvDesc& d, const T* in, const T* Wk, T* out, const T*
     int64_t npix = (MODE == 2) ? (int64_t)(d.Ho / 2) * (d.Wo / 2) : (int64_t)d.Ho * d.Wo;
     dim3 grid((unsigned)((npix + TP - 1) / TP), (unsigned)((d.Co + TCO - 1) / TCO),
               (unsigned)(d.B * (MODE == 2 ? 4 : 1)));
-    conv_simt_kernel<T, MODE, KS, TCO><<<grid, 256, 0, st>>>(d.Hi, d.Wi, d.Ci, d.Ho, d.Wo, d.Co, in, Wk, out, addend,
-                                                          sign, alpha, alpha_stride, alpha_on_input ? 1 : 0,
-                                                          alpha_on_addend ? 1 : 0);
+    auto launch = [&](auto ins, auto outs) {
+      constexpr bool IS = decltype(ins)::value, OS = decltype(outs)::value;
+      conv_simt_kernel<T, MODE, KS, TCO, IS, OS><<<grid, 256, 0, st>>>(
+          d.Hi, d.Wi, d.Ci, d.Ho, d.Wo, d.Co, in, Wk, out, addend, sign, alpha, alpha_stride,
+          alpha_on_input ? 1 : 0, alpha_on_addend ? 1 : 0);
+    };
+    using TT = std::true_type;
+    using FF = std::false_type;
+    if constexpr (std::is_same<T, float>::value) {
+      if (d.in_split && d.out_split) launch(TT{}, TT{});
+      else if (d.in_split) launch(TT{}, FF{});
+      else if (d.out_split) launch(FF{}, TT{});
+      else launch(FF{}, FF{});
+    } else {
+      launch(FF{}, FF{});
+    }
   };
   auto by_tco = [&](auto mode_tag, auto ks_tag) {
     if (d.Co <= 16) go(mode_tag, ks_tag, std::integral_constant<int, 16>{});
@@ -325,7 +355,9 @@ rte_status mgnet_create(const rte_problem* p, int levels, int c0, int nu, const 
         L.R = take(0, 2 * C, C, 3);
         L.P = take(1, C, 2 * C, 4);  // IOHW: Ci = 2C (coarse), Co = C (fine)
       }
-      size_t act = (size_t)p->B * L.H * L.H * C;
+      // levels whose convs run on the tensor cores keep their activations pre-split (hi/lo planes)
+      L.split = getenv("RTE_DISABLE_TC") == nullptr && C % 32 == 0;
+      size_t act = (size_t)p->B * L.H * L.H * C * (L.split ? 2 : 1);
       L.f = dalloc<float>(act);
       L.u = dalloc<float>(act);
       L.t = dalloc<float>(act);
@@ -435,6 +467,8 @@ template <typename T>
 void vcycle_run_t(const mgnet_net* net, const T* r, T* z, bool add_identity, const double* alpha,
                   int alpha_stride, cudaStream_t st) {
   const int L = net->L, M = net->M, N = net->N;
+  constexpr bool F32 = std::is_same<T, float>::value;
+  auto sp = [&](int l) { return F32 && net->lv[l].split; };  // level l's activation format
   auto conv = [&](int widx, ConvDesc d, const T* in, T* out, const T* addend, float sign, bool a_in = false,
                   bool a_add = false) {
     d.w = &net->convs[widx];
@@ -449,11 +483,14 @@ void vcycle_run_t(const mgnet_net* net, const T* r, T* z, bool add_identity, con
   // f^0 = Lambda (alpha r)
   {
     const Level& L0 = net->lv[0];
-    conv(net->lift, desc_for(net, 0, 1, N, M, N, L0.C), r, bf[0].f, nullptr, 1.f, true, false);
+    ConvDesc d = desc_for(net, 0, 1, N, M, N, L0.C);
+    d.out_split = sp(0);
+    conv(net->lift, d, r, bf[0].f, nullptr, 1.f, true, false);
   }
   auto smooth = [&](int l, int bidx, bool first) {
     const Level& V = net->lv[l];
     ConvDesc d = desc_for(net, 0, 3, V.H, V.C, V.H, V.C);
+    d.in_split = d.out_split = sp(l);
     const Bufs& b = bf[l];
     if (first) {  // u = 0: u <- B * f  (A * 0 = 0 exactly)
       conv(bidx, d, b.f, b.u, nullptr, 1.f);
@@ -466,28 +503,38 @@ void vcycle_run_t(const mgnet_net* net, const T* r, T* z, bool add_identity, con
     const Level& V = net->lv[l];
     std::vector<int> steps(V.Bpre.begin(), V.Bpre.end());
     if (l == L - 1) steps.insert(steps.end(), V.Bpost.begin(), V.Bpost.end());
-    if (steps.empty()) RTE_CHECK_CUDA(cudaMemsetAsync(bf[l].u, 0, sizeof(T) * (size_t)net->B * V.H * V.H * V.C, st));
+    if (steps.empty())
+      RTE_CHECK_CUDA(cudaMemsetAsync(bf[l].u, 0, sizeof(T) * (size_t)net->B * V.H * V.H * V.C * (sp(l) ? 2 : 1), st));
     for (size_t i = 0; i < steps.size(); ++i) smooth(l, steps[i], i == 0);
     if (l < L - 1) {
       const Level& W = net->lv[l + 1];
       ConvDesc d = desc_for(net, 0, 3, V.H, V.C, V.H, V.C);
+      d.in_split = d.out_split = sp(l);
+      ConvDesc dr = desc_for(net, 1, 3, V.H, V.C, W.H, W.C);
+      dr.in_split = sp(l);
+      dr.out_split = sp(l + 1);
       if (steps.empty()) {
-        conv(V.R, desc_for(net, 1, 3, V.H, V.C, W.H, W.C), bf[l].f, bf[l + 1].f, nullptr, 1.f);
+        conv(V.R, dr, bf[l].f, bf[l + 1].f, nullptr, 1.f);
       } else {
-        conv(V.A, d, bf[l].u, bf[l].t, bf[l].f, -1.f);                                          // t = f - A * u
-        conv(V.R, desc_for(net, 1, 3, V.H, V.C, W.H, W.C), bf[l].t, bf[l + 1].f, nullptr, 1.f);  // f^{l+1} = R *_2 t
+        conv(V.A, d, bf[l].u, bf[l].t, bf[l].f, -1.f);   // t = f - A * u
+        conv(V.R, dr, bf[l].t, bf[l + 1].f, nullptr, 1.f);  // f^{l+1} = R *_2 t
       }
     }
   }
   for (int l = L - 2; l >= 0; --l) {
     const Level& V = net->lv[l];
     const Level& W = net->lv[l + 1];
-    conv(V.P, desc_for(net, 2, 4, W.H, W.C, V.H, V.C), bf[l + 1].u, bf[l].u, bf[l].u, 1.f);  // u += P^T *_2 u^{l+1}
+    ConvDesc dp = desc_for(net, 2, 4, W.H, W.C, V.H, V.C);
+    dp.in_split = sp(l + 1);
+    dp.out_split = sp(l);
+    conv(V.P, dp, bf[l + 1].u, bf[l].u, bf[l].u, 1.f);  // u += P^T *_2 u^{l+1}
     for (size_t i = 0; i < V.Bpost.size(); ++i) smooth(l, V.Bpost[i], false);
   }
   // z = [alpha r] + Theta u^0
   const Level& L0 = net->lv[0];
-  conv(net->head, desc_for(net, 0, 1, N, L0.C, N, M), bf[0].u, z, add_identity ? r : nullptr, 1.f, false, true);
+  ConvDesc dh = desc_for(net, 0, 1, N, L0.C, N, M);
+  dh.in_split = sp(0);
+  conv(net->head, dh, bf[0].u, z, add_identity ? r : nullptr, 1.f, false, true);
 }
 
 void vcycle_run(const mgnet_net* net, const float* r, float* z, bool add_identity, const double* alpha,

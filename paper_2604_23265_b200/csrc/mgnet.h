@@ -22,6 +22,9 @@ struct ConvW {
 
 struct ConvDesc {
   int B = 1, mode = 0, ks = 3;       // mode 0: stride-1 (ks 1 or 3), 1: stride-2 3x3, 2: transposed 4x4 s2
+  // Activation formats (float V-cycle): split = two planes per batch sample, hi = rna_tf32(v) and
+  // lo = v - hi ([B][2][H][W][C]); plain = [B][H][W][C].  The addend has the output's format.
+  bool in_split = false, out_split = false;
   int Hi = 0, Wi = 0, Ci = 0, Ho = 0, Wo = 0, Co = 0;
   const ConvW* w = nullptr;
   const struct ::mgnet_net* ws_owner = nullptr;  // net owning the split-K workspace (tensor-core path)
@@ -34,6 +37,7 @@ struct Level {
   float* f = nullptr;   // [B][H][H][C]
   float* u = nullptr;
   float* t = nullptr;
+  bool split = false;  // f, u, t stored as hi/lo planes (levels whose convs run on the tensor cores)
   double *f64 = nullptr, *u64 = nullptr, *t64 = nullptr;  // fp64 V-cycle buffers (first use)
 };
 

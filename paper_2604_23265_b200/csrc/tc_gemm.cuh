@@ -69,21 +69,22 @@ struct Geom {
 // ring, and the epilogue staging tiles (one 128 x 32 fp32 tile per column half).
 constexpr int kHaloRows = 208;                  // (TW+2)(TH+2) <= 208, e.g. 34 x 6 for a 32 x 4 tile
 constexpr int kStageBytes = kTileM * 128;       // 128 rows x 32 fp32 per column half
-template <int BN, bool HALO>
+template <int BN, bool HALO, bool ASPLIT = false>
 struct Plan {
   static constexpr int kBBytes = BN * 128;                          // one of B hi / B lo
-  static constexpr int kASlot = HALO ? kHaloRows * 128 : kABytes;   // 1 KB multiples
+  static constexpr int kATile = HALO ? kHaloRows * 128 : kABytes;   // one A tile (1 KB multiple)
+  static constexpr int kASlot = (ASPLIT ? 2 : 1) * kATile;          // split activations: hi + lo tiles
   static constexpr int kBSlot = 2 * kBBytes;
   static constexpr int kBudget = 190 * 1024;                        // rings
-  static constexpr int kNA = HALO ? 2 : 4;                          // A ring depth
+  static constexpr int kNA = (HALO || ASPLIT) ? 2 : 4;              // A ring depth
   static constexpr int kNBraw = (kBudget - kNA * kASlot) / kBSlot;
   static constexpr int kNB = kNBraw > 8 ? 8 : kNBraw;               // B ring depth
   static constexpr int kRingBytes = kNA * kASlot + kNB * kBSlot;
 };
 
-template <int BN, bool HALO>
+template <int BN, bool HALO, bool ASPLIT = false>
 constexpr int gemm_smem_bytes() {
-  return Plan<BN, HALO>::kRingBytes + 2 * kStageBytes + 1024 /*align*/ + 1024 /*barriers*/ +
+  return Plan<BN, HALO, ASPLIT>::kRingBytes + 2 * kStageBytes + 1024 /*align*/ + 1024 /*barriers*/ +
          1024 /*row centres*/;
 }
 
@@ -189,13 +190,17 @@ __device__ __forceinline__ void tw_wait(uint64_t* bar, uint32_t par, bool on, lo
 // valid pixel (oy, ox) of the class grid (c_row = the row centre when Epi::kCenter: the GEMM then
 // computed (a - c_row 1) . B^T); epi.store4(row, col, v4) finishes columns col .. col+3;
 // epi.store_partial4(split, row, col, v4) stores raw partial sums when split-K is active.
-template <int BN, bool HALO, class Epi>
+// ASPLIT: the A activation is stored pre-split as two planes (hi = rna_tf32(a), lo = a - hi; see
+// EpiConv) and the tensor map has a plane dimension; the converters then only copy rows into
+// TMEM.  Otherwise A is plain fp32 and the converters split it.
+template <int BN, bool HALO, bool ASPLIT, class Epi>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm3xtf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBhi,
                       const __grid_constant__ CUtensorMap tmBlo, const Geom g, const Epi epi) {
   static_assert(BN == 32 || BN == 64 || BN == 128, "N tile must be 32, 64 or 128");
   static_assert(!(HALO && Epi::kCenter), "row centring is for the 1x1 (apply) kernels");
-  using PL = Plan<BN, HALO>;
+  static_assert(!(ASPLIT && Epi::kCenter), "row centring needs the plain fp32 A operand");
+  using PL = Plan<BN, HALO, ASPLIT>;
   constexpr int NAR = PL::kNA, NBR = PL::kNB;
   constexpr int NA = tmem_abufs<BN>();
   constexpr int BBYTES = PL::kBBytes;
@@ -293,8 +298,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             if (g.dbg & 16) {
               mbar_arrive(&afull[as]);
             } else {
-              mbar_arrive_expect_tx(&afull[as], a_bytes);
-              tma_load_4d(aring + as * PL::kASlot, &tmA, &afull[as], cc * 32, xA, yA, w.tc.b);
+              uint8_t* sa = aring + as * PL::kASlot;
+              if (ASPLIT) {  // 5-D map (C, W, H, plane, B): hi tile then lo tile
+                mbar_arrive_expect_tx(&afull[as], 2u * a_bytes);
+                tma_load_5d(sa, &tmA, &afull[as], cc * 32, xA, yA, 0, w.tc.b);
+                tma_load_5d(sa + PL::kATile, &tmA, &afull[as], cc * 32, xA, yA, 1, w.tc.b);
+              } else {
+                mbar_arrive_expect_tx(&afull[as], a_bytes);
+                tma_load_4d(sa, &tmA, &afull[as], cc * 32, xA, yA, w.tc.b);
+              }
             }
           }
           __syncwarp();
@@ -408,11 +420,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           if (skip) break;
-          const float4 v = lds128(row_s + (uint32_t)((q ^ (arow & 7)) << 4));
+          const uint32_t qo = (uint32_t)((q ^ (arow & 7)) << 4);
+          const float4 v = lds128(row_s + qo);
           hi[4 * q] = v.x;
           hi[4 * q + 1] = v.y;
           hi[4 * q + 2] = v.z;
           hi[4 * q + 3] = v.w;
+          if (ASPLIT) {
+            const float4 l = lds128(row_s + PL::kATile + qo);
+            lo[4 * q] = l.x;
+            lo[4 * q + 1] = l.y;
+            lo[4 * q + 2] = l.z;
+            lo[4 * q + 3] = l.w;
+          }
         }
         // done with this A tile after its last K block
         const bool last_of_tile = !HALO || tap == 8 || kb + 1 == w.kb1;
@@ -431,10 +451,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             mbar_arrive(&cfull[li & 1]);
           }
         }
+        if (!ASPLIT) {
 #pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          const float x = Epi::kCenter ? hi[e] - c : hi[e];
-          split_tf32_fast(x, hi[e], lo[e]);
+          for (int e = 0; e < 32; ++e) {
+            const float x = Epi::kCenter ? hi[e] - c : hi[e];
+            split_tf32_fast(x, hi[e], lo[e]);
+          }
         }
         const uint32_t ta = tmem_a + (uint32_t)(64 * ab) + lane_base;
         if (!skip) {

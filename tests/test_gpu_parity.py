@@ -210,7 +210,7 @@ def test_mgnet_rejects_bad_weight_count():
 
 
 # ---------------------------------------------------------------------------------------
-def _gmres_pair(cfg, precond, rtol, maxit, std=0.02, reorth=0, precision=0):
+def _gmres_pair(cfg, precond, rtol, maxit, std=0.02, reorth=2, precision=0):
     import paper_2604_23265_b200 as P
     media = W.make_media(cfg)
     p = _gpu_problem(cfg, media)
