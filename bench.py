@@ -33,6 +33,8 @@ if ROOT not in sys.path:
 
 import numpy as np  # noqa: E402
 
+import benchlib  # noqa: E402
+
 METRIC = "GMRES iter/s (rte_apply + MgNet V-cycle) at N²×M; % of roofline"
 UNIT = "GMRES iter/s"
 TF32_PER_BF16 = 1.1 / 2.25      # guide's nominal dense ratio (B200_PROFILING.md table)
@@ -298,12 +300,8 @@ def run_ours(args, cfg):
     clocks = sampler.stop()
     iters = rep[0]["iterations"] if cfg.B == 1 else sum(r["iterations"] for r in rep) / cfg.B
     assert iters == K, f"solve ran {iters} iterations, expected {K}"
-    ms_max = ms
-    if dist is not None:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_max = float(t.item())
-    value = K * ws / (ms_max * 1e-3)
+    ms_max = benchlib.max_over_ranks(ms, dist, dev)
+    value = benchlib.aggregate(K, ws, ms_max)
 
     # ---- e2e: same solve through the public API with HOST buffers -----------------------
     b_host = torch.empty(p.shape, dtype=torch.float32, pin_memory=True)
@@ -321,11 +319,7 @@ def run_ours(args, cfg):
     e1.record(stream)
     torch.cuda.synchronize()
     barrier()
-    ms_e2e = e0.elapsed_time(e1)
-    if dist is not None:
-        t = torch.tensor([ms_e2e], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_e2e = float(t.item())
+    ms_e2e = benchlib.max_over_ranks(e0.elapsed_time(e1), dist, dev)
     h2d = b_host.numel() * 4
     d2h = x_host.numel() * 8
 
@@ -364,7 +358,7 @@ def run_ours(args, cfg):
                            "precision": "fp32 storage/arithmetic, fp64 iterate, reductions and restart residual",
                            "gram_schmidt": {0: "CGS2", 1: "CGS1", 2: "selective (DGKS)"}[args.reorth]},
                 "roofline": roof,
-                "e2e": {"value": K * ws / (ms_e2e * 1e-3), "unit": UNIT,
+                "e2e": {"value": benchlib.aggregate(K, ws, ms_e2e), "unit": UNIT,
                         "h2d_bytes_per_step": h2d / K, "d2h_bytes_per_step": d2h / K,
                         "note": f"one solve of K={K} iterations per measurement: b (fp32) copied H2D from pinned "
                                 "host memory before it and x (fp64) D2H after it; bytes amortised per step"},
