@@ -355,8 +355,9 @@ rte_status mgnet_create(const rte_problem* p, int levels, int c0, int nu, const 
         L.R = take(0, 2 * C, C, 3);
         L.P = take(1, C, 2 * C, 4);  // IOHW: Ci = 2C (coarse), Co = C (fine)
       }
-      // levels whose convs run on the tensor cores keep their activations pre-split (hi/lo planes)
-      L.split = getenv("RTE_DISABLE_TC") == nullptr && C % 32 == 0;
+      // levels whose convs run on the tensor cores may keep their activations pre-split (hi/lo planes)
+      // (opt-in: measured slower on the B200 -- the doubled plane traffic outweighs the saved splits)
+      L.split = getenv("RTE_DISABLE_TC") == nullptr && getenv("RTE_TC_PRESPLIT") != nullptr && C % 32 == 0;
       size_t act = (size_t)p->B * L.H * L.H * C * (L.split ? 2 : 1);
       L.f = dalloc<float>(act);
       L.u = dalloc<float>(act);

@@ -95,9 +95,16 @@ template <int BN>
 constexpr bool tmem_fused() {
   return BN <= 64;
 }
+// Fused form: NG group buffers of 2BN columns (the MMA can run NG - 1 groups ahead of the
+// promoters, so a tile's epilogue overlaps the next tile's K loop) and 2 A buffers.
+// Split form: 2 main buffers + X + the rest as A buffers.
+template <int BN>
+constexpr int tmem_groups() {
+  return tmem_fused<BN>() ? ((512 - 128) / (2 * BN) < 6 ? (512 - 128) / (2 * BN) : 6) : 2;
+}
 template <int BN>
 constexpr int tmem_acc_cols() {
-  return tmem_fused<BN>() ? 4 * BN : 3 * BN;
+  return tmem_fused<BN>() ? tmem_groups<BN>() * 2 * BN : 3 * BN;
 }
 template <int BN>
 constexpr int tmem_abufs() {
@@ -217,9 +224,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* bempty = bfull + NBR;      // [NBR] MMAs done with the B tiles
   uint64_t* conv = bempty + NBR;       // [NA] TMEM A buffer written (4 converter warps)
   uint64_t* afree = conv + NA;         // [NA] MMAs done with the TMEM A buffer
-  uint64_t* mfull = afree + NA;        // [2] main buffer ready for promotion
-  uint64_t* mempty = mfull + 2;        // [2] main buffer drained (8 promoter warps)
-  uint64_t* xempty = mempty + 2;       // [1] unit-long X drained (8 promoter warps)
+  constexpr int NG = tmem_groups<BN>();
+  uint64_t* mfull = afree + NA;        // [NG] group buffer ready for promotion
+  uint64_t* mempty = mfull + NG;       // [NG] group buffer drained (8 promoter warps)
+  uint64_t* xempty = mempty + NG;      // [1] unit-long X drained (8 promoter warps)
   uint64_t* cfull = xempty + 1;        // [2] row centres written (128 converter threads)
   uint64_t* cempty = cfull + 2;        // [2] row centres read (256 epilogue threads)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cempty + 2);
@@ -252,9 +260,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       mbar_init(&conv[i], 4);
       mbar_init(&afree[i], 1);
     }
-    for (int t = 0; t < 2; ++t) {
+    for (int t = 0; t < NG; ++t) {
       mbar_init(&mfull[t], 1);
       mbar_init(&mempty[t], 8);
+    }
+    for (int t = 0; t < 2; ++t) {
       mbar_init(&cfull[t], 128);
       mbar_init(&cempty[t], 256);
     }
@@ -344,8 +354,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
       uint32_t acc_x = 0;
       for (int kbg = w.kb0; kbg < w.kb1; kbg += kPromoteKB, ++gcount) {
-        const int t = gcount & 1;
-        tw_wait(&mempty[t], ((uint32_t)(gcount >> 1) & 1u) ^ 1u, prof, w_b);
+        const int t = gcount % NG;
+        tw_wait(&mempty[t], ((uint32_t)(gcount / NG) & 1u) ^ 1u, prof, w_b);
         tc_fence_after();
         uint32_t acc_m = 0;
         const int kbe = min(w.kb1, kbg + kPromoteKB);
@@ -488,8 +498,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
       for (int i = 0; i < HB; ++i) acc[i] = 0.f;
       for (int kbg = w.kb0; kbg < w.kb1; kbg += kPromoteKB, ++gcount) {
-        const int t = gcount & 1;
-        tw_wait(&mfull[t], (uint32_t)(gcount >> 1) & 1u, prof, w_a);
+        const int t = gcount % NG;
+        tw_wait(&mfull[t], (uint32_t)(gcount / NG) & 1u, prof, w_a);
         tc_fence_after();
         const long long tl0 = prof ? clock64() : 0;
         // fused form: main_t at t*2BN, X_t at t*2BN + BN; split form: main_t at t*BN
