@@ -182,7 +182,7 @@ int64_t rte_launch_count(int reset);
  * pointer may be NULL.  Errors: RTE_EINVAL (idx out of range), RTE_ECUDA. */
 rte_status rte_timing_enable(int on);
 /* Experiments only: per-role cycle counters of the tensor-core GEMM (collected when the
- * environment variable RTE_TC_DBG has bit 6 set); copies min(n, 16) counters, then zeroes them
+ * environment variable RTE_TC_DBG has bit 6 set); copies min(n, 24) counters, then zeroes them
  * if reset != 0.  Slot meanings are listed in csrc/tc_gemm.cuh (g_tc_prof). */
 rte_status rte_debug_counters(uint64_t* out, int n, int reset);
 rte_status rte_timing_reset(void);

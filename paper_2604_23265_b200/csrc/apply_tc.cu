@@ -36,32 +36,56 @@ struct EpiApply {
   const double* alpha;
   int alpha_stride, N, M;
 
+  static constexpr int kBatch = 4, kBatchWide = 2;
+  struct Col {
+    int m, sx, sy;
+    float4 a_x, a_y;
+  };
   struct Row {
     long long cell;
     int i, j;
     float st, ss, al, c;
   };
-  __device__ __forceinline__ Row row(int b, int, int j, int i, float c) const {
-    const long long cell = ((long long)b * N + j) * N + i;
-    return Row{cell, i, j, sig_t[cell], sig_s[cell], alpha ? (float)alpha[(long long)b * alpha_stride] : 1.f, c};
-  }
+  struct Pre {
+    float4 p, nx, ny;  // psi at the cell and at its two upwind neighbours (0 at inflow faces)
+  };
   // columns m .. m+3 share a quadrant (M % 16 == 0), hence both upwind signs
-  __device__ __forceinline__ void store4(const Row& rw, int m, float4 v) const {
+  __device__ __forceinline__ Col col(int m) const {
+    return Col{m, sgx[m], sgy[m], *reinterpret_cast<const float4*>(ax + m), *reinterpret_cast<const float4*>(ay + m)};
+  }
+  struct Tile {
+    long long cell0;  // cell of the tile origin
+    float al;
+  };
+  __device__ __forceinline__ Tile tile(int b, int, int j0, int i0) const {
+    return Tile{((long long)b * N + j0) * N + i0, alpha ? (float)alpha[(long long)b * alpha_stride] : 1.f};
+  }
+  __device__ __forceinline__ int rel(int ly, int lx) const { return ly * N + lx; }
+  // tile pixel (oy, ox) of the class grid = cell (j, i)
+  __device__ __forceinline__ Row row(const Tile& t, int rel, int j, int i, float c) const {
+    const long long cell = t.cell0 + rel;
+    return Row{cell, i, j, sig_t[cell], sig_s[cell], t.al, c};
+  }
+  __device__ __forceinline__ Pre load(const Row& rw, const Col& cv) const {
     const long long cell = rw.cell;
-    const int sx = sgx[m], sy = sgy[m];
-    const float4 a_x = *reinterpret_cast<const float4*>(ax + m);
-    const float4 a_y = *reinterpret_cast<const float4*>(ay + m);
-    const float4 p = *reinterpret_cast<const float4*>(x + cell * M + m);
-    float4 nx = make_float4(0.f, 0.f, 0.f, 0.f), ny = nx;
-    if ((unsigned)(rw.i - sx) < (unsigned)N) nx = *reinterpret_cast<const float4*>(x + (cell - sx) * M + m);
-    if ((unsigned)(rw.j - sy) < (unsigned)N) ny = *reinterpret_cast<const float4*>(x + (cell - (long long)sy * N) * M + m);
+    const int m = cv.m, sx = cv.sx, sy = cv.sy;
+    Pre q;
+    q.p = *reinterpret_cast<const float4*>(x + cell * M + m);
+    q.nx = make_float4(0.f, 0.f, 0.f, 0.f);
+    q.ny = q.nx;
+    if ((unsigned)(rw.i - sx) < (unsigned)N) q.nx = *reinterpret_cast<const float4*>(x + (cell - sx) * M + m);
+    if ((unsigned)(rw.j - sy) < (unsigned)N) q.ny = *reinterpret_cast<const float4*>(x + (cell - (long long)sy * N) * M + m);
+    return q;
+  }
+  __device__ __forceinline__ void store4(const Row& rw, const Col& cv, float4 v, const Pre& q) const {
+    const float4 a_x = cv.a_x, a_y = cv.a_y, p = q.p, nx = q.nx, ny = q.ny;
     const float st = rw.st, ss = rw.ss, al = rw.al, c = rw.c;
     float4 r;
     r.x = al * ((a_x.x + a_y.x + st) * p.x - ss * (c + v.x) - a_x.x * nx.x - a_y.x * ny.x);
     r.y = al * ((a_x.y + a_y.y + st) * p.y - ss * (c + v.y) - a_x.y * nx.y - a_y.y * ny.y);
     r.z = al * ((a_x.z + a_y.z + st) * p.z - ss * (c + v.z) - a_x.z * nx.z - a_y.z * ny.z);
     r.w = al * ((a_x.w + a_y.w + st) * p.w - ss * (c + v.w) - a_x.w * nx.w - a_y.w * ny.w);
-    *reinterpret_cast<float4*>(y + cell * M + m) = r;
+    *reinterpret_cast<float4*>(y + rw.cell * M + cv.m) = r;
   }
   __device__ __forceinline__ void store_partial4(int, const Row&, int, float4) const {}
 };
@@ -69,8 +93,8 @@ struct EpiApply {
 template <int BN>
 void launch_apply_bn(const Geom& g, int mtiles, const CUtensorMap& ta, const CUtensorMap& tbh,
                      const CUtensorMap& tbl, const EpiApply& epi, cudaStream_t st) {
-  auto kern = gemm3xtf32_kernel<BN, false, false, EpiApply>;
-  constexpr int smem = gemm_smem_bytes<BN, false, false>();
+  auto kern = gemm3xtf32_kernel<BN, 0, false, EpiApply>;
+  constexpr int smem = gemm_smem_bytes<BN, 0, false>();
   ensure_smem((const void*)kern, smem);
   const int grid = std::min(mtiles * g.ntiles, num_sms());
   kern<<<grid, kGemmThreads, smem, st>>>(ta, tbh, tbl, g, epi);
@@ -96,6 +120,7 @@ void launch_apply_tc(const rte_problem* p, const float* x, float* y, const doubl
   g.Hc = g.Wc = N;
   g.TW = std::min(N, 128);
   g.TH = std::min(N, std::max(1, 128 / g.TW));
+  g.pitch = g.TW;
   g.tiles_x = (N + g.TW - 1) / g.TW;
   g.tiles_y = (N + g.TH - 1) / g.TH;
   g.kb_total = g.cchunks;

@@ -161,31 +161,57 @@ struct EpiConv {
     }
     return (((long long)b * Ho + Y) * Wo + X) * Co + col;
   }
+  static constexpr int kBatch = 4, kBatchWide = 4;
+  struct Col {
+    int col;
+  };
   struct Row {
     long long o;  // output offset of column 0 of this pixel
     long long po; // partial-sum offset of column 0 (split-K)
     float si, sa;
   };
-  __device__ __forceinline__ Row row(int b, int cls, int oy, int ox, float) const {
+  struct Pre {
+    float4 a;  // addend (hi + lo planes summed when split)
+  };
+  struct Tile {
+    long long o0, po0;  // output / partial-sum offsets of the tile origin
+    float si, sa;
+  };
+  __device__ __forceinline__ Col col(int c) const { return Col{c}; }
+  __device__ __forceinline__ Tile tile(int b, int cls, int oy0, int ox0) const {
     const float al = alpha ? (float)alpha[(long long)b * alpha_stride] : 1.f;
-    return Row{index(b, cls, oy, ox, 0), pindex(b, cls, oy, ox, 0), sign * (a_in ? al : 1.f), a_add ? al : 1.f};
+    return Tile{index(b, cls, oy0, ox0, 0), pindex(b, cls, oy0, ox0, 0), sign * (a_in ? al : 1.f), a_add ? al : 1.f};
   }
-  __device__ __forceinline__ void store4(const Row& rw, int col, float4 v) const {
-    const long long o = rw.o + col;
-    float4 r = make_float4(rw.si * v.x, rw.si * v.y, rw.si * v.z, rw.si * v.w);
+  // class-grid step (ly, lx) -> output offset step (transposed conv: the class grid is stride 2)
+  __device__ __forceinline__ int rel(int ly, int lx) const {
+    return mode == 2 ? 2 * (ly * Wo + lx) * Co : (ly * Wo + lx) * Co;
+  }
+  __device__ __forceinline__ Row row(const Tile& t, int rel, int, int, float) const {
+    return Row{t.o0 + rel, t.po0 + rel, t.si, t.sa};
+  }
+  __device__ __forceinline__ Pre load(const Row& rw, const Col& cv) const {
+    Pre p{make_float4(0.f, 0.f, 0.f, 0.f)};
     if (addend) {
-      float4 a = *reinterpret_cast<const float4*>(addend + o);
+      const long long o = rw.o + cv.col;
+      p.a = *reinterpret_cast<const float4*>(addend + o);
       if (out_split) {
         const float4 l = *reinterpret_cast<const float4*>(addend + o + plane());
-        a.x += l.x;
-        a.y += l.y;
-        a.z += l.z;
-        a.w += l.w;
+        p.a.x += l.x;
+        p.a.y += l.y;
+        p.a.z += l.z;
+        p.a.w += l.w;
       }
-      r.x = fmaf(rw.sa, a.x, r.x);
-      r.y = fmaf(rw.sa, a.y, r.y);
-      r.z = fmaf(rw.sa, a.z, r.z);
-      r.w = fmaf(rw.sa, a.w, r.w);
+    }
+    return p;
+  }
+  __device__ __forceinline__ void store4(const Row& rw, const Col& cv, float4 v, const Pre& p) const {
+    const long long o = rw.o + cv.col;
+    float4 r = make_float4(rw.si * v.x, rw.si * v.y, rw.si * v.z, rw.si * v.w);
+    if (addend) {
+      r.x = fmaf(rw.sa, p.a.x, r.x);
+      r.y = fmaf(rw.sa, p.a.y, r.y);
+      r.z = fmaf(rw.sa, p.a.z, r.z);
+      r.w = fmaf(rw.sa, p.a.w, r.w);
     }
     if (out_split) {
       float4 h, l;
@@ -261,6 +287,7 @@ namespace {
 struct Plan {
   bool ok = false;
   bool halo = false;  // stride-1 3x3: one halo tile per channel chunk feeds all 9 taps
+  int am = 0;         // kernel A mode (tc_gemm.cuh Plan): 0 window, 1 TS halo, 2 SS halo
   int BN = 0;
   tc::Geom g{};
   int mtiles = 0, ntiles = 0;
@@ -294,6 +321,32 @@ Plan make_plan(const ConvDesc& d) {
     g.TW = std::min(g.Wc, 128);
     g.TH = std::min(g.Hc, std::max(1, 128 / g.TW));
   }
+  g.pitch = g.TW;
+  P.am = P.halo ? 1 : 0;
+  // SS halo (see tc_gemm.cuh): lines of P = 16 or 32 MMA rows, TW = P - 2 output pixels.  Opt-in
+  // (RTE_TC_SS_MINW = the narrowest grid to use it on): measured shared-memory-bandwidth bound
+  // (two 16 KB A reads per K block) and slower than the TS halo kernel on every MgNet level
+  // (DESIGN.md §5); BN = 128 would need three A reads, so it is fused-form (BN <= 64) only
+  static const int ss_minw = [] {
+    const char* e = getenv("RTE_TC_SS_MINW");
+    return e ? atoi(e) : 1 << 30;
+  }();
+  if (P.halo && !d.in_split && BN <= 64 && g.Wc >= ss_minw) {
+    int bestP = 0;
+    double best_eff = 0.0;
+    for (int Pp : {32, 16}) {
+      const int tx = (g.Wc + Pp - 3) / (Pp - 2);
+      const double eff = (double)g.Wc / ((double)tx * Pp);
+      if (eff > best_eff + 1e-9) {
+        best_eff = eff;
+        bestP = Pp;
+      }
+    }
+    P.am = 2;
+    g.pitch = bestP;
+    g.TW = bestP - 2;
+    g.TH = std::min(128 / bestP, g.Hc);
+  }
   g.tiles_x = (g.Wc + g.TW - 1) / g.TW;
   g.tiles_y = (g.Hc + g.TH - 1) / g.TH;
   g.kb_total = g.taps * g.cchunks;
@@ -309,7 +362,8 @@ Plan make_plan(const ConvDesc& d) {
   // split-K from a wave model of the persistent kernel: time = ceil(units / SMs) * (k blocks per
   // unit * t_kb + t_unit) + (split-K reduction: (nsplit + 2) output-sized streams at ~6 TB/s)
   const int sms = num_sms();
-  const double t_kb = std::max(12.0 * BN / 2.0, 700.0) / 1.9e3;  // us per K block (MMA vs convert)
+  const double t_kb = (P.am == 2 ? (BN == 32 ? 400.0 : BN == 64 ? 500.0 : 800.0)  // SS MMA bound
+                                  : std::max(12.0 * BN / 2.0, 700.0)) / 1.9e3;    // us per K block
   const double t_unit = 0.5;
   const double out_us = 4.0 * (double)P.out_elems / 6.0e6;
   double best = 1e300;
@@ -332,11 +386,11 @@ Plan make_plan(const ConvDesc& d) {
   return P;
 }
 
-template <int BN, bool HALO, bool ASPLIT>
+template <int BN, int AM, bool ASPLIT>
 void launch_bn(const Plan& P, const CUtensorMap& ta, const CUtensorMap& tbh, const CUtensorMap& tbl,
                const tc::EpiConv& epi, cudaStream_t st) {
-  auto kern = tc::gemm3xtf32_kernel<BN, HALO, ASPLIT, tc::EpiConv>;
-  constexpr int smem = tc::gemm_smem_bytes<BN, HALO, ASPLIT>();
+  auto kern = tc::gemm3xtf32_kernel<BN, AM, ASPLIT, tc::EpiConv>;
+  constexpr int smem = tc::gemm_smem_bytes<BN, AM, ASPLIT>();
   tc::ensure_smem((const void*)kern, smem);
   const long long units = (long long)P.mtiles * P.ntiles * P.g.nsplit;
   const int grid = (int)std::min<long long>(units, num_sms());
@@ -352,7 +406,9 @@ bool conv_tc_try(const ConvDesc& d, const float* in, float* out, const float* ad
   if (!P.ok) return false;
   const tc::Geom& g = P.g;
   const int es = (d.mode == 1) ? 2 : 1;
-  const int bw = P.halo ? g.TW + 2 : g.TW, bh = P.halo ? g.TH + 2 : g.TH, ees = P.halo ? 1 : es;
+  // A box: SS halo (TH + 2) lines of P pixels; TS halo (TH + 2) x (TW + 2); else the TW x TH window
+  const int bw = P.am == 2 ? g.pitch : P.halo ? g.TW + 2 : g.TW;
+  const int bh = P.halo ? g.TH + 2 : g.TH, ees = P.halo ? 1 : es;
   CUtensorMap ta = d.in_split ? tc::make_map_act_split(in, d.Ci, d.Wi, d.Hi, d.B, bw, bh, ees)
                               : tc::make_map_act(in, d.Ci, d.Wi, d.Hi, d.B, bw, bh, ees);
   CUtensorMap tbh = tc::make_map_kmajor(d.w->d_hi, d.w->tc_K, d.w->tc_rows, P.BN);
@@ -382,12 +438,14 @@ bool conv_tc_try(const ConvDesc& d, const float* in, float* out, const float* ad
   prof_begin(st);
   auto dispatch = [&](auto bn_tag) {
     constexpr int BN = decltype(bn_tag)::value;
-    if (P.halo) {
-      if (d.in_split) launch_bn<BN, true, true>(P, ta, tbh, tbl, epi, st);
-      else launch_bn<BN, true, false>(P, ta, tbh, tbl, epi, st);
+    if (P.am == 2) {
+      if constexpr (BN <= 64) launch_bn<BN, 2, false>(P, ta, tbh, tbl, epi, st);
+    } else if (P.halo) {
+      if (d.in_split) launch_bn<BN, 1, true>(P, ta, tbh, tbl, epi, st);
+      else launch_bn<BN, 1, false>(P, ta, tbh, tbl, epi, st);
     } else {
-      if (d.in_split) launch_bn<BN, false, true>(P, ta, tbh, tbl, epi, st);
-      else launch_bn<BN, false, false>(P, ta, tbh, tbl, epi, st);
+      if (d.in_split) launch_bn<BN, 0, true>(P, ta, tbh, tbl, epi, st);
+      else launch_bn<BN, 0, false>(P, ta, tbh, tbl, epi, st);
     }
   };
   switch (P.BN) {
@@ -416,11 +474,11 @@ bool conv_tc_try(const ConvDesc& d, const float* in, float* out, const float* ad
 // Upload the tensor-core operand layouts of every conv weight and size the split-K workspace.
 // Per-role GEMM cycle counters (tc_gemm.cuh, RTE_TC_DBG bit 6): copy out and optionally reset.
 void tc_debug_counters(unsigned long long* out, int n, bool reset) {
-  unsigned long long h[16];
+  unsigned long long h[24];
   RTE_CHECK_CUDA(cudaMemcpyFromSymbol(h, tc::g_tc_prof, sizeof(h)));
-  for (int i = 0; i < n && i < 16; ++i) out[i] = h[i];
+  for (int i = 0; i < n && i < 24; ++i) out[i] = h[i];
   if (reset) {
-    unsigned long long z[16] = {0};
+    unsigned long long z[24] = {0};
     RTE_CHECK_CUDA(cudaMemcpyToSymbol(tc::g_tc_prof, z, sizeof(z)));
   }
 }

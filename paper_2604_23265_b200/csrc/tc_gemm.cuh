@@ -60,6 +60,7 @@ struct Geom {
   int ntiles;       // N tiles
   int mtiles;       // M tiles (B * classes * tiles_y * tiles_x)
   int bn;           // N tile (the kernel's BN)
+  int pitch;        // MMA-tile rows per output line (= TW, or the halo pitch P of SS-halo kernels)
   int dbg;          // perf-experiment switches (RTE_TC_DBG; 0 in production): bit0 converters skip
                     // the row load/split/TMEM store, bit3 no MMAs, bit4 no TMA loads, bit5 no
                     // epilogue global traffic, bit6 role timers
@@ -68,23 +69,27 @@ struct Geom {
 // Shared-memory plan: A ring (HALO: halo tiles of up to kHaloRows rows; else 128-row tiles), B
 // ring, and the epilogue staging tiles (one 128 x 32 fp32 tile per column half).
 constexpr int kHaloRows = 208;                  // (TW+2)(TH+2) <= 208, e.g. 34 x 6 for a 32 x 4 tile
+constexpr int kSSRows = 200;                    // SS-halo tile: (TH+2) P + 2 rows <= 200 (P = 16, 32)
 constexpr int kStageBytes = kTileM * 128;       // 128 rows x 32 fp32 per column half
-template <int BN, bool HALO, bool ASPLIT = false>
+// A modes: 0 = per-K-block window tiles (TS), 1 = halo tiles, 9 taps per tile (TS), 2 = SS halo:
+// the halo tile is split once in shared memory and each tap's A operand is a row-shifted SW128
+// descriptor into it (see the kernel comment).
+template <int BN, int AM, bool ASPLIT = false>
 struct Plan {
   static constexpr int kBBytes = BN * 128;                          // one of B hi / B lo
-  static constexpr int kATile = HALO ? kHaloRows * 128 : kABytes;   // one A tile (1 KB multiple)
-  static constexpr int kASlot = (ASPLIT ? 2 : 1) * kATile;          // split activations: hi + lo tiles
+  static constexpr int kATile = AM == 2 ? kSSRows * 128 : AM == 1 ? kHaloRows * 128 : kABytes;
+  static constexpr int kASlot = (ASPLIT || AM == 2 ? 2 : 1) * kATile;  // hi + lo tiles when split
   static constexpr int kBSlot = 2 * kBBytes;
   static constexpr int kBudget = 190 * 1024;                        // rings
-  static constexpr int kNA = (HALO || ASPLIT) ? 2 : 4;              // A ring depth
+  static constexpr int kNA = (AM != 0 || ASPLIT) ? 2 : 4;           // A ring depth
   static constexpr int kNBraw = (kBudget - kNA * kASlot) / kBSlot;
   static constexpr int kNB = kNBraw > 8 ? 8 : kNBraw;               // B ring depth
   static constexpr int kRingBytes = kNA * kASlot + kNB * kBSlot;
 };
 
-template <int BN, bool HALO, bool ASPLIT = false>
+template <int BN, int AM, bool ASPLIT = false>
 constexpr int gemm_smem_bytes() {
-  return Plan<BN, HALO, ASPLIT>::kRingBytes + 2 * kStageBytes + 1024 /*align*/ + 1024 /*barriers*/ +
+  return Plan<BN, AM, ASPLIT>::kRingBytes + 2 * kStageBytes + 1024 /*align*/ + 1024 /*barriers*/ +
          1024 /*row centres*/;
 }
 
@@ -98,9 +103,19 @@ constexpr bool tmem_fused() {
 // Fused form: NG group buffers of 2BN columns (the MMA can run NG - 1 groups ahead of the
 // promoters, so a tile's epilogue overlaps the next tile's K loop) and 2 A buffers.
 // Split form: 2 main buffers + X + the rest as A buffers.
+#ifndef RTE_EPI_BATCH_MAX
+#define RTE_EPI_BATCH_MAX 1
+#endif
+#ifndef RTE_TC_NG_MAX
+#define RTE_TC_NG_MAX 6
+#endif
+#ifndef RTE_TC_NA_MIN
+#define RTE_TC_NA_MIN 2
+#endif
 template <int BN>
 constexpr int tmem_groups() {
-  return tmem_fused<BN>() ? ((512 - 128) / (2 * BN) < 6 ? (512 - 128) / (2 * BN) : 6) : 2;
+  constexpr int room = (512 - 64 * RTE_TC_NA_MIN) / (2 * BN);
+  return tmem_fused<BN>() ? (room < RTE_TC_NG_MAX ? room : RTE_TC_NG_MAX) : 2;
 }
 template <int BN>
 constexpr int tmem_acc_cols() {
@@ -180,36 +195,51 @@ __device__ __forceinline__ void a_origin(const Geom& g, const TileCoord& c, int 
 // read with rte_debug_counters).  Slots: 0 producer total, 1 producer wait; 2 MMA total, 3 MMA
 // wait conv+bfull, 4 MMA wait mempty/xempty, 5 MMA issue; 6 converter total, 7 converter wait,
 // 8 converter work; 9 promoter total, 10 promoter wait mfull, 11 promoter TMEM loads,
-// 12 epilogue; 13 K blocks (per CTA, producer); 14 units.
-__device__ unsigned long long g_tc_prof[16];
+// 12 epilogue; 13 K blocks (per CTA, producer); 14 converter K-block loop, 15 MMA K-block loop;
+// 16 epilogue staging + first barrier, 17 epilogue row loop, 18 epilogue final barrier.
+__device__ unsigned long long g_tc_prof[24];
 
+// (the warp stays converged: the timer is predicated, the wait is executed once by all lanes)
 __device__ __forceinline__ void tw_wait(uint64_t* bar, uint32_t par, bool on, long long& acc) {
-  if (!on) {
-    mbar_wait(bar, par);
-    return;
-  }
-  const long long t0 = clock64();
+  const long long t0 = on ? clock64() : 0;
   mbar_wait(bar, par);
-  acc += clock64() - t0;
+  if (on) acc += clock64() - t0;
 }
 
-// Epilogue interface: row = epi.row(b, cls, oy, ox, c_row) prepares the per-output-pixel state of a
-// valid pixel (oy, ox) of the class grid (c_row = the row centre when Epi::kCenter: the GEMM then
-// computed (a - c_row 1) . B^T); epi.store4(row, col, v4) finishes columns col .. col+3;
-// epi.store_partial4(split, row, col, v4) stores raw partial sums when split-K is active.
+// Epilogue interface: cv = epi.col(col) holds per-column constants of columns col .. col+3;
+// t = epi.tile(b, cls, oy0, ox0) the per-unit constants of the tile with origin (oy0, ox0);
+// epi.rel(ly, lx) the output offset of tile pixel (ly, lx) relative to the origin's;
+// row = epi.row(t, rel, oy, ox, c_row) the per-output-pixel state of a valid pixel (oy, ox) of the
+// class grid (c_row = the row centre when Epi::kCenter: the GEMM then computed (a - c_row 1) . B^T);
+// pre = epi.load(row, cv) issues the pixel's global inputs; epi.store4(row, cv, v4, pre) finishes
+// the four columns; epi.store_partial4(split, row, col, v4) stores raw partial sums when split-K is
+// active.  Epi::kBatch = rows whose loads are in flight together.
 // ASPLIT: the A activation is stored pre-split as two planes (hi = rna_tf32(a), lo = a - hi; see
 // EpiConv) and the tensor map has a plane dimension; the converters then only copy rows into
 // TMEM.  Otherwise A is plain fp32 and the converters split it.
-template <int BN, bool HALO, bool ASPLIT, class Epi>
+//
+// SS halo (AM = 2, stride-1 3x3 convolutions): the output tile is TH lines of P = g.pitch MMA rows
+// (P = 16 or 32) of which TW = P - 2 are output pixels (the last two rows of each line are computed
+// and discarded).  The TMA loads the (TH + 2) x P halo of input lines at pitch P, so for tap
+// (dy, dx) the A operand of output row r = ly P + lx is halo row r + dy P + dx: ONE contiguous
+// 128-row slice, i.e. an SW128 descriptor starting dy P + dx rows in (the swizzle follows the
+// absolute shared-memory address, so any row offset is valid; scripts/ss_offset_test.cu).  The
+// converter warps split the halo once per tile in place (hi over the fp32 tile, lo into its twin)
+// and the tensor core reads both straight from shared memory: no per-tap conversion, no TMEM A.
+template <int BN, int AM, bool ASPLIT, class Epi>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm3xtf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBhi,
                       const __grid_constant__ CUtensorMap tmBlo, const Geom g, const Epi epi) {
+  constexpr bool HALO = AM != 0;
+  constexpr bool SSH = AM == 2;
   static_assert(BN == 32 || BN == 64 || BN == 128, "N tile must be 32, 64 or 128");
   static_assert(!(HALO && Epi::kCenter), "row centring is for the 1x1 (apply) kernels");
   static_assert(!(ASPLIT && Epi::kCenter), "row centring needs the plain fp32 A operand");
-  using PL = Plan<BN, HALO, ASPLIT>;
+  static_assert(!(SSH && ASPLIT), "SS-halo kernels split the activations themselves");
+  using PL = Plan<BN, AM, ASPLIT>;
   constexpr int NAR = PL::kNA, NBR = PL::kNB;
   constexpr int NA = tmem_abufs<BN>();
+  constexpr int NCV = NA > NAR ? NA : NAR;  // conv barriers (SSH: one per A ring slot)
   constexpr int BBYTES = PL::kBBytes;
   constexpr uint32_t TMEM_COLS = 512;
   constexpr bool FUSED = tmem_fused<BN>();
@@ -222,8 +252,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* aempty = afull + NAR;      // [NAR] converters done reading the A tile (4 warps)
   uint64_t* bfull = aempty + NAR;      // [NBR] B tiles landed
   uint64_t* bempty = bfull + NBR;      // [NBR] MMAs done with the B tiles
-  uint64_t* conv = bempty + NBR;       // [NA] TMEM A buffer written (4 converter warps)
-  uint64_t* afree = conv + NA;         // [NA] MMAs done with the TMEM A buffer
+  uint64_t* conv = bempty + NBR;       // [NA] TMEM A buffer written (4 converter warps); SSH: A slot split
+  uint64_t* afree = conv + NCV;        // [NA] MMAs done with the TMEM A buffer
   constexpr int NG = tmem_groups<BN>();
   uint64_t* mfull = afree + NA;        // [NG] group buffer ready for promotion
   uint64_t* mempty = mfull + NG;       // [NG] group buffer drained (8 promoter warps)
@@ -236,30 +266,31 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int units = g.mtiles * g.ntiles * g.nsplit;
-  const int rows = g.TW * g.TH;
-  const uint32_t a_bytes = HALO ? (uint32_t)((g.TW + 2) * (g.TH + 2)) * 128u : (uint32_t)rows * 128u;
+  const int rows = g.pitch * g.TH;  // MMA-tile rows in use
+  const uint32_t a_bytes = SSH    ? (uint32_t)((g.TH + 2) * g.pitch) * 128u
+                           : HALO ? (uint32_t)((g.TW + 2) * (g.TH + 2)) * 128u
+                                  : (uint32_t)rows * 128u;
   // bit6 enables the counters; bits 8..15 (if set) restrict them to kernels with that BN, bit16 to
   // halo kernels
   const bool prof = (g.dbg & 64) && lane == 0 && (((g.dbg >> 8) & 0xff) == 0 || ((g.dbg >> 8) & 0xff) == BN) &&
                     (!((g.dbg >> 16) & 1) || HALO);
   long long w_d = 0, w_e = 0;
   long long w_a = 0, w_b = 0, w_c = 0;
+  long long w_s1 = 0, w_s2 = 0, w_s3 = 0;
   const long long t_start = clock64();
   int n_kb = 0;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < NAR; ++i) {
       mbar_init(&afull[i], 1);
-      mbar_init(&aempty[i], 4);
+      mbar_init(&aempty[i], SSH ? 1 : 4);  // SSH: freed by the MMA commit after the 9th tap
     }
     for (int i = 0; i < NBR; ++i) {
       mbar_init(&bfull[i], 1);
       mbar_init(&bempty[i], 1);
     }
-    for (int i = 0; i < NA; ++i) {
-      mbar_init(&conv[i], 4);
-      mbar_init(&afree[i], 1);
-    }
+    for (int i = 0; i < NCV; ++i) mbar_init(&conv[i], 4);
+    for (int i = 0; i < NA; ++i) mbar_init(&afree[i], 1);
     for (int t = 0; t < NG; ++t) {
       mbar_init(&mfull[t], 1);
       mbar_init(&mempty[t], 8);
@@ -342,8 +373,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     // ===== MMA issuer: the whole warp walks the pipeline, one elected lane issues =====
     constexpr uint32_t idesc = idesc_tf32(kTileM, BN);
     const bool no_mma = (g.dbg & 8) != 0;
-    int bs = 0, ab = 0;
-    uint32_t bph = 0, abph = 0;
+    int bs = 0, ab = 0, as = 0;
+    uint32_t bph = 0, abph = 0, aph = 0;
     int gcount = 0;  // main-buffer groups issued so far (all units)
     int li = 0;      // local unit index
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++li) {
@@ -360,14 +391,42 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         uint32_t acc_m = 0;
         const int kbe = min(w.kb1, kbg + kPromoteKB);
         for (int kb = kbg; kb < kbe; ++kb, ++n_kb) {
-          tw_wait(&conv[ab], abph, prof, w_a);
+          const long long tk0 = prof ? clock64() : 0;
+          int tap = 0, cc = 0;
+          if (SSH) kb_split<true>(g, kb, tap, cc);
+          if (!SSH) tw_wait(&conv[ab], abph, prof, w_a);
+          else if (tap == 0 || kb == w.kb0) tw_wait(&conv[as], aph, prof, w_a);  // halo tile split
           tw_wait(&bfull[bs], bph, prof, w_a);
           tc_fence_after();
           const uint32_t sb = smem_u32(bring + bs * PL::kBSlot);
           const uint64_t d_bh = sdesc_sw128(sb), d_bl = sdesc_sw128(sb + BBYTES);
           const uint32_t a_hi = tmem_a + (uint32_t)(64 * ab), a_lo = a_hi + 32;
           const long long ti0 = prof ? clock64() : 0;
-          if (!no_mma) {
+          if (SSH && !no_mma) {
+            // tap (dy, dx) = row shift dy P + dx into the split halo (hi tile, lo tile)
+            const uint32_t sa = smem_u32(aring + as * PL::kASlot) + (uint32_t)((tap / 3) * g.pitch + tap % 3) * 128u;
+            const uint64_t d_ah = sdesc_sw128(sa), d_al = sdesc_sw128(sa + PL::kATile);
+            if constexpr (FUSED) {
+              constexpr uint32_t idesc2 = idesc_tf32(kTileM, 2 * BN);
+              const uint32_t tbuf = tmem + (uint32_t)(t * 2 * BN);
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                mma_tf32_elect(tbuf, d_ah + 2u * k, d_bh + 2u * k, idesc2, acc_m);
+                acc_m = 1;
+                mma_tf32_elect(tbuf + BN, d_al + 2u * k, d_bh + 2u * k, idesc, 1);
+              }
+            } else {
+              const uint32_t tm = tmem + (uint32_t)(t * BN);
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                mma_tf32_elect(tmem_x, d_al + 2u * k, d_bh + 2u * k, idesc, acc_x);
+                acc_x = 1;
+                mma_tf32_elect(tmem_x, d_ah + 2u * k, d_bl + 2u * k, idesc, 1);
+                mma_tf32_elect(tm, d_ah + 2u * k, d_bh + 2u * k, idesc, acc_m);
+                acc_m = 1;
+              }
+            }
+          } else if (!no_mma) {
             if constexpr (FUSED) {
               // hi.[B_hi; B_lo] -> [main_t | X_t] (N = 2BN), lo.B_hi -> X_t
               constexpr uint32_t idesc2 = idesc_tf32(kTileM, 2 * BN);
@@ -392,12 +451,58 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             }
           }
           mma_commit_elect(&bempty[bs]);
-          mma_commit_elect(&afree[ab]);
+          if (SSH) {
+            if (tap == 8 || kb + 1 == w.kb1) {  // last tap of this halo tile: release the A slot
+              mma_commit_elect(&aempty[as]);
+              if (++as == NAR) { as = 0; aph ^= 1; }
+            }
+          } else {
+            mma_commit_elect(&afree[ab]);
+            if (++ab == NA) { ab = 0; abph ^= 1; }
+          }
           if (prof) w_d += clock64() - ti0;
           if (++bs == NBR) { bs = 0; bph ^= 1; }
-          if (++ab == NA) { ab = 0; abph ^= 1; }
+          if (prof) w_e += clock64() - tk0;
         }
         mma_commit_elect(&mfull[t]);
+      }
+    }
+  } else if (SSH && warp < 6) {
+    // ===== SS-halo converters (warps 2..5): split each halo tile once, in place =====
+    const int tid = threadIdx.x - 64;
+    int as = 0;
+    uint32_t aph = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const Unit w = decode_unit(g, u);
+      for (int kb = w.kb0; kb < w.kb1; ++kb, ++n_kb) {
+        int tap, cc;
+        kb_split<true>(g, kb, tap, cc);
+        if (!(tap == 0 || kb == w.kb0)) continue;
+        const long long tk0 = prof ? clock64() : 0;
+        tw_wait(&afull[as], aph, prof, w_a);
+        const long long tc0 = prof ? clock64() : 0;
+        // elementwise, so the SW128 placement is irrelevant: hi = tf32 head in place, lo = rest
+        const uint32_t base = smem_u32(aring + as * PL::kASlot);
+        const int n16 = (int)(a_bytes >> 4);
+#pragma unroll 4
+        for (int i = tid; i < n16; i += 128) {
+          const float4 v = lds128(base + (uint32_t)i * 16u);
+          float4 h, l;
+          split_tf32_fast(v.x, h.x, l.x);
+          split_tf32_fast(v.y, h.y, l.y);
+          split_tf32_fast(v.z, h.z, l.z);
+          split_tf32_fast(v.w, h.w, l.w);
+          sts128(base + (uint32_t)i * 16u, h);
+          sts128(base + (uint32_t)PL::kATile + (uint32_t)i * 16u, l);
+        }
+        fence_proxy_async_smem();  // generic-proxy writes -> tensor-core (async proxy) reads
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&conv[as]);
+        if (++as == NAR) { as = 0; aph ^= 1; }
+        if (prof) {
+          w_d += clock64() - tc0;
+          w_e += clock64() - tk0;
+        }
       }
     }
   } else if (warp < 6) {
@@ -413,6 +518,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const Unit w = decode_unit(g, u);
       float c = 0.f;
       for (int kb = w.kb0; kb < w.kb1; ++kb, ++n_kb) {
+        const long long tk0 = prof ? clock64() : 0;
         int tap, cc;
         kb_split<HALO>(g, kb, tap, cc);
         const bool new_tile = !HALO || tap == 0 || kb == w.kb0;
@@ -479,6 +585,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if (lane == 0) mbar_arrive(&conv[ab]);
         if (prof) w_d += clock64() - tc0;
         if (++ab == NA) { ab = 0; abph ^= 1; }
+        if (prof) w_e += clock64() - tk0;
       }
     }
   } else {
@@ -490,6 +597,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
     const int r = quarter * 32 + lane;  // tile row = TMEM lane
     const int cbase = half * HB;
+    // epilogue row walk (unit-invariant): chunks of CW columns, LPR lanes per row, RPI rows per warp
+    // instruction; lane's first row e_rr0 = (e_ly0, e_lx0) in the tile, then steps of RPI rows
+    constexpr int CW = HB < 32 ? HB : 32;
+    constexpr int LPR = CW / 4;
+    constexpr int RPI = 32 / LPR;
+    const int e_rr0 = quarter * 32 + lane / LPR;
+    const int e_ly0 = e_rr0 / g.pitch, e_lx0 = e_rr0 - e_ly0 * g.pitch;
+    const int e_dly = RPI / g.pitch, e_dlx = RPI - e_dly * g.pitch;
     int gcount = 0;
     int li = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++li) {
@@ -540,37 +655,73 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       // shared tile (row r at r*128 B, 16-byte chunk q at position q ^ (r & 7): conflict-free both
       // ways), then the half's four warps walk their rows with float4 lanes, so every global
       // load/store instruction covers whole rows (128 B each) instead of 32 scattered lines.
-      constexpr int CW = HB < 32 ? HB : 32;   // chunk width (columns)
-      constexpr int LPR = CW / 4;             // lanes per row
-      constexpr int RPI = 32 / LPR;           // rows per warp instruction
       const uint32_t sh = stage_s + (uint32_t)(half * kStageBytes);
+      // per-unit epilogue state: tile origin in the class grid and the epilogue's tile constants
+      const int e_oy0 = w.tc.ty * g.TH, e_ox0 = w.tc.tx * g.TW;
+      const typename Epi::Tile et = epi.tile(w.tc.b, w.tc.cls, e_oy0, e_ox0);
 #pragma unroll
       for (int c0 = 0; c0 < HB; c0 += CW) {
+        const long long ts0 = prof ? clock64() : 0;
 #pragma unroll
         for (int k = 0; k < CW / 4; ++k)
           sts128(sh + (uint32_t)(r * 128 + ((k ^ (r & 7)) << 4)),
                  make_float4(acc[c0 + 4 * k], acc[c0 + 4 * k + 1], acc[c0 + 4 * k + 2], acc[c0 + 4 * k + 3]));
         named_bar_sync(2 + half, 128);
+        const long long ts1 = prof ? clock64() : 0;
+        if (prof) w_s1 += ts1 - ts0;
         if (!(g.dbg & 32)) {
+          // rows are finished in batches: every global input of a batch (epi.row + epi.load) is
+          // requested before any output of it is stored, so the batch costs one memory round trip
+          // (out may alias the epilogue inputs elementwise only, which this order preserves)
+          constexpr int NIT = 32 / RPI;
+          constexpr int BMAX0 = BN == 128 ? Epi::kBatchWide : Epi::kBatch;  // (BN = 128: acc is live)
+          constexpr int BMAX = BMAX0 < RTE_EPI_BATCH_MAX ? BMAX0 : RTE_EPI_BATCH_MAX;
+          constexpr int BATCH = NIT < BMAX ? NIT : BMAX;
           const int k = lane % LPR;
-#pragma unroll 4
-          for (int it = 0; it < 32 / RPI; ++it) {
-            const int rr = quarter * 32 + it * RPI + lane / LPR;
-            const int ly = rr / g.TW, lx = rr - ly * g.TW;
-            const int oy = w.tc.ty * g.TH + ly, ox = w.tc.tx * g.TW + lx;
-            if (rr < rows && oy < g.Hc && ox < g.Wc) {
+          const int col = w.n0 + cbase + c0 + 4 * k;
+          const typename Epi::Col cv = epi.col(col);
+          int ly = e_ly0, lx = e_lx0;  // tile-local pixel of this lane's row rr = e_rr0 + it * RPI
+#pragma unroll 1
+          for (int it0 = 0; it0 < NIT; it0 += BATCH) {
+            typename Epi::Row rw[BATCH];
+            typename Epi::Pre pre[BATCH];
+            bool ok[BATCH];
+#pragma unroll
+            for (int q = 0; q < BATCH; ++q) {
+              const int rr = e_rr0 + (it0 + q) * RPI;
+              const int oy = e_oy0 + ly, ox = e_ox0 + lx;
+              ok[q] = rr < rows && lx < g.TW && oy < g.Hc && ox < g.Wc;
+              if (ok[q]) {
+                const float crr = Epi::kCenter ? cvec[(li & 1) * 128 + rr] : 0.f;
+                rw[q] = epi.row(et, epi.rel(ly, lx), oy, ox, crr);
+                if (g.nsplit == 1) pre[q] = epi.load(rw[q], cv);
+              }
+              lx += e_dlx;
+              ly += e_dly;
+              if (lx >= g.pitch) {
+                lx -= g.pitch;
+                ++ly;
+              }
+            }
+#pragma unroll
+            for (int q = 0; q < BATCH; ++q) {
+              if (!ok[q]) continue;
+              const int rr = e_rr0 + (it0 + q) * RPI;
               const float4 v = lds128(sh + (uint32_t)(rr * 128 + ((k ^ (rr & 7)) << 4)));
-              const float crr = Epi::kCenter ? cvec[(li & 1) * 128 + rr] : 0.f;
-              const typename Epi::Row row = epi.row(w.tc.b, w.tc.cls, oy, ox, crr);
-              const int col = w.n0 + cbase + c0 + 4 * k;
               if (g.nsplit > 1)
-                epi.store_partial4(w.split, row, col, v);
+                epi.store_partial4(w.split, rw[q], col, v);
               else
-                epi.store4(row, col, v);
+                epi.store4(rw[q], cv, v, pre[q]);
             }
           }
         }
+        const long long ts2 = prof ? clock64() : 0;
         named_bar_sync(2 + half, 128);
+        if (prof) {
+          const long long ts3 = clock64();
+          w_s2 += ts2 - ts1;
+          w_s3 += ts3 - ts2;
+        }
       }
       if constexpr (Epi::kCenter) mbar_arrive(&cempty[li & 1]);
       if (prof) w_e += clock64() - te0;
@@ -587,15 +738,20 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       atomicAdd(&g_tc_prof[3], (unsigned long long)w_a);
       atomicAdd(&g_tc_prof[4], (unsigned long long)(w_b + w_c));
       atomicAdd(&g_tc_prof[5], (unsigned long long)w_d);
+      atomicAdd(&g_tc_prof[15], (unsigned long long)w_e);
     } else if (warp == 2) {
       atomicAdd(&g_tc_prof[6], tot);
       atomicAdd(&g_tc_prof[7], (unsigned long long)(w_a + w_b));
       atomicAdd(&g_tc_prof[8], (unsigned long long)w_d);
+      atomicAdd(&g_tc_prof[14], (unsigned long long)w_e);
     } else {
       atomicAdd(&g_tc_prof[9], tot);
       atomicAdd(&g_tc_prof[10], (unsigned long long)w_a);
       atomicAdd(&g_tc_prof[11], (unsigned long long)w_b);
       atomicAdd(&g_tc_prof[12], (unsigned long long)w_e);
+      atomicAdd(&g_tc_prof[16], (unsigned long long)w_s1);
+      atomicAdd(&g_tc_prof[17], (unsigned long long)w_s2);
+      atomicAdd(&g_tc_prof[18], (unsigned long long)w_s3);
     }
   }
   tc_fence_before();

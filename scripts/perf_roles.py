@@ -20,15 +20,15 @@ x = torch.from_numpy(W.make_vector(cfg)).cuda()
 z = torch.empty_like(x)
 P.mgnet_vcycle(net, x, z, True)
 torch.cuda.synchronize()
-buf = (C.c_uint64 * 16)()
-_lib.lib.rte_debug_counters(buf, 16, 1)
+buf = (C.c_uint64 * 24)()
+_lib.lib.rte_debug_counters(buf, 24, 1)
 P.mgnet_vcycle(net, x, z, True)
 torch.cuda.synchronize()
-_lib.lib.rte_debug_counters(buf, 16, 1)
+_lib.lib.rte_debug_counters(buf, 24, 1)
 v = list(buf)
 kb = max(v[13], 1)
 names = ["prod_total", "prod_wait", "mma_total", "mma_wait_in", "mma_wait_acc", "mma_issue", "conv_total",
-         "conv_wait", "conv_work", "prom_total", "prom_wait", "prom_tmem", "epilogue", "kblocks", "units"]
+         "conv_wait", "conv_work", "prom_total", "prom_wait", "prom_tmem", "epilogue", "kblocks", "conv_kbloop", "mma_kbloop", "epi_stage", "epi_rows", "epi_bar2"]
 print(f"dbg={os.environ.get('RTE_TC_DBG')} kblocks={v[13]} (cycles per K block, summed over CTAs):")
-for i, nm in enumerate(names[:13]):
+for i, nm in [(i, n) for i, n in enumerate(names) if i != 13]:
     print(f"  {nm:14s} {v[i] / kb:10.1f}")

@@ -167,6 +167,21 @@ def test_vcycle_parity_large(k):
     assert _rel(v_gpu, v_ref) <= 1e-5
 
 
+@pytest.mark.parametrize("env", [{"RTE_TC_SS_MINW": "16"}, {"RTE_TC_PRESPLIT": "1"}], ids=["ss_halo", "presplit"])
+def test_vcycle_parity_kernel_variants(env):
+    """The opt-in conv kernel variants (SS-halo 3x3 kernels, pre-split activations)
+    pass the same V-cycle parity: their switches are read once per process, so the V-cycle parity
+    tests rerun in a child process with the switch set."""
+    import os
+    import subprocess
+    import sys
+    e = dict(os.environ, **env)
+    r = subprocess.run([sys.executable, "-m", "pytest", __file__, "-q", "-x", "-p", "no:cacheprovider",
+                        "-k", "test_vcycle_parity and not large and not variants"],
+                       env=e, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
 def test_vcycle_zero_weights_is_identity():
     import paper_2604_23265_b200 as P
     cfg = W.small_config(2, N=16, M=16, n_polar=2, n_azim=8, L=3, C0=8)
