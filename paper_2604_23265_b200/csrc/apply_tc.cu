@@ -36,7 +36,7 @@ struct EpiApply {
   const double* alpha;
   int alpha_stride, N, M;
 
-  static constexpr int kBatch = 4, kBatchWide = 2;
+  static constexpr int kBatch = 2;  // rows whose global inputs are in flight together (measured best)
   struct Col {
     int m, sx, sy;
     float4 a_x, a_y;
@@ -92,15 +92,26 @@ struct EpiApply {
 
 template <int BN>
 void launch_apply_bn(const Geom& g, int mtiles, const CUtensorMap& ta, const CUtensorMap& tbh,
-                     const CUtensorMap& tbl, const EpiApply& epi, cudaStream_t st) {
+                     const CUtensorMap& tbl, const CUtensorMap& te, const EpiApply& epi, cudaStream_t st) {
   auto kern = gemm3xtf32_kernel<BN, 0, false, EpiApply>;
   constexpr int smem = gemm_smem_bytes<BN, 0, false>();
   ensure_smem((const void*)kern, smem);
   const int grid = std::min(mtiles * g.ntiles, num_sms());
-  kern<<<grid, kGemmThreads, smem, st>>>(ta, tbh, tbl, g, epi);
+  kern<<<grid, kGemmThreads, smem, st>>>(ta, tbh, tbl, te, g, epi);
 }
 
 }  // namespace tc
+
+// this translation unit's copy of the role counters (tc_gemm.cuh g_tc_prof; experiments only)
+void apply_tc_debug_counters(unsigned long long* out, int n, bool reset) {
+  unsigned long long h[24];
+  RTE_CHECK_CUDA(cudaMemcpyFromSymbol(h, tc::g_tc_prof, sizeof(h)));
+  for (int i = 0; i < n && i < 24; ++i) out[i] += h[i];
+  if (reset) {
+    unsigned long long z[24] = {0};
+    RTE_CHECK_CUDA(cudaMemcpyToSymbol(tc::g_tc_prof, z, sizeof(z)));
+  }
+}
 
 bool apply_tc_supported(int M) { return M >= 32 && M <= 1024 && M % 32 == 0; }
 
@@ -133,15 +144,18 @@ void launch_apply_tc(const rte_problem* p, const float* x, float* y, const doubl
   g.mtiles = mtiles;
   g.bn = BN;
   g.dbg = tc::tc_debug_flags();
+  g.epf = 2;  // prefetch x at the tile's rows j0 - 1 .. j0 + TH (cells and upwind neighbours)
+  g.epf_planes = 1;
+  CUtensorMap te = tc::make_map_prefetch(x, M, N, N, B, BN, g.TW, g.TH);
   CUtensorMap ta = tc::make_map_act(x, M, N, N, B, g.TW, g.TH, 1);
   CUtensorMap tbh = tc::make_map_kmajor(p->S_hi, M, B * M, BN);
   CUtensorMap tbl = tc::make_map_kmajor(p->S_lo, M, B * M, BN);
   tc::EpiApply epi{x, y, p->sig_t, p->sig_s, p->ax, p->ay, p->sgx, p->sgy, alpha, alpha_stride, N, M};
   prof_begin(st);
   switch (BN) {
-    case 32: tc::launch_apply_bn<32>(g, mtiles, ta, tbh, tbl, epi, st); break;
-    case 64: tc::launch_apply_bn<64>(g, mtiles, ta, tbh, tbl, epi, st); break;
-    default: tc::launch_apply_bn<128>(g, mtiles, ta, tbh, tbl, epi, st); break;
+    case 32: tc::launch_apply_bn<32>(g, mtiles, ta, tbh, tbl, te, epi, st); break;
+    case 64: tc::launch_apply_bn<64>(g, mtiles, ta, tbh, tbl, te, epi, st); break;
+    default: tc::launch_apply_bn<128>(g, mtiles, ta, tbh, tbl, te, epi, st); break;
   }
   after_launch("apply_f32_tc", st, apply_flops(p), apply_bytes(p, 4, 0), p->M >= 256 ? 1 : 0);
 }

@@ -52,9 +52,10 @@ EncodeTiledFn encode_fn() {
 }
 
 void encode(CUtensorMap* m, int rank, const void* base, const cuuint64_t* dims, const cuuint64_t* strides,
-            const cuuint32_t* box, const cuuint32_t* es) {
+            const cuuint32_t* box, const cuuint32_t* es, bool swizzle = true) {
   CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (cuuint32_t)rank, const_cast<void*>(base), dims,
-                           strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled failed (code " + std::to_string((int)r) + ")");
@@ -81,6 +82,18 @@ CUtensorMap make_map_act_split(const float* base, int C, int W, int H, int B, in
   cuuint32_t box[5] = {32u, (cuuint32_t)(box_w * es), (cuuint32_t)(box_h * es), 1u, 1u};
   cuuint32_t est[5] = {1u, (cuuint32_t)es, (cuuint32_t)es, 1u, 1u};
   encode(&m, 5, base, dims, strides, box, est);
+  return m;
+}
+
+// L2-prefetch map (no shared-memory destination, so no swizzle): [B'][H][W][C] fp32, box
+// (box_c, box_w, box_h, 1)
+CUtensorMap make_map_prefetch(const float* base, int C, int W, int H, int B, int box_c, int box_w, int box_h) {
+  CUtensorMap m;
+  cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)B};
+  cuuint64_t strides[3] = {(cuuint64_t)C * 4, (cuuint64_t)W * C * 4, (cuuint64_t)H * W * C * 4};
+  cuuint32_t box[4] = {(cuuint32_t)box_c, (cuuint32_t)box_w, (cuuint32_t)box_h, 1u};
+  cuuint32_t est[4] = {1u, 1u, 1u, 1u};
+  encode(&m, 4, base, dims, strides, box, est, false);
   return m;
 }
 
@@ -161,7 +174,7 @@ struct EpiConv {
     }
     return (((long long)b * Ho + Y) * Wo + X) * Co + col;
   }
-  static constexpr int kBatch = 4, kBatchWide = 4;
+  static constexpr int kBatch = 1;  // rows whose global inputs are in flight together (measured best)
   struct Col {
     int col;
   };
@@ -388,13 +401,13 @@ Plan make_plan(const ConvDesc& d) {
 
 template <int BN, int AM, bool ASPLIT>
 void launch_bn(const Plan& P, const CUtensorMap& ta, const CUtensorMap& tbh, const CUtensorMap& tbl,
-               const tc::EpiConv& epi, cudaStream_t st) {
+               const CUtensorMap& te, const tc::EpiConv& epi, cudaStream_t st) {
   auto kern = tc::gemm3xtf32_kernel<BN, AM, ASPLIT, tc::EpiConv>;
   constexpr int smem = tc::gemm_smem_bytes<BN, AM, ASPLIT>();
   tc::ensure_smem((const void*)kern, smem);
   const long long units = (long long)P.mtiles * P.ntiles * P.g.nsplit;
   const int grid = (int)std::min<long long>(units, num_sms());
-  kern<<<grid, tc::kGemmThreads, smem, st>>>(ta, tbh, tbl, P.g, epi);
+  kern<<<grid, tc::kGemmThreads, smem, st>>>(ta, tbh, tbl, te, P.g, epi);
 }
 
 }  // namespace
@@ -404,7 +417,14 @@ bool conv_tc_try(const ConvDesc& d, const float* in, float* out, const float* ad
   if (!d.w || !d.w->d_hi || !d.ws_owner || !d.ws_owner->tc) return false;
   Plan P = make_plan(d);
   if (!P.ok) return false;
+  // epilogue-input prefetch: the addend tile of each unit (dense output tiles only)
+  if (addend && P.g.nsplit == 1 && d.mode != 2 && P.g.TW <= 256 && P.g.TH <= 256) {
+    P.g.epf = 1;
+    P.g.epf_planes = d.out_split ? 2 : 1;
+  }
   const tc::Geom& g = P.g;
+  const CUtensorMap te = g.epf ? tc::make_map_prefetch(addend, d.Co, d.Wo, d.Ho, d.B * g.epf_planes, P.BN, g.TW, g.TH)
+                               : CUtensorMap{};
   const int es = (d.mode == 1) ? 2 : 1;
   // A box: SS halo (TH + 2) lines of P pixels; TS halo (TH + 2) x (TW + 2); else the TW x TH window
   const int bw = P.am == 2 ? g.pitch : P.halo ? g.TW + 2 : g.TW;
@@ -439,13 +459,13 @@ bool conv_tc_try(const ConvDesc& d, const float* in, float* out, const float* ad
   auto dispatch = [&](auto bn_tag) {
     constexpr int BN = decltype(bn_tag)::value;
     if (P.am == 2) {
-      if constexpr (BN <= 64) launch_bn<BN, 2, false>(P, ta, tbh, tbl, epi, st);
+      if constexpr (BN <= 64) launch_bn<BN, 2, false>(P, ta, tbh, tbl, te, epi, st);
     } else if (P.halo) {
-      if (d.in_split) launch_bn<BN, 1, true>(P, ta, tbh, tbl, epi, st);
-      else launch_bn<BN, 1, false>(P, ta, tbh, tbl, epi, st);
+      if (d.in_split) launch_bn<BN, 1, true>(P, ta, tbh, tbl, te, epi, st);
+      else launch_bn<BN, 1, false>(P, ta, tbh, tbl, te, epi, st);
     } else {
-      if (d.in_split) launch_bn<BN, 0, true>(P, ta, tbh, tbl, epi, st);
-      else launch_bn<BN, 0, false>(P, ta, tbh, tbl, epi, st);
+      if (d.in_split) launch_bn<BN, 0, true>(P, ta, tbh, tbl, te, epi, st);
+      else launch_bn<BN, 0, false>(P, ta, tbh, tbl, te, epi, st);
     }
   };
   switch (P.BN) {
@@ -481,6 +501,7 @@ void tc_debug_counters(unsigned long long* out, int n, bool reset) {
     unsigned long long z[24] = {0};
     RTE_CHECK_CUDA(cudaMemcpyToSymbol(tc::g_tc_prof, z, sizeof(z)));
   }
+  apply_tc_debug_counters(out, n, reset);  // the apply kernels' copy (separate translation unit)
 }
 
 void conv_tc_prepare(mgnet_net* net) {

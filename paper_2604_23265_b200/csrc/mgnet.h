@@ -51,6 +51,7 @@ bool conv_tc_try(const ConvDesc& d, const float* in, float* out, const float* ad
                  const double* alpha, int alpha_stride, bool alpha_on_input, bool alpha_on_addend, cudaStream_t st);
 void conv_tc_prepare(struct ::mgnet_net* net);
 void tc_debug_counters(unsigned long long* out, int n, bool reset);
+void apply_tc_debug_counters(unsigned long long* out, int n, bool reset);  // (apply_tc.cu)
 
 void vcycle_run(const struct ::mgnet_net* net, const float* r, float* z, bool add_identity, const double* alpha,
                 int alpha_stride, cudaStream_t st);

@@ -93,6 +93,13 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* m, uin
       "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
 }
+// Bulk L2 prefetch of one box of a 4-D tensor map (no shared memory, no completion tracking).
+__device__ __forceinline__ void tma_prefetch_l2_4d(const CUtensorMap* m, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+               : "memory");
+}
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2,
                                             int c3) {
   asm volatile(
@@ -169,6 +176,42 @@ __device__ __forceinline__ void mma_tf32_ts_elect(uint32_t d_tmem, uint32_t a_tm
       "setp.ne.b32 p, %4, 0;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
       "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// One whole 32-wide K block of the fused 3xTF32 form in a single elected issue: for k = 0..3,
+//   D[tb] (+)= A_hi[:, 8k..] . [B_hi; B_lo]^T   (N = 2BN, idesc2)
+//   D[tx] +=   A_lo[:, 8k..] . B_hi^T           (N = BN, idesc1)
+// A from TMEM (a_hi / a_lo columns, +8 per K step), B from shared memory (descriptor +2 = +32 B per
+// K step).  accumulate = 0 starts D[tb] afresh (its X half tx is always accumulated into).
+__device__ __forceinline__ void mma_kblock_fused_ts(uint32_t tb, uint32_t tx, uint32_t a_hi, uint32_t a_lo,
+                                                    uint64_t bdesc, uint32_t idesc2, uint32_t idesc1,
+                                                    uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e, t;\n\t.reg .b64 b1, b2, b3;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %7, 0;\n\t"
+      "setp.eq.b32 t, 0, 0;\n\t"
+      "add.u64 b1, %4, 2;\n\tadd.u64 b2, %4, 4;\n\tadd.u64 b3, %4, 6;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%2], %4, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%1], [%3], %4, %6, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%2+8], b1, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%1], [%3+8], b1, %6, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%2+16], b2, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%1], [%3+16], b2, %6, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%2+24], b3, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%1], [%3+24], b3, %6, t;\n\t}" ::"r"(tb),
+      "r"(tx), "r"(a_hi), "r"(a_lo), "l"(bdesc), "r"(idesc2), "r"(idesc1), "r"(accumulate)
+      : "memory");
+}
+// Two tcgen05.commit arrivals (e.g. the B slot and the TMEM A buffer) from one elected lane.
+__device__ __forceinline__ void mma_commit2_elect(uint64_t* bar0, uint64_t* bar1) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%1];\n\t}" ::"r"(smem_u32(bar0)),
+      "r"(smem_u32(bar1))
       : "memory");
 }
 

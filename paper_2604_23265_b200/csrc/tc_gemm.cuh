@@ -61,6 +61,10 @@ struct Geom {
   int mtiles;       // M tiles (B * classes * tiles_y * tiles_x)
   int bn;           // N tile (the kernel's BN)
   int pitch;        // MMA-tile rows per output line (= TW, or the halo pitch P of SS-halo kernels)
+  int epf;          // epilogue-input L2 prefetch through tmE at each unit start: 0 none, 1 the
+                    // output-shaped tile (conv addend; epf_planes planes), 2 the tile's rows
+                    // oy0 - 1 .. oy0 + TH (apply: the cell and its upwind neighbours)
+  int epf_planes;
   int dbg;          // perf-experiment switches (RTE_TC_DBG; 0 in production): bit0 converters skip
                     // the row load/split/TMEM store, bit3 no MMAs, bit4 no TMA loads, bit5 no
                     // epilogue global traffic, bit6 role timers
@@ -70,7 +74,12 @@ struct Geom {
 // ring, and the epilogue staging tiles (one 128 x 32 fp32 tile per column half).
 constexpr int kHaloRows = 208;                  // (TW+2)(TH+2) <= 208, e.g. 34 x 6 for a 32 x 4 tile
 constexpr int kSSRows = 200;                    // SS-halo tile: (TH+2) P + 2 rows <= 200 (P = 16, 32)
-constexpr int kStageBytes = kTileM * 128;       // 128 rows x 32 fp32 per column half
+constexpr int kStageBytes = kTileM * 128;       // one staging tile: 128 rows x 32 fp32
+// epilogue staging: per column half, one tile per 32-column chunk (BN = 128: 2 chunks)
+template <int BN>
+constexpr int stage_chunks() {
+  return BN / 2 > 32 ? BN / 64 : 1;
+}
 // A modes: 0 = per-K-block window tiles (TS), 1 = halo tiles, 9 taps per tile (TS), 2 = SS halo:
 // the halo tile is split once in shared memory and each tap's A operand is a row-shifted SW128
 // descriptor into it (see the kernel comment).
@@ -80,8 +89,10 @@ struct Plan {
   static constexpr int kATile = AM == 2 ? kSSRows * 128 : AM == 1 ? kHaloRows * 128 : kABytes;
   static constexpr int kASlot = (ASPLIT || AM == 2 ? 2 : 1) * kATile;  // hi + lo tiles when split
   static constexpr int kBSlot = 2 * kBBytes;
-  static constexpr int kBudget = 190 * 1024;                        // rings
-  static constexpr int kNA = (AM != 0 || ASPLIT) ? 2 : 4;           // A ring depth
+  static constexpr int kBudget = (222 - 32 * stage_chunks<BN>()) * 1024;  // rings (+ staging = 222 KB)
+  // A ring depth: halo tiles are reused for 9 K blocks; window tiles are one K block each, so
+  // they need a deeper ring to cover the HBM latency (BN = 32 leaves room for 8)
+  static constexpr int kNA = (AM != 0 || ASPLIT) ? 2 : BN == 32 ? 8 : BN == 64 ? 4 : 3;
   static constexpr int kNBraw = (kBudget - kNA * kASlot) / kBSlot;
   static constexpr int kNB = kNBraw > 8 ? 8 : kNBraw;               // B ring depth
   static constexpr int kRingBytes = kNA * kASlot + kNB * kBSlot;
@@ -89,7 +100,7 @@ struct Plan {
 
 template <int BN, int AM, bool ASPLIT = false>
 constexpr int gemm_smem_bytes() {
-  return Plan<BN, AM, ASPLIT>::kRingBytes + 2 * kStageBytes + 1024 /*align*/ + 1024 /*barriers*/ +
+  return Plan<BN, AM, ASPLIT>::kRingBytes + 2 * stage_chunks<BN>() * kStageBytes + 1024 /*align*/ + 1024 /*barriers*/ +
          1024 /*row centres*/;
 }
 
@@ -104,7 +115,7 @@ constexpr bool tmem_fused() {
 // promoters, so a tile's epilogue overlaps the next tile's K loop) and 2 A buffers.
 // Split form: 2 main buffers + X + the rest as A buffers.
 #ifndef RTE_EPI_BATCH_MAX
-#define RTE_EPI_BATCH_MAX 1
+#define RTE_EPI_BATCH_MAX 8
 #endif
 #ifndef RTE_TC_NG_MAX
 #define RTE_TC_NG_MAX 6
@@ -196,10 +207,23 @@ __device__ __forceinline__ void a_origin(const Geom& g, const TileCoord& c, int 
 // wait conv+bfull, 4 MMA wait mempty/xempty, 5 MMA issue; 6 converter total, 7 converter wait,
 // 8 converter work; 9 promoter total, 10 promoter wait mfull, 11 promoter TMEM loads,
 // 12 epilogue; 13 K blocks (per CTA, producer); 14 converter K-block loop, 15 MMA K-block loop;
-// 16 epilogue staging + first barrier, 17 epilogue row loop, 18 epilogue final barrier.
+// 16 epilogue staging + first barrier, 17 epilogue row loop, 18 epilogue final barrier; 19 producer
+// wait A slot, 20 producer A TMA issue, 21 producer B TMA issue; 22 MMA wait bfull; 23 converter
+// wait afull.
 __device__ unsigned long long g_tc_prof[24];
 
 // (the warp stays converged: the timer is predicated, the wait is executed once by all lanes)
+// Epilogue-input L2 prefetch for unit w (Geom::epf): the output-shaped tile (per plane), or the
+// tile's rows oy0 - 1 .. oy0 + TH.
+__device__ __forceinline__ void epi_prefetch(const Geom& g, const CUtensorMap* tmE, const Unit& w) {
+  const int x0 = w.tc.tx * g.TW, y0 = w.tc.ty * g.TH;
+  if (g.epf == 1) {
+    for (int pl = 0; pl < g.epf_planes; ++pl) tma_prefetch_l2_4d(tmE, w.n0, x0, y0, w.tc.b * g.epf_planes + pl);
+  } else {
+    for (int dy = -1; dy <= 1; ++dy) tma_prefetch_l2_4d(tmE, w.n0, x0, y0 + dy, w.tc.b);
+  }
+}
+
 __device__ __forceinline__ void tw_wait(uint64_t* bar, uint32_t par, bool on, long long& acc) {
   const long long t0 = on ? clock64() : 0;
   mbar_wait(bar, par);
@@ -229,7 +253,8 @@ __device__ __forceinline__ void tw_wait(uint64_t* bar, uint32_t par, bool on, lo
 template <int BN, int AM, bool ASPLIT, class Epi>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm3xtf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBhi,
-                      const __grid_constant__ CUtensorMap tmBlo, const Geom g, const Epi epi) {
+                      const __grid_constant__ CUtensorMap tmBlo, const __grid_constant__ CUtensorMap tmE,
+                      const Geom g, const Epi epi) {
   constexpr bool HALO = AM != 0;
   constexpr bool SSH = AM == 2;
   static_assert(BN == 32 || BN == 64 || BN == 128, "N tile must be 32, 64 or 128");
@@ -262,7 +287,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* cempty = cfull + 2;        // [2] row centres read (256 epilogue threads)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cempty + 2);
   float* cvec = reinterpret_cast<float*>(smem + PL::kRingBytes + 1024);  // [2][128] row centres
-  const uint32_t stage_s = smem_u32(smem + PL::kRingBytes + 2048);        // [2 halves][128][32] staging
+  const uint32_t stage_s = smem_u32(smem + PL::kRingBytes + 2048);        // [2 halves][chunks][128][32] staging
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int units = g.mtiles * g.ntiles * g.nsplit;
@@ -272,8 +297,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                                   : (uint32_t)rows * 128u;
   // bit6 enables the counters; bits 8..15 (if set) restrict them to kernels with that BN, bit16 to
   // halo kernels
+  // (bit 17: only non-halo kernels, bit 18: only row-centred (apply) kernels, bit 19: only convs)
   const bool prof = (g.dbg & 64) && lane == 0 && (((g.dbg >> 8) & 0xff) == 0 || ((g.dbg >> 8) & 0xff) == BN) &&
-                    (!((g.dbg >> 16) & 1) || HALO);
+                    (!((g.dbg >> 16) & 1) || HALO) && (!((g.dbg >> 17) & 1) || !HALO) &&
+                    (!((g.dbg >> 18) & 1) || Epi::kCenter) && (!((g.dbg >> 19) & 1) || !Epi::kCenter) &&
+                    (((g.dbg >> 24) & 0xff) == 0 || ((g.dbg >> 24) & 0xff) == g.kb_total);  // bits 24..31: K blocks
   long long w_d = 0, w_e = 0;
   long long w_a = 0, w_b = 0, w_c = 0;
   long long w_s1 = 0, w_s2 = 0, w_s3 = 0;
@@ -306,6 +334,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     tma_prefetch(&tmA);
     tma_prefetch(&tmBhi);
     tma_prefetch(&tmBlo);
+    if (g.epf) tma_prefetch(&tmE);
   }
   if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
   tc_fence_before();
@@ -322,6 +351,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       const Unit w = decode_unit(g, u);
       const int brow = w.n0 + w.tc.cls * g.b_rows_class + w.tc.b * g.b_rows_batch;
+      // epf = 2 (apply: long K loops): the producer's unit start is lead time enough
+      if (g.epf == 2 && elect_one()) epi_prefetch(g, &tmE, w);
+      __syncwarp();
       for (int kb = w.kb0; kb < w.kb1; ++kb, ++n_kb) {
         int tap, cc;
         kb_split<HALO>(g, kb, tap, cc);
@@ -335,6 +367,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           } else {
             a_origin(g, w.tc, tap, xA, yA);
           }
+          const long long tp0 = prof ? clock64() : 0;
           if (elect_one()) {
             if (g.dbg & 16) {
               mbar_arrive(&afull[as]);
@@ -351,9 +384,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             }
           }
           __syncwarp();
+          if (prof) w_s2 += clock64() - tp0;
           if (++as == NAR) { as = 0; aph ^= 1; }
         }
         tw_wait(&bempty[bs], bph ^ 1, prof, w_b);
+        const long long tp1 = prof ? clock64() : 0;
         if (elect_one()) {
           uint8_t* sb = bring + bs * PL::kBSlot;
           const int kcol = HALO ? tap * g.cchunks * 32 + cc * 32 : kb * 32;
@@ -366,6 +401,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
         }
         __syncwarp();
+        if (prof) w_s3 += clock64() - tp1;
         if (++bs == NBR) { bs = 0; bph ^= 1; }
       }
     }
@@ -396,7 +432,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           if (SSH) kb_split<true>(g, kb, tap, cc);
           if (!SSH) tw_wait(&conv[ab], abph, prof, w_a);
           else if (tap == 0 || kb == w.kb0) tw_wait(&conv[as], aph, prof, w_a);  // halo tile split
-          tw_wait(&bfull[bs], bph, prof, w_a);
+          tw_wait(&bfull[bs], bph, prof, w_s1);
           tc_fence_after();
           const uint32_t sb = smem_u32(bring + bs * PL::kBSlot);
           const uint64_t d_bh = sdesc_sw128(sb), d_bl = sdesc_sw128(sb + BBYTES);
@@ -428,15 +464,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             }
           } else if (!no_mma) {
             if constexpr (FUSED) {
-              // hi.[B_hi; B_lo] -> [main_t | X_t] (N = 2BN), lo.B_hi -> X_t
+              // hi.[B_hi; B_lo] -> [main_t | X_t] (N = 2BN), lo.B_hi -> X_t: one elected issue
               constexpr uint32_t idesc2 = idesc_tf32(kTileM, 2 * BN);
               const uint32_t tbuf = tmem + (uint32_t)(t * 2 * BN);
-#pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                mma_tf32_ts_elect(tbuf, a_hi + 8u * k, d_bh + 2u * k, idesc2, acc_m);
-                acc_m = 1;
-                mma_tf32_ts_elect(tbuf + BN, a_lo + 8u * k, d_bh + 2u * k, idesc, 1);
-              }
+              mma_kblock_fused_ts(tbuf, tbuf + BN, a_hi, a_lo, d_bh, idesc2, idesc, acc_m);
+              acc_m = 1;
             } else {
               const uint32_t tm = tmem + (uint32_t)(t * BN);
 #pragma unroll
@@ -450,14 +482,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               }
             }
           }
-          mma_commit_elect(&bempty[bs]);
           if (SSH) {
+            mma_commit_elect(&bempty[bs]);
             if (tap == 8 || kb + 1 == w.kb1) {  // last tap of this halo tile: release the A slot
               mma_commit_elect(&aempty[as]);
               if (++as == NAR) { as = 0; aph ^= 1; }
             }
           } else {
-            mma_commit_elect(&afree[ab]);
+            mma_commit2_elect(&bempty[bs], &afree[ab]);
             if (++ab == NA) { ab = 0; abph ^= 1; }
           }
           if (prof) w_d += clock64() - ti0;
@@ -609,12 +641,26 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     int li = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++li) {
       const Unit w = decode_unit(g, u);
+      if (g.epf == 1 && warp == 6 && lane == 0) {
+        // pull the epilogue's global inputs into L2 one unit ahead (this unit's at the first):
+        // far enough ahead to cover a short K loop, near enough that the output stream does not
+        // evict them first (measured)
+        if (li == 0) epi_prefetch(g, &tmE, w);
+        if (u + (int)gridDim.x < units) epi_prefetch(g, &tmE, decode_unit(g, u + gridDim.x));
+      }
       float acc[HB];
 #pragma unroll
       for (int i = 0; i < HB; ++i) acc[i] = 0.f;
       for (int kbg = w.kb0; kbg < w.kb1; kbg += kPromoteKB, ++gcount) {
         const int t = gcount % NG;
-        tw_wait(&mfull[t], (uint32_t)(gcount / NG) & 1u, prof, w_a);
+        {
+          // one leader polls the mbarrier; the other promoter warps block on a hardware named
+          // barrier (no issue slots spent polling), then order their TMEM loads after it
+          const long long tw0 = prof ? clock64() : 0;
+          if (warp == 6) mbar_wait(&mfull[t], (uint32_t)(gcount / NG) & 1u);
+          named_bar_sync(4, 256);
+          if (prof) w_a += clock64() - tw0;
+        }
         tc_fence_after();
         const long long tl0 = prof ? clock64() : 0;
         // fused form: main_t at t*2BN, X_t at t*2BN + BN; split form: main_t at t*BN
@@ -655,31 +701,36 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       // shared tile (row r at r*128 B, 16-byte chunk q at position q ^ (r & 7): conflict-free both
       // ways), then the half's four warps walk their rows with float4 lanes, so every global
       // load/store instruction covers whole rows (128 B each) instead of 32 scattered lines.
-      const uint32_t sh = stage_s + (uint32_t)(half * kStageBytes);
+      constexpr int NCH = stage_chunks<BN>();
+      const uint32_t sh = stage_s + (uint32_t)(half * NCH * kStageBytes);
       // per-unit epilogue state: tile origin in the class grid and the epilogue's tile constants
       const int e_oy0 = w.tc.ty * g.TH, e_ox0 = w.tc.tx * g.TW;
       const typename Epi::Tile et = epi.tile(w.tc.b, w.tc.cls, e_oy0, e_ox0);
+      const long long ts0 = prof ? clock64() : 0;
+      // stage every column chunk of this half first (the accumulators die here, leaving registers
+      // for a batch of rows in flight below)
 #pragma unroll
-      for (int c0 = 0; c0 < HB; c0 += CW) {
-        const long long ts0 = prof ? clock64() : 0;
+      for (int c0 = 0; c0 < HB; c0 += CW)
 #pragma unroll
         for (int k = 0; k < CW / 4; ++k)
-          sts128(sh + (uint32_t)(r * 128 + ((k ^ (r & 7)) << 4)),
+          sts128(sh + (uint32_t)((c0 / CW) * kStageBytes + r * 128 + ((k ^ (r & 7)) << 4)),
                  make_float4(acc[c0 + 4 * k], acc[c0 + 4 * k + 1], acc[c0 + 4 * k + 2], acc[c0 + 4 * k + 3]));
-        named_bar_sync(2 + half, 128);
-        const long long ts1 = prof ? clock64() : 0;
-        if (prof) w_s1 += ts1 - ts0;
-        if (!(g.dbg & 32)) {
-          // rows are finished in batches: every global input of a batch (epi.row + epi.load) is
-          // requested before any output of it is stored, so the batch costs one memory round trip
-          // (out may alias the epilogue inputs elementwise only, which this order preserves)
-          constexpr int NIT = 32 / RPI;
-          constexpr int BMAX0 = BN == 128 ? Epi::kBatchWide : Epi::kBatch;  // (BN = 128: acc is live)
-          constexpr int BMAX = BMAX0 < RTE_EPI_BATCH_MAX ? BMAX0 : RTE_EPI_BATCH_MAX;
-          constexpr int BATCH = NIT < BMAX ? NIT : BMAX;
-          const int k = lane % LPR;
-          const int col = w.n0 + cbase + c0 + 4 * k;
+      named_bar_sync(2 + half, 128);
+      const long long ts1 = prof ? clock64() : 0;
+      if (prof) w_s1 += ts1 - ts0;
+      if (!(g.dbg & 32)) {
+        // rows are finished in batches: every global input of a batch (epi.row + epi.load) is
+        // requested before any output of it is stored, so the batch costs one memory round trip
+        // (out may alias the epilogue inputs elementwise only, which this order preserves)
+        constexpr int NIT = 32 / RPI;
+        constexpr int BMAX = Epi::kBatch < RTE_EPI_BATCH_MAX ? Epi::kBatch : RTE_EPI_BATCH_MAX;
+        constexpr int BATCH = NIT < BMAX ? NIT : BMAX;
+        const int k = lane % LPR;
+#pragma unroll 1
+        for (int c = 0; c < NCH; ++c) {
+          const int col = w.n0 + cbase + c * CW + 4 * k;
           const typename Epi::Col cv = epi.col(col);
+          const uint32_t shc = sh + (uint32_t)(c * kStageBytes);
           int ly = e_ly0, lx = e_lx0;  // tile-local pixel of this lane's row rr = e_rr0 + it * RPI
 #pragma unroll 1
           for (int it0 = 0; it0 < NIT; it0 += BATCH) {
@@ -694,7 +745,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               if (ok[q]) {
                 const float crr = Epi::kCenter ? cvec[(li & 1) * 128 + rr] : 0.f;
                 rw[q] = epi.row(et, epi.rel(ly, lx), oy, ox, crr);
-                if (g.nsplit == 1) pre[q] = epi.load(rw[q], cv);
+                if (g.nsplit == 1 && !(g.dbg & (1 << 20))) pre[q] = epi.load(rw[q], cv);
               }
               lx += e_dlx;
               ly += e_dly;
@@ -705,9 +756,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             }
 #pragma unroll
             for (int q = 0; q < BATCH; ++q) {
-              if (!ok[q]) continue;
+              if (!ok[q] || (g.dbg & (1 << 21))) continue;
               const int rr = e_rr0 + (it0 + q) * RPI;
-              const float4 v = lds128(sh + (uint32_t)(rr * 128 + ((k ^ (rr & 7)) << 4)));
+              const float4 v = lds128(shc + (uint32_t)(rr * 128 + ((k ^ (rr & 7)) << 4)));
               if (g.nsplit > 1)
                 epi.store_partial4(w.split, rw[q], col, v);
               else
@@ -715,13 +766,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             }
           }
         }
-        const long long ts2 = prof ? clock64() : 0;
-        named_bar_sync(2 + half, 128);
-        if (prof) {
-          const long long ts3 = clock64();
-          w_s2 += ts2 - ts1;
-          w_s3 += ts3 - ts2;
-        }
+      }
+      const long long ts2 = prof ? clock64() : 0;
+      named_bar_sync(2 + half, 128);
+      if (prof) {
+        const long long ts3 = clock64();
+        w_s2 += ts2 - ts1;
+        w_s3 += ts3 - ts2;
       }
       if constexpr (Epi::kCenter) mbar_arrive(&cempty[li & 1]);
       if (prof) w_e += clock64() - te0;
@@ -733,17 +784,22 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       atomicAdd(&g_tc_prof[0], tot);
       atomicAdd(&g_tc_prof[1], (unsigned long long)(w_a + w_b));
       atomicAdd(&g_tc_prof[13], (unsigned long long)n_kb);
+      atomicAdd(&g_tc_prof[19], (unsigned long long)w_a);   // producer: wait A slot
+      atomicAdd(&g_tc_prof[20], (unsigned long long)w_s2);  // producer: issue A TMA
+      atomicAdd(&g_tc_prof[21], (unsigned long long)w_s3);  // producer: issue B TMAs
     } else if (warp == 1) {
       atomicAdd(&g_tc_prof[2], tot);
       atomicAdd(&g_tc_prof[3], (unsigned long long)w_a);
       atomicAdd(&g_tc_prof[4], (unsigned long long)(w_b + w_c));
       atomicAdd(&g_tc_prof[5], (unsigned long long)w_d);
       atomicAdd(&g_tc_prof[15], (unsigned long long)w_e);
+      atomicAdd(&g_tc_prof[22], (unsigned long long)w_s1);  // MMA: wait bfull (in mma_wait_in: no)
     } else if (warp == 2) {
       atomicAdd(&g_tc_prof[6], tot);
       atomicAdd(&g_tc_prof[7], (unsigned long long)(w_a + w_b));
       atomicAdd(&g_tc_prof[8], (unsigned long long)w_d);
       atomicAdd(&g_tc_prof[14], (unsigned long long)w_e);
+      atomicAdd(&g_tc_prof[23], (unsigned long long)w_a);  // converter: wait afull (new A tile)
     } else {
       atomicAdd(&g_tc_prof[9], tot);
       atomicAdd(&g_tc_prof[10], (unsigned long long)w_a);

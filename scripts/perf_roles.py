@@ -23,12 +23,13 @@ torch.cuda.synchronize()
 buf = (C.c_uint64 * 24)()
 _lib.lib.rte_debug_counters(buf, 24, 1)
 P.mgnet_vcycle(net, x, z, True)
+P.rte_apply(p, x, z)  # (the filter bits in RTE_TC_DBG select which kernels are counted)
 torch.cuda.synchronize()
 _lib.lib.rte_debug_counters(buf, 24, 1)
 v = list(buf)
 kb = max(v[13], 1)
 names = ["prod_total", "prod_wait", "mma_total", "mma_wait_in", "mma_wait_acc", "mma_issue", "conv_total",
-         "conv_wait", "conv_work", "prom_total", "prom_wait", "prom_tmem", "epilogue", "kblocks", "conv_kbloop", "mma_kbloop", "epi_stage", "epi_rows", "epi_bar2"]
+         "conv_wait", "conv_work", "prom_total", "prom_wait", "prom_tmem", "epilogue", "kblocks", "conv_kbloop", "mma_kbloop", "epi_stage", "epi_rows", "epi_bar2", "prod_waitA", "prod_issueA", "prod_issueB", "mma_wait_bfull", "conv_wait_afull"]
 print(f"dbg={os.environ.get('RTE_TC_DBG')} kblocks={v[13]} (cycles per K block, summed over CTAs):")
 for i, nm in [(i, n) for i, n in enumerate(names) if i != 13]:
     print(f"  {nm:14s} {v[i] / kb:10.1f}")
