@@ -122,6 +122,114 @@ __global__ void __launch_bounds__(256) apply_simt_kernel(
   }
 }
 
+// Wide-tile SIMT apply (M % 128 == 0; the fp64 restart residual): tile = 128 cells x 128
+// ordinates, 256 threads, each 8 cells x 8 ordinates (cells ty*4+a and 64+ty*4+a, ordinates tx*4+c
+// and 64+tx*4+c: conflict-free LDS.128 and 64 FMAs per 8 shared loads), K in chunks of 8 staged
+// through double-buffered shared memory with a register prefetch of the next chunk.  Same
+// arithmetic as apply_simt_kernel: centred contraction, then the stencil epilogue.
+template <typename T>
+__global__ void __launch_bounds__(256) apply_simt_wide_kernel(
+    int N, int M, const T* __restrict__ x, T* __restrict__ y, const T* __restrict__ St,
+    const T* __restrict__ sig_t, const T* __restrict__ sig_s, const T* __restrict__ axv,
+    const T* __restrict__ ayv, const int8_t* __restrict__ sgx, const int8_t* __restrict__ sgy,
+    const float* __restrict__ bvec, const double* __restrict__ alpha, int alpha_stride) {
+  constexpr int TP = 128, TMO = 128, KC = 8;
+  __shared__ __align__(16) T As[2][KC][TP];
+  __shared__ __align__(16) T Bs[2][KC][TMO];
+  const int tid = threadIdx.x;
+  const int tx = tid % 16, ty = tid / 16;
+  const int bsample = blockIdx.z;
+  const int64_t cells = (int64_t)N * N;
+  const int64_t c0 = (int64_t)blockIdx.x * TP;
+  const int m0 = blockIdx.y * TMO;
+  const T* xs = x + (int64_t)bsample * cells * M;
+  const T* Sts = St + (int64_t)bsample * M * M;
+  // global -> register staging: A chunk = 128 cells x 8 k (4 per thread: cell tid/8 + 32r,
+  // k tid%8), B chunk = 8 k x 128 ordinates (4 per thread: k tid/128*... row-contiguous)
+  const int a_cl = tid / KC, a_k = tid % KC;
+  T ctr[4];  // centres psi_{cell, 0} of this thread's 4 staged cells
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int64_t cell = c0 + a_cl + 32 * r;
+    ctr[r] = cell < cells ? xs[cell * M] : T(0);
+  }
+  T ra[4], rb[4];
+  auto load_chunk = [&](int k0) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int64_t cell = c0 + a_cl + 32 * r;
+      ra[r] = cell < cells ? xs[cell * M + k0 + a_k] - ctr[r] : T(0);
+      const int e = tid + 256 * r, kk = e / TMO, o = e % TMO;
+      rb[r] = Sts[(int64_t)(k0 + kk) * M + m0 + o];
+    }
+  };
+  auto store_chunk = [&](int buf) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      As[buf][a_k][a_cl + 32 * r] = ra[r];
+      const int e = tid + 256 * r;
+      Bs[buf][e / TMO][e % TMO] = rb[r];
+    }
+  };
+  T acc[8][8];
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc[a][c] = T(0);
+  load_chunk(0);
+  store_chunk(0);
+  __syncthreads();
+  int buf = 0;
+  for (int k0 = 0; k0 < M; k0 += KC) {
+    const bool more = k0 + KC < M;
+    if (more) load_chunk(k0 + KC);
+#pragma unroll
+    for (int kk = 0; kk < KC; ++kk) {
+      T av[8], bv[8];
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          av[4 * h + q] = As[buf][kk][64 * h + ty * 4 + q];
+          bv[4 * h + q] = Bs[buf][kk][64 * h + tx * 4 + q];
+        }
+#pragma unroll
+      for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc[a][c] = fma(av[a], bv[c], acc[a][c]);
+    }
+    if (more) {
+      store_chunk(buf ^ 1);
+      __syncthreads();
+      buf ^= 1;
+    }
+  }
+  const T al = alpha ? (T)alpha[(int64_t)bsample * alpha_stride] : T(1);
+#pragma unroll
+  for (int a = 0; a < 8; ++a) {
+    const int64_t cell = c0 + 64 * (a / 4) + ty * 4 + (a % 4);
+    if (cell >= cells) continue;
+    const int i = (int)(cell % N), j = (int)(cell / N);
+    const int64_t gcell = (int64_t)bsample * cells + cell;
+    const T st = sig_t[gcell], ss = sig_s[gcell];
+    const T cc = xs[cell * M];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int m = m0 + 64 * (c / 4) + tx * 4 + (c % 4);
+      const T ax = axv[m], ay = ayv[m];
+      const T psi = xs[cell * M + m];
+      T v = (ax + ay + st) * psi - ss * (cc + acc[a][c]);
+      const int ii = i - sgx[m], jj = j - sgy[m];
+      if (ii >= 0 && ii < N) v -= ax * xs[(cell - sgx[m]) * M + m];
+      if (jj >= 0 && jj < N) v -= ay * xs[(cell - (int64_t)sgy[m] * N) * M + m];
+      v *= al;
+      const int64_t o = gcell * M + m;
+      if (bvec) v = (T)bvec[o] - v;
+      y[o] = v;
+    }
+  }
+}
+
 template <typename T>
 void launch_simt(const rte_problem* p, const T* x, T* y, const T* St, const T* st, const T* ss,
                  const T* ax, const T* ay, const float* b, const double* alpha, int alpha_stride,
@@ -134,6 +242,12 @@ void launch_simt(const rte_problem* p, const T* x, T* y, const T* St, const T* s
     apply_simt_kernel<T, TMO><<<grid, 256, 0, stream>>>(p->N, p->M, x, y, St, st, ss, ax, ay, p->sgx, p->sgy,
                                                          b, alpha, alpha_stride);
   };
+  if (p->M % 128 == 0) {
+    dim3 grid((unsigned)((cells + 127) / 128), (unsigned)(p->M / 128), (unsigned)p->B);
+    apply_simt_wide_kernel<T><<<grid, 256, 0, stream>>>(p->N, p->M, x, y, St, st, ss, ax, ay, p->sgx, p->sgy, b,
+                                                        alpha, alpha_stride);
+    return;
+  }
   if (p->M <= 16) go(std::integral_constant<int, 16>{});
   else if (p->M <= 32) go(std::integral_constant<int, 32>{});
   else go(std::integral_constant<int, 64>{});

@@ -71,7 +71,13 @@ def test_apply_and_rhs_parity(cfg):
     assert _rel(b.cpu().numpy(), O.rhs(op)) <= 1e-7
 
 
-@pytest.mark.parametrize("cfg", [W.config(k) for k in (1, 2, 3)] + SMALL, ids=lambda c: f"cfg{c.k}-N{c.N}-M{c.M}")
+WIDE = [  # M % 128 == 0: the wide-tile SIMT kernel (fp64 restart residual), ragged cell tiles
+    W.small_config(4, N=13, M=128, n_polar=4, n_azim=32, B=2),
+    W.small_config(5, N=12, M=256, n_polar=4, n_azim=64),
+]
+
+
+@pytest.mark.parametrize("cfg", [W.config(k) for k in (1, 2, 3)] + SMALL + WIDE, ids=lambda c: f"cfg{c.k}-N{c.N}-M{c.M}")
 def test_apply_f64_parity(cfg):
     import paper_2604_23265_b200 as P
     media = W.make_media(cfg)
