@@ -278,12 +278,24 @@ def run_ours(args, cfg):
         if dist is not None:
             dist.barrier()
 
+    # ---- profiled solve (untimed): every launch bracketed by CUDA events -> per-class device
+    # times (the "kernels" breakdown) and the dominant class.  The event pairs of every launch
+    # cost ~10% of a step, so the timed solve below instruments only the dominant class.
+    x.zero_()
+    P.rte_timing_enable(True)
+    P.rte_timing_filter(None)
+    P.rte_timing_reset()
+    solve(x, b, K)
+    torch.cuda.synchronize()
+    all_classes = P.rte_timing_get()
+    dominant = max(all_classes, key=lambda c: c["ms"])["name"] if all_classes else None
+
     # ---- timed region: one solve of exactly K inner iterations --------------------------
     x.zero_()
     sampler = ClockSampler(_device_index(torch, local))
     sampler.start()
     P.rte_launch_count(reset=True)
-    P.rte_timing_enable(True)
+    P.rte_timing_filter(dominant)  # the dominant kernel's launches are timed live, nothing else
     P.rte_timing_reset()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
@@ -295,7 +307,8 @@ def run_ours(args, cfg):
     barrier()
     ms = ev0.elapsed_time(ev1)
     launches = P.rte_launch_count(reset=True)
-    classes = P.rte_timing_get()
+    classes = P.rte_timing_get()  # the dominant class only, timed inside the timed region
+    P.rte_timing_filter(None)
     P.rte_timing_enable(False)
     clocks = sampler.stop()
     iters = rep[0]["iterations"] if cfg.B == 1 else sum(r["iterations"] for r in rep) / cfg.B
@@ -344,9 +357,11 @@ def run_ours(args, cfg):
     if rank == 0:
         peaks, src = _peaks()
         roof, top = _roofline(classes, peaks, src)
-        tot_ms = sum(c["ms"] for c in classes) or 1.0
+        if roof is not None:
+            roof["timed"] = "live in the timed region (only this class carries CUDA events there)"
+        tot_ms = sum(c["ms"] for c in all_classes) or 1.0
         kernels = sorted(({"name": c["name"], "kind": c["kind"], "launches": c["launches"],
-                           "ms": round(c["ms"], 4), "share": round(c["ms"] / tot_ms, 4)} for c in classes),
+                           "ms": round(c["ms"], 4), "share": round(c["ms"] / tot_ms, 4)} for c in all_classes),
                          key=lambda d: -d["ms"])
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": Wm,
                 "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -362,7 +377,7 @@ def run_ours(args, cfg):
                         "h2d_bytes_per_step": h2d / K, "d2h_bytes_per_step": d2h / K,
                         "note": f"one solve of K={K} iterations per measurement: b (fp32) copied H2D from pinned "
                                 "host memory before it and x (fp64) D2H after it; bytes amortised per step"},
-                "gpu_launches": launches, "clocks": clocks, "ops": ops, "kernels": kernels[:12]}
+                "gpu_launches": launches, "clocks": clocks, "ops": ops, "kernels": kernels}
         if ws == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = _cpu_baseline(cfg, media, weights)
         print(json.dumps(line), flush=True)

@@ -181,6 +181,11 @@ int64_t rte_launch_count(int reset);
  * (idx = -1 only queries the count).  rte_timing_reset clears the aggregates.  Any output
  * pointer may be NULL.  Errors: RTE_EINVAL (idx out of range), RTE_ECUDA. */
 rte_status rte_timing_enable(int on);
+/* Restrict per-launch timing to the class named `name` (NULL or "" = every class): the other
+ * launches record no events (the event pairs of every launch cost ~10% of a GMRES step at
+ * config 5, so bench.py times its headline solve with only the dominant class instrumented).
+ * Errors: none. */
+rte_status rte_timing_filter(const char* name);
 /* Experiments only: per-role cycle counters of the tensor-core GEMM (collected when the
  * environment variable RTE_TC_DBG has bit 6 set); copies min(n, 24) counters, then zeroes them
  * if reset != 0.  Slot meanings are listed in csrc/tc_gemm.cuh (g_tc_prof). */

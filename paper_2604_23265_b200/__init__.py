@@ -16,7 +16,7 @@ from . import _lib
 from ._lib import RteError, check, gmres_opts, gmres_report, lib
 
 __all__ = ["Problem", "MgNet", "rte_setup", "rte_rhs", "rte_apply", "rte_apply_f64", "mgnet_create",
-           "mgnet_vcycle", "mgnet_vcycle_f64", "gmres_solve", "rte_quadrature", "rte_hg_matrix", "rte_launch_count", "rte_timing_enable", "rte_timing_reset",
+           "mgnet_vcycle", "mgnet_vcycle_f64", "gmres_solve", "rte_quadrature", "rte_hg_matrix", "rte_launch_count", "rte_timing_enable", "rte_timing_filter", "rte_timing_reset",
            "rte_timing_get", "RteError", "LIB_PATH"]
 
 LIB_PATH = _lib.LIB_PATH
@@ -216,6 +216,11 @@ def rte_launch_count(reset: bool = False) -> int:
 
 def rte_timing_enable(on: bool = True) -> None:
     check("rte_timing_enable", lib.rte_timing_enable(int(on)))
+
+
+def rte_timing_filter(name: Optional[str] = None) -> None:
+    """Time only the launches of class `name` (None = all classes)."""
+    check("rte_timing_filter", lib.rte_timing_filter(name.encode() if name else None))
 
 
 def rte_timing_reset() -> None:

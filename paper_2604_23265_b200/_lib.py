@@ -67,6 +67,7 @@ SIGS = {
     "rte_launch_count": (C.c_int64, [C.c_int]),
     "rte_last_error": (C.c_char_p, []),
     "rte_timing_enable": (C.c_int, [C.c_int]),
+    "rte_timing_filter": (C.c_int, [C.c_char_p]),
     "rte_debug_counters": (C.c_int, [C.POINTER(C.c_uint64), C.c_int, C.c_int]),
     "rte_timing_reset": (C.c_int, []),
     "rte_timing_get": (C.c_int, [C.c_int, C.c_char_p, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int64),

@@ -266,7 +266,7 @@ double apply_bytes(const rte_problem* p, int elt, int b_elt) {
 void launch_rhs(const rte_problem* p, float* b, cudaStream_t st) {
   int64_t n = p->n;
   int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 16);
-  prof_begin(st);
+  prof_begin(st, "rhs");
   rhs_kernel<<<blocks, 256, 0, st>>>(p->B, p->N, p->M, p->f, p->inflow, p->ax, p->ay, p->sgx, p->sgy, b);
   after_launch("rhs", st, 0.0, 4.0 * (double)n + 4.0 * p->ncell, 0);
 }
@@ -277,13 +277,13 @@ void launch_apply_f32(const rte_problem* p, const float* x, float* y, const doub
     launch_apply_tc(p, x, y, alpha, alpha_stride, st);
     return;
   }
-  prof_begin(st);
+  prof_begin(st, "apply_f32_simt");
   launch_simt<float>(p, x, y, p->St32, p->sig_t, p->sig_s, p->ax, p->ay, nullptr, alpha, alpha_stride, st);
   after_launch("apply_f32_simt", st, apply_flops(p), apply_bytes(p, 4, 0), 2);
 }
 
 void launch_apply_f64(const rte_problem* p, const double* x, double* y, const float* b, cudaStream_t st) {
-  prof_begin(st);
+  prof_begin(st, "apply_f64_simt");
   launch_simt<double>(p, x, y, p->St64, p->sig_t64, p->sig_s64, p->ax64, p->ay64, b, nullptr, 0, st);
   after_launch("apply_f64_simt", st, apply_flops(p), apply_bytes(p, 8, b ? 4 : 0), 3);
 }

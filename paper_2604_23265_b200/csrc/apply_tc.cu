@@ -151,7 +151,7 @@ void launch_apply_tc(const rte_problem* p, const float* x, float* y, const doubl
   CUtensorMap tbh = tc::make_map_kmajor(p->S_hi, M, B * M, BN);
   CUtensorMap tbl = tc::make_map_kmajor(p->S_lo, M, B * M, BN);
   tc::EpiApply epi{x, y, p->sig_t, p->sig_s, p->ax, p->ay, p->sgx, p->sgy, alpha, alpha_stride, N, M};
-  prof_begin(st);
+  prof_begin(st, "apply_f32_tc");
   switch (BN) {
     case 32: tc::launch_apply_bn<32>(g, mtiles, ta, tbh, tbl, te, epi, st); break;
     case 64: tc::launch_apply_bn<64>(g, mtiles, ta, tbh, tbl, te, epi, st); break;

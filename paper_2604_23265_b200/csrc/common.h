@@ -37,7 +37,9 @@ struct Fail {
 // launch's ALGORITHMIC flops and bytes (DESIGN.md §5 gives the per-unit figures).
 // kind: 0 HBM-bound streaming, 1 3xTF32 tensor-core contraction, 2 fp32 SIMT contraction,
 //       3 fp64 SIMT, 4 tiny/latency (Givens etc.).
-void prof_begin(cudaStream_t st);
+// cls = the launch's timing class (the name after_launch will book); with a class filter set
+// (rte_timing_filter), only launches whose class starts with it are timed.
+void prof_begin(cudaStream_t st, const char* cls = nullptr);
 void after_launch(const char* what, cudaStream_t st = 0, double flops = 0.0, double bytes = 0.0, int kind = 4);
 
 template <typename T>

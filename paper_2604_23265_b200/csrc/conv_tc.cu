@@ -455,7 +455,7 @@ bool conv_tc_try(const ConvDesc& d, const float* in, float* out, const float* ad
     }
     epi.part = d.ws_owner->tc_ws;
   }
-  prof_begin(st);
+  prof_begin(st, conv_class_name(d, true));
   auto dispatch = [&](auto bn_tag) {
     constexpr int BN = decltype(bn_tag)::value;
     if (P.am == 2) {
@@ -476,7 +476,7 @@ bool conv_tc_try(const ConvDesc& d, const float* in, float* out, const float* ad
   const bool split = g.nsplit > 1;
   after_launch(conv_class_name(d, true), st, conv_flops(d), split ? 0.0 : conv_bytes(d, addend != nullptr), 1);
   if (split) {
-    prof_begin(st);
+    prof_begin(st, "splitk_reduce");
     const long long n4 = P.out_elems / 4;
     const long long per4 = n4 / d.B;
     const int blocks = (int)std::min<long long>((n4 + 255) / 256, (long long)num_sms() * 8);

@@ -384,7 +384,8 @@ static void launch_cgs(const GmresWork& W, const TB* V, int nv, bool update, boo
   RedArgs ra{W.partials, W.counters, out, kMaxRestart + 2, W.nblk};
   dim3 grid(W.nblk, W.B);
   const int64_t vld = W.ns * W.B;
-  prof_begin(st);
+  const char* cls = sel_w2 ? "cgs_reorth_selective" : update ? (dots ? "cgs_update_dots" : "cgs_update") : "cgs_dots";
+  prof_begin(st, cls);
   auto go = [&](auto nv_tag, auto up_tag, auto dot_tag) {
     constexpr int NV = decltype(nv_tag)::value;
     constexpr bool UP = decltype(up_tag)::value;
@@ -417,16 +418,17 @@ static void launch_cgs(const GmresWork& W, const TB* V, int nv, bool update, boo
   const double ne = (double)W.ns * W.B;
   const double bytes = (double)sizeof(TB) * ne * (nv + 1 + (update ? 1 : 0));
   const double flops = ne * (2.0 * nv * ((update ? 1 : 0) + (dots ? 1 : 0)) + 2.0);
-  if (sel_w2)  // selective pass: whether it streamed is decided on the device, so no bytes are booked
-    after_launch("cgs_reorth_selective", st, 0.0, 0.0, 0);
+  // (selective pass: whether it streamed is decided on the device, so no bytes are booked)
+  if (sel_w2)
+    after_launch(cls, st, 0.0, 0.0, 0);
   else
-    after_launch(update ? (dots ? "cgs_update_dots" : "cgs_update") : "cgs_dots", st, flops, bytes, 0);
+    after_launch(cls, st, flops, bytes, 0);
 }
 
 template <typename T, typename TO>
 static void launch_norm(const GmresWork& W, const T* x, TO* xo, double* out, cudaStream_t st) {
   RedArgs ra{W.partials, W.counters, out, 1, W.nblk};
-  prof_begin(st);
+  prof_begin(st, "norm");
   norm_kernel<T, TO><<<dim3(W.nblk, W.B), kThreads, 0, st>>>(x, xo, W.ns, ra);
   const double ne = (double)W.ns * W.B;
   after_launch("norm", st, 2.0 * ne, ne * (sizeof(T) + (xo ? sizeof(TO) : 0.0)), 0);
@@ -546,7 +548,7 @@ extern "C" rte_status gmres_solve(const rte_problem* p, const mgnet_net* net, co
       else
         launch_norm<double, float>(W, W.r64, W.V, W.rn2, st);
       int stop_all = (total_all >= opts->maxit) ? 1 : 0;
-      prof_begin(st);
+      prof_begin(st, "cycle_init");
       cycle_init_kernel<<<(B + 63) / 64, 64, 0, st>>>(B, W.rn2, W.bnorm, opts->rtol, stop_all, W.alpha, m + 1, W.g,
                                                       m + 1, W.active, W.kcols, W.done, W.st_dev);
       after_launch("cycle_init", st);
@@ -588,7 +590,7 @@ extern "C" rte_status gmres_solve(const rte_problem* p, const mgnet_net* net, co
           // fp64 basis: z = P(alpha_j V_j) with the fp64 V-cycle, w = A z in fp64 (W.r64 is free
           // inside a cycle and holds P z)
           const double* vj = W.V64 + (size_t)j * n;
-          prof_begin(st);
+          prof_begin(st, "scale_f64");
           scale_f64_kernel<<<dim3(W.nblk, B), kThreads, 0, st>>>(vj, W.alpha + j, m + 1, W.z64, nullptr, W.ns,
                                                                   W.nblk);
           after_launch("scale_f64", st, 0.0, 16.0 * (double)n, 0);
@@ -612,7 +614,7 @@ extern "C" rte_status gmres_solve(const rte_problem* p, const mgnet_net* net, co
         }
         ++total_all;
         int last = (total_all >= opts->maxit) ? 1 : 0;
-        prof_begin(st);
+        prof_begin(st, "givens");
         givens_kernel<<<(B + 63) / 64, 64, 0, st>>>(B, j, m, W.h1, h2, hld, nrm, hld, reorth == 2 ? 1 : 0, W.Hr, W.Hraw,
                                                     first_cycle ? 1 : 0, W.cs, W.sn, W.g, W.alpha, m + 1, W.bnorm,
                                                     opts->rtol, last, W.active, W.kcols, W.st_dev);
@@ -640,11 +642,11 @@ extern "C" rte_status gmres_solve(const rte_problem* p, const mgnet_net* net, co
       }
       first_cycle = false;
       // x += P(V y)
-      prof_begin(st);
+      prof_begin(st, "backsolve");
       backsolve_kernel<<<(B + 63) / 64, 64, 0, st>>>(B, m, W.Hr, W.g, W.alpha, m + 1, W.kcols, W.coef, m + 1);
       after_launch("backsolve", st);
       if (f64) {
-        prof_begin(st);
+        prof_begin(st, "combine");
         combine_kernel<double, double><<<dim3(W.nblk, B), kThreads, 0, st>>>(W.V64, n, W.coef, m + 1, W.kcols, W.z64,
                                                                               W.ns, W.nblk);
         after_launch("combine", st, 2.0 * m * (double)n, 8.0 * (double)n * (m + 1), 0);
@@ -653,11 +655,11 @@ extern "C" rte_status gmres_solve(const rte_problem* p, const mgnet_net* net, co
           vcycle_run_f64(net, W.z64, W.r64, true, st);
           corr = W.r64;
         }
-        prof_begin(st);
+        prof_begin(st, "axpy64");
         axpy64_kernel<double><<<dim3(W.nblk, B), kThreads, 0, st>>>(x_dev, corr, nullptr, W.kcols, W.ns, W.nblk);
         after_launch("axpy64", st, (double)n, 28.0 * (double)n, 0);
       } else {
-        prof_begin(st);
+        prof_begin(st, "combine");
         combine_kernel<float, float><<<dim3(W.nblk, B), kThreads, 0, st>>>(W.V, n, W.coef, m + 1, W.kcols, W.w, W.ns,
                                                                             W.nblk);
         after_launch("combine", st, 2.0 * m * (double)n, 4.0 * (double)n * (m + 1), 0);
@@ -666,7 +668,7 @@ extern "C" rte_status gmres_solve(const rte_problem* p, const mgnet_net* net, co
           vcycle_run(net, W.w, W.z, true, nullptr, 0, st);
           corr = W.z;
         }
-        prof_begin(st);
+        prof_begin(st, "axpy64");
         axpy64_kernel<float><<<dim3(W.nblk, B), kThreads, 0, st>>>(x_dev, corr, nullptr, W.kcols, W.ns, W.nblk);
         after_launch("axpy64", st, (double)n, 20.0 * (double)n, 0);
       }

@@ -195,7 +195,7 @@ void launch_conv_t(const ConvDesc& d, const T* in, const T* Wk, T* out, const T*
   if constexpr (std::is_same<T, float>::value) {
     if (conv_tc_try(d, in, out, addend, sign, alpha, alpha_stride, alpha_on_input, alpha_on_addend, st)) return;
   }
-  prof_begin(st);
+  prof_begin(st, conv_class_name(d, false));
   auto go = [&](auto mode_tag, auto ks_tag, auto tco_tag) {
     constexpr int MODE = decltype(mode_tag)::value;
     constexpr int KS = decltype(ks_tag)::value;

@@ -11,6 +11,8 @@
 #include <vector>
 
 #include "common.h"
+
+#include <cstring>
 #include "mgnet.h"
 
 namespace rte {
@@ -78,8 +80,11 @@ void prof_resolve() {
 }
 }  // namespace
 
-void prof_begin(cudaStream_t st) {
+static std::string g_prof_filter;  // rte_timing_filter: the one class to time ("" = every class)
+
+void prof_begin(cudaStream_t st, const char* cls) {
   if (!g_prof_on) return;
+  if (!g_prof_filter.empty() && (!cls || g_prof_filter != cls)) return;
   if (!g_prof_pending) g_prof_pending = prof_event();
   RTE_CHECK_CUDA(cudaEventRecord(g_prof_pending, st));
 }
@@ -223,6 +228,12 @@ rte_status rte_debug_counters(uint64_t* out, int n, int reset) {
   RTE_API_BEGIN
   RTE_REQUIRE(out && n > 0, "rte_debug_counters: bad argument");
   tc_debug_counters(reinterpret_cast<unsigned long long*>(out), n, reset != 0);
+  RTE_API_END
+}
+
+rte_status rte_timing_filter(const char* prefix) {
+  RTE_API_BEGIN
+  g_prof_filter = prefix ? prefix : "";
   RTE_API_END
 }
 
