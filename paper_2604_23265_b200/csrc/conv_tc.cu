@@ -297,6 +297,39 @@ __global__ void splitk_reduce_kernel(const float4* __restrict__ part, long long 
 // ---- planning --------------------------------------------------------------------------------
 namespace {
 
+// Co-resident clusters of `cs` CTAs for the GEMM's footprint (448 threads, the largest shared
+// plan: one CTA per SM); cached per cluster size.  GPC boundaries make this smaller than
+// SMs / cs for large clusters, which the split-K cost model must see.
+int max_active_clusters(int cs) {
+  static int cache[9] = {0};
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  if (cs < 1 || cs > 8) return 0;
+  if (cache[cs] == 0) {
+    auto kern = tc::gemm3xtf32_kernel<128, 1, false, tc::EpiConv>;
+    constexpr int smem = tc::gemm_smem_bytes<128, 1, false>();
+    tc::ensure_smem((const void*)kern, smem);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(cs * 64), 1, 1);
+    cfg.blockDim = dim3(tc::kGemmThreads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) {
+      (void)cudaGetLastError();
+      n = -1;  // cluster launch unavailable: never plan it
+    }
+    cache[cs] = n;
+  }
+  return cache[cs];
+}
+
 struct Plan {
   bool ok = false;
   bool halo = false;  // stride-1 3x3: one halo tile per channel chunk feeds all 9 taps
@@ -379,15 +412,29 @@ Plan make_plan(const ConvDesc& d) {
                                   : std::max(12.0 * BN / 2.0, 700.0)) / 1.9e3;    // us per K block
   const double t_unit = 0.5;
   const double out_us = 4.0 * (double)P.out_elems / 6.0e6;
+  // Cluster split-K (opt-in, RTE_TC_CLUSTER=1): the <= 8 splits of a tile run as one thread-block
+  // cluster and reduce through distributed shared memory (no global partials, no reduction
+  // launch; one unit per CTA, grid = units).  Measured on the MgNet coarse levels: about equal to
+  // global partials + the reduction kernel, whose launches it removes but whose full-GPU
+  // parallelism it loses (the finishing rows of a tile are 1/nsplit of the cluster's threads)
+  static const bool cluster_ok = getenv("RTE_TC_CLUSTER") != nullptr;
   double best = 1e300;
   int best_kps = g.kb_total;
   const int quantum = P.halo ? 9 : 1;  // halo kernels split K in whole channel chunks (9 taps)
-  for (int ns = 1; ns <= std::max(1, std::min(64, g.kb_total / (2 * quantum))); ++ns) {
+  const int ns_max = cluster_ok ? 8 : 64;
+  for (int ns = 1; ns <= std::max(1, std::min(ns_max, g.kb_total / (2 * quantum))); ++ns) {
     const int kps = ((g.kb_total + ns - 1) / ns + quantum - 1) / quantum * quantum;
     const int nsr = (g.kb_total + kps - 1) / kps;
     const long long units = (long long)P.mtiles * P.ntiles * nsr;
-    const double waves = (double)((units + sms - 1) / sms);
-    const double t = waves * (kps * t_kb + t_unit) + (nsr > 1 ? (nsr + 2) * out_us + 3.0 : 0.0);
+    double waves = (double)((units + sms - 1) / sms);
+    if (cluster_ok && nsr > 1) {  // clusters of nsr CTAs: co-residency is per GPC, not per SM
+      const int mc = max_active_clusters(nsr);
+      if (mc <= 0) continue;
+      const long long tiles = (long long)P.mtiles * P.ntiles;
+      waves = (double)((tiles + mc - 1) / mc);
+    }
+    const double red = nsr == 1 ? 0.0 : cluster_ok ? 1.0 : (nsr + 2) * out_us + 3.0;
+    const double t = waves * (kps * t_kb + t_unit) + red;
     if (t < best * 0.97) {
       best = t;
       best_kps = kps;
@@ -395,6 +442,12 @@ Plan make_plan(const ConvDesc& d) {
   }
   g.kb_per_split = best_kps;
   g.nsplit = (g.kb_total + best_kps - 1) / best_kps;
+  g.cl = (cluster_ok && g.nsplit > 1) ? g.nsplit : 0;
+  static const bool planlog = getenv("RTE_TC_PLANLOG") != nullptr;  // (experiments)
+  if (planlog)
+    fprintf(stderr, "conv plan %s: BN=%d am=%d tiles=%dx%d kb=%d nsplit=%d cl=%d maxclusters(cl)=%d\n",
+            conv_class_name(d, true), BN, P.am, P.mtiles, P.ntiles, g.kb_total, g.nsplit, g.cl,
+            g.cl ? max_active_clusters(g.cl) : 0);
   P.ok = true;
   return P;
 }
@@ -406,6 +459,23 @@ void launch_bn(const Plan& P, const CUtensorMap& ta, const CUtensorMap& tbh, con
   constexpr int smem = tc::gemm_smem_bytes<BN, AM, ASPLIT>();
   tc::ensure_smem((const void*)kern, smem);
   const long long units = (long long)P.mtiles * P.ntiles * P.g.nsplit;
+  if (P.g.cl) {
+    // one unit per CTA, the nsplit CTAs of a tile form a cluster (consecutive blockIdx.x)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)units, 1, 1);
+    cfg.blockDim = dim3(tc::kGemmThreads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)P.g.cl;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    RTE_CHECK_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tbh, tbl, te, P.g, epi));
+    return;
+  }
   const int grid = (int)std::min<long long>(units, num_sms());
   kern<<<grid, tc::kGemmThreads, smem, st>>>(ta, tbh, tbl, te, P.g, epi);
 }
@@ -448,7 +518,7 @@ bool conv_tc_try(const ConvDesc& d, const float* in, float* out, const float* ad
   epi.out_split = d.out_split ? 1 : 0;
   epi.part = nullptr;
   epi.part_stride = P.out_elems;
-  if (g.nsplit > 1) {
+  if (g.nsplit > 1 && !g.cl) {
     if ((long long)g.nsplit * P.out_elems > (long long)d.ws_owner->tc_ws_elems) {
       set_error("conv_tc: split-K workspace too small (internal planning mismatch)");
       throw Fail{RTE_EINTERNAL};
@@ -473,7 +543,7 @@ bool conv_tc_try(const ConvDesc& d, const float* in, float* out, const float* ad
     case 64: dispatch(std::integral_constant<int, 64>{}); break;
     default: dispatch(std::integral_constant<int, 128>{}); break;
   }
-  const bool split = g.nsplit > 1;
+  const bool split = g.nsplit > 1 && !g.cl;  // (cluster split-K reduces inside the kernel)
   after_launch(conv_class_name(d, true), st, conv_flops(d), split ? 0.0 : conv_bytes(d, addend != nullptr), 1);
   if (split) {
     prof_begin(st, "splitk_reduce");
@@ -548,7 +618,7 @@ void conv_tc_prepare(mgnet_net* net) {
     d.Ho = d.Wo = Ho;
     d.Co = Co;
     Plan P = make_plan(d);
-    if (P.ok && P.g.nsplit > 1) need = std::max(need, (size_t)P.g.nsplit * (size_t)P.out_elems);
+    if (P.ok && P.g.nsplit > 1 && !P.g.cl) need = std::max(need, (size_t)P.g.nsplit * (size_t)P.out_elems);
   };
   consider(0, 1, net->N, net->M, net->N, net->C0);
   consider(0, 1, net->N, net->C0, net->N, net->M);

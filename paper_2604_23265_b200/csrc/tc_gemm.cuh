@@ -65,6 +65,9 @@ struct Geom {
                     // output-shaped tile (conv addend; epf_planes planes), 2 the tile's rows
                     // oy0 - 1 .. oy0 + TH (apply: the cell and its upwind neighbours)
   int epf_planes;
+  int cl;           // cluster split-K: 0 off; else = nsplit, the K splits of one output tile run
+                    // as one thread-block cluster (one unit per CTA) and are reduced through
+                    // distributed shared memory (no global partials, no reduction launch)
   int dbg;          // perf-experiment switches (RTE_TC_DBG; 0 in production): bit0 converters skip
                     // the row load/split/TMEM store, bit3 no MMAs, bit4 no TMA loads, bit5 no
                     // epilogue global traffic, bit6 role timers
@@ -162,10 +165,15 @@ struct Unit {
 
 __device__ __forceinline__ Unit decode_unit(const Geom& g, int u) {
   Unit w;
+  int split = 0;
+  if (g.cl) {  // cluster split-K: the splits of a tile are consecutive CTAs (the cluster)
+    split = u % g.cl;
+    u /= g.cl;
+  }
   const int nt = u % g.ntiles;
   u /= g.ntiles;
   const int mt = u % g.mtiles;
-  w.split = u / g.mtiles;
+  w.split = g.cl ? split : u / g.mtiles;
   w.tc = decode_tile(g, mt);
   w.n0 = nt * g.bn;
   w.kb0 = w.split * g.kb_per_split;
@@ -718,7 +726,40 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       named_bar_sync(2 + half, 128);
       const long long ts1 = prof ? clock64() : 0;
       if (prof) w_s1 += ts1 - ts0;
-      if (!(g.dbg & 32)) {
+      if (!Epi::kCenter && g.cl) {
+        // ---- cluster split-K: every CTA of the cluster staged its fp32 partial of the same
+        // tile; CTA `rank` finishes rows [rank R, rank R + R) by summing the partials in rank
+        // order (deterministic) straight out of the peers' shared memory, then the epilogue
+        cluster_sync_all();  // phase 1: all partials staged
+        const int ns = g.cl;
+        const int R = (kTileM + ns - 1) / ns;
+        const int rank = (int)cluster_ctarank();
+        const int ptid = threadIdx.x - 192;  // 0..255 over the promoter warps
+        constexpr int C4 = BN / 4;
+        uint32_t peer[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) peer[q] = q < ns ? mapa_shared(stage_s, (uint32_t)q) : 0u;
+        for (int item = ptid; item < R * C4; item += 256) {
+          const int rr = rank * R + item / C4, c = 4 * (item % C4);
+          if (rr >= rows || rr >= kTileM) continue;
+          const int ly = rr / g.pitch, lx = rr - ly * g.pitch;
+          const int oy = e_oy0 + ly, ox = e_ox0 + lx;
+          if (lx >= g.TW || oy >= g.Hc || ox >= g.Wc) continue;
+          const int h = c / HB, ch = c - h * HB, kq = (ch & 31) >> 2;
+          const uint32_t off = (uint32_t)((h * NCH + (ch >> 5)) * kStageBytes + rr * 128 + ((kq ^ (rr & 7)) << 4));
+          float4 v = ld_dsmem128(peer[0] + off);
+          for (int q = 1; q < ns; ++q) {  // rank order: deterministic
+            const float4 t = ld_dsmem128(peer[q] + off);
+            v.x += t.x;
+            v.y += t.y;
+            v.z += t.z;
+            v.w += t.w;
+          }
+          const typename Epi::Col cv = epi.col(w.n0 + c);
+          const typename Epi::Row rw = epi.row(et, epi.rel(ly, lx), oy, ox, 0.f);
+          epi.store4(rw, cv, v, epi.load(rw, cv));
+        }
+      } else if (!(g.dbg & 32)) {
         // rows are finished in batches: every global input of a batch (epi.row + epi.load) is
         // requested before any output of it is stored, so the batch costs one memory round trip
         // (out may alias the epilogue inputs elementwise only, which this order preserves)
@@ -777,6 +818,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       if constexpr (Epi::kCenter) mbar_arrive(&cempty[li & 1]);
       if (prof) w_e += clock64() - te0;
     }
+  }
+  if (g.cl) {
+    if (warp < 6) cluster_sync_all();  // phase 1 (the promoters passed it inside the epilogue)
+    cluster_sync_all();                // phase 2: no CTA leaves while peers read its partial
   }
   if (prof && (warp <= 2 || warp == 6)) {
     const unsigned long long tot = (unsigned long long)(clock64() - t_start);
