@@ -188,11 +188,131 @@ const char* conv_class_name(const ConvDesc& d, bool tc) {
   return names.insert(key).first->c_str();
 }
 
+// 1x1 conv with a short reduction (Ci <= 32, Co % 256 == 0, plain fp32 activations): the MgNet tail
+// lift C0 -> M ordinates (PAPER.md's channel lift back to the unknowns).  HBM-bound -- it streams
+// the M-wide output and addend -- so it runs on the fp32 FMA pipes, not the tensor cores (whose
+// conversion + epilogue dominated at K = 32).  Block = 64 pixels x 256 output channels (512
+// threads), weights [ci][co] and the pixels' inputs [ci][pixel] in shared memory; thread = 4 pixels
+// x 8 consecutive channels (32 FMAs per 3 LDS.128); each warp covers whole 1 KB output rows; the
+// tile's addend rows are bulk-prefetched into L2 at the block start.
+// out = (addend ? s_add addend : 0) + sign s_in (W in)  (same epilogue as conv_simt_kernel)
+constexpr int kSmallKMaxCi = 32;  // (static shared memory: 32 KB weights + 8 KB inputs)
+// (out and addend may be the same array: every element is read, then written, by one thread in
+// one iteration, so __restrict__ only lets the compiler batch the loads of different pixels)
+__global__ void __launch_bounds__(512, 2) conv1x1_smallk_kernel(int npix, int Ci, int Co, const float* __restrict__ in,
+                                                             const float* __restrict__ Wk, float* __restrict__ out,
+                                                             const float* __restrict__ addend, float sign,
+                                                             const double* __restrict__ alpha, int alpha_stride,
+                                                             int alpha_on_input, int alpha_on_addend) {
+  constexpr int TPX = 64, TCO = 256;
+  __shared__ __align__(128) float Ws[kSmallKMaxCi][TCO];  // [ci][co]
+  __shared__ __align__(128) float Us[TPX][kSmallKMaxCi];  // [pixel][ci] at pitch Ci (the input's layout)
+  __shared__ __align__(8) uint64_t bar;
+  const int tid = threadIdx.x, tx = tid % 32, ty = tid / 32;  // 8 channels x 4 pixels per thread
+  const int b = blockIdx.z;
+  const int co0 = blockIdx.y * TCO;
+  const int64_t p0 = (int64_t)blockIdx.x * TPX;
+  const int np = (int)std::min<int64_t>(TPX, npix - p0);
+  if (tid == 0) {
+    if (addend && Co == TCO) {
+      // the tile's addend rows (contiguous: 64 pixels x 1 KB) start streaming into L2 now
+      const float* src = addend + ((int64_t)b * npix + p0) * Co;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"((uint32_t)(np * Co * 4)) : "memory");
+    }
+    // weights (contiguous when Co == 256) and the tile's inputs: two bulk async copies
+    const uint32_t wbytes = (uint32_t)(Ci * TCO * 4), ubytes = (uint32_t)(np * Ci * 4);
+    const uint32_t sb = (uint32_t)__cvta_generic_to_shared(&bar);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sb) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sb), "r"(wbytes + ubytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(&Ws[0][0])),
+                 "l"(Wk + co0), "r"(wbytes), "r"(sb)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(&Us[0][0])),
+                 "l"(in + ((int64_t)b * npix + p0) * Ci), "r"(ubytes), "r"(sb)
+                 : "memory");
+  }
+  __syncthreads();  // (barrier initialised)
+  {
+    const uint32_t sb = (uint32_t)__cvta_generic_to_shared(&bar);
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tW_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t"
+        "@!p bra W_%=;\n\t}" ::"r"(sb)
+        : "memory");
+  }
+  float acc[4][8];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc[a][c] = 0.f;
+  for (int k = 0; k < Ci; ++k) {
+    const float4 w0 = *reinterpret_cast<const float4*>(&Ws[k][tx * 8]);
+    const float4 w1 = *reinterpret_cast<const float4*>(&Ws[k][tx * 8 + 4]);
+    const float* uc = &Us[0][0] + ty * 4 * Ci + k;  // [pixel][ci] at pitch Ci (as copied)
+    const float uv[4] = {uc[0], uc[Ci], uc[2 * Ci], uc[3 * Ci]};
+    const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc[a][c] = fmaf(uv[a], wv[c], acc[a][c]);
+  }
+  const float al = alpha ? (float)alpha[(int64_t)b * alpha_stride] : 1.f;
+  const float s_in = (alpha_on_input ? al : 1.f) * sign;
+  const float s_add = alpha_on_addend ? al : 1.f;
+  // the addend loads of two pixels are issued before their stores
+#pragma unroll
+  for (int a0 = 0; a0 < 4; a0 += 2) {
+    float4 ad[2][2];
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+      const int64_t p = p0 + ty * 4 + a0 + a;
+      const int64_t o = ((int64_t)b * npix + p) * Co + co0 + tx * 8;
+      ad[a][0] = ad[a][1] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (addend && p < npix) {
+        ad[a][0] = *reinterpret_cast<const float4*>(addend + o);
+        ad[a][1] = *reinterpret_cast<const float4*>(addend + o + 4);
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+      const int64_t p = p0 + ty * 4 + a0 + a;
+      if (p >= npix) continue;
+      const int64_t o = ((int64_t)b * npix + p) * Co + co0 + tx * 8;
+      const float* r = acc[a0 + a];
+      const float4 r0 = make_float4(fmaf(s_add, ad[a][0].x, s_in * r[0]), fmaf(s_add, ad[a][0].y, s_in * r[1]),
+                                    fmaf(s_add, ad[a][0].z, s_in * r[2]), fmaf(s_add, ad[a][0].w, s_in * r[3]));
+      const float4 r1 = make_float4(fmaf(s_add, ad[a][1].x, s_in * r[4]), fmaf(s_add, ad[a][1].y, s_in * r[5]),
+                                    fmaf(s_add, ad[a][1].z, s_in * r[6]), fmaf(s_add, ad[a][1].w, s_in * r[7]));
+      *reinterpret_cast<float4*>(out + o) = r0;
+      *reinterpret_cast<float4*>(out + o + 4) = r1;
+    }
+  }
+}
+
+bool conv1x1_smallk_ok(const ConvDesc& d) {
+  // (Co == 256: the weight block [ci][co0 .. co0+255] is contiguous for the bulk copy)
+  return d.mode == 0 && d.ks == 1 && d.Ci <= kSmallKMaxCi && d.Ci % 4 == 0 && d.Co == 256 && !d.in_split &&
+         !d.out_split && getenv("RTE_NO_SMALLK") == nullptr;
+}
+
 template <typename T>
 void launch_conv_t(const ConvDesc& d, const T* in, const T* Wk, T* out, const T* addend, float sign,
                    const double* alpha, int alpha_stride, bool alpha_on_input, bool alpha_on_addend,
                    cudaStream_t st) {
   if constexpr (std::is_same<T, float>::value) {
+    if (conv1x1_smallk_ok(d)) {
+      prof_begin(st, conv_class_name(d, false));
+      const int npix = d.Ho * d.Wo;
+      const unsigned bx = (unsigned)((npix + 63) / 64);
+      conv1x1_smallk_kernel<<<dim3(bx, (unsigned)(d.Co / 256), (unsigned)d.B), 512, 0, st>>>(
+          npix, d.Ci, d.Co, in, Wk, out, addend, sign, alpha, alpha_stride, alpha_on_input ? 1 : 0,
+          alpha_on_addend ? 1 : 0);
+      after_launch(conv_class_name(d, false), st, conv_flops(d), conv_bytes(d, addend != nullptr), 2);
+      return;
+    }
     if (conv_tc_try(d, in, out, addend, sign, alpha, alpha_stride, alpha_on_input, alpha_on_addend, st)) return;
   }
   prof_begin(st, conv_class_name(d, false));

@@ -125,6 +125,9 @@ VSMALL = [
     W.small_config(2, N=24, M=8, n_polar=1, n_azim=8, L=3, C0=8, B=2),
     W.small_config(3, N=16, M=16, n_polar=2, n_azim=8, L=1, C0=16),
     W.small_config(5, N=32, M=32, n_polar=2, n_azim=16, L=4, C0=32),
+    # M = 256: the 32 -> 256 lift runs on the small-K SIMT kernel (mgnet.cu); 22^2 = 484 pixels is
+    # a ragged multiple of its 64-pixel tile
+    W.small_config(5, N=22, M=256, n_polar=4, n_azim=64, L=2, C0=32),
 ]
 
 
