@@ -222,7 +222,7 @@ def run_reference(args, cfg):
     A = lambda v: O.apply(op, v)
     Pc = lambda v: O.vcycle(onet, v)
     # warm-up: W Arnoldi steps on a small copy of the workload (loads BLAS, touches code paths)
-    small = W.small_config(cfg.k, N=min(cfg.N, 32), M=min(cfg.M, 16), L=min(cfg.L, 3))
+    small = W.small_config(cfg.k, N=min(cfg.N, 32), M=16, n_polar=2, n_azim=8, L=min(cfg.L, 3))
     sm = W.make_media(small)
     sop = O.setup_from_media(small, sm)
     snet = O.make_mgnet(W.make_weights(small), small.M, small.L, small.C0, small.nu)
