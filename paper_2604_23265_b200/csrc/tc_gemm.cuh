@@ -86,6 +86,9 @@ constexpr int stage_chunks() {
 // A modes: 0 = per-K-block window tiles (TS), 1 = halo tiles, 9 taps per tile (TS), 2 = SS halo:
 // the halo tile is split once in shared memory and each tap's A operand is a row-shifted SW128
 // descriptor into it (see the kernel comment).
+#ifndef RTE_NA128
+#define RTE_NA128 4  // A ring depth of N = 128 window kernels (measured: 3 -> 4 is 4% on the apply, 5 no better)
+#endif
 template <int BN, int AM, bool ASPLIT = false>
 struct Plan {
   static constexpr int kBBytes = BN * 128;                          // one of B hi / B lo
@@ -95,7 +98,7 @@ struct Plan {
   static constexpr int kBudget = (222 - 32 * stage_chunks<BN>()) * 1024;  // rings (+ staging = 222 KB)
   // A ring depth: halo tiles are reused for 9 K blocks; window tiles are one K block each, so
   // they need a deeper ring to cover the HBM latency (BN = 32 leaves room for 8)
-  static constexpr int kNA = (AM != 0 || ASPLIT) ? 2 : BN == 32 ? 8 : BN == 64 ? 4 : 3;
+  static constexpr int kNA = (AM != 0 || ASPLIT) ? 2 : BN == 32 ? 8 : BN == 64 ? 4 : RTE_NA128;
   static constexpr int kNBraw = (kBudget - kNA * kASlot) / kBSlot;
   static constexpr int kNB = kNBraw > 8 ? 8 : kNBraw;               // B ring depth
   static constexpr int kRingBytes = kNA * kASlot + kNB * kBSlot;
