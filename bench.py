@@ -13,6 +13,8 @@ reported time is the max over ranks.  Config-5 vectors are 256 MiB (> 126 MB L2)
 streams its inputs from HBM ("inputs larger than L2").  Multi-GPU: config 5 is ONE medium and does
 not shard without a halo exchange, so N ranks run N independent replicas (DESIGN.md §8,
 "replicas only"); value = total iterations of all ranks / max-over-ranks time ("scaling": "weak").
+Batched configs (config 4) shard their independent samples across ranks, no data-path collective:
+value = K iterations of the whole batch / max-over-ranks time ("scaling": "strong").
 
 Rank 0 prints ONE JSON line.  --impl reference times the fp64 CPU oracle (oracle/, the
 reference arm of this tier) on the host cores for the same metric and config.
@@ -261,8 +263,16 @@ def run_ours(args, cfg):
     stream = torch.cuda.current_stream(dev)
     media = W.make_media(cfg)
     weights = W.make_weights(cfg)
-    p = P.rte_setup(cfg.N, media.sigma_T, media.sigma_a, media.q, media.eps, media.g, media.inflow,
-                    n_polar=cfg.n_polar, n_azim=cfg.n_azim)
+    # batched configs (config 4: independent samples, independent solves) shard the samples across
+    # ranks with no data-path collective: total work fixed, "scaling": "strong".
+    # B = 1 configs run one replica per rank ("weak").
+    sharded = cfg.B > 1 and ws > 1
+    lo, hi = benchlib.shard(cfg.B, rank, ws) if sharded else (0, cfg.B)
+    if sharded and hi == lo:
+        raise SystemExit(f"rank {rank}: no sample to solve (world size {ws} > batch {cfg.B})")
+    sl = slice(lo, hi)
+    p = P.rte_setup(cfg.N, media.sigma_T[sl], media.sigma_a[sl], media.q[sl], media.eps[sl], media.g[sl],
+                    media.inflow[sl], n_polar=cfg.n_polar, n_azim=cfg.n_azim)
     net = P.mgnet_create(p, cfg.L, cfg.C0, cfg.nu, weights)
     b = torch.empty(p.shape, dtype=torch.float32, device=dev)
     P.rte_rhs(p, b)
@@ -311,10 +321,11 @@ def run_ours(args, cfg):
     P.rte_timing_filter(None)
     P.rte_timing_enable(False)
     clocks = sampler.stop()
-    iters = rep[0]["iterations"] if cfg.B == 1 else sum(r["iterations"] for r in rep) / cfg.B
+    iters = sum(r["iterations"] for r in rep) / len(rep)
     assert iters == K, f"solve ran {iters} iterations, expected {K}"
     ms_max = benchlib.max_over_ranks(ms, dist, dev)
-    value = benchlib.aggregate(K, ws, ms_max)
+    # sharded: the job is K iterations of the whole batch; replicas: ws jobs of K iterations
+    value = benchlib.aggregate(K, 1 if sharded else ws, ms_max)
 
     # ---- e2e: same solve through the public API with HOST buffers -----------------------
     b_host = torch.empty(p.shape, dtype=torch.float32, pin_memory=True)
@@ -364,16 +375,18 @@ def run_ours(args, cfg):
                            "ms": round(c["ms"], 4), "share": round(c["ms"] / tot_ms, 4)} for c in all_classes),
                          key=lambda d: -d["ms"])
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": Wm,
-                "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "strong" if sharded else "weak",
+                "vs_baseline": None,
                 "dtype": "f32", "data": "synthetic",
                 "config": {"workload": _workload_name(cfg), "unknowns": cfg.unknowns,
                            "l2": "inputs larger than L2 (each vector 4 B x unknowns)" if cfg.unknowns * 4 > 126e6
                            else "working set L2-resident (small config)",
-                           "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
+                           "parallelism": (f"{cfg.B} samples sharded over {ws} ranks" if sharded
+                                           else f"replicas x{ws}" if ws > 1 else "single GPU"),
                            "precision": "fp32 storage/arithmetic, fp64 iterate, reductions and restart residual",
                            "gram_schmidt": {0: "CGS2", 1: "CGS1", 2: "selective (DGKS)"}[args.reorth]},
                 "roofline": roof,
-                "e2e": {"value": benchlib.aggregate(K, ws, ms_e2e), "unit": UNIT,
+                "e2e": {"value": benchlib.aggregate(K, 1 if sharded else ws, ms_e2e), "unit": UNIT,
                         "h2d_bytes_per_step": h2d / K, "d2h_bytes_per_step": d2h / K,
                         "note": f"one solve of K={K} iterations per measurement: b (fp32) copied H2D from pinned "
                                 "host memory before it and x (fp64) D2H after it; bytes amortised per step"},
