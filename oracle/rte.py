@@ -281,17 +281,23 @@ def make_mgnet(w, M, L, C0, nu) -> MgNet:
     return MgNet(unpack_weights(w, M, L, C0, nu), M, L, C0, nu)
 
 
-def vcycle(net: MgNet, r: np.ndarray, add_identity: bool = True) -> np.ndarray:
+def vcycle(net: MgNet, r: np.ndarray, add_identity: bool = True, mod: Optional[dict] = None) -> np.ndarray:
     """z = [r +] Theta u^0 after one MgNet V-cycle on f^0 = Lambda r (Q13-Q17).
 
-    Smoothing step (Q13, modulation a = abar = 1): u <- u + B * (f - A * u).
-    Down (l < L-1): nu pre-steps with B^{l,i}; f^{l+1} = R^l *_2 (f - A^l * u); u^{l+1} = 0 (Q16).
+    Smoothing step (Q13; "update the current solution based on the discrete operator
+    information a[l] and the solution operator information a^{-1}[l]"):
+        u <- u + abar^[l] (.) (B * (f - a^[l] (.) (A^l * u)))       ((.) = elementwise)
+    with a = mod["a"][l], abar = mod["abar"][l] from CoeffNet (R31-R33); mod=None means
+    a = abar = 1 (v1).  The restriction residual uses the same modulated operator.
+    Down (l < L-1): nu pre-steps with B^{l,i}; f^{l+1} = R^l *_2 (f - a (.) A^l * u); u^{l+1} = 0 (Q16).
     Coarsest: 2 nu steps, pre then post B (Q15).
     Up: u^l += P^l^T *_2 u^{l+1}; nu post-steps with B'^{l,i}.
     """
     W = net.W
     r = np.asarray(r, np.float64)
     L, nu = net.L, net.nu
+    a = (lambda l: mod["a"][l]) if mod is not None else (lambda l: 1.0)
+    ab = (lambda l: mod["abar"][l]) if mod is not None else (lambda l: 1.0)
     f = [None] * L
     u = [None] * L
     f[0] = conv1x1(r, W["Lambda"])
@@ -301,15 +307,56 @@ def vcycle(net: MgNet, r: np.ndarray, add_identity: bool = True) -> np.ndarray:
         if l == L - 1:
             steps += [W[f"Bpost{l}_{i}"] for i in range(nu)]
         for Bw in steps:
-            u[l] = u[l] + conv3x3(f[l] - conv3x3(u[l], W[f"A{l}"]), Bw)
+            u[l] = u[l] + ab(l) * conv3x3(f[l] - a(l) * conv3x3(u[l], W[f"A{l}"]), Bw)
         if l < L - 1:
-            f[l + 1] = conv3x3(f[l] - conv3x3(u[l], W[f"A{l}"]), W[f"R{l}"], stride=2)
+            f[l + 1] = conv3x3(f[l] - a(l) * conv3x3(u[l], W[f"A{l}"]), W[f"R{l}"], stride=2)
     for l in range(L - 2, -1, -1):
         u[l] = u[l] + conv_transpose4x4_s2(u[l + 1], W[f"P{l}"])
         for i in range(nu):
-            u[l] = u[l] + conv3x3(f[l] - conv3x3(u[l], W[f"A{l}"]), W[f"Bpost{l}_{i}"])
+            u[l] = u[l] + ab(l) * conv3x3(f[l] - a(l) * conv3x3(u[l], W[f"A{l}"]), W[f"Bpost{l}_{i}"])
     z = conv1x1(u[0], W["Theta"])
     return r + z if add_identity else z
+
+
+# ---------------------------------------------------------------------------
+# 3b. CoeffNet (§3.2; readings R31-R33 in DESIGN.md)
+# ---------------------------------------------------------------------------
+def coeffnet_weight_shapes(L: int, C0: int):
+    """Packed CoeffNet weight order (R33): per level l, the trunk conv K_l (C_l x C_in x 3 x 3,
+    C_in = 3 at l = 0 else C_{l-1}; stride 1 at l = 0, 2 after) and its bias beta_l (C_l), then
+    the two 1x1 heads G^a_l, g^a_l and G^abar_l, g^abar_l (C_l x C_l and C_l).  C_l = C0 2^l."""
+    shapes = []
+    for l in range(L):
+        C = C0 << l
+        Cin = 3 if l == 0 else (C0 << (l - 1))
+        shapes += [(f"K{l}", (C, Cin, 3, 3)), (f"beta{l}", (C,)), (f"Ga{l}", (C, C, 1, 1)), (f"ga{l}", (C,)),
+                   (f"Gb{l}", (C, C, 1, 1)), (f"gb{l}", (C,))]
+    return shapes
+
+
+def coeffnet(sigma_T, sigma_a, eps, w, L: int, C0: int) -> dict:
+    """CoeffNet forward: x = [sigma_T, sigma_a, eps] along channels (NHWC
+    [B][N][N][3]); trunk h^0 = ReLU(K_0 * x + beta_0), h^{l+1} = ReLU(K_{l+1} *_2 h^l + beta_{l+1})
+    (conv + batch normalisation folded into (K, beta) + activation, strided for the pyramid);
+    heads a^[l] = G^a_l h^l + g^a_l, abar^[l] = G^abar_l h^l + g^abar_l (1x1, linear), each
+    [B][N/2^l][N/2^l][C0 2^l].  Returns {"a": [...], "abar": [...]}."""
+    w = np.asarray(w, np.float64)
+    P, off = {}, 0
+    for name, shp in coeffnet_weight_shapes(L, C0):
+        n = int(np.prod(shp))
+        P[name] = w[off:off + n].reshape(shp)
+        off += n
+    if off != w.size:
+        raise ValueError(f"CoeffNet weight count mismatch: expected {off}, got {w.size}")
+    x = np.stack([np.asarray(sigma_T, np.float64), np.asarray(sigma_a, np.float64),
+                  np.asarray(eps, np.float64)], axis=-1)
+    out = {"a": [], "abar": []}
+    h = x
+    for l in range(L):
+        h = np.maximum(conv3x3(h, P[f"K{l}"], stride=1 if l == 0 else 2) + P[f"beta{l}"], 0.0)
+        out["a"].append(conv1x1(h, P[f"Ga{l}"]) + P[f"ga{l}"])
+        out["abar"].append(conv1x1(h, P[f"Gb{l}"]) + P[f"gb{l}"])
+    return out
 
 
 # ---------------------------------------------------------------------------

@@ -197,6 +197,43 @@ def make_weights(cfg: Config, std: float = 0.02, seed: Optional[int] = None) -> 
     return (rng.standard_normal(n) * std).astype(np.float32)
 
 
+def coeffnet_weight_layout(L: int, C0: int):
+    """(name, shape) of the packed CoeffNet weights in order (R33; layout only): per level
+    l, trunk conv K_l [C_l][C_in][3][3] (C_in = 3 at l = 0, else C_{l-1}), its bias [C_l], the
+    a-head [C_l][C_l] and bias [C_l], the abar-head [C_l][C_l] and bias [C_l]; C_l = C0 2^l."""
+    out = []
+    for l in range(L):
+        C = C0 << l
+        Cin = 3 if l == 0 else (C0 << (l - 1))
+        out += [(f"K{l}", (C, Cin, 3, 3)), (f"beta{l}", (C,)), (f"Ga{l}", (C, C)), (f"ga{l}", (C,)),
+                (f"Gb{l}", (C, C)), (f"gb{l}", (C,))]
+    return out
+
+
+def coeffnet_weight_count(L: int, C0: int) -> int:
+    return int(sum(math.prod(s) for _, s in coeffnet_weight_layout(L, C0)))
+
+
+def make_coeffnet_weights(cfg: Config, head_std: float = 0.02, seed: Optional[int] = None) -> np.ndarray:
+    """Packed float32 CoeffNet weights (seed 4000+k), drawn in fp64 and cast RN: trunk convs
+    N(0, 2/fan_in) (He), trunk biases 0, head weights N(0, head_std^2), head biases 1 -- a
+    near-identity modulation (the paper's trained weights are not released)."""
+    rng = np.random.Generator(np.random.PCG64(4000 + cfg.k if seed is None else seed))
+    parts = []
+    for name, shp in coeffnet_weight_layout(cfg.L, cfg.C0):
+        n = math.prod(shp)
+        if name.startswith("K"):
+            fan_in = shp[1] * 9
+            parts.append(rng.standard_normal(n) * math.sqrt(2.0 / fan_in))
+        elif name.startswith("beta"):
+            parts.append(np.zeros(n))
+        elif name.startswith("G"):
+            parts.append(rng.standard_normal(n) * head_std)
+        else:
+            parts.append(np.ones(n))
+    return np.concatenate(parts).astype(np.float32)
+
+
 def make_vector(cfg: Config, which: int = 0) -> np.ndarray:
     """Parity vector x ~ N(0,1) i.i.d. per unknown, float32 [B][N][N][M] (seed 3000+k)."""
     rng = np.random.Generator(np.random.PCG64([3000 + cfg.k, which]))
