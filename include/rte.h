@@ -132,6 +132,24 @@ rte_status mgnet_vcycle(const mgnet_net* net, const float* r_dev, float* z_dev,
 rte_status mgnet_vcycle_f64(const mgnet_net* net, const double* r_dev, double* z_dev, int add_identity,
                             void* stream);
 
+/* CoeffNet (NEXT-1; R31-R33): computes the modulation maps a^[l] and
+ * abar^[l] = a^{-1,[l]} of every level from the medium (sigma_T, sigma_a, eps: host float32
+ * [batch][N][N], the rte_setup arrays) and attaches them to `net`.  Every later V-cycle (fp32 and
+ * fp64, and gmres_solve through it) then smooths with u <- u + abar (.) (B * (f - a (.) (A * u))).
+ * Weights: host float32, packed per level l as trunk conv K_l [C_l][C_in][3][3] (C_in = 3 at l = 0,
+ * else C_{l-1}; stride 1 at l = 0, 2 after), bias [C_l], a-head [C_l][C_l], bias [C_l], abar-head
+ * [C_l][C_l], bias [C_l], C_l = c0 2^l; the trunk applies ReLU, the heads are linear (BatchNorm
+ * folded).  n_floats must equal mgnet_coeffnet_weight_count(levels, c0).  weights == NULL removes
+ * the maps (a = abar = 1).  Runs in fp64 at setup time and synchronises the device.  Must not run
+ * concurrently with a V-cycle of the same net.  Errors: RTE_EINVAL (NULL field, count mismatch),
+ * RTE_ENOMEM, RTE_ECUDA. */
+size_t mgnet_coeffnet_weight_count(int levels, int c0);
+rte_status mgnet_coeffnet(mgnet_net* net, const float* sigma_T, const float* sigma_a, const float* eps,
+                          const float* weights, size_t n_floats);
+/* Copies the fp64 map a^[level] (which = 0) or abar^[level] (which = 1), [batch][N_l][N_l][C_l]
+ * NHWC, to host_out.  Errors: RTE_EINVAL (bad level/which, or no maps attached). */
+rte_status mgnet_modulation(const mgnet_net* net, int level, int which, double* host_out);
+
 /* Restarted right-preconditioned GMRES(m) (R21, R22).
  * Preconditioner P = I + V (precond=1, requires net) or P = I (precond=0).
  * Iterate x is float64; the Krylov basis is float32 (precision=0) or float64 (precision=1); dot

@@ -16,7 +16,7 @@ from . import _lib
 from ._lib import RteError, check, gmres_opts, gmres_report, lib
 
 __all__ = ["Problem", "MgNet", "rte_setup", "rte_rhs", "rte_apply", "rte_apply_f64", "mgnet_create",
-           "mgnet_vcycle", "mgnet_vcycle_f64", "gmres_solve", "rte_quadrature", "rte_hg_matrix", "rte_launch_count", "rte_timing_enable", "rte_timing_filter", "rte_timing_reset",
+           "mgnet_vcycle", "mgnet_vcycle_f64", "mgnet_coeffnet", "mgnet_coeffnet_weight_count", "mgnet_modulation", "gmres_solve", "rte_quadrature", "rte_hg_matrix", "rte_launch_count", "rte_timing_enable", "rte_timing_filter", "rte_timing_reset",
            "rte_timing_get", "RteError", "LIB_PATH"]
 
 LIB_PATH = _lib.LIB_PATH
@@ -165,6 +165,30 @@ def mgnet_create(p: Problem, levels: int, c0: int, nu: int, weights) -> MgNet:
     h = C.c_void_p()
     check("mgnet_create", lib.mgnet_create(p.handle, levels, c0, nu, _fptr(w), w.size, C.byref(h)))
     return MgNet(h, p, levels, c0, nu)
+
+
+def mgnet_coeffnet_weight_count(levels: int, c0: int) -> int:
+    return int(lib.mgnet_coeffnet_weight_count(levels, c0))
+
+
+def mgnet_coeffnet(net: MgNet, sigma_T, sigma_a, eps, weights) -> None:
+    """CoeffNet (NEXT-1): compute the modulation maps of every level from the medium and attach them
+    to `net` (weights=None removes them).  sigma_T, sigma_a, eps: [batch][N][N] like rte_setup."""
+    if weights is None:
+        check("mgnet_coeffnet", lib.mgnet_coeffnet(net.handle, None, None, None, None, 0))
+        return
+    B, N = net.problem.shape[0], net.problem.shape[1]
+    f = [_f32(a).reshape(B, N, N) for a in (sigma_T, sigma_a, eps)]
+    w = _f32(weights).ravel()
+    check("mgnet_coeffnet", lib.mgnet_coeffnet(net.handle, _fptr(f[0]), _fptr(f[1]), _fptr(f[2]), _fptr(w), w.size))
+
+
+def mgnet_modulation(net: MgNet, level: int, which: int) -> np.ndarray:
+    """The fp64 map a^[level] (which=0) or abar^[level] (which=1), [batch][N_l][N_l][C_l]."""
+    B, N = net.problem.shape[0], net.problem.shape[1]
+    out = np.empty((B, N >> level, N >> level, net.c0 << level), np.float64)
+    check("mgnet_modulation", lib.mgnet_modulation(net.handle, level, which, _dptr(out)))
+    return out
 
 
 def mgnet_vcycle(net: MgNet, r, z, add_identity: bool = True, stream=None) -> None:

@@ -63,6 +63,9 @@ SIGS = {
     "mgnet_destroy": (None, [_vp]),
     "mgnet_vcycle": (C.c_int, [_vp, _vp, _vp, C.c_int, _vp]),
     "mgnet_vcycle_f64": (C.c_int, [_vp, _vp, _vp, C.c_int, _vp]),
+    "mgnet_coeffnet_weight_count": (C.c_size_t, [C.c_int, C.c_int]),
+    "mgnet_coeffnet": (C.c_int, [_vp, _fp, _fp, _fp, _fp, C.c_size_t]),
+    "mgnet_modulation": (C.c_int, [_vp, C.c_int, C.c_int, C.POINTER(C.c_double)]),
     "gmres_solve": (C.c_int, [_vp, _vp, _vp, _vp, C.POINTER(gmres_opts), C.POINTER(gmres_report), _vp]),
     "rte_launch_count": (C.c_int64, [C.c_int]),
     "rte_last_error": (C.c_char_p, []),

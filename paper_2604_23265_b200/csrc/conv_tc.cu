@@ -154,6 +154,7 @@ struct EpiConv {
   int alpha_stride, a_in, a_add;
   int mode, Ho, Wo, Co;
   int out_split;  // output and addend stored as hi/lo planes (ConvDesc::out_split)
+  const float* mod;  // CoeffNet modulation of the conv result (plain layout) or NULL
 
   __device__ __forceinline__ long long plane() const { return (long long)Ho * Wo * Co; }
   // offset of (pixel, col) in the output layout (plane 0 for split outputs)
@@ -185,6 +186,7 @@ struct EpiConv {
   };
   struct Pre {
     float4 a;  // addend (hi + lo planes summed when split)
+    float4 m;  // modulation (1 when none)
   };
   struct Tile {
     long long o0, po0;  // output / partial-sum offsets of the tile origin
@@ -203,7 +205,8 @@ struct EpiConv {
     return Row{t.o0 + rel, t.po0 + rel, t.si, t.sa};
   }
   __device__ __forceinline__ Pre load(const Row& rw, const Col& cv) const {
-    Pre p{make_float4(0.f, 0.f, 0.f, 0.f)};
+    Pre p{make_float4(0.f, 0.f, 0.f, 0.f), make_float4(1.f, 1.f, 1.f, 1.f)};
+    if (mod) p.m = *reinterpret_cast<const float4*>(mod + rw.po + cv.col);
     if (addend) {
       const long long o = rw.o + cv.col;
       p.a = *reinterpret_cast<const float4*>(addend + o);
@@ -219,7 +222,7 @@ struct EpiConv {
   }
   __device__ __forceinline__ void store4(const Row& rw, const Col& cv, float4 v, const Pre& p) const {
     const long long o = rw.o + cv.col;
-    float4 r = make_float4(rw.si * v.x, rw.si * v.y, rw.si * v.z, rw.si * v.w);
+    float4 r = make_float4(rw.si * (p.m.x * v.x), rw.si * (p.m.y * v.y), rw.si * (p.m.z * v.z), rw.si * (p.m.w * v.w));
     if (addend) {
       r.x = fmaf(rw.sa, p.a.x, r.x);
       r.y = fmaf(rw.sa, p.a.y, r.y);
@@ -248,7 +251,7 @@ struct EpiConv {
 __global__ void splitk_reduce_kernel(const float4* __restrict__ part, long long stride4, int nsplit, float4* out,
                                      const float4* addend, float sign, const double* __restrict__ alpha,
                                      int alpha_stride, int a_in, int a_add, long long n4, long long per_sample4,
-                                     int out_split) {
+                                     int out_split, const float4* __restrict__ mod) {
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n4; e += (long long)gridDim.x * blockDim.x) {
     float4 s = part[e];
     for (int k = 1; k < nsplit; ++k) {
@@ -257,6 +260,13 @@ __global__ void splitk_reduce_kernel(const float4* __restrict__ part, long long 
       s.y += p.y;
       s.z += p.z;
       s.w += p.w;
+    }
+    if (mod) {  // CoeffNet modulation of the conv result (plain layout, index e)
+      const float4 m = mod[e];
+      s.x *= m.x;
+      s.y *= m.y;
+      s.z *= m.z;
+      s.w *= m.w;
     }
     const int b = (int)(e / per_sample4);
     const float al = alpha ? (float)alpha[(long long)b * alpha_stride] : 1.f;
@@ -516,6 +526,7 @@ bool conv_tc_try(const ConvDesc& d, const float* in, float* out, const float* ad
   epi.Wo = d.Wo;
   epi.Co = d.Co;
   epi.out_split = d.out_split ? 1 : 0;
+  epi.mod = static_cast<const float*>(d.mod);
   epi.part = nullptr;
   epi.part_stride = P.out_elems;
   if (g.nsplit > 1 && !g.cl) {
@@ -554,7 +565,7 @@ bool conv_tc_try(const ConvDesc& d, const float* in, float* out, const float* ad
                                                      g.nsplit, reinterpret_cast<float4*>(out),
                                                      reinterpret_cast<const float4*>(addend), sign, alpha,
                                                      alpha_stride, epi.a_in, epi.a_add, n4, per4,
-                                                     d.out_split ? 1 : 0);
+                                                     d.out_split ? 1 : 0, reinterpret_cast<const float4*>(d.mod));
     // the conv's algorithmic bytes are booked on the reduction (it writes the output)
     after_launch("splitk_reduce", st, 0.0, conv_bytes(d, addend != nullptr) + 4.0 * g.nsplit * P.out_elems, 0);
   }

@@ -28,8 +28,9 @@ template <typename T, int MODE, int KS, int TCO, bool IN_SPLIT, bool OUT_SPLIT>
 __global__ void __launch_bounds__(256) conv_simt_kernel(
     int Hi, int Wi, int Ci, int Ho, int Wo, int Co, const T* __restrict__ in, const T* __restrict__ Wk,
     T* out, const T* addend, float sign, const double* __restrict__ alpha, int alpha_stride,
-    int alpha_on_input, int alpha_on_addend) {
+    int alpha_on_input, int alpha_on_addend, const T* __restrict__ mod) {
   // split formats (float only): value = hi plane + lo plane, planes Hi*Wi*Ci (in) / Ho*Wo*Co (out) apart
+  // mod: CoeffNet modulation of the conv result, plain [B][Ho][Wo][Co] (NULL = 1)
   const int64_t in_plane = IN_SPLIT ? (int64_t)Hi * Wi * Ci : 0;
   const int64_t out_plane = OUT_SPLIT ? (int64_t)Ho * Wo * Co : 0;
   constexpr int TP = 4096 / TCO;
@@ -142,7 +143,7 @@ __global__ void __launch_bounds__(256) conv_simt_kernel(
     for (int c = 0; c < 4; ++c) {
       int co = co0 + tx * 4 + c;
       if (co >= Co) continue;
-      T v = s_in * acc[a][c];
+      T v = s_in * (mod ? mod[((int64_t)b * Ho * Wo + opix) * Co + co] * acc[a][c] : acc[a][c]);
       if (addend) {
         T av = addend[base + co];
         if (OUT_SPLIT) av += addend[base + co + out_plane];
@@ -294,7 +295,7 @@ __global__ void __launch_bounds__(512, 2) conv1x1_smallk_kernel(int npix, int Ci
 
 bool conv1x1_smallk_ok(const ConvDesc& d) {
   // (Co == 256: the weight block [ci][co0 .. co0+255] is contiguous for the bulk copy)
-  return d.mode == 0 && d.ks == 1 && d.Ci <= kSmallKMaxCi && d.Ci % 4 == 0 && d.Co == 256 && !d.in_split &&
+  return d.mode == 0 && d.ks == 1 && d.Ci <= kSmallKMaxCi && d.Ci % 4 == 0 && d.Co == 256 && !d.in_split && !d.mod &&
          !d.out_split && getenv("RTE_NO_SMALLK") == nullptr;
 }
 
@@ -328,7 +329,7 @@ void launch_conv_t(const ConvDesc& d, const T* in, const T* Wk, T* out, const T*
       constexpr bool IS = decltype(ins)::value, OS = decltype(outs)::value;
       conv_simt_kernel<T, MODE, KS, TCO, IS, OS><<<grid, 256, 0, st>>>(
           d.Hi, d.Wi, d.Ci, d.Ho, d.Wo, d.Co, in, Wk, out, addend, sign, alpha, alpha_stride,
-          alpha_on_input ? 1 : 0, alpha_on_addend ? 1 : 0);
+          alpha_on_input ? 1 : 0, alpha_on_addend ? 1 : 0, static_cast<const T*>(d.mod));
     };
     using TT = std::true_type;
     using FF = std::false_type;
@@ -423,6 +424,10 @@ void mgnet_destroy(mgnet_net* net) {
     dfree(lv.f64);
     dfree(lv.u64);
     dfree(lv.t64);
+    dfree(lv.a32);
+    dfree(lv.ab32);
+    dfree(lv.a64);
+    dfree(lv.ab64);
   }
   delete net;
 }
@@ -502,6 +507,147 @@ rte_status mgnet_vcycle(const mgnet_net* net, const float* r_dev, float* z_dev, 
     RTE_REQUIRE(net && r_dev && z_dev, "mgnet_vcycle: NULL argument");
     RTE_REQUIRE((const void*)r_dev != (const void*)z_dev, "mgnet_vcycle: r and z must not alias");
     vcycle_run(net, r_dev, z_dev, add_identity != 0, nullptr, 0, as_stream(stream));
+    return RTE_OK;
+  } catch (const Fail& f) {
+    return f.st;
+  }
+}
+
+// ---- CoeffNet (NEXT-1, R31-R33) ---------------------------------------
+namespace rte {
+namespace {
+// Setup-time direct convolution in fp64 (once per medium): one thread per output element.
+// NHWC in [B][Hi][Wi][Ci], OIHW K [Co][Ci][ks][ks], zero padding ks/2, out = act(K * in + bias),
+// act = ReLU if relu; out32 (optional) receives the float copy.
+__global__ void coeffnet_conv_kernel(const double* __restrict__ in, int B, int Hi, int Wi, int Ci,
+                                     const double* __restrict__ K, const double* __restrict__ bias, int Co, int ks,
+                                     int stride, int relu, int Ho, int Wo, double* __restrict__ out,
+                                     float* __restrict__ out32) {
+  const int64_t n = (int64_t)B * Ho * Wo * Co;
+  const int pad = ks / 2;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int co = (int)(e % Co);
+    const int64_t pix = e / Co;
+    const int x = (int)(pix % Wo), y = (int)((pix / Wo) % Ho), b = (int)(pix / ((int64_t)Wo * Ho));
+    double acc = bias[co];
+    for (int ky = 0; ky < ks; ++ky) {
+      const int yi = stride * y + ky - pad;
+      if (yi < 0 || yi >= Hi) continue;
+      for (int kx = 0; kx < ks; ++kx) {
+        const int xi = stride * x + kx - pad;
+        if (xi < 0 || xi >= Wi) continue;
+        const double* ip = in + (((int64_t)b * Hi + yi) * Wi + xi) * Ci;
+        const double* kp = K + ((int64_t)co * Ci * ks + ky) * ks + kx;
+        for (int ci = 0; ci < Ci; ++ci) acc += kp[(int64_t)ci * ks * ks] * ip[ci];
+      }
+    }
+    if (relu && acc < 0.0) acc = 0.0;
+    out[e] = acc;
+    if (out32) out32[e] = (float)acc;
+  }
+}
+
+void free_modulation(mgnet_net* net) {
+  for (auto& lv : net->lv) {
+    dfree(lv.a32);
+    dfree(lv.ab32);
+    dfree(lv.a64);
+    dfree(lv.ab64);
+    lv.a32 = lv.ab32 = nullptr;
+    lv.a64 = lv.ab64 = nullptr;
+  }
+}
+}  // namespace
+}  // namespace rte
+
+size_t mgnet_coeffnet_weight_count(int levels, int c0) {
+  size_t n = 0;
+  for (int l = 0; l < levels; ++l) {
+    const size_t C = (size_t)c0 << l, Cin = l == 0 ? 3 : ((size_t)c0 << (l - 1));
+    n += C * Cin * 9 + C + 2 * (C * C + C);
+  }
+  return n;
+}
+
+rte_status mgnet_coeffnet(mgnet_net* net, const float* sigma_T, const float* sigma_a, const float* eps,
+                          const float* weights, size_t n_floats) {
+  try {
+    RTE_REQUIRE(net, "mgnet_coeffnet: NULL net");
+    free_modulation(net);
+    if (!weights) return RTE_OK;  // back to the unmodulated smoother (a = abar = 1)
+    RTE_REQUIRE(sigma_T && sigma_a && eps, "mgnet_coeffnet: NULL medium field");
+    const size_t need = mgnet_coeffnet_weight_count(net->L, net->C0);
+    RTE_REQUIRE(n_floats == need, "mgnet_coeffnet: weight count mismatch (expected " + std::to_string(need) +
+                                      ", got " + std::to_string(n_floats) + ")");
+    const int B = net->B, N = net->N, L = net->L, C0 = net->C0;
+    // input x = [sigma_T, sigma_a, eps] along channels, NHWC fp64
+    const size_t ncell = (size_t)B * N * N;
+    std::vector<double> xh(ncell * 3), wh(weights, weights + n_floats);
+    for (size_t c = 0; c < ncell; ++c) {
+      xh[3 * c] = sigma_T[c];
+      xh[3 * c + 1] = sigma_a[c];
+      xh[3 * c + 2] = eps[c];
+    }
+    double* dx = dalloc<double>(xh.size());
+    double* dw = dalloc<double>(wh.size());
+    RTE_CHECK_CUDA(cudaMemcpy(dx, xh.data(), sizeof(double) * xh.size(), cudaMemcpyHostToDevice));
+    RTE_CHECK_CUDA(cudaMemcpy(dw, wh.data(), sizeof(double) * wh.size(), cudaMemcpyHostToDevice));
+    const double* h_in = dx;
+    double* h_prev = nullptr;
+    int Hin = N, Cin = 3;
+    size_t off = 0;
+    auto launch = [&](const double* in, int Hi, int Ci, size_t k_off, size_t b_off, int Co, int ks, int stride,
+                      int relu, int Ho, double* out, float* out32) {
+      const int64_t n = (int64_t)B * Ho * Ho * Co;
+      const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 32);
+      prof_begin(nullptr, "coeffnet");
+      coeffnet_conv_kernel<<<blocks, 256>>>(in, B, Hi, Hi, Ci, dw + k_off, dw + b_off, Co, ks, stride, relu, Ho, Ho,
+                                            out, out32);
+      after_launch("coeffnet", nullptr, 2.0 * (double)n * Ci * ks * ks, 8.0 * (double)n, 3);
+    };
+    for (int l = 0; l < L; ++l) {
+      const int C = C0 << l, Ho = l == 0 ? N : Hin / 2;
+      Level& V = net->lv[l];
+      RTE_REQUIRE(V.H == Ho && V.C == C, "mgnet_coeffnet: internal level-shape mismatch");
+      const size_t kK = off, kb = kK + (size_t)C * Cin * 9, kGa = kb + C, kga = kGa + (size_t)C * C,
+                   kGb = kga + C, kgb = kGb + (size_t)C * C;
+      off = kgb + C;
+      const size_t nel = (size_t)B * Ho * Ho * C;
+      double* h = dalloc<double>(nel);
+      launch(h_in, Hin, Cin, kK, kb, C, 3, l == 0 ? 1 : 2, 1, Ho, h, nullptr);  // trunk
+      V.a64 = dalloc<double>(nel);
+      V.ab64 = dalloc<double>(nel);
+      V.a32 = dalloc<float>(nel);
+      V.ab32 = dalloc<float>(nel);
+      launch(h, Ho, C, kGa, kga, C, 1, 1, 0, Ho, V.a64, V.a32);   // a^[l]
+      launch(h, Ho, C, kGb, kgb, C, 1, 1, 0, Ho, V.ab64, V.ab32); // abar^[l] = a^{-1,[l]}
+      dfree(h_prev);
+      h_prev = h;
+      h_in = h;
+      Hin = Ho;
+      Cin = C;
+    }
+    RTE_CHECK_CUDA(cudaDeviceSynchronize());
+    dfree(h_prev);
+    dfree(dx);
+    dfree(dw);
+    return RTE_OK;
+  } catch (const Fail& f) {
+    return f.st;
+  } catch (const std::exception& e) {
+    set_error(std::string("internal: ") + e.what());
+    return RTE_EINTERNAL;
+  }
+}
+
+rte_status mgnet_modulation(const mgnet_net* net, int level, int which, double* host_out) {
+  try {
+    RTE_REQUIRE(net && host_out, "mgnet_modulation: NULL argument");
+    RTE_REQUIRE(level >= 0 && level < net->L && (which == 0 || which == 1), "mgnet_modulation: bad level/which");
+    const Level& V = net->lv[level];
+    const double* src = which == 0 ? V.a64 : V.ab64;
+    RTE_REQUIRE(src != nullptr, "mgnet_modulation: no CoeffNet maps (call mgnet_coeffnet first)");
+    RTE_CHECK_CUDA(cudaMemcpy(host_out, src, sizeof(double) * (size_t)net->B * V.H * V.H * V.C, cudaMemcpyDeviceToHost));
     return RTE_OK;
   } catch (const Fail& f) {
     return f.st;
@@ -608,16 +754,22 @@ void vcycle_run_t(const mgnet_net* net, const T* r, T* z, bool add_identity, con
     d.out_split = sp(0);
     conv(net->lift, d, r, bf[0].f, nullptr, 1.f, true, false);
   }
+  // CoeffNet modulation maps (R33; NULL = 1): a multiplies A * u, abar multiplies B * t
+  auto amap = [&](int l) -> const void* { return F32 ? (const void*)net->lv[l].a32 : (const void*)net->lv[l].a64; };
+  auto bmap = [&](int l) -> const void* { return F32 ? (const void*)net->lv[l].ab32 : (const void*)net->lv[l].ab64; };
   auto smooth = [&](int l, int bidx, bool first) {
     const Level& V = net->lv[l];
     ConvDesc d = desc_for(net, 0, 3, V.H, V.C, V.H, V.C);
     d.in_split = d.out_split = sp(l);
+    ConvDesc da = d, db = d;
+    da.mod = amap(l);
+    db.mod = bmap(l);
     const Bufs& b = bf[l];
-    if (first) {  // u = 0: u <- B * f  (A * 0 = 0 exactly)
-      conv(bidx, d, b.f, b.u, nullptr, 1.f);
+    if (first) {  // u = 0: u <- abar (.) B * f  (A * 0 = 0 exactly)
+      conv(bidx, db, b.f, b.u, nullptr, 1.f);
     } else {
-      conv(V.A, d, b.u, b.t, b.f, -1.f);   // t = f - A * u
-      conv(bidx, d, b.t, b.u, b.u, 1.f);   // u = u + B * t
+      conv(V.A, da, b.u, b.t, b.f, -1.f);   // t = f - a (.) A * u
+      conv(bidx, db, b.t, b.u, b.u, 1.f);   // u = u + abar (.) B * t
     }
   };
   for (int l = 0; l < L; ++l) {
@@ -631,13 +783,14 @@ void vcycle_run_t(const mgnet_net* net, const T* r, T* z, bool add_identity, con
       const Level& W = net->lv[l + 1];
       ConvDesc d = desc_for(net, 0, 3, V.H, V.C, V.H, V.C);
       d.in_split = d.out_split = sp(l);
+      d.mod = amap(l);
       ConvDesc dr = desc_for(net, 1, 3, V.H, V.C, W.H, W.C);
       dr.in_split = sp(l);
       dr.out_split = sp(l + 1);
       if (steps.empty()) {
         conv(V.R, dr, bf[l].f, bf[l + 1].f, nullptr, 1.f);
       } else {
-        conv(V.A, d, bf[l].u, bf[l].t, bf[l].f, -1.f);   // t = f - A * u
+        conv(V.A, d, bf[l].u, bf[l].t, bf[l].f, -1.f);   // t = f - a (.) A * u
         conv(V.R, dr, bf[l].t, bf[l + 1].f, nullptr, 1.f);  // f^{l+1} = R *_2 t
       }
     }

@@ -28,6 +28,10 @@ struct ConvDesc {
   int Hi = 0, Wi = 0, Ci = 0, Ho = 0, Wo = 0, Co = 0;
   const ConvW* w = nullptr;
   const struct ::mgnet_net* ws_owner = nullptr;  // net owning the split-K workspace (tensor-core path)
+  // CoeffNet modulation (R33): the conv result is multiplied elementwise by this map before the
+  // addend is added, out = s_add addend + s_in (mod (.) (W * in)); plain [B][Ho][Wo][Co] of the
+  // launch's element type (float or double), NULL = 1
+  const void* mod = nullptr;
 };
 
 struct Level {
@@ -39,6 +43,9 @@ struct Level {
   float* t = nullptr;
   bool split = false;  // f, u, t stored as hi/lo planes (levels whose convs run on the tensor cores)
   double *f64 = nullptr, *u64 = nullptr, *t64 = nullptr;  // fp64 V-cycle buffers (first use)
+  // CoeffNet modulation maps a^[l], abar^[l] (mgnet_coeffnet; NULL = unmodulated): [B][H][H][C]
+  float *a32 = nullptr, *ab32 = nullptr;
+  double *a64 = nullptr, *ab64 = nullptr;
 };
 
 double conv_flops(const ConvDesc& d);

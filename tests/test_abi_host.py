@@ -75,3 +75,11 @@ def test_rejects_bad_quadrature_request():
     import paper_2604_23265_b200 as P
     with pytest.raises(P.RteError):
         P.rte_quadrature(2, 6)
+
+
+@pytest.mark.parametrize("L,C0", [(1, 4), (3, 16), (6, 32)])
+def test_coeffnet_weight_count_matches_packed_layout(L, C0):
+    """mgnet_coeffnet_weight_count (host) equals the documented packed layout (R33)."""
+    import paper_2604_23265_b200 as P
+    import workloads as W
+    assert P.mgnet_coeffnet_weight_count(L, C0) == W.coeffnet_weight_count(L, C0)
