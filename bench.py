@@ -274,6 +274,11 @@ def run_ours(args, cfg):
     p = P.rte_setup(cfg.N, media.sigma_T[sl], media.sigma_a[sl], media.q[sl], media.eps[sl], media.g[sl],
                     media.inflow[sl], n_polar=cfg.n_polar, n_azim=cfg.n_azim)
     net = P.mgnet_create(p, cfg.L, cfg.C0, cfg.nu, weights)
+    coeffnet_ms = None
+    if args.coeffnet:  # NEXT-1: the medium-conditioned smoother (setup once per medium, untimed)
+        t0 = time.perf_counter()
+        P.mgnet_coeffnet(net, media.sigma_T[sl], media.sigma_a[sl], media.eps[sl], W.make_coeffnet_weights(cfg))
+        coeffnet_ms = (time.perf_counter() - t0) * 1e3
     b = torch.empty(p.shape, dtype=torch.float32, device=dev)
     P.rte_rhs(p, b)
     x = torch.zeros(p.shape, dtype=torch.float64, device=dev)
@@ -378,7 +383,9 @@ def run_ours(args, cfg):
                 "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "strong" if sharded else "weak",
                 "vs_baseline": None,
                 "dtype": "f32", "data": "synthetic",
-                "config": {"workload": _workload_name(cfg), "unknowns": cfg.unknowns,
+                "config": {"workload": _workload_name(cfg) + (" + CoeffNet-modulated smoother" if args.coeffnet else ""),
+                           "unknowns": cfg.unknowns,
+                           **({"coeffnet_setup_ms": round(coeffnet_ms, 1)} if args.coeffnet else {}),
                            "l2": "inputs larger than L2 (each vector 4 B x unknowns)" if cfg.unknowns * 4 > 126e6
                            else "working set L2-resident (small config)",
                            "parallelism": (f"{cfg.B} samples sharded over {ws} ranks" if sharded
@@ -406,6 +413,8 @@ def main():
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--coeffnet", action="store_true",
+                    help="NEXT-1: precondition with the CoeffNet-modulated MgNet (DESIGN.md R31-R33)")
     ap.add_argument("--reorth", type=int, default=2, choices=[0, 1, 2],
                     help="Gram-Schmidt: 2 selective re-orthogonalisation (default), 0 CGS2, 1 CGS1")
     args = ap.parse_args()

@@ -214,10 +214,11 @@ def coeffnet_weight_count(L: int, C0: int) -> int:
     return int(sum(math.prod(s) for _, s in coeffnet_weight_layout(L, C0)))
 
 
-def make_coeffnet_weights(cfg: Config, head_std: float = 0.02, seed: Optional[int] = None) -> np.ndarray:
+def make_coeffnet_weights(cfg: Config, head_std: float = 0.002, seed: Optional[int] = None) -> np.ndarray:
     """Packed float32 CoeffNet weights (seed 4000+k), drawn in fp64 and cast RN: trunk convs
-    N(0, 2/fan_in) (He), trunk biases 0, head weights N(0, head_std^2), head biases 1 -- a
-    near-identity modulation (the paper's trained weights are not released)."""
+    N(0, 2/fan_in) (He), trunk biases 0, head weights N(0, head_std^2 / C_l), head biases 1 -- a
+    near-identity modulation (config 5: maps within ~1 +- 0.4; the paper's trained weights are
+    not released)."""
     rng = np.random.Generator(np.random.PCG64(4000 + cfg.k if seed is None else seed))
     parts = []
     for name, shp in coeffnet_weight_layout(cfg.L, cfg.C0):
@@ -228,7 +229,7 @@ def make_coeffnet_weights(cfg: Config, head_std: float = 0.02, seed: Optional[in
         elif name.startswith("beta"):
             parts.append(np.zeros(n))
         elif name.startswith("G"):
-            parts.append(rng.standard_normal(n) * head_std)
+            parts.append(rng.standard_normal(n) * head_std / math.sqrt(shp[0]))
         else:
             parts.append(np.ones(n))
     return np.concatenate(parts).astype(np.float32)
