@@ -465,6 +465,27 @@ def arnoldi_columns(A, b, P, steps: int):
 # ---------------------------------------------------------------------------
 # 5. Dense reference (tests only; PAPER.md:44 direct LU)
 # ---------------------------------------------------------------------------
+def cell_blocks(prob: Problem) -> np.ndarray:
+    """The per-cell diagonal blocks of A (NEXT-2 block Jacobi; "the standard Block
+    Jacobi preconditioner"; SPEC.md:380 cell blocks): the terms of apply() that couple ordinates of
+    one cell,  A_cc = diag(|c_m|/h + |s_m|/h + sigma_t) - sigma_s S.  [B][N][N][M][M]."""
+    h = prob.h
+    lam = (np.abs(prob.qd.c) + np.abs(prob.qd.s)) / h
+    eye = np.eye(prob.M)
+    return (lam[None, None, None, :, None] * eye + prob.sig_t[..., None, None] * eye
+            - prob.sig_s[..., None, None] * prob.S[:, None, None, :, :])
+
+
+def block_jacobi(prob: Problem) -> Callable[[np.ndarray], np.ndarray]:
+    """P r = A_cc^{-1} r_c for every cell c (numpy.linalg.solve per block, one library step)."""
+    Acc = cell_blocks(prob)
+
+    def P(r):
+        r = np.asarray(r, np.float64).reshape(prob.shape)
+        return np.linalg.solve(Acc, r[..., None])[..., 0]
+    return P
+
+
 def dense_matrix(prob: Problem) -> np.ndarray:
     """Assemble A column by column via apply(e_k) (small problems only)."""
     n = int(np.prod(prob.shape))

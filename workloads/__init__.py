@@ -235,6 +235,56 @@ def make_coeffnet_weights(cfg: Config, head_std: float = 0.002, seed: Optional[i
     return np.concatenate(parts).astype(np.float32)
 
 
+PAPER_REGIMES = ("diffusion", "transport", "lr", "rl", "tb", "bt", "centre", "outer")
+
+
+def paper_media(n_samples: int, N: int = 32, degree: int = 2, regime: str = "diffusion", M: int = 4,
+                seed: int = 0) -> Media:
+    """The paper's test media (§4.1; NEXT-2): per sample,
+      sigma = (2 + sum_{k<=n} c_{x,k} (x - 1/2)^k) (2 + sum_{k<=n} c_{y,k} (y - 1/2)^k),
+      c ~ U[-1, 1], drawn independently for sigma_T and sigma_a, evaluated at cell centres
+      (R34); sigma_T is shifted so that sigma_T - sigma_a >= 0.2 everywhere.
+    eps regimes: "diffusion" eps = 0.01 (c + 0.1), c ~ U[0, 1] per sample; "transport" eps = 1;
+    the six sharp-interface layouts mix the two in space: "lr"/"rl" (left/right half diffusive),
+    "tb"/"bt" (bottom/top half diffusive), "centre" ([1/4, 3/4]^2 diffusive, transport outside)
+    and "outer" (vice versa).  q = 0, g = 0, no inflow: the paper pairs the media with random
+    right-hand sides, so the GMRES experiments draw b directly (make_paper_rhs)."""
+    if regime not in PAPER_REGIMES:
+        raise ValueError(f"regime must be one of {PAPER_REGIMES}")
+    rng = np.random.Generator(np.random.PCG64([5000, seed]))
+    X, Y = _cell_centres(N)
+
+    def poly():
+        cx = rng.uniform(-1.0, 1.0, degree + 1)
+        cy = rng.uniform(-1.0, 1.0, degree + 1)
+        px = 2.0 + sum(cx[k] * (X - 0.5) ** k for k in range(degree + 1))
+        py = 2.0 + sum(cy[k] * (Y - 0.5) ** k for k in range(degree + 1))
+        return px * py
+    sT = np.zeros((n_samples, N, N)); sa = np.zeros_like(sT); eps = np.ones_like(sT)
+    for b in range(n_samples):
+        t, a = poly(), poly()
+        gap = (t - a).min()
+        if gap < 0.2:
+            t = t + (0.2 - gap)
+        sT[b], sa[b] = t, a
+        e_diff = 0.01 * (rng.uniform(0.0, 1.0) + 0.1)
+        diff = {"diffusion": np.ones((N, N), bool), "transport": np.zeros((N, N), bool),
+                "lr": np.broadcast_to(X < 0.5, (N, N)), "rl": np.broadcast_to(X >= 0.5, (N, N)),
+                "tb": np.broadcast_to(Y < 0.5, (N, N)), "bt": np.broadcast_to(Y >= 0.5, (N, N)),
+                "centre": (X > 0.25) & (X < 0.75) & (Y > 0.25) & (Y < 0.75)}
+        diff["outer"] = ~diff["centre"]
+        eps[b] = np.where(diff[regime], e_diff, 1.0)
+    f32 = lambda a: np.asarray(a, np.float32)
+    return Media(f32(sT), f32(sa), f32(np.zeros_like(sT)), f32(eps), np.zeros(n_samples, np.float32),
+                 np.zeros((n_samples, 4, N, M), np.float32))
+
+
+def make_paper_rhs(n_samples: int, N: int = 32, M: int = 4, seed: int = 0) -> np.ndarray:
+    """Random right-hand sides for the paper workload: b ~ U[0, 1] i.i.d. per unknown (float32)."""
+    rng = np.random.Generator(np.random.PCG64([6000, seed]))
+    return rng.uniform(0.0, 1.0, (n_samples, N, N, M)).astype(np.float32)
+
+
 def make_vector(cfg: Config, which: int = 0) -> np.ndarray:
     """Parity vector x ~ N(0,1) i.i.d. per unknown, float32 [B][N][N][M] (seed 3000+k)."""
     rng = np.random.Generator(np.random.PCG64([3000 + cfg.k, which]))
