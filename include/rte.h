@@ -150,8 +150,17 @@ rte_status mgnet_coeffnet(mgnet_net* net, const float* sigma_T, const float* sig
  * NHWC, to host_out.  Errors: RTE_EINVAL (bad level/which, or no maps attached). */
 rte_status mgnet_modulation(const mgnet_net* net, int level, int which, double* host_out);
 
+/* Block-Jacobi preconditioner (NEXT-2; R35): z = A_cc^{-1} r per cell,
+ * A_cc = diag((|c_m| + |s_m|)/h + sigma_t) - sigma_s S the restriction of A to the cell's M
+ * ordinates.  r_dev, z_dev [n] (float32 / float64), must not alias.  Builds the inverse blocks on the
+ * first call (fp64 Gauss-Jordan, kept by the problem).  Errors: RTE_EINVAL (sizes, see gmres_opts). */
+rte_status rte_blockjacobi_apply(const rte_problem* p, const float* r_dev, float* z_dev, void* stream);
+rte_status rte_blockjacobi_apply_f64(const rte_problem* p, const double* r_dev, double* z_dev, void* stream);
+
 /* Restarted right-preconditioned GMRES(m) (R21, R22).
- * Preconditioner P = I + V (precond=1, requires net) or P = I (precond=0).
+ * Preconditioner P = I + V (precond=1, requires net), P = I (precond=0), or block Jacobi
+ * (precond=2, NEXT-2: P = A_cc^{-1} per cell, R35; the inverse blocks are built on the
+ * first use and kept by the problem; RTE_EINVAL if cells x M^2 x 12 B > 24 GiB or M > 128).
  * Iterate x is float64; the Krylov basis is float32 (precision=0) or float64 (precision=1); dot
  * products accumulate in float64; every restart recomputes r = b - A x in float64.  The batch's
  * samples are independent solves with their own Arnoldi/Givens state. */
@@ -159,7 +168,7 @@ typedef struct {
   int restart;       /* m, 1..64 */
   int maxit;         /* cap on total inner iterations per sample */
   double rtol;       /* stop when ||b - A x|| <= rtol ||b|| */
-  int precond;       /* 0 none, 1 MgNet (I + V) */
+  int precond;       /* 0 none, 1 MgNet (I + V), 2 block Jacobi */
   int reorth;        /* 0 = CGS2: two classical Gram-Schmidt passes; 1 = one CGS pass;
                         2 = selective (DGKS, recommended): the second pass runs only when
                         ||v'|| < ||w||/sqrt(2), decided on the device */

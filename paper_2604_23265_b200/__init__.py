@@ -15,7 +15,7 @@ import numpy as np
 from . import _lib
 from ._lib import RteError, check, gmres_opts, gmres_report, lib
 
-__all__ = ["Problem", "MgNet", "rte_setup", "rte_rhs", "rte_apply", "rte_apply_f64", "mgnet_create",
+__all__ = ["Problem", "MgNet", "rte_setup", "rte_rhs", "rte_apply", "rte_apply_f64", "rte_blockjacobi_apply", "mgnet_create",
            "mgnet_vcycle", "mgnet_vcycle_f64", "mgnet_coeffnet", "mgnet_coeffnet_weight_count", "mgnet_modulation", "gmres_solve", "rte_quadrature", "rte_hg_matrix", "rte_launch_count", "rte_timing_enable", "rte_timing_filter", "rte_timing_reset",
            "rte_timing_get", "RteError", "LIB_PATH"]
 
@@ -130,6 +130,16 @@ def rte_rhs(p: Problem, b, stream=None) -> None:
 
 def rte_apply(p: Problem, x, y, stream=None) -> None:
     check("rte_apply", lib.rte_apply(p.handle, _dev(x, "f32"), _dev(y, "f32"), C.c_void_p(_stream(stream))))
+
+
+def rte_blockjacobi_apply(p: Problem, r, z, stream=None) -> None:
+    """z = A_cc^{-1} r per cell (NEXT-2 block Jacobi; float32 or float64 tensors)."""
+    if r.dtype == np.float64 or str(getattr(r, "dtype", "")) == "torch.float64":
+        check("rte_blockjacobi_apply_f64", lib.rte_blockjacobi_apply_f64(p.handle, _dev(r, "f64"), _dev(z, "f64"),
+                                                                        C.c_void_p(_stream(stream))))
+    else:
+        check("rte_blockjacobi_apply", lib.rte_blockjacobi_apply(p.handle, _dev(r, "f32"), _dev(z, "f32"),
+                                                                C.c_void_p(_stream(stream))))
 
 
 def rte_apply_f64(p: Problem, x, y, stream=None) -> None:

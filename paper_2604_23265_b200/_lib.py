@@ -64,6 +64,8 @@ SIGS = {
     "mgnet_vcycle": (C.c_int, [_vp, _vp, _vp, C.c_int, _vp]),
     "mgnet_vcycle_f64": (C.c_int, [_vp, _vp, _vp, C.c_int, _vp]),
     "mgnet_coeffnet_weight_count": (C.c_size_t, [C.c_int, C.c_int]),
+    "rte_blockjacobi_apply": (C.c_int, [_vp, _vp, _vp, _vp]),
+    "rte_blockjacobi_apply_f64": (C.c_int, [_vp, _vp, _vp, _vp]),
     "mgnet_coeffnet": (C.c_int, [_vp, _fp, _fp, _fp, _fp, C.c_size_t]),
     "mgnet_modulation": (C.c_int, [_vp, C.c_int, C.c_int, C.POINTER(C.c_double)]),
     "gmres_solve": (C.c_int, [_vp, _vp, _vp, _vp, C.POINTER(gmres_opts), C.POINTER(gmres_report), _vp]),

@@ -95,6 +95,9 @@ struct rte_problem {
   bool tc_apply = false;    // tensor-core apply path available for this M
   mutable void* tc_state = nullptr;  // lazily created TMA descriptors etc.
   mutable double* scratch64 = nullptr;  // small device scratch
+  // block-Jacobi inverse cell blocks [ncell][M][M] (blockjacobi.cu; built on first use)
+  mutable double* bj64 = nullptr;
+  mutable float* bj32 = nullptr;
 };
 
 // ---- kernel launchers (apply.cu) --------------------------------------------
@@ -106,6 +109,10 @@ void launch_apply_f32(const rte_problem* p, const float* x, float* y, const doub
 // y = A x (fp64); if b != NULL: y = b - A x.
 void launch_apply_f64(const rte_problem* p, const double* x, double* y, const float* b, cudaStream_t st);
 bool apply_tc_supported(int M);
+// block Jacobi (blockjacobi.cu): y = A_cc^{-1} (alpha x) per cell; builds the blocks on first use
+void bj_prepare(const rte_problem* p);
+template <typename T>
+void bj_apply(const rte_problem* p, const T* x, T* y, const double* alpha, int alpha_stride, cudaStream_t st);
 double apply_flops(const rte_problem* p);
 double apply_bytes(const rte_problem* p, int elt, int b_elt);
 void free_tc_state(rte_problem* p);

@@ -500,7 +500,9 @@ extern "C" rte_status gmres_solve(const rte_problem* p, const mgnet_net* net, co
     RTE_REQUIRE(m >= 1 && m <= 32, "gmres_solve: restart must be in [1, 32]");
     RTE_REQUIRE(opts->maxit >= 0, "gmres_solve: maxit must be >= 0");
     RTE_REQUIRE(opts->rtol > 0.0, "gmres_solve: rtol must be > 0");
-    RTE_REQUIRE(opts->precond == 0 || (opts->precond == 1 && net), "gmres_solve: precond=1 requires a net");
+    RTE_REQUIRE(opts->precond == 0 || opts->precond == 2 || (opts->precond == 1 && net),
+                "gmres_solve: precond must be 0 (none), 1 (MgNet, requires a net) or 2 (block Jacobi)");
+    if (opts->precond == 2) bj_prepare(p);  // (NEXT-2; builds the inverse cell blocks once)
     RTE_REQUIRE(!net || net->prob == p, "gmres_solve: net was created for another problem");
     cudaStream_t st = as_stream(stream);
     GmresWork& W = get_work(p, m);
@@ -598,6 +600,9 @@ extern "C" rte_status gmres_solve(const rte_problem* p, const mgnet_net* net, co
           if (opts->precond == 1) {
             vcycle_run_f64(net, W.z64, W.r64, true, st);
             zin = W.r64;
+          } else if (opts->precond == 2) {
+            bj_apply<double>(p, W.z64, W.r64, nullptr, 0, st);
+            zin = W.r64;
           }
           launch_apply_f64(p, zin, W.w64, nullptr, st);
           cgs_passes(W.V64, W.w64);
@@ -606,6 +611,9 @@ extern "C" rte_status gmres_solve(const rte_problem* p, const mgnet_net* net, co
           const float* vj = W.V + (size_t)j * n;
           if (opts->precond == 1) {
             vcycle_run(net, vj, W.z, true, W.alpha + j, m + 1, st);
+            launch_apply_f32(p, W.z, W.w, nullptr, 0, st);
+          } else if (opts->precond == 2) {
+            bj_apply<float>(p, vj, W.z, W.alpha + j, m + 1, st);
             launch_apply_f32(p, W.z, W.w, nullptr, 0, st);
           } else {
             launch_apply_f32(p, vj, W.w, W.alpha + j, m + 1, st);
@@ -654,6 +662,9 @@ extern "C" rte_status gmres_solve(const rte_problem* p, const mgnet_net* net, co
         if (opts->precond == 1) {
           vcycle_run_f64(net, W.z64, W.r64, true, st);
           corr = W.r64;
+        } else if (opts->precond == 2) {
+          bj_apply<double>(p, W.z64, W.r64, nullptr, 0, st);
+          corr = W.r64;
         }
         prof_begin(st, "axpy64");
         axpy64_kernel<double><<<dim3(W.nblk, B), kThreads, 0, st>>>(x_dev, corr, nullptr, W.kcols, W.ns, W.nblk);
@@ -666,6 +677,9 @@ extern "C" rte_status gmres_solve(const rte_problem* p, const mgnet_net* net, co
         const float* corr = W.w;
         if (opts->precond == 1) {
           vcycle_run(net, W.w, W.z, true, nullptr, 0, st);
+          corr = W.z;
+        } else if (opts->precond == 2) {
+          bj_apply<float>(p, W.w, W.z, nullptr, 0, st);
           corr = W.z;
         }
         prof_begin(st, "axpy64");

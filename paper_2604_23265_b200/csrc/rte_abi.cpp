@@ -274,7 +274,8 @@ rte_status rte_timing_get(int idx, char* name, int name_len, int* kind, int64_t*
 static void free_problem(rte_problem* p) {
   if (!p) return;
   void* ptrs[] = {p->sig_t, p->sig_s, p->f, p->sig_t64, p->sig_s64, p->S32, p->St32, p->St64, p->S_hi,
-                  p->S_lo, p->ax, p->ay, p->ax64, p->ay64, p->sgx, p->sgy, p->inflow, p->scratch64};
+                  p->S_lo, p->ax, p->ay, p->ax64, p->ay64, p->sgx, p->sgy, p->inflow, p->scratch64,
+                  p->bj64, p->bj32};
   for (void* q : ptrs) dfree(q);
   free_tc_state(p);
   free_gmres_work(p);
