@@ -462,11 +462,11 @@ Plan make_plan(const ConvDesc& d) {
   return P;
 }
 
-template <int BN, int AM, bool ASPLIT>
+template <int BN, int AM, bool ASPLIT, int CPS = 1>
 void launch_bn(const Plan& P, const CUtensorMap& ta, const CUtensorMap& tbh, const CUtensorMap& tbl,
                const CUtensorMap& te, const tc::EpiConv& epi, cudaStream_t st) {
-  auto kern = tc::gemm3xtf32_kernel<BN, AM, ASPLIT, tc::EpiConv>;
-  constexpr int smem = tc::gemm_smem_bytes<BN, AM, ASPLIT>();
+  auto kern = tc::gemm3xtf32_kernel<BN, AM, ASPLIT, tc::EpiConv, CPS>;
+  constexpr int smem = tc::gemm_smem_bytes<BN, AM, ASPLIT, CPS>();
   tc::ensure_smem((const void*)kern, smem);
   const long long units = (long long)P.mtiles * P.ntiles * P.g.nsplit;
   if (P.g.cl) {
@@ -486,7 +486,7 @@ void launch_bn(const Plan& P, const CUtensorMap& ta, const CUtensorMap& tbh, con
     RTE_CHECK_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tbh, tbl, te, P.g, epi));
     return;
   }
-  const int grid = (int)std::min<long long>(units, num_sms());
+  const int grid = (int)std::min<long long>(units, (long long)CPS * num_sms());
   kern<<<grid, tc::kGemmThreads, smem, st>>>(ta, tbh, tbl, te, P.g, epi);
 }
 
@@ -537,16 +537,25 @@ bool conv_tc_try(const ConvDesc& d, const float* in, float* out, const float* ad
     epi.part = d.ws_owner->tc_ws;
   }
   prof_begin(st, conv_class_name(d, true));
+  // BN = 32 kernels run two CTAs per SM (each half the TMEM, ~113 KB of shared memory): their
+  // pipelines are hand-off-latency bound, so two of them per SM hide each other (RTE_TC_CPS1=1: one)
+  static const bool two_per_sm = getenv("RTE_TC_CPS1") == nullptr;
   auto dispatch = [&](auto bn_tag) {
     constexpr int BN = decltype(bn_tag)::value;
     if (P.am == 2) {
       if constexpr (BN <= 64) launch_bn<BN, 2, false>(P, ta, tbh, tbl, te, epi, st);
     } else if (P.halo) {
       if (d.in_split) launch_bn<BN, 1, true>(P, ta, tbh, tbl, te, epi, st);
-      else launch_bn<BN, 1, false>(P, ta, tbh, tbl, te, epi, st);
+      else if constexpr (BN == 32) {
+        if (two_per_sm && !g.cl) launch_bn<BN, 1, false, 2>(P, ta, tbh, tbl, te, epi, st);
+        else launch_bn<BN, 1, false>(P, ta, tbh, tbl, te, epi, st);
+      } else launch_bn<BN, 1, false>(P, ta, tbh, tbl, te, epi, st);
     } else {
       if (d.in_split) launch_bn<BN, 0, true>(P, ta, tbh, tbl, te, epi, st);
-      else launch_bn<BN, 0, false>(P, ta, tbh, tbl, te, epi, st);
+      else if constexpr (BN == 32) {
+        if (two_per_sm && !g.cl) launch_bn<BN, 0, false, 2>(P, ta, tbh, tbl, te, epi, st);
+        else launch_bn<BN, 0, false>(P, ta, tbh, tbl, te, epi, st);
+      } else launch_bn<BN, 0, false>(P, ta, tbh, tbl, te, epi, st);
     }
   };
   switch (P.BN) {

@@ -89,24 +89,27 @@ constexpr int stage_chunks() {
 #ifndef RTE_NA128
 #define RTE_NA128 4  // A ring depth of N = 128 window kernels (measured: 3 -> 4 is 4% on the apply, 5 no better)
 #endif
-template <int BN, int AM, bool ASPLIT = false>
+// CPS = CTAs per SM (1, or 2 for BN = 32: two independent pipelines per SM hide each other's
+// hand-off latency; each gets half of TMEM and ~113 KB of shared memory)
+template <int BN, int AM, bool ASPLIT = false, int CPS = 1>
 struct Plan {
   static constexpr int kBBytes = BN * 128;                          // one of B hi / B lo
   static constexpr int kATile = AM == 2 ? kSSRows * 128 : AM == 1 ? kHaloRows * 128 : kABytes;
   static constexpr int kASlot = (ASPLIT || AM == 2 ? 2 : 1) * kATile;  // hi + lo tiles when split
   static constexpr int kBSlot = 2 * kBBytes;
-  static constexpr int kBudget = (222 - 32 * stage_chunks<BN>()) * 1024;  // rings (+ staging = 222 KB)
+  static constexpr int kBudget = ((CPS == 1 ? 222 : 110) - 32 * stage_chunks<BN>()) * 1024;  // rings
   // A ring depth: halo tiles are reused for 9 K blocks; window tiles are one K block each, so
   // they need a deeper ring to cover the HBM latency (BN = 32 leaves room for 8)
-  static constexpr int kNA = (AM != 0 || ASPLIT) ? 2 : BN == 32 ? 8 : BN == 64 ? 4 : RTE_NA128;
+  static constexpr int kNA = (AM != 0 || ASPLIT) ? 2 : CPS == 2 ? 3 : BN == 32 ? 8 : BN == 64 ? 4 : RTE_NA128;
   static constexpr int kNBraw = (kBudget - kNA * kASlot) / kBSlot;
   static constexpr int kNB = kNBraw > 8 ? 8 : kNBraw;               // B ring depth
+  static_assert(kNB >= 1, "shared-memory plan leaves no B slot");
   static constexpr int kRingBytes = kNA * kASlot + kNB * kBSlot;
 };
 
-template <int BN, int AM, bool ASPLIT = false>
+template <int BN, int AM, bool ASPLIT = false, int CPS = 1>
 constexpr int gemm_smem_bytes() {
-  return Plan<BN, AM, ASPLIT>::kRingBytes + 2 * stage_chunks<BN>() * kStageBytes + 1024 /*align*/ + 1024 /*barriers*/ +
+  return Plan<BN, AM, ASPLIT, CPS>::kRingBytes + 2 * stage_chunks<BN>() * kStageBytes + 1024 /*align*/ + 1024 /*barriers*/ +
          1024 /*row centres*/;
 }
 
@@ -120,6 +123,11 @@ constexpr bool tmem_fused() {
 // Fused form: NG group buffers of 2BN columns (the MMA can run NG - 1 groups ahead of the
 // promoters, so a tile's epilogue overlaps the next tile's K loop) and 2 A buffers.
 // Split form: 2 main buffers + X + the rest as A buffers.
+// per-role cycle counters (dbg bit 6) are compiled in only with -DRTE_TC_PROF=1 (experiment builds:
+// scripts/perf_roles.py); the production build keeps their registers free
+#ifndef RTE_TC_PROF
+#define RTE_TC_PROF 0
+#endif
 #ifndef RTE_EPI_BATCH_MAX
 #define RTE_EPI_BATCH_MAX 8
 #endif
@@ -129,18 +137,19 @@ constexpr bool tmem_fused() {
 #ifndef RTE_TC_NA_MIN
 #define RTE_TC_NA_MIN 2
 #endif
-template <int BN>
+// (TC = TMEM columns of one CTA: 512 / CPS)
+template <int BN, int TC = 512>
 constexpr int tmem_groups() {
-  constexpr int room = (512 - 64 * RTE_TC_NA_MIN) / (2 * BN);
+  constexpr int room = (TC - 64 * RTE_TC_NA_MIN) / (2 * BN);
   return tmem_fused<BN>() ? (room < RTE_TC_NG_MAX ? room : RTE_TC_NG_MAX) : 2;
 }
-template <int BN>
+template <int BN, int TC = 512>
 constexpr int tmem_acc_cols() {
-  return tmem_fused<BN>() ? tmem_groups<BN>() * 2 * BN : 3 * BN;
+  return tmem_fused<BN>() ? tmem_groups<BN, TC>() * 2 * BN : 3 * BN;
 }
-template <int BN>
+template <int BN, int TC = 512>
 constexpr int tmem_abufs() {
-  return (512 - tmem_acc_cols<BN>()) / 64 < 6 ? (512 - tmem_acc_cols<BN>()) / 64 : 6;
+  return (TC - tmem_acc_cols<BN, TC>()) / 64 < 6 ? (TC - tmem_acc_cols<BN, TC>()) / 64 : 6;
 }
 
 struct TileCoord {
@@ -261,8 +270,8 @@ __device__ __forceinline__ void tw_wait(uint64_t* bar, uint32_t par, bool on, lo
 // absolute shared-memory address, so any row offset is valid; scripts/ss_offset_test.cu).  The
 // converter warps split the halo once per tile in place (hi over the fp32 tile, lo into its twin)
 // and the tensor core reads both straight from shared memory: no per-tap conversion, no TMEM A.
-template <int BN, int AM, bool ASPLIT, class Epi>
-__global__ void __launch_bounds__(kGemmThreads, 1)
+template <int BN, int AM, bool ASPLIT, class Epi, int CPS = 1>
+__global__ void __launch_bounds__(kGemmThreads, CPS)
     gemm3xtf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBhi,
                       const __grid_constant__ CUtensorMap tmBlo, const __grid_constant__ CUtensorMap tmE,
                       const Geom g, const Epi epi) {
@@ -272,12 +281,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   static_assert(!(HALO && Epi::kCenter), "row centring is for the 1x1 (apply) kernels");
   static_assert(!(ASPLIT && Epi::kCenter), "row centring needs the plain fp32 A operand");
   static_assert(!(SSH && ASPLIT), "SS-halo kernels split the activations themselves");
-  using PL = Plan<BN, AM, ASPLIT>;
+  static_assert(CPS == 1 || (CPS == 2 && BN == 32 && !ASPLIT && AM != 2), "two CTAs per SM: BN = 32 only");
+  using PL = Plan<BN, AM, ASPLIT, CPS>;
+  constexpr int TCOLS = 512 / CPS;
   constexpr int NAR = PL::kNA, NBR = PL::kNB;
-  constexpr int NA = tmem_abufs<BN>();
+  constexpr int NA = tmem_abufs<BN, TCOLS>();
   constexpr int NCV = NA > NAR ? NA : NAR;  // conv barriers (SSH: one per A ring slot)
   constexpr int BBYTES = PL::kBBytes;
-  constexpr uint32_t TMEM_COLS = 512;
+  constexpr uint32_t TMEM_COLS = TCOLS;
   constexpr bool FUSED = tmem_fused<BN>();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -290,7 +301,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* bempty = bfull + NBR;      // [NBR] MMAs done with the B tiles
   uint64_t* conv = bempty + NBR;       // [NA] TMEM A buffer written (4 converter warps); SSH: A slot split
   uint64_t* afree = conv + NCV;        // [NA] MMAs done with the TMEM A buffer
-  constexpr int NG = tmem_groups<BN>();
+  constexpr int NG = tmem_groups<BN, TCOLS>();
   uint64_t* mfull = afree + NA;        // [NG] group buffer ready for promotion
   uint64_t* mempty = mfull + NG;       // [NG] group buffer drained (8 promoter warps)
   uint64_t* xempty = mempty + NG;      // [1] unit-long X drained (8 promoter warps)
@@ -309,7 +320,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   // bit6 enables the counters; bits 8..15 (if set) restrict them to kernels with that BN, bit16 to
   // halo kernels
   // (bit 17: only non-halo kernels, bit 18: only row-centred (apply) kernels, bit 19: only convs)
-  const bool prof = (g.dbg & 64) && lane == 0 && (((g.dbg >> 8) & 0xff) == 0 || ((g.dbg >> 8) & 0xff) == BN) &&
+  const bool prof = RTE_TC_PROF && (g.dbg & 64) && lane == 0 && (((g.dbg >> 8) & 0xff) == 0 || ((g.dbg >> 8) & 0xff) == BN) &&
                     (!((g.dbg >> 16) & 1) || HALO) && (!((g.dbg >> 17) & 1) || !HALO) &&
                     (!((g.dbg >> 18) & 1) || Epi::kCenter) && (!((g.dbg >> 19) & 1) || !Epi::kCenter) &&
                     (((g.dbg >> 24) & 0xff) == 0 || ((g.dbg >> 24) & 0xff) == g.kb_total);  // bits 24..31: K blocks
@@ -353,7 +364,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t tmem_x = tmem + 2 * BN;  // split form only
-  const uint32_t tmem_a = tmem + tmem_acc_cols<BN>();
+  const uint32_t tmem_a = tmem + tmem_acc_cols<BN, TCOLS>();
 
   if (warp == 0) {
     // ===== TMA producer: the whole warp walks the pipeline, one elected lane issues =====
@@ -575,54 +586,64 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const uint32_t row_s = smem_u32(aring + as * PL::kASlot) + (uint32_t)arow * 128u;
         const bool skip = (g.dbg & 1) != 0;
         const long long tc0 = prof ? clock64() : 0;
-        float hi[32], lo[32];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          if (skip) break;
-          const uint32_t qo = (uint32_t)((q ^ (arow & 7)) << 4);
-          const float4 v = lds128(row_s + qo);
-          hi[4 * q] = v.x;
-          hi[4 * q + 1] = v.y;
-          hi[4 * q + 2] = v.z;
-          hi[4 * q + 3] = v.w;
-          if (ASPLIT) {
-            const float4 l = lds128(row_s + PL::kATile + qo);
-            lo[4 * q] = l.x;
-            lo[4 * q + 1] = l.y;
-            lo[4 * q + 2] = l.z;
-            lo[4 * q + 3] = l.w;
-          }
-        }
-        // done with this A tile after its last K block
+        // the K block's 32 columns in passes of CWC (CPS = 2: 16, to fit the register budget)
+        constexpr int CWC = CPS == 1 ? 32 : 16;
         const bool last_of_tile = !HALO || tap == 8 || kb + 1 == w.kb1;
-        if (last_of_tile) {
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&aempty[as]);
-          if (++as == NAR) { as = 0; aph ^= 1; }
-        }
-        if constexpr (Epi::kCenter) {
-          // row centre c_r = the row's first element in the unit's first K block; the GEMM then
-          // runs on a - c_r (see EpiApply); published to the epilogue through cvec
-          if (kb == w.kb0) {
-            c = hi[0];
-            mbar_wait(&cempty[li & 1], ((uint32_t)(li >> 1) & 1u) ^ 1u);
-            cvec[(li & 1) * 128 + r] = c;
-            mbar_arrive(&cfull[li & 1]);
-          }
-        }
-        if (!ASPLIT) {
-#pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            const float x = Epi::kCenter ? hi[e] - c : hi[e];
-            split_tf32_fast(x, hi[e], lo[e]);
-          }
-        }
         const uint32_t ta = tmem_a + (uint32_t)(64 * ab) + lane_base;
-        if (!skip) {
-          tmem_st32(ta, hi);
-          tmem_st32(ta + 32, lo);
-          tmem_wait_st();
+#pragma unroll
+        for (int c0 = 0; c0 < 32; c0 += CWC) {
+          float hi[CWC], lo[CWC];
+#pragma unroll
+          for (int q = 0; q < CWC / 4; ++q) {
+            if (skip) break;
+            const uint32_t qo = (uint32_t)(((c0 / 4 + q) ^ (arow & 7)) << 4);
+            const float4 v = lds128(row_s + qo);
+            hi[4 * q] = v.x;
+            hi[4 * q + 1] = v.y;
+            hi[4 * q + 2] = v.z;
+            hi[4 * q + 3] = v.w;
+            if (ASPLIT) {
+              const float4 l = lds128(row_s + PL::kATile + qo);
+              lo[4 * q] = l.x;
+              lo[4 * q + 1] = l.y;
+              lo[4 * q + 2] = l.z;
+              lo[4 * q + 3] = l.w;
+            }
+          }
+          // done with this A tile after its last K block's last pass
+          if (last_of_tile && c0 + CWC == 32) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&aempty[as]);
+            if (++as == NAR) { as = 0; aph ^= 1; }
+          }
+          if constexpr (Epi::kCenter) {
+            // row centre c_r = the row's first element in the unit's first K block; the GEMM then
+            // runs on a - c_r (see EpiApply); published to the epilogue through cvec
+            if (kb == w.kb0 && c0 == 0) {
+              c = hi[0];
+              mbar_wait(&cempty[li & 1], ((uint32_t)(li >> 1) & 1u) ^ 1u);
+              cvec[(li & 1) * 128 + r] = c;
+              mbar_arrive(&cfull[li & 1]);
+            }
+          }
+          if (!ASPLIT) {
+#pragma unroll
+            for (int e = 0; e < CWC; ++e) {
+              const float x = Epi::kCenter ? hi[e] - c : hi[e];
+              split_tf32_fast(x, hi[e], lo[e]);
+            }
+          }
+          if (!skip) {
+            if constexpr (CWC == 32) {
+              tmem_st32(ta, hi);
+              tmem_st32(ta + 32, lo);
+            } else {
+              tmem_st16(ta + (uint32_t)c0, hi);
+              tmem_st16(ta + 32 + (uint32_t)c0, lo);
+            }
+          }
         }
+        if (!skip) tmem_wait_st();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&conv[ab]);

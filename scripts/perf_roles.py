@@ -1,5 +1,6 @@
-"""Per-role cycle breakdown of the tensor-core GEMM over one V-cycle (experiments: needs
-RTE_TC_DBG with bit 6; see csrc/tc_gemm.cuh g_tc_prof)."""
+"""Per-role cycle breakdown of the tensor-core GEMM over one V-cycle (experiments: needs a library
+built with -DRTE_TC_PROF=1 -- var_libs/librte_prof.so, selected with RTE_LIB_PATH -- and RTE_TC_DBG
+with bit 6; see csrc/tc_gemm.cuh g_tc_prof)."""
 import ctypes as C
 import os
 import sys
