@@ -36,7 +36,10 @@ struct EpiApply {
   const double* alpha;
   int alpha_stride, N, M;
 
-  static constexpr int kBatch = 2;  // rows whose global inputs are in flight together (measured best)
+#ifndef RTE_APPLY_BATCH
+#define RTE_APPLY_BATCH 2
+#endif
+  static constexpr int kBatch = RTE_APPLY_BATCH;  // rows whose global inputs are in flight together (measured best)
   struct Col {
     int m, sx, sy;
     float4 a_x, a_y;

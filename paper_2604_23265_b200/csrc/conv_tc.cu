@@ -540,20 +540,21 @@ bool conv_tc_try(const ConvDesc& d, const float* in, float* out, const float* ad
   // BN = 32 kernels run two CTAs per SM (each half the TMEM, ~113 KB of shared memory): their
   // pipelines are hand-off-latency bound, so two of them per SM hide each other (RTE_TC_CPS1=1: one)
   static const bool two_per_sm = getenv("RTE_TC_CPS1") == nullptr;
+  static const bool two_per_sm64 = two_per_sm;  // (N = 64 too: single halo slot per CTA, NG = 1)
   auto dispatch = [&](auto bn_tag) {
     constexpr int BN = decltype(bn_tag)::value;
     if (P.am == 2) {
       if constexpr (BN <= 64) launch_bn<BN, 2, false>(P, ta, tbh, tbl, te, epi, st);
     } else if (P.halo) {
       if (d.in_split) launch_bn<BN, 1, true>(P, ta, tbh, tbl, te, epi, st);
-      else if constexpr (BN == 32) {
-        if (two_per_sm && !g.cl) launch_bn<BN, 1, false, 2>(P, ta, tbh, tbl, te, epi, st);
+      else if constexpr (BN <= 64) {
+        if ((BN == 32 ? two_per_sm : two_per_sm64) && !g.cl) launch_bn<BN, 1, false, 2>(P, ta, tbh, tbl, te, epi, st);
         else launch_bn<BN, 1, false>(P, ta, tbh, tbl, te, epi, st);
       } else launch_bn<BN, 1, false>(P, ta, tbh, tbl, te, epi, st);
     } else {
       if (d.in_split) launch_bn<BN, 0, true>(P, ta, tbh, tbl, te, epi, st);
-      else if constexpr (BN == 32) {
-        if (two_per_sm && !g.cl) launch_bn<BN, 0, false, 2>(P, ta, tbh, tbl, te, epi, st);
+      else if constexpr (BN <= 64) {
+        if ((BN == 32 ? two_per_sm : two_per_sm64) && !g.cl) launch_bn<BN, 0, false, 2>(P, ta, tbh, tbl, te, epi, st);
         else launch_bn<BN, 0, false>(P, ta, tbh, tbl, te, epi, st);
       } else launch_bn<BN, 0, false>(P, ta, tbh, tbl, te, epi, st);
     }

@@ -100,7 +100,9 @@ struct Plan {
   static constexpr int kBudget = ((CPS == 1 ? 222 : 110) - 32 * stage_chunks<BN>()) * 1024;  // rings
   // A ring depth: halo tiles are reused for 9 K blocks; window tiles are one K block each, so
   // they need a deeper ring to cover the HBM latency (BN = 32 leaves room for 8)
-  static constexpr int kNA = (AM != 0 || ASPLIT) ? 2 : CPS == 2 ? 3 : BN == 32 ? 8 : BN == 64 ? 4 : RTE_NA128;
+  // (CPS = 2, N = 64: a single halo slot -- the other CTA on the SM covers its load latency)
+  static constexpr int kNA = (AM != 0 || ASPLIT) ? (CPS == 2 && BN == 64 ? 1 : 2)
+                             : CPS == 2 ? (BN == 64 ? 2 : 3) : BN == 32 ? 8 : BN == 64 ? 4 : RTE_NA128;
   static constexpr int kNBraw = (kBudget - kNA * kASlot) / kBSlot;
   static constexpr int kNB = kNBraw > 8 ? 8 : kNBraw;               // B ring depth
   static_assert(kNB >= 1, "shared-memory plan leaves no B slot");
@@ -281,7 +283,7 @@ __global__ void __launch_bounds__(kGemmThreads, CPS)
   static_assert(!(HALO && Epi::kCenter), "row centring is for the 1x1 (apply) kernels");
   static_assert(!(ASPLIT && Epi::kCenter), "row centring needs the plain fp32 A operand");
   static_assert(!(SSH && ASPLIT), "SS-halo kernels split the activations themselves");
-  static_assert(CPS == 1 || (CPS == 2 && BN == 32 && !ASPLIT && AM != 2), "two CTAs per SM: BN = 32 only");
+  static_assert(CPS == 1 || (CPS == 2 && BN <= 64 && !ASPLIT && AM != 2), "two CTAs per SM: BN <= 64 only");
   using PL = Plan<BN, AM, ASPLIT, CPS>;
   constexpr int TCOLS = 512 / CPS;
   constexpr int NAR = PL::kNA, NBR = PL::kNB;
