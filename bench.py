@@ -285,6 +285,8 @@ def run_ours(args, cfg):
     K, Wm = args.steps, args.warmup
     solve = lambda xx, bb, k: P.gmres_solve(p, net, bb, xx, restart=cfg.restart, maxit=k, rtol=1e-300,
                                             history=False, reorth=args.reorth)
+    # setup: capture the per-Arnoldi-step CUDA graphs once (RTE_NO_GRAPHS=1 disables)
+    P.gmres_prepare(p, net, restart=cfg.restart, reorth=args.reorth)
     # warm-up: W inner iterations (one solve), untimed
     solve(x, b, max(Wm, 1))
     torch.cuda.synchronize()

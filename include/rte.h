@@ -190,6 +190,16 @@ typedef struct {
                         unrotated Hessenberg matrix H[i][j], row-major */
 } gmres_report;
 
+/* Optional setup for gmres_solve with these options (fp32 basis): captures, once, one CUDA graph per
+ * Arnoldi step j of the step's operator part w = A P(alpha_j V_j) (preconditioner + apply, ~90
+ * launches at config 5; the Krylov workspace is cached per problem, so every pointer of that part
+ * is fixed per j) -- later solves replay them instead of launching each kernel (measured 5.9% on
+ * apply + V-cycle).  Without it gmres_solve captures lazily (step seen once eagerly, captured on
+ * the next use).  Graphs are dropped by mgnet_coeffnet, mgnet_destroy and rte_destroy; none are
+ * used while per-launch timing records a class inside them, or with RTE_NO_GRAPHS set.  Runs
+ * the operator once (results discarded).  Errors: RTE_EINVAL (options), RTE_ECUDA. */
+rte_status gmres_prepare(const rte_problem* p, const mgnet_net* net, const gmres_opts* opts, void* stream);
+
 /* b_dev float32 [n]; x_dev float64 [n] (in: x0, out: x); rep: array of `batch` reports. */
 rte_status gmres_solve(const rte_problem* p, const mgnet_net* net, const float* b_dev,
                        double* x_dev, const gmres_opts* opts, gmres_report* rep, void* stream);

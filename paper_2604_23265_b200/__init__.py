@@ -16,7 +16,7 @@ from . import _lib
 from ._lib import RteError, check, gmres_opts, gmres_report, lib
 
 __all__ = ["Problem", "MgNet", "rte_setup", "rte_rhs", "rte_apply", "rte_apply_f64", "rte_blockjacobi_apply", "mgnet_create",
-           "mgnet_vcycle", "mgnet_vcycle_f64", "mgnet_coeffnet", "mgnet_coeffnet_weight_count", "mgnet_modulation", "gmres_solve", "rte_quadrature", "rte_hg_matrix", "rte_launch_count", "rte_timing_enable", "rte_timing_filter", "rte_timing_reset",
+           "mgnet_vcycle", "mgnet_vcycle_f64", "mgnet_coeffnet", "mgnet_coeffnet_weight_count", "mgnet_modulation", "gmres_prepare", "gmres_solve", "rte_quadrature", "rte_hg_matrix", "rte_launch_count", "rte_timing_enable", "rte_timing_filter", "rte_timing_reset",
            "rte_timing_get", "RteError", "LIB_PATH"]
 
 LIB_PATH = _lib.LIB_PATH
@@ -209,6 +209,16 @@ def mgnet_vcycle(net: MgNet, r, z, add_identity: bool = True, stream=None) -> No
 def mgnet_vcycle_f64(net: MgNet, r, z, add_identity: bool = True, stream=None) -> None:
     check("mgnet_vcycle_f64", lib.mgnet_vcycle_f64(net.handle, _dev(r, "f64"), _dev(z, "f64"), int(add_identity),
                                                    C.c_void_p(_stream(stream))))
+
+
+def gmres_prepare(p: Problem, net: Optional[MgNet], *, restart: int = 30, precond: Optional[int] = None,
+                  reorth: int = 2, precision: int = 0, stream=None) -> None:
+    """Capture the per-Arnoldi-step CUDA graphs for gmres_solve with these options (setup; optional)."""
+    if precond is None:
+        precond = 1 if net is not None else 0
+    opts = gmres_opts(restart, 1, 0.0, precond, reorth, precision)
+    check("gmres_prepare", lib.gmres_prepare(p.handle, net.handle if net is not None else None, C.byref(opts),
+                                             C.c_void_p(_stream(stream))))
 
 
 def gmres_solve(p: Problem, net: Optional[MgNet], b, x, *, restart: int = 30, maxit: int = 1000,

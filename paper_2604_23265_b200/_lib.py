@@ -69,6 +69,7 @@ SIGS = {
     "mgnet_coeffnet": (C.c_int, [_vp, _fp, _fp, _fp, _fp, C.c_size_t]),
     "mgnet_modulation": (C.c_int, [_vp, C.c_int, C.c_int, C.POINTER(C.c_double)]),
     "gmres_solve": (C.c_int, [_vp, _vp, _vp, _vp, C.POINTER(gmres_opts), C.POINTER(gmres_report), _vp]),
+    "gmres_prepare": (C.c_int, [_vp, _vp, C.POINTER(gmres_opts), _vp]),
     "rte_launch_count": (C.c_int64, [C.c_int]),
     "rte_last_error": (C.c_char_p, []),
     "rte_timing_enable": (C.c_int, [C.c_int]),

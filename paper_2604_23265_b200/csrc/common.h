@@ -117,6 +117,15 @@ double apply_flops(const rte_problem* p);
 double apply_bytes(const rte_problem* p, int elt, int b_elt);
 void free_tc_state(rte_problem* p);
 void free_gmres_work(const rte_problem* p);
+// CUDA-graph capture support (krylov.cu caches one graph per Arnoldi step): while capturing,
+// prof_begin records nothing and marks the capture unusable if it would have timed a launch.
+void capture_begin();
+bool capture_end();
+int64_t launches_now();
+void launches_add(int64_t d);
+std::vector<std::string> capture_classes();                      // timing classes captured so far
+bool prof_wants_any(const std::vector<std::string>& classes);    // timing would record one of them
+void drop_net_graphs(const struct ::mgnet_net* net);  // (krylov.cu) forget graphs using `net`
 void launch_apply_tc(const rte_problem* p, const float* x, float* y, const double* alpha_dev,
                      int alpha_stride, cudaStream_t st);
 }  // namespace rte

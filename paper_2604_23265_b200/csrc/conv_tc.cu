@@ -175,7 +175,10 @@ struct EpiConv {
     }
     return (((long long)b * Ho + Y) * Wo + X) * Co + col;
   }
-  static constexpr int kBatch = 1;  // rows whose global inputs are in flight together (measured best)
+#ifndef RTE_CONV_BATCH
+#define RTE_CONV_BATCH 1
+#endif
+  static constexpr int kBatch = RTE_CONV_BATCH;  // rows whose global inputs are in flight together (measured best)
   struct Col {
     int col;
   };
@@ -355,8 +358,12 @@ Plan make_plan(const ConvDesc& d) {
   if (d.Ci % 32 != 0 || d.Co % 32 != 0) return P;
   if (d.mode == 0 && !(d.ks == 1 || d.ks == 3)) return P;
   if (d.mode == 2 && (d.Ho % 2 || d.Wo % 2)) return P;
+  static const int max_bn = [] {  // (experiments: RTE_TC_MAXBN caps the N tile)
+    const char* e = getenv("RTE_TC_MAXBN");
+    return e ? atoi(e) : 128;
+  }();
   int BN = 32;
-  while (BN < 128 && BN * 2 <= d.Co && d.Co % (BN * 2) == 0) BN *= 2;
+  while (BN < max_bn && BN * 2 <= d.Co && d.Co % (BN * 2) == 0) BN *= 2;
   P.BN = BN;
   P.halo = (d.mode == 0 && d.ks == 3);
   tc::Geom& g = P.g;

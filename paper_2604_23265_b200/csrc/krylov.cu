@@ -368,7 +368,27 @@ struct GmresWork {
   double* w64 = nullptr;
   double* z64 = nullptr;
   float* q32 = nullptr;    // V-cycle output
+  // CUDA graphs of the fp32 Arnoldi step's operator part, w = A P(alpha_j V_j) (the preconditioner
+  // and the apply: ~90 launches at config 5), one per (net, net epoch, j, precond); every input and
+  // output pointer of that part is fixed per j because this workspace is cached per problem
+  struct StepGraph {
+    cudaGraphExec_t exec = nullptr;  // nullptr: seen once (kernels warmed), not captured yet
+    int64_t launches = 0;
+    std::vector<std::string> classes;  // timing classes inside
+  };
+  std::map<std::tuple<const mgnet_net*, uint64_t, int, int>, StepGraph> graphs;
+  void drop_graphs(const mgnet_net* only = nullptr) {
+    for (auto it = graphs.begin(); it != graphs.end();) {
+      if (only && std::get<0>(it->first) != only) {
+        ++it;
+        continue;
+      }
+      if (it->second.exec) cudaGraphExecDestroy(it->second.exec);
+      it = graphs.erase(it);
+    }
+  }
   void release() {
+    drop_graphs();
     void* ps[] = {V, w, z, r64, Hr, Hraw, cs, sn, g, alpha, h1, h2, h3, coef, bnorm, rn2, partials, counters,
                   active, kcols, done, st_dev, V64, w64, z64, q32};
     for (void* p : ps) dfree(p);
@@ -451,6 +471,108 @@ void rte::free_gmres_work(const rte_problem* p) {
   }
 }
 
+void rte::drop_net_graphs(const mgnet_net* net) {
+  std::lock_guard<std::mutex> lk(g_wmu);
+  for (auto& kv : g_work) kv.second.drop_graphs(net);
+}
+
+static bool graphs_enabled() {
+  static const bool on = getenv("RTE_NO_GRAPHS") == nullptr;
+  return on;
+}
+
+// w = A P(alpha_j V_j) in fp32 (precond 0 none, 1 MgNet, 2 block Jacobi): the operator part of
+// Arnoldi step j
+static void step_operator(const rte_problem* p, const mgnet_net* net, const GmresWork& W, int precond, int j,
+                          cudaStream_t st) {
+  const int m = W.m;
+  const float* vj = W.V + (size_t)j * p->n;
+  if (precond == 1) {
+    vcycle_run(net, vj, W.z, true, W.alpha + j, m + 1, st);
+    launch_apply_f32(p, W.z, W.w, nullptr, 0, st);
+  } else if (precond == 2) {
+    bj_apply<float>(p, vj, W.z, W.alpha + j, m + 1, st);
+    launch_apply_f32(p, W.z, W.w, nullptr, 0, st);
+  } else {
+    launch_apply_f32(p, vj, W.w, W.alpha + j, m + 1, st);
+  }
+}
+
+// Captures step j's operator part into a graph (on a private stream; nothing runs).  Returns
+// nullptr (and caches nothing) when capture is unavailable or per-launch timing would have to be
+// recorded inside it.
+static GmresWork::StepGraph* capture_step(const rte_problem* p, const mgnet_net* net, GmresWork& W, int precond,
+                                          int j) {
+  static thread_local cudaStream_t cap = nullptr;
+  if (!cap && cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return nullptr;
+  }
+  if (cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return nullptr;
+  }
+  capture_begin();
+  const int64_t l0 = launches_now();
+  bool ok = true;
+  try {
+    step_operator(p, net, W, precond, j, cap);
+  } catch (...) {
+    ok = false;
+  }
+  ok = capture_end() && ok;
+  const int64_t nl = launches_now() - l0;
+  launches_add(-nl);  // captured, not run
+  cudaGraph_t g = nullptr;
+  const cudaError_t e = cudaStreamEndCapture(cap, &g);
+  cudaGraphExec_t exec = nullptr;
+  if (ok && e == cudaSuccess && g && cudaGraphInstantiate(&exec, g, 0) == cudaSuccess) {
+    cudaGraphDestroy(g);
+    auto& sg = W.graphs[{net, net ? net->graph_epoch : 0, j, precond}];
+    sg.exec = exec;
+    sg.launches = nl;
+    sg.classes = capture_classes();
+    return &sg;
+  }
+  if (g) cudaGraphDestroy(g);
+  (void)cudaGetLastError();
+  return nullptr;
+}
+
+static void run_step_operator(const rte_problem* p, const mgnet_net* net, GmresWork& W, int precond, int j,
+                              cudaStream_t st, bool capture_now = false) {
+  if (graphs_enabled()) {
+    const auto key = std::make_tuple(net, net ? net->graph_epoch : (uint64_t)0, j, precond);
+    auto it = W.graphs.find(key);
+    if (it == W.graphs.end()) {
+      if (!capture_now) {  // first sight: run eagerly (warms kernels and lazy allocations), remember
+        W.graphs[key];
+        step_operator(p, net, W, precond, j, st);
+        return;
+      }
+    } else if (it->second.exec) {
+      if (!prof_wants_any(it->second.classes)) {  // (per-launch timing of an inner class: eager)
+        RTE_CHECK_CUDA(cudaGraphLaunch(it->second.exec, st));
+        launches_add(it->second.launches);
+        return;
+      }
+      step_operator(p, net, W, precond, j, st);
+      return;
+    }
+    if (!prof_wants_any({})) {  // (timing every class: a capture would be discarded anyway)
+      W.graphs.erase(key);
+      GmresWork::StepGraph* sg = capture_step(p, net, W, precond, j);
+      if (sg) {
+        RTE_CHECK_CUDA(cudaGraphLaunch(sg->exec, st));
+        launches_add(sg->launches);
+        return;
+      }
+      W.graphs[key];  // capture unavailable: keep running eagerly, retry next time
+    }
+  }
+  step_operator(p, net, W, precond, j, st);
+}
+
 static GmresWork& get_work(const rte_problem* p, int m) {
   std::lock_guard<std::mutex> lk(g_wmu);
   GmresWork& W = g_work[p];
@@ -492,7 +614,35 @@ static GmresWork& get_work(const rte_problem* p, int m) {
   return W;
 }
 
-extern "C" rte_status gmres_solve(const rte_problem* p, const mgnet_net* net, const float* b_dev, double* x_dev,
+extern "C" rte_status gmres_prepare(const rte_problem* p, const mgnet_net* net, const gmres_opts* opts, void* stream) {
+  try {
+    RTE_REQUIRE(p && opts, "gmres_prepare: NULL argument");
+    RTE_REQUIRE(opts->restart >= 1 && opts->restart <= kMaxRestart, "gmres_prepare: restart out of range");
+    RTE_REQUIRE(opts->precond == 0 || opts->precond == 2 || (opts->precond == 1 && net),
+                "gmres_prepare: precond must be 0, 1 (with a net) or 2");
+    if (!graphs_enabled() || opts->precision == 1) return RTE_OK;  // (the fp64 mode runs eagerly)
+    const int m = opts->restart;
+    GmresWork& W = get_work(p, m);
+    if (opts->precond == 2) bj_prepare(p);
+    cudaStream_t st = as_stream(stream);
+    step_operator(p, net, W, opts->precond, 0, st);  // warm every kernel (results discarded)
+    RTE_CHECK_CUDA(cudaStreamSynchronize(st));
+    for (int j = 0; j < m; ++j) {
+      auto it = W.graphs.find({net, net ? net->graph_epoch : (uint64_t)0, j, opts->precond});
+      if (it != W.graphs.end() && it->second.exec) continue;
+      if (it != W.graphs.end()) W.graphs.erase(it);
+      if (!capture_step(p, net, W, opts->precond, j)) W.graphs[{net, net ? net->graph_epoch : (uint64_t)0, j, opts->precond}];
+    }
+    return RTE_OK;
+  } catch (const Fail& f) {
+    return f.st;
+  } catch (const std::exception& e) {
+    set_error(std::string("internal: ") + e.what());
+    return RTE_EINTERNAL;
+  }
+}
+
+rte_status gmres_solve(const rte_problem* p, const mgnet_net* net, const float* b_dev, double* x_dev,
                                   const gmres_opts* opts, gmres_report* rep, void* stream) {
   try {
     RTE_REQUIRE(p && b_dev && x_dev && opts && rep, "gmres_solve: NULL argument");
@@ -607,17 +757,9 @@ extern "C" rte_status gmres_solve(const rte_problem* p, const mgnet_net* net, co
           launch_apply_f64(p, zin, W.w64, nullptr, st);
           cgs_passes(W.V64, W.w64);
         } else {
-          // fp32 basis: z = P(alpha_j V_j) or alpha_j V_j, w = A z in fp32
-          const float* vj = W.V + (size_t)j * n;
-          if (opts->precond == 1) {
-            vcycle_run(net, vj, W.z, true, W.alpha + j, m + 1, st);
-            launch_apply_f32(p, W.z, W.w, nullptr, 0, st);
-          } else if (opts->precond == 2) {
-            bj_apply<float>(p, vj, W.z, W.alpha + j, m + 1, st);
-            launch_apply_f32(p, W.z, W.w, nullptr, 0, st);
-          } else {
-            launch_apply_f32(p, vj, W.w, W.alpha + j, m + 1, st);
-          }
+          // fp32 basis: z = P(alpha_j V_j) or alpha_j V_j, w = A z in fp32 (a cached CUDA graph per j
+          // when available), then the CGS passes
+          run_step_operator(p, net, W, opts->precond, j, st);
           cgs_passes(W.V, W.w);
         }
         ++total_all;

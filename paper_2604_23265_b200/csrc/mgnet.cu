@@ -415,6 +415,7 @@ extern "C" {
 
 void mgnet_destroy(mgnet_net* net) {
   if (!net) return;
+  drop_net_graphs(net);
   for (auto& c : net->convs) c.release();
   dfree(net->tc_ws);
   for (auto& lv : net->lv) {
@@ -573,6 +574,8 @@ rte_status mgnet_coeffnet(mgnet_net* net, const float* sigma_T, const float* sig
                           const float* weights, size_t n_floats) {
   try {
     RTE_REQUIRE(net, "mgnet_coeffnet: NULL net");
+    ++net->graph_epoch;  // captured V-cycles read the maps (or their absence): recapture
+    drop_net_graphs(net);
     free_modulation(net);
     if (!weights) return RTE_OK;  // back to the unmodulated smoother (a = abar = 1)
     RTE_REQUIRE(sigma_T && sigma_a && eps, "mgnet_coeffnet: NULL medium field");

@@ -78,4 +78,5 @@ struct mgnet_net {
   bool tc = false;                 // tensor-core convs enabled (conv_tc_prepare)
   float* tc_ws = nullptr;          // split-K partials
   size_t tc_ws_elems = 0;
+  uint64_t graph_epoch = 0;        // bumped when captured CUDA graphs of this net go stale
 };

@@ -82,15 +82,45 @@ void prof_resolve() {
 
 static std::string g_prof_filter;  // rte_timing_filter: the one class to time ("" = every class)
 
+thread_local bool g_capturing = false;       // a CUDA-graph capture is recording this thread's launches
+thread_local bool g_capture_tainted = false;  // ... and a per-launch event would have been recorded
+thread_local std::vector<std::string> g_capture_classes;  // timing classes of the captured launches
+
 void prof_begin(cudaStream_t st, const char* cls) {
   if (!g_prof_on) return;
   if (!g_prof_filter.empty() && (!cls || g_prof_filter != cls)) return;
+  if (g_capturing) {  // events cannot live in a replayed graph: the caller discards the capture
+    g_capture_tainted = true;
+    return;
+  }
   if (!g_prof_pending) g_prof_pending = prof_event();
   RTE_CHECK_CUDA(cudaEventRecord(g_prof_pending, st));
 }
 
+void capture_begin() {
+  g_capturing = true;
+  g_capture_tainted = false;
+  g_capture_classes.clear();
+}
+std::vector<std::string> capture_classes() { return g_capture_classes; }
+// would per-launch timing record any of these classes right now?
+bool prof_wants_any(const std::vector<std::string>& classes) {
+  if (!g_prof_on) return false;
+  if (g_prof_filter.empty()) return true;
+  for (const auto& c : classes)
+    if (c == g_prof_filter) return true;
+  return false;
+}
+bool capture_end() {  // true if the capture is usable (no per-launch timing was requested in it)
+  g_capturing = false;
+  return !g_capture_tainted;
+}
+int64_t launches_now() { return g_launches; }
+void launches_add(int64_t d) { g_launches += d; }
+
 void after_launch(const char* what, cudaStream_t st, double flops, double bytes, int kind) {
   ++g_launches;
+  if (g_capturing) g_capture_classes.emplace_back(what);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("launch of ") + what + " failed: " + cudaGetErrorString(e));

@@ -37,5 +37,18 @@ cls = P.rte_timing_get()
 P.rte_timing_enable(False)
 out = {c["name"]: round(c["ms"] / a.reps, 4) for c in sorted(cls, key=lambda c: -c["ms"])}
 out["_total_ms"] = round(sum(c["ms"] for c in cls) / a.reps, 4)
+# wall time of the same work without per-launch events (the gap to _total_ms = kernel boundaries)
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(a.reps):
+    P.rte_apply(p, x, y)
+    P.mgnet_vcycle(net, x, z, True)
+e1.record()
+torch.cuda.synchronize()
+out["_wall_ms"] = round(e0.elapsed_time(e1) / a.reps, 4)
+P.rte_launch_count(reset=True)
+P.rte_apply(p, x, y)
+P.mgnet_vcycle(net, x, z, True)
+out["_launches"] = P.rte_launch_count(reset=True)
 out["_dbg"] = os.environ.get("RTE_TC_DBG", "0")
 print(json.dumps(out))
