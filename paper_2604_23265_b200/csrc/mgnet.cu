@@ -200,16 +200,19 @@ const char* conv_class_name(const ConvDesc& d, bool tc) {
 constexpr int kSmallKMaxCi = 32;  // (static shared memory: 32 KB weights + 8 KB inputs)
 // (out and addend may be the same array: every element is read, then written, by one thread in
 // one iteration, so __restrict__ only lets the compiler batch the loads of different pixels)
+template <int TCO>  // output channels = TCO (64, 128 or 256): the weight block is contiguous
 __global__ void __launch_bounds__(512, 2) conv1x1_smallk_kernel(int npix, int Ci, int Co, const float* __restrict__ in,
                                                              const float* __restrict__ Wk, float* __restrict__ out,
                                                              const float* __restrict__ addend, float sign,
                                                              const double* __restrict__ alpha, int alpha_stride,
                                                              int alpha_on_input, int alpha_on_addend) {
-  constexpr int TPX = 64, TCO = 256;
+  constexpr int TPX = 16384 / TCO;       // pixels per block: every block writes 64 KB (4 per thread)
+  constexpr int TXN = TCO / 8;           // threads along channels (8 channels each)
+  constexpr int PPT = TPX * TXN / 512;   // pixels per thread (= 4)
   __shared__ __align__(128) float Ws[kSmallKMaxCi][TCO];  // [ci][co]
   __shared__ __align__(128) float Us[TPX][kSmallKMaxCi];  // [pixel][ci] at pitch Ci (the input's layout)
   __shared__ __align__(8) uint64_t bar;
-  const int tid = threadIdx.x, tx = tid % 32, ty = tid / 32;  // 8 channels x 4 pixels per thread
+  const int tid = threadIdx.x, tx = tid % TXN, ty = tid / TXN;  // 8 channels x PPT pixels per thread
   const int b = blockIdx.z;
   const int co0 = blockIdx.y * TCO;
   const int64_t p0 = (int64_t)blockIdx.x * TPX;
@@ -244,32 +247,35 @@ __global__ void __launch_bounds__(512, 2) conv1x1_smallk_kernel(int npix, int Ci
         "@!p bra W_%=;\n\t}" ::"r"(sb)
         : "memory");
   }
-  float acc[4][8];
+  float acc[PPT][8];
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int a = 0; a < PPT; ++a)
 #pragma unroll
     for (int c = 0; c < 8; ++c) acc[a][c] = 0.f;
   for (int k = 0; k < Ci; ++k) {
     const float4 w0 = *reinterpret_cast<const float4*>(&Ws[k][tx * 8]);
     const float4 w1 = *reinterpret_cast<const float4*>(&Ws[k][tx * 8 + 4]);
-    const float* uc = &Us[0][0] + ty * 4 * Ci + k;  // [pixel][ci] at pitch Ci (as copied)
-    const float uv[4] = {uc[0], uc[Ci], uc[2 * Ci], uc[3 * Ci]};
+    const float* uc = &Us[0][0] + ty * PPT * Ci + k;  // [pixel][ci] at pitch Ci (as copied)
+    float uv[PPT];
+#pragma unroll
+    for (int a = 0; a < PPT; ++a) uv[a] = uc[a * Ci];
     const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < PPT; ++a)
 #pragma unroll
       for (int c = 0; c < 8; ++c) acc[a][c] = fmaf(uv[a], wv[c], acc[a][c]);
   }
   const float al = alpha ? (float)alpha[(int64_t)b * alpha_stride] : 1.f;
   const float s_in = (alpha_on_input ? al : 1.f) * sign;
   const float s_add = alpha_on_addend ? al : 1.f;
-  // the addend loads of two pixels are issued before their stores
+  // the addend loads of (up to) two pixels are issued before their stores
+  constexpr int PB = PPT < 2 ? PPT : 2;
 #pragma unroll
-  for (int a0 = 0; a0 < 4; a0 += 2) {
-    float4 ad[2][2];
+  for (int a0 = 0; a0 < PPT; a0 += PB) {
+    float4 ad[PB][2];
 #pragma unroll
-    for (int a = 0; a < 2; ++a) {
-      const int64_t p = p0 + ty * 4 + a0 + a;
+    for (int a = 0; a < PB; ++a) {
+      const int64_t p = p0 + ty * PPT + a0 + a;
       const int64_t o = ((int64_t)b * npix + p) * Co + co0 + tx * 8;
       ad[a][0] = ad[a][1] = make_float4(0.f, 0.f, 0.f, 0.f);
       if (addend && p < npix) {
@@ -278,8 +284,8 @@ __global__ void __launch_bounds__(512, 2) conv1x1_smallk_kernel(int npix, int Ci
       }
     }
 #pragma unroll
-    for (int a = 0; a < 2; ++a) {
-      const int64_t p = p0 + ty * 4 + a0 + a;
+    for (int a = 0; a < PB; ++a) {
+      const int64_t p = p0 + ty * PPT + a0 + a;
       if (p >= npix) continue;
       const int64_t o = ((int64_t)b * npix + p) * Co + co0 + tx * 8;
       const float* r = acc[a0 + a];
@@ -294,8 +300,9 @@ __global__ void __launch_bounds__(512, 2) conv1x1_smallk_kernel(int npix, int Ci
 }
 
 bool conv1x1_smallk_ok(const ConvDesc& d) {
-  // (Co == 256: the weight block [ci][co0 .. co0+255] is contiguous for the bulk copy)
-  return d.mode == 0 && d.ks == 1 && d.Ci <= kSmallKMaxCi && d.Ci % 4 == 0 && d.Co == 256 && !d.in_split && !d.mod &&
+  // (Co = 64, 128 or 256, one channel tile: the weight block [ci][0 .. Co) is contiguous for the bulk copy)
+  return d.mode == 0 && d.ks == 1 && d.Ci <= kSmallKMaxCi && d.Ci % 4 == 0 &&
+         (d.Co == 64 || d.Co == 128 || d.Co == 256) && !d.in_split && !d.mod &&
          !d.out_split && getenv("RTE_NO_SMALLK") == nullptr;
 }
 
@@ -307,10 +314,16 @@ void launch_conv_t(const ConvDesc& d, const T* in, const T* Wk, T* out, const T*
     if (conv1x1_smallk_ok(d)) {
       prof_begin(st, conv_class_name(d, false));
       const int npix = d.Ho * d.Wo;
-      const unsigned bx = (unsigned)((npix + 63) / 64);
-      conv1x1_smallk_kernel<<<dim3(bx, (unsigned)(d.Co / 256), (unsigned)d.B), 512, 0, st>>>(
-          npix, d.Ci, d.Co, in, Wk, out, addend, sign, alpha, alpha_stride, alpha_on_input ? 1 : 0,
-          alpha_on_addend ? 1 : 0);
+      const unsigned bx = (unsigned)((npix + 16384 / d.Co - 1) / (16384 / d.Co));
+      auto go = [&](auto tco_tag) {
+        constexpr int TCO = decltype(tco_tag)::value;
+        conv1x1_smallk_kernel<TCO><<<dim3(bx, 1, (unsigned)d.B), 512, 0, st>>>(
+            npix, d.Ci, d.Co, in, Wk, out, addend, sign, alpha, alpha_stride, alpha_on_input ? 1 : 0,
+            alpha_on_addend ? 1 : 0);
+      };
+      if (d.Co == 256) go(std::integral_constant<int, 256>{});
+      else if (d.Co == 128) go(std::integral_constant<int, 128>{});
+      else go(std::integral_constant<int, 64>{});
       after_launch(conv_class_name(d, false), st, conv_flops(d), conv_bytes(d, addend != nullptr), 2);
       return;
     }
