@@ -6,6 +6,8 @@
 //                   - (|s_m|/h) psi_{j-sgn s_m,i,m} - sigma_s sum_n S_mn psi_{jin}
 // Layout psi[b][j][i][m]; the scattering term is the GEMM  Psi[cells x M] . S^T[M x M], computed
 // in the conservation-preserving form S psi = c + S (psi - c), c = psi_{cell, m=0} (apply_tc.cu).
+#include <type_traits>
+
 #include "common.h"
 
 namespace rte {
@@ -230,6 +232,119 @@ __global__ void __launch_bounds__(256) apply_simt_wide_kernel(
   }
 }
 
+// fp64 apply on the DMMA pipe (mma.sync m8n8k4 f64: measured 37 TF/s on the B200 vs 36 for SIMT
+// DFMA, scripts/fp64_bench.cu), M % 64 == 0.  Block = 128 cells x 64 ordinates, 8 warps, warp tile
+// 32 x 32 = 4 x 4 MMA tiles (32 fp64 accumulators per thread, so several blocks per SM); K in
+// chunks of 8 through double-buffered shared memory: A[k][cell] = psi - c (centred, as the other
+// paths), B[k][m] = S^T.  Fragments (PTX m8n8k4 .f64): A row = lane/4, k = lane%4; B k = lane%4,
+// col = lane/4; C row = lane/4, cols 2(lane%4) + {0, 1}.  Same epilogue as apply_simt_kernel.
+__global__ void __launch_bounds__(256) apply_dmma_kernel(
+    int N, int M, const double* __restrict__ x, double* __restrict__ y, const double* __restrict__ St,
+    const double* __restrict__ sig_t, const double* __restrict__ sig_s, const double* __restrict__ axv,
+    const double* __restrict__ ayv, const int8_t* __restrict__ sgx, const int8_t* __restrict__ sgy,
+    const float* __restrict__ bvec) {
+  constexpr int TP = 128, TM = 64, KC = 8, PA = TP + 4, PB = TM + 4;
+  __shared__ __align__(16) double As[2][KC][PA];
+  __shared__ __align__(16) double Bs[2][KC][PB];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp & 3, wn = warp >> 2;  // warp tile: cells wm*32.., ordinates wn*32..
+  const int bsample = blockIdx.z;
+  const int64_t cells = (int64_t)N * N;
+  const int64_t c0 = (int64_t)blockIdx.x * TP;
+  const int m0 = blockIdx.y * TM;
+  const double* xs = x + (int64_t)bsample * cells * M;
+  const double* Sts = St + (int64_t)bsample * M * M;
+  // staging: A chunk 128 cells x 8 k (4 per thread: cell tid/8 + 32 r, k tid%8),
+  // B chunk 8 k x 64 ordinates (2 per thread)
+  const int a_cl = tid >> 3, a_k = tid & 7;
+  double ctr[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int64_t cell = c0 + a_cl + 32 * r;
+    ctr[r] = cell < cells ? xs[cell * M] : 0.0;
+  }
+  double ra[4], rb[2];
+  auto load_chunk = [&](int k0) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int64_t cell = c0 + a_cl + 32 * r;
+      ra[r] = cell < cells ? xs[cell * M + k0 + a_k] - ctr[r] : 0.0;
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int e = tid + 256 * r, kk = e / TM, o = e % TM;
+      rb[r] = Sts[(int64_t)(k0 + kk) * M + m0 + o];
+    }
+  };
+  auto store_chunk = [&](int buf) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) As[buf][a_k][a_cl + 32 * r] = ra[r];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int e = tid + 256 * r;
+      Bs[buf][e / TM][e % TM] = rb[r];
+    }
+  };
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  load_chunk(0);
+  store_chunk(0);
+  __syncthreads();
+  int buf = 0;
+  const int fr = lane >> 2, fk = lane & 3;
+  for (int k0 = 0; k0 < M; k0 += KC) {
+    const bool more = k0 + KC < M;
+    if (more) load_chunk(k0 + KC);
+#pragma unroll
+    for (int ks = 0; ks < KC; ks += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = As[buf][ks + fk][wm * 32 + 8 * i + fr];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = Bs[buf][ks + fk][wn * 32 + 8 * j + fr];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                       : "+d"(acc[i][j][0]), "+d"(acc[i][j][1])
+                       : "d"(af[i]), "d"(bf[j]));
+    }
+    if (more) {
+      store_chunk(buf ^ 1);
+      __syncthreads();
+      buf ^= 1;
+    }
+  }
+  // epilogue: stencil + diagonal - sigma_s * (c + S (psi - c))
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t cell = c0 + wm * 32 + 8 * i + fr;
+    if (cell >= cells) continue;
+    const int ci = (int)(cell % N), cj = (int)(cell / N);
+    const int64_t gcell = (int64_t)bsample * cells + cell;
+    const double st = sig_t[gcell], ss = sig_s[gcell];
+    const double cc = xs[cell * M];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int m = m0 + wn * 32 + 8 * j + 2 * fk + h;
+        const double ax = axv[m], ay = ayv[m];
+        double v = (ax + ay + st) * xs[cell * M + m] - ss * (cc + acc[i][j][h]);
+        const int ii = ci - sgx[m], jj = cj - sgy[m];
+        if (ii >= 0 && ii < N) v -= ax * xs[(cell - sgx[m]) * M + m];
+        if (jj >= 0 && jj < N) v -= ay * xs[(cell - (int64_t)sgy[m] * N) * M + m];
+        const int64_t o = gcell * M + m;
+        if (bvec) v = (double)bvec[o] - v;
+        y[o] = v;
+      }
+  }
+}
+
 template <typename T>
 void launch_simt(const rte_problem* p, const T* x, T* y, const T* St, const T* st, const T* ss,
                  const T* ax, const T* ay, const float* b, const double* alpha, int alpha_stride,
@@ -242,6 +357,13 @@ void launch_simt(const rte_problem* p, const T* x, T* y, const T* St, const T* s
     apply_simt_kernel<T, TMO><<<grid, 256, 0, stream>>>(p->N, p->M, x, y, St, st, ss, ax, ay, p->sgx, p->sgy,
                                                          b, alpha, alpha_stride);
   };
+  if constexpr (std::is_same<T, double>::value) {
+    if (p->M % 64 == 0 && alpha == nullptr && getenv("RTE_NO_DMMA") == nullptr) {
+      dim3 grid((unsigned)((cells + 127) / 128), (unsigned)(p->M / 64), (unsigned)p->B);
+      apply_dmma_kernel<<<grid, 256, 0, stream>>>(p->N, p->M, x, y, St, st, ss, ax, ay, p->sgx, p->sgy, b);
+      return;
+    }
+  }
   if (p->M % 128 == 0) {
     dim3 grid((unsigned)((cells + 127) / 128), (unsigned)(p->M / 128), (unsigned)p->B);
     apply_simt_wide_kernel<T><<<grid, 256, 0, stream>>>(p->N, p->M, x, y, St, st, ss, ax, ay, p->sgx, p->sgy, b,
