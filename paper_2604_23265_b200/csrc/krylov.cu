@@ -362,7 +362,8 @@ struct GmresWork {
   unsigned* counters = nullptr;
   int *active = nullptr, *kcols = nullptr, *done = nullptr;
   Status* st_dev = nullptr;
-  Status* st_host = nullptr;  // pinned
+  Status* st_host = nullptr;  // pinned, 2 slots of B (the step statuses are read one step late)
+  cudaEvent_t st_ev[2] = {nullptr, nullptr};  // slot copies done
   // fp64-basis mode (gmres_opts.precision = 1), allocated on first use
   double* V64 = nullptr;   // (m+1) x n
   double* w64 = nullptr;
@@ -393,6 +394,8 @@ struct GmresWork {
                   active, kcols, done, st_dev, V64, w64, z64, q32};
     for (void* p : ps) dfree(p);
     if (st_host) cudaFreeHost(st_host);
+    for (auto& e : st_ev)
+      if (e) cudaEventDestroy(e);
     *this = GmresWork();
   }
 };
@@ -610,7 +613,8 @@ static GmresWork& get_work(const rte_problem* p, int m) {
   W.st_dev = dalloc<Status>(B);
   RTE_CHECK_CUDA(cudaMemset(W.counters, 0, sizeof(unsigned) * B));
   RTE_CHECK_CUDA(cudaMemset(W.Hraw, 0, sizeof(double) * B * (m + 1) * m));
-  RTE_CHECK_CUDA(cudaHostAlloc(&W.st_host, sizeof(Status) * B, cudaHostAllocDefault));
+  RTE_CHECK_CUDA(cudaHostAlloc(&W.st_host, sizeof(Status) * 2 * B, cudaHostAllocDefault));
+  for (auto& e : W.st_ev) RTE_CHECK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   return W;
 }
 
@@ -716,6 +720,24 @@ rte_status gmres_solve(const rte_problem* p, const mgnet_net* net, const float* 
         }
       }
       if (n_active == 0) break;
+      int pending = -1;  // step whose status has not been read yet
+      // read step k's statuses (slot k & 1): history, counts, breakdown; returns the active count
+      auto process_step = [&](int k) -> int {
+        RTE_CHECK_CUDA(cudaEventSynchronize(W.st_ev[k & 1]));
+        const Status* slot = W.st_host + (size_t)(k & 1) * B;
+        int still = 0;
+        for (int b = 0; b < B; ++b) {
+          const Status& s = slot[b];
+          bool was_active = (s.active || s.kcols == k + 1);
+          if (!was_active) continue;
+          if (rep[b].history) rep[b].history[total[b]] = s.est;
+          ++total[b];
+          est_last[b] = s.est;
+          if (s.breakdown) brk[b] = 1;
+          if (s.active) ++still;
+        }
+        return still;
+      };
       for (int j = 0; j < m; ++j) {
         // Arnoldi step j: w = A P(alpha_j V_j), then CGS passes against V_0..V_j (basis type TB)
         const double* h2 = nullptr;
@@ -769,20 +791,28 @@ rte_status gmres_solve(const rte_problem* p, const mgnet_net* net, const float* 
                                                     first_cycle ? 1 : 0, W.cs, W.sn, W.g, W.alpha, m + 1, W.bnorm,
                                                     opts->rtol, last, W.active, W.kcols, W.st_dev);
         after_launch("givens", st);
-        RTE_CHECK_CUDA(cudaMemcpyAsync(W.st_host, W.st_dev, sizeof(Status) * B, cudaMemcpyDeviceToHost, st));
-        RTE_CHECK_CUDA(cudaStreamSynchronize(st));
-        int still = 0;
-        for (int b = 0; b < B; ++b) {
-          const Status& s = W.st_host[b];
-          bool was_active = (s.active || s.kcols == j + 1);
-          if (!was_active) continue;
-          if (rep[b].history) rep[b].history[total[b]] = s.est;
-          ++total[b];
-          est_last[b] = s.est;
-          if (s.breakdown) brk[b] = 1;
-          if (s.active) ++still;
+        // The step's status is read one step late: step j + 1 is enqueued before the host waits for
+        // step j, so the GPU never idles on the host round trip.  When step j turns out to have
+        // stopped every sample, the already queued step j + 1 is gated out on the device (its CGS
+        // passes and Givens rotation skip inactive samples; the operator part writes scratch only).
+        RTE_CHECK_CUDA(cudaMemcpyAsync(W.st_host + (size_t)(j & 1) * B, W.st_dev, sizeof(Status) * B,
+                                       cudaMemcpyDeviceToHost, st));
+        RTE_CHECK_CUDA(cudaEventRecord(W.st_ev[j & 1], st));
+        if (pending >= 0 && process_step(pending) == 0) {
+          pending = -1;
+          --total_all;  // (step j was queued but did no work: it does not count toward maxit)
+          break;
         }
-        if (still == 0) break;
+        pending = j;
+        if (last) {  // the budget ends here: nothing more to enqueue, read this step now
+          process_step(j);
+          pending = -1;
+          break;
+        }
+      }
+      if (pending >= 0) {
+        process_step(pending);
+        pending = -1;
       }
       if (first_cycle) {
         for (int b = 0; b < B; ++b)
