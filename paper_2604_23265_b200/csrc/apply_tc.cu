@@ -100,7 +100,7 @@ void launch_apply_bn(const Geom& g, int mtiles, const CUtensorMap& ta, const CUt
   constexpr int smem = gemm_smem_bytes<BN, 0, false>();
   ensure_smem((const void*)kern, smem);
   const int grid = std::min(mtiles * g.ntiles, num_sms());
-  kern<<<grid, kGemmThreads, smem, st>>>(ta, tbh, tbl, te, g, epi);
+  launch_gemm(kern, grid, smem, st, ta, tbh, tbl, te, g, epi);
 }
 
 }  // namespace tc

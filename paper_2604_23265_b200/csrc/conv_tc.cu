@@ -494,7 +494,7 @@ void launch_bn(const Plan& P, const CUtensorMap& ta, const CUtensorMap& tbh, con
     return;
   }
   const int grid = (int)std::min<long long>(units, (long long)CPS * num_sms());
-  kern<<<grid, tc::kGemmThreads, smem, st>>>(ta, tbh, tbl, te, P.g, epi);
+  tc::launch_gemm(kern, grid, smem, st, ta, tbh, tbl, te, P.g, epi);
 }
 
 }  // namespace

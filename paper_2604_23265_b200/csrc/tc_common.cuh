@@ -45,6 +45,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// ---- programmatic dependent launch: a kernel's prologue overlaps the previous kernel's tail ----
+// (launched with cudaLaunchAttributeProgrammaticStreamSerialization; see tc::launch_gemm)
+__device__ __forceinline__ void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ---- thread-block clusters (split-K reduction through distributed shared memory) ----
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;

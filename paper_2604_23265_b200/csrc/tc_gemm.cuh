@@ -38,6 +38,26 @@ namespace rte {
 namespace tc {
 
 constexpr int kGemmThreads = 448;   // 14 warps (see above)
+
+// Launches a GEMM kernel with programmatic dependent launch (PDL: its prologue overlaps the previous
+// kernel's tail; the kernel waits at griddepcontrol.wait before reading dependent data).
+// RTE_NO_PDL=1 launches plainly.
+template <typename K, typename... Args>
+void launch_gemm(K kern, int grid, int smem, cudaStream_t st, Args... args) {
+  static const bool pdl = getenv("RTE_NO_PDL") == nullptr;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid, 1, 1);
+  cfg.blockDim = dim3(kGemmThreads, 1, 1);
+  cfg.dynamicSmemBytes = (size_t)smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  RTE_CHECK_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
+}
+
 constexpr int kPromoteKB = 4;       // K blocks per TMEM accumulation group
 constexpr int kTileM = 128;
 constexpr int kABytes = kTileM * 128;   // 128 rows x 32 fp32
@@ -364,12 +384,18 @@ __global__ void __launch_bounds__(kGemmThreads, CPS)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  // PDL: the next kernel in the stream may start its prologue as SMs free up; it waits for this
+  // grid's completion (and memory) at its own griddepcontrol.wait before reading our outputs
+  if (threadIdx.x == 0) griddep_launch_dependents();
   const uint32_t tmem = *tmem_slot;
   const uint32_t tmem_x = tmem + 2 * BN;  // split form only
   const uint32_t tmem_a = tmem + tmem_acc_cols<BN, TCOLS>();
 
   if (warp == 0) {
     // ===== TMA producer: the whole warp walks the pipeline, one elected lane issues =====
+    // every read of the previous kernel's outputs is causally after this wait (the A/B tiles here;
+    // the epilogue's addend and maps through the pipeline barriers); a no-op without PDL
+    griddep_wait();
     int as = 0, bs = 0;
     uint32_t aph = 0, bph = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {

@@ -17,8 +17,9 @@ CUtensorMap make_map_act(const float* base, int C, int W, int H, int B, int box_
 // 5-D map over a pre-split activation [B][2][H][W][C] (plane 0 hi, plane 1 lo), dims
 // (C, W, H, plane, B), same boxes as make_map_act with a plane extent of 1.
 CUtensorMap make_map_act_split(const float* base, int C, int W, int H, int B, int box_w, int box_h, int es);
-// 2-D map over a row-major fp32 matrix [rows][K] (K contiguous), SWIZZLE_128B, box (32, box_rows).
+// L2-prefetch map (no swizzle, no shared-memory destination) over NHWC [B][H][W][C], box (box_c, box_w, box_h, 1).
 CUtensorMap make_map_prefetch(const float* base, int C, int W, int H, int B, int box_c, int box_w, int box_h);
+// 2-D map over a row-major fp32 matrix [rows][K] (K contiguous), SWIZZLE_128B, box (32, box_rows).
 CUtensorMap make_map_kmajor(const float* base, int K, int rows, int box_rows);
 
 // Host 3xTF32 split (round-to-nearest, ties away -- the same rule as cvt.rna.tf32.f32).
