@@ -324,7 +324,8 @@ void launch_conv_t(const ConvDesc& d, const T* in, const T* Wk, T* out, const T*
       if (d.Co == 256) go(std::integral_constant<int, 256>{});
       else if (d.Co == 128) go(std::integral_constant<int, 128>{});
       else go(std::integral_constant<int, 64>{});
-      after_launch(conv_class_name(d, false), st, conv_flops(d), conv_bytes(d, addend != nullptr), 2);
+      // (bound: HBM -- it streams the M-wide output and addend; its flops are a fraction of the ALU peak)
+      after_launch(conv_class_name(d, false), st, conv_flops(d), conv_bytes(d, addend != nullptr), 0);
       return;
     }
     if (conv_tc_try(d, in, out, addend, sign, alpha, alpha_stride, alpha_on_input, alpha_on_addend, st)) return;
