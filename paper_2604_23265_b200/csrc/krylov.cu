@@ -146,15 +146,39 @@ __global__ void __launch_bounds__(kThreads, 1) cgs_kernel(
 template <typename T, typename TO>
 __global__ void __launch_bounds__(kThreads) norm_kernel(const T* __restrict__ x, TO* __restrict__ xo, int64_t ns,
                                                          RedArgs ra) {
+  // 4 elements per thread per trip, all loads issued first (bytes in flight for the HBM stream;
+  // ns % 4 == 0 since M % 4 == 0)
   const int b = blockIdx.y;
   double acc[1] = {0.0};
   const T* xb = x + (int64_t)b * ns;
-  for (int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x; e < ns; e += (int64_t)ra.nblk * kThreads) {
-    double v = (double)xb[e];
-    acc[0] += v * v;
-    if (xo) xo[(int64_t)b * ns + e] = (TO)v;
+  TO* xob = xo ? xo + (int64_t)b * ns : nullptr;
+  const int64_t n4 = ns / 4;
+  for (int64_t q = (int64_t)blockIdx.x * kThreads + threadIdx.x; q < n4; q += (int64_t)ra.nblk * kThreads) {
+    double v[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = (double)xb[4 * q + i];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[0] += v[i] * v[i];
+    if (xob)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) xob[4 * q + i] = (TO)v[i];
   }
   reduce_finalize<1>(acc, ra, b, nullptr, 0);
+}
+
+// acc += sum_{u < U} cs[i+u] V_{i+u}[q]: all U 16-byte loads issued before the first FMA.
+template <int U, typename T, typename VT, int W>
+__device__ __forceinline__ void combine_cols(double (&acc)[W], const T* __restrict__ Vb, int64_t vld, int64_t q,
+                                             const double* cs, int i) {
+  VT v[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) v[u] = __ldg(reinterpret_cast<const VT*>(Vb + (int64_t)(i + u) * vld) + q);
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const T* x = reinterpret_cast<const T*>(&v[u]);
+#pragma unroll
+    for (int e = 0; e < W; ++e) acc[e] += cs[i + u] * (double)x[e];
+  }
 }
 
 // dst = sum_{i < k_b} coef_i V_i   (coef already includes alpha), fp64 accumulation; 16-byte
@@ -164,6 +188,7 @@ __global__ void __launch_bounds__(kThreads) combine_kernel(const T* __restrict__
                                                             const double* __restrict__ coef, int coef_ld,
                                                             const int* __restrict__ kcols, TO* __restrict__ dst,
                                                             int64_t ns, int nblk) {
+  static_assert(sizeof(TO) == sizeof(T), "combine stores in the basis type");
   using VT = typename Vec16<T>::type;
   constexpr int W = (int)(sizeof(VT) / sizeof(T));
   const int b = blockIdx.y;
@@ -178,26 +203,17 @@ __global__ void __launch_bounds__(kThreads) combine_kernel(const T* __restrict__
 #pragma unroll
     for (int e = 0; e < W; ++e) acc[e] = 0.0;
     int i = 0;
-    for (; i + 4 <= k; i += 4) {  // four columns in flight per thread
-      VT v[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) v[u] = reinterpret_cast<const VT*>(Vb + (int64_t)(i + u) * vld)[q];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const T* x = reinterpret_cast<const T*>(&v[u]);
-#pragma unroll
-        for (int e = 0; e < W; ++e) acc[e] += cs[i + u] * (double)x[e];
-      }
+    for (; i + 8 <= k; i += 8) combine_cols<8, T, VT, W>(acc, Vb, vld, q, cs, i);  // 8 columns in flight
+    if (i + 4 <= k) {
+      combine_cols<4, T, VT, W>(acc, Vb, vld, q, cs, i);
+      i += 4;
     }
-    for (; i < k; ++i) {
-      const VT v = reinterpret_cast<const VT*>(Vb + (int64_t)i * vld)[q];
-      const T* x = reinterpret_cast<const T*>(&v);
+    for (; i < k; ++i) combine_cols<1, T, VT, W>(acc, Vb, vld, q, cs, i);
+    VT o;  // TO == T at every call site: one 16-byte store
+    T* ov = reinterpret_cast<T*>(&o);
 #pragma unroll
-      for (int e = 0; e < W; ++e) acc[e] += cs[i] * (double)x[e];
-    }
-    TO* d = dst + (int64_t)b * ns + q * W;
-#pragma unroll
-    for (int e = 0; e < W; ++e) d[e] = (TO)acc[e];
+    for (int e = 0; e < W; ++e) ov[e] = (T)acc[e];
+    reinterpret_cast<VT*>(dst + (int64_t)b * ns)[q] = o;
   }
 }
 
@@ -207,9 +223,17 @@ __global__ void axpy64_kernel(double* __restrict__ x, const TZ* __restrict__ z, 
                               const int* __restrict__ kcols, int64_t ns, int nblk) {
   const int b = blockIdx.y;
   if (kcols[b] <= 0) return;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < ns; e += (int64_t)nblk * blockDim.x) {
-    const int64_t o = (int64_t)b * ns + e;
-    x[o] += (double)z[o] + (q ? (double)q[o] : 0.0);
+  const int64_t n4 = ns / 4;  // 4 elements per thread per trip, loads first
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n4; e += (int64_t)nblk * blockDim.x) {
+    const int64_t o = (int64_t)b * ns + 4 * e;
+    double xv[4], zv[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      xv[i] = x[o + i];
+      zv[i] = (double)z[o + i] + (q ? (double)q[o + i] : 0.0);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) x[o + i] = xv[i] + zv[i];
   }
 }
 
