@@ -176,6 +176,9 @@ typedef struct {
                         iterate, reductions and restart residual;  1 = everything in float64 (basis,
                         apply, V-cycle on SIMT kernels): for tight tolerances and iteration-count
                         parity with an fp64 reference; not the fast path */
+  int x0_zero;       /* 1 = the initial guess is zero: x is set to 0 by the call (its contents are not
+                        read) and the first restart residual is b itself, so A x0 is not applied (same
+                        result bits as passing x0 = 0 with x0_zero = 0); 0 = x holds x0 on entry */
 } gmres_opts;
 
 typedef struct {
@@ -203,6 +206,17 @@ rte_status gmres_prepare(const rte_problem* p, const mgnet_net* net, const gmres
 /* b_dev float32 [n]; x_dev float64 [n] (in: x0, out: x); rep: array of `batch` reports. */
 rte_status gmres_solve(const rte_problem* p, const mgnet_net* net, const float* b_dev,
                        double* x_dev, const gmres_opts* opts, gmres_report* rep, void* stream);
+
+/* gmres_solve with HOST buffers (the end-to-end call): b_host float32 [n], x_host float64 [n]
+ * (in: x0 unless opts->x0_zero, out: x); page-locked memory gives full-rate copies, pageable works.
+ * b (and x0) are copied into problem-owned device buffers on `stream` (allocated on the first call,
+ * 12 B per unknown, freed by rte_destroy); x is copied back as soon as the host knows the last cycle
+ * has ended (budget spent, or every sample's Arnoldi estimate converged or broke down), on an
+ * internal copy stream overlapping the closing fp64 true-residual apply -- if that residual starts
+ * another cycle, x is copied again at exit.  Returns after x_host and rep are written.  Errors: as
+ * gmres_solve. */
+rte_status gmres_solve_host(const rte_problem* p, const mgnet_net* net, const float* b_host, double* x_host,
+                            const gmres_opts* opts, gmres_report* rep, void* stream);
 
 /* Kernel launches issued by this thread since the last call (reset to 0). */
 int64_t rte_launch_count(int reset);

@@ -16,7 +16,7 @@ from . import _lib
 from ._lib import RteError, check, gmres_opts, gmres_report, lib
 
 __all__ = ["Problem", "MgNet", "rte_setup", "rte_rhs", "rte_apply", "rte_apply_f64", "rte_blockjacobi_apply", "mgnet_create",
-           "mgnet_vcycle", "mgnet_vcycle_f64", "mgnet_coeffnet", "mgnet_coeffnet_weight_count", "mgnet_modulation", "gmres_prepare", "gmres_solve", "rte_quadrature", "rte_hg_matrix", "rte_launch_count", "rte_timing_enable", "rte_timing_filter", "rte_timing_reset",
+           "mgnet_vcycle", "mgnet_vcycle_f64", "mgnet_coeffnet", "mgnet_coeffnet_weight_count", "mgnet_modulation", "gmres_prepare", "gmres_solve", "gmres_solve_host", "rte_quadrature", "rte_hg_matrix", "rte_launch_count", "rte_timing_enable", "rte_timing_filter", "rte_timing_reset",
            "rte_timing_get", "RteError", "LIB_PATH"]
 
 LIB_PATH = _lib.LIB_PATH
@@ -221,17 +221,26 @@ def gmres_prepare(p: Problem, net: Optional[MgNet], *, restart: int = 30, precon
                                              C.c_void_p(_stream(stream))))
 
 
-def gmres_solve(p: Problem, net: Optional[MgNet], b, x, *, restart: int = 30, maxit: int = 1000,
-                rtol: float = 1e-8, precond: Optional[int] = None, reorth: int = 2, precision: int = 0,
-                history: bool = True, hessenberg: bool = False, stream=None):
-    """Restarted right-preconditioned GMRES; x (float64 CUDA tensor) holds x0 on entry, x on exit.
-    reorth: 2 = selective re-orthogonalisation (default), 0 = CGS2, 1 = CGS1 (gmres_opts).
+def _host(t, dtype_name: str):
+    """Host buffer pointer: a contiguous CPU torch tensor (pinned for full-rate copies) or numpy array."""
+    import torch
+    want_np = {"f32": np.float32, "f64": np.float64}[dtype_name]
+    if isinstance(t, torch.Tensor):
+        if t.is_cuda or not t.is_contiguous():
+            raise ValueError("expected a contiguous CPU tensor")
+        if t.dtype != {"f32": torch.float32, "f64": torch.float64}[dtype_name]:
+            raise ValueError(f"expected dtype {dtype_name}, got {t.dtype}")
+        return C.c_void_p(t.data_ptr())
+    if not (isinstance(t, np.ndarray) and t.dtype == want_np and t.flags.c_contiguous and t.flags.writeable):
+        raise ValueError(f"expected a contiguous writeable {want_np.__name__} array")
+    return C.c_void_p(t.ctypes.data)
 
-    Returns a list of per-sample dicts (iterations, restarts, converged, breakdown, relres_true,
-    relres_est, history [, hessenberg])."""
+
+def _gmres_call(name, fn, p, net, b_ptr, x_ptr, restart, maxit, rtol, precond, reorth, precision, x0_zero,
+                history, hessenberg, stream):
     if precond is None:
         precond = 1 if net is not None else 0
-    opts = gmres_opts(restart, maxit, rtol, precond, reorth, precision)
+    opts = gmres_opts(restart, maxit, rtol, precond, reorth, precision, int(x0_zero))
     B = p.batch
     reps = (gmres_report * B)()
     hist = [np.zeros(max(maxit, 1)) for _ in range(B)]
@@ -239,8 +248,8 @@ def gmres_solve(p: Problem, net: Optional[MgNet], b, x, *, restart: int = 30, ma
     for i in range(B):
         reps[i].history = _dptr(hist[i]) if history else None
         reps[i].hessenberg = _dptr(hess[i]) if hessenberg else None
-    check("gmres_solve", lib.gmres_solve(p.handle, net.handle if net is not None else None, _dev(b, "f32"),
-                                         _dev(x, "f64"), C.byref(opts), reps, C.c_void_p(_stream(stream))))
+    check(name, fn(p.handle, net.handle if net is not None else None, b_ptr, x_ptr, C.byref(opts), reps,
+                   C.c_void_p(_stream(stream))))
     out = []
     for i in range(B):
         r = reps[i]
@@ -252,6 +261,28 @@ def gmres_solve(p: Problem, net: Optional[MgNet], b, x, *, restart: int = 30, ma
             d["hessenberg"] = hess[i].reshape(restart + 1, restart)
         out.append(d)
     return out
+
+
+def gmres_solve(p: Problem, net: Optional[MgNet], b, x, *, restart: int = 30, maxit: int = 1000,
+                rtol: float = 1e-8, precond: Optional[int] = None, reorth: int = 2, precision: int = 0,
+                x0_zero: bool = False, history: bool = True, hessenberg: bool = False, stream=None):
+    """Restarted right-preconditioned GMRES; x (float64 CUDA tensor) holds x0 on entry (unless
+    x0_zero: then it is set to 0 and A x0 is not applied), x on exit.
+    reorth: 2 = selective re-orthogonalisation (default), 0 = CGS2, 1 = CGS1 (gmres_opts).
+
+    Returns a list of per-sample dicts (iterations, restarts, converged, breakdown, relres_true,
+    relres_est, history [, hessenberg])."""
+    return _gmres_call("gmres_solve", lib.gmres_solve, p, net, _dev(b, "f32"), _dev(x, "f64"), restart, maxit,
+                       rtol, precond, reorth, precision, x0_zero, history, hessenberg, stream)
+
+
+def gmres_solve_host(p: Problem, net: Optional[MgNet], b, x, *, restart: int = 30, maxit: int = 1000,
+                     rtol: float = 1e-8, precond: Optional[int] = None, reorth: int = 2, precision: int = 0,
+                     x0_zero: bool = False, history: bool = True, hessenberg: bool = False, stream=None):
+    """gmres_solve with HOST buffers (include/rte.h): b float32, x float64 (CPU tensors, pinned for
+    full-rate copies, or numpy arrays); the copies in and out happen inside the call."""
+    return _gmres_call("gmres_solve_host", lib.gmres_solve_host, p, net, _host(b, "f32"), _host(x, "f64"), restart,
+                       maxit, rtol, precond, reorth, precision, x0_zero, history, hessenberg, stream)
 
 
 def rte_launch_count(reset: bool = False) -> int:

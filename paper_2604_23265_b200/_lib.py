@@ -33,7 +33,7 @@ class rte_ordinates(C.Structure):
 
 class gmres_opts(C.Structure):
     _fields_ = [("restart", C.c_int), ("maxit", C.c_int), ("rtol", C.c_double),
-                ("precond", C.c_int), ("reorth", C.c_int), ("precision", C.c_int)]
+                ("precond", C.c_int), ("reorth", C.c_int), ("precision", C.c_int), ("x0_zero", C.c_int)]
 
 
 class gmres_report(C.Structure):
@@ -70,6 +70,7 @@ SIGS = {
     "mgnet_modulation": (C.c_int, [_vp, C.c_int, C.c_int, C.POINTER(C.c_double)]),
     "gmres_solve": (C.c_int, [_vp, _vp, _vp, _vp, C.POINTER(gmres_opts), C.POINTER(gmres_report), _vp]),
     "gmres_prepare": (C.c_int, [_vp, _vp, C.POINTER(gmres_opts), _vp]),
+    "gmres_solve_host": (C.c_int, [_vp, _vp, _vp, _vp, C.POINTER(gmres_opts), C.POINTER(gmres_report), _vp]),
     "rte_launch_count": (C.c_int64, [C.c_int]),
     "rte_last_error": (C.c_char_p, []),
     "rte_timing_enable": (C.c_int, [C.c_int]),

@@ -393,6 +393,12 @@ struct GmresWork {
   double* w64 = nullptr;
   double* z64 = nullptr;
   float* q32 = nullptr;    // V-cycle output
+  // gmres_solve_host, allocated on first use: device copies of b and x, a copy stream, and the
+  // events ordering the early device->host copy of x against the solve stream
+  float* bh = nullptr;     // n
+  double* xh = nullptr;    // n
+  cudaStream_t cp = nullptr;
+  cudaEvent_t ev_x = nullptr, ev_cp = nullptr;
   // CUDA graphs of the fp32 Arnoldi step's operator part, w = A P(alpha_j V_j) (the preconditioner
   // and the apply: ~90 launches at config 5), one per (net, net epoch, j, precond); every input and
   // output pointer of that part is fixed per j because this workspace is cached per problem
@@ -415,8 +421,11 @@ struct GmresWork {
   void release() {
     drop_graphs();
     void* ps[] = {V, w, z, r64, Hr, Hraw, cs, sn, g, alpha, h1, h2, h3, coef, bnorm, rn2, partials, counters,
-                  active, kcols, done, st_dev, V64, w64, z64, q32};
+                  active, kcols, done, st_dev, V64, w64, z64, q32, bh, xh};
     for (void* p : ps) dfree(p);
+    if (cp) cudaStreamDestroy(cp);
+    if (ev_x) cudaEventDestroy(ev_x);
+    if (ev_cp) cudaEventDestroy(ev_cp);
     if (st_host) cudaFreeHost(st_host);
     for (auto& e : st_ev)
       if (e) cudaEventDestroy(e);
@@ -670,8 +679,15 @@ extern "C" rte_status gmres_prepare(const rte_problem* p, const mgnet_net* net, 
   }
 }
 
-rte_status gmres_solve(const rte_problem* p, const mgnet_net* net, const float* b_dev, double* x_dev,
-                                  const gmres_opts* opts, gmres_report* rep, void* stream) {
+// Host side of gmres_solve_host: where x goes when the solve has (probably) finished.
+struct HostOut {
+  double* x_host;
+  bool copied = false;  // the early copy of the final x is in flight / done
+};
+
+static rte_status solve_impl(const rte_problem* p, const mgnet_net* net, const float* b_dev, double* x_dev,
+                             const gmres_opts* opts, gmres_report* rep, cudaStream_t st, GmresWork* Wh,
+                             HostOut* ho) {
   try {
     RTE_REQUIRE(p && b_dev && x_dev && opts && rep, "gmres_solve: NULL argument");
     const int m = opts->restart;
@@ -680,10 +696,10 @@ rte_status gmres_solve(const rte_problem* p, const mgnet_net* net, const float* 
     RTE_REQUIRE(opts->rtol > 0.0, "gmres_solve: rtol must be > 0");
     RTE_REQUIRE(opts->precond == 0 || opts->precond == 2 || (opts->precond == 1 && net),
                 "gmres_solve: precond must be 0 (none), 1 (MgNet, requires a net) or 2 (block Jacobi)");
+    RTE_REQUIRE(opts->x0_zero == 0 || opts->x0_zero == 1, "gmres_solve: x0_zero must be 0 or 1");
     if (opts->precond == 2) bj_prepare(p);  // (NEXT-2; builds the inverse cell blocks once)
     RTE_REQUIRE(!net || net->prob == p, "gmres_solve: net was created for another problem");
-    cudaStream_t st = as_stream(stream);
-    GmresWork& W = get_work(p, m);
+    GmresWork& W = Wh ? *Wh : get_work(p, m);
     const int B = p->B;
     const int64_t n = p->n;
     const int hld = kMaxRestart + 2;
@@ -708,6 +724,7 @@ rte_status gmres_solve(const rte_problem* p, const mgnet_net* net, const float* 
       rep[b].relres_est = 0;
     }
     RTE_CHECK_CUDA(cudaMemsetAsync(W.done, 0, sizeof(int) * B, st));
+    if (opts->x0_zero) RTE_CHECK_CUDA(cudaMemsetAsync(x_dev, 0, sizeof(double) * n, st));
     // ||b|| per sample
     launch_norm<float, float>(W, b_dev, nullptr, W.rn2, st);
     {
@@ -721,12 +738,20 @@ rte_status gmres_solve(const rte_problem* p, const mgnet_net* net, const float* 
     bool first_cycle = true;
     int total_all = 0;  // lockstep inner iterations
     while (true) {
-      // r = b - A x (fp64), v0 = r (basis precision, unnormalised), ||r||^2
-      launch_apply_f64(p, x_dev, W.r64, b_dev, st);
-      if (f64)
-        launch_norm<double, double>(W, W.r64, W.V64, W.rn2, st);
-      else
-        launch_norm<double, float>(W, W.r64, W.V, W.rn2, st);
+      // r = b - A x (fp64), v0 = r (basis precision, unnormalised), ||r||^2.  With x0 = 0 the first
+      // residual is b itself (A 0 = 0 and b - 0 = b exactly in fp64): no apply, same bits.
+      if (first_cycle && opts->x0_zero) {
+        if (f64)
+          launch_norm<float, double>(W, b_dev, W.V64, W.rn2, st);
+        else
+          launch_norm<float, float>(W, b_dev, W.V, W.rn2, st);
+      } else {
+        launch_apply_f64(p, x_dev, W.r64, b_dev, st);
+        if (f64)
+          launch_norm<double, double>(W, W.r64, W.V64, W.rn2, st);
+        else
+          launch_norm<double, float>(W, W.r64, W.V, W.rn2, st);
+      }
       int stop_all = (total_all >= opts->maxit) ? 1 : 0;
       prof_begin(st, "cycle_init");
       cycle_init_kernel<<<(B + 63) / 64, 64, 0, st>>>(B, W.rn2, W.bnorm, opts->rtol, stop_all, W.alpha, m + 1, W.g,
@@ -845,7 +870,14 @@ rte_status gmres_solve(const rte_problem* p, const mgnet_net* net, const float* 
                                            sizeof(double) * (m + 1) * m, cudaMemcpyDeviceToHost, st));
       }
       first_cycle = false;
-      // x += P(V y)
+      // x += P(V y).  (gmres_solve_host: an early copy of x from the previous cycle must land before
+      // x changes again)
+      auto wait_host_copy = [&]() {
+        if (ho && ho->copied) {
+          RTE_CHECK_CUDA(cudaStreamWaitEvent(st, W.ev_cp, 0));
+          ho->copied = false;
+        }
+      };
       prof_begin(st, "backsolve");
       backsolve_kernel<<<(B + 63) / 64, 64, 0, st>>>(B, m, W.Hr, W.g, W.alpha, m + 1, W.kcols, W.coef, m + 1);
       after_launch("backsolve", st);
@@ -862,6 +894,7 @@ rte_status gmres_solve(const rte_problem* p, const mgnet_net* net, const float* 
           bj_apply<double>(p, W.z64, W.r64, nullptr, 0, st);
           corr = W.r64;
         }
+        wait_host_copy();
         prof_begin(st, "axpy64");
         axpy64_kernel<double><<<dim3(W.nblk, B), kThreads, 0, st>>>(x_dev, corr, nullptr, W.kcols, W.ns, W.nblk);
         after_launch("axpy64", st, (double)n, 28.0 * (double)n, 0);
@@ -878,6 +911,7 @@ rte_status gmres_solve(const rte_problem* p, const mgnet_net* net, const float* 
           bj_apply<float>(p, W.w, W.z, nullptr, 0, st);
           corr = W.z;
         }
+        wait_host_copy();
         prof_begin(st, "axpy64");
         axpy64_kernel<float><<<dim3(W.nblk, B), kThreads, 0, st>>>(x_dev, corr, nullptr, W.kcols, W.ns, W.nblk);
         after_launch("axpy64", st, (double)n, 20.0 * (double)n, 0);
@@ -887,6 +921,24 @@ rte_status gmres_solve(const rte_problem* p, const mgnet_net* net, const float* 
       for (int b = 0; b < B; ++b)
         if (brk[b] && !done[b]) { done[b] = 1; any_brk = true; }
       if (any_brk) RTE_CHECK_CUDA(cudaMemcpyAsync(W.done, done.data(), sizeof(int) * B, cudaMemcpyHostToDevice, st));
+      if (ho) {
+        // gmres_solve_host: x is final unless another cycle runs, i.e. unless the budget is left and
+        // some sample's estimate has not converged.  Start its device->host copy now on the copy
+        // stream, overlapping the closing fp64 true residual; a wrong guess costs a second copy.
+        bool fin = total_all >= opts->maxit;
+        if (!fin) {
+          fin = true;
+          for (int b = 0; b < B; ++b)
+            if (!brk[b] && !(est_last[b] <= opts->rtol)) fin = false;
+        }
+        if (fin) {
+          RTE_CHECK_CUDA(cudaEventRecord(W.ev_x, st));
+          RTE_CHECK_CUDA(cudaStreamWaitEvent(W.cp, W.ev_x, 0));
+          RTE_CHECK_CUDA(cudaMemcpyAsync(ho->x_host, x_dev, sizeof(double) * n, cudaMemcpyDeviceToHost, W.cp));
+          RTE_CHECK_CUDA(cudaEventRecord(W.ev_cp, W.cp));
+          ho->copied = true;
+        }
+      }
     }
     for (int b = 0; b < B; ++b) {
       rep[b].iterations = total[b];
@@ -896,8 +948,43 @@ rte_status gmres_solve(const rte_problem* p, const mgnet_net* net, const float* 
       rep[b].relres_true = relres[b];
       rep[b].relres_est = est_last[b];
     }
+    if (ho && !ho->copied)
+      RTE_CHECK_CUDA(cudaMemcpyAsync(ho->x_host, x_dev, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
     RTE_CHECK_CUDA(cudaStreamSynchronize(st));
+    if (ho && ho->copied) RTE_CHECK_CUDA(cudaEventSynchronize(W.ev_cp));
     return RTE_OK;
+  } catch (const Fail& f) {
+    return f.st;
+  } catch (const std::exception& e) {
+    set_error(std::string("internal: ") + e.what());
+    return RTE_EINTERNAL;
+  }
+}
+
+extern "C" rte_status gmres_solve(const rte_problem* p, const mgnet_net* net, const float* b_dev, double* x_dev,
+                                  const gmres_opts* opts, gmres_report* rep, void* stream) {
+  return solve_impl(p, net, b_dev, x_dev, opts, rep, as_stream(stream), nullptr, nullptr);
+}
+
+extern "C" rte_status gmres_solve_host(const rte_problem* p, const mgnet_net* net, const float* b_host,
+                                       double* x_host, const gmres_opts* opts, gmres_report* rep, void* stream) {
+  try {
+    RTE_REQUIRE(p && b_host && x_host && opts && rep, "gmres_solve_host: NULL argument");
+    RTE_REQUIRE(opts->restart >= 1 && opts->restart <= 32, "gmres_solve: restart must be in [1, 32]");
+    GmresWork& W = get_work(p, opts->restart);
+    const int64_t n = p->n;
+    if (!W.bh) {
+      W.bh = dalloc<float>(n);
+      W.xh = dalloc<double>(n);
+      RTE_CHECK_CUDA(cudaStreamCreateWithFlags(&W.cp, cudaStreamNonBlocking));
+      RTE_CHECK_CUDA(cudaEventCreateWithFlags(&W.ev_x, cudaEventDisableTiming));
+      RTE_CHECK_CUDA(cudaEventCreateWithFlags(&W.ev_cp, cudaEventDisableTiming));
+    }
+    cudaStream_t st = as_stream(stream);
+    RTE_CHECK_CUDA(cudaMemcpyAsync(W.bh, b_host, sizeof(float) * n, cudaMemcpyHostToDevice, st));
+    if (!opts->x0_zero) RTE_CHECK_CUDA(cudaMemcpyAsync(W.xh, x_host, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+    HostOut ho{x_host};
+    return solve_impl(p, net, W.bh, W.xh, opts, rep, st, &W, &ho);
   } catch (const Fail& f) {
     return f.st;
   } catch (const std::exception& e) {
