@@ -342,3 +342,31 @@ def test_gmres_first_arnoldi_columns(k, steps, reorth):
                              lambda v: O.vcycle(onet, v), steps)
     for j in range(steps):
         assert _rel(H[:j + 2, j], Href[:j + 2, j]) <= 1e-5, j
+
+
+@pytest.mark.slow
+def test_gmres_full_size_bench_configuration():
+    """Config 5 at full size in the launch configuration bench.py times (gmres_prepare's CUDA graphs,
+    x0_zero, selective re-orthogonalisation): the first two Arnoldi columns (unrotated H) agree with
+    the fp64 oracle to 1e-5, and the iterate of the 2-step solve is finite."""
+    import paper_2604_23265_b200 as P
+    cfg = W.config(5)
+    media = W.make_media(cfg)
+    p = _gpu_problem(cfg, media)
+    op = O.setup_from_media(cfg, media)
+    w = W.make_weights(cfg)
+    net = P.mgnet_create(p, cfg.L, cfg.C0, cfg.nu, w)
+    onet = O.make_mgnet(w, cfg.M, cfg.L, cfg.C0, cfg.nu)
+    bd = torch.empty(p.shape, dtype=torch.float32, device="cuda")
+    P.rte_rhs(p, bd)
+    P.gmres_prepare(p, net, restart=cfg.restart)
+    x = torch.full(p.shape, float("nan"), dtype=torch.float64, device="cuda")
+    steps = 2
+    rep = P.gmres_solve(p, net, bd, x, restart=cfg.restart, maxit=steps, rtol=1e-300, hessenberg=True,
+                        x0_zero=True)
+    assert rep[0]["iterations"] == steps and bool(torch.isfinite(x).all())
+    H = rep[0]["hessenberg"][:steps + 1, :steps]
+    Href = O.arnoldi_columns(lambda v: O.apply(op, v), bd.cpu().numpy().astype(np.float64),
+                             lambda v: O.vcycle(onet, v), steps)
+    for j in range(steps):
+        assert _rel(H[:j + 2, j], Href[:j + 2, j]) <= 1e-5, j
