@@ -221,7 +221,7 @@ def gmres_prepare(p: Problem, net: Optional[MgNet], *, restart: int = 30, precon
                                              C.c_void_p(_stream(stream))))
 
 
-def _host(t, dtype_name: str):
+def _host(t, dtype_name: str, writeable: bool = False):
     """Host buffer pointer: a contiguous CPU torch tensor (pinned for full-rate copies) or numpy array."""
     import torch
     want_np = {"f32": np.float32, "f64": np.float64}[dtype_name]
@@ -231,8 +231,9 @@ def _host(t, dtype_name: str):
         if t.dtype != {"f32": torch.float32, "f64": torch.float64}[dtype_name]:
             raise ValueError(f"expected dtype {dtype_name}, got {t.dtype}")
         return C.c_void_p(t.data_ptr())
-    if not (isinstance(t, np.ndarray) and t.dtype == want_np and t.flags.c_contiguous and t.flags.writeable):
-        raise ValueError(f"expected a contiguous writeable {want_np.__name__} array")
+    if not (isinstance(t, np.ndarray) and t.dtype == want_np and t.flags.c_contiguous
+            and (t.flags.writeable or not writeable)):
+        raise ValueError(f"expected a contiguous{' writeable' if writeable else ''} {want_np.__name__} array")
     return C.c_void_p(t.ctypes.data)
 
 
@@ -281,7 +282,7 @@ def gmres_solve_host(p: Problem, net: Optional[MgNet], b, x, *, restart: int = 3
                      x0_zero: bool = False, history: bool = True, hessenberg: bool = False, stream=None):
     """gmres_solve with HOST buffers (include/rte.h): b float32, x float64 (CPU tensors, pinned for
     full-rate copies, or numpy arrays); the copies in and out happen inside the call."""
-    return _gmres_call("gmres_solve_host", lib.gmres_solve_host, p, net, _host(b, "f32"), _host(x, "f64"), restart,
+    return _gmres_call("gmres_solve_host", lib.gmres_solve_host, p, net, _host(b, "f32"), _host(x, "f64", True), restart,
                        maxit, rtol, precond, reorth, precision, x0_zero, history, hessenberg, stream)
 
 

@@ -83,3 +83,24 @@ def test_coeffnet_weight_count_matches_packed_layout(L, C0):
     import paper_2604_23265_b200 as P
     import workloads as W
     assert P.mgnet_coeffnet_weight_count(L, C0) == W.coeffnet_weight_count(L, C0)
+
+
+def test_host_buffer_validation():
+    """gmres_solve_host's marshalling (no GPU): b may be read-only, x must be writeable; dtype,
+    contiguity and device are checked before the C call."""
+    import torch
+    import paper_2604_23265_b200 as P
+    b = np.zeros(8, np.float32)
+    b.flags.writeable = False
+    assert P._host(b, "f32").value == b.ctypes.data
+    x = np.zeros(8)
+    assert P._host(x, "f64", True).value == x.ctypes.data
+    ro = np.zeros(8)
+    ro.flags.writeable = False
+    for bad, dt, w in ((ro, "f64", True), (np.zeros(8, np.float32), "f64", True), (np.zeros((4, 4))[:, ::2], "f64", True),
+                       (torch.zeros(8, dtype=torch.float64), "f32", False), ([0.0] * 8, "f64", True)):
+        with pytest.raises(ValueError):
+            P._host(bad, dt, w)
+    t = torch.zeros(8, dtype=torch.float64)
+    assert P._host(t, "f64", True).value == t.data_ptr()
+    assert [f[0] for f in P.gmres_opts._fields_][-1] == "x0_zero"
