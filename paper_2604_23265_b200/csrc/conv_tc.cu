@@ -255,6 +255,10 @@ __global__ void splitk_reduce_kernel(const float4* __restrict__ part, long long 
                                      const float4* addend, float sign, const double* __restrict__ alpha,
                                      int alpha_stride, int a_in, int a_add, long long n4, long long per_sample4,
                                      int out_split, const float4* __restrict__ mod) {
+  // programmatic dependent launch: let the next GEMM start its prologue, then wait for the GEMM
+  // that wrote the partials (its completion and memory flush)
+  griddep_launch_dependents();
+  griddep_wait();
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n4; e += (long long)gridDim.x * blockDim.x) {
     float4 s = part[e];
     for (int k = 1; k < nsplit; ++k) {
@@ -578,11 +582,10 @@ bool conv_tc_try(const ConvDesc& d, const float* in, float* out, const float* ad
     const long long n4 = P.out_elems / 4;
     const long long per4 = n4 / d.B;
     const int blocks = (int)std::min<long long>((n4 + 255) / 256, (long long)num_sms() * 8);
-    tc::splitk_reduce_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const float4*>(d.ws_owner->tc_ws), n4,
-                                                     g.nsplit, reinterpret_cast<float4*>(out),
-                                                     reinterpret_cast<const float4*>(addend), sign, alpha,
-                                                     alpha_stride, epi.a_in, epi.a_add, n4, per4,
-                                                     d.out_split ? 1 : 0, reinterpret_cast<const float4*>(d.mod));
+    tc::launch_pdl(tc::splitk_reduce_kernel, blocks, 256, 0, st, reinterpret_cast<const float4*>(d.ws_owner->tc_ws),
+                   n4, g.nsplit, reinterpret_cast<float4*>(out), reinterpret_cast<const float4*>(addend), sign,
+                   alpha, alpha_stride, epi.a_in, epi.a_add, n4, per4, d.out_split ? 1 : 0,
+                   reinterpret_cast<const float4*>(d.mod));
     // the conv's algorithmic bytes are booked on the reduction (it writes the output)
     after_launch("splitk_reduce", st, 0.0, conv_bytes(d, addend != nullptr) + 4.0 * g.nsplit * P.out_elems, 0);
   }

@@ -43,11 +43,11 @@ constexpr int kGemmThreads = 448;   // 14 warps (see above)
 // kernel's tail; the kernel waits at griddepcontrol.wait before reading dependent data).
 // RTE_NO_PDL=1 launches plainly.
 template <typename K, typename... Args>
-void launch_gemm(K kern, int grid, int smem, cudaStream_t st, Args... args) {
+void launch_pdl(K kern, int grid, int block, int smem, cudaStream_t st, Args... args) {
   static const bool pdl = getenv("RTE_NO_PDL") == nullptr;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid, 1, 1);
-  cfg.blockDim = dim3(kGemmThreads, 1, 1);
+  cfg.blockDim = dim3((unsigned)block, 1, 1);
   cfg.dynamicSmemBytes = (size_t)smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -56,6 +56,10 @@ void launch_gemm(K kern, int grid, int smem, cudaStream_t st, Args... args) {
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
   RTE_CHECK_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
+}
+template <typename K, typename... Args>
+void launch_gemm(K kern, int grid, int smem, cudaStream_t st, Args... args) {
+  launch_pdl(kern, grid, kGemmThreads, smem, st, args...);
 }
 
 constexpr int kPromoteKB = 4;       // K blocks per TMEM accumulation group
