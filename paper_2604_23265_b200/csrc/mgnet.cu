@@ -17,6 +17,7 @@
 
 #include "common.h"
 #include "mgnet.h"
+#include "tc_host.h"
 
 namespace rte {
 namespace {
@@ -189,113 +190,129 @@ const char* conv_class_name(const ConvDesc& d, bool tc) {
   return names.insert(key).first->c_str();
 }
 
-// 1x1 conv with a short reduction (Ci <= 32, Co % 256 == 0, plain fp32 activations): the MgNet tail
-// lift C0 -> M ordinates (PAPER.md's channel lift back to the unknowns).  HBM-bound -- it streams
-// the M-wide output and addend -- so it runs on the fp32 FMA pipes, not the tensor cores (whose
-// conversion + epilogue dominated at K = 32).  Block = 64 pixels x 256 output channels (512
-// threads), weights [ci][co] and the pixels' inputs [ci][pixel] in shared memory; thread = 4 pixels
-// x 8 consecutive channels (32 FMAs per 3 LDS.128); each warp covers whole 1 KB output rows; the
-// tile's addend rows are bulk-prefetched into L2 at the block start.
-// out = (addend ? s_add addend : 0) + sign s_in (W in)  (same epilogue as conv_simt_kernel)
-constexpr int kSmallKMaxCi = 32;  // (static shared memory: 32 KB weights + 8 KB inputs)
+// 1x1 conv with a short reduction (Ci <= 32, Co = 64, 128 or 256, plain fp32 activations): the MgNet
+// head Theta, C0 -> M ordinates, z = r + Theta u (PAPER.md's channel lift back to the unknowns).
+// HBM-bound -- it streams the M-wide addend and output -- so it runs on the fp32 FMA pipes, not the
+// tensor cores (whose conversion + epilogue dominated at K = 32).
+constexpr int kSmallKMaxCi = 32;
+// acc[a][c] += sum_k u[pixel a][k] W[k][channel c] for a thread's PPT pixels (rows of ub at pitch Ci)
+// and 8 channels {4 tx .. 4 tx + 3} and {TCO/2 + 4 tx .. + 3}: a warp's weight loads are 512
+// contiguous bytes (no bank conflicts) and the inputs are read as float4 (4 K steps; the warp's
+// lanes share the pixels, so those loads broadcast).  k ascends: the FMA chain of every output is
+// the plain sum order.
+template <int TCO, int PPT>
+__device__ __forceinline__ void smallk_mac(float (&acc)[PPT][8], const float* Ws, const float* ub, int Ci, int tx) {
+  for (int k = 0; k < Ci; k += 4) {
+    float4 u4[PPT];
+#pragma unroll
+    for (int a = 0; a < PPT; ++a) u4[a] = *reinterpret_cast<const float4*>(ub + a * Ci + k);
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      const float* wr = Ws + (k + kk) * TCO;
+      const float4 w0 = *reinterpret_cast<const float4*>(wr + tx * 4);
+      const float4 w1 = *reinterpret_cast<const float4*>(wr + TCO / 2 + tx * 4);
+      const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+      for (int a = 0; a < PPT; ++a) {
+        const float uva = kk == 0 ? u4[a].x : kk == 1 ? u4[a].y : kk == 2 ? u4[a].z : u4[a].w;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc[a][c] = fmaf(uva, wv[c], acc[a][c]);
+      }
+    }
+  }
+}
 // (out and addend may be the same array: every element is read, then written, by one thread in
 // one iteration, so __restrict__ only lets the compiler batch the loads of different pixels)
-template <int TCO>  // output channels = TCO (64, 128 or 256): the weight block is contiguous
-__global__ void __launch_bounds__(512, 2) conv1x1_smallk_kernel(int npix, int Ci, int Co, const float* __restrict__ in,
-                                                             const float* __restrict__ Wk, float* __restrict__ out,
-                                                             const float* __restrict__ addend, float sign,
-                                                             const double* __restrict__ alpha, int alpha_stride,
-                                                             int alpha_on_input, int alpha_on_addend) {
-  constexpr int TPX = 16384 / TCO;       // pixels per block: every block writes 64 KB (4 per thread)
-  constexpr int TXN = TCO / 8;           // threads along channels (8 channels each)
-  constexpr int PPT = TPX * TXN / 512;   // pixels per thread (= 4)
-  __shared__ __align__(128) float Ws[kSmallKMaxCi][TCO];  // [ci][co]
-  __shared__ __align__(128) float Us[TPX][kSmallKMaxCi];  // [pixel][ci] at pitch Ci (the input's layout)
-  __shared__ __align__(8) uint64_t bar;
-  const int tid = threadIdx.x, tx = tid % TXN, ty = tid / TXN;  // 8 channels x PPT pixels per thread
+// Every global transfer is a bulk async copy: one thread loads the weights, the tile's inputs and its
+// addend rows (contiguous: TPX pixels x Co channels) into shared memory on one mbarrier; the block
+// computes in place over the addend tile; after a generic -> async proxy fence one thread stores
+// the result with one bulk copy.  NT threads per block (4 pixels x 8 channels each): NT = 256 ->
+// 32 KB tiles, 3 blocks per SM (measured at config 5: 0.135 ms against 0.138 for NT = 512 and
+// 0.157 for per-thread addend loads and stores; 0.187 before the conflict-free channel mapping).
+template <int TCO, int NT>
+constexpr int smallk_bulk_smem_bytes() {
+  return ((NT * 32 / TCO) * TCO + kSmallKMaxCi * TCO + (NT * 32 / TCO) * kSmallKMaxCi) * 4 + 128;
+}
+template <int TCO, int NT>
+__global__ void __launch_bounds__(NT, NT == 512 ? 2 : NT == 256 ? 3 : 4) conv1x1_smallk_kernel(int npix, int Ci, int Co, const float* __restrict__ in,
+                                                                  const float* __restrict__ Wk, float* out,
+                                                                  const float* addend, float sign,
+                                                                  const double* __restrict__ alpha, int alpha_stride,
+                                                                  int alpha_on_input, int alpha_on_addend) {
+  constexpr int TPX = NT * 32 / TCO;  // pixels per tile
+  constexpr int TXN = TCO / 8;
+  constexpr int PPT = TPX * TXN / NT;  // (= 4)
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* As = reinterpret_cast<float*>(smem_raw);  // [TPX][TCO]: addend, then the result
+  float* Ws = As + TPX * TCO;                      // [ci][TCO]
+  float* Us = Ws + kSmallKMaxCi * TCO;             // [pixel][ci] at pitch Ci
+  uint64_t* bar = reinterpret_cast<uint64_t*>(Us + TPX * kSmallKMaxCi);
+  const int tid = threadIdx.x, tx = tid % TXN, ty = tid / TXN;
   const int b = blockIdx.z;
-  const int co0 = blockIdx.y * TCO;
   const int64_t p0 = (int64_t)blockIdx.x * TPX;
   const int np = (int)std::min<int64_t>(TPX, npix - p0);
+  const int64_t row0 = (int64_t)b * npix + p0;
+  const uint32_t sb = (uint32_t)__cvta_generic_to_shared(bar);
   if (tid == 0) {
-    if (addend && Co == TCO) {
-      // the tile's addend rows (contiguous: 64 pixels x 1 KB) start streaming into L2 now
-      const float* src = addend + ((int64_t)b * npix + p0) * Co;
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"((uint32_t)(np * Co * 4)) : "memory");
-    }
-    // weights (contiguous when Co == 256) and the tile's inputs: two bulk async copies
-    const uint32_t wbytes = (uint32_t)(Ci * TCO * 4), ubytes = (uint32_t)(np * Ci * 4);
-    const uint32_t sb = (uint32_t)__cvta_generic_to_shared(&bar);
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sb) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sb), "r"(wbytes + ubytes) : "memory");
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     (uint32_t)__cvta_generic_to_shared(&Ws[0][0])),
-                 "l"(Wk + co0), "r"(wbytes), "r"(sb)
+    const uint32_t wbytes = (uint32_t)(Ci * TCO * 4), ubytes = (uint32_t)(np * Ci * 4);
+    const uint32_t abytes = addend ? (uint32_t)(np * TCO * 4) : 0u;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sb), "r"(wbytes + ubytes + abytes)
                  : "memory");
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     (uint32_t)__cvta_generic_to_shared(&Us[0][0])),
-                 "l"(in + ((int64_t)b * npix + p0) * Ci), "r"(ubytes), "r"(sb)
+                     (uint32_t)__cvta_generic_to_shared(Ws)),
+                 "l"(Wk), "r"(wbytes), "r"(sb)
                  : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(Us)),
+                 "l"(in + row0 * Ci), "r"(ubytes), "r"(sb)
+                 : "memory");
+    if (addend)
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       (uint32_t)__cvta_generic_to_shared(As)),
+                   "l"(addend + row0 * Co), "r"(abytes), "r"(sb)
+                   : "memory");
   }
   __syncthreads();  // (barrier initialised)
-  {
-    const uint32_t sb = (uint32_t)__cvta_generic_to_shared(&bar);
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tW_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t"
-        "@!p bra W_%=;\n\t}" ::"r"(sb)
-        : "memory");
-  }
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tW_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t"
+      "@!p bra W_%=;\n\t}" ::"r"(sb)
+      : "memory");
   float acc[PPT][8];
 #pragma unroll
   for (int a = 0; a < PPT; ++a)
 #pragma unroll
     for (int c = 0; c < 8; ++c) acc[a][c] = 0.f;
-  for (int k = 0; k < Ci; ++k) {
-    const float4 w0 = *reinterpret_cast<const float4*>(&Ws[k][tx * 8]);
-    const float4 w1 = *reinterpret_cast<const float4*>(&Ws[k][tx * 8 + 4]);
-    const float* uc = &Us[0][0] + ty * PPT * Ci + k;  // [pixel][ci] at pitch Ci (as copied)
-    float uv[PPT];
-#pragma unroll
-    for (int a = 0; a < PPT; ++a) uv[a] = uc[a * Ci];
-    const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-#pragma unroll
-    for (int a = 0; a < PPT; ++a)
-#pragma unroll
-      for (int c = 0; c < 8; ++c) acc[a][c] = fmaf(uv[a], wv[c], acc[a][c]);
-  }
+  smallk_mac<TCO, PPT>(acc, Ws, Us + ty * PPT * Ci, Ci, tx);
   const float al = alpha ? (float)alpha[(int64_t)b * alpha_stride] : 1.f;
   const float s_in = (alpha_on_input ? al : 1.f) * sign;
   const float s_add = alpha_on_addend ? al : 1.f;
-  // the addend loads of (up to) two pixels are issued before their stores
-  constexpr int PB = PPT < 2 ? PPT : 2;
 #pragma unroll
-  for (int a0 = 0; a0 < PPT; a0 += PB) {
-    float4 ad[PB][2];
-#pragma unroll
-    for (int a = 0; a < PB; ++a) {
-      const int64_t p = p0 + ty * PPT + a0 + a;
-      const int64_t o = ((int64_t)b * npix + p) * Co + co0 + tx * 8;
-      ad[a][0] = ad[a][1] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (addend && p < npix) {
-        ad[a][0] = *reinterpret_cast<const float4*>(addend + o);
-        ad[a][1] = *reinterpret_cast<const float4*>(addend + o + 4);
-      }
+  for (int a = 0; a < PPT; ++a) {
+    const int pl = ty * PPT + a;
+    if (pl >= np) continue;
+    float* r = As + pl * TCO + tx * 4;  // channels r.., r + TCO/2..
+    float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
+    if (addend) {
+      a0 = *reinterpret_cast<const float4*>(r);
+      a1 = *reinterpret_cast<const float4*>(r + TCO / 2);
     }
-#pragma unroll
-    for (int a = 0; a < PB; ++a) {
-      const int64_t p = p0 + ty * PPT + a0 + a;
-      if (p >= npix) continue;
-      const int64_t o = ((int64_t)b * npix + p) * Co + co0 + tx * 8;
-      const float* r = acc[a0 + a];
-      const float4 r0 = make_float4(fmaf(s_add, ad[a][0].x, s_in * r[0]), fmaf(s_add, ad[a][0].y, s_in * r[1]),
-                                    fmaf(s_add, ad[a][0].z, s_in * r[2]), fmaf(s_add, ad[a][0].w, s_in * r[3]));
-      const float4 r1 = make_float4(fmaf(s_add, ad[a][1].x, s_in * r[4]), fmaf(s_add, ad[a][1].y, s_in * r[5]),
-                                    fmaf(s_add, ad[a][1].z, s_in * r[6]), fmaf(s_add, ad[a][1].w, s_in * r[7]));
-      *reinterpret_cast<float4*>(out + o) = r0;
-      *reinterpret_cast<float4*>(out + o + 4) = r1;
-    }
+    const float* q = acc[a];
+    *reinterpret_cast<float4*>(r) = make_float4(fmaf(s_add, a0.x, s_in * q[0]), fmaf(s_add, a0.y, s_in * q[1]),
+                                                fmaf(s_add, a0.z, s_in * q[2]), fmaf(s_add, a0.w, s_in * q[3]));
+    *reinterpret_cast<float4*>(r + TCO / 2) = make_float4(fmaf(s_add, a1.x, s_in * q[4]), fmaf(s_add, a1.y, s_in * q[5]),
+                                                    fmaf(s_add, a1.z, s_in * q[6]), fmaf(s_add, a1.w, s_in * q[7]));
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> the bulk store
+  __syncthreads();
+  if (tid == 0) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out + row0 * Co),
+                 "r"((uint32_t)__cvta_generic_to_shared(As)), "r"((uint32_t)(np * TCO * 4))
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // smem stays live until read
   }
 }
 
@@ -314,12 +331,21 @@ void launch_conv_t(const ConvDesc& d, const T* in, const T* Wk, T* out, const T*
     if (conv1x1_smallk_ok(d)) {
       prof_begin(st, conv_class_name(d, false));
       const int npix = d.Ho * d.Wo;
-      const unsigned bx = (unsigned)((npix + 16384 / d.Co - 1) / (16384 / d.Co));
       auto go = [&](auto tco_tag) {
         constexpr int TCO = decltype(tco_tag)::value;
-        conv1x1_smallk_kernel<TCO><<<dim3(bx, 1, (unsigned)d.B), 512, 0, st>>>(
-            npix, d.Ci, d.Co, in, Wk, out, addend, sign, alpha, alpha_stride, alpha_on_input ? 1 : 0,
-            alpha_on_addend ? 1 : 0);
+        static const int nt_env = getenv("RTE_SMALLK_NT") ? atoi(getenv("RTE_SMALLK_NT")) : 256;  // (A/B)
+        auto bulk = [&](auto nt_tag) {
+          constexpr int NT = decltype(nt_tag)::value;
+          constexpr int smem = smallk_bulk_smem_bytes<TCO, NT>();
+          constexpr int tpx = NT * 32 / TCO;
+          tc::ensure_smem((const void*)conv1x1_smallk_kernel<TCO, NT>, smem);
+          conv1x1_smallk_kernel<TCO, NT><<<dim3((unsigned)((npix + tpx - 1) / tpx), 1, (unsigned)d.B), NT, smem, st>>>(
+              npix, d.Ci, d.Co, in, Wk, out, addend, sign, alpha, alpha_stride, alpha_on_input ? 1 : 0,
+              alpha_on_addend ? 1 : 0);
+        };
+        if (nt_env == 128) bulk(std::integral_constant<int, 128>{});
+        else if (nt_env == 512) bulk(std::integral_constant<int, 512>{});
+        else bulk(std::integral_constant<int, 256>{});
       };
       if (d.Co == 256) go(std::integral_constant<int, 256>{});
       else if (d.Co == 128) go(std::integral_constant<int, 128>{});
