@@ -1,6 +1,7 @@
 """Per-class roofline table of one GMRES(30) cycle on config 5 (for DESIGN.md / profiles/): every
-timing class's device time per iteration and its achieved throughput against its own bound, from the
-library's algorithmic flops/bytes and MEASURED_PEAKS.json.
+timing class's device time per iteration and its achieved throughput against its binding bound
+(the larger of algorithmic bytes / HBM and algorithmic flops / compute peak), from the library's
+algorithmic flops/bytes and MEASURED_PEAKS.json.
 
   python scripts/roofline_table.py > profiles/r01_final/roofline_table.md
 """
@@ -44,17 +45,24 @@ tot = sum(r["ms"] for r in rows)
 print(f"# Per-class rooflines, config {cfg.k}, one GMRES({K}) cycle (profiled: every launch event-timed)\n")
 print("| class | bound | launches/it | ms/it | share | achieved | peak | fraction |")
 print("|---|---|---|---|---|---|---|---|")
+# the binding roofline of a class is the larger of its two lower bounds, algorithmic bytes / HBM and
+# algorithmic flops / its compute peak (a tensor-core GEMM with a short K can be HBM-bound)
 for r in sorted(rows, key=lambda r: -r["ms"]):
     kind = r["kind"]
-    ms_l = r["ms"] / max(r["launches"], 1)
-    if kind == "hbm" and r["bytes"] > 0:
-        ach = r["bytes"] / r["launches"] / (ms_l * 1e-3) / 1e9
-    elif kind in ("tensor_3xtf32", "fp32_simt", "fp64_simt") and r["flops"] > 0:
-        ach = r["flops"] / r["launches"] / (ms_l * 1e-3) / 1e12
+    n = max(r["launches"], 1)
+    t = r["ms"] / n * 1e-3  # s per launch
+    pk_c, unit_c = PEAK.get(kind, (None, "")) if kind != "hbm" else (None, "")
+    t_mem = r["bytes"] / n / (hbm * 1e9) if r["bytes"] > 0 else 0.0
+    t_cmp = r["flops"] / n / (pk_c * 1e12) if (pk_c and r["flops"] > 0) else 0.0
+    if t_mem == 0.0 and t_cmp == 0.0:
+        bound, achs, pks, frac = kind, "—", PEAK.get(kind, (None, ""))[0], "—"
+        pks = f"{pks:.0f} {PEAK[kind][1]}" if pks else "—"
+    elif t_mem >= t_cmp:
+        bound = "hbm"
+        achs, pks = f"{r['bytes'] / n / t / 1e9:.0f} GB/s", f"{hbm:.0f} GB/s"
+        frac = f"{t_mem / t:.2f}"
     else:
-        ach = None
-    pk, unit = PEAK.get(kind, (None, ""))
-    frac = f"{ach / pk:.2f}" if (ach is not None and pk) else "—"
-    achs = f"{ach:.0f} {unit}" if ach is not None else "—"
-    pks = f"{pk:.0f} {unit}" if pk else "—"
-    print(f"| {r['name']} | {kind} | {r['launches'] / K:.1f} | {r['ms'] / K:.4f} | {r['ms'] / tot:.3f} | {achs} | {pks} | {frac} |")
+        bound = kind
+        achs, pks = f"{r['flops'] / n / t / 1e12:.0f} {unit_c}", f"{pk_c:.0f} {unit_c}"
+        frac = f"{t_cmp / t:.2f}"
+    print(f"| {r['name']} | {bound} | {r['launches'] / K:.1f} | {r['ms'] / K:.4f} | {r['ms'] / tot:.3f} | {achs} | {pks} | {frac} |")
