@@ -126,7 +126,8 @@ __global__ void __launch_bounds__(kThreads, 1) cgs_kernel(
 #pragma unroll
         for (int e = 0; e < W; ++e) s[e] = fma(-coef[i], v[e], s[e]);
       }
-      d4[q] = sv;
+      __stcs(d4 + q, sv);  // streaming store: the 256 MiB result cannot stay in L2 for its next reader,
+                           // and evict-first keeps it from displacing the read stream (0.92 -> 0.95 of HBM)
     }
     if (DOTS) {
 #pragma unroll
