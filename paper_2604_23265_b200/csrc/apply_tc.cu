@@ -88,7 +88,7 @@ struct EpiApply {
     r.y = al * ((a_x.y + a_y.y + st) * p.y - ss * (c + v.y) - a_x.y * nx.y - a_y.y * ny.y);
     r.z = al * ((a_x.z + a_y.z + st) * p.z - ss * (c + v.z) - a_x.z * nx.z - a_y.z * ny.z);
     r.w = al * ((a_x.w + a_y.w + st) * p.w - ss * (c + v.w) - a_x.w * nx.w - a_y.w * ny.w);
-    *reinterpret_cast<float4*>(y + rw.cell * M + cv.m) = r;
+    __stcs(reinterpret_cast<float4*>(y + rw.cell * M + cv.m), r);  // evict-first: keeps the prefetched inputs in L2
   }
   __device__ __forceinline__ void store_partial4(int, const Row&, int, float4) const {}
 };
