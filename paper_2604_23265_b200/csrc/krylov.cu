@@ -985,7 +985,10 @@ extern "C" rte_status gmres_solve_host(const rte_problem* p, const mgnet_net* ne
     RTE_CHECK_CUDA(cudaMemcpyAsync(W.bh, b_host, sizeof(float) * n, cudaMemcpyHostToDevice, st));
     if (!opts->x0_zero) RTE_CHECK_CUDA(cudaMemcpyAsync(W.xh, x_host, sizeof(double) * n, cudaMemcpyHostToDevice, st));
     HostOut ho{x_host};
-    return solve_impl(p, net, W.bh, W.xh, opts, rep, st, &W, &ho);
+    const rte_status rc = solve_impl(p, net, W.bh, W.xh, opts, rep, st, &W, &ho);
+    // (on an error return too: no copy into the caller's x_host may still be in flight)
+    if (rc != RTE_OK && W.cp) cudaStreamSynchronize(W.cp);
+    return rc;
   } catch (const Fail& f) {
     return f.st;
   } catch (const std::exception& e) {
