@@ -441,7 +441,12 @@ Plan make_plan(const ConvDesc& d) {
   static const bool cluster_ok = getenv("RTE_TC_CLUSTER") != nullptr;
   double best = 1e300;
   int best_kps = g.kb_total;
-  const int quantum = P.halo ? 9 : 1;  // halo kernels split K in whole channel chunks (9 taps)
+  // K-split granularity in K blocks.  A halo split may start or end inside a channel chunk (its
+  // first K block loads the chunk's halo tile), so any K block boundary is allowed; the wave model
+  // picks e.g. 9 splits of 32 K blocks for the 16 x 16 x 1024 conv (144 of 148 SMs busy, was 8 x
+  // 36 on 128: 0.259 -> 0.234 ms/it at config 5).  RTE_TC_KQ=9 restores whole-chunk splits.
+  static const int kq_env = getenv("RTE_TC_KQ") ? atoi(getenv("RTE_TC_KQ")) : 1;
+  const int quantum = P.halo ? std::max(1, std::min(9, kq_env)) : 1;
   const int ns_max = cluster_ok ? 8 : 64;
   for (int ns = 1; ns <= std::max(1, std::min(ns_max, g.kb_total / (2 * quantum))); ++ns) {
     const int kps = ((g.kb_total + ns - 1) / ns + quantum - 1) / quantum * quantum;
