@@ -132,7 +132,11 @@ void launch_apply_tc(const rte_problem* p, const float* x, float* y, const doubl
   g.taps = 1;
   g.classes = 1;
   g.Hc = g.Wc = N;
-  g.TW = std::min(N, 128);
+  // 16 x 8-cell tiles: most upwind y-neighbours are rows of the same tile, which the epilogue's other
+  // lanes have just loaded (a 128 x 1 strip takes every one from L2): apply 0.328 -> 0.291 ms at
+  // config 5, also best at configs 3-4 (RTE_APPLY_TW overrides the width)
+  static const int tw_env = getenv("RTE_APPLY_TW") ? atoi(getenv("RTE_APPLY_TW")) : 16;
+  g.TW = std::min(N, std::max(1, std::min(128, tw_env)));
   g.TH = std::min(N, std::max(1, 128 / g.TW));
   g.pitch = g.TW;
   g.tiles_x = (N + g.TW - 1) / g.TW;
