@@ -151,9 +151,9 @@ void launch_apply_tc(const rte_problem* p, const float* x, float* y, const doubl
   g.mtiles = mtiles;
   g.bn = BN;
   g.dbg = tc::tc_debug_flags();
-  g.epf = 2;  // prefetch x at the tile's rows j0 - 1 .. j0 + TH (cells and upwind neighbours)
+  g.epf = 2;  // prefetch x over the tile and its one-cell halo (cells and upwind neighbours)
   g.epf_planes = 1;
-  CUtensorMap te = tc::make_map_prefetch(x, M, N, N, B, BN, g.TW, g.TH);
+  CUtensorMap te = tc::make_map_prefetch(x, M, N, N, B, BN, g.TW + 2, g.TH + 2);  // (halo box, epi_prefetch)
   CUtensorMap ta = tc::make_map_act(x, M, N, N, B, g.TW, g.TH, 1);
   CUtensorMap tbh = tc::make_map_kmajor(p->S_hi, M, B * M, BN);
   CUtensorMap tbl = tc::make_map_kmajor(p->S_lo, M, B * M, BN);

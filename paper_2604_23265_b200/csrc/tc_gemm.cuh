@@ -87,7 +87,7 @@ struct Geom {
   int pitch;        // MMA-tile rows per output line (= TW, or the halo pitch P of SS-halo kernels)
   int epf;          // epilogue-input L2 prefetch through tmE at each unit start: 0 none, 1 the
                     // output-shaped tile (conv addend; epf_planes planes), 2 the tile's rows
-                    // oy0 - 1 .. oy0 + TH (apply: the cell and its upwind neighbours)
+                    // with its one-cell halo (apply: the cells and their upwind neighbours)
   int epf_planes;
   int cl;           // cluster split-K: 0 off; else = nsplit, the K splits of one output tile run
                     // as one thread-block cluster (one unit per CTA) and are reduced through
@@ -266,7 +266,9 @@ __device__ __forceinline__ void epi_prefetch(const Geom& g, const CUtensorMap* t
   if (g.epf == 1) {
     for (int pl = 0; pl < g.epf_planes; ++pl) tma_prefetch_l2_4d(tmE, w.n0, x0, y0, w.tc.b * g.epf_planes + pl);
   } else {
-    for (int dy = -1; dy <= 1; ++dy) tma_prefetch_l2_4d(tmE, w.n0, x0, y0 + dy, w.tc.b);
+    // the tile's cells and their upwind neighbours: one (TW + 2) x (TH + 2) box at (x0 - 1, y0 - 1)
+    // (out-of-range coordinates at the domain edge are skipped by the TMA unit)
+    tma_prefetch_l2_4d(tmE, w.n0, x0 - 1, y0 - 1, w.tc.b);
   }
 }
 
