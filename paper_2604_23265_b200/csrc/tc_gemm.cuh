@@ -86,8 +86,8 @@ struct Geom {
   int bn;           // N tile (the kernel's BN)
   int pitch;        // MMA-tile rows per output line (= TW, or the halo pitch P of SS-halo kernels)
   int epf;          // epilogue-input L2 prefetch through tmE at each unit start: 0 none, 1 the
-                    // output-shaped tile (conv addend; epf_planes planes), 2 the tile's rows
-                    // with its one-cell halo (apply: the cells and their upwind neighbours)
+                    // output-shaped tile (conv addend; epf_planes planes), 2 the tile with its
+                    // one-cell halo (apply: the cells and their upwind neighbours)
   int epf_planes;
   int cl;           // cluster split-K: 0 off; else = nsplit, the K splits of one output tile run
                     // as one thread-block cluster (one unit per CTA) and are reduced through
