@@ -176,11 +176,13 @@ def test_vcycle_parity_large(k):
     assert _rel(v_gpu, v_ref) <= 1e-5
 
 
-@pytest.mark.parametrize("env", [{"RTE_TC_SS_MINW": "16"}, {"RTE_TC_PRESPLIT": "1"}, {"RTE_TC_CLUSTER": "1"}],
-                         ids=["ss_halo", "presplit", "cluster_splitk"])
+@pytest.mark.parametrize("env", [{"RTE_TC_SS_MINW": "16"}, {"RTE_TC_PRESPLIT": "1"}, {"RTE_TC_CLUSTER": "1"},
+                                 {"RTE_TC_KQ": "9"}, {"RTE_SMALLK_NT": "512"}],
+                         ids=["ss_halo", "presplit", "cluster_splitk", "whole_chunk_splitk", "head_512"])
 def test_vcycle_parity_kernel_variants(env):
     """The opt-in conv kernel variants (SS-halo 3x3 kernels, pre-split activations, cluster
-    split-K through distributed shared memory)
+    split-K through distributed shared memory, K splits in whole 9-tap chunks, 64 KB head-conv
+    tiles)
     pass the same V-cycle parity: their switches are read once per process, so the V-cycle parity
     tests rerun in a child process with the switch set."""
     import os
