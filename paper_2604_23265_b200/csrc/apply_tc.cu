@@ -97,7 +97,7 @@ template <int BN>
 void launch_apply_bn(const Geom& g, int mtiles, const CUtensorMap& ta, const CUtensorMap& tbh,
                      const CUtensorMap& tbl, const CUtensorMap& te, const EpiApply& epi, cudaStream_t st) {
   auto kern = gemm3xtf32_kernel<BN, 0, false, EpiApply>;
-  constexpr int smem = gemm_smem_bytes<BN, 0, false>();
+  constexpr int smem = gemm_smem_bytes<BN, 0, false, 1, true>();
   ensure_smem((const void*)kern, smem);
   const int grid = std::min(mtiles * g.ntiles, num_sms());
   launch_gemm(kern, grid, smem, st, ta, tbh, tbl, te, g, epi);

@@ -111,11 +111,16 @@ constexpr int stage_chunks() {
 // the halo tile is split once in shared memory and each tap's A operand is a row-shifted SW128
 // descriptor into it (see the kernel comment).
 #ifndef RTE_NA128
-#define RTE_NA128 4  // A ring depth of N = 128 window kernels (measured: 3 -> 4 is 4% on the apply, 5 no better)
+#define RTE_NA128 4  // A ring depth of the N = 128 apply (measured: 3 -> 4 is 4% on the apply, 5 no better)
+#endif
+#ifndef RTE_NA128C
+#define RTE_NA128C 3  // ... and of the N = 128 window convs (strided / transposed / 1x1): the slot they
+                      // free becomes a B slot for their long weight streams (e.g. the 32 x 1024
+                      // transposed conv 0.039 -> 0.032 ms/it; the apply streams A and keeps 4)
 #endif
 // CPS = CTAs per SM (1, or 2 for BN = 32: two independent pipelines per SM hide each other's
 // hand-off latency; each gets half of TMEM and ~113 KB of shared memory)
-template <int BN, int AM, bool ASPLIT = false, int CPS = 1>
+template <int BN, int AM, bool ASPLIT = false, int CPS = 1, bool APPLY = false>
 struct Plan {
   static constexpr int kBBytes = BN * 128;                          // one of B hi / B lo
   static constexpr int kATile = AM == 2 ? kSSRows * 128 : AM == 1 ? kHaloRows * 128 : kABytes;
@@ -126,16 +131,17 @@ struct Plan {
   // they need a deeper ring to cover the HBM latency (BN = 32 leaves room for 8)
   // (CPS = 2, N = 64: a single halo slot -- the other CTA on the SM covers its load latency)
   static constexpr int kNA = (AM != 0 || ASPLIT) ? (CPS == 2 && BN == 64 ? 1 : 2)
-                             : CPS == 2 ? (BN == 64 ? 2 : 3) : BN == 32 ? 8 : BN == 64 ? 4 : RTE_NA128;
+                             : CPS == 2 ? (BN == 64 ? 2 : 3) : BN == 32 ? 8 : BN == 64 ? 4
+                             : APPLY ? RTE_NA128 : RTE_NA128C;
   static constexpr int kNBraw = (kBudget - kNA * kASlot) / kBSlot;
   static constexpr int kNB = kNBraw > 8 ? 8 : kNBraw;               // B ring depth
   static_assert(kNB >= 1, "shared-memory plan leaves no B slot");
   static constexpr int kRingBytes = kNA * kASlot + kNB * kBSlot;
 };
 
-template <int BN, int AM, bool ASPLIT = false, int CPS = 1>
+template <int BN, int AM, bool ASPLIT = false, int CPS = 1, bool APPLY = false>
 constexpr int gemm_smem_bytes() {
-  return Plan<BN, AM, ASPLIT, CPS>::kRingBytes + 2 * stage_chunks<BN>() * kStageBytes + 1024 /*align*/ + 1024 /*barriers*/ +
+  return Plan<BN, AM, ASPLIT, CPS, APPLY>::kRingBytes + 2 * stage_chunks<BN>() * kStageBytes + 1024 /*align*/ + 1024 /*barriers*/ +
          1024 /*row centres*/;
 }
 
@@ -310,7 +316,7 @@ __global__ void __launch_bounds__(kGemmThreads, CPS)
   static_assert(!(ASPLIT && Epi::kCenter), "row centring needs the plain fp32 A operand");
   static_assert(!(SSH && ASPLIT), "SS-halo kernels split the activations themselves");
   static_assert(CPS == 1 || (CPS == 2 && BN <= 64 && !ASPLIT && AM != 2), "two CTAs per SM: BN <= 64 only");
-  using PL = Plan<BN, AM, ASPLIT, CPS>;
+  using PL = Plan<BN, AM, ASPLIT, CPS, Epi::kCenter>;
   constexpr int TCOLS = 512 / CPS;
   constexpr int NAR = PL::kNA, NBR = PL::kNB;
   constexpr int NA = tmem_abufs<BN, TCOLS>();
