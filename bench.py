@@ -5,11 +5,13 @@ BASELINE.json (default: config 5, 512^2 cells x M=256 ordinates, MgNet L=6 C0=32
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config k] [--impl ours|reference]
 
-A "step" is one GMRES inner iteration.  The timed region is ONE gmres_solve call
-of exactly K inner iterations from x0 = 0 (so it also carries the restart work: the fp64 residual
-at cycle start and the cycle-end update, amortised over the K steps), bracketed by a barrier and
-torch.cuda.synchronize() on both sides and timed with CUDA events on the launching stream; the
-reported time is the max over ranks.  Config-5 vectors are 256 MiB (> 126 MB L2), so every step
+A "step" is one whole GMRES(30) restart cycle: 30 inner iterations (V-cycle + apply + Arnoldi +
+Givens each) and the cycle end (back-solve, x += P(V y), the fp64 restart residual), DESIGN.md §7.
+Whole cycles, because an Arnoldi step's cost grows with j: a partial cycle would time only the
+cheap early steps.  The timed region is ONE gmres_solve call of exactly K cycles (30 K inner
+iterations) from x0 = 0, bracketed by a barrier and torch.cuda.synchronize() on both sides and
+timed with CUDA events on the launching stream; the reported time is the max over ranks, and
+value = inner iterations / s.  Config-5 vectors are 256 MiB (> 126 MB L2), so every step
 streams its inputs from HBM ("inputs larger than L2").  Multi-GPU: config 5 is ONE medium and does
 not shard without a halo exchange, so N ranks run N independent replicas (DESIGN.md §8,
 "replicas only"); value = total iterations of all ranks / max-over-ranks time ("scaling": "weak").
@@ -133,15 +135,64 @@ def _device_index(torch, local):
     return local
 
 
-def _roofline(classes, peaks, src):
-    """Roofline of the dominant kernel class (max total device time in the timed region)."""
+def _tensor_peaks(peaks):
+    """3xTF32 algorithmic-fp32 peaks (TFLOP/s): measured bf16 x the guide's nominal tf32/bf16 ratio /
+    3 MMAs per product; burst (a kernel timed alone / at full clocks) and sustained (power-capped)."""
+    burst = peaks.get("bf16_tflops", 1590.0) * TF32_PER_BF16 / 3.0
+    sus = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1400.0)) * TF32_PER_BF16 / 3.0
+    return burst, sus
+
+
+def _class_roofline_ms(c, peaks, tensor_peak):
+    """Roofline time of one class's launches: max(algorithmic bytes / HBM, flops / its compute peak)."""
+    smax = peaks.get("sm_max_mhz", 1965.0)
+    t_hbm = c["bytes"] / (peaks["hbm_gbs"] * 1e9) * 1e3
+    kind = c["kind"]
+    if kind == "tensor_3xtf32":
+        t_c = c["flops"] / (tensor_peak * 1e12) * 1e3
+    elif kind == "fp32_simt":
+        t_c = c["flops"] / (N_SM * 128 * 2 * smax * 1e6) * 1e3
+    elif kind == "fp64_simt":
+        t_c = c["flops"] / (N_SM * 64 * 2 * smax * 1e6) * 1e3
+    else:
+        t_c = 0.0
+    return max(t_hbm, t_c)
+
+
+# timing classes that are not the V-cycle (the Arnoldi/Givens/restart bookkeeping and the operator)
+_NOT_VCYCLE = ("apply_", "cgs_", "norm", "combine", "axpy64", "givens", "cycle_init", "backsolve", "rhs",
+               "scale_f64")
+
+
+def _composite_roofline(classes, select, peaks, label):
+    """Roofline of a multi-launch operator (the V-cycle): its roofline time is the sum over its
+    kernels of max(bytes/HBM, flops/peak); frac = roofline time / measured device time.  Both the
+    burst and the sustained 3xTF32 denominators are reported."""
+    sel = [c for c in classes if select(c["name"])]
+    if not sel:
+        return None
+    burst, sus = _tensor_peaks(peaks)
+    meas = sum(c["ms"] for c in sel)
+    r_b = sum(_class_roofline_ms(c, peaks, burst) for c in sel)
+    r_s = sum(_class_roofline_ms(c, peaks, sus) for c in sel)
+    return {"what": label, "measured_ms": meas, "roofline_ms_burst": r_b, "roofline_ms_sustained": r_s,
+            "frac": r_b / meas if meas else None, "frac_sustained": r_s / meas if meas else None,
+            "flops": sum(c["flops"] for c in sel), "bytes": sum(c["bytes"] for c in sel),
+            "classes": sorted(c["name"] for c in sel),
+            "peaks": {"tensor_3xtf32_burst_tflops": burst, "tensor_3xtf32_sustained_tflops": sus,
+                      "hbm_gbs": peaks["hbm_gbs"]},
+            "note": "per-class device times of the profiled solve (every launch bracketed by CUDA events)"}
+
+
+def _roofline(classes, peaks, src, top=None):
+    """Roofline of one kernel class (default: the dominant one, max total device time)."""
     if not classes:
         return None, None
-    top = max(classes, key=lambda c: c["ms"])
+    if top is None:
+        top = max(classes, key=lambda c: c["ms"])
     avg_ms = top["ms"] / max(top["launches"], 1)
     per_launch_flops = top["flops"] / max(top["launches"], 1)
     per_launch_bytes = top["bytes"] / max(top["launches"], 1)
-    sus = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
     smax = peaks.get("sm_max_mhz", 1965.0)
     kind = top["kind"]
     if kind == "hbm":
@@ -150,10 +201,11 @@ def _roofline(classes, peaks, src):
         note = f"HBM copy bandwidth ({src} MEASURED_PEAKS.json hbm_gbs)"
     elif kind == "tensor_3xtf32":
         ach = per_launch_flops / (avg_ms * 1e-3) / 1e12
-        peak = sus * TF32_PER_BF16 / 3.0
+        peak, peak_sus = _tensor_peaks(peaks)
         unit, bound = "TFLOP/s", "tensor"
-        note = (f"3xTF32 fp32-emulation peak = {src} sustained bf16 {sus} TF x {TF32_PER_BF16:.3f} (nominal "
-                "tf32/bf16) / 3 MMAs per product; achieved counts algorithmic fp32 flops")
+        note = (f"3xTF32 fp32-emulation peak = {src} burst bf16 {peaks.get('bf16_tflops')} TF x "
+                f"{TF32_PER_BF16:.3f} (nominal tf32/bf16) / 3 MMAs per product (sustained: {peak_sus:.1f} TF, "
+                f"frac_sustained); achieved counts algorithmic fp32 flops")
     elif kind == "fp32_simt":
         ach = per_launch_flops / (avg_ms * 1e-3) / 1e12
         peak = N_SM * 128 * 2 * smax * 1e6 / 1e12
@@ -176,6 +228,7 @@ def _roofline(classes, peaks, src):
             traffic = None
     roof = {"kernel": top["name"], "bound": bound, "achieved": ach, "peak": peak, "unit": unit,
             "frac": (ach / peak) if (ach is not None and peak) else None, "traffic": traffic,
+            **({"frac_sustained": ach / peak_sus} if kind == "tensor_3xtf32" else {}),
             "avg_launch_ms": avg_ms, "launches": top["launches"],
             "algorithmic_flops_per_launch": per_launch_flops, "algorithmic_bytes_per_launch": per_launch_bytes,
             "peak_source": note}
@@ -231,16 +284,18 @@ def run_reference(args, cfg):
     O.arnoldi_columns(lambda v: O.apply(sop, v), O.rhs(sop), lambda v: O.vcycle(snet, v), max(1, args.warmup))
     # bounded sample: at most K steps, capped so the run ends within a few minutes
     cap = max(2, int(3e8 // max(cfg.unknowns, 1)))
-    steps = max(1, min(args.steps, cap))
+    steps = max(1, min(args.steps * cfg.restart, cap))  # (inner iterations; a bench step is a cycle)
     t0 = time.perf_counter()
     O.arnoldi_columns(A, b, Pc, steps)
     dt = time.perf_counter() - t0
     val = steps / dt
-    line = {"metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus, "steps": steps,
-            "warmup": args.warmup, "ms_per_step": dt / steps * 1e3, "higher_is_better": True,
+    line = {"metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dt / steps * 1e3 * cfg.restart, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": _workload_name(cfg), "unknowns": cfg.unknowns},
+            "config": {"workload": _workload_name(cfg), "unknowns": cfg.unknowns,
+                       "step": f"one GMRES({cfg.restart}) restart cycle (timed on a bounded sample of "
+                               f"{steps} inner iterations; ms_per_step extrapolated per cycle)"},
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle",
                              "sample": f"{steps} Arnoldi steps (oracle.arnoldi_columns: V-cycle + apply + MGS) "
                                        f"of the fp64 numpy oracle on the full config-{cfg.k} problem "
@@ -282,7 +337,8 @@ def run_ours(args, cfg):
     b = torch.empty(p.shape, dtype=torch.float32, device=dev)
     P.rte_rhs(p, b)
     x = torch.zeros(p.shape, dtype=torch.float64, device=dev)
-    K, Wm = args.steps, args.warmup
+    # a step = one whole restart cycle (module docstring): K cycles = K * restart inner iterations
+    K, Wm = args.steps * cfg.restart, args.warmup * cfg.restart
     # x0 = 0 (the usual GMRES start): x0_zero sets x to 0 inside the call and skips A x0
     solve = lambda xx, bb, k: P.gmres_solve(p, net, bb, xx, restart=cfg.restart, maxit=k, rtol=1e-300,
                                             history=False, reorth=args.reorth, x0_zero=True)
@@ -383,12 +439,24 @@ def run_ours(args, cfg):
         kernels = sorted(({"name": c["name"], "kind": c["kind"], "launches": c["launches"],
                            "ms": round(c["ms"], 4), "share": round(c["ms"] / tot_ms, 4)} for c in all_classes),
                          key=lambda d: -d["ms"])
-        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": Wm,
-                "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "strong" if sharded else "weak",
+        roof_apply = None
+        app = [c for c in all_classes if c["name"].startswith("apply_f32")]
+        if app:
+            roof_apply, _ = _roofline(app, peaks, src, top=max(app, key=lambda c: c["ms"]))
+            roof_apply["timed"] = "profiled solve (every launch bracketed by CUDA events)"
+        roof_v = _composite_roofline(all_classes, lambda n: not n.startswith(_NOT_VCYCLE), peaks,
+                                     "MgNet V-cycle (lift, smoother/restriction/prolongation convs, split-K "
+                                     "reductions, head + pass-through)")
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+                "scaling": "strong" if sharded else "weak",
                 "vs_baseline": None,
                 "dtype": "f32", "data": "synthetic",
                 "config": {"workload": _workload_name(cfg) + (" + CoeffNet-modulated smoother" if args.coeffnet else ""),
                            "unknowns": cfg.unknowns,
+                           "step": f"one GMRES({cfg.restart}) restart cycle: {cfg.restart} inner iterations + "
+                                   "cycle end (back-solve, x += P(V y), fp64 restart residual)",
+                           "restart": cfg.restart, "inner_iterations_timed": K,
                            **({"coeffnet_setup_ms": round(coeffnet_ms, 1)} if args.coeffnet else {}),
                            "l2": "inputs larger than L2 (each vector 4 B x unknowns)" if cfg.unknowns * 4 > 126e6
                            else "working set L2-resident (small config)",
@@ -396,10 +464,10 @@ def run_ours(args, cfg):
                                            else f"replicas x{ws}" if ws > 1 else "single GPU"),
                            "precision": "fp32 storage/arithmetic, fp64 iterate, reductions and restart residual",
                            "gram_schmidt": {0: "CGS2", 1: "CGS1", 2: "selective (DGKS)"}[args.reorth]},
-                "roofline": roof,
+                "roofline": roof, "roofline_apply": roof_apply, "roofline_vcycle": roof_v,
                 "e2e": {"value": benchlib.aggregate(K, 1 if sharded else ws, ms_e2e), "unit": UNIT,
                         "h2d_bytes_per_step": h2d / K, "d2h_bytes_per_step": d2h / K,
-                        "note": f"one gmres_solve_host call of K={K} iterations (C ABI, host buffers): b (fp32) "
+                        "note": f"one gmres_solve_host call of {K} iterations (C ABI, host buffers): b (fp32) "
                                 "copied H2D from pinned host memory inside it, x (fp64) D2H into pinned memory "
                                 "(overlapping the closing fp64 residual); bytes amortised per step"},
                 "gpu_launches": launches, "clocks": clocks, "ops": ops, "kernels": kernels}
@@ -413,8 +481,8 @@ def run_ours(args, cfg):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=3, help="restart cycles timed (x restart inner iterations)")
+    ap.add_argument("--warmup", type=int, default=3, help="untimed warm-up cycles")
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -44,7 +44,9 @@ typedef enum {
   RTE_EINVAL = 1,    /* invalid argument (message says which) */
   RTE_ENOMEM = 2,    /* device or host allocation failed */
   RTE_ECUDA = 3,     /* CUDA error (message holds cudaGetErrorString) */
-  RTE_EINTERNAL = 4
+  RTE_EINTERNAL = 4,
+  RTE_ENUMERIC = 5   /* gmres_solve: a non-finite (NaN/Inf) Arnoldi column stopped a sample; the
+                        reports are filled and that sample's breakdown is 2 */
 } rte_status;
 
 /* Uniform grid on the unit square; nx == ny == N required; h = 1/N. */
@@ -165,7 +167,8 @@ rte_status rte_blockjacobi_apply_f64(const rte_problem* p, const double* r_dev, 
  * products accumulate in float64; every restart recomputes r = b - A x in float64.  The batch's
  * samples are independent solves with their own Arnoldi/Givens state. */
 typedef struct {
-  int restart;       /* m, 1..64 */
+  int restart;       /* m, 1..32 (gmres_prepare, gmres_solve and gmres_solve_host alike; a call
+                        with another m than the cached workspace's re-allocates it) */
   int maxit;         /* cap on total inner iterations per sample */
   double rtol;       /* stop when ||b - A x|| <= rtol ||b|| */
   int precond;       /* 0 none, 1 MgNet (I + V), 2 block Jacobi */
@@ -185,7 +188,9 @@ typedef struct {
   int iterations;    /* total inner iterations */
   int restarts;      /* cycles started */
   int converged;     /* true residual <= rtol ||b|| at exit */
-  int breakdown;     /* lucky breakdown happened */
+  int breakdown;     /* 0 none; 1 lucky breakdown (h_{j+1,j} <= 1e-14 |col|: the Krylov space is
+                        invariant, the solve ends); 2 a non-finite Arnoldi column stopped the
+                        sample (x keeps the update of the finite columns; RTE_ENUMERIC) */
   double relres_true;/* ||b - A x|| / ||b|| in float64 at exit */
   double relres_est; /* last Arnoldi estimate |g_{j+1}| / ||b|| */
   double* history;   /* optional caller buffer, >= maxit doubles: estimate after each iteration */

@@ -13,7 +13,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 from . import _lib
-from ._lib import RteError, check, gmres_opts, gmres_report, lib
+from ._lib import RTE_ENUMERIC, RTE_OK, RteError, check, gmres_opts, gmres_report, lib
 
 __all__ = ["Problem", "MgNet", "rte_setup", "rte_rhs", "rte_apply", "rte_apply_f64", "rte_blockjacobi_apply", "mgnet_create",
            "mgnet_vcycle", "mgnet_vcycle_f64", "mgnet_coeffnet", "mgnet_coeffnet_weight_count", "mgnet_modulation", "gmres_prepare", "gmres_solve", "gmres_solve_host", "rte_quadrature", "rte_hg_matrix", "rte_launch_count", "rte_timing_enable", "rte_timing_filter", "rte_timing_reset",
@@ -249,18 +249,24 @@ def _gmres_call(name, fn, p, net, b_ptr, x_ptr, restart, maxit, rtol, precond, r
     for i in range(B):
         reps[i].history = _dptr(hist[i]) if history else None
         reps[i].hessenberg = _dptr(hess[i]) if hessenberg else None
-    check(name, fn(p.handle, net.handle if net is not None else None, b_ptr, x_ptr, C.byref(opts), reps,
-                   C.c_void_p(_stream(stream))))
+    status = fn(p.handle, net.handle if net is not None else None, b_ptr, x_ptr, C.byref(opts), reps,
+                C.c_void_p(_stream(stream)))
+    if status not in (RTE_OK, RTE_ENUMERIC):
+        check(name, status)
     out = []
     for i in range(B):
         r = reps[i]
         d = dict(iterations=r.iterations, restarts=r.restarts, converged=bool(r.converged),
-                 breakdown=bool(r.breakdown), relres_true=r.relres_true, relres_est=r.relres_est)
+                 breakdown=int(r.breakdown), relres_true=r.relres_true, relres_est=r.relres_est)
         if history:
             d["history"] = hist[i][:r.iterations].copy()
         if hessenberg:
             d["hessenberg"] = hess[i].reshape(restart + 1, restart)
         out.append(d)
+    if status == RTE_ENUMERIC:  # a NaN/Inf stopped a sample: loud, with the filled reports attached
+        err = RteError(name, status)
+        err.reports = out
+        raise err
     return out
 
 

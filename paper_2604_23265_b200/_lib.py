@@ -18,7 +18,7 @@ if not os.path.exists(LIB_PATH):
                       "(there is no CPU fallback)")
 lib = C.CDLL(LIB_PATH)
 
-RTE_OK, RTE_EINVAL, RTE_ENOMEM, RTE_ECUDA, RTE_EINTERNAL = range(5)
+RTE_OK, RTE_EINVAL, RTE_ENOMEM, RTE_ECUDA, RTE_EINTERNAL, RTE_ENUMERIC = range(6)
 
 
 class rte_grid(C.Structure):

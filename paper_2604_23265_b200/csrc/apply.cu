@@ -42,7 +42,7 @@ __global__ void rhs_kernel(int B, int N, int M, const float* __restrict__ f, con
 template <typename T, int TMO>
 __global__ void __launch_bounds__(256) apply_simt_kernel(
     int N, int M, const T* __restrict__ x, T* __restrict__ y, const T* __restrict__ St,
-    const T* __restrict__ sig_t, const T* __restrict__ sig_s, const T* __restrict__ axv,
+    const T* __restrict__ sig_d, const T* __restrict__ sig_s, const T* __restrict__ axv,
     const T* __restrict__ ayv, const int8_t* __restrict__ sgx, const int8_t* __restrict__ sgy,
     const float* __restrict__ bvec, const double* __restrict__ alpha, int alpha_stride) {
   constexpr int TP = 4096 / TMO;
@@ -104,19 +104,17 @@ __global__ void __launch_bounds__(256) apply_simt_kernel(
     if (cell >= cells) continue;
     int i = (int)(cell % N), j = (int)(cell / N);
     int64_t gcell = (int64_t)bsample * cells + cell;
-    T st = sig_t[gcell], ss = sig_s[gcell];
+    const T sd = sig_d[gcell], ss = sig_s[gcell];
     const T cc = xs[cell * M];
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       int m = m0 + tx * 4 + c;
       if (m >= M) continue;
-      T ax = axv[m], ay = ayv[m];
-      T psi = xs[cell * M + m];
-      T v = (ax + ay + st) * psi - ss * (cc + acc[a][c]);
-      int ii = i - sgx[m], jj = j - sgy[m];
-      if (ii >= 0 && ii < N) v -= ax * xs[(cell - sgx[m]) * M + m];
-      if (jj >= 0 && jj < N) v -= ay * xs[(cell - (int64_t)sgy[m] * N) * M + m];
-      v *= al;
+      const T psi = xs[cell * M + m];
+      const int ii = i - sgx[m], jj = j - sgy[m];
+      const T nx = (ii >= 0 && ii < N) ? xs[(cell - sgx[m]) * M + m] : T(0);
+      const T ny = (jj >= 0 && jj < N) ? xs[(cell - (int64_t)sgy[m] * N) * M + m] : T(0);
+      T v = al * stencil_diag(axv[m], ayv[m], sd, ss, psi, nx, ny, cc, acc[a][c]);
       int64_t o = gcell * M + m;
       if (bvec) v = (T)bvec[o] - v;
       y[o] = v;
@@ -132,7 +130,7 @@ __global__ void __launch_bounds__(256) apply_simt_kernel(
 template <typename T>
 __global__ void __launch_bounds__(256) apply_simt_wide_kernel(
     int N, int M, const T* __restrict__ x, T* __restrict__ y, const T* __restrict__ St,
-    const T* __restrict__ sig_t, const T* __restrict__ sig_s, const T* __restrict__ axv,
+    const T* __restrict__ sig_d, const T* __restrict__ sig_s, const T* __restrict__ axv,
     const T* __restrict__ ayv, const int8_t* __restrict__ sgx, const int8_t* __restrict__ sgy,
     const float* __restrict__ bvec, const double* __restrict__ alpha, int alpha_stride) {
   constexpr int TP = 128, TMO = 128, KC = 8;
@@ -213,18 +211,16 @@ __global__ void __launch_bounds__(256) apply_simt_wide_kernel(
     if (cell >= cells) continue;
     const int i = (int)(cell % N), j = (int)(cell / N);
     const int64_t gcell = (int64_t)bsample * cells + cell;
-    const T st = sig_t[gcell], ss = sig_s[gcell];
+    const T sd = sig_d[gcell], ss = sig_s[gcell];
     const T cc = xs[cell * M];
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       const int m = m0 + 64 * (c / 4) + tx * 4 + (c % 4);
-      const T ax = axv[m], ay = ayv[m];
       const T psi = xs[cell * M + m];
-      T v = (ax + ay + st) * psi - ss * (cc + acc[a][c]);
       const int ii = i - sgx[m], jj = j - sgy[m];
-      if (ii >= 0 && ii < N) v -= ax * xs[(cell - sgx[m]) * M + m];
-      if (jj >= 0 && jj < N) v -= ay * xs[(cell - (int64_t)sgy[m] * N) * M + m];
-      v *= al;
+      const T nx = (ii >= 0 && ii < N) ? xs[(cell - sgx[m]) * M + m] : T(0);
+      const T ny = (jj >= 0 && jj < N) ? xs[(cell - (int64_t)sgy[m] * N) * M + m] : T(0);
+      T v = al * stencil_diag(axv[m], ayv[m], sd, ss, psi, nx, ny, cc, acc[a][c]);
       const int64_t o = gcell * M + m;
       if (bvec) v = (T)bvec[o] - v;
       y[o] = v;
@@ -240,7 +236,7 @@ __global__ void __launch_bounds__(256) apply_simt_wide_kernel(
 // col = lane/4; C row = lane/4, cols 2(lane%4) + {0, 1}.  Same epilogue as apply_simt_kernel.
 __global__ void __launch_bounds__(256) apply_dmma_kernel(
     int N, int M, const double* __restrict__ x, double* __restrict__ y, const double* __restrict__ St,
-    const double* __restrict__ sig_t, const double* __restrict__ sig_s, const double* __restrict__ axv,
+    const double* __restrict__ sig_d, const double* __restrict__ sig_s, const double* __restrict__ axv,
     const double* __restrict__ ayv, const int8_t* __restrict__ sgx, const int8_t* __restrict__ sgy,
     const float* __restrict__ bvec) {
   constexpr int TP = 128, TM = 64, KC = 8, PA = TP + 4, PB = TM + 4;
@@ -326,18 +322,17 @@ __global__ void __launch_bounds__(256) apply_dmma_kernel(
     if (cell >= cells) continue;
     const int ci = (int)(cell % N), cj = (int)(cell / N);
     const int64_t gcell = (int64_t)bsample * cells + cell;
-    const double st = sig_t[gcell], ss = sig_s[gcell];
+    const double sd = sig_d[gcell], ss = sig_s[gcell];
     const double cc = xs[cell * M];
 #pragma unroll
     for (int j = 0; j < 4; ++j)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int m = m0 + wn * 32 + 8 * j + 2 * fk + h;
-        const double ax = axv[m], ay = ayv[m];
-        double v = (ax + ay + st) * xs[cell * M + m] - ss * (cc + acc[i][j][h]);
         const int ii = ci - sgx[m], jj = cj - sgy[m];
-        if (ii >= 0 && ii < N) v -= ax * xs[(cell - sgx[m]) * M + m];
-        if (jj >= 0 && jj < N) v -= ay * xs[(cell - (int64_t)sgy[m] * N) * M + m];
+        const double nx = (ii >= 0 && ii < N) ? xs[(cell - sgx[m]) * M + m] : 0.0;
+        const double ny = (jj >= 0 && jj < N) ? xs[(cell - (int64_t)sgy[m] * N) * M + m] : 0.0;
+        double v = stencil_diag(axv[m], ayv[m], sd, ss, xs[cell * M + m], nx, ny, cc, acc[i][j][h]);
         const int64_t o = gcell * M + m;
         if (bvec) v = (double)bvec[o] - v;
         y[o] = v;
@@ -400,13 +395,13 @@ void launch_apply_f32(const rte_problem* p, const float* x, float* y, const doub
     return;
   }
   prof_begin(st, "apply_f32_simt");
-  launch_simt<float>(p, x, y, p->St32, p->sig_t, p->sig_s, p->ax, p->ay, nullptr, alpha, alpha_stride, st);
+  launch_simt<float>(p, x, y, p->St32, p->sig_d, p->sig_s, p->ax, p->ay, nullptr, alpha, alpha_stride, st);
   after_launch("apply_f32_simt", st, apply_flops(p), apply_bytes(p, 4, 0), 2);
 }
 
 void launch_apply_f64(const rte_problem* p, const double* x, double* y, const float* b, cudaStream_t st) {
   prof_begin(st, "apply_f64_simt");
-  launch_simt<double>(p, x, y, p->St64, p->sig_t64, p->sig_s64, p->ax64, p->ay64, b, nullptr, 0, st);
+  launch_simt<double>(p, x, y, p->St64, p->sig_d64, p->sig_s64, p->ax64, p->ay64, b, nullptr, 0, st);
   after_launch("apply_f64_simt", st, apply_flops(p), apply_bytes(p, 8, b ? 4 : 0), 3);
 }
 

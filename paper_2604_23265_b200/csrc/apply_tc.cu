@@ -4,6 +4,8 @@
 // the sigma_t diagonal in the epilogue (R9):
 //   y_{jim} = alpha [ (|c_m|/h + |s_m|/h + sigma_t) psi_{jim} - sigma_s (Psi S^T)_{jim}
 //                     - (|c_m|/h) psi_{j,i-sgn c_m,m} - (|s_m|/h) psi_{j-sgn s_m,i,m} ]
+// evaluated as stencil_diag (common.h): a_x (psi - nx) + a_y (psi - ny) + (sigma_t - sigma_s) psi
+// + sigma_s ((psi - c) - [S (psi - c)]), the same operator with no sigma_t psi product to cancel.
 // The epilogue runs warp-per-cell with lane = ordinate (coalesced 128-byte rows); psi at the cell
 // and at its two upwind neighbours is re-read from L2 (the A tiles just streamed through it).
 // Conservation-preserving contraction: because S is row-stochastic (R5),
@@ -27,7 +29,7 @@ struct EpiApply {
   static constexpr bool kCenter = true;
   const float* x;
   float* y;
-  const float* sig_t;
+  const float* sig_d;  // sigma_t - sigma_s (= eps sigma_a)
   const float* sig_s;
   const float* ax;
   const float* ay;
@@ -47,7 +49,7 @@ struct EpiApply {
   struct Row {
     long long cell;
     int i, j;
-    float st, ss, al, c;
+    float sd, ss, al, c;
   };
   struct Pre {
     float4 p, nx, ny;  // psi at the cell and at its two upwind neighbours (0 at inflow faces)
@@ -67,7 +69,7 @@ struct EpiApply {
   // tile pixel (oy, ox) of the class grid = cell (j, i)
   __device__ __forceinline__ Row row(const Tile& t, int rel, int j, int i, float c) const {
     const long long cell = t.cell0 + rel;
-    return Row{cell, i, j, sig_t[cell], sig_s[cell], t.al, c};
+    return Row{cell, i, j, sig_d[cell], sig_s[cell], t.al, c};
   }
   __device__ __forceinline__ Pre load(const Row& rw, const Col& cv) const {
     const long long cell = rw.cell;
@@ -82,12 +84,12 @@ struct EpiApply {
   }
   __device__ __forceinline__ void store4(const Row& rw, const Col& cv, float4 v, const Pre& q) const {
     const float4 a_x = cv.a_x, a_y = cv.a_y, p = q.p, nx = q.nx, ny = q.ny;
-    const float st = rw.st, ss = rw.ss, al = rw.al, c = rw.c;
+    const float sd = rw.sd, ss = rw.ss, al = rw.al, c = rw.c;
     float4 r;
-    r.x = al * ((a_x.x + a_y.x + st) * p.x - ss * (c + v.x) - a_x.x * nx.x - a_y.x * ny.x);
-    r.y = al * ((a_x.y + a_y.y + st) * p.y - ss * (c + v.y) - a_x.y * nx.y - a_y.y * ny.y);
-    r.z = al * ((a_x.z + a_y.z + st) * p.z - ss * (c + v.z) - a_x.z * nx.z - a_y.z * ny.z);
-    r.w = al * ((a_x.w + a_y.w + st) * p.w - ss * (c + v.w) - a_x.w * nx.w - a_y.w * ny.w);
+    r.x = al * stencil_diag(a_x.x, a_y.x, sd, ss, p.x, nx.x, ny.x, c, v.x);
+    r.y = al * stencil_diag(a_x.y, a_y.y, sd, ss, p.y, nx.y, ny.y, c, v.y);
+    r.z = al * stencil_diag(a_x.z, a_y.z, sd, ss, p.z, nx.z, ny.z, c, v.z);
+    r.w = al * stencil_diag(a_x.w, a_y.w, sd, ss, p.w, nx.w, ny.w, c, v.w);
     __stcs(reinterpret_cast<float4*>(y + rw.cell * M + cv.m), r);  // evict-first: keeps the prefetched inputs in L2
   }
   __device__ __forceinline__ void store_partial4(int, const Row&, int, float4) const {}
@@ -157,7 +159,7 @@ void launch_apply_tc(const rte_problem* p, const float* x, float* y, const doubl
   CUtensorMap ta = tc::make_map_act(x, M, N, N, B, g.TW, g.TH, 1);
   CUtensorMap tbh = tc::make_map_kmajor(p->S_hi, M, B * M, BN);
   CUtensorMap tbl = tc::make_map_kmajor(p->S_lo, M, B * M, BN);
-  tc::EpiApply epi{x, y, p->sig_t, p->sig_s, p->ax, p->ay, p->sgx, p->sgy, alpha, alpha_stride, N, M};
+  tc::EpiApply epi{x, y, p->sig_d, p->sig_s, p->ax, p->ay, p->sgx, p->sgy, alpha, alpha_stride, N, M};
   prof_begin(st, "apply_f32_tc");
   switch (BN) {
     case 32: tc::launch_apply_bn<32>(g, mtiles, ta, tbh, tbl, te, epi, st); break;

@@ -64,6 +64,22 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 
 int num_sms();
 
+#ifdef __CUDACC__
+// One output of the operator (PAPER.md:91-93 eq:DORTE_2d, upwind stencil R9) from the cell's psi,
+// its two upwind neighbours nx, ny (0 outside the grid), the centre c = psi_{cell, 0} and the
+// centred contraction v = [S (psi - c)]_m (S row-stochastic, R5):
+//   (A psi)_m = a_x (psi - nx) + a_y (psi - ny) + (sigma_t - sigma_s) psi + sigma_s ((psi - c) - v)
+// This is eq:DORTE_2d rearranged exactly (sigma_t psi - sigma_s S psi = (sigma_t - sigma_s) psi +
+// sigma_s (psi - S psi), S psi = c + v), with sigma_t - sigma_s = eps sigma_a (sd) taken from the
+// host in fp64.  Written this way no product of sigma_t ~ 1/eps with psi is ever formed, so in the
+// diffusive regime (sigma_t ~ 1e2..1e6, eps sigma_a ~ 1e-3) nothing cancels at the scale of
+// sigma_t psi; the rounding error scales with the terms that survive.
+template <typename T>
+__host__ __device__ __forceinline__ T stencil_diag(T ax, T ay, T sd, T ss, T psi, T nx, T ny, T c, T v) {
+  return fma(ax, psi - nx, fma(ay, psi - ny, fma(sd, psi, ss * ((psi - c) - v))));
+}
+#endif
+
 }  // namespace rte
 
 // ---- problem ----------------------------------------------------------------
@@ -75,8 +91,10 @@ struct rte_problem {
   std::vector<double> c, s, zeta, w;
   std::vector<double> S;   // [B][M][M] row-stochastic K W
   // device
-  float* sig_t = nullptr;   // [B][N][N]
-  float* sig_s = nullptr;
+  float* sig_t = nullptr;   // [B][N][N]  sigma_T / eps
+  float* sig_s = nullptr;   //            sigma_T / eps - eps sigma_a
+  float* sig_d = nullptr;   //            sigma_t - sigma_s = eps sigma_a (stencil_diag)
+  double* sig_d64 = nullptr;
   float* f = nullptr;
   double* sig_t64 = nullptr;
   double* sig_s64 = nullptr;

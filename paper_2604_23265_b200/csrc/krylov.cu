@@ -27,7 +27,8 @@ namespace rte {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kMaxRestart = 64;
+constexpr int kMaxRestart = 64;     // array bound of the per-sample device scratch
+constexpr int kMaxRestartApi = 32;  // restart range accepted by the API (the fused CGS kernels' NV)
 
 struct RedArgs {
   double* partials;   // [B][nblk][nq]
@@ -313,7 +314,23 @@ __global__ void givens_kernel(int B, int j, int m, const double* __restrict__ h1
     if (!use_h2) nr = h2 + (int64_t)b * h_ld + j + 1;
   }
   double col[kMaxRestart + 1];
-  for (int i = 0; i <= j; ++i) col[i] = h1[(int64_t)b * h_ld + i] + (use_h2 ? h2[(int64_t)b * h_ld + i] : 0.0);
+  bool finite = isfinite(*nr);
+  for (int i = 0; i <= j; ++i) {
+    col[i] = h1[(int64_t)b * h_ld + i] + (use_h2 ? h2[(int64_t)b * h_ld + i] : 0.0);
+    finite = finite && isfinite(col[i]);
+  }
+  if (!finite) {
+    // NaN/Inf guard: a non-finite Arnoldi column (an operator or preconditioner that produced
+    // NaN/Inf) stops the sample before anything of this step is applied; the cycle-end update
+    // uses the j finite columns before it (breakdown = 2, gmres_solve returns RTE_ENUMERIC)
+    active[b] = 0;
+    kcols[b] = j;
+    st[b].est = NAN;
+    st[b].active = 0;
+    st[b].breakdown = 2;
+    st[b].kcols = j;
+    return;
+  }
   double hj1 = sqrt(fmax(*nr, 0.0));
   const int ldh = m;  // H stored [B][m+1][m]
   double* Hb = Hr + (int64_t)b * (m + 1) * m;
@@ -613,7 +630,9 @@ static void run_step_operator(const rte_problem* p, const mgnet_net* net, GmresW
 static GmresWork& get_work(const rte_problem* p, int m) {
   std::lock_guard<std::mutex> lk(g_wmu);
   GmresWork& W = g_work[p];
-  if (W.V && W.m >= m) return W;
+  // exact match only: every per-sample array (alpha, g, coef, H, the fp64 basis) is laid out with
+  // stride m + 1 and captured graphs bake W.m in, so a different restart re-allocates
+  if (W.V && W.m == m) return W;
   W.release();
   W.B = p->B;
   W.m = m;
@@ -655,7 +674,7 @@ static GmresWork& get_work(const rte_problem* p, int m) {
 extern "C" rte_status gmres_prepare(const rte_problem* p, const mgnet_net* net, const gmres_opts* opts, void* stream) {
   try {
     RTE_REQUIRE(p && opts, "gmres_prepare: NULL argument");
-    RTE_REQUIRE(opts->restart >= 1 && opts->restart <= kMaxRestart, "gmres_prepare: restart out of range");
+    RTE_REQUIRE(opts->restart >= 1 && opts->restart <= kMaxRestartApi, "gmres_prepare: restart must be in [1, 32]");
     RTE_REQUIRE(opts->precond == 0 || opts->precond == 2 || (opts->precond == 1 && net),
                 "gmres_prepare: precond must be 0, 1 (with a net) or 2");
     if (!graphs_enabled() || opts->precision == 1) return RTE_OK;  // (the fp64 mode runs eagerly)
@@ -692,7 +711,7 @@ static rte_status solve_impl(const rte_problem* p, const mgnet_net* net, const f
   try {
     RTE_REQUIRE(p && b_dev && x_dev && opts && rep, "gmres_solve: NULL argument");
     const int m = opts->restart;
-    RTE_REQUIRE(m >= 1 && m <= 32, "gmres_solve: restart must be in [1, 32]");
+    RTE_REQUIRE(m >= 1 && m <= kMaxRestartApi, "gmres_solve: restart must be in [1, 32]");
     RTE_REQUIRE(opts->maxit >= 0, "gmres_solve: maxit must be >= 0");
     RTE_REQUIRE(opts->rtol > 0.0, "gmres_solve: rtol must be > 0");
     RTE_REQUIRE(opts->precond == 0 || opts->precond == 2 || (opts->precond == 1 && net),
@@ -778,12 +797,12 @@ static rte_status solve_impl(const rte_problem* p, const mgnet_net* net, const f
         int still = 0;
         for (int b = 0; b < B; ++b) {
           const Status& s = slot[b];
-          bool was_active = (s.active || s.kcols == k + 1);
+          bool was_active = (s.active || s.kcols == k + 1 || (s.breakdown == 2 && s.kcols == k));
           if (!was_active) continue;
           if (rep[b].history) rep[b].history[total[b]] = s.est;
           ++total[b];
           est_last[b] = s.est;
-          if (s.breakdown) brk[b] = 1;
+          if (s.breakdown) brk[b] = s.breakdown;
           if (s.active) ++still;
         }
         return still;
@@ -953,6 +972,12 @@ static rte_status solve_impl(const rte_problem* p, const mgnet_net* net, const f
       RTE_CHECK_CUDA(cudaMemcpyAsync(ho->x_host, x_dev, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
     RTE_CHECK_CUDA(cudaStreamSynchronize(st));
     if (ho && ho->copied) RTE_CHECK_CUDA(cudaEventSynchronize(W.ev_cp));
+    for (int b = 0; b < B; ++b)
+      if (brk[b] == 2) {
+        set_error("gmres_solve: non-finite value (NaN/Inf) in the Arnoldi process of sample " + std::to_string(b) +
+                  " at iteration " + std::to_string(total[b]) + "; the reports are filled (breakdown = 2)");
+        return RTE_ENUMERIC;
+      }
     return RTE_OK;
   } catch (const Fail& f) {
     return f.st;
@@ -971,7 +996,7 @@ extern "C" rte_status gmres_solve_host(const rte_problem* p, const mgnet_net* ne
                                        double* x_host, const gmres_opts* opts, gmres_report* rep, void* stream) {
   try {
     RTE_REQUIRE(p && b_host && x_host && opts && rep, "gmres_solve_host: NULL argument");
-    RTE_REQUIRE(opts->restart >= 1 && opts->restart <= 32, "gmres_solve: restart must be in [1, 32]");
+    RTE_REQUIRE(opts->restart >= 1 && opts->restart <= kMaxRestartApi, "gmres_solve: restart must be in [1, 32]");
     GmresWork& W = get_work(p, opts->restart);
     const int64_t n = p->n;
     if (!W.bh) {

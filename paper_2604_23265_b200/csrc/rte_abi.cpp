@@ -303,7 +303,7 @@ rte_status rte_timing_get(int idx, char* name, int name_len, int* kind, int64_t*
 
 static void free_problem(rte_problem* p) {
   if (!p) return;
-  void* ptrs[] = {p->sig_t, p->sig_s, p->f, p->sig_t64, p->sig_s64, p->S32, p->St32, p->St64, p->S_hi,
+  void* ptrs[] = {p->sig_t, p->sig_s, p->sig_d, p->sig_d64, p->f, p->sig_t64, p->sig_s64, p->S32, p->St32, p->St64, p->S_hi,
                   p->S_lo, p->ax, p->ay, p->ax64, p->ay64, p->sgx, p->sgy, p->inflow, p->scratch64,
                   p->bj64, p->bj32};
   for (void* q : ptrs) dfree(q);
@@ -351,8 +351,8 @@ rte_status rte_setup(const rte_grid* grid, const rte_ordinates* ord, const float
     p->n = p->ncell * M;
     const double h = 1.0 / N;
     // coefficients (R7)
-    std::vector<float> st(p->ncell), ss(p->ncell), ff(p->ncell);
-    std::vector<double> st64(p->ncell), ss64(p->ncell);
+    std::vector<float> st(p->ncell), ss(p->ncell), ff(p->ncell), sd(p->ncell);
+    std::vector<double> st64(p->ncell), ss64(p->ncell), sd64(p->ncell);
     for (int64_t k = 0; k < p->ncell; ++k) {
       double e = eps[k], sT = sigma_T[k], sA = sigma_a[k];
       RTE_REQUIRE(e > 0.0 && e <= 1.0, "rte_setup: eps must lie in (0,1]");
@@ -363,6 +363,8 @@ rte_status rte_setup(const rte_grid* grid, const rte_ordinates* ord, const float
       ss64[k] = sc;
       st[k] = (float)t;
       ss[k] = (float)sc;
+      sd64[k] = e * sA;  // sigma_t - sigma_s, formed without the cancellation
+      sd[k] = (float)sd64[k];
       ff[k] = (float)(e * (double)q[k]);
     }
     // scattering matrices per sample
@@ -403,6 +405,8 @@ rte_status rte_setup(const rte_grid* grid, const rte_ordinates* ord, const float
     p->f = dalloc<float>(p->ncell); upload(p->f, ff.data(), p->ncell);
     p->sig_t64 = dalloc<double>(p->ncell); upload(p->sig_t64, st64.data(), p->ncell);
     p->sig_s64 = dalloc<double>(p->ncell); upload(p->sig_s64, ss64.data(), p->ncell);
+    p->sig_d = dalloc<float>(p->ncell); upload(p->sig_d, sd.data(), p->ncell);
+    p->sig_d64 = dalloc<double>(p->ncell); upload(p->sig_d64, sd64.data(), p->ncell);
     size_t mm = (size_t)B * M * M;
     p->S32 = dalloc<float>(mm); upload(p->S32, S32.data(), mm);
     p->St32 = dalloc<float>(mm); upload(p->St32, St32.data(), mm);

@@ -139,3 +139,75 @@ def test_config_weight_counts():
     mib = {k: W.mgnet_weight_count(c.M, c.L, c.C0, c.nu) * 4 / 2 ** 20 for k, c in W.CONFIGS.items()}
     for k, v in {1: 1.2, 2: 4.8, 3: 19, 4: 77, 5: 307}.items():
         assert abs(mib[k] - v) / v < 0.05, (k, mib[k])
+
+
+# ---------------------------------------------------------------------------------------------
+# Two-level closed form (multi-level branch of vcycle) and the packed weight
+# order (reading R20/Q20), pinned together.  Every 3x3 / 4x4 kernel has only its centre tap
+# (ky = kx = 1) non-zero, so each conv is a per-pixel channel matrix: the stride-2 restriction
+# reads fine pixel (2y, 2x) (pad 1: padded index 2y + 1 = input 2y) and the transposed conv adds
+# into fine pixel (2y, 2x) (2y - 1 + 1).  The V-cycle then collapses to per-pixel matrix algebra
+# written out below by hand from the algorithm's steps: pre-smooth, restrict the residual of the
+# pre-smoothed u, 2 nu coarse steps (pre then post B), prolongate-and-add, post-smooth, head.
+# All channel matrices are random and non-symmetric and every B is distinct, so a wrong step order,
+# a swapped pre/post set, a restriction of f instead of the residual, an OIHW/IOHW transposition
+# or a misplaced block in the packed vector changes the result.
+# ---------------------------------------------------------------------------------------------
+def _pack_r20(blocks):
+    """Pack named tensors in the order DESIGN.md R20 states, written out here independently of
+    workloads.mgnet_weight_shapes and oracle.unpack_weights: Lambda; per level l: A^l, pre B x nu,
+    post B x nu, then (l < L-1) R^l (OIHW) and P^l (IOHW); Theta."""
+    return np.concatenate([blocks[k].ravel() for k in blocks])
+
+
+def _centre(mat, kh):
+    """[O][I] (or [I][O] for IOHW) channel matrix -> kernel with only the centre tap set."""
+    Wk = np.zeros(mat.shape + (kh, kh))
+    Wk[:, :, 1, 1] = mat
+    return Wk
+
+
+@pytest.mark.parametrize("nu", [1, 2])
+def test_two_level_closed_form_and_weight_order(nu):
+    M, C0, L = 3, 2, 2
+    C1 = 2 * C0
+    rng = np.random.default_rng(11 + nu)
+    mats = {}
+    blocks = {}
+    mats["Lambda"] = rng.standard_normal((C0, M))
+    blocks["Lambda"] = mats["Lambda"].reshape(C0, M, 1, 1)
+    for l, C in ((0, C0), (1, C1)):
+        for nm in [f"A{l}"] + [f"Bpre{l}_{i}" for i in range(nu)] + [f"Bpost{l}_{i}" for i in range(nu)]:
+            mats[nm] = 0.5 * rng.standard_normal((C, C))
+            blocks[nm] = _centre(mats[nm], 3)
+        if l == 0:
+            mats["R0"] = rng.standard_normal((C1, C0))          # OIHW: out = R0 @ in
+            blocks["R0"] = _centre(mats["R0"], 3)
+            mats["P0"] = rng.standard_normal((C1, C0))          # IOHW: out = P0.T @ in
+            blocks["P0"] = _centre(mats["P0"], 4)
+    mats["Theta"] = rng.standard_normal((M, C0))
+    blocks["Theta"] = mats["Theta"].reshape(M, C0, 1, 1)
+    w = _pack_r20(blocks)
+    assert w.size == W.mgnet_weight_count(M, L, C0, nu)
+    net = O.make_mgnet(w, M, L, C0, nu)
+
+    H = 6
+    r = rng.standard_normal((1, H, H, M))
+    expect = np.array(r)
+    m = mats
+    smooth = lambda u, f, A, Bs: [u := u + B @ (f - A @ u) for B in Bs][-1]
+    for y in range(H):
+        for x in range(H):
+            f0 = m["Lambda"] @ r[0, y, x]
+            u0 = smooth(np.zeros(C0), f0, m["A0"], [m[f"Bpre0_{i}"] for i in range(nu)])
+            if y % 2 == 0 and x % 2 == 0:                      # fine pixel (2y', 2x') of coarse (y', x')
+                f1 = m["R0"] @ (f0 - m["A0"] @ u0)
+                u1 = smooth(np.zeros(C1), f1, m["A1"],
+                            [m[f"Bpre1_{i}"] for i in range(nu)] + [m[f"Bpost1_{i}"] for i in range(nu)])
+                u0 = u0 + m["P0"].T @ u1
+            u0 = smooth(u0, f0, m["A0"], [m[f"Bpost0_{i}"] for i in range(nu)])
+            expect[0, y, x] += m["Theta"] @ u0
+    got = O.vcycle(net, r)
+    assert np.allclose(got, expect, rtol=1e-12, atol=1e-12)
+    # and the workloads layout the CUDA path is fed with is this same order
+    assert [n for n, _ in W.mgnet_weight_shapes(M, L, C0, nu)] == list(blocks)

@@ -21,7 +21,7 @@ import numpy as np
 
 __all__ = [
     "Config", "CONFIGS", "config", "Media", "make_media", "mgnet_weight_shapes",
-    "mgnet_weight_count", "make_weights", "make_vector", "grf", "small_config",
+    "mgnet_weight_count", "make_weights", "make_vector", "grf", "small_config", "sample_indices",
 ]
 
 
@@ -289,3 +289,11 @@ def make_vector(cfg: Config, which: int = 0) -> np.ndarray:
     """Parity vector x ~ N(0,1) i.i.d. per unknown, float32 [B][N][N][M] (seed 3000+k)."""
     rng = np.random.Generator(np.random.PCG64([3000 + cfg.k, which]))
     return rng.standard_normal((cfg.B, cfg.N, cfg.N, cfg.M)).astype(np.float32)
+
+
+def sample_indices(cfg: Config, count: int = 65536) -> np.ndarray:
+    """Seeded, sorted, distinct indices into one sample's flattened unknowns (seed 4000+k): where the
+    fixed-budget parity tests compare the iterate x of configs too large to store whole."""
+    n = cfg.N * cfg.N * cfg.M
+    rng = np.random.Generator(np.random.PCG64([4000 + cfg.k]))
+    return np.sort(rng.choice(n, size=min(count, n), replace=False))
