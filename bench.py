@@ -160,7 +160,7 @@ def _class_roofline_ms(c, peaks, tensor_peak):
 
 
 # timing classes that are not the V-cycle (the Arnoldi/Givens/restart bookkeeping and the operator)
-_NOT_VCYCLE = ("apply_", "cgs_", "norm", "combine", "axpy64", "givens", "cycle_init", "backsolve", "rhs",
+_NOT_VCYCLE = ("apply_", "cgs_", "dcgs_", "norm", "combine", "axpy64", "givens", "cycle_init", "backsolve", "rhs",
                "scale_f64")
 
 
@@ -463,7 +463,8 @@ def run_ours(args, cfg):
                            "parallelism": (f"{cfg.B} samples sharded over {ws} ranks" if sharded
                                            else f"replicas x{ws}" if ws > 1 else "single GPU"),
                            "precision": "fp32 storage/arithmetic, fp64 iterate, reductions and restart residual",
-                           "gram_schmidt": {0: "CGS2", 1: "CGS1", 2: "selective (DGKS)"}[args.reorth]},
+                           "gram_schmidt": {0: "CGS2", 1: "CGS1", 2: "selective (DGKS)",
+                                            3: "DCGS2 (delayed re-orthogonalisation)"}[args.reorth]},
                 "roofline": roof, "roofline_apply": roof_apply, "roofline_vcycle": roof_v,
                 "e2e": {"value": benchlib.aggregate(K, 1 if sharded else ws, ms_e2e), "unit": UNIT,
                         "h2d_bytes_per_step": h2d / K, "d2h_bytes_per_step": d2h / K,
@@ -488,8 +489,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--coeffnet", action="store_true",
                     help="NEXT-1: precondition with the CoeffNet-modulated MgNet (DESIGN.md R31-R33)")
-    ap.add_argument("--reorth", type=int, default=2, choices=[0, 1, 2],
-                    help="Gram-Schmidt: 2 selective re-orthogonalisation (default), 0 CGS2, 1 CGS1")
+    ap.add_argument("--reorth", type=int, default=3, choices=[0, 1, 2, 3],
+                    help="Gram-Schmidt: 3 DCGS2 (default), 0 CGS2, 1 CGS1, 2 selective re-orthogonalisation")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

@@ -172,9 +172,17 @@ typedef struct {
   int maxit;         /* cap on total inner iterations per sample */
   double rtol;       /* stop when ||b - A x|| <= rtol ||b|| */
   int precond;       /* 0 none, 1 MgNet (I + V), 2 block Jacobi */
-  int reorth;        /* 0 = CGS2: two classical Gram-Schmidt passes; 1 = one CGS pass;
-                        2 = selective (DGKS, recommended): the second pass runs only when
-                        ||v'|| < ||w||/sqrt(2), decided on the device */
+  int reorth;        /* Gram-Schmidt of the Arnoldi step (all equal MGS in exact arithmetic):
+                        3 = DCGS2 (recommended): delayed CGS2 -- the second CGS pass of the candidate
+                            vector is deferred to the next step and fused with the first pass of the
+                            new vector, so each step streams the basis twice (CGS1's traffic) with
+                            CGS2's orthogonality; the Hessenberg column it corrects is finalised then
+                            (the last one at the cycle end);
+                        0 = CGS2: two classical Gram-Schmidt passes (three basis streams);
+                        1 = one CGS pass;
+                        2 = selective (DGKS): the second pass runs only when ||v'|| < ||w||/sqrt(2),
+                            decided on the device (its fp32 orthogonality is too loose for
+                            iteration-count parity on diffusive problems) */
   int precision;     /* 0 = mixed (default): float32 Krylov basis, operator apply and V-cycle, float64
                         iterate, reductions and restart residual;  1 = everything in float64 (basis,
                         apply, V-cycle on SIMT kernels): for tight tolerances and iteration-count

@@ -212,7 +212,7 @@ def mgnet_vcycle_f64(net: MgNet, r, z, add_identity: bool = True, stream=None) -
 
 
 def gmres_prepare(p: Problem, net: Optional[MgNet], *, restart: int = 30, precond: Optional[int] = None,
-                  reorth: int = 2, precision: int = 0, stream=None) -> None:
+                  reorth: int = 3, precision: int = 0, stream=None) -> None:
     """Capture the per-Arnoldi-step CUDA graphs for gmres_solve with these options (setup; optional)."""
     if precond is None:
         precond = 1 if net is not None else 0
@@ -271,11 +271,12 @@ def _gmres_call(name, fn, p, net, b_ptr, x_ptr, restart, maxit, rtol, precond, r
 
 
 def gmres_solve(p: Problem, net: Optional[MgNet], b, x, *, restart: int = 30, maxit: int = 1000,
-                rtol: float = 1e-8, precond: Optional[int] = None, reorth: int = 2, precision: int = 0,
+                rtol: float = 1e-8, precond: Optional[int] = None, reorth: int = 3, precision: int = 0,
                 x0_zero: bool = False, history: bool = True, hessenberg: bool = False, stream=None):
     """Restarted right-preconditioned GMRES; x (float64 CUDA tensor) holds x0 on entry (unless
     x0_zero: then it is set to 0 and A x0 is not applied), x on exit.
-    reorth: 2 = selective re-orthogonalisation (default), 0 = CGS2, 1 = CGS1 (gmres_opts).
+    reorth: 3 = DCGS2, delayed re-orthogonalisation (default: CGS2's orthogonality at two basis
+    passes per step), 0 = CGS2, 1 = CGS1, 2 = selective re-orthogonalisation (gmres_opts).
 
     Returns a list of per-sample dicts (iterations, restarts, converged, breakdown, relres_true,
     relres_est, history [, hessenberg])."""
@@ -284,7 +285,7 @@ def gmres_solve(p: Problem, net: Optional[MgNet], b, x, *, restart: int = 30, ma
 
 
 def gmres_solve_host(p: Problem, net: Optional[MgNet], b, x, *, restart: int = 30, maxit: int = 1000,
-                     rtol: float = 1e-8, precond: Optional[int] = None, reorth: int = 2, precision: int = 0,
+                     rtol: float = 1e-8, precond: Optional[int] = None, reorth: int = 3, precision: int = 0,
                      x0_zero: bool = False, history: bool = True, hessenberg: bool = False, stream=None):
     """gmres_solve with HOST buffers (include/rte.h): b float32, x float64 (CPU tensors, pinned for
     full-rate copies, or numpy arrays); the copies in and out happen inside the call."""

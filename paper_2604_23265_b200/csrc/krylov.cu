@@ -144,6 +144,189 @@ __global__ void __launch_bounds__(kThreads, 1) cgs_kernel(
   reduce_finalize<NQ>(acc, ra, b, DOTS ? alpha + (int64_t)b * alpha_ld : nullptr, DOTS ? NV : 0);
 }
 
+// DCGS2 (reorth = 3; delayed classical Gram-Schmidt with re-orthogonalisation): the
+// second CGS pass of the candidate q~_j is delayed to step j and fused with the first pass of the new
+// vector, so every Arnoldi step streams the basis twice (pass 1: dots; this pass: both updates) --
+// CGS1's traffic -- with CGS2's orthogonality.  With NV = j final vectors V_0..V_{j-1}, the
+// candidate V_j (first-pass projected at step j-1, not yet re-orthogonalised) and w = A P(q~_j):
+//   V_j     <- V_j - sum_{i<j} cA_i V_i                  (the delayed second pass: q_j = alpha_j V_j)
+//   V_{j+1} <- w - sum_{i<j} cB_i V_i - cB_j V_j(old)     (first pass of the new vector, times r_j)
+// and the next step's re-orthogonalisation dots: out[i] = alpha_i <V_i, V_{j+1}> for i <= j (V_j the
+// corrected one, alpha_j its final scale), out[j+1] = ||V_{j+1}||^2.  Coefficients: dcgs_coef_kernel.
+template <typename T, int NV>
+__global__ void __launch_bounds__(kThreads, 1) dcgs_update_kernel(
+    T* V, int64_t vld, const double* __restrict__ alpha, int alpha_ld, const double* __restrict__ cA,
+    const double* __restrict__ cB, int c_ld, const T* __restrict__ w, int64_t ns, const int* __restrict__ active,
+    RedArgs ra) {
+  using VT = typename Vec16<T>::type;
+  constexpr int W = (int)(sizeof(VT) / sizeof(T));
+  constexpr int NQ = NV + 2;
+  const int b = blockIdx.y;
+  if (active && !active[b]) return;
+  __shared__ T sA[NV > 0 ? NV : 1];
+  __shared__ T sB[NV + 1];
+  for (int i = threadIdx.x; i <= NV; i += blockDim.x) {
+    if (i < NV) sA[i] = (T)cA[(int64_t)b * c_ld + i];
+    sB[i] = (T)cB[(int64_t)b * c_ld + i];
+  }
+  __syncthreads();
+  double acc[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
+  const int64_t nv = ns / W;
+  T* Vb = V + (int64_t)b * ns;
+  VT* vj4 = reinterpret_cast<VT*>(Vb + (int64_t)NV * vld);
+  VT* vn4 = reinterpret_cast<VT*>(Vb + (int64_t)(NV + 1) * vld);
+  const VT* w4 = reinterpret_cast<const VT*>(w + (int64_t)b * ns);
+  for (int64_t q = (int64_t)blockIdx.x * kThreads + threadIdx.x; q < nv; q += (int64_t)ra.nblk * kThreads) {
+    VT wv = w4[q];
+    VT jv = vj4[q];
+    VT vv[NV > 0 ? NV : 1];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) vv[i] = reinterpret_cast<const VT*>(Vb + (int64_t)i * vld)[q];
+    T* wn = reinterpret_cast<T*>(&wv);
+    T* jn = reinterpret_cast<T*>(&jv);
+#pragma unroll
+    for (int e = 0; e < W; ++e) wn[e] = fma(-sB[NV], jn[e], wn[e]);  // (uses the candidate before its correction)
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const T* v = reinterpret_cast<const T*>(&vv[i]);
+#pragma unroll
+      for (int e = 0; e < W; ++e) {
+        jn[e] = fma(-sA[i], v[e], jn[e]);
+        wn[e] = fma(-sB[i], v[e], wn[e]);
+      }
+    }
+    if (NV > 0) vj4[q] = jv;
+    __stcs(vn4 + q, wv);
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const T* v = reinterpret_cast<const T*>(&vv[i]);
+#pragma unroll
+      for (int e = 0; e < W; ++e) acc[i] += (double)v[e] * (double)wn[e];
+    }
+#pragma unroll
+    for (int e = 0; e < W; ++e) {
+      acc[NV] += (double)jn[e] * (double)wn[e];
+      acc[NV + 1] += (double)wn[e] * (double)wn[e];
+    }
+  }
+  reduce_finalize<NQ>(acc, ra, b, alpha + (int64_t)b * alpha_ld, NV + 1);
+}
+
+// DCGS2 step-j coefficients (per sample, fp64), between pass 1 and dcgs_update_kernel.  Inputs:
+//   a[i] = alpha_i <V_i, V_j>, i < j  (q_i . V_j, from the previous step's update pass; a[j] = ||V_j||^2)
+//   z[i] = alpha_i <V_i, w>, i <= j   (pass 1; alpha_j = alpha~_j = 1/||V_j||, so z_j = q~_j . w)
+// With s_i = q_i . q~_j = a_i alpha~_j and r = ||q~_j - sum s_i q_i|| = sqrt(1 - |s|^2):
+//   q_j = (q~_j - sum_{i<j} s_i q_i) / r                       (the delayed re-orthogonalisation)
+//   column j-1 of H becomes exact for q_j: h_{i,j-1} += h_{j,j-1} s_i, h_{j,j-1} *= r
+//   A P q_j = (w - Q_j c) / r with c = H[0..j][0..j-1] s      (Arnoldi relation A P Q_{j-1} = Q_j H)
+//   h_{i,j} = (z_i - c_i) / r (i < j),  h_{j,j} = ((z_j - s.z) / r - c_j) / r
+//   V_{j+1} = r w~ = w - Q_j d,  d = c + r h_{.,j}               (w~: first-pass projection of A P q_j)
+// expressed on the stored vectors (cA: V_j's correction, cB: V_{j+1}'s projection).  Writes the final
+// alpha_j = alpha~_j / r, column j of the unrotated H (Hc, also hcol for the Givens kernel) and r.
+__global__ void dcgs_coef_kernel(int B, int j, int m, const double* __restrict__ a, const double* __restrict__ z,
+                                 int hld, double* Hc, double* alpha, int alpha_ld, double* cA, double* cB,
+                                 double* hcol, double* rbuf, const int* __restrict__ active) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B || !active[b]) return;
+  double* H = Hc + (int64_t)b * (m + 1) * m;  // [m+1][m]
+  double* al = alpha + (int64_t)b * alpha_ld;
+  const double* ab = a + (int64_t)b * hld;
+  const double* zb = z + (int64_t)b * hld;
+  const double at = al[j];
+  double s[kMaxRestart + 1], c[kMaxRestart + 1], h[kMaxRestart + 1];
+  double ss = 0.0;
+  for (int i = 0; i < j; ++i) {
+    s[i] = ab[i] * at;
+    ss += s[i] * s[i];
+  }
+  const double r = sqrt(fmax(1.0 - ss, 1e-300));
+  if (j > 0) {
+    const double hl = H[j * m + (j - 1)];
+    for (int i = 0; i < j; ++i) H[i * m + (j - 1)] += hl * s[i];
+    H[j * m + (j - 1)] = hl * r;
+  }
+  double sz = 0.0;
+  for (int i = 0; i <= j; ++i) {
+    double ci = 0.0;
+    for (int k = (i > 0 ? i - 1 : 0); k < j; ++k) ci += H[i * m + k] * s[k];  // (upper Hessenberg)
+    c[i] = ci;
+    if (i < j) sz += s[i] * zb[i];
+  }
+  for (int i = 0; i < j; ++i) h[i] = (zb[i] - c[i]) / r;
+  h[j] = ((zb[j] - sz) / r - c[j]) / r;
+  double* cAb = cA + (int64_t)b * hld;
+  double* cBb = cB + (int64_t)b * hld;
+  double* hc = hcol + (int64_t)b * hld;
+  const double dj = c[j] + r * h[j];
+  for (int i = 0; i < j; ++i) {
+    const double di = c[i] + r * h[i];
+    cAb[i] = s[i] * al[i] / at;
+    cBb[i] = (di - dj * s[i] / r) * al[i];
+  }
+  cBb[j] = dj * at / r;
+  al[j] = at / r;
+  for (int i = 0; i <= j; ++i) {
+    hc[i] = h[i];
+    H[i * m + j] = h[i];
+  }
+  rbuf[b] = r;
+}
+
+// DCGS2 cycle end (per sample): finalise the last column k-1 with the re-orthogonalisation dots of the
+// candidate q~_k (the last update pass computed them), then QR of the unrotated H[0..k][0..k-1] by
+// Givens rotations, y = R^{-1} (beta e_1) and coef_i = y_i alpha_i.
+__global__ void dcgs_backsolve_kernel(int B, int m, double* Hc, const double* __restrict__ a, int hld,
+                                      const double* __restrict__ alpha, int alpha_ld, const int* __restrict__ kcols,
+                                      const int* __restrict__ brk, double* coef, int coef_ld) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const int k = kcols[b];
+  if (k <= 0) return;
+  double* H = Hc + (int64_t)b * (m + 1) * m;
+  const double* al = alpha + (int64_t)b * alpha_ld;
+  const double* ab = a + (int64_t)b * hld;
+  const double n2 = ab[k];
+  if (!brk[b] && n2 > 0.0) {
+    const double at = 1.0 / sqrt(n2);
+    double ss = 0.0, s[kMaxRestart + 1];
+    for (int i = 0; i < k; ++i) {
+      s[i] = ab[i] * at;
+      ss += s[i] * s[i];
+    }
+    const double hl = H[k * m + (k - 1)];
+    for (int i = 0; i < k; ++i) H[i * m + (k - 1)] += hl * s[i];
+    H[k * m + (k - 1)] = hl * sqrt(fmax(1.0 - ss, 1e-300));
+  }
+  double R[kMaxRestart + 1][kMaxRestart];
+  double g[kMaxRestart + 1];
+  for (int i = 0; i <= k; ++i) {
+    g[i] = 0.0;
+    for (int l = 0; l < k; ++l) R[i][l] = H[i * m + l];
+  }
+  g[0] = 1.0 / al[0];  // beta = ||r|| (alpha_0 = 1/beta; r_0 = 1 keeps it)
+  for (int l = 0; l < k; ++l) {
+    const double x = R[l][l], yv = R[l + 1][l];
+    const double den = hypot(x, yv);
+    const double cs = den > 0 ? x / den : 1.0, sn = den > 0 ? yv / den : 0.0;
+    for (int q = l; q < k; ++q) {
+      const double t = cs * R[l][q] + sn * R[l + 1][q];
+      R[l + 1][q] = -sn * R[l][q] + cs * R[l + 1][q];
+      R[l][q] = t;
+    }
+    g[l + 1] = -sn * g[l];
+    g[l] = cs * g[l];
+  }
+  double y[kMaxRestart];
+  for (int i = k - 1; i >= 0; --i) {
+    double t = g[i];
+    for (int l = i + 1; l < k; ++l) t -= R[i][l] * y[l];
+    y[i] = t / R[i][i];
+  }
+  for (int i = 0; i < k; ++i) coef[(int64_t)b * coef_ld + i] = y[i] * al[i];
+}
+
 // ||x||^2 per sample (x fp32 or fp64); optionally writes xo = (TO)x.
 template <typename T, typename TO>
 __global__ void __launch_bounds__(kThreads) norm_kernel(const T* __restrict__ x, TO* __restrict__ xo, int64_t ns,
@@ -297,7 +480,10 @@ __global__ void givens_kernel(int B, int j, int m, const double* __restrict__ h1
                               int h_ld, const double* __restrict__ nrm2, int nrm_ld, int selective, double* Hr, double* Hraw,
                               int save_raw, double* cs, double* sn, double* g, double* alpha, int alpha_ld,
                               const double* __restrict__ bnorm, double rtol, int last, int* active, int* kcols,
-                              Status* st) {
+                              Status* st, const double* __restrict__ hcol, const double* __restrict__ rbuf,
+                              int* brkd) {
+  // hcol != NULL: DCGS2 (reorth = 3): column j comes from dcgs_coef_kernel, h2[j+1] = ||V_{j+1}||^2 from
+  // the update pass, and h_{j+1,j} = ||V_{j+1}|| / r_j (V_{j+1} = r_j w~)
   int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   if (!active[b]) {
@@ -314,9 +500,16 @@ __global__ void givens_kernel(int B, int j, int m, const double* __restrict__ h1
     if (!use_h2) nr = h2 + (int64_t)b * h_ld + j + 1;
   }
   double col[kMaxRestart + 1];
-  bool finite = isfinite(*nr);
+  double dc_r = 1.0;
+  if (hcol) {
+    nr = h2 + (int64_t)b * h_ld + j + 1;
+    dc_r = rbuf[b];
+    use_h2 = false;
+  }
+  bool finite = isfinite(*nr) && isfinite(dc_r);
   for (int i = 0; i <= j; ++i) {
-    col[i] = h1[(int64_t)b * h_ld + i] + (use_h2 ? h2[(int64_t)b * h_ld + i] : 0.0);
+    col[i] = hcol ? hcol[(int64_t)b * h_ld + i]
+                  : h1[(int64_t)b * h_ld + i] + (use_h2 ? h2[(int64_t)b * h_ld + i] : 0.0);
     finite = finite && isfinite(col[i]);
   }
   if (!finite) {
@@ -325,16 +518,20 @@ __global__ void givens_kernel(int B, int j, int m, const double* __restrict__ h1
     // uses the j finite columns before it (breakdown = 2, gmres_solve returns RTE_ENUMERIC)
     active[b] = 0;
     kcols[b] = j;
+    brkd[b] = 2;
     st[b].est = NAN;
     st[b].active = 0;
     st[b].breakdown = 2;
     st[b].kcols = j;
     return;
   }
-  double hj1 = sqrt(fmax(*nr, 0.0));
+  const double vn = sqrt(fmax(*nr, 0.0));
+  double hj1 = vn / dc_r;
   const int ldh = m;  // H stored [B][m+1][m]
   double* Hb = Hr + (int64_t)b * (m + 1) * m;
-  if (save_raw) {
+  if (hcol) {
+    Hraw[(int64_t)b * (m + 1) * m + (j + 1) * ldh + j] = hj1;  // (rows 0..j: dcgs_coef_kernel)
+  } else if (save_raw) {
     double* R = Hraw + (int64_t)b * (m + 1) * m;
     for (int i = 0; i <= j; ++i) R[i * ldh + j] = col[i];
     R[(j + 1) * ldh + j] = hj1;
@@ -357,11 +554,12 @@ __global__ void givens_kernel(int B, int j, int m, const double* __restrict__ h1
   gb[j] = c * gb[j];
   double est = fabs(gb[j + 1]) / bnorm[b];
   int brk = (hj1 <= 1e-14 * den) ? 1 : 0;
-  alpha[(int64_t)b * alpha_ld + j + 1] = brk ? 0.0 : 1.0 / hj1;
+  alpha[(int64_t)b * alpha_ld + j + 1] = brk ? 0.0 : 1.0 / (hcol ? vn : hj1);
   int stop = brk || (fabs(gb[j + 1]) <= rtol * bnorm[b]) || last || (j + 1 == m);
   if (stop) {
     active[b] = 0;
     kcols[b] = j + 1;
+    brkd[b] = brk;  // (how the cycle ended, for the DCGS2 back-solve)
   }
   st[b].est = est;
   st[b].active = !stop;
@@ -400,9 +598,10 @@ struct GmresWork {
   double* r64 = nullptr;   // n
   double *Hr = nullptr, *Hraw = nullptr, *cs = nullptr, *sn = nullptr, *g = nullptr, *alpha = nullptr;
   double *h1 = nullptr, *h2 = nullptr, *h3 = nullptr, *coef = nullptr, *bnorm = nullptr, *rn2 = nullptr;
+  double *cA = nullptr, *cB = nullptr, *hcol = nullptr, *rbuf = nullptr;  // DCGS2 step coefficients
   double* partials = nullptr;
   unsigned* counters = nullptr;
-  int *active = nullptr, *kcols = nullptr, *done = nullptr;
+  int *active = nullptr, *kcols = nullptr, *done = nullptr, *brkd = nullptr;
   Status* st_dev = nullptr;
   Status* st_host = nullptr;  // pinned, 2 slots of B (the step statuses are read one step late)
   cudaEvent_t st_ev[2] = {nullptr, nullptr};  // slot copies done
@@ -438,8 +637,8 @@ struct GmresWork {
   }
   void release() {
     drop_graphs();
-    void* ps[] = {V, w, z, r64, Hr, Hraw, cs, sn, g, alpha, h1, h2, h3, coef, bnorm, rn2, partials, counters,
-                  active, kcols, done, st_dev, V64, w64, z64, q32, bh, xh};
+    void* ps[] = {V, w, z, r64, Hr, Hraw, cs, sn, g, alpha, h1, h2, h3, coef, bnorm, rn2, cA, cB, hcol, rbuf, partials, counters,
+                  active, kcols, done, brkd, st_dev, V64, w64, z64, q32, bh, xh};
     for (void* p : ps) dfree(p);
     if (cp) cudaStreamDestroy(cp);
     if (ev_x) cudaEventDestroy(ev_x);
@@ -497,6 +696,37 @@ static void launch_cgs(const GmresWork& W, const TB* V, int nv, bool update, boo
     after_launch(cls, st, 0.0, 0.0, 0);
   else
     after_launch(cls, st, flops, bytes, 0);
+}
+
+// DCGS2 update pass at step j (NV = j final vectors before the candidate V_j).
+template <typename TB>
+static void launch_dcgs_update(const GmresWork& W, TB* V, int j, const TB* w, cudaStream_t st) {
+  RedArgs ra{W.partials, W.counters, W.h2, kMaxRestart + 2, W.nblk};
+  dim3 grid(W.nblk, W.B);
+  const int64_t vld = W.ns * W.B;
+  prof_begin(st, "dcgs_update");
+  auto go = [&](auto nv_tag) {
+    constexpr int NV = decltype(nv_tag)::value;
+    dcgs_update_kernel<TB, NV><<<grid, kThreads, 0, st>>>(V, vld, W.alpha, W.m + 1, W.cA, W.cB, kMaxRestart + 2, w,
+                                                          W.ns, W.active, ra);
+  };
+  switch (j) {
+#define RTE_NV_CASE(K) case K: go(std::integral_constant<int, K>{}); break;
+    RTE_NV_CASE(0) RTE_NV_CASE(1) RTE_NV_CASE(2) RTE_NV_CASE(3) RTE_NV_CASE(4) RTE_NV_CASE(5) RTE_NV_CASE(6)
+    RTE_NV_CASE(7) RTE_NV_CASE(8) RTE_NV_CASE(9) RTE_NV_CASE(10) RTE_NV_CASE(11) RTE_NV_CASE(12) RTE_NV_CASE(13)
+    RTE_NV_CASE(14) RTE_NV_CASE(15) RTE_NV_CASE(16) RTE_NV_CASE(17) RTE_NV_CASE(18) RTE_NV_CASE(19)
+    RTE_NV_CASE(20) RTE_NV_CASE(21) RTE_NV_CASE(22) RTE_NV_CASE(23) RTE_NV_CASE(24) RTE_NV_CASE(25)
+    RTE_NV_CASE(26) RTE_NV_CASE(27) RTE_NV_CASE(28) RTE_NV_CASE(29) RTE_NV_CASE(30) RTE_NV_CASE(31)
+#undef RTE_NV_CASE
+    default:
+      set_error("gmres: restart > 32 is not supported by the fused DCGS2 kernels");
+      throw Fail{RTE_EINVAL};
+  }
+  // bytes: j final vectors + the candidate + w read, the candidate and the new vector written;
+  // flops: 2 per (vector, element) for the two updates and the dots, + 2 per element for the norm
+  const double ne = (double)W.ns * W.B;
+  after_launch("dcgs_update", st, ne * (2.0 * j + 2.0 * (j + 1) + 2.0 * (j + 1) + 2.0),
+               (double)sizeof(TB) * ne * (j + 4), 0);
 }
 
 template <typename T, typename TO>
@@ -655,6 +885,10 @@ static GmresWork& get_work(const rte_problem* p, int m) {
   W.h1 = dalloc<double>((size_t)B * (kMaxRestart + 2));
   W.h2 = dalloc<double>((size_t)B * (kMaxRestart + 2));
   W.h3 = dalloc<double>((size_t)B * (kMaxRestart + 2));
+  W.cA = dalloc<double>((size_t)B * (kMaxRestart + 2));
+  W.cB = dalloc<double>((size_t)B * (kMaxRestart + 2));
+  W.hcol = dalloc<double>((size_t)B * (kMaxRestart + 2));
+  W.rbuf = dalloc<double>(B);
   W.coef = dalloc<double>((size_t)B * (m + 1));
   W.bnorm = dalloc<double>(B);
   W.rn2 = dalloc<double>(B);
@@ -663,6 +897,7 @@ static GmresWork& get_work(const rte_problem* p, int m) {
   W.active = dalloc<int>(B);
   W.kcols = dalloc<int>(B);
   W.done = dalloc<int>(B);
+  W.brkd = dalloc<int>(B);
   W.st_dev = dalloc<Status>(B);
   RTE_CHECK_CUDA(cudaMemset(W.counters, 0, sizeof(unsigned) * B));
   RTE_CHECK_CUDA(cudaMemset(W.Hraw, 0, sizeof(double) * B * (m + 1) * m));
@@ -723,8 +958,8 @@ static rte_status solve_impl(const rte_problem* p, const mgnet_net* net, const f
     const int B = p->B;
     const int64_t n = p->n;
     const int hld = kMaxRestart + 2;
-    const int reorth = opts->reorth;  // 0 CGS2, 1 CGS1, 2 selective (DGKS)
-    RTE_REQUIRE(reorth >= 0 && reorth <= 2, "gmres_solve: reorth must be 0, 1 or 2");
+    const int reorth = opts->reorth;  // 0 CGS2, 1 CGS1, 2 selective (DGKS), 3 DCGS2 (delayed CGS2)
+    RTE_REQUIRE(reorth >= 0 && reorth <= 3, "gmres_solve: reorth must be 0, 1, 2 or 3");
     RTE_REQUIRE(opts->precision == 0 || opts->precision == 1, "gmres_solve: precision must be 0 or 1");
     const bool f64 = opts->precision == 1;
     if (f64 && !W.V64) {
@@ -815,7 +1050,15 @@ static rte_status solve_impl(const rte_problem* p, const mgnet_net* net, const f
           using TB = std::remove_pointer_t<decltype(V)>;
           TB* vnext = V + (size_t)(j + 1) * n;
           launch_cgs<TB>(W, V, j + 1, false, true, nullptr, wv, nullptr, W.h1, st);      // pass A
-          if (reorth != 1) {
+          if (reorth == 3) {  // DCGS2: coefficients, then one fused update pass (V_j corrected, V_{j+1})
+            prof_begin(st, "dcgs_coef");
+            dcgs_coef_kernel<<<(B + 63) / 64, 64, 0, st>>>(B, j, m, W.h2, W.h1, hld, W.Hraw, W.alpha, m + 1, W.cA,
+                                                           W.cB, W.hcol, W.rbuf, W.active);
+            after_launch("dcgs_coef", st);
+            launch_dcgs_update<TB>(W, V, j, wv, st);
+            h2 = W.h2;
+            nrm = W.h2;
+          } else if (reorth != 1) {
             launch_cgs<TB>(W, V, j + 1, true, true, W.h1, wv, vnext, W.h2, st);          // pass B
             if (reorth == 2)                                                          // pass C (selective)
               launch_cgs<TB>(W, V, j + 1, true, false, W.h2, vnext, vnext, W.h3, st, W.h1 + (j + 1), W.h2 + (j + 1));
@@ -858,7 +1101,8 @@ static rte_status solve_impl(const rte_problem* p, const mgnet_net* net, const f
         prof_begin(st, "givens");
         givens_kernel<<<(B + 63) / 64, 64, 0, st>>>(B, j, m, W.h1, h2, hld, nrm, hld, reorth == 2 ? 1 : 0, W.Hr, W.Hraw,
                                                     first_cycle ? 1 : 0, W.cs, W.sn, W.g, W.alpha, m + 1, W.bnorm,
-                                                    opts->rtol, last, W.active, W.kcols, W.st_dev);
+                                                    opts->rtol, last, W.active, W.kcols, W.st_dev,
+                                                    reorth == 3 ? W.hcol : nullptr, W.rbuf, W.brkd);
         after_launch("givens", st);
         // The step's status is read one step late: step j + 1 is enqueued before the host waits for
         // step j, so the GPU never idles on the host round trip.  When step j turns out to have
@@ -883,13 +1127,7 @@ static rte_status solve_impl(const rte_problem* p, const mgnet_net* net, const f
         process_step(pending);
         pending = -1;
       }
-      if (first_cycle) {
-        for (int b = 0; b < B; ++b)
-          if (rep[b].hessenberg)
-            RTE_CHECK_CUDA(cudaMemcpyAsync(rep[b].hessenberg, W.Hraw + (size_t)b * (m + 1) * m,
-                                           sizeof(double) * (m + 1) * m, cudaMemcpyDeviceToHost, st));
-      }
-      first_cycle = false;
+
       // x += P(V y).  (gmres_solve_host: an early copy of x from the previous cycle must land before
       // x changes again)
       auto wait_host_copy = [&]() {
@@ -899,8 +1137,21 @@ static rte_status solve_impl(const rte_problem* p, const mgnet_net* net, const f
         }
       };
       prof_begin(st, "backsolve");
-      backsolve_kernel<<<(B + 63) / 64, 64, 0, st>>>(B, m, W.Hr, W.g, W.alpha, m + 1, W.kcols, W.coef, m + 1);
+      if (reorth == 3) {
+        dcgs_backsolve_kernel<<<(B + 63) / 64, 64, 0, st>>>(B, m, W.Hraw, W.h2, hld, W.alpha, m + 1, W.kcols,
+                                                            W.brkd, W.coef, m + 1);
+      } else {
+        backsolve_kernel<<<(B + 63) / 64, 64, 0, st>>>(B, m, W.Hr, W.g, W.alpha, m + 1, W.kcols, W.coef, m + 1);
+      }
       after_launch("backsolve", st);
+      if (first_cycle) {  // the first cycle's unrotated Hessenberg matrix (DCGS2: after its last column's
+                          // delayed correction in the back-solve)
+        for (int b = 0; b < B; ++b)
+          if (rep[b].hessenberg)
+            RTE_CHECK_CUDA(cudaMemcpyAsync(rep[b].hessenberg, W.Hraw + (size_t)b * (m + 1) * m,
+                                           sizeof(double) * (m + 1) * m, cudaMemcpyDeviceToHost, st));
+      }
+      first_cycle = false;
       if (f64) {
         prof_begin(st, "combine");
         combine_kernel<double, double><<<dim3(W.nblk, B), kThreads, 0, st>>>(W.V64, n, W.coef, m + 1, W.kcols, W.z64,

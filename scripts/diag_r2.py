@@ -75,7 +75,7 @@ if "conv" in which:
         w = W.make_weights(cfg)
         net = P.mgnet_create(p, cfg.L, cfg.C0, cfg.nu, w)
         for precond in (0, 1):
-            for reorth in (2, 0):
+            for reorth in (3, 0, 2):
                 x = torch.zeros(p.shape, dtype=torch.float64, device="cuda")
                 rep = P.gmres_solve(p, net if precond else None, bd, x, restart=30, maxit=cfg.maxit, rtol=cfg.rtol,
                                     reorth=reorth)[0]
@@ -85,6 +85,25 @@ if "conv" in which:
                 out[tag + "_hist"] = rep["history"]
                 out[tag + "_x"] = x.cpu().numpy()
     np.savez_compressed(os.path.join(OUT, "diag_r2_conv.npz"), **out)
+
+if "conv2" in which:  # config 2 only, every mode
+    out = {}
+    cfg = W.config(2)
+    media, p = setup(cfg)
+    bd = torch.empty(p.shape, dtype=torch.float32, device="cuda")
+    P.rte_rhs(p, bd)
+    net = P.mgnet_create(p, cfg.L, cfg.C0, cfg.nu, W.make_weights(cfg))
+    for precond in (0, 1):
+        for reorth in (3, 0):
+            x = torch.zeros(p.shape, dtype=torch.float64, device="cuda")
+            rep = P.gmres_solve(p, net if precond else None, bd, x, restart=30, maxit=cfg.maxit, rtol=cfg.rtol,
+                                reorth=reorth)[0]
+            tag = f"cfg2_p{precond}_r{reorth}"
+            print(tag, rep["iterations"], rep["relres_true"], flush=True)
+            out[tag + "_it"] = rep["iterations"]
+            out[tag + "_hist"] = rep["history"]
+            out[tag + "_x"] = x.cpu().numpy()
+    np.savez_compressed(os.path.join(OUT, "diag_r2_conv2.npz"), **out)
 
 if "budget" in which:
     out = {}
@@ -96,7 +115,8 @@ if "budget" in which:
         w = W.make_weights(cfg)
         net = P.mgnet_create(p, cfg.L, cfg.C0, cfg.nu, w)
         x = torch.zeros(p.shape, dtype=torch.float64, device="cuda")
-        reps = P.gmres_solve(p, net, bd, x, restart=30, maxit=cfg.maxit, rtol=cfg.rtol, hessenberg=True)
+        reps = P.gmres_solve(p, net, bd, x, restart=30, maxit=cfg.maxit, rtol=cfg.rtol, hessenberg=True,
+                             reorth=int(os.environ.get("DIAG_REORTH", "2")))
         for s, rep in enumerate(reps):
             out[f"cfg{k}_s{s}_hist"] = rep["history"]
             out[f"cfg{k}_s{s}_H"] = rep["hessenberg"]

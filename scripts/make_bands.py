@@ -9,9 +9,8 @@ and K = 4 perturbed runs.  Run k perturbs, with its own seeded noise xi ~ N(0, 1
   * every operator output:  A_k(v) = A(v) (1 + d_A xi)         (an fp32 apply's per-op error)
   * every V-cycle output:   P_k(v) = v + V(v) (1 + d_V xi)     (the correction V(v) = z - v carries
                                                                the fp32 V-cycle's error, R27)
-d_A, d_V are the per-op relative errors an fp32 implementation of the operators is allowed to make
-here (DESIGN.md §6 R36: 2e-6, ~5x the fp32 path's measured per-op error and 5x below the north
-star's 1e-5 per-op bound).  The band of a quantity is the max deviation of the 4 perturbed runs
+d = d_A = d_V (--delta) is the per-op relative error of an fp32 implementation of the operators
+(reading R36).  The band of a quantity is the max deviation of the 4 perturbed runs
 from the reference run; the GPU must lie within 2x that band (tests/test_gpu_bands.py).
 
 Stored per config (tests/golden/bands_cfg{k}.npz): the reference histories and iteration counts
@@ -35,8 +34,7 @@ import workloads as W  # noqa: E402
 from oracle import rte as O  # noqa: E402
 
 D_B = 6e-8
-D_A = 2e-6
-D_V = 2e-6
+D_OP = 2e-6   # default per-op relative perturbation of A and V (--delta)
 TMP = os.environ.get("BANDS_TMP", "/tmp/bands")
 
 
@@ -47,7 +45,7 @@ def noisy(fn, delta, rng):
     return g
 
 
-def run(cfg, s, b32, op_s, onet, k):
+def run(cfg, s, b32, op_s, onet, k, delta):
     """Reference run (k < 0) or perturbed run k of sample s."""
     A = lambda v: O.apply(op_s, v)
     V = lambda v: O.vcycle(onet, v, add_identity=False)
@@ -55,8 +53,8 @@ def run(cfg, s, b32, op_s, onet, k):
     if k >= 0:
         rng = np.random.Generator(np.random.PCG64([5000 + cfg.k, s, k]))
         b = b32 * (1.0 + D_B * rng.standard_normal(b32.shape))
-        A = noisy(A, D_A, rng)
-        V = noisy(V, D_V, rng)
+        A = noisy(A, delta, rng)
+        V = noisy(V, delta, rng)
     P = lambda v: v + V(v)
     return O.gmres(A, b, P=P, restart=cfg.restart, rtol=cfg.rtol, maxit=cfg.maxit)
 
@@ -66,6 +64,7 @@ def main():
     ap.add_argument("configs", type=int, nargs="+")
     ap.add_argument("--runs", type=int, default=4)
     ap.add_argument("--samples", type=str, default=None)
+    ap.add_argument("--delta", type=float, default=D_OP)
     args = ap.parse_args()
     os.makedirs(TMP, exist_ok=True)
     for k in args.configs:
@@ -81,28 +80,33 @@ def main():
                              op.inflow[s:s + 1])
             b32 = b32_all[s:s + 1]
             for r in [-1] + list(range(args.runs)):
-                path = os.path.join(TMP, f"cfg{k}_s{s}_r{r}.npz")
+                path = _path(k, s, r, args.delta)
                 if os.path.exists(path):
                     continue
                 t0 = time.time()
-                res = run(cfg, s, b32, op_s, onet, r)
+                res = run(cfg, s, b32, op_s, onet, r, args.delta)
                 x = res.x.ravel()
                 np.savez(path, hist=np.array(res.history), it=res.iterations, conv=res.converged,
                          relres=res.relres_true, xs=x if idx is None else x[idx], xnorm=np.linalg.norm(x))
                 print(f"cfg{k} s{s} run{r}: {res.iterations} it, conv {res.converged}, relres {res.relres_true:.3e}, "
                       f"{time.time() - t0:.0f} s", flush=True)
-        assemble(cfg, samples, args.runs)
+        if args.runs > 0:
+            assemble(cfg, samples, args.runs, args.delta)
 
 
-def assemble(cfg, samples, runs):
-    out = {"d_b": D_B, "d_a": D_A, "d_v": D_V, "runs": runs}
+def _path(k, s, r, delta):
+    return os.path.join(TMP, f"cfg{k}_s{s}_r{r}.npz" if r < 0 else f"cfg{k}_s{s}_r{r}_d{delta:.0e}.npz")
+
+
+def assemble(cfg, samples, runs, delta):
+    out = {"d_b": D_B, "d_op": delta, "runs": runs}
     for s in samples:
-        ref = np.load(os.path.join(TMP, f"cfg{cfg.k}_s{s}_r-1.npz"))
+        ref = np.load(_path(cfg.k, s, -1, delta))
         for key in ("hist", "it", "conv", "relres", "xs", "xnorm"):
             out[f"s{s}_ref_{key}"] = ref[key]
         dh, dx, dit = [], [], []
         for r in range(runs):
-            d = np.load(os.path.join(TMP, f"cfg{cfg.k}_s{s}_r{r}.npz"))
+            d = np.load(_path(cfg.k, s, r, delta))
             n = min(len(d["hist"]), len(ref["hist"]))
             dh.append(float(np.max(np.abs(d["hist"][:n] - ref["hist"][:n]) / ref["hist"][:n])))
             dx.append(float(np.linalg.norm(d["xs"] - ref["xs"]) / np.linalg.norm(ref["xs"])))
@@ -113,7 +117,7 @@ def assemble(cfg, samples, runs):
         out[f"s{s}_band_x"] = max(dx)
         out[f"s{s}_band_it"] = max(dit)
         print(f"cfg{cfg.k} s{s}: ref it {int(ref['it'])} conv {bool(ref['conv'])}; band hist {max(dh):.3e} "
-              f"x {max(dx):.3e} it {max(dit)} (runs: {[int(np.load(os.path.join(TMP, f'cfg{cfg.k}_s{s}_r{r}.npz'))['it']) for r in range(runs)]})",
+              f"x {max(dx):.3e} it {max(dit)} (runs: {[int(np.load(_path(cfg.k, s, r, delta))['it']) for r in range(runs)]})",
               flush=True)
     os.makedirs(os.path.join(ROOT, "tests", "golden"), exist_ok=True)
     np.savez_compressed(os.path.join(ROOT, "tests", "golden", f"bands_cfg{cfg.k}.npz"), **out)

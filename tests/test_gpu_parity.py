@@ -238,7 +238,7 @@ def test_mgnet_rejects_bad_weight_count():
 
 
 # ---------------------------------------------------------------------------------------
-def _gmres_pair(cfg, precond, rtol, maxit, std=0.02, reorth=2, precision=0):
+def _gmres_pair(cfg, precond, rtol, maxit, std=0.02, reorth=3, precision=0):
     import paper_2604_23265_b200 as P
     media = W.make_media(cfg)
     p = _gpu_problem(cfg, media)
@@ -260,9 +260,10 @@ def _gmres_pair(cfg, precond, rtol, maxit, std=0.02, reorth=2, precision=0):
 
 
 @pytest.mark.parametrize("precond,reorth,precision", [(False, 0, 0), (True, 0, 0), (False, 2, 0), (True, 2, 0),
-                                                      (True, 1, 0), (True, 0, 1), (False, 2, 1)])
+                                                      (True, 1, 0), (True, 0, 1), (False, 2, 1), (False, 3, 0),
+                                                      (True, 3, 0), (True, 3, 1)])
 def test_gmres_config1_converges_like_oracle(precond, reorth, precision):
-    """reorth 0 = CGS2, 1 = CGS1, 2 = selective (DGKS); all equal MGS in exact arithmetic.
+    """reorth 0 = CGS2, 1 = CGS1, 2 = selective (DGKS), 3 = DCGS2; all equal MGS in exact arithmetic.
     precision 0 = fp32 basis (mixed), 1 = fp64 basis."""
     cfg = W.config(1)
     rep, x, ref = _gmres_pair(cfg, precond, cfg.rtol, cfg.maxit, reorth=reorth, precision=precision)
@@ -323,7 +324,8 @@ def test_gmres_small_batch_independent_solves():
             assert _rel(x[s], ref.x[0]) <= 1e-4
 
 
-@pytest.mark.parametrize("k,steps,reorth", [(3, 5, 0), (2, 8, 0), (3, 5, 2), (2, 8, 2)])
+@pytest.mark.parametrize("k,steps,reorth", [(3, 5, 0), (2, 8, 0), (3, 5, 2), (2, 8, 2), (3, 5, 3), (2, 8, 3),
+                                             (1, 12, 3)])
 def test_gmres_first_arnoldi_columns(k, steps, reorth):
     """Non-converging protocol: the first Arnoldi columns (unrotated H) agree to 1e-5."""
     import paper_2604_23265_b200 as P

@@ -291,7 +291,7 @@ def make_vector(cfg: Config, which: int = 0) -> np.ndarray:
     return rng.standard_normal((cfg.B, cfg.N, cfg.N, cfg.M)).astype(np.float32)
 
 
-def sample_indices(cfg: Config, count: int = 65536) -> np.ndarray:
+def sample_indices(cfg: Config, count: int = 16384) -> np.ndarray:
     """Seeded, sorted, distinct indices into one sample's flattened unknowns (seed 4000+k): where the
     fixed-budget parity tests compare the iterate x of configs too large to store whole."""
     n = cfg.N * cfg.N * cfg.M
