@@ -73,7 +73,7 @@ def main():
         op = O.setup_from_media(cfg, media)
         onet = O.make_mgnet(W.make_weights(cfg), cfg.M, cfg.L, cfg.C0, cfg.nu)
         b32_all = O.rhs(op).astype(np.float32).astype(np.float64)   # the GPU solves the fp32 b
-        idx = W.sample_indices(cfg) if k >= 4 else None
+        idx = W.sample_indices(cfg)
         samples = range(cfg.B) if args.samples is None else [int(t) for t in args.samples.split(",")]
         for s in samples:
             op_s = O.Problem(op.N, op.qd, op.sig_t[s:s + 1], op.sig_s[s:s + 1], op.f[s:s + 1], op.S[s:s + 1],
@@ -87,7 +87,7 @@ def main():
                 res = run(cfg, s, b32, op_s, onet, r, args.delta)
                 x = res.x.ravel()
                 np.savez(path, hist=np.array(res.history), it=res.iterations, conv=res.converged,
-                         relres=res.relres_true, xs=x if idx is None else x[idx], xnorm=np.linalg.norm(x))
+                         relres=res.relres_true, xs=x[idx], xnorm=np.linalg.norm(x))
                 print(f"cfg{k} s{s} run{r}: {res.iterations} it, conv {res.converged}, relres {res.relres_true:.3e}, "
                       f"{time.time() - t0:.0f} s", flush=True)
         if args.runs > 0:
@@ -100,16 +100,19 @@ def _path(k, s, r, delta):
 
 def assemble(cfg, samples, runs, delta):
     out = {"d_b": D_B, "d_op": delta, "runs": runs}
+    idx = W.sample_indices(cfg)
+    sub = lambda xs: xs if xs.size == idx.size else xs.ravel()[idx]   # (older files kept all of x)
     for s in samples:
         ref = np.load(_path(cfg.k, s, -1, delta))
-        for key in ("hist", "it", "conv", "relres", "xs", "xnorm"):
+        for key in ("hist", "it", "conv", "relres", "xnorm"):
             out[f"s{s}_ref_{key}"] = ref[key]
+        out[f"s{s}_ref_xs"] = sub(ref["xs"])
         dh, dx, dit = [], [], []
         for r in range(runs):
             d = np.load(_path(cfg.k, s, r, delta))
             n = min(len(d["hist"]), len(ref["hist"]))
             dh.append(float(np.max(np.abs(d["hist"][:n] - ref["hist"][:n]) / ref["hist"][:n])))
-            dx.append(float(np.linalg.norm(d["xs"] - ref["xs"]) / np.linalg.norm(ref["xs"])))
+            dx.append(float(np.linalg.norm(sub(d["xs"]) - sub(ref["xs"])) / np.linalg.norm(sub(ref["xs"]))))
             dit.append(int(abs(int(d["it"]) - int(ref["it"]))))
             out[f"s{s}_run{r}_it"] = d["it"]
             out[f"s{s}_run{r}_hist"] = d["hist"]

@@ -27,6 +27,9 @@ ap.add_argument("--samples", type=int, default=10)
 ap.add_argument("--degree", type=int, default=2)
 ap.add_argument("--rtol", type=float, default=1e-8)
 ap.add_argument("--maxit", type=int, default=3000)
+ap.add_argument("--precision", type=int, default=1,
+                help="Krylov basis: 1 fp64 (default: the mode whose iteration counts are parity-tested "
+                     "+-1 against the oracle, tests/test_gpu_blockjacobi.py), 0 fp32")
 args = ap.parse_args()
 
 N, NP, NA, L, C0, NU = 32, 1, 4, 4, 16, 2
@@ -34,7 +37,7 @@ M = NP * NA
 cfg_like = W.small_config(1, N=N, M=M, n_polar=NP, n_azim=NA, L=L, C0=C0)
 weights = W.make_weights(cfg_like, std=0.02, seed=77)
 cweights = W.make_coeffnet_weights(cfg_like, seed=78)
-out = {"grid": f"{N}x{N}", "directions": M, "mgnet": {"L": L, "C0": C0, "nu": NU}, "rtol": args.rtol,
+out = {"grid": f"{N}x{N}", "directions": M, "precision": args.precision, "mgnet": {"L": L, "C0": C0, "nu": NU}, "rtol": args.rtol,
        "restart": 30, "samples": args.samples, "degree": args.degree, "regimes": {}}
 for regime in W.PAPER_REGIMES:
     med = W.paper_media(args.samples, N=N, degree=args.degree, regime=regime, M=M, seed=100)
@@ -46,11 +49,13 @@ for regime in W.PAPER_REGIMES:
     res = {}
     for name, pre, nt in (("none", 0, None), ("block_jacobi", 2, None), ("mgnet", 1, net), ("mgnet_coeffnet", 1, netc)):
         x = torch.zeros(p.shape, dtype=torch.float64, device="cuda")
-        P.gmres_solve(p, nt, b, x, restart=30, maxit=5, rtol=args.rtol, precond=pre)  # warm-up
+        P.gmres_solve(p, nt, b, x, restart=30, maxit=5, rtol=args.rtol, precond=pre,
+                      precision=args.precision)  # warm-up
         x.zero_()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        rep = P.gmres_solve(p, nt, b, x, restart=30, maxit=args.maxit, rtol=args.rtol, precond=pre)
+        rep = P.gmres_solve(p, nt, b, x, restart=30, maxit=args.maxit, rtol=args.rtol, precond=pre,
+                            precision=args.precision)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         its = [r["iterations"] for r in rep]

@@ -28,7 +28,7 @@ def _pair(med, N, n_polar=1, n_azim=4, g=0.0):
 
 @pytest.mark.parametrize("regime,N,n_polar,n_azim,g", [("diffusion", 32, 1, 4, 0.0), ("centre", 32, 1, 4, 0.0),
                                                        ("transport", 13, 2, 8, 0.5), ("lr", 8, 2, 16, 0.8)])
-def test_block_jacobi_apply_parity(regime, N, n_polar, n_azim, g):
+def test_block_jacobi_apply_parity(regime, N, n_polar, n_azim, g, margin):
     M = n_polar * n_azim
     med = W.paper_media(3, N=N, degree=3, regime=regime, M=M, seed=11)
     P, p, op = _pair(med, N, n_polar, n_azim, g)
@@ -41,21 +41,24 @@ def test_block_jacobi_apply_parity(regime, N, n_polar, n_azim, g):
     z32 = torch.empty_like(r32)
     P.rte_blockjacobi_apply(p, r32, z32)
     torch.cuda.synchronize()
-    assert _rel(z64.cpu().numpy(), ref) <= 1e-12
-    assert _rel(z32.cpu().numpy(), ref) <= 1e-5
+    assert margin(_rel(z64.cpu().numpy(), ref), 1e-12, "fp64 block-Jacobi rel-L2") <= 1e-12
+    assert margin(_rel(z32.cpu().numpy(), ref), 1e-5, "fp32 block-Jacobi rel-L2") <= 1e-5
 
 
-@pytest.mark.parametrize("regime", ["transport", "centre"])
-def test_gmres_block_jacobi_iteration_parity(regime):
-    """Paper workload (32 x 32, 4 directions): block-Jacobi GMRES reaches rtol in the oracle's
-    iteration count +-1 (fp64 Krylov basis, DESIGN.md §6 protocol) with x to 1e-4."""
+@pytest.mark.parametrize("regime,precision", [("transport", 1), ("centre", 1), ("diffusion", 1), ("diffusion", 0),
+                                              ("transport", 0), ("centre", 0)])
+def test_gmres_block_jacobi_iteration_parity(regime, precision, margin):
+    """Paper workload (32 x 32, 4 directions): block-Jacobi GMRES reaches rtol in the
+    oracle's iteration count +-1 with x to 1e-4, with the fp64 Krylov basis (precision 1) and in the
+    fp32-basis mode scripts/paper_workload.py measures (precision 0), including the diffusion regime
+    the paper's >= 10x claim is about."""
     N = 32
     med = W.paper_media(2, N=N, degree=2, regime=regime, M=4, seed=12)
     P, p, op = _pair(med, N)
     b = W.make_paper_rhs(2, N=N, M=4, seed=3)
     bd = torch.from_numpy(b).cuda()
     x = torch.zeros(p.shape, dtype=torch.float64, device="cuda")
-    rep = P.gmres_solve(p, None, bd, x, restart=30, maxit=2000, rtol=1e-8, precond=2, precision=1)
+    rep = P.gmres_solve(p, None, bd, x, restart=30, maxit=2000, rtol=1e-8, precond=2, precision=precision)
     torch.cuda.synchronize()
     Pbj = O.block_jacobi(op)
     for s in range(2):
@@ -64,8 +67,9 @@ def test_gmres_block_jacobi_iteration_parity(regime):
         ref = O.gmres(lambda v: O.apply(sub, v), b[s:s + 1].astype(np.float64), O.block_jacobi(sub), restart=30,
                       rtol=1e-8, maxit=2000)
         assert ref.converged and rep[s]["converged"]
-        assert abs(rep[s]["iterations"] - ref.iterations) <= 1, (rep[s]["iterations"], ref.iterations)
-        assert _rel(x[s].cpu().numpy(), ref.x[0]) <= 1e-4
+        assert margin(abs(rep[s]["iterations"] - ref.iterations), 1, f"iterations[{s}] vs oracle") <= 1, \
+            (rep[s]["iterations"], ref.iterations)
+        assert margin(_rel(x[s].cpu().numpy(), ref.x[0]), 1e-4, f"x[{s}] rel-L2") <= 1e-4
     assert Pbj is not None
 
 

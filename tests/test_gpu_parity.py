@@ -54,7 +54,7 @@ SMALL = [
 
 @pytest.mark.parametrize("cfg", [W.config(k) for k in (1, 2, 3, 4, 5)] + SMALL,
                          ids=lambda c: f"cfg{c.k}-N{c.N}-M{c.M}-B{c.B}")
-def test_apply_and_rhs_parity(cfg):
+def test_apply_and_rhs_parity(cfg, margin):
     import paper_2604_23265_b200 as P
     media = W.make_media(cfg)
     p = _gpu_problem(cfg, media)
@@ -67,8 +67,8 @@ def test_apply_and_rhs_parity(cfg):
     P.rte_rhs(p, b)
     torch.cuda.synchronize()
     y_ref = O.apply(op, x)
-    assert _rel(y.cpu().numpy(), y_ref) <= 1e-5
-    assert _rel(b.cpu().numpy(), O.rhs(op)) <= 1e-7
+    assert margin(_rel(y.cpu().numpy(), y_ref), 1e-5, "apply rel-L2") <= 1e-5
+    assert margin(_rel(b.cpu().numpy(), O.rhs(op)), 1e-7, "rhs rel-L2") <= 1e-7
 
 
 WIDE = [  # M % 128 == 0: the wide-tile SIMT kernel (fp64 restart residual), ragged cell tiles
@@ -78,7 +78,7 @@ WIDE = [  # M % 128 == 0: the wide-tile SIMT kernel (fp64 restart residual), rag
 
 
 @pytest.mark.parametrize("cfg", [W.config(k) for k in (1, 2, 3)] + SMALL + WIDE, ids=lambda c: f"cfg{c.k}-N{c.N}-M{c.M}")
-def test_apply_f64_parity(cfg):
+def test_apply_f64_parity(cfg, margin):
     import paper_2604_23265_b200 as P
     media = W.make_media(cfg)
     p = _gpu_problem(cfg, media)
@@ -88,10 +88,10 @@ def test_apply_f64_parity(cfg):
     y = torch.empty_like(xd)
     P.rte_apply_f64(p, xd, y)
     torch.cuda.synchronize()
-    assert _rel(y.cpu().numpy(), O.apply(op, x)) <= 1e-12
+    assert margin(_rel(y.cpu().numpy(), O.apply(op, x)), 1e-12, "fp64 apply rel-L2") <= 1e-12
 
 
-def test_apply_manufactured_constant():
+def test_apply_manufactured_constant(margin):
     """q = C sigma_a, inflow C: b - A(C 1) = 0 up to fp32 rounding (closed form)."""
     import paper_2604_23265_b200 as P
     N, M, C = 16, 32, 1.5
@@ -106,7 +106,7 @@ def test_apply_manufactured_constant():
     b = torch.empty((1, N, N, M), dtype=torch.float32, device="cuda")
     P.rte_rhs(p, b)
     torch.cuda.synchronize()
-    assert _rel(y.cpu().numpy(), b.cpu().numpy().astype(np.float64)) < 1e-6
+    assert margin(_rel(y.cpu().numpy(), b.cpu().numpy().astype(np.float64)), 1e-6, "manufactured constant") < 1e-6
 
 
 # ---------------------------------------------------------------------------------------
@@ -132,7 +132,7 @@ VSMALL = [
 
 
 @pytest.mark.parametrize("cfg", [W.config(k) for k in (1, 2, 3)] + VSMALL, ids=lambda c: f"cfg{c.k}-N{c.N}-L{c.L}")
-def test_vcycle_parity(cfg):
+def test_vcycle_parity(cfg, margin):
     import paper_2604_23265_b200 as P
     p, net, onet, _ = _net_pair(cfg, std=0.05)
     r = W.make_vector(cfg, 2)
@@ -142,11 +142,11 @@ def test_vcycle_parity(cfg):
     torch.cuda.synchronize()
     v_gpu = z.cpu().numpy().astype(np.float64) - r
     v_ref = O.vcycle(onet, r, add_identity=False)
-    assert _rel(v_gpu, v_ref) <= 1e-5
+    assert margin(_rel(v_gpu, v_ref), 1e-5, "V(r) rel-L2") <= 1e-5
 
 
 @pytest.mark.parametrize("cfg", [W.config(k) for k in (1, 2)] + VSMALL, ids=lambda c: f"cfg{c.k}-N{c.N}-L{c.L}")
-def test_vcycle_f64_parity(cfg):
+def test_vcycle_f64_parity(cfg, margin):
     """The fp64 V-cycle (SIMT, same data flow) equals the oracle to 1e-12."""
     import paper_2604_23265_b200 as P
     p, net, onet, _ = _net_pair(cfg, std=0.05)
@@ -155,12 +155,12 @@ def test_vcycle_f64_parity(cfg):
     z = torch.empty_like(rd)
     P.mgnet_vcycle_f64(net, rd, z, add_identity=True)
     torch.cuda.synchronize()
-    assert _rel(z.cpu().numpy() - r, O.vcycle(onet, r, add_identity=False)) <= 1e-12
+    assert margin(_rel(z.cpu().numpy() - r, O.vcycle(onet, r, add_identity=False)), 1e-12, "fp64 V(r) rel-L2") <= 1e-12
 
 
 @pytest.mark.slow
 @pytest.mark.parametrize("k", [4, 5])
-def test_vcycle_parity_large(k):
+def test_vcycle_parity_large(k, margin):
     """Full-size configs 4 and 5 (config 4: oracle on the first two samples)."""
     import paper_2604_23265_b200 as P
     cfg = W.config(k)
@@ -173,7 +173,7 @@ def test_vcycle_parity_large(k):
     nb = 2 if k == 4 else 1
     v_gpu = z[:nb].cpu().numpy()
     v_ref = O.vcycle(onet, r[:nb], add_identity=False)
-    assert _rel(v_gpu, v_ref) <= 1e-5
+    assert margin(_rel(v_gpu, v_ref), 1e-5, "V(r) rel-L2") <= 1e-5
 
 
 @pytest.mark.parametrize("env", [{"RTE_TC_SS_MINW": "16"}, {"RTE_TC_PRESPLIT": "1"}, {"RTE_TC_CLUSTER": "1"},
@@ -262,49 +262,64 @@ def _gmres_pair(cfg, precond, rtol, maxit, std=0.02, reorth=3, precision=0):
 @pytest.mark.parametrize("precond,reorth,precision", [(False, 0, 0), (True, 0, 0), (False, 2, 0), (True, 2, 0),
                                                       (True, 1, 0), (True, 0, 1), (False, 2, 1), (False, 3, 0),
                                                       (True, 3, 0), (True, 3, 1)])
-def test_gmres_config1_converges_like_oracle(precond, reorth, precision):
+def test_gmres_config1_converges_like_oracle(precond, reorth, precision, margin):
     """reorth 0 = CGS2, 1 = CGS1, 2 = selective (DGKS), 3 = DCGS2; all equal MGS in exact arithmetic.
     precision 0 = fp32 basis (mixed), 1 = fp64 basis."""
     cfg = W.config(1)
     rep, x, ref = _gmres_pair(cfg, precond, cfg.rtol, cfg.maxit, reorth=reorth, precision=precision)
     r = rep[0]
     assert ref.converged and r["converged"]
-    assert abs(r["iterations"] - ref.iterations) <= 1
-    assert _rel(x, ref.x) <= 1e-4
+    assert margin(abs(r["iterations"] - ref.iterations), max(1, 1), "iterations vs oracle") <= 1
+    assert margin(_rel(x, ref.x), 1e-4, "x rel-L2") <= 1e-4
     assert r["relres_true"] <= cfg.rtol
 
 
 @pytest.mark.slow
 @pytest.mark.parametrize("precond", [False, True])
-def test_gmres_config2_fp64_basis_iterations_exact(precond):
+def test_gmres_config2_fp64_basis_iterations_exact(precond, margin):
     """Everything in fp64 (precision=1: basis, apply, V-cycle): the iteration count is within +-1
     of the oracle's and the solution within 1e-4 (north star), on the diffusive config 2."""
     cfg = W.config(2)
     rep, x, ref = _gmres_pair(cfg, precond, cfg.rtol, cfg.maxit, precision=1)
     r = rep[0]
     assert ref.converged and r["converged"]
-    assert abs(r["iterations"] - ref.iterations) <= 1
-    assert _rel(x, ref.x) <= 1e-4
+    assert margin(abs(r["iterations"] - ref.iterations), max(1, 1), "iterations vs oracle") <= 1
+    assert margin(_rel(x, ref.x), 1e-4, "x rel-L2") <= 1e-4
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("precond", [False, True])
-def test_gmres_config2_mixed_precision_band(precond):
-    """fp32 basis (the benchmarked mode): solution within 1e-4 and the iteration count within 2%.
-
-    Near rtol the restarted-GMRES residual of this diffusive problem falls ~1% per iteration, so
-    rounding-level differences in the Krylov vectors move the crossing by a few iterations and,
-    across a restart boundary, by up to ~1%: fp32 GPU variants measured 1313..1337 against the
-    oracle's 1327.  The +-1 count is asserted on the fp64-basis mode above."""
+def test_gmres_config2_benchmarked_mode_iterations_exact(margin):
+    """The north star on the hot path itself: MgNet-preconditioned GMRES(30) on the diffusive config 2 in
+    the benchmarked mode (fp32 Krylov basis, DCGS2 Gram-Schmidt, fp32 operator and V-cycle, fp64 iterate
+    and restart residual) reaches rtol in the oracle's iteration count +-1, with x to 1e-4."""
     cfg = W.config(2)
-    rep, x, ref = _gmres_pair(cfg, precond, cfg.rtol, cfg.maxit)
+    rep, x, ref = _gmres_pair(cfg, True, cfg.rtol, cfg.maxit)
     r = rep[0]
     assert ref.converged and r["converged"]
-    assert abs(r["iterations"] - ref.iterations) <= max(1, int(0.02 * ref.iterations))
-    assert _rel(x, ref.x) <= 1e-4
+    assert margin(abs(r["iterations"] - ref.iterations), 1, "iterations vs oracle") <= 1
+    assert margin(_rel(x, ref.x), 1e-4, "x rel-L2") <= 1e-4
 
 
-def test_gmres_small_batch_independent_solves():
+@pytest.mark.slow
+def test_gmres_config2_unpreconditioned_fp32_basis(margin):
+    """Secondary check, not the hot path (P = I, no MgNet): unpreconditioned GMRES(30) on config 2 with
+    the fp32 basis converges with x to 1e-4; its iteration count is held to 2% of the oracle's.
+
+    Why not +-1: without the preconditioner this diffusive solve takes 43 restart cycles and near rtol
+    the residual falls ~1% per iteration, so fp32 storage alone moves the crossing.  The fp32-storage
+    emulation of the same algorithm on the oracle's operator (scripts/emulate_fp32_gmres.py, oracle-only,
+    profiles/r02/emulate_fp32_gmres.json) takes 1289 (CGS2) and 1282 (DCGS2) iterations against the fp64
+    oracle's 1290; this GPU path measured 1288 (CGS2) and 1272 (DCGS2)."""
+    cfg = W.config(2)
+    rep, x, ref = _gmres_pair(cfg, False, cfg.rtol, cfg.maxit)
+    r = rep[0]
+    assert ref.converged and r["converged"]
+    band = max(1, int(0.02 * ref.iterations))
+    assert margin(abs(r["iterations"] - ref.iterations), band, "iterations vs oracle (2%)") <= band
+    assert margin(_rel(x, ref.x), 1e-4, "x rel-L2") <= 1e-4
+
+
+def test_gmres_small_batch_independent_solves(margin):
     """Config-4 style batch: each sample's solve matches the oracle solve of that sample alone."""
     cfg = W.small_config(4, N=8, M=16, n_polar=2, n_azim=8, B=3, L=2, C0=8)
     rep, x, _ = _gmres_pair(cfg, True, 1e-6, 600)
@@ -321,12 +336,12 @@ def test_gmres_small_batch_independent_solves():
         assert ref.converged == rep[s]["converged"]
         if ref.converged:
             assert abs(rep[s]["iterations"] - ref.iterations) <= 1
-            assert _rel(x[s], ref.x[0]) <= 1e-4
+            assert margin(_rel(x[s], ref.x[0]), 1e-4, f"x[{s}] rel-L2") <= 1e-4
 
 
 @pytest.mark.parametrize("k,steps,reorth", [(3, 5, 0), (2, 8, 0), (3, 5, 2), (2, 8, 2), (3, 5, 3), (2, 8, 3),
                                              (1, 12, 3)])
-def test_gmres_first_arnoldi_columns(k, steps, reorth):
+def test_gmres_first_arnoldi_columns(k, steps, reorth, margin):
     """Non-converging protocol: the first Arnoldi columns (unrotated H) agree to 1e-5."""
     import paper_2604_23265_b200 as P
     cfg = W.config(k)
@@ -345,11 +360,11 @@ def test_gmres_first_arnoldi_columns(k, steps, reorth):
     Href = O.arnoldi_columns(lambda v: O.apply(op, v), bd.cpu().numpy().astype(np.float64),
                              lambda v: O.vcycle(onet, v), steps)
     for j in range(steps):
-        assert _rel(H[:j + 2, j], Href[:j + 2, j]) <= 1e-5, j
+        assert margin(_rel(H[:j + 2, j], Href[:j + 2, j]), 1e-5, f"H column {j}") <= 1e-5, j
 
 
 @pytest.mark.slow
-def test_gmres_full_size_bench_configuration():
+def test_gmres_full_size_bench_configuration(margin):
     """Config 5 at full size in the launch configuration bench.py times (gmres_prepare's CUDA graphs,
     x0_zero, selective re-orthogonalisation): the first two Arnoldi columns (unrotated H) agree with
     the fp64 oracle to 1e-5, and the iterate of the 2-step solve is finite."""
@@ -373,4 +388,4 @@ def test_gmres_full_size_bench_configuration():
     Href = O.arnoldi_columns(lambda v: O.apply(op, v), bd.cpu().numpy().astype(np.float64),
                              lambda v: O.vcycle(onet, v), steps)
     for j in range(steps):
-        assert _rel(H[:j + 2, j], Href[:j + 2, j]) <= 1e-5, j
+        assert margin(_rel(H[:j + 2, j], Href[:j + 2, j]), 1e-5, f"H column {j}") <= 1e-5, j
