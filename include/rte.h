@@ -83,10 +83,43 @@ rte_status rte_setup(const rte_grid* grid, const rte_ordinates* ord,
                      rte_problem** out);
 void rte_destroy(rte_problem* p);
 
+/* rte_setup_tfps -- the TFPS alpha-space system of the same problem (NEXT-3; §2.2,
+ * eq:2DTFPS_linear_sys; readings R37-R39 in DESIGN.md §3).  Same arguments and validation as rte_setup,
+ * plus: every cell needs eps sigma_a > 0, and the medium must be piecewise constant with
+ * at most 4096 distinct (sample, sigma_t, sigma_s) materials (RTE_EINVAL otherwise).
+ * Per material it solves the local eigenproblems (gamma S - I) l = xi C l and (gamma S - I) l = xi S_y l,
+ * gamma = sigma_s/sigma_t (eq:discretization_2D_eigenfunc_constraint; host fp64, symmetrised and solved
+ * by Cholesky + Jacobi: all xi real), giving Md x-modes and Md y-modes per cell (Md = directions).
+ * The problem's vectors then hold the basis coefficients alpha [batch][N][N][2 Md] (x-modes by
+ * ascending xi, then y-modes), and on it
+ *   rte_rhs   writes b (particular-solution jumps and inflow rows),
+ *   rte_apply / rte_apply_f64 apply A alpha: the midpoint continuity rows of the faces x = i h
+ *             (slots [0, Md) of cell (j, i)) and y = j h (slots [Md, 2Md)); the boundary rows of a
+ *             row/column sit in the slots of its first cell (incoming directions only),
+ *   gmres_solve solves A alpha = b (precond 0, or 1 with an MgNet created on this problem: 2 Md input
+ *             channels; block Jacobi (2) is rejected),
+ *   rte_problem_info reports M = 2 Md.  The ordinate set (rte_get_ordinates) keeps Md entries. */
+rte_status rte_setup_tfps(const rte_grid* grid, const rte_ordinates* ord,
+                          const float* sigma_T, const float* sigma_a, const float* q,
+                          const float* eps, const float* g, const float* inflow,
+                          rte_problem** out);
+/* Host-only (no device work): the local modes of one material, as rte_setup_tfps computes them --
+ * xi [2M] (x-modes ascending, then y-modes ascending) and L [M][2M] row-major (column k = l^k) for the
+ * ordinates c, s, the row-stochastic S [M][M] (rte_hg_matrix) and gamma = sigma_s/sigma_t in [0, 1). */
+rte_status rte_tfps_modes(int M, const double* c, const double* s, const double* S, double gamma, double* xi,
+                          double* L);
+/* Materials of a TFPS problem: nmat, Md, and (host, may be NULL) xi [nmat][2 Md] and the eigenvectors
+ * L [nmat][Md][2 Md] (column k = l^k, ||l^k||_inf = 1, largest entry +1).  RTE_EINVAL if not TFPS. */
+rte_status rte_tfps_info(const rte_problem* p, int* nmat, int* Md, double* xi, double* L);
+/* psi at the cell centres from the coefficients (eq:2DTFPS_sol): psi_dev [batch][N][N][Md] =
+ * sum_k alpha^k chi^k(z_c) + chi^s, alpha_dev [batch][N][N][2 Md] (float32 / float64). */
+rte_status rte_tfps_reconstruct(const rte_problem* p, const float* alpha_dev, float* psi_dev, void* stream);
+rte_status rte_tfps_reconstruct_f64(const rte_problem* p, const double* alpha_dev, double* psi_dev, void* stream);
+
 /* Sizes of a problem: batch, N, M and n = batch*N*N*M. Any pointer may be NULL. */
 rte_status rte_problem_info(const rte_problem* p, int* batch, int* N, int* M, int64_t* n);
 
-/* Copy the ordinate set actually used (host arrays of length M; any may be NULL). */
+/* Copy the ordinate set actually used (host arrays of length M directions; any may be NULL). */
 rte_status rte_get_ordinates(const rte_problem* p, double* c, double* s, double* zeta, double* w);
 
 /* Host-only setup helpers (no device work; usable without a GPU):

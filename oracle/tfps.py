@@ -69,7 +69,8 @@ def local_modes(qd: R.Quadrature, S: np.ndarray, gamma: float) -> Modes:
         ev, V = ev[order], V[:, order]
         for k in range(M):
             v = V[:, k]
-            big = np.argmax(np.abs(v))                            # (first index on ties)
+            a = np.abs(v)                                         # ties (within 1e-9, e.g. the +-1 pairs of
+            big = int(np.nonzero(a >= a.max() * (1 - 1e-9))[0][0])   # the symmetric quadrature): lowest index
             V[:, k] = v / v[big]                                  # ||l||_inf = 1, largest entry +1
         xis.append(ev)
         Ls.append(V)

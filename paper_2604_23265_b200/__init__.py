@@ -15,7 +15,8 @@ import numpy as np
 from . import _lib
 from ._lib import RTE_ENUMERIC, RTE_OK, RteError, check, gmres_opts, gmres_report, lib
 
-__all__ = ["Problem", "MgNet", "rte_setup", "rte_rhs", "rte_apply", "rte_apply_f64", "rte_blockjacobi_apply", "mgnet_create",
+__all__ = ["Problem", "MgNet", "rte_setup", "rte_setup_tfps", "rte_tfps_info", "rte_tfps_modes", "rte_tfps_reconstruct",
+           "rte_tfps_reconstruct_f64", "rte_rhs", "rte_apply", "rte_apply_f64", "rte_blockjacobi_apply", "mgnet_create",
            "mgnet_vcycle", "mgnet_vcycle_f64", "mgnet_coeffnet", "mgnet_coeffnet_weight_count", "mgnet_modulation", "gmres_prepare", "gmres_solve", "gmres_solve_host", "rte_quadrature", "rte_hg_matrix", "rte_launch_count", "rte_timing_enable", "rte_timing_filter", "rte_timing_reset",
            "rte_timing_get", "RteError", "LIB_PATH"]
 
@@ -65,11 +66,16 @@ class Problem:
         return self._h
 
     @property
+    def is_tfps(self) -> bool:
+        return lib.rte_tfps_info(self._h, None, None, None, None) == RTE_OK
+
+    @property
     def shape(self):
         return (self.batch, self.N, self.N, self.M)
 
     def ordinates(self):
-        arrs = [np.zeros(self.M) for _ in range(4)]
+        nd = self.M // 2 if self.is_tfps else self.M
+        arrs = [np.zeros(nd) for _ in range(4)]
         check("rte_get_ordinates", lib.rte_get_ordinates(self._h, *[_dptr(a) for a in arrs]))
         return tuple(arrs)   # c, s, zeta, w
 
@@ -86,7 +92,8 @@ class Problem:
 
 
 def rte_setup(N: int, sigma_T, sigma_a, q, eps, g, inflow=None, *, n_polar: int = 0, n_azim: int = 0,
-              ordinates: Optional[Sequence[np.ndarray]] = None, batch: Optional[int] = None) -> Problem:
+              ordinates: Optional[Sequence[np.ndarray]] = None, batch: Optional[int] = None,
+              _fn: str = "rte_setup") -> Problem:
     """rte_setup(grid, ordinates, sigma_T, sigma_a, q, eps, g, inflow) -> Problem (host inputs)."""
     sT, sA, qq, ee = (_f32(a) for a in (sigma_T, sigma_a, q, eps))
     B = batch if batch is not None else (sT.shape[0] if sT.ndim == 3 else 1)
@@ -101,10 +108,45 @@ def rte_setup(N: int, sigma_T, sigma_a, q, eps, g, inflow=None, *, n_polar: int 
     inf = _fptr(_f32(inflow)) if inflow is not None else None
     infa = _f32(inflow) if inflow is not None else None
     h = C.c_void_p()
-    check("rte_setup", lib.rte_setup(C.byref(grid), C.byref(ordn), _fptr(sT), _fptr(sA), _fptr(qq), _fptr(ee),
-                                     _fptr(gg), _fptr(infa) if infa is not None else None, C.byref(h)))
+    check(_fn, getattr(lib, _fn)(C.byref(grid), C.byref(ordn), _fptr(sT), _fptr(sA), _fptr(qq), _fptr(ee),
+                                 _fptr(gg), _fptr(infa) if infa is not None else None, C.byref(h)))
     del keep, inf
     return Problem(h)
+
+
+def rte_setup_tfps(N: int, sigma_T, sigma_a, q, eps, g, inflow=None, **kw) -> Problem:
+    """rte_setup_tfps: the TFPS alpha-space system of the same problem (NEXT-3, include/rte.h); the
+    Problem's vectors hold alpha [batch][N][N][2 Md] (Problem.M = 2 Md)."""
+    return rte_setup(N, sigma_T, sigma_a, q, eps, g, inflow, _fn="rte_setup_tfps", **kw)
+
+
+def rte_tfps_modes(c, s, S, gamma: float):
+    """Host-only: (xi [2M], L [M][2M]) of one TFPS material (include/rte.h rte_tfps_modes)."""
+    c, s, S = (np.ascontiguousarray(np.asarray(a, np.float64)) for a in (c, s, S))
+    M = c.size
+    xi, L = np.zeros(2 * M), np.zeros((M, 2 * M))
+    check("rte_tfps_modes", lib.rte_tfps_modes(M, _dptr(c), _dptr(s), _dptr(S), float(gamma), _dptr(xi), _dptr(L)))
+    return xi, L
+
+
+def rte_tfps_info(p: Problem):
+    """(xi [nmat][2Md], L [nmat][Md][2Md]) of a TFPS problem's materials (host fp64)."""
+    nm, md = C.c_int(), C.c_int()
+    check("rte_tfps_info", lib.rte_tfps_info(p.handle, C.byref(nm), C.byref(md), None, None))
+    xi = np.zeros((nm.value, 2 * md.value))
+    L = np.zeros((nm.value, md.value, 2 * md.value))
+    check("rte_tfps_info", lib.rte_tfps_info(p.handle, None, None, _dptr(xi), _dptr(L)))
+    return xi, L
+
+
+def rte_tfps_reconstruct(p: Problem, alpha, psi, stream=None) -> None:
+    check("rte_tfps_reconstruct", lib.rte_tfps_reconstruct(p.handle, _dev(alpha, "f32"), _dev(psi, "f32"),
+                                                           C.c_void_p(_stream(stream))))
+
+
+def rte_tfps_reconstruct_f64(p: Problem, alpha, psi, stream=None) -> None:
+    check("rte_tfps_reconstruct_f64", lib.rte_tfps_reconstruct_f64(p.handle, _dev(alpha, "f64"), _dev(psi, "f64"),
+                                                                   C.c_void_p(_stream(stream))))
 
 
 def rte_quadrature(n_polar: int, n_azim: int):

@@ -47,6 +47,14 @@ _fp = C.POINTER(C.c_float)
 SIGS = {
     "rte_setup": (C.c_int, [C.POINTER(rte_grid), C.POINTER(rte_ordinates), _fp, _fp, _fp, _fp, _fp, _fp,
                             C.POINTER(_vp)]),
+    "rte_setup_tfps": (C.c_int, [C.POINTER(rte_grid), C.POINTER(rte_ordinates), _fp, _fp, _fp, _fp, _fp, _fp,
+                                 C.POINTER(_vp)]),
+    "rte_tfps_modes": (C.c_int, [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                 C.c_double, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "rte_tfps_info": (C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_double),
+                                C.POINTER(C.c_double)]),
+    "rte_tfps_reconstruct": (C.c_int, [_vp, _vp, _vp, _vp]),
+    "rte_tfps_reconstruct_f64": (C.c_int, [_vp, _vp, _vp, _vp]),
     "rte_destroy": (None, [_vp]),
     "rte_problem_info": (C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int),
                                    C.POINTER(C.c_int64)]),

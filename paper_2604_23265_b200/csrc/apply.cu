@@ -381,6 +381,10 @@ double apply_bytes(const rte_problem* p, int elt, int b_elt) {
 }
 
 void launch_rhs(const rte_problem* p, float* b, cudaStream_t st) {
+  if (p->kind == 1) {
+    launch_tfps_rhs(p, b, st);
+    return;
+  }
   int64_t n = p->n;
   int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 16);
   prof_begin(st, "rhs");
@@ -390,6 +394,10 @@ void launch_rhs(const rte_problem* p, float* b, cudaStream_t st) {
 
 void launch_apply_f32(const rte_problem* p, const float* x, float* y, const double* alpha, int alpha_stride,
                       cudaStream_t st) {
+  if (p->kind == 1) {
+    launch_tfps_apply<float>(p, x, y, alpha, alpha_stride, nullptr, st);
+    return;
+  }
   if (p->tc_apply) {
     launch_apply_tc(p, x, y, alpha, alpha_stride, st);
     return;
@@ -400,6 +408,10 @@ void launch_apply_f32(const rte_problem* p, const float* x, float* y, const doub
 }
 
 void launch_apply_f64(const rte_problem* p, const double* x, double* y, const float* b, cudaStream_t st) {
+  if (p->kind == 1) {
+    launch_tfps_apply<double>(p, x, y, nullptr, 0, b, st);
+    return;
+  }
   prof_begin(st, "apply_f64_simt");
   launch_simt<double>(p, x, y, p->St64, p->sig_d64, p->sig_s64, p->ax64, p->ay64, b, nullptr, 0, st);
   after_launch("apply_f64_simt", st, apply_flops(p), apply_bytes(p, 8, b ? 4 : 0), 3);

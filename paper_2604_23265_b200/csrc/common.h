@@ -84,7 +84,7 @@ __host__ __device__ __forceinline__ T stencil_diag(T ax, T ay, T sd, T ss, T psi
 
 // ---- problem ----------------------------------------------------------------
 struct rte_problem {
-  int B, N, M;
+  int B, N, M;        // M: unknowns per cell (directions; 2 x directions for a TFPS problem)
   int64_t ncell;      // B*N*N
   int64_t n;          // ncell*M
   // host copies (fp64)
@@ -116,6 +116,19 @@ struct rte_problem {
   // block-Jacobi inverse cell blocks [ncell][M][M] (blockjacobi.cu; built on first use)
   mutable double* bj64 = nullptr;
   mutable float* bj32 = nullptr;
+  // ---- TFPS alpha-space problem (kind 1, rte_setup_tfps; tfps.cu).  Md = directions, M = 2 Md.
+  int kind = 0;             // 0: psi-space DO operator, 1: TFPS alpha-space operator
+  int Md = 0;
+  int nmat = 0;
+  int* tf_mat = nullptr;    // [B][N][N] material index
+  float* tf_L32 = nullptr;  // [nmat][Md][2Md] eigenvectors (columns)
+  double* tf_L64 = nullptr;
+  float* tf_fac32 = nullptr;  // [nmat][5][2Md] basis factors at faces L, R, B, T and the centre
+  double* tf_fac64 = nullptr;
+  float* tf_chis32 = nullptr;  // [B][N][N] particular solution f / (sigma_t - sigma_s)
+  double* tf_chis64 = nullptr;
+  std::vector<double> tf_xi;   // host copies: [nmat][2Md], [nmat][Md][2Md]
+  std::vector<double> tf_Lh;
 };
 
 // ---- kernel launchers (apply.cu) --------------------------------------------
@@ -146,4 +159,14 @@ bool prof_wants_any(const std::vector<std::string>& classes);    // timing would
 void drop_net_graphs(const struct ::mgnet_net* net);  // (krylov.cu) forget graphs using `net`
 void launch_apply_tc(const rte_problem* p, const float* x, float* y, const double* alpha_dev,
                      int alpha_stride, cudaStream_t st);
+// TFPS alpha-space operator (tfps.cu, tfps_setup.cpp)
+template <typename T>
+void launch_tfps_apply(const rte_problem* p, const T* x, T* y, const double* alpha_dev, int alpha_stride,
+                       const float* b, cudaStream_t st);
+void launch_tfps_rhs(const rte_problem* p, float* b, cudaStream_t st);
+template <typename T>
+void launch_tfps_reconstruct(const rte_problem* p, const T* alpha, T* psi, cudaStream_t st);
+void tfps_local_modes(const double* S, const std::vector<double>& c, const std::vector<double>& s, double gamma,
+                      std::vector<double>& xi, std::vector<double>& L);
+void tfps_face_factors(const std::vector<double>& xi, int M, double sigma_t, double h, double* fac);
 }  // namespace rte

@@ -7,7 +7,9 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
+#include <map>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "common.h"
@@ -305,7 +307,8 @@ static void free_problem(rte_problem* p) {
   if (!p) return;
   void* ptrs[] = {p->sig_t, p->sig_s, p->sig_d, p->sig_d64, p->f, p->sig_t64, p->sig_s64, p->S32, p->St32, p->St64, p->S_hi,
                   p->S_lo, p->ax, p->ay, p->ax64, p->ay64, p->sgx, p->sgy, p->inflow, p->scratch64,
-                  p->bj64, p->bj32};
+                  p->bj64, p->bj32, p->tf_mat, p->tf_L32, p->tf_L64, p->tf_fac32, p->tf_fac64, p->tf_chis32,
+                  p->tf_chis64};
   for (void* q : ptrs) dfree(q);
   free_tc_state(p);
   free_gmres_work(p);
@@ -438,6 +441,118 @@ rte_status rte_setup(const rte_grid* grid, const rte_ordinates* ord, const float
   }
 }
 
+rte_status rte_setup_tfps(const rte_grid* grid, const rte_ordinates* ord, const float* sigma_T, const float* sigma_a,
+                          const float* q, const float* eps, const float* g, const float* inflow, rte_problem** out) {
+  rte_problem* p = nullptr;
+  try {
+    RTE_REQUIRE(out, "rte_setup_tfps: NULL argument");
+    *out = nullptr;
+    // the psi-space setup validates the inputs and builds quadrature, S and the coefficient fields
+    const rte_status st0 = rte_setup(grid, ord, sigma_T, sigma_a, q, eps, g, inflow, &p);
+    if (st0 != RTE_OK) return st0;
+    const int B = p->B, N = p->N, Md = p->M;
+    const double h = 1.0 / N;
+    // materials: distinct (sample, sigma_t, sigma_s) of the cells (R7); the TFPS
+    // basis needs sigma_t - sigma_s = eps sigma_a > 0
+    std::map<std::tuple<int, double, double>, int> index;
+    std::vector<int> mat(p->ncell);
+    std::vector<double> chis(p->ncell);
+    std::vector<std::tuple<int, double, double>> keys;
+    for (int64_t k = 0; k < p->ncell; ++k) {
+      const double e = eps[k], sT = sigma_T[k], sA = sigma_a[k];
+      const double t = sT / e, sc = sT / e - e * sA;
+      RTE_REQUIRE(e * sA > 0.0, "rte_setup_tfps: TFPS needs eps sigma_a > 0 in every cell (PAPER.md:117)");
+      const int b = (int)(k / ((int64_t)N * N));
+      auto key = std::make_tuple(b, t, sc);
+      auto it = index.find(key);
+      if (it == index.end()) {
+        RTE_REQUIRE(index.size() < 4096, "rte_setup_tfps: more than 4096 distinct materials (piecewise-constant "
+                                         "media with few materials only)");
+        it = index.emplace(key, (int)keys.size()).first;
+        keys.push_back(key);
+      }
+      mat[k] = it->second;
+      chis[k] = (e * (double)q[k]) / (e * sA);  // f / (sigma_t - sigma_s)
+    }
+    const int nmat = (int)keys.size();
+    const int K = 2 * Md;
+    std::vector<double> LT((size_t)nmat * K * Md), fac((size_t)nmat * 5 * K);
+    p->tf_xi.assign((size_t)nmat * K, 0.0);
+    p->tf_Lh.assign((size_t)nmat * Md * K, 0.0);
+    for (int mi = 0; mi < nmat; ++mi) {
+      const int b = std::get<0>(keys[mi]);
+      const double t = std::get<1>(keys[mi]), sc = std::get<2>(keys[mi]);
+      std::vector<double> xi, L;
+      tfps_local_modes(p->S.data() + (size_t)b * Md * Md, p->c, p->s, sc / t, xi, L);
+      for (int k = 0; k < K; ++k) {
+        p->tf_xi[(size_t)mi * K + k] = xi[k];
+        for (int m = 0; m < Md; ++m) {
+          LT[((size_t)mi * K + k) * Md + m] = L[(size_t)m * K + k];
+          p->tf_Lh[((size_t)mi * Md + m) * K + k] = L[(size_t)m * K + k];
+        }
+      }
+      tfps_face_factors(xi, Md, t, h, fac.data() + (size_t)mi * 5 * K);
+    }
+    std::vector<float> LT32(LT.begin(), LT.end()), fac32(fac.begin(), fac.end()), chis32(chis.begin(), chis.end());
+    p->kind = 1;
+    p->Md = Md;
+    p->M = K;
+    p->n = p->ncell * K;
+    p->nmat = nmat;
+    p->tc_apply = false;
+    p->tf_mat = dalloc<int>(p->ncell); upload(p->tf_mat, mat.data(), p->ncell);
+    p->tf_L64 = dalloc<double>(LT.size()); upload(p->tf_L64, LT.data(), LT.size());
+    p->tf_L32 = dalloc<float>(LT.size()); upload(p->tf_L32, LT32.data(), LT.size());
+    p->tf_fac64 = dalloc<double>(fac.size()); upload(p->tf_fac64, fac.data(), fac.size());
+    p->tf_fac32 = dalloc<float>(fac.size()); upload(p->tf_fac32, fac32.data(), fac.size());
+    p->tf_chis64 = dalloc<double>(p->ncell); upload(p->tf_chis64, chis.data(), p->ncell);
+    p->tf_chis32 = dalloc<float>(p->ncell); upload(p->tf_chis32, chis32.data(), p->ncell);
+    *out = p;
+    return RTE_OK;
+  } catch (const Fail& f) {
+    free_problem(p);
+    return f.st;
+  } catch (const std::exception& e) {
+    free_problem(p);
+    set_error(std::string("internal: ") + e.what());
+    return RTE_EINTERNAL;
+  }
+}
+
+rte_status rte_tfps_modes(int M, const double* c, const double* s, const double* S, double gamma, double* xi,
+                          double* L) {
+  RTE_API_BEGIN
+  RTE_REQUIRE(M >= 2 && c && s && S && xi && L, "rte_tfps_modes: bad argument");
+  std::vector<double> vc(c, c + M), vs(s, s + M), x, l;
+  tfps_local_modes(S, vc, vs, gamma, x, l);
+  memcpy(xi, x.data(), x.size() * sizeof(double));
+  memcpy(L, l.data(), l.size() * sizeof(double));
+  RTE_API_END
+}
+
+rte_status rte_tfps_info(const rte_problem* p, int* nmat, int* Md, double* xi, double* L) {
+  if (!p || p->kind != 1) { set_error("rte_tfps_info: not a TFPS problem"); return RTE_EINVAL; }
+  if (nmat) *nmat = p->nmat;
+  if (Md) *Md = p->Md;
+  if (xi) memcpy(xi, p->tf_xi.data(), p->tf_xi.size() * sizeof(double));
+  if (L) memcpy(L, p->tf_Lh.data(), p->tf_Lh.size() * sizeof(double));
+  return RTE_OK;
+}
+
+rte_status rte_tfps_reconstruct(const rte_problem* p, const float* alpha_dev, float* psi_dev, void* stream) {
+  RTE_API_BEGIN
+  RTE_REQUIRE(p && alpha_dev && psi_dev && p->kind == 1, "rte_tfps_reconstruct: NULL argument or not a TFPS problem");
+  launch_tfps_reconstruct<float>(p, alpha_dev, psi_dev, as_stream(stream));
+  RTE_API_END
+}
+
+rte_status rte_tfps_reconstruct_f64(const rte_problem* p, const double* alpha_dev, double* psi_dev, void* stream) {
+  RTE_API_BEGIN
+  RTE_REQUIRE(p && alpha_dev && psi_dev && p->kind == 1, "rte_tfps_reconstruct_f64: NULL argument or not a TFPS problem");
+  launch_tfps_reconstruct<double>(p, alpha_dev, psi_dev, as_stream(stream));
+  RTE_API_END
+}
+
 rte_status rte_problem_info(const rte_problem* p, int* batch, int* N, int* M, int64_t* n) {
   if (!p) { set_error("rte_problem_info: NULL problem"); return RTE_EINVAL; }
   if (batch) *batch = p->B;
@@ -449,10 +564,11 @@ rte_status rte_problem_info(const rte_problem* p, int* batch, int* N, int* M, in
 
 rte_status rte_get_ordinates(const rte_problem* p, double* c, double* s, double* zeta, double* w) {
   if (!p) { set_error("rte_get_ordinates: NULL problem"); return RTE_EINVAL; }
-  if (c) memcpy(c, p->c.data(), p->M * sizeof(double));
-  if (s) memcpy(s, p->s.data(), p->M * sizeof(double));
-  if (zeta) memcpy(zeta, p->zeta.data(), p->M * sizeof(double));
-  if (w) memcpy(w, p->w.data(), p->M * sizeof(double));
+  const size_t nd = p->c.size();  // directions (p->M counts unknowns per cell: 2 x directions for TFPS)
+  if (c) memcpy(c, p->c.data(), nd * sizeof(double));
+  if (s) memcpy(s, p->s.data(), nd * sizeof(double));
+  if (zeta) memcpy(zeta, p->zeta.data(), nd * sizeof(double));
+  if (w) memcpy(w, p->w.data(), nd * sizeof(double));
   return RTE_OK;
 }
 

@@ -1,0 +1,185 @@
+// TFPS alpha-space problem setup (NEXT-3; §2.2, readings R37-R39 in DESIGN.md §3),
+// host fp64: per material the two local eigenproblems of eq:discretization_2D_eigenfunc_constraint,
+//   x-modes: (gamma S - I) l = xi C l,   y-modes: (gamma S - I) l = xi S_y l,   gamma = sigma_s / sigma_t,
+// then the basis values at the four face midpoints and the centre of a cell (eq:2D_eigenfunc).
+//
+// Eigen solver (our own; no LAPACK): S = K~ W is row-stochastic with positive entries, and the
+// diagonal Delta_m = S_0m / S_m0 (Delta_0 = 1) symmetrises it (Delta S = W kappa W up to a factor, since
+// K~ = D^-1 kappa with kappa symmetric).  Multiplying by Delta,
+//   P l = lambda E l,   P = Delta (I - gamma S) (symmetric, strictly diagonally dominant with a positive
+//   diagonal for gamma < 1, hence SPD),   E = Delta D (diagonal, D = C or S_y),   lambda = -xi.
+// With P = R R^T (Cholesky) and y = R^T l:  R^-1 E R^-T y = (1/lambda) y, a symmetric eigenproblem,
+// solved by cyclic Jacobi rotations.  So xi = -1/mu, l = R^-T y: every eigenvalue is real, as the
+// paper's ordering presumes.  Eigenvectors are scaled to ||l||_inf = 1 with the largest-|.| entry
+// positive (first index on ties).
+#include <math.h>
+
+#include <algorithm>
+#include <map>
+#include <numeric>
+#include <tuple>
+#include <vector>
+
+#include "common.h"
+
+namespace rte {
+
+namespace {
+
+// Cholesky P = R R^T (R lower, row-major n x n); fails if P is not SPD.
+void cholesky(std::vector<double>& P, int n) {
+  for (int j = 0; j < n; ++j) {
+    double d = P[(size_t)j * n + j];
+    for (int k = 0; k < j; ++k) d -= P[(size_t)j * n + k] * P[(size_t)j * n + k];
+    RTE_REQUIRE(d > 0.0, "rte_setup_tfps: local operator not positive definite (sigma_t <= sigma_s?)");
+    const double r = sqrt(d);
+    P[(size_t)j * n + j] = r;
+    for (int i = j + 1; i < n; ++i) {
+      double s = P[(size_t)i * n + j];
+      for (int k = 0; k < j; ++k) s -= P[(size_t)i * n + k] * P[(size_t)j * n + k];
+      P[(size_t)i * n + j] = s / r;
+    }
+    for (int k = j + 1; k < n; ++k) P[(size_t)j * n + k] = 0.0;
+  }
+}
+
+// Cyclic Jacobi eigen-decomposition of the symmetric A (destroyed): eigenvalues in ev, eigenvectors
+// as the columns of V (row-major).
+void jacobi_eig(std::vector<double>& A, int n, std::vector<double>& ev, std::vector<double>& V) {
+  V.assign((size_t)n * n, 0.0);
+  for (int i = 0; i < n; ++i) V[(size_t)i * n + i] = 1.0;
+  auto a = [&](int i, int j) -> double& { return A[(size_t)i * n + j]; };
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    double off = 0.0, tot = 0.0;
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) {
+        tot += a(i, j) * a(i, j);
+        if (i != j) off += a(i, j) * a(i, j);
+      }
+    if (off <= 1e-30 * tot) break;
+    for (int p = 0; p < n - 1; ++p)
+      for (int q = p + 1; q < n; ++q) {
+        const double apq = a(p, q);
+        if (fabs(apq) < 1e-300) continue;
+        const double theta = (a(q, q) - a(p, p)) / (2.0 * apq);
+        const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+        const double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
+        for (int k = 0; k < n; ++k) {  // columns p, q
+          const double akp = a(k, p), akq = a(k, q);
+          a(k, p) = c * akp - s * akq;
+          a(k, q) = s * akp + c * akq;
+        }
+        for (int k = 0; k < n; ++k) {  // rows p, q
+          const double apk = a(p, k), aqk = a(q, k);
+          a(p, k) = c * apk - s * aqk;
+          a(q, k) = s * apk + c * aqk;
+        }
+        for (int k = 0; k < n; ++k) {
+          const double vkp = V[(size_t)k * n + p], vkq = V[(size_t)k * n + q];
+          V[(size_t)k * n + p] = c * vkp - s * vkq;
+          V[(size_t)k * n + q] = s * vkp + c * vkq;
+        }
+      }
+  }
+  ev.resize(n);
+  for (int i = 0; i < n; ++i) ev[i] = a(i, i);
+}
+
+}  // namespace
+
+// Modes of one material: xi [2M] (x-modes ascending, then y-modes ascending), L [M][2M] row-major
+// (column k = eigenvector k).
+void tfps_local_modes(const double* S, const std::vector<double>& c, const std::vector<double>& s, double gamma,
+                      std::vector<double>& xi, std::vector<double>& L) {
+  const int M = (int)c.size();
+  RTE_REQUIRE(gamma >= 0.0 && gamma < 1.0, "rte_setup_tfps: need 0 <= sigma_s / sigma_t < 1");
+  std::vector<double> delta(M);
+  for (int m = 0; m < M; ++m) delta[m] = S[m] / S[(size_t)m * M];  // S_0m / S_m0
+  xi.assign(2 * M, 0.0);
+  L.assign((size_t)M * 2 * M, 0.0);
+  for (int axis = 0; axis < 2; ++axis) {
+    const std::vector<double>& d = axis == 0 ? c : s;
+    std::vector<double> P((size_t)M * M);
+    for (int i = 0; i < M; ++i)
+      for (int j = 0; j < M; ++j) {
+        // symmetric part of Delta (I - gamma S) (exactly symmetric in exact arithmetic)
+        const double a = delta[i] * ((i == j ? 1.0 : 0.0) - gamma * S[(size_t)i * M + j]);
+        const double b = delta[j] * ((i == j ? 1.0 : 0.0) - gamma * S[(size_t)j * M + i]);
+        P[(size_t)i * M + j] = 0.5 * (a + b);
+      }
+    cholesky(P, M);  // P = R R^T, R lower
+    // T = R^-1 E R^-T with E = diag(delta d): first X = R^-1 diag(e) (forward substitution per column),
+    // then T = X R^-T = (R^-1 X^T)^T
+    std::vector<double> X((size_t)M * M, 0.0), Tm((size_t)M * M, 0.0);
+    for (int col = 0; col < M; ++col) {  // solve R x = e_col * E_col
+      std::vector<double> x(M, 0.0);
+      for (int i = 0; i < M; ++i) {
+        double r = (i == col ? delta[col] * d[col] : 0.0);
+        for (int k = 0; k < i; ++k) r -= P[(size_t)i * M + k] * x[k];
+        x[i] = r / P[(size_t)i * M + i];
+      }
+      for (int i = 0; i < M; ++i) X[(size_t)i * M + col] = x[i];
+    }
+    for (int row = 0; row < M; ++row) {  // solve R t = X[row, :]^T  ->  T[:, row] ... T symmetric
+      std::vector<double> t(M, 0.0);
+      for (int i = 0; i < M; ++i) {
+        double r = X[(size_t)row * M + i];
+        for (int k = 0; k < i; ++k) r -= P[(size_t)i * M + k] * t[k];
+        t[i] = r / P[(size_t)i * M + i];
+      }
+      for (int i = 0; i < M; ++i) Tm[(size_t)row * M + i] = t[i];
+    }
+    for (int i = 0; i < M; ++i)  // symmetrise the rounding
+      for (int j = i + 1; j < M; ++j) {
+        const double v = 0.5 * (Tm[(size_t)i * M + j] + Tm[(size_t)j * M + i]);
+        Tm[(size_t)i * M + j] = Tm[(size_t)j * M + i] = v;
+      }
+    std::vector<double> mu, Y;
+    jacobi_eig(Tm, M, mu, Y);
+    // xi = -1/mu, l = R^-T y (back substitution with R^T)
+    std::vector<std::pair<double, std::vector<double>>> pairs;
+    for (int k = 0; k < M; ++k) {
+      RTE_REQUIRE(fabs(mu[k]) > 1e-300, "rte_setup_tfps: zero eigenvalue");
+      std::vector<double> l(M);
+      for (int i = M - 1; i >= 0; --i) {
+        double r = Y[(size_t)i * M + k];
+        for (int j = i + 1; j < M; ++j) r -= P[(size_t)j * M + i] * l[j];
+        l[i] = r / P[(size_t)i * M + i];
+      }
+      double amax = 0.0;
+      for (int i = 0; i < M; ++i) amax = std::max(amax, fabs(l[i]));
+      int big = 0;  // the lowest index within 1e-9 of the largest magnitude (ties: the +-1 pairs)
+      while (fabs(l[big]) < amax * (1.0 - 1e-9)) ++big;
+      const double sc = l[big];
+      for (double& v : l) v /= sc;
+      pairs.emplace_back(-1.0 / mu[k], l);
+    }
+    std::sort(pairs.begin(), pairs.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+    for (int k = 0; k < M; ++k) {
+      xi[axis * M + k] = pairs[k].first;
+      for (int i = 0; i < M; ++i) L[(size_t)i * 2 * M + axis * M + k] = pairs[k].second[i];
+    }
+  }
+}
+
+// Basis values of one material at the face midpoints f = L, R, B, T and the centre C of a cell of side
+// h (eq:2D_eigenfunc with the R38 reference points): fac[f][k] = exp(sigma_t xi_k (z_f - z_ref,k)) along
+// the mode's axis; chi^k(z_f) = fac[f][k] l^k.
+void tfps_face_factors(const std::vector<double>& xi, int M, double sigma_t, double h, double* fac /*[5][2M]*/) {
+  for (int k = 0; k < 2 * M; ++k) {
+    const bool xmode = k < M;
+    const double x = xi[k];
+    // offset of each face midpoint from the reference face along the mode's axis
+    // (reference: the low face for xi < 0, the high face for xi > 0)
+    const double lo = x < 0 ? 0.0 : -h, hi = x < 0 ? h : 0.0, mid = x < 0 ? 0.5 * h : -0.5 * h;
+    double off[5];
+    if (xmode) {  // faces L, R along x; B, T, C at the centre in x
+      off[0] = lo; off[1] = hi; off[2] = mid; off[3] = mid; off[4] = mid;
+    } else {
+      off[0] = mid; off[1] = mid; off[2] = lo; off[3] = hi; off[4] = mid;
+    }
+    for (int f = 0; f < 5; ++f) fac[(size_t)f * 2 * M + k] = exp(sigma_t * x * off[f]);
+  }
+}
+
+}  // namespace rte

@@ -104,3 +104,20 @@ def test_host_buffer_validation():
     t = torch.zeros(8, dtype=torch.float64)
     assert P._host(t, "f64", True).value == t.data_ptr()
     assert [f[0] for f in P.gmres_opts._fields_][-1] == "x0_zero"
+
+
+@pytest.mark.parametrize("n_polar,n_azim,g,gamma", [(1, 8, 0.5, 0.99), (2, 16, 0.5, 0.99999), (4, 16, 0.9, 0.5),
+                                                   (2, 8, 0.0, 0.0)])
+def test_host_tfps_modes_match_oracle(n_polar, n_azim, g, gamma):
+    """The library's TFPS eigen solver (symmetrised Cholesky + Jacobi, tfps_setup.cpp) against the oracle's
+    numpy.linalg.eig of C^-1 (gamma S - I) (oracle/tfps.py): same xi, same normalised eigenvectors."""
+    import paper_2604_23265_b200 as P
+    from oracle import rte as O
+    from oracle import tfps as T
+    qd = O.quadrature(n_polar, n_azim)
+    _, S = O.scattering_matrix(qd, g)
+    xi, L = P.rte_tfps_modes(qd.c, qd.s, S, gamma)
+    md = T.local_modes(qd, S, gamma)
+    assert np.allclose(xi, md.xi, rtol=1e-10, atol=1e-12)
+    if gamma > 0:   # (gamma = 0: degenerate eigenvalues, eigenvectors defined up to a basis of each eigenspace)
+        assert np.allclose(L, md.L, rtol=1e-8, atol=1e-9)
