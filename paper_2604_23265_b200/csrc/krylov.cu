@@ -225,53 +225,61 @@ __global__ void __launch_bounds__(kThreads, 1) dcgs_update_kernel(
 //   V_{j+1} = r w~ = w - Q_j d,  d = c + r h_{.,j}               (w~: first-pass projection of A P q_j)
 // expressed on the stored vectors (cA: V_j's correction, cB: V_{j+1}'s projection).  Writes the final
 // alpha_j = alpha~_j / r, column j of the unrotated H (Hc, also hcol for the Givens kernel) and r.
-__global__ void dcgs_coef_kernel(int B, int j, int m, const double* __restrict__ a, const double* __restrict__ z,
-                                 int hld, double* Hc, double* alpha, int alpha_ld, double* cA, double* cB,
-                                 double* hcol, double* rbuf, const int* __restrict__ active) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(32) dcgs_coef_kernel(int B, int j, int m, const double* __restrict__ a,
+                                                       const double* __restrict__ z, int hld, double* Hc,
+                                                       double* alpha, int alpha_ld, double* cA, double* cB,
+                                                       double* hcol, double* rbuf, const int* __restrict__ active) {
+  // one warp per sample; lane i owns row i of the column (j <= 31 < 32 lanes, restart <= 32)
+  const int b = blockIdx.x, i = threadIdx.x;
   if (b >= B || !active[b]) return;
+  __shared__ double s_sh[32];
   double* H = Hc + (int64_t)b * (m + 1) * m;  // [m+1][m]
   double* al = alpha + (int64_t)b * alpha_ld;
   const double* ab = a + (int64_t)b * hld;
   const double* zb = z + (int64_t)b * hld;
   const double at = al[j];
-  double s[kMaxRestart + 1], c[kMaxRestart + 1], h[kMaxRestart + 1];
-  double ss = 0.0;
-  for (int i = 0; i < j; ++i) {
-    s[i] = ab[i] * at;
-    ss += s[i] * s[i];
+  const double si = i < j ? ab[i] * at : 0.0;
+  const double zi = i <= j ? zb[i] : 0.0;
+  const double ali = i < j ? al[i] : 0.0;
+  s_sh[i] = si;
+  double ss = si * si, sz = si * zi;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    sz += __shfl_xor_sync(0xffffffffu, sz, o);
   }
   const double r = sqrt(fmax(1.0 - ss, 1e-300));
   if (j > 0) {
     const double hl = H[j * m + (j - 1)];
-    for (int i = 0; i < j; ++i) H[i * m + (j - 1)] += hl * s[i];
-    H[j * m + (j - 1)] = hl * r;
+    if (i < j) H[i * m + (j - 1)] += hl * si;
+    __syncwarp();
+    if (i == j) H[j * m + (j - 1)] = hl * r;
   }
-  double sz = 0.0;
-  for (int i = 0; i <= j; ++i) {
-    double ci = 0.0;
-    for (int k = (i > 0 ? i - 1 : 0); k < j; ++k) ci += H[i * m + k] * s[k];  // (upper Hessenberg)
-    c[i] = ci;
-    if (i < j) sz += s[i] * zb[i];
-  }
-  for (int i = 0; i < j; ++i) h[i] = (zb[i] - c[i]) / r;
-  h[j] = ((zb[j] - sz) / r - c[j]) / r;
+  __syncwarp();
+  double ci = 0.0;
+  if (i <= j)
+    for (int k = (i > 0 ? i - 1 : 0); k < j; ++k) ci += H[i * m + k] * s_sh[k];  // (upper Hessenberg)
+  const double cj = __shfl_sync(0xffffffffu, ci, j);
+  const double zj = __shfl_sync(0xffffffffu, zi, j);
+  const double hj = ((zj - sz) / r - cj) / r;
+  const double dj = cj + r * hj;
+  const double hi_ = i < j ? (zi - ci) / r : hj;
   double* cAb = cA + (int64_t)b * hld;
   double* cBb = cB + (int64_t)b * hld;
-  double* hc = hcol + (int64_t)b * hld;
-  const double dj = c[j] + r * h[j];
-  for (int i = 0; i < j; ++i) {
-    const double di = c[i] + r * h[i];
-    cAb[i] = s[i] * al[i] / at;
-    cBb[i] = (di - dj * s[i] / r) * al[i];
+  if (i < j) {
+    const double di = ci + r * hi_;
+    cAb[i] = si * ali / at;
+    cBb[i] = (di - dj * si / r) * ali;
   }
-  cBb[j] = dj * at / r;
-  al[j] = at / r;
-  for (int i = 0; i <= j; ++i) {
-    hc[i] = h[i];
-    H[i * m + j] = h[i];
+  if (i <= j) {
+    hcol[(int64_t)b * hld + i] = hi_;
+    H[i * m + j] = hi_;
   }
-  rbuf[b] = r;
+  if (i == j) {
+    cBb[j] = dj * at / r;
+    al[j] = at / r;
+    rbuf[b] = r;
+  }
 }
 
 // DCGS2 cycle end (per sample): finalise the last column k-1 with the re-orthogonalisation dots of the
@@ -1052,8 +1060,8 @@ static rte_status solve_impl(const rte_problem* p, const mgnet_net* net, const f
           launch_cgs<TB>(W, V, j + 1, false, true, nullptr, wv, nullptr, W.h1, st);      // pass A
           if (reorth == 3) {  // DCGS2: coefficients, then one fused update pass (V_j corrected, V_{j+1})
             prof_begin(st, "dcgs_coef");
-            dcgs_coef_kernel<<<(B + 63) / 64, 64, 0, st>>>(B, j, m, W.h2, W.h1, hld, W.Hraw, W.alpha, m + 1, W.cA,
-                                                           W.cB, W.hcol, W.rbuf, W.active);
+            dcgs_coef_kernel<<<B, 32, 0, st>>>(B, j, m, W.h2, W.h1, hld, W.Hraw, W.alpha, m + 1, W.cA, W.cB,
+                                               W.hcol, W.rbuf, W.active);
             after_launch("dcgs_coef", st);
             launch_dcgs_update<TB>(W, V, j, wv, st);
             h2 = W.h2;
