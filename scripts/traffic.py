@@ -1,13 +1,16 @@
 """Per-launch DRAM traffic of the Arnoldi kernels over the timed bench steps -> profiles/traffic.json
 (bench.py reports it as roofline.traffic for the dominant class).
 
-  ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:cgs_kernel \
-      --csv python bench.py --steps 30 --warmup 3 --no-cpu-baseline > gpurun_out/cgs_traffic.csv
+  ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+      -k regex:"cgs_kernel|dcgs_update_kernel" --csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline \
+      > gpurun_out/cgs_traffic.csv
   python scripts/traffic.py gpurun_out/cgs_traffic.csv 30 > profiles/traffic.json
 
 Template arguments of cgs_kernel<T, NV, UPDATE, DOTS> name the timing class (csrc/krylov.cu):
-UPDATE && DOTS = cgs_update_dots, DOTS only = cgs_dots, UPDATE only = cgs_update.  The last
-`steps` launches of each class are the timed region's (one per GMRES step)."""
+UPDATE && DOTS = cgs_update_dots, DOTS only = cgs_dots, UPDATE only = cgs_update;
+dcgs_update_kernel<T, NV> is dcgs_update.  The last `steps` launches of each class (one per GMRES
+step: a whole restart cycle = 30) are averaged, so the figure is per launch over every j of a cycle,
+the same average the bench's roofline takes."""
 import collections
 import csv
 import io
@@ -28,11 +31,14 @@ for r in rows:
 scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 classes = collections.defaultdict(list)
 for v in per.values():
-    m = re.search(r"cgs_kernel<[^,]+,\s*\d+,\s*(\d+),\s*(\d+)>", v["name"])
-    if not m:
-        continue
-    upd, dots = int(m.group(1)), int(m.group(2))
-    cls = "cgs_update_dots" if upd and dots else ("cgs_dots" if dots else "cgs_update")
+    if "dcgs_update_kernel" in v["name"]:
+        cls = "dcgs_update"
+    else:
+        m = re.search(r"cgs_kernel<[^,]+,\s*\d+,\s*(\d+),\s*(\d+)>", v["name"])
+        if not m:
+            continue
+        upd, dots = int(m.group(1)), int(m.group(2))
+        cls = "cgs_update_dots" if upd and dots else ("cgs_dots" if dots else "cgs_update")
     b = v.get("dram__bytes_read.sum", 0) * scale[unit["dram__bytes_read.sum"]] + \
         v.get("dram__bytes_write.sum", 0) * scale[unit["dram__bytes_write.sum"]]
     classes[cls].append(b)
