@@ -116,6 +116,34 @@ rte_status rte_tfps_info(const rte_problem* p, int* nmat, int* Md, double* xi, d
 rte_status rte_tfps_reconstruct(const rte_problem* p, const float* alpha_dev, float* psi_dev, void* stream);
 rte_status rte_tfps_reconstruct_f64(const rte_problem* p, const double* alpha_dev, double* psi_dev, void* stream);
 
+/* rte_setup_atfps -- the ATFPS compressed system (NEXT-3b, eq:2DAdaptiveTFPS_linear_sys;
+ * readings R40-R42 in DESIGN.md §3): the TFPS problem of rte_setup_tfps (same arguments, same checks)
+ * compressed with the tolerance delta in (0, 1).  A mode k of a cell is kept iff
+ * exp(-1/2 |xi_k| sigma_t h) > delta (eq:def_V_delta).  At every interface the kept centred eigenvectors
+ * of both cells are orthonormalised (QR; each eta signed with its largest entry +1 and scaled to
+ * ||eta||_inf = 1), the dropped ones follow, and P = [eta_kept | l_dropped]^-1 gives the projections;
+ * the row of a kept mode is its P-row applied to the jump of the kept-mode traces at its interface
+ * midpoint (eq:2DAdaptiveTFPS_continuity_cond), or to the incoming trace on a boundary face
+ * (eq:2DAdaptiveTFPS_boundary_cond).  Vectors use the padded layout [batch][N][N][2 Md]: the row of a kept
+ * mode sits at its own slot, dropped slots carry the identity row (b = 0 there), so the system is square
+ * and its solution is 0 on dropped slots; rte_rhs / rte_apply / rte_apply_f64 / gmres_solve work on it as
+ * on a TFPS problem.  Errors: RTE_EINVAL (delta, as rte_setup_tfps, linearly dependent kept modes at an
+ * interface). */
+rte_status rte_setup_atfps(const rte_grid* grid, const rte_ordinates* ord,
+                           const float* sigma_T, const float* sigma_a, const float* q,
+                           const float* eps, const float* g, const float* inflow, double delta,
+                           rte_problem** out);
+/* delta, the compressed dimension (kept unknowns over all cells) and (host, may be NULL) the kept mask
+ * [nmat][2 Md] of an ATFPS problem. */
+rte_status rte_atfps_info(const rte_problem* p, double* delta, int64_t* dim, uint8_t* sel);
+/* Layer reconstruction (eq:2DAdaptive_TFPS_layer1/2): from the compressed solution alpha_dev (padded),
+ * fills the dropped coefficients from the projected jumps of the smooth solution into full_dev (may be
+ * NULL: problem scratch) and writes psi_delta at the cell centres to psi_dev [batch][N][N][Md]. */
+rte_status rte_atfps_reconstruct(const rte_problem* p, const float* alpha_dev, float* psi_dev, float* full_dev,
+                                 void* stream);
+rte_status rte_atfps_reconstruct_f64(const rte_problem* p, const double* alpha_dev, double* psi_dev,
+                                     double* full_dev, void* stream);
+
 /* Sizes of a problem: batch, N, M and n = batch*N*N*M. Any pointer may be NULL. */
 rte_status rte_problem_info(const rte_problem* p, int* batch, int* N, int* M, int64_t* n);
 

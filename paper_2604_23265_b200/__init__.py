@@ -15,7 +15,8 @@ import numpy as np
 from . import _lib
 from ._lib import RTE_ENUMERIC, RTE_OK, RteError, check, gmres_opts, gmres_report, lib
 
-__all__ = ["Problem", "MgNet", "rte_setup", "rte_setup_tfps", "rte_tfps_info", "rte_tfps_modes", "rte_tfps_reconstruct",
+__all__ = ["Problem", "MgNet", "rte_setup", "rte_setup_tfps", "rte_setup_atfps", "rte_atfps_info",
+           "rte_atfps_reconstruct", "rte_atfps_reconstruct_f64", "rte_tfps_info", "rte_tfps_modes", "rte_tfps_reconstruct",
            "rte_tfps_reconstruct_f64", "rte_rhs", "rte_apply", "rte_apply_f64", "rte_blockjacobi_apply", "mgnet_create",
            "mgnet_vcycle", "mgnet_vcycle_f64", "mgnet_coeffnet", "mgnet_coeffnet_weight_count", "mgnet_modulation", "gmres_prepare", "gmres_solve", "gmres_solve_host", "rte_quadrature", "rte_hg_matrix", "rte_launch_count", "rte_timing_enable", "rte_timing_filter", "rte_timing_reset",
            "rte_timing_get", "RteError", "LIB_PATH"]
@@ -93,7 +94,7 @@ class Problem:
 
 def rte_setup(N: int, sigma_T, sigma_a, q, eps, g, inflow=None, *, n_polar: int = 0, n_azim: int = 0,
               ordinates: Optional[Sequence[np.ndarray]] = None, batch: Optional[int] = None,
-              _fn: str = "rte_setup") -> Problem:
+              _fn: str = "rte_setup", _extra: tuple = ()) -> Problem:
     """rte_setup(grid, ordinates, sigma_T, sigma_a, q, eps, g, inflow) -> Problem (host inputs)."""
     sT, sA, qq, ee = (_f32(a) for a in (sigma_T, sigma_a, q, eps))
     B = batch if batch is not None else (sT.shape[0] if sT.ndim == 3 else 1)
@@ -109,7 +110,7 @@ def rte_setup(N: int, sigma_T, sigma_a, q, eps, g, inflow=None, *, n_polar: int 
     infa = _f32(inflow) if inflow is not None else None
     h = C.c_void_p()
     check(_fn, getattr(lib, _fn)(C.byref(grid), C.byref(ordn), _fptr(sT), _fptr(sA), _fptr(qq), _fptr(ee),
-                                 _fptr(gg), _fptr(infa) if infa is not None else None, C.byref(h)))
+                                 _fptr(gg), _fptr(infa) if infa is not None else None, *_extra, C.byref(h)))
     del keep, inf
     return Problem(h)
 
@@ -118,6 +119,34 @@ def rte_setup_tfps(N: int, sigma_T, sigma_a, q, eps, g, inflow=None, **kw) -> Pr
     """rte_setup_tfps: the TFPS alpha-space system of the same problem (NEXT-3, include/rte.h); the
     Problem's vectors hold alpha [batch][N][N][2 Md] (Problem.M = 2 Md)."""
     return rte_setup(N, sigma_T, sigma_a, q, eps, g, inflow, _fn="rte_setup_tfps", **kw)
+
+
+def rte_setup_atfps(N: int, sigma_T, sigma_a, q, eps, g, inflow=None, *, delta: float, **kw) -> Problem:
+    """rte_setup_atfps: the ATFPS compressed system (NEXT-3b, include/rte.h) on the padded [B][N][N][2 Md]
+    layout."""
+    return rte_setup(N, sigma_T, sigma_a, q, eps, g, inflow, _fn="rte_setup_atfps", _extra=(C.c_double(delta),), **kw)
+
+
+def rte_atfps_info(p: Problem):
+    """(delta, compressed dimension, kept mask [nmat][2 Md] as bool)."""
+    d, n = C.c_double(), C.c_int64()
+    check("rte_atfps_info", lib.rte_atfps_info(p.handle, C.byref(d), C.byref(n), None))
+    nm = rte_tfps_info(p)[0].shape[0]
+    sel = np.zeros(nm * p.M, np.uint8)
+    check("rte_atfps_info", lib.rte_atfps_info(p.handle, None, None, sel.ctypes.data_as(C.POINTER(C.c_uint8))))
+    return d.value, n.value, sel.reshape(nm, p.M).astype(bool)
+
+
+def rte_atfps_reconstruct(p: Problem, alpha, psi, full=None, stream=None) -> None:
+    check("rte_atfps_reconstruct", lib.rte_atfps_reconstruct(p.handle, _dev(alpha, "f32"), _dev(psi, "f32"),
+                                                             _dev(full, "f32") if full is not None else None,
+                                                             C.c_void_p(_stream(stream))))
+
+
+def rte_atfps_reconstruct_f64(p: Problem, alpha, psi, full=None, stream=None) -> None:
+    check("rte_atfps_reconstruct_f64", lib.rte_atfps_reconstruct_f64(
+        p.handle, _dev(alpha, "f64"), _dev(psi, "f64"), _dev(full, "f64") if full is not None else None,
+        C.c_void_p(_stream(stream))))
 
 
 def rte_tfps_modes(c, s, S, gamma: float):

@@ -54,6 +54,11 @@ SIGS = {
     "rte_tfps_info": (C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_double),
                                 C.POINTER(C.c_double)]),
     "rte_tfps_reconstruct": (C.c_int, [_vp, _vp, _vp, _vp]),
+    "rte_setup_atfps": (C.c_int, [C.POINTER(rte_grid), C.POINTER(rte_ordinates), _fp, _fp, _fp, _fp, _fp, _fp,
+                                  C.c_double, C.POINTER(_vp)]),
+    "rte_atfps_info": (C.c_int, [_vp, C.POINTER(C.c_double), C.POINTER(C.c_int64), C.POINTER(C.c_uint8)]),
+    "rte_atfps_reconstruct": (C.c_int, [_vp, _vp, _vp, _vp, _vp]),
+    "rte_atfps_reconstruct_f64": (C.c_int, [_vp, _vp, _vp, _vp, _vp]),
     "rte_tfps_reconstruct_f64": (C.c_int, [_vp, _vp, _vp, _vp]),
     "rte_destroy": (None, [_vp]),
     "rte_problem_info": (C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int),

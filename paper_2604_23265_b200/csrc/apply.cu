@@ -385,6 +385,10 @@ void launch_rhs(const rte_problem* p, float* b, cudaStream_t st) {
     launch_tfps_rhs(p, b, st);
     return;
   }
+  if (p->kind == 2) {
+    launch_atfps<float>(p, 1, nullptr, b, nullptr, 0, nullptr, st);
+    return;
+  }
   int64_t n = p->n;
   int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 16);
   prof_begin(st, "rhs");
@@ -396,6 +400,10 @@ void launch_apply_f32(const rte_problem* p, const float* x, float* y, const doub
                       cudaStream_t st) {
   if (p->kind == 1) {
     launch_tfps_apply<float>(p, x, y, alpha, alpha_stride, nullptr, st);
+    return;
+  }
+  if (p->kind == 2) {
+    launch_atfps<float>(p, 0, x, y, alpha, alpha_stride, nullptr, st);
     return;
   }
   if (p->tc_apply) {
@@ -410,6 +418,10 @@ void launch_apply_f32(const rte_problem* p, const float* x, float* y, const doub
 void launch_apply_f64(const rte_problem* p, const double* x, double* y, const float* b, cudaStream_t st) {
   if (p->kind == 1) {
     launch_tfps_apply<double>(p, x, y, nullptr, 0, b, st);
+    return;
+  }
+  if (p->kind == 2) {
+    launch_atfps<double>(p, 0, x, y, nullptr, 0, b, st);
     return;
   }
   prof_begin(st, "apply_f64_simt");

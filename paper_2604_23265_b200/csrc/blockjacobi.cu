@@ -104,7 +104,7 @@ __global__ void bj_apply_kernel(const T* __restrict__ Binv, const T* __restrict_
 
 void bj_prepare(const rte_problem* p) {
   if (p->bj64) return;
-  RTE_REQUIRE(p->kind == 0, "block Jacobi: defined for the psi-space DO operator (not the TFPS alpha-space system)");
+  RTE_REQUIRE(p->kind == 0, "block Jacobi: defined for the psi-space DO operator (not the (A)TFPS alpha-space systems)");
   const size_t blk = (size_t)p->M * p->M;
   const double gib = (double)p->ncell * blk * 12.0 / (1 << 30);
   RTE_REQUIRE(gib <= 24.0, "block Jacobi: the inverse cell blocks would need " + std::to_string(gib) +

@@ -129,6 +129,16 @@ struct rte_problem {
   double* tf_chis64 = nullptr;
   std::vector<double> tf_xi;   // host copies: [nmat][2Md], [nmat][Md][2Md]
   std::vector<double> tf_Lh;
+  // ---- ATFPS compressed system (kind 2, rte_setup_atfps; tfps.cu).  Padded [cells][2Md] layout.
+  double at_delta = 0.0;
+  int64_t at_dim = 0;           // selected unknowns (the compressed dimension)
+  uint8_t* at_sel = nullptr;    // [nmat][2Md] mode kept (eq:def_V_delta)
+  float* at_P32 = nullptr;      // interface projections: interior [2][nmat][nmat][Md][Md], then
+  double* at_P64 = nullptr;     //   boundary [4][nmat][Md/2][Md/2]
+  int* at_row = nullptr;        // P-row of each (side, mode): interior [2][nmat][nmat][2][2Md], boundary [4][nmat][2][2Md]
+  int* at_dirs = nullptr;       // [4][Md/2] incoming directions of the faces L, R, B, T
+  float* at_tmp32 = nullptr;    // [n] full coefficients (layer reconstruction scratch)
+  double* at_tmp64 = nullptr;
 };
 
 // ---- kernel launchers (apply.cu) --------------------------------------------
@@ -169,4 +179,9 @@ void launch_tfps_reconstruct(const rte_problem* p, const T* alpha, T* psi, cudaS
 void tfps_local_modes(const double* S, const std::vector<double>& c, const std::vector<double>& s, double gamma,
                       std::vector<double>& xi, std::vector<double>& L);
 void tfps_face_factors(const std::vector<double>& xi, int M, double sigma_t, double h, double* fac);
+void atfps_interface(const std::vector<double>& Lh, const std::vector<uint8_t>& sel, int M, int a, int b, int fm,
+                     int fp, const std::vector<int>& dirs, std::vector<double>& P, int* rowmap);
+template <typename T>
+void launch_atfps(const rte_problem* p, int mode, const T* x, T* y, const double* alpha_dev, int alpha_stride,
+                  const float* b, cudaStream_t st);  // mode 0: A x (y = b - A x if b), 1: rhs (T = float), 2: layer
 }  // namespace rte

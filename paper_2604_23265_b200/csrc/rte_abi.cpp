@@ -8,6 +8,7 @@
 #include <atomic>
 #include <cstdio>
 #include <map>
+#include <numeric>
 #include <string>
 #include <tuple>
 #include <vector>
@@ -308,7 +309,8 @@ static void free_problem(rte_problem* p) {
   void* ptrs[] = {p->sig_t, p->sig_s, p->sig_d, p->sig_d64, p->f, p->sig_t64, p->sig_s64, p->S32, p->St32, p->St64, p->S_hi,
                   p->S_lo, p->ax, p->ay, p->ax64, p->ay64, p->sgx, p->sgy, p->inflow, p->scratch64,
                   p->bj64, p->bj32, p->tf_mat, p->tf_L32, p->tf_L64, p->tf_fac32, p->tf_fac64, p->tf_chis32,
-                  p->tf_chis64};
+                  p->tf_chis64, p->at_sel, p->at_P32, p->at_P64, p->at_row, p->at_dirs, p->at_tmp32,
+                  p->at_tmp64};
   for (void* q : ptrs) dfree(q);
   free_tc_state(p);
   free_gmres_work(p);
@@ -519,6 +521,114 @@ rte_status rte_setup_tfps(const rte_grid* grid, const rte_ordinates* ord, const 
   }
 }
 
+rte_status rte_setup_atfps(const rte_grid* grid, const rte_ordinates* ord, const float* sigma_T,
+                           const float* sigma_a, const float* q, const float* eps, const float* g, const float* inflow,
+                           double delta, rte_problem** out) {
+  rte_problem* p = nullptr;
+  try {
+    RTE_REQUIRE(out, "rte_setup_atfps: NULL argument");
+    *out = nullptr;
+    RTE_REQUIRE(delta > 0.0 && delta < 1.0, "rte_setup_atfps: delta must lie in (0, 1)");
+    const rte_status st0 = rte_setup_tfps(grid, ord, sigma_T, sigma_a, q, eps, g, inflow, &p);
+    if (st0 != RTE_OK) return st0;
+    const int Md = p->Md, K = 2 * Md, H = Md / 2, nmat = p->nmat;
+    RTE_REQUIRE(Md % 2 == 0, "rte_setup_atfps: the number of directions must be even");
+    const double h = 1.0 / p->N;
+    // selection (eq:def_V_delta): exp(-1/2 |xi| sigma_t h) > delta
+    std::vector<uint8_t> sel((size_t)nmat * K);
+    std::vector<double> st_of(nmat, 0.0);
+    {
+      std::vector<int> mat(p->ncell);
+      RTE_CHECK_CUDA(cudaMemcpy(mat.data(), p->tf_mat, sizeof(int) * p->ncell, cudaMemcpyDeviceToHost));
+      for (int64_t k = 0; k < p->ncell; ++k) st_of[mat[k]] = (double)sigma_T[k] / (double)eps[k];
+      std::vector<int64_t> count(nmat, 0);
+      for (int64_t k = 0; k < p->ncell; ++k) ++count[mat[k]];
+      p->at_dim = 0;
+      for (int m = 0; m < nmat; ++m)
+        for (int k = 0; k < K; ++k) {
+          sel[(size_t)m * K + k] = exp(-0.5 * fabs(p->tf_xi[(size_t)m * K + k]) * st_of[m] * h) > delta ? 1 : 0;
+          p->at_dim += sel[(size_t)m * K + k] ? count[m] : 0;
+        }
+    }
+    // interface bases and projections (R40): interior [2 orient][a][b], boundary [4 faces][a]
+    const size_t nint = (size_t)2 * nmat * nmat, nbnd = (size_t)4 * nmat;
+    std::vector<double> P(nint * Md * Md + nbnd * H * H, 0.0);
+    std::vector<int> row((nint + nbnd) * 2 * K, -1);
+    std::vector<int> alld(Md), dirs[4];
+    std::iota(alld.begin(), alld.end(), 0);
+    for (int m = 0; m < Md; ++m) {
+      (p->c[m] > 0 ? dirs[0] : dirs[1]).push_back(m);  // incoming at x = 0 (L) / x = 1 (R)
+      (p->s[m] > 0 ? dirs[2] : dirs[3]).push_back(m);  // incoming at y = 0 (B) / y = 1 (T)
+    }
+    for (int f = 0; f < 4; ++f) RTE_REQUIRE((int)dirs[f].size() == H, "rte_setup_atfps: unbalanced ordinate set");
+    std::vector<double> Pt;
+    for (int o = 0; o < 2; ++o)
+      for (int a = 0; a < nmat; ++a)
+        for (int b = 0; b < nmat; ++b) {
+          const size_t t = ((size_t)o * nmat + a) * nmat + b;
+          // C- contributes its R- (T-) centred modes, C+ its L- (B-) centred modes
+          atfps_interface(p->tf_Lh, sel, Md, a, b, o == 0 ? 1 : 3, o == 0 ? 0 : 2, alld, Pt, row.data() + t * 2 * K);
+          std::copy(Pt.begin(), Pt.end(), P.begin() + t * Md * Md);
+        }
+    for (int f = 0; f < 4; ++f)
+      for (int a = 0; a < nmat; ++a) {
+        const size_t t = (size_t)f * nmat + a;
+        atfps_interface(p->tf_Lh, sel, Md, a, a, f, -1, dirs[f], Pt, row.data() + (nint + t) * 2 * K);
+        std::copy(Pt.begin(), Pt.end(), P.begin() + nint * Md * Md + t * H * H);
+      }
+    std::vector<float> P32(P.begin(), P.end());
+    std::vector<int> dflat;
+    for (int f = 0; f < 4; ++f) dflat.insert(dflat.end(), dirs[f].begin(), dirs[f].end());
+    p->kind = 2;
+    p->at_delta = delta;
+    p->at_sel = dalloc<uint8_t>(sel.size()); upload(p->at_sel, sel.data(), sel.size());
+    p->at_P64 = dalloc<double>(P.size()); upload(p->at_P64, P.data(), P.size());
+    p->at_P32 = dalloc<float>(P.size()); upload(p->at_P32, P32.data(), P.size());
+    p->at_row = dalloc<int>(row.size()); upload(p->at_row, row.data(), row.size());
+    p->at_dirs = dalloc<int>(dflat.size()); upload(p->at_dirs, dflat.data(), dflat.size());
+    p->at_tmp32 = dalloc<float>(p->n);
+    p->at_tmp64 = dalloc<double>(p->n);
+    *out = p;
+    return RTE_OK;
+  } catch (const Fail& f) {
+    free_problem(p);
+    return f.st;
+  } catch (const std::exception& e) {
+    free_problem(p);
+    set_error(std::string("internal: ") + e.what());
+    return RTE_EINTERNAL;
+  }
+}
+
+rte_status rte_atfps_info(const rte_problem* p, double* delta, int64_t* dim, uint8_t* sel) {
+  RTE_API_BEGIN
+  RTE_REQUIRE(p && p->kind == 2, "rte_atfps_info: not an ATFPS problem");
+  if (delta) *delta = p->at_delta;
+  if (dim) *dim = p->at_dim;
+  if (sel) RTE_CHECK_CUDA(cudaMemcpy(sel, p->at_sel, (size_t)p->nmat * 2 * p->Md, cudaMemcpyDeviceToHost));
+  RTE_API_END
+}
+
+rte_status rte_atfps_reconstruct(const rte_problem* p, const float* alpha_dev, float* psi_dev, float* full_dev,
+                                 void* stream) {
+  RTE_API_BEGIN
+  RTE_REQUIRE(p && alpha_dev && psi_dev && p->kind == 2, "rte_atfps_reconstruct: NULL argument or not ATFPS");
+  float* full = full_dev ? full_dev : p->at_tmp32;
+  launch_atfps<float>(p, 2, alpha_dev, full, nullptr, 0, nullptr, as_stream(stream));
+  launch_tfps_reconstruct<float>(p, full, psi_dev, as_stream(stream));
+  RTE_API_END
+}
+
+rte_status rte_atfps_reconstruct_f64(const rte_problem* p, const double* alpha_dev, double* psi_dev, double* full_dev,
+                                     void* stream) {
+  RTE_API_BEGIN
+  RTE_REQUIRE(p && alpha_dev && psi_dev && p->kind == 2, "rte_atfps_reconstruct_f64: NULL argument or not ATFPS");
+  double* full = full_dev ? full_dev : p->at_tmp64;
+  launch_atfps<double>(p, 2, alpha_dev, full, nullptr, 0, nullptr, as_stream(stream));
+  launch_tfps_reconstruct<double>(p, full, psi_dev, as_stream(stream));
+  RTE_API_END
+}
+
 rte_status rte_tfps_modes(int M, const double* c, const double* s, const double* S, double gamma, double* xi,
                           double* L) {
   RTE_API_BEGIN
@@ -531,7 +641,7 @@ rte_status rte_tfps_modes(int M, const double* c, const double* s, const double*
 }
 
 rte_status rte_tfps_info(const rte_problem* p, int* nmat, int* Md, double* xi, double* L) {
-  if (!p || p->kind != 1) { set_error("rte_tfps_info: not a TFPS problem"); return RTE_EINVAL; }
+  if (!p || (p->kind != 1 && p->kind != 2)) { set_error("rte_tfps_info: not a TFPS problem"); return RTE_EINVAL; }
   if (nmat) *nmat = p->nmat;
   if (Md) *Md = p->Md;
   if (xi) memcpy(xi, p->tf_xi.data(), p->tf_xi.size() * sizeof(double));
@@ -541,14 +651,14 @@ rte_status rte_tfps_info(const rte_problem* p, int* nmat, int* Md, double* xi, d
 
 rte_status rte_tfps_reconstruct(const rte_problem* p, const float* alpha_dev, float* psi_dev, void* stream) {
   RTE_API_BEGIN
-  RTE_REQUIRE(p && alpha_dev && psi_dev && p->kind == 1, "rte_tfps_reconstruct: NULL argument or not a TFPS problem");
+  RTE_REQUIRE(p && alpha_dev && psi_dev && p->kind >= 1, "rte_tfps_reconstruct: NULL argument or not a TFPS problem");
   launch_tfps_reconstruct<float>(p, alpha_dev, psi_dev, as_stream(stream));
   RTE_API_END
 }
 
 rte_status rte_tfps_reconstruct_f64(const rte_problem* p, const double* alpha_dev, double* psi_dev, void* stream) {
   RTE_API_BEGIN
-  RTE_REQUIRE(p && alpha_dev && psi_dev && p->kind == 1, "rte_tfps_reconstruct_f64: NULL argument or not a TFPS problem");
+  RTE_REQUIRE(p && alpha_dev && psi_dev && p->kind >= 1, "rte_tfps_reconstruct_f64: NULL argument or not a TFPS problem");
   launch_tfps_reconstruct<double>(p, alpha_dev, psi_dev, as_stream(stream));
   RTE_API_END
 }

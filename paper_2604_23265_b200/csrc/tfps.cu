@@ -13,6 +13,8 @@
 // [2Md] -> [Md] with per-material matrices: a grouped GEMV per face, one warp per cell, the four
 // scaled coefficient vectors staged in shared memory, L stored k-major so a warp's loads of one k
 // row are coalesced over the output directions.
+#include <type_traits>
+
 #include "common.h"
 
 namespace rte {
@@ -137,6 +139,134 @@ __global__ void __launch_bounds__(32 * kWarps) tfps_reconstruct_kernel(int64_t c
   }
 }
 
+// ---- ATFPS compressed system (NEXT-3b, readings R40-R42) ------------------------
+// Padded layout [cells][2 Md]: the row of a selected mode k of cell C sits at slot (C, k); dropped modes
+// carry the identity row.  Mode k is centred at face k / (Md/2) in L, R, B, T.  Per cell (one warp): the
+// selected-mode traces of the cell at its 4 faces and of the 4 neighbours at the shared faces, the jump
+// vector of each face, then each selected mode's row = its P-row (interface type: the material pair, or
+// the boundary face and material) dotted with the jump of its face.
+//   MODE 0 (A x):  jumps of the selected traces, y = x on dropped slots (y = b - A x with b);
+//   MODE 1 (b):    particular-solution jumps / inflow minus the particular solution; 0 on dropped slots;
+//   MODE 2 (layer, eq:2DAdaptive_TFPS_layer1/2): the full coefficients -- selected = x, dropped = the
+//                  projected jump of the smooth solution psi_bar = sum_sel x chi + chi^s.
+template <typename T, int MODE>
+__global__ void __launch_bounds__(32 * kWarps) atfps_kernel(
+    int B, int N, int Md, int nmat, const int* __restrict__ mat, const uint8_t* __restrict__ sel,
+    const T* __restrict__ LT, const T* __restrict__ fac, const T* __restrict__ chis, const float* __restrict__ inflow,
+    const T* __restrict__ P, const int* __restrict__ row, const int* __restrict__ dirs, const T* __restrict__ x,
+    T* __restrict__ y, const double* __restrict__ alpha, int alpha_stride, const float* __restrict__ bvec) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int K = 2 * Md, H = Md / 2;
+  T* u = reinterpret_cast<T*>(smem_raw) + (size_t)warp * (8 * K + 4 * Md);  // 8 scaled coefficient vectors
+  T* v = u + 8 * K;                                                          // 4 jump vectors (L, R, B, T)
+  const int64_t cells = (int64_t)B * N * N;
+  const int64_t cell = (int64_t)blockIdx.x * kWarps + warp;
+  if (cell >= cells) return;
+  const int i = (int)(cell % N), j = (int)((cell / N) % N);
+  const int64_t base = cell - ((int64_t)j * N + i);
+  const int b = (int)(base / ((int64_t)N * N));
+  const T al = alpha ? (T)alpha[(int64_t)b * alpha_stride] : T(1);
+  const int mC = mat[cell];
+  // neighbours across L, R, B, T (-1 outside the grid)
+  const int64_t nb[4] = {i > 0 ? cell - 1 : -1, i < N - 1 ? cell + 1 : -1, j > 0 ? cell - N : -1,
+                         j < N - 1 ? cell + N : -1};
+  // traces: s = 0..3 the cell at its faces L, R, B, T; s = 4..7 the neighbour across face s-4 at the
+  // shared face (R, L, T, B of the neighbour)
+  int tm[8];
+  int64_t tc[8];
+  int tf[8];
+  const int opp[4] = {1, 0, 3, 2};
+  for (int s = 0; s < 8; ++s) {
+    tc[s] = s < 4 ? cell : nb[s - 4];
+    tf[s] = s < 4 ? s : opp[s - 4];
+    tm[s] = tc[s] >= 0 ? mat[tc[s]] : 0;
+  }
+  if (MODE != 1) {
+    for (int s = 0; s < 8; ++s) {
+      if (tc[s] < 0) continue;
+      const T* f = fac + ((size_t)tm[s] * 5 + tf[s]) * K;
+      const uint8_t* sl = sel + (size_t)tm[s] * K;
+      const T* a = x + tc[s] * K;
+      for (int k = lane; k < K; k += 32) u[s * K + k] = sl[k] ? f[k] * a[k] * al : T(0);
+    }
+    __syncwarp();
+  }
+  // the jump vector of each face (the component list of boundary faces is dirs[face])
+  for (int fa = 0; fa < 4; ++fa) {
+    const bool interior = nb[fa] >= 0;
+    const int d = interior ? Md : H;
+    const bool low = fa == 0 || fa == 2;  // L or B: the cell is C+ (the neighbour is C-)
+    for (int q = lane; q < d; q += 32) {
+      const int m = interior ? q : dirs[fa * H + q];
+      T tC = T(0), tN = T(0);
+      if (MODE != 1) {
+        const T* Lm = LT + m;
+        for (int s2 = 0; s2 < 2; ++s2) {
+          const int s = s2 == 0 ? fa : 4 + fa;
+          if (tc[s] < 0) continue;
+          const T* Lms = Lm + (size_t)tm[s] * K * Md;
+          const T* us = u + s * K;
+          T acc = T(0);
+          for (int k = 0; k < K; ++k) acc = fma(Lms[(size_t)k * Md], us[k], acc);
+          (s2 == 0 ? tC : tN) = acc;
+        }
+      }
+      T val;
+      if (interior) {
+        const T cC = chis[cell], cN = chis[nb[fa]];
+        const T tm_ = low ? tN : tC, tp_ = low ? tC : tN;         // traces of C- and C+
+        const T cm_ = low ? cN : cC, cp_ = low ? cC : cN;
+        if (MODE == 0) val = tm_ - tp_;
+        else if (MODE == 1) val = cp_ - cm_;
+        else val = low ? (tm_ + cm_) - (tp_ + cp_) : (tp_ + cp_) - (tm_ + cm_);  // P^k(other) - P^k(own)
+      } else {
+        const int pos = (fa < 2) ? j : i;
+        const T psi_in = inflow ? (T)inflow[(((int64_t)b * 4 + fa) * N + pos) * Md + m] : T(0);
+        if (MODE == 0) val = tC;
+        else if (MODE == 1) val = psi_in - chis[cell];
+        else val = psi_in - (tC + chis[cell]);
+      }
+      v[fa * Md + q] = val;
+    }
+  }
+  __syncwarp();
+  const uint8_t* slC = sel + (size_t)mC * K;
+  const size_t nint = (size_t)2 * nmat * nmat;
+  for (int k = lane; k < K; k += 32) {
+    const int fa = k / H;
+    const bool keep = slC[k] != 0;
+    T out;
+    if ((MODE == 2) == keep) {
+      out = MODE == 0 ? x[cell * K + k] * al : MODE == 1 ? T(0) : x[cell * K + k];
+    } else {
+      const bool interior = nb[fa] >= 0;
+      const T* Pr;
+      int r, d;
+      if (interior) {
+        const bool low = fa == 0 || fa == 2;
+        const int o = fa < 2 ? 0 : 1;
+        const int mm = low ? mat[nb[fa]] : mC, mp = low ? mC : mat[nb[fa]];
+        const size_t t = ((size_t)o * nmat + mm) * nmat + mp;
+        d = Md;
+        r = row[t * 2 * K + (low ? 1 : 0) * K + k];
+        Pr = P + t * Md * Md + (size_t)r * Md;
+      } else {
+        const size_t t = (size_t)fa * nmat + mC;
+        d = H;
+        r = row[(nint + t) * 2 * K + k];
+        Pr = P + nint * Md * Md + t * H * H + (size_t)r * H;
+      }
+      T acc = T(0);
+      const T* vf = v + fa * Md;
+      for (int q = 0; q < d; ++q) acc = fma(Pr[q], vf[q], acc);
+      out = acc;
+    }
+    if (MODE == 0 && bvec) out = (T)bvec[cell * K + k] - out;
+    y[cell * K + k] = out;
+  }
+}
+
 }  // namespace
 
 template <typename T>
@@ -185,5 +315,37 @@ void launch_tfps_reconstruct(const rte_problem* p, const T* alpha, T* psi, cudaS
 }
 template void launch_tfps_reconstruct<float>(const rte_problem*, const float*, float*, cudaStream_t);
 template void launch_tfps_reconstruct<double>(const rte_problem*, const double*, double*, cudaStream_t);
+
+template <typename T>
+void launch_atfps(const rte_problem* p, int mode, const T* x, T* y, const double* alpha, int alpha_stride,
+                  const float* b, cudaStream_t st) {
+  const bool f64 = sizeof(T) == 8;
+  const char* cls = mode == 1 ? "atfps_rhs" : mode == 2 ? "atfps_layer" : f64 ? "atfps_apply_f64" : "atfps_apply_f32";
+  prof_begin(st, cls);
+  const int64_t cells = p->ncell;
+  const int K = 2 * p->Md;
+  const size_t smem = sizeof(T) * kWarps * (8 * K + 4 * p->Md);
+  auto go = [&](auto mode_tag) {
+    constexpr int MODE = decltype(mode_tag)::value;
+    auto kern = atfps_kernel<T, MODE>;
+    if (smem > 48 * 1024) RTE_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<(unsigned)((cells + kWarps - 1) / kWarps), 32 * kWarps, smem, st>>>(
+        p->B, p->N, p->Md, p->nmat, p->tf_mat, p->at_sel, f64 ? (const T*)p->tf_L64 : (const T*)p->tf_L32,
+        f64 ? (const T*)p->tf_fac64 : (const T*)p->tf_fac32, f64 ? (const T*)p->tf_chis64 : (const T*)p->tf_chis32,
+        p->inflow, f64 ? (const T*)p->at_P64 : (const T*)p->at_P32, p->at_row, p->at_dirs, x, y, alpha,
+        alpha_stride, b);
+  };
+  if (mode == 0) go(std::integral_constant<int, 0>{});
+  else if (mode == 1) go(std::integral_constant<int, 1>{});
+  else go(std::integral_constant<int, 2>{});
+  // 8 trace contractions [2Md] -> [Md] and 2Md projections of length Md per cell
+  const double Kd = 2.0 * p->Md;
+  after_launch(cls, st, (double)cells * (8.0 * 2.0 * Kd * p->Md + 2.0 * Kd * p->Md),
+               (double)cells * (Kd * sizeof(T) * 2 + (b ? Kd * 4 : 0) + 4), f64 ? 3 : 2);
+}
+template void launch_atfps<float>(const rte_problem*, int, const float*, float*, const double*, int, const float*,
+                                  cudaStream_t);
+template void launch_atfps<double>(const rte_problem*, int, const double*, double*, const double*, int,
+                                   const float*, cudaStream_t);
 
 }  // namespace rte

@@ -182,4 +182,110 @@ void tfps_face_factors(const std::vector<double>& xi, int M, double sigma_t, dou
   }
 }
 
+// ---- ATFPS interface bases (NEXT-3b, readings R40-R42) ------------------------
+namespace {
+
+// Orthonormalise the columns of S (d x n, row-major) in order by Gram-Schmidt applied twice (CGS2, fp64;
+// the same Q as a QR with positive diagonal); then each column gets its largest-|.| entry +1 (lowest
+// index on ties within 1e-9) and ||.||_inf = 1 (R40).
+void qr_eta(std::vector<double>& S, int d, int n) {
+  for (int j = 0; j < n; ++j) {
+    for (int pass = 0; pass < 2; ++pass)
+      for (int q = 0; q < j; ++q) {
+        double dot = 0.0, nq = 0.0;
+        for (int i = 0; i < d; ++i) {
+          dot += S[(size_t)i * n + q] * S[(size_t)i * n + j];
+          nq += S[(size_t)i * n + q] * S[(size_t)i * n + q];
+        }
+        const double c = dot / nq;
+        for (int i = 0; i < d; ++i) S[(size_t)i * n + j] -= c * S[(size_t)i * n + q];
+      }
+    double nr = 0.0;
+    for (int i = 0; i < d; ++i) nr += S[(size_t)i * n + j] * S[(size_t)i * n + j];
+    RTE_REQUIRE(nr > 0.0, "rte_setup_atfps: linearly dependent selected modes at an interface");
+  }
+  for (int j = 0; j < n; ++j) {  // (the scaling leaves the span and the orthogonality intact)
+    double amax = 0.0;
+    for (int i = 0; i < d; ++i) amax = std::max(amax, fabs(S[(size_t)i * n + j]));
+    int big = 0;
+    while (fabs(S[(size_t)big * n + j]) < amax * (1.0 - 1e-9)) ++big;
+    const double sc = S[(size_t)big * n + j];
+    for (int i = 0; i < d; ++i) S[(size_t)i * n + j] /= sc;
+  }
+}
+
+// In-place inverse of the d x d row-major A by Gauss-Jordan with partial pivoting (fp64).
+void invert(std::vector<double>& A, int d) {
+  std::vector<double> I((size_t)d * d, 0.0);
+  for (int i = 0; i < d; ++i) I[(size_t)i * d + i] = 1.0;
+  for (int c = 0; c < d; ++c) {
+    int piv = c;
+    for (int r = c + 1; r < d; ++r)
+      if (fabs(A[(size_t)r * d + c]) > fabs(A[(size_t)piv * d + c])) piv = r;
+    RTE_REQUIRE(fabs(A[(size_t)piv * d + c]) > 0.0, "rte_setup_atfps: singular interface basis");
+    if (piv != c)
+      for (int k = 0; k < d; ++k) {
+        std::swap(A[(size_t)c * d + k], A[(size_t)piv * d + k]);
+        std::swap(I[(size_t)c * d + k], I[(size_t)piv * d + k]);
+      }
+    const double inv = 1.0 / A[(size_t)c * d + c];
+    for (int k = 0; k < d; ++k) {
+      A[(size_t)c * d + k] *= inv;
+      I[(size_t)c * d + k] *= inv;
+    }
+    for (int r = 0; r < d; ++r) {
+      if (r == c) continue;
+      const double f = A[(size_t)r * d + c];
+      if (f == 0.0) continue;
+      for (int k = 0; k < d; ++k) {
+        A[(size_t)r * d + k] -= f * A[(size_t)c * d + k];
+        I[(size_t)r * d + k] -= f * I[(size_t)c * d + k];
+      }
+    }
+  }
+  A.swap(I);
+}
+
+}  // namespace
+
+// One interface type: the centred modes of C- (`fm`, material a) and of C+ (`fp`, material b; fp < 0 for a
+// boundary face of material a), restricted to the direction list `dirs`.  Modes are ordered
+// [x-modes ascending | y-modes ascending], so the face a mode is centred at is k / (M/2) in L, R, B, T.
+// Outputs P (d x d, row-major) and rowmap[2][2M] (the P-row of each centred mode of each side, -1 else).
+void atfps_interface(const std::vector<double>& Lh /*[nmat][M][2M]*/, const std::vector<uint8_t>& sel /*[nmat][2M]*/,
+                     int M, int a, int b, int fm, int fp, const std::vector<int>& dirs, std::vector<double>& P,
+                     int* rowmap) {
+  const int K = 2 * M, d = (int)dirs.size();
+  std::vector<std::pair<int, int>> cols_s, cols_u;  // (side, k)
+  for (int side = 0; side < 2; ++side) {
+    const int f = side == 0 ? fm : fp;
+    if (f < 0) continue;
+    const int mt = side == 0 ? a : b;
+    for (int k = f * (M / 2); k < (f + 1) * (M / 2); ++k)
+      (sel[(size_t)mt * K + k] ? cols_s : cols_u).push_back({side, k});
+  }
+  const int ns = (int)cols_s.size(), n = ns + (int)cols_u.size();
+  RTE_REQUIRE(n == d, "rte_setup_atfps: interface basis is not square");
+  auto vecv = [&](int side, int k, int i) {
+    const int mt = side == 0 ? a : b;
+    return Lh[((size_t)mt * M + dirs[i]) * K + k];
+  };
+  std::vector<double> Sq((size_t)d * std::max(ns, 1), 0.0);
+  for (int j = 0; j < ns; ++j)
+    for (int i = 0; i < d; ++i) Sq[(size_t)i * ns + j] = vecv(cols_s[j].first, cols_s[j].second, i);
+  if (ns > 0) qr_eta(Sq, d, ns);
+  std::vector<double> E((size_t)d * d);
+  for (int i = 0; i < d; ++i) {
+    for (int j = 0; j < ns; ++j) E[(size_t)i * d + j] = Sq[(size_t)i * ns + j];
+    for (int j = ns; j < d; ++j) E[(size_t)i * d + j] = vecv(cols_u[j - ns].first, cols_u[j - ns].second, i);
+  }
+  invert(E, d);
+  P.swap(E);
+  for (int t = 0; t < 2 * K; ++t) rowmap[t] = -1;
+  for (int j = 0; j < n; ++j) {
+    const auto& c = j < ns ? cols_s[j] : cols_u[j - ns];
+    rowmap[c.first * K + c.second] = j;
+  }
+}
+
 }  // namespace rte
