@@ -22,6 +22,7 @@ import workloads as W  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--cycles", type=int, default=3)
 ap.add_argument("--oracle", action="store_true", help="also time one oracle apply (host cores)")
+ap.add_argument("--delta", type=float, default=1e-4, help="ATFPS tolerance of the compressed-system runs")
 a = ap.parse_args()
 cfg = W.config(2)
 media = W.make_media(cfg)
@@ -79,6 +80,31 @@ for name, nt in (("none", None), ("mgnet", net)):
     ms = e0.elapsed_time(e1)
     out[f"gmres_{name}"] = {"iter_per_s": K / (ms * 1e-3), "inner_iterations": K, "ms": ms,
                             "relres_true_after": rep[0]["relres_true"]}
+# ATFPS (NEXT-3b): the compressed system of the same problem at delta
+pa = P.rte_setup_atfps(cfg.N, media.sigma_T, media.sigma_a, media.q, media.eps, media.g, media.inflow,
+                       delta=a.delta, n_polar=cfg.n_polar, n_azim=cfg.n_azim)
+_, dim, _ = P.rte_atfps_info(pa)
+out["atfps"] = {"delta": a.delta, "dimension": dim, "padded": pa.n, "compression": dim / pa.n,
+                "apply_f32_per_s": rate(lambda: P.rte_apply(pa, x, y))}
+ba = torch.empty(pa.shape, dtype=torch.float32, device="cuda")
+P.rte_rhs(pa, ba)
+neta = P.mgnet_create(pa, cfg.L, cfg.C0, cfg.nu, W.make_weights(cm))
+for name, nt in (("none", None), ("mgnet", neta)):
+    K = a.cycles * 30
+    xs = torch.zeros(pa.shape, dtype=torch.float64, device="cuda")
+    P.gmres_prepare(pa, nt, restart=30, precond=1 if nt else 0)
+    P.gmres_solve(pa, nt, ba, xs, restart=30, maxit=30, rtol=1e-300, x0_zero=True, history=False,
+                  precond=1 if nt else 0)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    rep = P.gmres_solve(pa, nt, ba, xs, restart=30, maxit=K, rtol=1e-300, x0_zero=True, history=False,
+                        precond=1 if nt else 0)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    out["atfps"][f"gmres_{name}"] = {"iter_per_s": K / (ms * 1e-3), "inner_iterations": K, "ms": ms,
+                                     "relres_true_after": rep[0]["relres_true"]}
 if a.oracle:
     import numpy as np
     from oracle import tfps as T
