@@ -479,6 +479,76 @@ def run_ours(args, cfg):
         dist.destroy_process_group()
 
 
+def run_time_to_tol(args, cfg):
+    """Time-to-tolerance (north star: "GMRES iterations/s, time-to-tolerance"): the full MgNet-
+    preconditioned GMRES(30) solve from x0 = 0 to the config's rtol (configs 1, 2 converge; 3-5 run their
+    fixed budgets and report the residual reached), on the device (CUDA events, best of 3 after a warm-up
+    solve) and end to end through gmres_solve_host (host wall clock), next to the fp64 oracle's solve on
+    the host cores (configs 1-2 only: the cpu_baseline leg).  One JSON line."""
+    import torch
+    import paper_2604_23265_b200 as P
+    import workloads as W
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
+    media = W.make_media(cfg)
+    weights = W.make_weights(cfg)
+    p = P.rte_setup(cfg.N, media.sigma_T, media.sigma_a, media.q, media.eps, media.g, media.inflow,
+                    n_polar=cfg.n_polar, n_azim=cfg.n_azim)
+    net = P.mgnet_create(p, cfg.L, cfg.C0, cfg.nu, weights)
+    b = torch.empty(p.shape, dtype=torch.float32, device="cuda")
+    P.rte_rhs(p, b)
+    x = torch.zeros(p.shape, dtype=torch.float64, device="cuda")
+    P.gmres_prepare(p, net, restart=cfg.restart, reorth=args.reorth)
+    kw = dict(restart=cfg.restart, maxit=cfg.maxit, rtol=cfg.rtol, reorth=args.reorth, x0_zero=True, history=False)
+    P.gmres_solve(p, net, b, x, **kw)
+    torch.cuda.synchronize()
+    best, rep = None, None
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        rep = P.gmres_solve(p, net, b, x, **kw)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        best = ms if best is None else min(best, ms)
+    bh = b.cpu().pin_memory()
+    xh = torch.zeros(p.shape, dtype=torch.float64).pin_memory()
+    P.gmres_solve_host(p, net, bh, xh, **kw)
+    t0 = time.perf_counter()
+    P.gmres_solve_host(p, net, bh, xh, **kw)
+    e2e_s = time.perf_counter() - t0
+    its = [r["iterations"] for r in rep]
+    line = {"metric": "time-to-tolerance (s)", "value": best * 1e-3, "unit": "s", "higher_is_better": False,
+            "n_gpus": 1, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": _workload_name(cfg), "rtol": cfg.rtol, "budget": cfg.maxit,
+                       "fixed_budget": cfg.fixed_budget, "restart": cfg.restart,
+                       "gram_schmidt": {0: "CGS2", 1: "CGS1", 2: "selective (DGKS)",
+                                        3: "DCGS2 (delayed re-orthogonalisation)"}[args.reorth]},
+            "iterations": its, "converged": [bool(r["converged"]) for r in rep],
+            "relres_true": [r["relres_true"] for r in rep],
+            "iter_per_s": sum(its) / len(its) / (best * 1e-3),
+            "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes": bh.numel() * 4, "d2h_bytes": xh.numel() * 8,
+                    "note": "one gmres_solve_host call (host buffers), host wall clock"}}
+    if not cfg.fixed_budget and not args.no_cpu_baseline:
+        from oracle import rte as O
+        try:
+            from threadpoolctl import threadpool_info
+            cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+        except Exception:
+            cores = os.cpu_count()
+        op = O.setup_from_media(cfg, media)
+        onet = O.make_mgnet(weights, cfg.M, cfg.L, cfg.C0, cfg.nu)
+        b64 = O.rhs(op).astype(np.float32).astype(np.float64)
+        t0 = time.perf_counter()
+        res = O.gmres(lambda v: O.apply(op, v), b64, P=lambda v: O.vcycle(onet, v), restart=cfg.restart,
+                      rtol=cfg.rtol, maxit=cfg.maxit)
+        line["cpu_baseline"] = {"value": time.perf_counter() - t0, "unit": "s", "cores": cores, "kind": "oracle",
+                                "iterations": res.iterations, "converged": bool(res.converged),
+                                "sample": "the whole solve of the fp64 numpy oracle (oracle.gmres with MGS) on the "
+                                          "same fp32-rounded b"}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -489,6 +559,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--coeffnet", action="store_true",
                     help="NEXT-1: precondition with the CoeffNet-modulated MgNet (DESIGN.md R31-R33)")
+    ap.add_argument("--time-to-tol", action="store_true",
+                    help="time the full solve to the config's rtol (or its budget) instead of K cycles")
     ap.add_argument("--reorth", type=int, default=3, choices=[0, 1, 2, 3],
                     help="Gram-Schmidt: 3 DCGS2 (default), 0 CGS2, 1 CGS1, 2 selective re-orthogonalisation")
     args = ap.parse_args()
@@ -498,6 +570,8 @@ def main():
     cfg = W.config(args.config)
     if args.impl == "reference":
         run_reference(args, cfg)
+    elif args.time_to_tol:
+        run_time_to_tol(args, cfg)
     else:
         run_ours(args, cfg)
 

@@ -11,8 +11,8 @@ if [ "${PART:-all}" = "bench" ] || [ "${PART:-all}" = "all" ]; then
   for k in 1 2 3 4; do run python bench.py --config $k --steps 5 --warmup 3 --no-cpu-baseline > $O/bench_cfg$k.json 2> $O/bench_cfg$k.err; done
   run python bench.py --steps 5 --warmup 3 --coeffnet --no-cpu-baseline > $O/bench_cfg5_coeffnet.json 2> $O/bench_cfg5_coeffnet.err
   run python bench.py --impl reference --steps 1 --warmup 3 > $O/bench_reference.json 2> $O/bench_reference.err
-  run python scripts/time_to_tol.py > $O/time_to_tol.json 2> $O/time_to_tol.err
-  run python scripts/tfps_bench.py --oracle > $O/tfps_cfg2.json 2> $O/tfps_cfg2.err
+  for k in 1 2 3 5; do run python bench.py --time-to-tol --config $k > $O/time_to_tol_cfg$k.json 2> $O/time_to_tol_cfg$k.err; done
+  run python scripts/tfps_bench.py > $O/tfps_cfg2.json 2> $O/tfps_cfg2.err
   run python scripts/paper_workload.py > $O/paper_workload.json 2> $O/paper_workload.err
 fi
 if [ "${PART:-all}" = "ncu" ] || [ "${PART:-all}" = "all" ]; then

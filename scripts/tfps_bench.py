@@ -4,7 +4,7 @@ iterations/s of whole restart cycles, unpreconditioned and with an MgNet (L = 4,
 64-channel alpha vectors -- with the kernel's algorithmic flops/bytes per launch (include/rte.h
 rte_setup_tfps; csrc/tfps.cu).  Prints one JSON object.
 
-  python scripts/tfps_bench.py [--cycles 3] > profiles/r02/tfps_cfg2.json
+  python scripts/tfps_bench.py [--cycles 3] [--delta 1e-4] > profiles/r02/tfps_cfg2.json
 """
 import argparse
 import json
@@ -21,7 +21,6 @@ import workloads as W  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--cycles", type=int, default=3)
-ap.add_argument("--oracle", action="store_true", help="also time one oracle apply (host cores)")
 ap.add_argument("--delta", type=float, default=1e-4, help="ATFPS tolerance of the compressed-system runs")
 a = ap.parse_args()
 cfg = W.config(2)
@@ -105,12 +104,4 @@ for name, nt in (("none", None), ("mgnet", neta)):
     ms = e0.elapsed_time(e1)
     out["atfps"][f"gmres_{name}"] = {"iter_per_s": K / (ms * 1e-3), "inner_iterations": K, "ms": ms,
                                      "relres_true_after": rep[0]["relres_true"]}
-if a.oracle:
-    import numpy as np
-    from oracle import tfps as T
-    tp = T.setup_from_media(cfg, media)
-    xa = np.random.default_rng(0).standard_normal(tp.shape)
-    t0 = time.perf_counter()
-    T.apply(tp, xa)
-    out["oracle_apply_s"] = time.perf_counter() - t0
 print(json.dumps(out, indent=1))
