@@ -249,10 +249,20 @@ def _cpu_baseline(cfg, media, weights):
     t0 = time.perf_counter()
     O.arnoldi_columns(lambda v: O.apply(op, v), b, lambda v: O.vcycle(onet, v), 1)
     dt = time.perf_counter() - t0
-    return {"value": 1.0 / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"one GMRES inner iteration of the fp64 numpy oracle on the full {cfg.k}-config problem "
-                      f"(oracle.arnoldi_columns steps=1: P=I+V-cycle, apply, MGS, norm), {dt:.1f} s wall; "
-                      f"BLAS threads={cores}, host cpus={os.cpu_count()}"}
+    out = {"value": 1.0 / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+           "sample": f"one GMRES inner iteration of the fp64 numpy oracle on the full {cfg.k}-config problem "
+                     f"(oracle.arnoldi_columns steps=1: P=I+V-cycle, apply, MGS, norm), {dt:.1f} s wall; "
+                     f"BLAS threads={cores}, host cpus={os.cpu_count()}"}
+    if cfg.unknowns <= 2 ** 21:  # configs 1-3: also single-threaded (SURVEY §8(d) oracle timing)
+        try:
+            from threadpoolctl import threadpool_limits
+            with threadpool_limits(limits=1):
+                t0 = time.perf_counter()
+                O.arnoldi_columns(lambda v: O.apply(op, v), b, lambda v: O.vcycle(onet, v), 1)
+                out["single_thread_value"] = 1.0 / (time.perf_counter() - t0)
+        except Exception:
+            pass
+    return out
 
 
 def run_reference(args, cfg):
