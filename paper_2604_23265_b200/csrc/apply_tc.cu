@@ -95,11 +95,21 @@ struct EpiApply {
   __device__ __forceinline__ void store_partial4(int, const Row&, int, float4) const {}
 };
 
-template <int BN>
+// The same operator with the TMA epilogue (tc_gemm.cuh, APPLY = 2): the epilogue reads psi at the
+// cell and its upwind neighbours from a TMA-loaded (TW + 2) x (TH + 2) halo chunk in shared memory
+// (tmH, box 32 ordinates x (TW + 2) x (TH + 2), zero fill = inflow faces) and writes y through a
+// swizzled staging tile and one bulk tensor store per chunk (tmY, box 32 x TW x TH).
+struct EpiApplyT : EpiApply {
+  static constexpr bool kTmaEpi = true;
+  CUtensorMap tmH;
+  CUtensorMap tmY;
+};
+
+template <int BN, class E>
 void launch_apply_bn(const Geom& g, int mtiles, const CUtensorMap& ta, const CUtensorMap& tbh,
-                     const CUtensorMap& tbl, const CUtensorMap& te, const EpiApply& epi, cudaStream_t st) {
-  auto kern = gemm3xtf32_kernel<BN, 0, false, EpiApply>;
-  constexpr int smem = gemm_smem_bytes<BN, 0, false, 1, true>();
+                     const CUtensorMap& tbl, const CUtensorMap& te, const E& epi, cudaStream_t st) {
+  auto kern = gemm3xtf32_kernel<BN, 0, false, E>;
+  constexpr int smem = gemm_smem_bytes<BN, 0, false, 1, tma_epi_of<E>::value ? 2 : 1>();
   ensure_smem((const void*)kern, smem);
   const int grid = std::min(mtiles * g.ntiles, num_sms());
   launch_gemm(kern, grid, smem, st, ta, tbh, tbl, te, g, epi);
@@ -160,11 +170,26 @@ void launch_apply_tc(const rte_problem* p, const float* x, float* y, const doubl
   CUtensorMap tbh = tc::make_map_kmajor(p->S_hi, M, B * M, BN);
   CUtensorMap tbl = tc::make_map_kmajor(p->S_lo, M, B * M, BN);
   tc::EpiApply epi{x, y, p->sig_d, p->sig_s, p->ax, p->ay, p->sgx, p->sgy, alpha, alpha_stride, N, M};
+  // TMA epilogue for N tiles of 64 / 128 whose halo box fits a slot (RTE_APPLY_OLDEPI: the per-lane
+  // L2 epilogue, kept as the measured alternative)
+  static const bool old_epi = getenv("RTE_APPLY_OLDEPI") != nullptr;
+  const bool tma_epi = !old_epi && BN >= 64 && (g.TW + 2) * (g.TH + 2) <= tc::kHaloEpiRows;
   prof_begin(st, "apply_f32_tc");
-  switch (BN) {
-    case 32: tc::launch_apply_bn<32>(g, mtiles, ta, tbh, tbl, te, epi, st); break;
-    case 64: tc::launch_apply_bn<64>(g, mtiles, ta, tbh, tbl, te, epi, st); break;
-    default: tc::launch_apply_bn<128>(g, mtiles, ta, tbh, tbl, te, epi, st); break;
+  if (tma_epi) {
+    tc::EpiApplyT et;
+    static_cast<tc::EpiApply&>(et) = epi;
+    et.tmH = tc::make_map_act(x, M, N, N, B, g.TW + 2, g.TH + 2, 1);
+    et.tmY = tc::make_map_act(y, M, N, N, B, g.TW, g.TH, 1);
+    if (BN == 64)
+      tc::launch_apply_bn<64>(g, mtiles, ta, tbh, tbl, te, et, st);
+    else
+      tc::launch_apply_bn<128>(g, mtiles, ta, tbh, tbl, te, et, st);
+  } else {
+    switch (BN) {
+      case 32: tc::launch_apply_bn<32>(g, mtiles, ta, tbh, tbl, te, epi, st); break;
+      case 64: tc::launch_apply_bn<64>(g, mtiles, ta, tbh, tbl, te, epi, st); break;
+      default: tc::launch_apply_bn<128>(g, mtiles, ta, tbh, tbl, te, epi, st); break;
+    }
   }
   after_launch("apply_f32_tc", st, apply_flops(p), apply_bytes(p, 4, 0), p->M >= 256 ? 1 : 0);
 }

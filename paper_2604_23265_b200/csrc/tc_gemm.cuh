@@ -120,13 +120,36 @@ constexpr int stage_chunks() {
 #endif
 // CPS = CTAs per SM (1, or 2 for BN = 32: two independent pipelines per SM hide each other's
 // hand-off latency; each gets half of TMEM and ~113 KB of shared memory)
-template <int BN, int AM, bool ASPLIT = false, int CPS = 1, bool APPLY = false>
+// TMA epilogue of the apply (APPLY = 2, Epi::kTmaEpi): per column half, RTE_EPI_HS halo slots of
+// one 32-ordinate chunk of the tile's (TW + 2) x (TH + 2) cell box (<= 184 rows of 128 B, SW128) and
+// one 128 x 32 output staging tile that a bulk tensor store drains
+constexpr int kHaloEpiRows = 184;
+constexpr int kHaloEpiBytes = kHaloEpiRows * 128;   // 23 KB: a multiple of the 1024-byte SW128 atom
+#ifndef RTE_EPI_HS
+#define RTE_EPI_HS 1
+#endif
+template <int BN, int APPLY>
+constexpr int epi_smem_bytes() {
+  return APPLY == 2 ? 2 * (RTE_EPI_HS * kHaloEpiBytes + kStageBytes) : 2 * stage_chunks<BN>() * kStageBytes;
+}
+// Epi::kTmaEpi if the epilogue type declares it, else false
+template <class E, class = void>
+struct tma_epi_of {
+  static constexpr bool value = false;
+};
+template <class E>
+struct tma_epi_of<E, decltype(void(E::kTmaEpi))> {
+  static constexpr bool value = E::kTmaEpi;
+};
+
+// APPLY: 0 = convolution, 1 = apply (row-centred), 2 = apply with the TMA epilogue
+template <int BN, int AM, bool ASPLIT = false, int CPS = 1, int APPLY = 0>
 struct Plan {
   static constexpr int kBBytes = BN * 128;                          // one of B hi / B lo
   static constexpr int kATile = AM == 2 ? kSSRows * 128 : AM == 1 ? kHaloRows * 128 : kABytes;
   static constexpr int kASlot = (ASPLIT || AM == 2 ? 2 : 1) * kATile;  // hi + lo tiles when split
   static constexpr int kBSlot = 2 * kBBytes;
-  static constexpr int kBudget = ((CPS == 1 ? 222 : 110) - 32 * stage_chunks<BN>()) * 1024;  // rings
+  static constexpr int kBudget = (CPS == 1 ? 222 : 110) * 1024 - epi_smem_bytes<BN, APPLY>();  // rings
   // A ring depth: halo tiles are reused for 9 K blocks; window tiles are one K block each, so
   // they need a deeper ring to cover the HBM latency (BN = 32 leaves room for 8)
   // (CPS = 2, N = 64: a single halo slot -- the other CTA on the SM covers its load latency)
@@ -139,9 +162,9 @@ struct Plan {
   static constexpr int kRingBytes = kNA * kASlot + kNB * kBSlot;
 };
 
-template <int BN, int AM, bool ASPLIT = false, int CPS = 1, bool APPLY = false>
+template <int BN, int AM, bool ASPLIT = false, int CPS = 1, int APPLY = 0>
 constexpr int gemm_smem_bytes() {
-  return Plan<BN, AM, ASPLIT, CPS, APPLY>::kRingBytes + 2 * stage_chunks<BN>() * kStageBytes + 1024 /*align*/ + 1024 /*barriers*/ +
+  return Plan<BN, AM, ASPLIT, CPS, APPLY>::kRingBytes + epi_smem_bytes<BN, APPLY>() + 1024 /*align*/ + 1024 /*barriers*/ +
          1024 /*row centres*/;
 }
 
@@ -308,7 +331,7 @@ template <int BN, int AM, bool ASPLIT, class Epi, int CPS = 1>
 __global__ void __launch_bounds__(kGemmThreads, CPS)
     gemm3xtf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBhi,
                       const __grid_constant__ CUtensorMap tmBlo, const __grid_constant__ CUtensorMap tmE,
-                      const Geom g, const Epi epi) {
+                      const Geom g, const __grid_constant__ Epi epi) {
   constexpr bool HALO = AM != 0;
   constexpr bool SSH = AM == 2;
   static_assert(BN == 32 || BN == 64 || BN == 128, "N tile must be 32, 64 or 128");
@@ -316,7 +339,10 @@ __global__ void __launch_bounds__(kGemmThreads, CPS)
   static_assert(!(ASPLIT && Epi::kCenter), "row centring needs the plain fp32 A operand");
   static_assert(!(SSH && ASPLIT), "SS-halo kernels split the activations themselves");
   static_assert(CPS == 1 || (CPS == 2 && BN <= 64 && !ASPLIT && AM != 2), "two CTAs per SM: BN <= 64 only");
-  using PL = Plan<BN, AM, ASPLIT, CPS, Epi::kCenter>;
+  constexpr bool TMAEPI = tma_epi_of<Epi>::value;
+  static_assert(!TMAEPI || (Epi::kCenter && AM == 0 && !ASPLIT && CPS == 1 && BN >= 64), "TMA epilogue: apply kernels");
+  constexpr int HS = RTE_EPI_HS;
+  using PL = Plan<BN, AM, ASPLIT, CPS, Epi::kCenter ? (TMAEPI ? 2 : 1) : 0>;
   constexpr int TCOLS = 512 / CPS;
   constexpr int NAR = PL::kNA, NBR = PL::kNB;
   constexpr int NA = tmem_abufs<BN, TCOLS>();
@@ -341,7 +367,8 @@ __global__ void __launch_bounds__(kGemmThreads, CPS)
   uint64_t* xempty = mempty + NG;      // [1] unit-long X drained (8 promoter warps)
   uint64_t* cfull = xempty + 1;        // [2] row centres written (128 converter threads)
   uint64_t* cempty = cfull + 2;        // [2] row centres read (256 epilogue threads)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cempty + 2);
+  uint64_t* hfull = cempty + 2;        // [2 halves][HS] TMA epilogue: halo chunk landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hfull + 2 * HS);
   float* cvec = reinterpret_cast<float*>(smem + PL::kRingBytes + 1024);  // [2][128] row centres
   const uint32_t stage_s = smem_u32(smem + PL::kRingBytes + 2048);        // [2 halves][chunks][128][32] staging
 
@@ -384,6 +411,7 @@ __global__ void __launch_bounds__(kGemmThreads, CPS)
       mbar_init(&cempty[t], 256);
     }
     mbar_init(xempty, 8);
+    for (int i = 0; i < 2 * HS; ++i) mbar_init(&hfull[i], 1);
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
@@ -710,6 +738,30 @@ __global__ void __launch_bounds__(kGemmThreads, CPS)
     const int e_ly0 = e_rr0 / g.pitch, e_lx0 = e_rr0 - e_ly0 * g.pitch;
     const int e_dly = RPI / g.pitch, e_dlx = RPI - e_dly * g.pitch;
     int gcount = 0;
+    // TMA epilogue (apply): this half's halo chunks s = li * ECH + j run through HS slots; the half's
+    // leader (first warp of the half, lane 0) issues the loads ahead and drains the output staging
+    constexpr int ECH = HB / 32 > 0 ? HB / 32 : 1;
+    const bool hlead = TMAEPI && ((warp - 6) & 3) == 0 && lane == 0;
+    const uint32_t epi_s = stage_s + (uint32_t)(half * (HS * kHaloEpiBytes + kStageBytes));
+    const uint32_t ostage = epi_s + (uint32_t)(HS * kHaloEpiBytes);
+    const uint32_t hbytes = (uint32_t)((g.TW + 2) * (g.TH + 2)) * 128u;
+    auto issue_halo = [&](int s) {
+      if constexpr (TMAEPI) {
+        const int lj = s / ECH, j = s - lj * ECH;
+        const int uu = (int)blockIdx.x + lj * (int)gridDim.x;
+        if (uu >= units) return;
+        const Unit w2 = decode_unit(g, uu);
+        const int slot = s % HS;
+        uint64_t* hb = &hfull[half * HS + slot];
+        mbar_arrive_expect_tx(hb, hbytes);
+        tma_load_4d(smem + (epi_s - smem_u32(smem)) + (uint32_t)(slot * kHaloEpiBytes), &epi.tmH, hb,
+                    w2.n0 + 32 * (half * ECH + j), w2.tc.tx * g.TW - 1, w2.tc.ty * g.TH - 1, w2.tc.b);
+      }
+    };
+    if (hlead) {
+      griddep_wait();  // the halos read the previous kernel's output (PDL)
+      for (int s = 0; s < HS; ++s) issue_halo(s);
+    }
     int li = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++li) {
       const Unit w = decode_unit(g, u);
@@ -719,6 +771,17 @@ __global__ void __launch_bounds__(kGemmThreads, CPS)
         // evict them first (measured)
         if (li == 0) epi_prefetch(g, &tmE, w);
         if (u + (int)gridDim.x < units) epi_prefetch(g, &tmE, decode_unit(g, u + gridDim.x));
+      }
+      // TMA epilogue: this thread's cell constants, loaded while the K loop runs
+      float t_sd = 0.f, t_ss = 0.f;
+      if constexpr (TMAEPI) {
+        const int ly = r / g.TW, lx = r - ly * g.TW;
+        const int oy = w.tc.ty * g.TH + ly, ox = w.tc.tx * g.TW + lx;
+        if (r < rows && oy < g.Hc && ox < g.Wc) {
+          const long long cell = ((long long)w.tc.b * g.Hc + oy) * g.Wc + ox;
+          t_sd = epi.sig_d[cell];
+          t_ss = epi.sig_s[cell];
+        }
       }
       float acc[HB];
 #pragma unroll
@@ -769,6 +832,64 @@ __global__ void __launch_bounds__(kGemmThreads, CPS)
         if (lane == 0) mbar_arrive(xempty);
       }
       if constexpr (Epi::kCenter) mbar_wait(&cfull[li & 1], (uint32_t)(li >> 1) & 1u);
+      if constexpr (TMAEPI) {
+        // ---- apply epilogue through TMA: thread = cell r (its TMEM lane), 32
+        // ordinates per chunk.  psi at the cell and at both upwind neighbours comes from the halo
+        // chunk in shared memory (out-of-domain neighbours = the TMA's zero fill = the inflow
+        // face), the outputs go to a swizzled staging tile that one bulk tensor store writes out.
+        const int e_oy0 = w.tc.ty * g.TH, e_ox0 = w.tc.tx * g.TW;
+        const typename Epi::Tile et = epi.tile(w.tc.b, w.tc.cls, e_oy0, e_ox0);
+        const int hw = g.TW + 2;
+        const int ly = r / g.TW, lx = r - ly * g.TW;
+        // rows beyond the tile compute on a valid halo row; their staging rows are not stored
+        const int hrow = r < rows ? (ly + 1) * hw + lx + 1 : hw + 1;
+        const float cr = cvec[(li & 1) * 128 + r];
+#pragma unroll
+        for (int j = 0; j < ECH; ++j) {  // unrolled: acc stays in registers
+          const int s = li * ECH + j;
+          const long long tq0 = prof ? clock64() : 0;
+          if (hlead) bulk_wait_read0();  // the previous chunk's store has read the staging tile
+          named_bar_sync(2 + half, 128);
+          const long long tq1 = prof ? clock64() : 0;
+          mbar_wait(&hfull[half * HS + s % HS], (uint32_t)(s / HS) & 1u);
+          const long long tq2 = prof ? clock64() : 0;
+          const uint32_t hs = epi_s + (uint32_t)((s % HS) * kHaloEpiBytes);
+          const int m0 = w.n0 + 32 * (half * ECH + j);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int m = m0 + 4 * q;  // columns m .. m+3 share a quadrant (M % 16 == 0)
+            const int sx = epi.sgx[m], sy = epi.sgy[m];
+            const float4 a_x = *reinterpret_cast<const float4*>(epi.ax + m);
+            const float4 a_y = *reinterpret_cast<const float4*>(epi.ay + m);
+            const int rx = hrow - sx, ry = hrow - sy * hw;
+            const float4 p = lds128(hs + (uint32_t)(hrow * 128 + ((q ^ (hrow & 7)) << 4)));
+            const float4 nx = lds128(hs + (uint32_t)(rx * 128 + ((q ^ (rx & 7)) << 4)));
+            const float4 ny = lds128(hs + (uint32_t)(ry * 128 + ((q ^ (ry & 7)) << 4)));
+            const float* v = &acc[32 * j + 4 * q];
+            const float al = et.al;
+            float4 o;
+            o.x = al * stencil_diag(a_x.x, a_y.x, t_sd, t_ss, p.x, nx.x, ny.x, cr, v[0]);
+            o.y = al * stencil_diag(a_x.y, a_y.y, t_sd, t_ss, p.y, nx.y, ny.y, cr, v[1]);
+            o.z = al * stencil_diag(a_x.z, a_y.z, t_sd, t_ss, p.z, nx.z, ny.z, cr, v[2]);
+            o.w = al * stencil_diag(a_x.w, a_y.w, t_sd, t_ss, p.w, nx.w, ny.w, cr, v[3]);
+            sts128(ostage + (uint32_t)(r * 128 + ((q ^ (r & 7)) << 4)), o);
+          }
+          const long long tq3 = prof ? clock64() : 0;
+          fence_proxy_async_smem();  // staging writes -> the bulk store (async proxy)
+          named_bar_sync(2 + half, 128);
+          if (hlead) {
+            tma_store_4d(ostage, &epi.tmY, m0, e_ox0, e_oy0, w.tc.b);
+            bulk_commit();
+            issue_halo(s + HS);  // every thread of the half has read this slot
+          }
+          if (prof) {  // slots 16 / 17 / 18: staging-free barrier, halo wait, compute (+ store barrier)
+            w_s1 += tq1 - tq0;
+            w_s2 += tq2 - tq1;
+            w_s3 += clock64() - tq2;
+          }
+          (void)tq3;
+        }
+      } else {
       // Coalesced epilogue.  Each column chunk (<= 32 columns) of this half is staged through a
       // shared tile (row r at r*128 B, 16-byte chunk q at position q ^ (r & 7): conflict-free both
       // ways), then the half's four warps walk their rows with float4 lanes, so every global
@@ -879,9 +1000,11 @@ __global__ void __launch_bounds__(kGemmThreads, CPS)
         w_s2 += ts2 - ts1;
         w_s3 += ts3 - ts2;
       }
+      }
       if constexpr (Epi::kCenter) mbar_arrive(&cempty[li & 1]);
       if (prof) w_e += clock64() - te0;
     }
+    if (hlead) bulk_wait0();  // every output store of this half is complete before the CTA exits
   }
   if (g.cl) {
     if (warp < 6) cluster_sync_all();  // phase 1 (the promoters passed it inside the epilogue)

@@ -52,7 +52,17 @@ SMALL = [
 ]
 
 
-@pytest.mark.parametrize("cfg", [W.config(k) for k in (1, 2, 3, 4, 5)] + SMALL,
+# M % 64 == 0 with ragged cell tiles: the TMA-epilogue apply (halo boxes clipped at the domain edge,
+# partial output boxes; N = 4 is a single 4 x 4-cell tile)
+TMA_EPI = [
+    W.small_config(4, N=13, M=128, n_polar=4, n_azim=32, B=2),
+    W.small_config(5, N=12, M=256, n_polar=4, n_azim=64),
+    W.small_config(5, N=4, M=128, n_polar=4, n_azim=32),
+    W.small_config(3, N=21, M=64, n_polar=4, n_azim=16, B=2),
+]
+
+
+@pytest.mark.parametrize("cfg", [W.config(k) for k in (1, 2, 3, 4, 5)] + SMALL + TMA_EPI,
                          ids=lambda c: f"cfg{c.k}-N{c.N}-M{c.M}-B{c.B}")
 def test_apply_and_rhs_parity(cfg, margin):
     import paper_2604_23265_b200 as P
