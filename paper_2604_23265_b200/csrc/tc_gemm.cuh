@@ -149,7 +149,8 @@ struct Plan {
   static constexpr int kATile = AM == 2 ? kSSRows * 128 : AM == 1 ? kHaloRows * 128 : kABytes;
   static constexpr int kASlot = (ASPLIT || AM == 2 ? 2 : 1) * kATile;  // hi + lo tiles when split
   static constexpr int kBSlot = 2 * kBBytes;
-  static constexpr int kBudget = (CPS == 1 ? 222 : 110) * 1024 - epi_smem_bytes<BN, APPLY>();  // rings
+  static constexpr int kBudget = (CPS == 1 ? 222 : 110) * 1024 - epi_smem_bytes<BN, APPLY>() -
+                                 (APPLY == 2 ? 10 * 1024 : 0);  // rings (APPLY 2: minus the column table)
   // A ring depth: halo tiles are reused for 9 K blocks; window tiles are one K block each, so
   // they need a deeper ring to cover the HBM latency (BN = 32 leaves room for 8)
   // (CPS = 2, N = 64: a single halo slot -- the other CTA on the SM covers its load latency)
@@ -162,10 +163,14 @@ struct Plan {
   static constexpr int kRingBytes = kNA * kASlot + kNB * kBSlot;
 };
 
+// TMA epilogue column table: per group of 4 ordinates {a_x[4], a_y[4]} and the two upwind halo-row
+// offsets (M <= 1024: 256 groups)
+constexpr int kColGroups = 256;
+constexpr int kColTabBytes = kColGroups * (32 + 8);
 template <int BN, int AM, bool ASPLIT = false, int CPS = 1, int APPLY = 0>
 constexpr int gemm_smem_bytes() {
   return Plan<BN, AM, ASPLIT, CPS, APPLY>::kRingBytes + epi_smem_bytes<BN, APPLY>() + 1024 /*align*/ + 1024 /*barriers*/ +
-         1024 /*row centres*/;
+         1024 /*row centres*/ + (APPLY == 2 ? kColTabBytes : 0);
 }
 
 // TMEM layout.  Fused form (BN <= 64): two group buffers t = 0, 1 of 2BN columns [main_t | X_t].
@@ -371,6 +376,13 @@ __global__ void __launch_bounds__(kGemmThreads, CPS)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hfull + 2 * HS);
   float* cvec = reinterpret_cast<float*>(smem + PL::kRingBytes + 1024);  // [2][128] row centres
   const uint32_t stage_s = smem_u32(smem + PL::kRingBytes + 2048);        // [2 halves][chunks][128][32] staging
+  // TMA epilogue column table (after the epilogue region): coltab[2g], coltab[2g + 1] = a_x, a_y of
+  // ordinates 4g .. 4g+3 (one quadrant); coloff[g] = halo-row offsets of their x / y upwind neighbours
+  // (pointers derived from smem_raw by an offset keep the shared state space: LDS / STS, not generic
+  // LD / ST as through the uintptr_t-aligned `smem`)
+  uint8_t* smem_sh = smem_raw + (smem_u32(smem) - smem_u32(smem_raw));
+  float4* coltab = reinterpret_cast<float4*>(smem_sh + PL::kRingBytes + 2048 + epi_smem_bytes<BN, 2>());
+  int2* coloff = reinterpret_cast<int2*>(coltab + 2 * kColGroups);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int units = g.mtiles * g.ntiles * g.nsplit;
@@ -421,6 +433,15 @@ __global__ void __launch_bounds__(kGemmThreads, CPS)
     if (g.epf) tma_prefetch(&tmE);
   }
   if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
+  if constexpr (TMAEPI) {  // (problem constants: no PDL wait needed)
+    const int hw = g.TW + 2;
+    for (int gi = threadIdx.x; gi < epi.M / 4; gi += blockDim.x) {
+      const int m = 4 * gi;
+      coltab[2 * gi] = *reinterpret_cast<const float4*>(epi.ax + m);
+      coltab[2 * gi + 1] = *reinterpret_cast<const float4*>(epi.ay + m);
+      coloff[gi] = make_int2(-(int)epi.sgx[m], -(int)epi.sgy[m] * hw);
+    }
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -841,6 +862,7 @@ __global__ void __launch_bounds__(kGemmThreads, CPS)
         const typename Epi::Tile et = epi.tile(w.tc.b, w.tc.cls, e_oy0, e_ox0);
         const int hw = g.TW + 2;
         const int ly = r / g.TW, lx = r - ly * g.TW;
+        (void)hw;
         // rows beyond the tile compute on a valid halo row; their staging rows are not stored
         const int hrow = r < rows ? (ly + 1) * hw + lx + 1 : hw + 1;
         const float cr = cvec[(li & 1) * 128 + r];
@@ -853,26 +875,28 @@ __global__ void __launch_bounds__(kGemmThreads, CPS)
           const long long tq1 = prof ? clock64() : 0;
           mbar_wait(&hfull[half * HS + s % HS], (uint32_t)(s / HS) & 1u);
           const long long tq2 = prof ? clock64() : 0;
-          const uint32_t hs = epi_s + (uint32_t)((s % HS) * kHaloEpiBytes);
+          // plain C++ shared-memory accesses (not volatile asm): the compiler may interleave the eight
+          // column groups' loads; the barrier / mbarrier asm above and below carry memory clobbers
+          const float4* hsp = reinterpret_cast<const float4*>(smem_sh + (epi_s - smem_u32(smem)) + (s % HS) * kHaloEpiBytes);
+          float4* osp = reinterpret_cast<float4*>(smem_sh + (ostage - smem_u32(smem)));
           const int m0 = w.n0 + 32 * (half * ECH + j);
+          const int g0 = m0 >> 2;  // columns 4g .. 4g+3 share a quadrant (M % 16 == 0)
+          const float al = et.al;
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
-            const int m = m0 + 4 * q;  // columns m .. m+3 share a quadrant (M % 16 == 0)
-            const int sx = epi.sgx[m], sy = epi.sgy[m];
-            const float4 a_x = *reinterpret_cast<const float4*>(epi.ax + m);
-            const float4 a_y = *reinterpret_cast<const float4*>(epi.ay + m);
-            const int rx = hrow - sx, ry = hrow - sy * hw;
-            const float4 p = lds128(hs + (uint32_t)(hrow * 128 + ((q ^ (hrow & 7)) << 4)));
-            const float4 nx = lds128(hs + (uint32_t)(rx * 128 + ((q ^ (rx & 7)) << 4)));
-            const float4 ny = lds128(hs + (uint32_t)(ry * 128 + ((q ^ (ry & 7)) << 4)));
+            const float4 a_x = coltab[2 * (g0 + q)], a_y = coltab[2 * (g0 + q) + 1];
+            const int2 off = coloff[g0 + q];
+            const int rx = hrow + off.x, ry = hrow + off.y;
+            const float4 p = hsp[hrow * 8 + (q ^ (hrow & 7))];
+            const float4 nx = hsp[rx * 8 + (q ^ (rx & 7))];
+            const float4 ny = hsp[ry * 8 + (q ^ (ry & 7))];
             const float* v = &acc[32 * j + 4 * q];
-            const float al = et.al;
             float4 o;
             o.x = al * stencil_diag(a_x.x, a_y.x, t_sd, t_ss, p.x, nx.x, ny.x, cr, v[0]);
             o.y = al * stencil_diag(a_x.y, a_y.y, t_sd, t_ss, p.y, nx.y, ny.y, cr, v[1]);
             o.z = al * stencil_diag(a_x.z, a_y.z, t_sd, t_ss, p.z, nx.z, ny.z, cr, v[2]);
             o.w = al * stencil_diag(a_x.w, a_y.w, t_sd, t_ss, p.w, nx.w, ny.w, cr, v[3]);
-            sts128(ostage + (uint32_t)(r * 128 + ((q ^ (r & 7)) << 4)), o);
+            osp[r * 8 + (q ^ (r & 7))] = o;
           }
           const long long tq3 = prof ? clock64() : 0;
           fence_proxy_async_smem();  // staging writes -> the bulk store (async proxy)
