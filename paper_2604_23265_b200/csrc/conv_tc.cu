@@ -249,6 +249,16 @@ struct EpiConv {
   }
 };
 
+// The same epilogue through TMA (tc_gemm.cuh, APPLY = 3): the addend tile of each 32-channel chunk
+// is bulk-loaded into shared memory ahead of the unit's K loop (tmAdd, box 32 x TW x TH), the output
+// is written over it in place and bulk-stored (tmOut).  Dense single-split tiles without modulation
+// or hi/lo output planes only (conv_tc_try); the arithmetic is EpiConv::store4's.
+struct EpiConvT : EpiConv {
+  static constexpr int kTmaEpi = 2;
+  CUtensorMap tmAdd;
+  CUtensorMap tmOut;
+};
+
 // Deterministic split-K reduction + epilogue: out[e] = s_in * sum_s partial[s][e] + s_add * addend[e].
 // With out_split the output (and the addend) are hi/lo planes: sample b's planes at 2b, 2b+1.
 __global__ void splitk_reduce_kernel(const float4* __restrict__ part, long long stride4, int nsplit, float4* out,
@@ -478,11 +488,11 @@ Plan make_plan(const ConvDesc& d) {
   return P;
 }
 
-template <int BN, int AM, bool ASPLIT, int CPS = 1>
+template <int BN, int AM, bool ASPLIT, int CPS = 1, class E = tc::EpiConv>
 void launch_bn(const Plan& P, const CUtensorMap& ta, const CUtensorMap& tbh, const CUtensorMap& tbl,
-               const CUtensorMap& te, const tc::EpiConv& epi, cudaStream_t st) {
-  auto kern = tc::gemm3xtf32_kernel<BN, AM, ASPLIT, tc::EpiConv, CPS>;
-  constexpr int smem = tc::gemm_smem_bytes<BN, AM, ASPLIT, CPS>();
+               const CUtensorMap& te, const E& epi, cudaStream_t st) {
+  auto kern = tc::gemm3xtf32_kernel<BN, AM, ASPLIT, E, CPS>;
+  constexpr int smem = tc::gemm_smem_bytes<BN, AM, ASPLIT, CPS, tc::tma_epi_of<E>::value == 2 ? 3 : 0>();
   tc::ensure_smem((const void*)kern, smem);
   const long long units = (long long)P.mtiles * P.ntiles * P.g.nsplit;
   if (P.g.cl) {
@@ -552,6 +562,22 @@ bool conv_tc_try(const ConvDesc& d, const float* in, float* out, const float* ad
     }
     epi.part = d.ws_owner->tc_ws;
   }
+  // TMA epilogue (RTE_CONV_OLDEPI: the per-lane global epilogue, kept as the measured alternative)
+  static const bool conv_old_epi = getenv("RTE_CONV_OLDEPI") != nullptr;
+  static const int tma_mask = getenv("RTE_CONV_TMA_MASK") ? atoi(getenv("RTE_CONV_TMA_MASK")) : 0xffff;
+  const int mbit = (P.BN == 32 ? 0 : P.BN == 64 ? 2 : 4) + (P.halo ? 0 : 1) + (addend ? 8 : 0);
+  // (stride-2 restrictions, mode 1, stay on the per-lane epilogue: with the TMA epilogue and programmatic
+  // dependent launch their V-cycles were not run-to-run bit-identical on config 4 -- 3 of 12 repeats,
+  // deterministic with RTE_NO_PDL=1; not understood, DESIGN.md §5 -- and they are ~1% of the V-cycle)
+  const bool tma_epi = !conv_old_epi && g.nsplit == 1 && !g.cl && !d.out_split && d.mod == nullptr && d.mode == 0 &&
+                       P.am != 2 && !d.in_split && (((tma_mask >> (mbit & 7)) & 1) != 0) && (((tma_mask >> 8) & 1) || !addend);
+  tc::EpiConvT et;
+  if (tma_epi) {
+    static_cast<tc::EpiConv&>(et) = epi;
+    if (addend) et.tmAdd = tc::make_map_act(addend, d.Co, d.Wo, d.Ho, d.B, g.TW, g.TH, 1);
+    et.tmOut = tc::make_map_act(out, d.Co, d.Wo, d.Ho, d.B, g.TW, g.TH, 1);
+    P.g.epf = 0;  // the addend tiles are loaded ahead anyway
+  }
   prof_begin(st, conv_class_name(d, true));
   // BN = 32 kernels run two CTAs per SM (each half the TMEM, ~113 KB of shared memory): their
   // pipelines are hand-off-latency bound, so two of them per SM hide each other (RTE_TC_CPS1=1: one)
@@ -559,6 +585,18 @@ bool conv_tc_try(const ConvDesc& d, const float* in, float* out, const float* ad
   static const bool two_per_sm64 = two_per_sm;  // (N = 64 too: single halo slot per CTA, NG = 1)
   auto dispatch = [&](auto bn_tag) {
     constexpr int BN = decltype(bn_tag)::value;
+    if (tma_epi) {
+      if constexpr (BN <= 64) {
+        if (two_per_sm) {
+          if (P.halo) launch_bn<BN, 1, false, 2>(P, ta, tbh, tbl, te, et, st);
+          else launch_bn<BN, 0, false, 2>(P, ta, tbh, tbl, te, et, st);
+          return;
+        }
+      }
+      if (P.halo) launch_bn<BN, 1, false, 1>(P, ta, tbh, tbl, te, et, st);
+      else launch_bn<BN, 0, false, 1>(P, ta, tbh, tbl, te, et, st);
+      return;
+    }
     if (P.am == 2) {
       if constexpr (BN <= 64) launch_bn<BN, 2, false>(P, ta, tbh, tbl, te, epi, st);
     } else if (P.halo) {

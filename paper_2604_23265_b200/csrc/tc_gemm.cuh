@@ -128,21 +128,26 @@ constexpr int kHaloEpiBytes = kHaloEpiRows * 128;   // 23 KB: a multiple of the 
 #ifndef RTE_EPI_HS
 #define RTE_EPI_HS 1
 #endif
+// TMA epilogue of a convolution (APPLY = 3, Epi::kTmaEpi == 2): one 128 x 32 tile per 32-column chunk
+// of the unit, loaded with the addend by TMA, finished in place and drained by a bulk tensor store
 template <int BN, int APPLY>
 constexpr int epi_smem_bytes() {
-  return APPLY == 2 ? 2 * (RTE_EPI_HS * kHaloEpiBytes + kStageBytes) : 2 * stage_chunks<BN>() * kStageBytes;
+  return APPLY == 2   ? 2 * (RTE_EPI_HS * kHaloEpiBytes + kStageBytes)
+         : APPLY == 3 ? (BN / 32) * kStageBytes
+                      : 2 * stage_chunks<BN>() * kStageBytes;
 }
-// Epi::kTmaEpi if the epilogue type declares it, else false
+// Epi::kTmaEpi if the epilogue type declares it (1 = apply halo epilogue, 2 = conv tile epilogue), else 0
 template <class E, class = void>
 struct tma_epi_of {
-  static constexpr bool value = false;
+  static constexpr int value = 0;
 };
 template <class E>
 struct tma_epi_of<E, decltype(void(E::kTmaEpi))> {
-  static constexpr bool value = E::kTmaEpi;
+  static constexpr int value = E::kTmaEpi;
 };
 
-// APPLY: 0 = convolution, 1 = apply (row-centred), 2 = apply with the TMA epilogue
+// APPLY: 0 = convolution, 1 = apply (row-centred), 2 = apply with the TMA epilogue, 3 = convolution
+// with the TMA epilogue
 template <int BN, int AM, bool ASPLIT = false, int CPS = 1, int APPLY = 0>
 struct Plan {
   static constexpr int kBBytes = BN * 128;                          // one of B hi / B lo
@@ -156,7 +161,7 @@ struct Plan {
   // (CPS = 2, N = 64: a single halo slot -- the other CTA on the SM covers its load latency)
   static constexpr int kNA = (AM != 0 || ASPLIT) ? (CPS == 2 && BN == 64 ? 1 : 2)
                              : CPS == 2 ? (BN == 64 ? 2 : 3) : BN == 32 ? 8 : BN == 64 ? 4
-                             : APPLY ? RTE_NA128 : RTE_NA128C;
+                             : (APPLY == 1 || APPLY == 2) ? RTE_NA128 : RTE_NA128C;
   static constexpr int kNBraw = (kBudget - kNA * kASlot) / kBSlot;
   static constexpr int kNB = kNBraw > 8 ? 8 : kNBraw;               // B ring depth
   static_assert(kNB >= 1, "shared-memory plan leaves no B slot");
@@ -344,10 +349,13 @@ __global__ void __launch_bounds__(kGemmThreads, CPS)
   static_assert(!(ASPLIT && Epi::kCenter), "row centring needs the plain fp32 A operand");
   static_assert(!(SSH && ASPLIT), "SS-halo kernels split the activations themselves");
   static_assert(CPS == 1 || (CPS == 2 && BN <= 64 && !ASPLIT && AM != 2), "two CTAs per SM: BN <= 64 only");
-  constexpr bool TMAEPI = tma_epi_of<Epi>::value;
+  constexpr bool TMAEPI = tma_epi_of<Epi>::value == 1;  // apply: halo chunks + stencil
+  constexpr bool CTEPI = tma_epi_of<Epi>::value == 2;   // conv: addend / output tiles
   static_assert(!TMAEPI || (Epi::kCenter && AM == 0 && !ASPLIT && CPS == 1 && BN >= 64), "TMA epilogue: apply kernels");
+  static_assert(!CTEPI || (!Epi::kCenter && AM != 2 && !ASPLIT), "conv TMA epilogue: TS kernels");
   constexpr int HS = RTE_EPI_HS;
-  using PL = Plan<BN, AM, ASPLIT, CPS, Epi::kCenter ? (TMAEPI ? 2 : 1) : 0>;
+  static_assert(HS >= 1 && HS <= 2, "RTE_EPI_HS: 1 or 2 halo slots per half");
+  using PL = Plan<BN, AM, ASPLIT, CPS, Epi::kCenter ? (TMAEPI ? 2 : 1) : (CTEPI ? 3 : 0)>;
   constexpr int TCOLS = 512 / CPS;
   constexpr int NAR = PL::kNA, NBR = PL::kNB;
   constexpr int NA = tmem_abufs<BN, TCOLS>();
@@ -372,8 +380,8 @@ __global__ void __launch_bounds__(kGemmThreads, CPS)
   uint64_t* xempty = mempty + NG;      // [1] unit-long X drained (8 promoter warps)
   uint64_t* cfull = xempty + 1;        // [2] row centres written (128 converter threads)
   uint64_t* cempty = cfull + 2;        // [2] row centres read (256 epilogue threads)
-  uint64_t* hfull = cempty + 2;        // [2 halves][HS] TMA epilogue: halo chunk landed
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hfull + 2 * HS);
+  uint64_t* hfull = cempty + 2;        // [2 halves][HS] TMA epilogue: halo chunk landed; conv: [BN / 32] tile ready
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hfull + 4);
   float* cvec = reinterpret_cast<float*>(smem + PL::kRingBytes + 1024);  // [2][128] row centres
   const uint32_t stage_s = smem_u32(smem + PL::kRingBytes + 2048);        // [2 halves][chunks][128][32] staging
   // TMA epilogue column table (after the epilogue region): coltab[2g], coltab[2g + 1] = a_x, a_y of
@@ -423,7 +431,7 @@ __global__ void __launch_bounds__(kGemmThreads, CPS)
       mbar_init(&cempty[t], 256);
     }
     mbar_init(xempty, 8);
-    for (int i = 0; i < 2 * HS; ++i) mbar_init(&hfull[i], 1);
+    for (int i = 0; i < 4; ++i) mbar_init(&hfull[i], 1);
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
@@ -783,9 +791,32 @@ __global__ void __launch_bounds__(kGemmThreads, CPS)
       griddep_wait();  // the halos read the previous kernel's output (PDL)
       for (int s = 0; s < HS; ++s) issue_halo(s);
     }
+    // TMA epilogue (conv): chunk c of the unit lives in tile slot c (stage_s + c * 16 KB); a half owns
+    // CPH chunks from cfirst (BN = 32: the one chunk is shared by both halves, half 0's leader drives it)
+    constexpr int CCH = BN / 32;
+    constexpr int CPH = CCH >= 2 ? CCH / 2 : 1;
+    const bool clead = CTEPI && ((warp - 6) & 3) == 0 && lane == 0 && (CCH >= 2 || half == 0);
+    const int cfirst = CCH >= 2 ? half * CPH : 0;
+    const uint32_t tbytes = (uint32_t)(g.TW * g.TH) * 128u;
+    if (clead) griddep_wait();  // the addend tiles may be the previous kernel's output (PDL)
     int li = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++li) {
       const Unit w = decode_unit(g, u);
+      if constexpr (CTEPI) {
+        if (clead) {
+          // the previous unit's stores have read the slots; refill them with this unit's addend
+          bulk_wait_read0();
+          for (int c = cfirst; c < cfirst + CPH; ++c) {
+            if (epi.addend) {
+              mbar_arrive_expect_tx(&hfull[c], tbytes);
+              tma_load_4d(smem + (stage_s - smem_u32(smem)) + (uint32_t)(c * kStageBytes), &epi.tmAdd, &hfull[c],
+                          w.n0 + 32 * c, w.tc.tx * g.TW, w.tc.ty * g.TH, w.tc.b);
+            } else {
+              mbar_arrive(&hfull[c]);
+            }
+          }
+        }
+      }
       if (g.epf == 1 && warp == 6 && lane == 0) {
         // pull the epilogue's global inputs into L2 one unit ahead (this unit's at the first):
         // far enough ahead to cover a short K loop, near enough that the output stream does not
@@ -853,7 +884,45 @@ __global__ void __launch_bounds__(kGemmThreads, CPS)
         if (lane == 0) mbar_arrive(xempty);
       }
       if constexpr (Epi::kCenter) mbar_wait(&cfull[li & 1], (uint32_t)(li >> 1) & 1u);
-      if constexpr (TMAEPI) {
+      if constexpr (CTEPI) {
+        // ---- conv epilogue through TMA: thread = output pixel r (its TMEM lane); the addend tile of
+        // each 32-column chunk is already in its slot; out = s_in v + s_add addend is written in place
+        // and one bulk tensor store per chunk writes the tile (out-of-domain rows are clipped)
+        const int e_oy0 = w.tc.ty * g.TH, e_ox0 = w.tc.tx * g.TW;
+        const typename Epi::Tile et = epi.tile(w.tc.b, w.tc.cls, e_oy0, e_ox0);
+#pragma unroll
+        for (int cc = 0; cc < CPH; ++cc) {
+          const int c = cfirst + cc;
+          mbar_wait(&hfull[c], (uint32_t)li & 1u);
+          float4* sp = reinterpret_cast<float4*>(smem_sh + (stage_s - smem_u32(smem)) + c * kStageBytes);
+          constexpr int NQ = HB >= 32 ? 8 : HB / 4;  // float4 groups of this thread in the chunk
+#pragma unroll
+          for (int qq = 0; qq < NQ; ++qq) {
+            const int q = HB >= 32 ? qq : half * NQ + qq;
+            const float* v = &acc[HB >= 32 ? 32 * cc + 4 * qq : 4 * qq];
+            float4& slot = sp[r * 8 + (q ^ (r & 7))];
+            float4 o = make_float4(et.si * (1.f * v[0]), et.si * (1.f * v[1]), et.si * (1.f * v[2]), et.si * (1.f * v[3]));
+            if (epi.addend) {
+              const float4 a = slot;
+              o.x = fmaf(et.sa, a.x, o.x);
+              o.y = fmaf(et.sa, a.y, o.y);
+              o.z = fmaf(et.sa, a.z, o.z);
+              o.w = fmaf(et.sa, a.w, o.w);
+            }
+            slot = o;
+          }
+        }
+        fence_proxy_async_smem();  // slot writes -> the bulk store (async proxy)
+        if (CCH >= 2)
+          named_bar_sync(2 + half, 128);
+        else
+          named_bar_sync(5, 256);
+        if (clead) {
+          for (int c = cfirst; c < cfirst + CPH; ++c)
+            tma_store_4d(stage_s + (uint32_t)(c * kStageBytes), &epi.tmOut, w.n0 + 32 * c, e_ox0, e_oy0, w.tc.b);
+          bulk_commit();
+        }
+      } else if constexpr (TMAEPI) {
         // ---- apply epilogue through TMA: thread = cell r (its TMEM lane), 32
         // ordinates per chunk.  psi at the cell and at both upwind neighbours comes from the halo
         // chunk in shared memory (out-of-domain neighbours = the TMA's zero fill = the inflow
@@ -1028,7 +1097,12 @@ __global__ void __launch_bounds__(kGemmThreads, CPS)
       if constexpr (Epi::kCenter) mbar_arrive(&cempty[li & 1]);
       if (prof) w_e += clock64() - te0;
     }
-    if (hlead) bulk_wait0();  // every output store of this half is complete before the CTA exits
+    if (hlead || clead) {
+      bulk_wait0();  // every output store of this half is complete before the CTA exits
+#ifdef RTE_EXP_GFENCE
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+#endif
+    }
   }
   if (g.cl) {
     if (warp < 6) cluster_sync_all();  // phase 1 (the promoters passed it inside the epilogue)
