@@ -144,6 +144,32 @@ rte_status rte_atfps_reconstruct(const rte_problem* p, const float* alpha_dev, f
 rte_status rte_atfps_reconstruct_f64(const rte_problem* p, const double* alpha_dev, double* psi_dev,
                                      double* full_dev, void* stream);
 
+/* rte_set_source -- replace the source q (host [batch][N][N], >= 0) and, if inflow != NULL, the inflow
+ * (host [batch][4][N][directions], layout of rte_setup) of an existing problem of any kind, keeping the
+ * medium and everything derived from it: the right-hand side (rte_rhs; f = eps q, and chi^s = f / (eps sigma_a)
+ * of a TFPS / ATFPS problem) changes, the operator does not.  For training over many right-hand sides per
+ * medium (NEXT-4).  Synchronous.  Errors: RTE_EINVAL (NULL p or q, negative q). */
+rte_status rte_set_source(rte_problem* p, const float* q, const float* inflow);
+
+/* rte_atfps_fit -- D_delta of the filtered loss (NEXT-4, eq:loss / eq:loss_delta; reading
+ * R43 in DESIGN.md §3): maps a discrete angular flux psi_dev [batch][N][N][Md] (cell centres, the
+ * psi-space layout of rte_setup) to coefficients alpha_dev [batch][N][N][2 Md] (padded ATFPS layout) by a
+ * per-cell least-squares fit: the samples at the centre and the four face midpoints (the average of the two
+ * adjacent centre values; the cell's own value on a boundary face) minus the particular solution chi^s,
+ * fitted by the cell's kept modes (minimum-norm solution); dropped slots get 0.  Device pointers, no
+ * aliasing, asynchronous on `stream`.  The fit operators are built on the first call (host fp64).
+ * Errors: RTE_EINVAL (NULL, not an ATFPS problem). */
+rte_status rte_atfps_fit(const rte_problem* p, const float* psi_dev, float* alpha_dev, void* stream);
+rte_status rte_atfps_fit_f64(const rte_problem* p, const double* psi_dev, double* alpha_dev, void* stream);
+/* rte_atfps_loss -- the filtered loss loss_delta = ||b_bar - A_bar D_delta psi_d||_2 per sample (eq:loss_delta)
+ * into the host array loss [batch] (the call synchronises `stream`), and, if grad_dev != NULL, its gradient
+ * with respect to psi_d (sum over samples) into grad_dev [batch][N][N][Md]: D_lin^T A_bar^T (-r / ||r||)
+ * (reading R45).  Reductions in fp64 (fixed order).  Errors: RTE_EINVAL (NULL psi/loss, aliasing, not an
+ * ATFPS problem). */
+rte_status rte_atfps_loss(const rte_problem* p, const float* psi_dev, double* loss, float* grad_dev, void* stream);
+rte_status rte_atfps_loss_f64(const rte_problem* p, const double* psi_dev, double* loss, double* grad_dev,
+                              void* stream);
+
 /* Sizes of a problem: batch, N, M and n = batch*N*N*M. Any pointer may be NULL. */
 rte_status rte_problem_info(const rte_problem* p, int* batch, int* N, int* M, int64_t* n);
 

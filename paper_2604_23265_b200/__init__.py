@@ -16,7 +16,8 @@ from . import _lib
 from ._lib import RTE_ENUMERIC, RTE_OK, RteError, check, gmres_opts, gmres_report, lib
 
 __all__ = ["Problem", "MgNet", "rte_setup", "rte_setup_tfps", "rte_setup_atfps", "rte_atfps_info",
-           "rte_atfps_reconstruct", "rte_atfps_reconstruct_f64", "rte_tfps_info", "rte_tfps_modes", "rte_tfps_reconstruct",
+           "rte_atfps_reconstruct", "rte_atfps_reconstruct_f64", "rte_atfps_fit", "rte_atfps_fit_f64", "rte_set_source",
+           "rte_atfps_loss", "rte_atfps_loss_f64", "rte_tfps_info", "rte_tfps_modes", "rte_tfps_reconstruct",
            "rte_tfps_reconstruct_f64", "rte_rhs", "rte_apply", "rte_apply_f64", "rte_blockjacobi_apply", "mgnet_create",
            "mgnet_vcycle", "mgnet_vcycle_f64", "mgnet_coeffnet", "mgnet_coeffnet_weight_count", "mgnet_modulation", "gmres_prepare", "gmres_solve", "gmres_solve_host", "rte_quadrature", "rte_hg_matrix", "rte_launch_count", "rte_timing_enable", "rte_timing_filter", "rte_timing_reset",
            "rte_timing_get", "RteError", "LIB_PATH"]
@@ -147,6 +148,39 @@ def rte_atfps_reconstruct_f64(p: Problem, alpha, psi, full=None, stream=None) ->
     check("rte_atfps_reconstruct_f64", lib.rte_atfps_reconstruct_f64(
         p.handle, _dev(alpha, "f64"), _dev(psi, "f64"), _dev(full, "f64") if full is not None else None,
         C.c_void_p(_stream(stream))))
+
+
+def rte_set_source(p: Problem, q, inflow=None) -> None:
+    """Replace the source q [batch][N][N] (and the inflow [batch][4][N][directions] if given); host arrays."""
+    qa = _f32(q)
+    ia = _f32(inflow) if inflow is not None else None
+    check("rte_set_source", lib.rte_set_source(p.handle, _fptr(qa), _fptr(ia) if ia is not None else None))
+
+
+def rte_atfps_fit(p: Problem, psi, alpha, stream=None) -> None:
+    check("rte_atfps_fit", lib.rte_atfps_fit(p.handle, _dev(psi, "f32"), _dev(alpha, "f32"), C.c_void_p(_stream(stream))))
+
+
+def rte_atfps_fit_f64(p: Problem, psi, alpha, stream=None) -> None:
+    check("rte_atfps_fit_f64", lib.rte_atfps_fit_f64(p.handle, _dev(psi, "f64"), _dev(alpha, "f64"),
+                                                     C.c_void_p(_stream(stream))))
+
+
+def rte_atfps_loss(p: Problem, psi, grad=None, stream=None) -> np.ndarray:
+    """loss_delta per sample (host float64 [batch]); fills grad (device, psi's layout) if given."""
+    out = np.zeros(p.batch, np.float64)
+    check("rte_atfps_loss", lib.rte_atfps_loss(p.handle, _dev(psi, "f32"), _dptr(out),
+                                               _dev(grad, "f32") if grad is not None else None,
+                                               C.c_void_p(_stream(stream))))
+    return out
+
+
+def rte_atfps_loss_f64(p: Problem, psi, grad=None, stream=None) -> np.ndarray:
+    out = np.zeros(p.batch, np.float64)
+    check("rte_atfps_loss_f64", lib.rte_atfps_loss_f64(p.handle, _dev(psi, "f64"), _dptr(out),
+                                                       _dev(grad, "f64") if grad is not None else None,
+                                                       C.c_void_p(_stream(stream))))
+    return out
 
 
 def rte_tfps_modes(c, s, S, gamma: float):

@@ -59,6 +59,11 @@ SIGS = {
     "rte_atfps_info": (C.c_int, [_vp, C.POINTER(C.c_double), C.POINTER(C.c_int64), C.POINTER(C.c_uint8)]),
     "rte_atfps_reconstruct": (C.c_int, [_vp, _vp, _vp, _vp, _vp]),
     "rte_atfps_reconstruct_f64": (C.c_int, [_vp, _vp, _vp, _vp, _vp]),
+    "rte_set_source": (C.c_int, [_vp, _fp, _fp]),
+    "rte_atfps_fit": (C.c_int, [_vp, _vp, _vp, _vp]),
+    "rte_atfps_fit_f64": (C.c_int, [_vp, _vp, _vp, _vp]),
+    "rte_atfps_loss": (C.c_int, [_vp, _vp, C.POINTER(C.c_double), _vp, _vp]),
+    "rte_atfps_loss_f64": (C.c_int, [_vp, _vp, C.POINTER(C.c_double), _vp, _vp]),
     "rte_tfps_reconstruct_f64": (C.c_int, [_vp, _vp, _vp, _vp]),
     "rte_destroy": (None, [_vp]),
     "rte_problem_info": (C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int),

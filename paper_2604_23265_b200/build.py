@@ -21,7 +21,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
          "-I" + os.path.join(ROOT, "include")]
 SOURCES = ["rte_abi.cpp", "apply.cu", "apply_tc.cu", "mgnet.cu", "conv_tc.cu", "krylov.cu", "blockjacobi.cu",
-           "tfps_setup.cpp", "tfps.cu"]
+           "tfps_setup.cpp", "tfps.cu", "loss.cu"]
 
 
 def _deps():

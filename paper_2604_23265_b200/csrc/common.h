@@ -90,6 +90,7 @@ struct rte_problem {
   // host copies (fp64)
   std::vector<double> c, s, zeta, w;
   std::vector<double> S;   // [B][M][M] row-stochastic K W
+  std::vector<float> h_eps, h_sa;  // [B][N][N] eps and sigma_a as given (rte_set_source)
   // device
   float* sig_t = nullptr;   // [B][N][N]  sigma_T / eps
   float* sig_s = nullptr;   //            sigma_T / eps - eps sigma_a
@@ -139,6 +140,12 @@ struct rte_problem {
   int* at_dirs = nullptr;       // [4][Md/2] incoming directions of the faces L, R, B, T
   float* at_tmp32 = nullptr;    // [n] full coefficients (layer reconstruction scratch)
   double* at_tmp64 = nullptr;
+  // ---- filtered loss (NEXT-4, loss.cu; built on the first rte_atfps_loss / rte_atfps_fit call)
+  mutable float* ls_Dp32 = nullptr;   // [nmat][2Md][5Md] D_delta fit operators (R43)
+  mutable double* ls_Dp64 = nullptr;
+  mutable void* ls_ws = nullptr;      // scratch: alpha, residual, b_bar (n each), fit adjoint [cells][5Md]
+  mutable size_t ls_ws_bytes = 0;
+  mutable double* ls_norm = nullptr;  // [B] ||r||^2 per sample
 };
 
 // ---- kernel launchers (apply.cu) --------------------------------------------
@@ -184,4 +191,10 @@ void atfps_interface(const std::vector<double>& Lh, const std::vector<uint8_t>& 
 template <typename T>
 void launch_atfps(const rte_problem* p, int mode, const T* x, T* y, const double* alpha_dev, int alpha_stride,
                   const float* b, cudaStream_t st);  // mode 0: A x (y = b - A x if b), 1: rhs (T = float), 2: layer
+// filtered loss (NEXT-4, loss.cu, tfps_setup.cpp)
+void atfps_fit_pinv(const double* L, const double* fac, const uint8_t* sel, int M, double* Dp);
+template <typename T>
+void atfps_fit(const rte_problem* p, const T* psi, T* alpha, cudaStream_t st);
+template <typename T>
+void atfps_loss(const rte_problem* p, const T* psi, double* loss_host, T* grad, cudaStream_t st);
 }  // namespace rte

@@ -310,7 +310,7 @@ static void free_problem(rte_problem* p) {
                   p->S_lo, p->ax, p->ay, p->ax64, p->ay64, p->sgx, p->sgy, p->inflow, p->scratch64,
                   p->bj64, p->bj32, p->tf_mat, p->tf_L32, p->tf_L64, p->tf_fac32, p->tf_fac64, p->tf_chis32,
                   p->tf_chis64, p->at_sel, p->at_P32, p->at_P64, p->at_row, p->at_dirs, p->at_tmp32,
-                  p->at_tmp64};
+                  p->at_tmp64, p->ls_Dp32, p->ls_Dp64, p->ls_ws, p->ls_norm};
   for (void* q : ptrs) dfree(q);
   free_tc_state(p);
   free_gmres_work(p);
@@ -372,6 +372,8 @@ rte_status rte_setup(const rte_grid* grid, const rte_ordinates* ord, const float
       sd[k] = (float)sd64[k];
       ff[k] = (float)(e * (double)q[k]);
     }
+    p->h_eps.assign(eps, eps + p->ncell);
+    p->h_sa.assign(sigma_a, sigma_a + p->ncell);
     // scattering matrices per sample
     p->S.assign((size_t)B * M * M, 0.0);
     for (int b = 0; b < B; ++b) {
@@ -626,6 +628,68 @@ rte_status rte_atfps_reconstruct_f64(const rte_problem* p, const double* alpha_d
   double* full = full_dev ? full_dev : p->at_tmp64;
   launch_atfps<double>(p, 2, alpha_dev, full, nullptr, 0, nullptr, as_stream(stream));
   launch_tfps_reconstruct<double>(p, full, psi_dev, as_stream(stream));
+  RTE_API_END
+}
+
+rte_status rte_set_source(rte_problem* p, const float* q, const float* inflow) {
+  RTE_API_BEGIN
+  RTE_REQUIRE(p && q, "rte_set_source: NULL argument");
+  const int64_t nc = p->ncell;
+  std::vector<float> ff(nc);
+  std::vector<double> chis(nc);
+  for (int64_t k = 0; k < nc; ++k) {
+    RTE_REQUIRE(q[k] >= 0.0f, "rte_set_source: q must be >= 0");
+    const double e = p->h_eps[k];
+    ff[k] = (float)(e * (double)q[k]);
+    chis[k] = (e * (double)q[k]) / (e * (double)p->h_sa[k]);  // f / (sigma_t - sigma_s), as rte_setup_tfps
+  }
+  upload(p->f, ff.data(), nc);
+  if (p->kind != 0) {
+    std::vector<float> c32(chis.begin(), chis.end());
+    upload(p->tf_chis64, chis.data(), nc);
+    upload(p->tf_chis32, c32.data(), nc);
+  }
+  if (inflow) {
+    const int Md = p->kind == 0 ? p->M : p->Md;
+    const size_t ni = (size_t)p->B * 4 * p->N * Md;
+    if (!p->inflow) p->inflow = dalloc<float>(ni);
+    upload(p->inflow, inflow, ni);
+  }
+  RTE_API_END
+}
+
+rte_status rte_atfps_fit(const rte_problem* p, const float* psi_dev, float* alpha_dev, void* stream) {
+  RTE_API_BEGIN
+  RTE_REQUIRE(p && psi_dev && alpha_dev, "rte_atfps_fit: NULL argument");
+  RTE_REQUIRE(p->kind == 2, "rte_atfps_fit: not an ATFPS problem (rte_setup_atfps)");
+  atfps_fit<float>(p, psi_dev, alpha_dev, as_stream(stream));
+  RTE_API_END
+}
+
+rte_status rte_atfps_fit_f64(const rte_problem* p, const double* psi_dev, double* alpha_dev, void* stream) {
+  RTE_API_BEGIN
+  RTE_REQUIRE(p && psi_dev && alpha_dev, "rte_atfps_fit_f64: NULL argument");
+  RTE_REQUIRE(p->kind == 2, "rte_atfps_fit_f64: not an ATFPS problem (rte_setup_atfps)");
+  atfps_fit<double>(p, psi_dev, alpha_dev, as_stream(stream));
+  RTE_API_END
+}
+
+rte_status rte_atfps_loss(const rte_problem* p, const float* psi_dev, double* loss, float* grad_dev, void* stream) {
+  RTE_API_BEGIN
+  RTE_REQUIRE(p && psi_dev && loss, "rte_atfps_loss: NULL argument");
+  RTE_REQUIRE(p->kind == 2, "rte_atfps_loss: not an ATFPS problem (rte_setup_atfps)");
+  RTE_REQUIRE((const void*)psi_dev != (const void*)grad_dev, "rte_atfps_loss: psi and grad must not alias");
+  atfps_loss<float>(p, psi_dev, loss, grad_dev, as_stream(stream));
+  RTE_API_END
+}
+
+rte_status rte_atfps_loss_f64(const rte_problem* p, const double* psi_dev, double* loss, double* grad_dev,
+                              void* stream) {
+  RTE_API_BEGIN
+  RTE_REQUIRE(p && psi_dev && loss, "rte_atfps_loss_f64: NULL argument");
+  RTE_REQUIRE(p->kind == 2, "rte_atfps_loss_f64: not an ATFPS problem (rte_setup_atfps)");
+  RTE_REQUIRE((const void*)psi_dev != (const void*)grad_dev, "rte_atfps_loss_f64: psi and grad must not alias");
+  atfps_loss<double>(p, psi_dev, loss, grad_dev, as_stream(stream));
   RTE_API_END
 }
 

@@ -289,3 +289,54 @@ void atfps_interface(const std::vector<double>& Lh /*[nmat][M][2M]*/, const std:
 }
 
 }  // namespace rte
+
+namespace rte {
+
+// The D_delta fit of the filtered loss (NEXT-4; reading R43): for one material, the
+// minimum-norm least-squares solution operator of the collocation fit over the selected modes,
+// Dp [2M][5M] row-major (rows of dropped modes 0; columns point-major C, L, R, B, T x direction), so that
+// alpha = Dp (samples - chi^s).  G[p M + i][k] = L[i][k] fac[p][k] (the basis value chi^k_i at point p;
+// fac order L, R, B, T, C) over the selected k.  Dp = V diag(1/lambda) V^T G^T from the Jacobi
+// eigen-decomposition of G^T G; eigenvalues at or below 1e-13 lambda_max are dropped (the numerical null
+// space of the fit: the minimum-norm solution).
+void atfps_fit_pinv(const double* L, const double* fac, const uint8_t* sel, int M, double* Dp) {
+  const int K = 2 * M, R = 5 * M;
+  static const int fpos[5] = {4, 0, 1, 2, 3};  // point C, L, R, B, T -> fac row
+  std::vector<int> ks;
+  for (int k = 0; k < K; ++k)
+    if (sel[k]) ks.push_back(k);
+  const int n = (int)ks.size();
+  std::fill(Dp, Dp + (size_t)K * R, 0.0);
+  if (n == 0) return;
+  std::vector<double> G((size_t)R * n);
+  for (int p = 0; p < 5; ++p)
+    for (int i = 0; i < M; ++i)
+      for (int c = 0; c < n; ++c) G[((size_t)p * M + i) * n + c] = L[(size_t)i * K + ks[c]] * fac[(size_t)fpos[p] * K + ks[c]];
+  std::vector<double> GtG((size_t)n * n, 0.0);
+  for (int a = 0; a < n; ++a)
+    for (int b = 0; b < n; ++b) {
+      double s = 0.0;
+      for (int r = 0; r < R; ++r) s += G[(size_t)r * n + a] * G[(size_t)r * n + b];
+      GtG[(size_t)a * n + b] = s;
+    }
+  std::vector<double> ev, V;
+  jacobi_eig(GtG, n, ev, V);
+  double lmax = 0.0;
+  for (double l : ev) lmax = std::max(lmax, l);
+  // X = V diag(1/lambda) V^T  (n x n), then Dp rows = X G^T
+  std::vector<double> X((size_t)n * n, 0.0);
+  for (int e = 0; e < n; ++e) {
+    if (!(ev[e] > 1e-13 * lmax)) continue;
+    const double inv = 1.0 / ev[e];
+    for (int a = 0; a < n; ++a)
+      for (int b = 0; b < n; ++b) X[(size_t)a * n + b] += V[(size_t)a * n + e] * inv * V[(size_t)b * n + e];
+  }
+  for (int a = 0; a < n; ++a)
+    for (int r = 0; r < R; ++r) {
+      double s = 0.0;
+      for (int b = 0; b < n; ++b) s += X[(size_t)a * n + b] * G[(size_t)r * n + b];
+      Dp[(size_t)ks[a] * R + r] = s;
+    }
+}
+
+}  // namespace rte
