@@ -257,6 +257,8 @@ struct EpiConvT : EpiConv {
   static constexpr int kTmaEpi = 2;
   CUtensorMap tmAdd;
   CUtensorMap tmOut;
+  CUtensorMap tmPart;  // split-K partials [nsplit * nb][Ho][Wo][Co] (box 32 x TW x TH)
+  int nb;              // batch samples
 };
 
 // Deterministic split-K reduction + epilogue: out[e] = s_in * sum_s partial[s][e] + s_add * addend[e].
@@ -469,7 +471,8 @@ Plan make_plan(const ConvDesc& d) {
       const long long tiles = (long long)P.mtiles * P.ntiles;
       waves = (double)((tiles + mc - 1) / mc);
     }
-    const double red = nsr == 1 ? 0.0 : cluster_ok ? 1.0 : (nsr + 2) * out_us + 3.0;
+    static const double red_fixed = getenv("RTE_TC_RED_US") ? atof(getenv("RTE_TC_RED_US")) : 3.0;
+    const double red = nsr == 1 ? 0.0 : cluster_ok ? 1.0 : (nsr + 2) * out_us + red_fixed;
     const double t = waves * (kps * t_kb + t_unit) + red;
     if (t < best * 0.97) {
       best = t;
@@ -569,13 +572,15 @@ bool conv_tc_try(const ConvDesc& d, const float* in, float* out, const float* ad
   // (stride-2 restrictions, mode 1, stay on the per-lane epilogue: with the TMA epilogue and programmatic
   // dependent launch their V-cycles were not run-to-run bit-identical on config 4 -- 3 of 12 repeats,
   // deterministic with RTE_NO_PDL=1; not understood, DESIGN.md §5 -- and they are ~1% of the V-cycle)
-  const bool tma_epi = !conv_old_epi && g.nsplit == 1 && !g.cl && !d.out_split && d.mod == nullptr && d.mode == 0 &&
+  const bool tma_epi = !conv_old_epi && !g.cl && !d.out_split && d.mod == nullptr && d.mode == 0 &&
                        P.am != 2 && !d.in_split && (((tma_mask >> (mbit & 7)) & 1) != 0) && (((tma_mask >> 8) & 1) || !addend);
   tc::EpiConvT et;
   if (tma_epi) {
     static_cast<tc::EpiConv&>(et) = epi;
     if (addend) et.tmAdd = tc::make_map_act(addend, d.Co, d.Wo, d.Ho, d.B, g.TW, g.TH, 1);
     et.tmOut = tc::make_map_act(out, d.Co, d.Wo, d.Ho, d.B, g.TW, g.TH, 1);
+    et.nb = d.B;
+    if (g.nsplit > 1) et.tmPart = tc::make_map_act(epi.part, d.Co, d.Wo, d.Ho, d.B * g.nsplit, g.TW, g.TH, 1);
     P.g.epf = 0;  // the addend tiles are loaded ahead anyway
   }
   prof_begin(st, conv_class_name(d, true));

@@ -159,7 +159,10 @@ struct Plan {
   // A ring depth: halo tiles are reused for 9 K blocks; window tiles are one K block each, so
   // they need a deeper ring to cover the HBM latency (BN = 32 leaves room for 8)
   // (CPS = 2, N = 64: a single halo slot -- the other CTA on the SM covers its load latency)
-  static constexpr int kNA = (AM != 0 || ASPLIT) ? (CPS == 2 && BN == 64 ? 1 : 2)
+#ifndef RTE_HALO_NA32
+#define RTE_HALO_NA32 2  // halo A slots of the two-per-SM N = 32 convs (experiments: the TMA epilogue frees 16 KB)
+#endif
+  static constexpr int kNA = (AM != 0 || ASPLIT) ? (CPS == 2 && BN == 64 ? 1 : CPS == 2 && BN == 32 && APPLY == 3 ? RTE_HALO_NA32 : 2)
                              : CPS == 2 ? (BN == 64 ? 2 : 3) : BN == 32 ? 8 : BN == 64 ? 4
                              : (APPLY == 1 || APPLY == 2) ? RTE_NA128 : RTE_NA128C;
   static constexpr int kNBraw = (kBudget - kNA * kASlot) / kBSlot;
@@ -807,7 +810,7 @@ __global__ void __launch_bounds__(kGemmThreads, CPS)
           // the previous unit's stores have read the slots; refill them with this unit's addend
           bulk_wait_read0();
           for (int c = cfirst; c < cfirst + CPH; ++c) {
-            if (epi.addend) {
+            if (epi.addend && g.nsplit == 1) {
               mbar_arrive_expect_tx(&hfull[c], tbytes);
               tma_load_4d(smem + (stage_s - smem_u32(smem)) + (uint32_t)(c * kStageBytes), &epi.tmAdd, &hfull[c],
                           w.n0 + 32 * c, w.tc.tx * g.TW, w.tc.ty * g.TH, w.tc.b);
@@ -901,6 +904,10 @@ __global__ void __launch_bounds__(kGemmThreads, CPS)
             const int q = HB >= 32 ? qq : half * NQ + qq;
             const float* v = &acc[HB >= 32 ? 32 * cc + 4 * qq : 4 * qq];
             float4& slot = sp[r * 8 + (q ^ (r & 7))];
+            if (g.nsplit > 1) {  // split-K: the raw partial sums (EpiConv::store_partial4)
+              slot = make_float4(v[0], v[1], v[2], v[3]);
+              continue;
+            }
             float4 o = make_float4(et.si * (1.f * v[0]), et.si * (1.f * v[1]), et.si * (1.f * v[2]), et.si * (1.f * v[3]));
             if (epi.addend) {
               const float4 a = slot;
@@ -918,8 +925,13 @@ __global__ void __launch_bounds__(kGemmThreads, CPS)
         else
           named_bar_sync(5, 256);
         if (clead) {
-          for (int c = cfirst; c < cfirst + CPH; ++c)
-            tma_store_4d(stage_s + (uint32_t)(c * kStageBytes), &epi.tmOut, w.n0 + 32 * c, e_ox0, e_oy0, w.tc.b);
+          for (int c = cfirst; c < cfirst + CPH; ++c) {
+            if (g.nsplit > 1)  // partial plane `split` of the [nsplit B][Ho][Wo][Co] workspace
+              tma_store_4d(stage_s + (uint32_t)(c * kStageBytes), &epi.tmPart, w.n0 + 32 * c, e_ox0, e_oy0,
+                           w.split * epi.nb + w.tc.b);
+            else
+              tma_store_4d(stage_s + (uint32_t)(c * kStageBytes), &epi.tmOut, w.n0 + 32 * c, e_ox0, e_oy0, w.tc.b);
+          }
           bulk_commit();
         }
       } else if constexpr (TMAEPI) {
