@@ -196,6 +196,9 @@ constexpr bool tmem_fused() {
 #ifndef RTE_TC_PROF
 #define RTE_TC_PROF 0
 #endif
+#ifndef RTE_CONV_EARLY_LOAD
+#define RTE_CONV_EARLY_LOAD 1  // converters load + split before waiting for the TMEM A buffer
+#endif
 #ifndef RTE_EPI_BATCH_MAX
 #define RTE_EPI_BATCH_MAX 8
 #endif
@@ -677,8 +680,10 @@ __global__ void __launch_bounds__(kGemmThreads, CPS)
         kb_split<HALO>(g, kb, tap, cc);
         const bool new_tile = !HALO || tap == 0 || kb == w.kb0;
         if (new_tile) tw_wait(&afull[as], aph, prof, w_a);
+#if !RTE_CONV_EARLY_LOAD
         tw_wait(&afree[ab], abph ^ 1, prof, w_b);
         tc_fence_after();
+#endif
         // source row in the A tile: the tap-shifted halo row (HALO) or the row itself; 16-byte
         // chunk q of a row sits at chunk position q ^ (row & 7) (SW128)
         int arow = rr;
@@ -733,6 +738,14 @@ __global__ void __launch_bounds__(kGemmThreads, CPS)
               split_tf32_fast(x, hi[e], lo[e]);
             }
           }
+#if RTE_CONV_EARLY_LOAD
+          // the TMEM A buffer is needed only from here: the first pass's shared-memory loads and
+          // split overlap the wait for the MMAs to release it
+          if (c0 == 0) {
+            tw_wait(&afree[ab], abph ^ 1, prof, w_b);
+            tc_fence_after();
+          }
+#endif
           if (!skip) {
             if constexpr (CWC == 32) {
               tmem_st32(ta, hi);
