@@ -4,8 +4,9 @@ DCGS2, graphs, x0 = 0) against the fp64 oracle's reference run of the same budge
 
 The budgets (300 / 60 per sample / 30 iterations) end far from rtol, so there is no converged count to
 compare; instead the residual history |g_{j+1}|/||b|| over the whole budget and the final iterate x (at
-the seeded indices workloads.sample_indices) must lie within 2x the band of K = 4 perturbed oracle runs
-(the max deviation of a perturbed run from the reference run).  The reference run, the perturbed runs
+the seeded indices workloads.sample_indices) must lie within 2x the band of the perturbed oracle runs
+(the max deviation of a perturbed run from the reference run): K = 4 fp64 runs on perturbed inputs and
+one run of the GPU's Gram-Schmidt with fp32 storage (scripts/make_bands_fp32.py; reading R36 v3).  The reference run, the perturbed runs
 and the bands are stored in tests/golden/bands_cfg{k}.npz by scripts/make_bands.py, which calls only
 oracle/ and workloads/ (the perturbation model is reading R36 in DESIGN.md §3).  Any config-4 sample
 whose reference run converges within the budget is held to the north star's +-1 instead.
@@ -58,7 +59,10 @@ def test_fixed_budget_gmres_within_oracle_band(k, margin):
         assert rep["iterations"] == cfg.maxit == int(g[f"s{s}_ref_it"])
         dh = float(np.max(np.abs(rep["history"] - ref_hist) / ref_hist))
         dx = float(np.linalg.norm(xs[s, idx] - g[f"s{s}_ref_xs"]) / np.linalg.norm(g[f"s{s}_ref_xs"]))
-        bh, bx = 2.0 * float(g[f"s{s}_band_hist"]), 2.0 * float(g[f"s{s}_band_x"])
+        # the band: the largest deviation from the reference among the perturbed runs -- the K input-
+        # perturbed fp64 runs and the fp32-storage run of the GPU's own Gram-Schmidt (R36 v3)
+        bh = 2.0 * max(float(g[f"s{s}_band_hist"]), float(g.get(f"s{s}_band_fp32_hist", 0.0)))
+        bx = 2.0 * max(float(g[f"s{s}_band_x"]), float(g.get(f"s{s}_band_fp32_x", 0.0)))
         assert margin(dh, bh, f"s{s} residual history vs 2x band") <= bh, (s, dh, bh)
         assert margin(dx, bx, f"s{s} iterate x vs 2x band") <= bx, (s, dx, bx)
         # and the iterate's norm agrees with the reference to the same band
