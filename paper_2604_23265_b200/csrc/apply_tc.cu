@@ -100,7 +100,7 @@ struct EpiApply {
 // (tmH, box 32 ordinates x (TW + 2) x (TH + 2), zero fill = inflow faces) and writes y through a
 // swizzled staging tile and one bulk tensor store per chunk (tmY, box 32 x TW x TH).
 struct EpiApplyT : EpiApply {
-  static constexpr bool kTmaEpi = true;
+  static constexpr int kTmaEpi = 1;
   CUtensorMap tmH;
   CUtensorMap tmY;
 };

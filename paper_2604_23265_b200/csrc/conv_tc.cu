@@ -569,18 +569,17 @@ bool conv_tc_try(const ConvDesc& d, const float* in, float* out, const float* ad
   static const bool conv_old_epi = getenv("RTE_CONV_OLDEPI") != nullptr;
   static const int tma_mask = getenv("RTE_CONV_TMA_MASK") ? atoi(getenv("RTE_CONV_TMA_MASK")) : 0xffff;
   const int mbit = (P.BN == 32 ? 0 : P.BN == 64 ? 2 : 4) + (P.halo ? 0 : 1) + (addend ? 8 : 0);
-  // (stride-2 restrictions, mode 1, stay on the per-lane epilogue: with the TMA epilogue and programmatic
-  // dependent launch their V-cycles were not run-to-run bit-identical on config 4 -- 3 of 12 repeats,
-  // deterministic with RTE_NO_PDL=1; not understood, DESIGN.md §5 -- and they are ~1% of the V-cycle)
-  const bool tma_epi = !conv_old_epi && !g.cl && !d.out_split && d.mod == nullptr && d.mode == 0 &&
+  const bool tma_epi = !conv_old_epi && !g.cl && !d.out_split && d.mod == nullptr &&
                        P.am != 2 && !d.in_split && (((tma_mask >> (mbit & 7)) & 1) != 0) && (((tma_mask >> 8) & 1) || !addend);
   tc::EpiConvT et;
   if (tma_epi) {
     static_cast<tc::EpiConv&>(et) = epi;
-    if (addend) et.tmAdd = tc::make_map_act(addend, d.Co, d.Wo, d.Ho, d.B, g.TW, g.TH, 1);
-    et.tmOut = tc::make_map_act(out, d.Co, d.Wo, d.Ho, d.B, g.TW, g.TH, 1);
+    // transposed convs (mode 2): a class tile is every other pixel of a 2TW x 2TH output box (stride-2 box)
+    const int oes = d.mode == 2 ? 2 : 1;
+    if (addend) et.tmAdd = tc::make_map_act(addend, d.Co, d.Wo, d.Ho, d.B, g.TW, g.TH, oes);
+    et.tmOut = tc::make_map_act(out, d.Co, d.Wo, d.Ho, d.B, g.TW, g.TH, oes);
     et.nb = d.B;
-    if (g.nsplit > 1) et.tmPart = tc::make_map_act(epi.part, d.Co, d.Wo, d.Ho, d.B * g.nsplit, g.TW, g.TH, 1);
+    if (g.nsplit > 1) et.tmPart = tc::make_map_act(epi.part, d.Co, d.Wo, d.Ho, d.B * g.nsplit, g.TW, g.TH, oes);
     P.g.epf = 0;  // the addend tiles are loaded ahead anyway
   }
   prof_begin(st, conv_class_name(d, true));

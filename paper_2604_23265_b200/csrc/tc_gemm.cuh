@@ -824,9 +824,12 @@ __global__ void __launch_bounds__(kGemmThreads, CPS)
           bulk_wait_read0();
           for (int c = cfirst; c < cfirst + CPH; ++c) {
             if (epi.addend && g.nsplit == 1) {
+              // (transposed convs: class cls = (py, px) is the stride-2 box at (2 x0 + px, 2 y0 + py))
+              const int ax = g.mode == 2 ? 2 * w.tc.tx * g.TW + (w.tc.cls & 1) : w.tc.tx * g.TW;
+              const int ay = g.mode == 2 ? 2 * w.tc.ty * g.TH + (w.tc.cls >> 1) : w.tc.ty * g.TH;
               mbar_arrive_expect_tx(&hfull[c], tbytes);
               tma_load_4d(smem + (stage_s - smem_u32(smem)) + (uint32_t)(c * kStageBytes), &epi.tmAdd, &hfull[c],
-                          w.n0 + 32 * c, w.tc.tx * g.TW, w.tc.ty * g.TH, w.tc.b);
+                          w.n0 + 32 * c, ax, ay, w.tc.b);
             } else {
               mbar_arrive(&hfull[c]);
             }
@@ -837,7 +840,12 @@ __global__ void __launch_bounds__(kGemmThreads, CPS)
         // pull the epilogue's global inputs into L2 one unit ahead (this unit's at the first):
         // far enough ahead to cover a short K loop, near enough that the output stream does not
         // evict them first (measured)
-        if (li == 0) epi_prefetch(g, &tmE, w);
+        if (li == 0) {
+          // (after the PDL wait: an L2 prefetch of lines the previous kernel is still writing through
+          // TMA stores was the suspected source of the stride-2 TMA-epilogue nondeterminism, §5)
+          griddep_wait();
+          epi_prefetch(g, &tmE, w);
+        }
         if (u + (int)gridDim.x < units) epi_prefetch(g, &tmE, decode_unit(g, u + gridDim.x));
       }
       // TMA epilogue: this thread's cell constants, loaded while the K loop runs
@@ -938,12 +946,14 @@ __global__ void __launch_bounds__(kGemmThreads, CPS)
         else
           named_bar_sync(5, 256);
         if (clead) {
+          const int sx = g.mode == 2 ? 2 * e_ox0 + (w.tc.cls & 1) : e_ox0;
+          const int sy = g.mode == 2 ? 2 * e_oy0 + (w.tc.cls >> 1) : e_oy0;
           for (int c = cfirst; c < cfirst + CPH; ++c) {
             if (g.nsplit > 1)  // partial plane `split` of the [nsplit B][Ho][Wo][Co] workspace
-              tma_store_4d(stage_s + (uint32_t)(c * kStageBytes), &epi.tmPart, w.n0 + 32 * c, e_ox0, e_oy0,
+              tma_store_4d(stage_s + (uint32_t)(c * kStageBytes), &epi.tmPart, w.n0 + 32 * c, sx, sy,
                            w.split * epi.nb + w.tc.b);
             else
-              tma_store_4d(stage_s + (uint32_t)(c * kStageBytes), &epi.tmOut, w.n0 + 32 * c, e_ox0, e_oy0, w.tc.b);
+              tma_store_4d(stage_s + (uint32_t)(c * kStageBytes), &epi.tmOut, w.n0 + 32 * c, sx, sy, w.tc.b);
           }
           bulk_commit();
         }
