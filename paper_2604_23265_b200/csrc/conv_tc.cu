@@ -581,6 +581,14 @@ bool conv_tc_try(const ConvDesc& d, const float* in, float* out, const float* ad
     et.nb = d.B;
     if (g.nsplit > 1) et.tmPart = tc::make_map_act(epi.part, d.Co, d.Wo, d.Ho, d.B * g.nsplit, g.TW, g.TH, oes);
     P.g.epf = 0;  // the addend tiles are loaded ahead anyway
+    // split-K fixup inside the kernel when every unit has its own resident CTA (tc_gemm.cuh Geom::fix):
+    // no reduction launch.  Opt-in (RTE_TC_FIX=1): measured slower -- config-5 V-cycle 2.057 -> 2.130 ms;
+    // the grid barrier waits for the slowest split and the reduction no longer overlaps the next
+    // kernel's prologue
+    static const bool nofix = getenv("RTE_TC_FIX") == nullptr;
+    const int cps = (P.BN <= 64 && getenv("RTE_TC_CPS1") == nullptr) ? 2 : 1;
+    const long long units = (long long)P.mtiles * P.ntiles * g.nsplit;
+    P.g.fix = (!nofix && g.nsplit > 1 && units <= (long long)cps * num_sms()) ? 1 : 0;
   }
   prof_begin(st, conv_class_name(d, true));
   // BN = 32 kernels run two CTAs per SM (each half the TMEM, ~113 KB of shared memory): their
@@ -622,8 +630,9 @@ bool conv_tc_try(const ConvDesc& d, const float* in, float* out, const float* ad
     case 64: dispatch(std::integral_constant<int, 64>{}); break;
     default: dispatch(std::integral_constant<int, 128>{}); break;
   }
-  const bool split = g.nsplit > 1 && !g.cl;  // (cluster split-K reduces inside the kernel)
-  after_launch(conv_class_name(d, true), st, conv_flops(d), split ? 0.0 : conv_bytes(d, addend != nullptr), 1);
+  const bool split = g.nsplit > 1 && !g.cl && !g.fix;  // (cluster split-K and the fixup reduce in the kernel)
+  after_launch(conv_class_name(d, true), st, conv_flops(d),
+               split ? 0.0 : conv_bytes(d, addend != nullptr) + (g.fix ? 8.0 * g.nsplit * P.out_elems : 0.0), 1);
   if (split) {
     prof_begin(st, "splitk_reduce");
     const long long n4 = P.out_elems / 4;

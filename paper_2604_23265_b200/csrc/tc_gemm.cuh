@@ -89,6 +89,8 @@ struct Geom {
                     // output-shaped tile (conv addend; epf_planes planes), 2 the tile with its
                     // one-cell halo (apply: the cells and their upwind neighbours)
   int epf_planes;
+  int fix;          // split-K fixup in the kernel (conv TMA epilogue, one unit per CTA, every CTA resident):
+                    // after a grid barrier every CTA reduces a slice of the output (no reduction launch)
   int cl;           // cluster split-K: 0 off; else = nsplit, the K splits of one output tile run
                     // as one thread-block cluster (one unit per CTA) and are reduced through
                     // distributed shared memory (no global partials, no reduction launch)
@@ -302,6 +304,37 @@ __device__ __forceinline__ void a_origin(const Geom& g, const TileCoord& c, int 
 // wait A slot, 20 producer A TMA issue, 21 producer B TMA issue; 22 MMA wait bfull; 23 converter
 // wait afull.
 __device__ unsigned long long g_tc_prof[24];
+
+// Grid barrier of the in-kernel split-K fixup (Geom::fix): arrival count and generation.  Safe because
+// the fixup is planned only when every CTA of the grid is resident (one unit per CTA, grid <= SMs) --
+// a later kernel launched early by PDL cannot take an SM before all of this grid's CTAs have started --
+// and a later kernel reaches its own barrier only after its griddepcontrol.wait (this grid complete).
+__device__ unsigned int g_fix_cnt;
+__device__ unsigned int g_fix_gen;
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void grid_barrier_fix() {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned g0 = ld_acquire_u32(&g_fix_gen);
+    asm volatile("fence.proxy.async.global;" ::: "memory");  // the bulk (async-proxy) partial stores
+    __threadfence();
+    if (atomicAdd(&g_fix_cnt, 1u) == gridDim.x - 1) {
+      atomicExch(&g_fix_cnt, 0u);
+      __threadfence();
+      atomicAdd(&g_fix_gen, 1u);
+    } else {
+      while (ld_acquire_u32(&g_fix_gen) == g0) __nanosleep(64);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
 
 // (the warp stays converged: the timer is predicated, the wait is executed once by all lanes)
 // Epilogue-input L2 prefetch for unit w (Geom::epf): the output-shaped tile (per plane), or the
@@ -1177,6 +1210,41 @@ __global__ void __launch_bounds__(kGemmThreads, CPS)
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (CTEPI) {
+    if (g.fix) {
+      // ---- in-kernel split-K fixup: every partial tile is stored (the leaders waited for their bulk
+      // stores); after the grid barrier CTA c reduces float4 slice c of the output, summing the splits
+      // in order and applying the epilogue exactly as splitk_reduce_kernel does (bit-identical)
+      grid_barrier_fix();
+      const long long n4 = epi.part_stride / 4, per4 = n4 / epi.nb;
+      const long long e0 = n4 * blockIdx.x / gridDim.x, e1 = n4 * (blockIdx.x + 1) / gridDim.x;
+      const float4* part = reinterpret_cast<const float4*>(epi.part);
+      float4* out4 = reinterpret_cast<float4*>(epi.out);
+      const float4* add4 = reinterpret_cast<const float4*>(epi.addend);
+      for (long long e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+        float4 sacc = __ldcg(part + e);
+        for (int k = 1; k < g.nsplit; ++k) {
+          const float4 q = __ldcg(part + k * n4 + e);
+          sacc.x += q.x;
+          sacc.y += q.y;
+          sacc.z += q.z;
+          sacc.w += q.w;
+        }
+        const int b = (int)(e / per4);
+        const float al = epi.alpha ? (float)epi.alpha[(long long)b * epi.alpha_stride] : 1.f;
+        const float si = epi.sign * (epi.a_in ? al : 1.f), sa = epi.a_add ? al : 1.f;
+        float4 r = make_float4(si * sacc.x, si * sacc.y, si * sacc.z, si * sacc.w);
+        if (add4) {
+          const float4 a = __ldcg(add4 + e);
+          r.x = fmaf(sa, a.x, r.x);
+          r.y = fmaf(sa, a.y, r.y);
+          r.z = fmaf(sa, a.z, r.z);
+          r.w = fmaf(sa, a.w, r.w);
+        }
+        out4[e] = r;
+      }
+    }
+  }
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, TMEM_COLS);
