@@ -80,7 +80,14 @@ for name, kw in (("none", dict(precond=0)), ("block_jacobi", dict(precond=2)),
                          **({"precond": kw["precond"]} if "precond" in kw else {}))
     res[name] = [int(r["iterations"]) for r in reps]
     res[name + "_converged"] = [bool(r["converged"]) for r in reps]
+    if name == "block_jacobi":
+        # the loss floor: loss_delta of the converged upwind (psi-space) solution itself -- the gap between
+        # the two discretisations (upwind DO vs ATFPS) that no network output can close
+        with torch.no_grad():
+            res["upwind_solution_test_loss_delta"] = [float(v) for v in
+                                                      TR.loss_delta(x.float().contiguous(), p2).cpu().numpy()]
 summary = {k: float(np.median(v)) for k, v in res.items() if not k.endswith(("_converged", "_loss_delta"))}
+summary.update({k: float(np.median(v)) for k, v in res.items() if k.endswith("_loss_delta")})
 report = {
     "what": "NEXT-4: MgNet trained on loss_delta (library-evaluated), GMRES(30) iterations to rtol 1e-8 on "
             "held-out media/sources (psi-space operator), median over test samples",
