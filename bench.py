@@ -184,6 +184,34 @@ def _composite_roofline(classes, select, peaks, label):
             "note": "per-class device times of the profiled solve (every launch bracketed by CUDA events)"}
 
 
+def _vcycle_direct(roof_v, classes, ops):
+    """The V-cycle fraction from whole mgnet_vcycle calls timed back to back by one pair of CUDA events
+    (the production launch sequence: programmatic dependent launch overlaps each kernel's prologue with
+    its predecessor's tail, which the per-launch events of the profiled solve prevent).  The roofline
+    time per V-cycle is the profiled solve's composite divided by its number of V-cycles (= launches of
+    the once-per-V-cycle 1x1 lift / head classes).  `frac` becomes this directly timed figure; the
+    per-class sums stay as frac_profiled / frac_sustained_profiled."""
+    per_s = ops.get("mgnet_vcycle_per_s")
+    once = [c["launches"] for c in classes if c["name"].startswith("conv1x1")]
+    if roof_v is None or not per_s or not once:
+        return roof_v
+    n_v = min(once)
+    ms = 1e3 / per_s
+    roof_v["vcycles_profiled"] = n_v
+    roof_v["frac_profiled"] = roof_v["frac"]
+    roof_v["frac_sustained_profiled"] = roof_v["frac_sustained"]
+    roof_v["measured_ms_per_vcycle"] = ms
+    roof_v["roofline_ms_per_vcycle_burst"] = roof_v["roofline_ms_burst"] / n_v
+    roof_v["roofline_ms_per_vcycle_sustained"] = roof_v["roofline_ms_sustained"] / n_v
+    roof_v["frac"] = roof_v["roofline_ms_burst"] / n_v / ms
+    roof_v["frac_sustained"] = roof_v["roofline_ms_sustained"] / n_v / ms
+    roof_v["note"] = ("frac / frac_sustained: whole mgnet_vcycle calls timed back to back by one pair of CUDA "
+                      "events (production launch sequence, PDL overlap intact) against the per-V-cycle roofline "
+                      "time; frac_profiled: per-class device times of the profiled solve (every launch "
+                      "bracketed by CUDA events, which serialises the PDL overlap)")
+    return roof_v
+
+
 def _roofline(classes, peaks, src, top=None):
     """Roofline of one kernel class (default: the dominant one, max total device time)."""
     if not classes:
@@ -431,7 +459,7 @@ def run_ours(args, cfg):
                          ("mgnet_vcycle_per_s", lambda: P.mgnet_vcycle(net, b, z, True))):
             fn()
             torch.cuda.synchronize()
-            reps = 5
+            reps = 20
             a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a0.record(stream)
             for _ in range(reps):
@@ -457,6 +485,7 @@ def run_ours(args, cfg):
         roof_v = _composite_roofline(all_classes, lambda n: not n.startswith(_NOT_VCYCLE), peaks,
                                      "MgNet V-cycle (lift, smoother/restriction/prolongation convs, split-K "
                                      "reductions, head + pass-through)")
+        roof_v = _vcycle_direct(roof_v, all_classes, ops)
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
                 "scaling": "strong" if sharded else "weak",

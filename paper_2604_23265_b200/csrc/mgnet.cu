@@ -318,9 +318,15 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 2 : NT == 256 ? 3 : 4) conv1x1
 
 bool conv1x1_smallk_ok(const ConvDesc& d) {
   // (Co = 64, 128 or 256, one channel tile: the weight block [ci][0 .. Co) is contiguous for the bulk copy)
+  // With C0 = 32 the tensor-core GEMM and its TMA epilogue (addend tiles bulk-loaded, output tiles
+  // bulk-stored, PDL) now beats this kernel -- config 5: 0.119 against 0.136 ms, config 4: 0.117
+  // against 0.135, config 3 equal -- so the small-K kernel serves the C0 = 16 heads (configs 1-2),
+  // which the tensor-core path does not take (RTE_SMALLK=1 forces it, RTE_NO_SMALLK=1 disables it)
+  static const bool force = getenv("RTE_SMALLK") != nullptr;
+  const bool tc_can = d.w && d.w->d_hi && d.ws_owner && d.ws_owner->tc && d.Ci % 32 == 0 && d.Co % 32 == 0;
   return d.mode == 0 && d.ks == 1 && d.Ci <= kSmallKMaxCi && d.Ci % 4 == 0 &&
          (d.Co == 64 || d.Co == 128 || d.Co == 256) && !d.in_split && !d.mod &&
-         !d.out_split && getenv("RTE_NO_SMALLK") == nullptr;
+         !d.out_split && getenv("RTE_NO_SMALLK") == nullptr && (force || !tc_can);
 }
 
 template <typename T>

@@ -201,6 +201,19 @@ constexpr bool tmem_fused() {
 #ifndef RTE_CONV_EARLY_LOAD
 #define RTE_CONV_EARLY_LOAD 1  // converters load + split before waiting for the TMEM A buffer
 #endif
+#ifndef RTE_TC_HALFK
+#define RTE_TC_HALFK 1  // split form (BN = 128): the converter -> MMA hand-off runs in half K blocks (16 K
+                        // columns): each TMEM A buffer has a barrier pair per half, so the MMAs of the
+                        // first half issue while the converters still write the second, and a half is
+                        // refilled as soon as its two k-steps retire
+#endif
+#ifndef RTE_TC_DEFER
+#define RTE_TC_DEFER 0  // (experiment, off) fused-form halo convs (BN <= 64, the 32/64-channel levels): a K
+                        // block's tcgen05.wait::st + arrive is deferred until the next K block's first
+                        // pass is loaded and split.  Measured slower (level 0 0.371 -> 0.385 ms per
+                        // V-cycle, level 1 0.266 -> 0.276): the converter -> MMA -> converter loop is
+                        // latency-bound, and the deferral lengthens it
+#endif
 #ifndef RTE_EPI_BATCH_MAX
 #define RTE_EPI_BATCH_MAX 8
 #endif
@@ -211,9 +224,12 @@ constexpr bool tmem_fused() {
 #define RTE_TC_NA_MIN 2
 #endif
 // (TC = TMEM columns of one CTA: 512 / CPS)
+#ifndef RTE_TC_NA_MIN32
+#define RTE_TC_NA_MIN32 RTE_TC_NA_MIN  // (experiments: TMEM A buffers kept for the N = 32 kernels)
+#endif
 template <int BN, int TC = 512>
 constexpr int tmem_groups() {
-  constexpr int room = (TC - 64 * RTE_TC_NA_MIN) / (2 * BN);
+  constexpr int room = (TC - 64 * (BN == 32 ? RTE_TC_NA_MIN32 : RTE_TC_NA_MIN)) / (2 * BN);
   return tmem_fused<BN>() ? (room < RTE_TC_NG_MAX ? room : RTE_TC_NG_MAX) : 2;
 }
 template <int BN, int TC = 512>
@@ -398,7 +414,9 @@ __global__ void __launch_bounds__(kGemmThreads, CPS)
   constexpr int TCOLS = 512 / CPS;
   constexpr int NAR = PL::kNA, NBR = PL::kNB;
   constexpr int NA = tmem_abufs<BN, TCOLS>();
-  constexpr int NCV = NA > NAR ? NA : NAR;  // conv barriers (SSH: one per A ring slot)
+  constexpr bool HK = RTE_TC_HALFK && !tmem_fused<BN>() && !SSH;  // half-K-block hand-off (see RTE_TC_HALFK)
+  constexpr int NAH = HK ? 2 * NA : NA;     // conv / afree barriers of the TMEM A buffers
+  constexpr int NCV = NAH > NAR ? NAH : NAR;  // conv barriers (SSH: one per A ring slot)
   constexpr int BBYTES = PL::kBBytes;
   constexpr uint32_t TMEM_COLS = TCOLS;
   constexpr bool FUSED = tmem_fused<BN>();
@@ -414,7 +432,7 @@ __global__ void __launch_bounds__(kGemmThreads, CPS)
   uint64_t* conv = bempty + NBR;       // [NA] TMEM A buffer written (4 converter warps); SSH: A slot split
   uint64_t* afree = conv + NCV;        // [NA] MMAs done with the TMEM A buffer
   constexpr int NG = tmem_groups<BN, TCOLS>();
-  uint64_t* mfull = afree + NA;        // [NG] group buffer ready for promotion
+  uint64_t* mfull = afree + NAH;       // [NG] group buffer ready for promotion
   uint64_t* mempty = mfull + NG;       // [NG] group buffer drained (8 promoter warps)
   uint64_t* xempty = mempty + NG;      // [1] unit-long X drained (8 promoter warps)
   uint64_t* cfull = xempty + 1;        // [2] row centres written (128 converter threads)
@@ -443,7 +461,7 @@ __global__ void __launch_bounds__(kGemmThreads, CPS)
   const bool prof = RTE_TC_PROF && (g.dbg & 64) && lane == 0 && (((g.dbg >> 8) & 0xff) == 0 || ((g.dbg >> 8) & 0xff) == BN) &&
                     (!((g.dbg >> 16) & 1) || HALO) && (!((g.dbg >> 17) & 1) || !HALO) &&
                     (!((g.dbg >> 18) & 1) || Epi::kCenter) && (!((g.dbg >> 19) & 1) || !Epi::kCenter) &&
-                    (((g.dbg >> 24) & 0xff) == 0 || ((g.dbg >> 24) & 0xff) == g.kb_total);  // bits 24..31: K blocks
+                    (((g.dbg >> 24) & 0x7f) == 0 || ((g.dbg >> 24) & 0x7f) == (g.kb_total & 0x7f));  // bits 24..30: K blocks (mod 128)
   long long w_d = 0, w_e = 0;
   long long w_a = 0, w_b = 0, w_c = 0;
   long long w_s1 = 0, w_s2 = 0, w_s3 = 0;
@@ -460,7 +478,7 @@ __global__ void __launch_bounds__(kGemmThreads, CPS)
       mbar_init(&bempty[i], 1);
     }
     for (int i = 0; i < NCV; ++i) mbar_init(&conv[i], 4);
-    for (int i = 0; i < NA; ++i) mbar_init(&afree[i], 1);
+    for (int i = 0; i < NAH; ++i) mbar_init(&afree[i], 1);
     for (int t = 0; t < NG; ++t) {
       mbar_init(&mfull[t], 1);
       mbar_init(&mempty[t], 8);
@@ -503,8 +521,31 @@ __global__ void __launch_bounds__(kGemmThreads, CPS)
     // ===== TMA producer: the whole warp walks the pipeline, one elected lane issues =====
     // every read of the previous kernel's outputs is causally after this wait (the A/B tiles here;
     // the epilogue's addend and maps through the pipeline barriers); a no-op without PDL
+    // The B operand (weights, or S for the apply) is a constant of the problem, never a previous
+    // kernel's output: the first unit's first NBR B tiles are requested *before* the PDL wait, so
+    // their HBM latency overlaps the previous kernel's tail (dbg bit 22 switches this off; measured
+    // neutral to +0.8% on the V-cycle.  Also pulling the rest of the unit's weight range towards L2
+    // with bulk prefetches there was 7% slower: the prefetches compete with the previous kernel's tail)
+    int b_pre = 0;
+    if ((int)blockIdx.x < units && !(g.dbg & (1 << 22)) && !(g.dbg & 16)) {
+      const Unit w = decode_unit(g, blockIdx.x);
+      const int brow = w.n0 + w.tc.cls * g.b_rows_class + w.tc.b * g.b_rows_batch;
+      b_pre = min(NBR, w.kb1 - w.kb0);
+      if (elect_one()) {
+        for (int i = 0; i < b_pre; ++i) {
+          int tap, cc;
+          kb_split<HALO>(g, w.kb0 + i, tap, cc);
+          const int kcol = HALO ? tap * g.cchunks * 32 + cc * 32 : (w.kb0 + i) * 32;
+          uint8_t* sb = bring + i * PL::kBSlot;
+          mbar_arrive_expect_tx(&bfull[i], 2u * BBYTES);
+          tma_load_2d(sb, &tmBhi, &bfull[i], kcol, brow);
+          tma_load_2d(sb + BBYTES, &tmBlo, &bfull[i], kcol, brow);
+        }
+      }
+      __syncwarp();
+    }
     griddep_wait();
-    int as = 0, bs = 0;
+    int as = 0, bs = 0, b_cnt = 0;
     uint32_t aph = 0, bph = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       const Unit w = decode_unit(g, u);
@@ -544,6 +585,11 @@ __global__ void __launch_bounds__(kGemmThreads, CPS)
           __syncwarp();
           if (prof) w_s2 += clock64() - tp0;
           if (++as == NAR) { as = 0; aph ^= 1; }
+        }
+        if (b_cnt < b_pre) {  // requested before the PDL wait (slot b_cnt = bs, first use)
+          ++b_cnt;
+          if (++bs == NBR) { bs = 0; bph ^= 1; }
+          continue;
         }
         tw_wait(&bempty[bs], bph ^ 1, prof, w_b);
         const long long tp1 = prof ? clock64() : 0;
@@ -588,7 +634,7 @@ __global__ void __launch_bounds__(kGemmThreads, CPS)
           const long long tk0 = prof ? clock64() : 0;
           int tap = 0, cc = 0;
           if (SSH) kb_split<true>(g, kb, tap, cc);
-          if (!SSH) tw_wait(&conv[ab], abph, prof, w_a);
+          if (!SSH) tw_wait(&conv[HK ? 2 * ab : ab], abph, prof, w_a);
           else if (tap == 0 || kb == w.kb0) tw_wait(&conv[as], aph, prof, w_a);  // halo tile split
           tw_wait(&bfull[bs], bph, prof, w_s1);
           tc_fence_after();
@@ -631,6 +677,13 @@ __global__ void __launch_bounds__(kGemmThreads, CPS)
               const uint32_t tm = tmem + (uint32_t)(t * BN);
 #pragma unroll
               for (int k = 0; k < 4; ++k) {
+                if constexpr (HK) {
+                  if (k == 2) {  // first half retired -> refillable; second half written?
+                    mma_commit_elect(&afree[2 * ab]);
+                    tw_wait(&conv[2 * ab + 1], abph, prof, w_a);
+                    tc_fence_after();
+                  }
+                }
                 // K step of 8 tf32: +8 TMEM columns for A, +32 B (= +2) in the B descriptors
                 mma_tf32_ts_elect(tmem_x, a_lo + 8u * k, d_bh + 2u * k, idesc, acc_x);
                 acc_x = 1;
@@ -640,6 +693,12 @@ __global__ void __launch_bounds__(kGemmThreads, CPS)
               }
             }
           }
+          if constexpr (HK) {
+            if (no_mma) {  // (debug skeleton: keep the half hand-off protocol alive)
+              mma_commit_elect(&afree[2 * ab]);
+              tw_wait(&conv[2 * ab + 1], abph, prof, w_a);
+            }
+          }
           if (SSH) {
             mma_commit_elect(&bempty[bs]);
             if (tap == 8 || kb + 1 == w.kb1) {  // last tap of this halo tile: release the A slot
@@ -647,7 +706,7 @@ __global__ void __launch_bounds__(kGemmThreads, CPS)
               if (++as == NAR) { as = 0; aph ^= 1; }
             }
           } else {
-            mma_commit2_elect(&bempty[bs], &afree[ab]);
+            mma_commit2_elect(&bempty[bs], &afree[HK ? 2 * ab + 1 : ab]);
             if (++ab == NA) { ab = 0; abph ^= 1; }
           }
           if (prof) w_d += clock64() - ti0;
@@ -704,6 +763,20 @@ __global__ void __launch_bounds__(kGemmThreads, CPS)
     int as = 0, ab = 0;
     uint32_t aph = 0, abph = 0;
     int li = 0;
+    // deferred publication (RTE_TC_DEFER): the TMEM A buffer whose stores are issued but not yet waited
+    // for / announced; flushed before the next buffer's stores, before waiting for a new A tile (so the
+    // MMAs never wait on a TMA load through it) and after the last unit
+    constexpr bool DEFER = RTE_TC_DEFER && RTE_CONV_EARLY_LOAD && HALO && !HK && !ASPLIT && !Epi::kCenter;
+    int pend = -1;
+    auto flush_pend = [&]() {
+      if (pend >= 0) {
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&conv[pend]);
+        pend = -1;
+      }
+    };
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++li) {
       const Unit w = decode_unit(g, u);
       float c = 0.f;
@@ -712,9 +785,13 @@ __global__ void __launch_bounds__(kGemmThreads, CPS)
         int tap, cc;
         kb_split<HALO>(g, kb, tap, cc);
         const bool new_tile = !HALO || tap == 0 || kb == w.kb0;
-        if (new_tile) tw_wait(&afull[as], aph, prof, w_a);
+        if (new_tile) {
+          if constexpr (DEFER) flush_pend();
+          tw_wait(&afull[as], aph, prof, w_a);
+        }
 #if !RTE_CONV_EARLY_LOAD
-        tw_wait(&afree[ab], abph ^ 1, prof, w_b);
+        tw_wait(&afree[HK ? 2 * ab : ab], abph ^ 1, prof, w_b);
+        if (HK) tw_wait(&afree[2 * ab + 1], abph ^ 1, prof, w_b);
         tc_fence_after();
 #endif
         // source row in the A tile: the tap-shifted halo row (HALO) or the row itself; 16-byte
@@ -725,7 +802,7 @@ __global__ void __launch_bounds__(kGemmThreads, CPS)
         const bool skip = (g.dbg & 1) != 0;
         const long long tc0 = prof ? clock64() : 0;
         // the K block's 32 columns in passes of CWC (CPS = 2: 16, to fit the register budget)
-        constexpr int CWC = CPS == 1 ? 32 : 16;
+        constexpr int CWC = (CPS == 1 && !HK) ? 32 : 16;
         const bool last_of_tile = !HALO || tap == 8 || kb + 1 == w.kb1;
         const uint32_t ta = tmem_a + (uint32_t)(64 * ab) + lane_base;
 #pragma unroll
@@ -774,8 +851,9 @@ __global__ void __launch_bounds__(kGemmThreads, CPS)
 #if RTE_CONV_EARLY_LOAD
           // the TMEM A buffer is needed only from here: the first pass's shared-memory loads and
           // split overlap the wait for the MMAs to release it
-          if (c0 == 0) {
-            tw_wait(&afree[ab], abph ^ 1, prof, w_b);
+          if (HK || c0 == 0) {
+            if constexpr (DEFER) flush_pend();
+            tw_wait(&afree[HK ? 2 * ab + c0 / 16 : ab], abph ^ 1, prof, w_b);
             tc_fence_after();
           }
 #endif
@@ -788,16 +866,27 @@ __global__ void __launch_bounds__(kGemmThreads, CPS)
               tmem_st16(ta + 32 + (uint32_t)c0, lo);
             }
           }
+          if constexpr (HK) {  // publish this half
+            if (!skip) tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&conv[2 * ab + c0 / 16]);
+          }
         }
-        if (!skip) tmem_wait_st();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&conv[ab]);
+        if constexpr (DEFER) {
+          pend = ab;
+        } else if constexpr (!HK) {
+          if (!skip) tmem_wait_st();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&conv[ab]);
+        }
         if (prof) w_d += clock64() - tc0;
         if (++ab == NA) { ab = 0; abph ^= 1; }
         if (prof) w_e += clock64() - tk0;
       }
     }
+    if constexpr (DEFER) flush_pend();
   } else {
     // ===== promoters + epilogue (warps 6..13): warp w owns TMEM lanes 32*(w%4) .. +31 and the
     // column half h = (w - 6) / 4 of the tile =====
