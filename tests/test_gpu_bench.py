@@ -26,5 +26,12 @@ def test_bench_line_contract():
                - 1.0) < 1e-6                      # value = inner iterations / s, step = one cycle
     for key in ("roofline_apply", "roofline_vcycle"):
         assert line[key] is not None and line[key]["frac"] > 0
-    assert line["roofline_vcycle"]["roofline_ms_burst"] <= line["roofline_vcycle"]["roofline_ms_sustained"]
+    rv = line["roofline_vcycle"]
+    assert rv["roofline_ms_burst"] <= rv["roofline_ms_sustained"]
+    # frac = directly timed whole V-cycles; the per-class sums of the profiled solve and the in-solve bound stay
+    for key in ("frac_profiled", "measured_ms_per_vcycle", "roofline_ms_per_vcycle_burst", "in_solve"):
+        assert key in rv, key
+    assert abs(rv["frac"] * rv["measured_ms_per_vcycle"] / rv["roofline_ms_per_vcycle_burst"] - 1.0) < 1e-9
+    assert rv["in_solve"]["ms_per_vcycle_upper_bound"] > 0
+    assert "input" in line["ops"]
     assert line["e2e"]["h2d_bytes_per_step"] > 0 and line["e2e"]["d2h_bytes_per_step"] > 0
