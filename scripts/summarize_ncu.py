@@ -73,5 +73,28 @@ def full(path):
                 print(f"  {m:66s} {r[i]:>16s} {units[i]}")
 
 
+def table(path):
+    """One line per captured launch of a `full` summary file (this script's own output): duration, tensor
+    pipe activity, DRAM bytes, grid -- e.g. every GEMM of one V-cycle in launch order."""
+    rows, cur = [], None
+    for line in open(path):
+        if line.startswith("## "):
+            cur = {"k": line[3:].strip().replace("void gemm3xtf32_kernel", "gemm3xtf32")}
+            rows.append(cur)
+        elif cur is not None and line.startswith("  "):
+            parts = line.split()
+            cur[parts[0]] = (float(parts[1].replace(",", "")), parts[2] if len(parts) > 2 else "")
+    print(f"# {len(rows)} launches of {path} (ncu --set full: serialised, cold-cache; template arguments = "
+          "<N tile, A mode (1 = halo), pre-split A, epilogue, CTAs per SM>)")
+    print(f"{'#':>3s} {'kernel':40s} {'grid':>5s} {'us':>8s} {'tensor%':>8s} {'dram_rd_MB':>11s} {'dram_wr_MB':>11s}")
+    for i, r in enumerate(rows):
+        t, u = r.get("gpu__time_duration.sum", (0.0, "us"))
+        t *= {"ns": 1e-3, "us": 1.0, "ms": 1e3}.get(u, 1.0)
+        mb = lambda k: r.get(k, (0.0, ""))[0] * {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}.get(r.get(k, (0, "Mbyte"))[1], 1.0)
+        print(f"{i:3d} {r['k'][:40]:40s} {int(r.get('launch__grid_size', (0, ''))[0]):5d} {t:8.1f} "
+              f"{r.get('sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active', (0, ''))[0]:8.1f} "
+              f"{mb('dram__bytes_read.sum'):11.1f} {mb('dram__bytes_write.sum'):11.1f}")
+
+
 if __name__ == "__main__":
-    {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2])
+    {"launches": launches, "full": full, "table": table}[sys.argv[1]](sys.argv[2])
