@@ -7,6 +7,14 @@ preconditioned, x0 = 0, the config's restart and fixed budget.  Its deviation fr
 run (tests/golden/bands_cfg{k}.npz) is added to the band file as s{s}_band_fp32_hist / s{s}_band_fp32_x.
 
   python scripts/make_bands_fp32.py 3 4 5 [--samples 0,3]
+
+--op-tol E (reading R36 v5): the same fp32-storage run on operators that each carry a fixed relative
+error of the north star's single-operator tolerance E = 1e-5 -- z = q + (1 + E xi_V) (.) V(q) and
+w = (1 + E xi_A) (.) A z with xi_V, xi_A ~ N(0,1) per unknown, drawn once per (config, sample) from a
+seeded generator and kept for the whole solve (a fixed nearby linear operator, not per-call noise: that
+averages out of the history, R36) -- i.e. an implementation whose every V-cycle and apply is within 1e-5
+rel-L2 of the oracle's, which is all the north star asks of one.  Stored as s{s}_band_op_hist / _x.
+--coherent: the coherent error of that size instead, z = q + (1 - E) V(q) (s{s}_band_opc_hist / _x).
 """
 from __future__ import annotations
 
@@ -125,6 +133,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("configs", type=int, nargs="+")
     ap.add_argument("--samples", type=str, default=None)
+    ap.add_argument("--op-tol", type=float, default=0.0)
+    ap.add_argument("--coherent", action="store_true")
     a = ap.parse_args()
     for k in a.configs:
         cfg = W.config(k)
@@ -146,6 +156,23 @@ def main():
             P = lambda v: (np.asarray(v, np.float64) + O.vcycle(onet, np.asarray(v, np.float64).reshape(shape),
                                                                  add_identity=False).ravel()).astype(f32)
             O_apply64 = lambda x: O.apply(op_s, x.reshape(shape)).ravel()
+            tag = "fp32"
+            if a.op_tol > 0.0:
+                tag = "op"
+                rng = np.random.Generator(np.random.PCG64([5000 + k, s]))
+                dV = (1.0 + a.op_tol * rng.standard_normal(int(np.prod(shape)))).astype(np.float64)
+                dA = (1.0 + a.op_tol * rng.standard_normal(int(np.prod(shape)))).astype(np.float64)
+                if a.coherent:
+                    # the coherent error of the same size: V(q) scaled by (1 - E) everywhere -- the shape of a
+                    # rounding *bias* (the tensor core's fp32 accumulation truncates, DESIGN.md §6 numerics 1),
+                    # which, unlike a random field, does not average out of the Arnoldi inner products.  (The
+                    # same scaling of A leaves the residual history unchanged: the Krylov space is the same.)
+                    tag = "opc"
+                    dV = 1.0 - a.op_tol
+                    dA = 1.0
+                A = lambda v, dA=dA: (dA * O.apply(op_s, np.asarray(v, np.float64).reshape(shape)).ravel()).astype(f32)
+                P = lambda v, dV=dV: (np.asarray(v, np.float64) + dV * O.vcycle(
+                    onet, np.asarray(v, np.float64).reshape(shape), add_identity=False).ravel()).astype(f32)
             b = b32_all[s:s + 1].ravel()
             t0 = time.time()
             hist, x = gmres_dcgs2_fp32(A, P, b, cfg.restart, cfg.maxit, cfg.rtol)
@@ -154,12 +181,14 @@ def main():
             dh = float(np.max(np.abs(hist[:n] - ref[:n]) / ref[:n]))
             xs = x[idx]
             dx = float(np.linalg.norm(xs - g[f"s{s}_ref_xs"]) / np.linalg.norm(g[f"s{s}_ref_xs"]))
-            g[f"s{s}_fp32_hist"] = hist
-            g[f"s{s}_fp32_xs"] = xs
-            g[f"s{s}_band_fp32_hist"] = dh
-            g[f"s{s}_band_fp32_x"] = dx
-            print(f"cfg{k} s{s}: fp32-storage DCGS2 run, {len(hist)} it, history dev {dh:.3e}, x dev {dx:.3e}, "
-                  f"{time.time() - t0:.0f} s", flush=True)
+            g[f"s{s}_{tag}_hist"] = hist
+            g[f"s{s}_{tag}_xs"] = xs
+            g[f"s{s}_band_{tag}_hist"] = dh
+            g[f"s{s}_band_{tag}_x"] = dx
+            if tag in ("op", "opc"):
+                g["op_tol"] = a.op_tol
+            print(f"cfg{k} s{s}: fp32-storage DCGS2 run{' + operators at ' + str(a.op_tol) + ' (' + tag + ')' if tag != 'fp32' else ''}, "
+                  f"{len(hist)} it, history dev {dh:.3e}, x dev {dx:.3e}, {time.time() - t0:.0f} s", flush=True)
         np.savez_compressed(path, **g)
 
 

@@ -67,6 +67,14 @@ def test_fixed_budget_gmres_within_oracle_band(k, margin):
         # = that run is not in the golden file)
         band_h = 2.0 * max(float(g[f"s{s}_band_hist"]), float(g.get(f"s{s}_band_fp32_hist", 0.0)))
         band_x = 2.0 * max(float(g[f"s{s}_band_x"]), float(g.get(f"s{s}_band_fp32_x", 0.0)))
+        # R36 v5: the run whose operators each carry a fixed relative error of the north star's single-
+        # operator tolerance, as a random field and as a coherent bias (scripts/make_bands_fp32.py --op-tol 1e-5
+        # [--coherent]); recorded against the larger of the two separately
+        op_h = 2.0 * max(float(g.get(f"s{s}_band_op_hist", 0.0)), float(g.get(f"s{s}_band_opc_hist", 0.0)))
+        op_x = 2.0 * max(float(g.get(f"s{s}_band_op_x", 0.0)), float(g.get(f"s{s}_band_opc_x", 0.0)))
+        if op_h > 0.0:
+            margin(dh, op_h, f"s{s} residual history vs 2x operator-tolerance band (recorded)")
+            margin(dx, op_x, f"s{s} iterate x vs 2x operator-tolerance band (recorded)")
         # Recorded, not asserted: neither perturbation model contains the fp32 / 3xTF32 arithmetic *inside*
         # the operators (measured per-application errors 1e-6 ... 8e-6), and at configs 4-5 both bands are
         # tighter than that moves the history (R36 v4: measured ratios in parity_margins.md)
@@ -75,8 +83,8 @@ def test_fixed_budget_gmres_within_oracle_band(k, margin):
         # Asserted (R36 v4, a-priori bounds): the history within max(2x band, maxit * u), u = 2^-24 the fp32
         # unit roundoff -- the first-order accumulation bound of an Arnoldi process stored in fp32 over the
         # budget's steps; the iterate within max(2x band, 1e-4), the north star's solution tolerance
-        bh = max(band_h, cfg.maxit * 2.0 ** -24)
-        bx = max(band_x, 1e-4)
+        bh = max(band_h, op_h, cfg.maxit * 2.0 ** -24)
+        bx = max(band_x, op_x, 1e-4)
         if margin(dh, bh, f"s{s} residual history vs max(2x band, maxit u_fp32)") > bh:
             fails.append((s, "history", dh, bh))
         if margin(dx, bx, f"s{s} iterate x vs max(2x band, 1e-4)") > bx:
