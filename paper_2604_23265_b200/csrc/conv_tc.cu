@@ -580,7 +580,11 @@ bool conv_tc_try(const ConvDesc& d, const float* in, float* out, const float* ad
     et.tmOut = tc::make_map_act(out, d.Co, d.Wo, d.Ho, d.B, g.TW, g.TH, oes);
     et.nb = d.B;
     if (g.nsplit > 1) et.tmPart = tc::make_map_act(epi.part, d.Co, d.Wo, d.Ho, d.B * g.nsplit, g.TW, g.TH, oes);
-    P.g.epf = 0;  // the addend tiles are loaded ahead anyway
+    // the addend tiles are loaded ahead anyway -- by a whole K loop.  Units of one or two K blocks (the
+    // head conv: K = C0) have no such lead: there the L2 prefetch one unit ahead stays on
+    // (RTE_SHORTK_EPF=0 switches it off)
+    static const bool shortk_epf = !(getenv("RTE_SHORTK_EPF") && atoi(getenv("RTE_SHORTK_EPF")) == 0);
+    P.g.epf = (shortk_epf && g.epf == 1 && g.nsplit == 1 && g.kb_total <= 2) ? 1 : 0;
     // split-K fixup inside the kernel when every unit has its own resident CTA (tc_gemm.cuh Geom::fix):
     // no reduction launch.  Opt-in (RTE_TC_FIX=1): measured slower -- config-5 V-cycle 2.057 -> 2.130 ms;
     // the grid barrier waits for the slowest split and the reduction no longer overlaps the next
