@@ -187,12 +187,15 @@ def test_vcycle_parity_large(k, margin):
 
 
 @pytest.mark.parametrize("env", [{"RTE_TC_SS_MINW": "16"}, {"RTE_TC_PRESPLIT": "1"}, {"RTE_TC_CLUSTER": "1"},
-                                 {"RTE_TC_KQ": "9"}, {"RTE_SMALLK_NT": "512"}],
-                         ids=["ss_halo", "presplit", "cluster_splitk", "whole_chunk_splitk", "head_512"])
+                                 {"RTE_TC_KQ": "9"}, {"RTE_SMALLK_NT": "512"}, {"RTE_SMALLK": "1"},
+                                 {"RTE_SHORTK_EPF": "0"}, {"RTE_TC_DBG": "4194304"}],
+                         ids=["ss_halo", "presplit", "cluster_splitk", "whole_chunk_splitk", "head_512",
+                              "head_simt_c32", "no_shortk_prefetch", "no_early_b"])
 def test_vcycle_parity_kernel_variants(env):
     """The opt-in conv kernel variants (SS-halo 3x3 kernels, pre-split activations, cluster
     split-K through distributed shared memory, K splits in whole 9-tap chunks, 64 KB head-conv
-    tiles)
+    tiles, the small-K SIMT head for C0 = 32 nets, no addend L2 prefetch for short-K units, no B tiles
+    before the PDL wait)
     pass the same V-cycle parity: their switches are read once per process, so the V-cycle parity
     tests rerun in a child process with the switch set."""
     import os
